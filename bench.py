@@ -1,0 +1,424 @@
+"""Benchmark: cells/sec minibatch assembly on B200 (BASELINE.json metric).
+
+A *step* is the assembly of one minibatch (b rows) of the loader's epoch
+stream.  Default workload = BASELINE config 1 (the single-GPU config; config 2
+does not fit one GPU's HBM): synthetic CSR
+100k cells x 20k genes, ~2k nnz/cell f32, f=64 rows/fetch, B=4096, b=4096,
+densify to fp32.
+
+  value  — device-resident: the store's chunk records resident in HBM and the
+           step's row references precomputed on the device; K timed launches
+           of the densify kernel.  Whole-job cells/s = N * cells / max-rank time.
+  e2e    — the same metric through the public API (BatchIterator.next()) with
+           the store in pinned host memory: every step stages the fetched
+           blocks host->device (cudaMemcpyAsync), replays the schedule on the
+           host, assembles, and reads the batch's global_indices back.
+
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+        [--workload cfg1|cfg2|cfg3|cfg4]; N>1 under torchrun (one rank/GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: synth config, loader config, output
+    "cfg1": dict(desc="cfg1: synthetic CSR 100k cells x 20k genes, ~2k nnz/cell f32 (density 0.1), chunk 64, "
+                      "f=64 B=4096 b=4096, densify fp32",
+                 synth=dict(n_obs=100_000, n_var=20_000, layout="csr", value_dtype="f32", index_dtype="u32",
+                            density=0.1, seed=0, chunk_rows=64, chunks_per_shard=128),
+                 loader=dict(fetch_block_rows=64, buffer_capacity_rows=4096, batch_rows=4096, seed=0),
+                 out=dict(output="dense", out_dtype="f32", transform=None), dtype="f32"),
+    "cfg2": dict(desc="cfg2-shaped: synthetic CSR 36k genes ~3k nnz/cell f32, 1M cells resident per GPU, "
+                      "f=1024 B=16384 b=4096, densify fp32 + library-size/log1p",
+                 synth=dict(n_obs=1_000_000, n_var=36_000, layout="csr", value_dtype="f32", index_dtype="u32",
+                            density=3000 / 36000, seed=1, chunk_rows=1024, chunks_per_shard=128),
+                 loader=dict(fetch_block_rows=1024, buffer_capacity_rows=16384, batch_rows=4096, seed=0),
+                 out=dict(output="dense", out_dtype="f32", transform="normalize_log1p"), dtype="f32"),
+    "cfg3": dict(desc="cfg3: dense 3x64x64 u8 crops (2M samples), chunk 256, f=256 B=16384 b=1024, cast bf16",
+                 synth=dict(n_obs=2_000_000, n_var=12288, layout="dense", value_dtype="u8", density=0.1, seed=2,
+                            chunk_rows=256, chunks_per_shard=128),
+                 loader=dict(fetch_block_rows=256, buffer_capacity_rows=16384, batch_rows=1024, seed=0),
+                 out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16"),
+    "cfg4": dict(desc="cfg4: dense 4x1024 u8 windows (5M), chunk 512, f=512 B=16384 b=2048, raw u8",
+                 synth=dict(n_obs=5_000_000, n_var=4096, layout="dense", value_dtype="u8", density=0.1, seed=3,
+                            chunk_rows=512, chunks_per_shard=128),
+                 loader=dict(fetch_block_rows=512, buffer_capacity_rows=16384, batch_rows=2048, seed=0),
+                 out=dict(output="dense", out_dtype="native", transform=None), dtype="u8"),
+}
+METRIC = "cells/sec minibatch assembly"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, idx: int):
+        self.idx = idx
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def ensure_store(wl, rank, world, dist):
+    import paper_2604_01949_b200 as R
+    base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
+    path = base / wl
+    s = WORKLOADS[wl]["synth"]
+    if rank == 0 and not (path / "manifest.json").exists():
+        base.mkdir(parents=True, exist_ok=True)
+        tmp = base / f".{wl}.{os.getpid()}"
+        R.synth_store(tmp, R.SynthConfig(**s))
+        os.replace(tmp, path)
+    if dist:
+        dist.barrier()
+    return path
+
+
+def schedule_batches(n_obs, lcfg, rank, world, need):
+    """The exact global_indices stream of this rank, chained over epochs."""
+    import paper_2604_01949_b200 as R
+    out, epoch = [], 0
+    while len(out) < need:
+        cfg = R.LoaderConfig(**lcfg, rank=rank, world=world)
+        for g in R.EpochSchedule(n_obs, cfg, epoch):
+            out.append(g)
+            if len(out) >= need:
+                break
+        epoch += 1
+    return out
+
+
+def run_ours(args, wl, rank, world, local, dist):
+    import ctypes as C
+
+    import torch
+
+    import paper_2604_01949_b200 as R
+    from paper_2604_01949_b200 import _lib as L
+
+    torch.cuda.set_device(local)
+    W = WORKLOADS[wl]
+    path = ensure_store(wl, rank, world, dist)
+    reader = R.StoreReader(path)
+    man = reader.manifest()
+    K, Wm = args.steps, args.warmup
+
+    # ------------------------------------------------ device-resident value --
+    ds = R.DeviceStore(reader, local, "resident")
+    base, offs = ds.arena()
+    desc = ds.arena_desc()
+    batches = schedule_batches(man.n_obs, W["loader"], rank, world, Wm + K)
+    b = W["loader"]["batch_rows"]
+    refs = np.zeros((Wm + K, b, 2), np.uint64)
+    rows = []
+    for i, g in enumerate(batches):
+        refs[i, :len(g), 0] = offs[g.astype(np.int64) // man.chunk_rows]
+        refs[i, :len(g), 1] = g
+        rows.append(len(g))
+    d_refs = torch.from_numpy(refs.view(np.int64)).cuda()
+    esz = {"f32": 4, "bf16": 2, "native": {"f32": 4, "f64": 8, "i32": 4, "u8": 1}[man.value_dtype]}[
+        W["out"]["out_dtype"]]
+    out = torch.empty(b * man.n_var * esz + 16, dtype=torch.uint8, device="cuda")
+    gout = torch.empty(b, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+    od = {"f32": L.F32, "bf16": L.BF16, "native": L.NATIVE}[W["out"]["out_dtype"]]
+    xf = L.XF_NORMALIZE_LOG1P if W["out"]["transform"] else L.XF_NONE
+    lib = L.lib()
+
+    def launch(i):
+        if man.layout == "csr":
+            rc = lib.rfl_csr_densify(C.byref(desc), d_refs[i].data_ptr(), rows[i], od, xf, 1e4, out.data_ptr(),
+                                     gout.data_ptr(), C.c_void_p(stream.cuda_stream))
+        else:
+            rc = lib.rfl_dense_gather(C.byref(desc), d_refs[i].data_ptr(), rows[i], od, out.data_ptr(),
+                                      gout.data_ptr(), C.c_void_p(stream.cuda_stream))
+        L.check(rc)
+
+    for i in range(Wm):
+        launch(i)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for k in range(K):
+            ev[k][0].record(stream)
+            launch(Wm + k)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    per = [s.elapsed_time(e) for s, e in ev]
+    total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    cells = sum(rows[Wm:])
+    t = torch.tensor([total_ms], device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+
+    # algorithmic bytes per launch: read row refs + indptr pair +
+    # indices/values of every nnz; write the dense rows + gidx.
+    alg = 0
+    if man.layout == "csr":
+        isz, vsz = 4 if man.index_dtype == "u32" else 8, {"f32": 4, "f64": 8, "i32": 4, "u8": 1}[man.value_dtype]
+        nnz_tot = 0
+        rn = _row_nnz(reader, man)
+        for i in range(Wm, Wm + K):
+            nnz_tot += int(rn[refs[i, :rows[i], 1].astype(np.int64)].sum())
+        alg = nnz_tot * (isz + vsz) + cells * (16 + 2 * isz + man.n_var * esz + 8)
+    else:
+        alg = cells * (16 + man.n_var * 1 + man.n_var * esz + 8)
+    alg_per_launch = alg / K
+    avg_launch_s = statistics.mean(per) / 1e3
+    peak, peak_src = peaks()
+    achieved = alg_per_launch / avg_launch_s / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / f"traffic_{wl}.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
+
+    # ---------------------------------------------------------------- e2e --
+    e2e = run_e2e(args, wl, reader, W, rank, world, local, dist)
+    ds.close()
+
+    res = None
+    if rank == 0:
+        value = world * (cells / K) / (max_ms / K / 1e3)  # whole job: N ranks x cells per step / step time
+        res = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": K, "warmup": Wm,
+            "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": W["dtype"], "data": "synthetic (product synth_store == reference synth_store bytes)",
+            "config": {"workload": W["desc"], "staging": "resident (chunk records in HBM)",
+                       "l2": "inputs larger than L2 (store %.2f GB, batch output %.0f MB)" % (
+                           ds_bytes(reader) / 1e9, b * man.n_var * esz / 1e6),
+                       "parallelism": f"dp{world} (disjoint plan positions per rank, no collective)",
+                       "cells_per_step_per_rank": cells / K},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k_csr_densify" if man.layout == "csr" else "k_dense_gather",
+                         "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": avg_launch_s * 1e3},
+            "e2e": e2e,
+            "gpu_launches": K,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline(path, W, threads=1)
+    return res
+
+
+def ds_bytes(reader):
+    p = Path(reader.root) / "shards"
+    return sum(f.stat().st_size for f in p.iterdir())
+
+
+def _row_nnz(reader, man):
+    """Per-row nnz from the records' indptrs (host, for the algorithmic byte count)."""
+    out = np.zeros(man.n_obs, np.int64)
+    it = np.uint32 if man.index_dtype == "u32" else np.uint64
+    for q in range(man.chunk_count()):
+        rec = reader.read_record(q)
+        rows = int(np.frombuffer(rec, np.uint32, 1, 0)[0])
+        ip = np.frombuffer(rec, it, rows + 1, 12).astype(np.int64)
+        out[q * man.chunk_rows:q * man.chunk_rows + rows] = np.diff(ip)
+    return out
+
+
+def run_e2e(args, wl, reader, W, rank, world, local, dist):
+    import torch
+
+    import paper_2604_01949_b200 as R
+    K, Wm = args.steps, args.warmup
+    ds = R.DeviceStore(reader, local, "stream_pinned")
+    stream = torch.cuda.current_stream()
+    epoch = 0
+    cfg = R.LoaderConfig(**W["loader"], prefetch_depth=4, rank=rank, world=world)
+
+    def make_it(e):
+        return R.BatchIterator(ds, cfg, e, output=W["out"]["output"], out_dtype=W["out"]["out_dtype"],
+                               transform=W["out"]["transform"], out_slots=3, stream=stream)
+
+    it = make_it(epoch)
+    host = torch.empty(W["loader"]["batch_rows"], dtype=torch.int64).pin_memory()
+    h2d_done = [0]  # bytes staged by iterators already retired
+
+    def step():
+        nonlocal it, epoch
+        b = it.next()
+        if b is None:
+            h2d_done[0] += it.counters().h2d_bytes
+            it.close()
+            epoch += 1
+            it = make_it(epoch)
+            b = it.next()
+        host[:b.n_rows].copy_(b.global_indices, non_blocking=True)  # D2H of the step's result ids
+        return b.n_rows
+
+    for _ in range(Wm):
+        step()
+    torch.cuda.synchronize()
+    h2d0 = h2d_done[0] + it.counters().h2d_bytes
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s_ev.record(stream)
+    cells = 0
+    for _ in range(K):
+        cells += step()
+    e_ev.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = s_ev.elapsed_time(e_ev)
+    h2d = h2d_done[0] + it.counters().h2d_bytes - h2d0
+    t = torch.tensor([max(ms, wall * 1e3)], device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    it.close()
+    ds.close()
+    return {"value": world * cells / (float(t.item()) / 1e3), "unit": "cells/s",
+            "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": 8 * cells / K,
+            "staging": "stream_pinned (records in pinned host RAM; blocks cudaMemcpyAsync'd per fetch)",
+            "api": "paper_2604_01949_b200.BatchIterator.next -> rfl_loader_next",
+            "gpu_launches": K}
+
+
+def cpu_baseline(path, W, threads):
+    """The reference's CPU path (oracle/_ref = /root/reference compiled unmodified),
+    BatchIterator + to_dense per batch, on a bounded sample (metrics.cpp:99-136 timing)."""
+    from oracle.oracle import Ref
+    ld = W["loader"]
+    dens = W["out"]["output"] == "dense" and W["synth"]["layout"] == "csr"
+    nb = int(os.environ.get("RIFFLE_CPU_BATCHES", "12"))
+    v, rows, wall = Ref.throughput(path, ld["fetch_block_rows"], ld["buffer_capacity_rows"], ld["batch_rows"],
+                                   seed=ld["seed"], depth=4, epoch0=0, threads=threads, max_batches=nb,
+                                   densify=dens)
+    return {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
+            "sample": f"{rows} cells = first {nb} batches of epoch(s) 0..{threads - 1} per thread, "
+                      f"BatchIterator(prefetch_depth=4){' + to_dense' if dens else ''}, wall {wall:.1f}s",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args, wl, rank, world):
+    """--impl reference: the reference CPU implementation, all host threads, rank 0 only."""
+    if rank != 0:
+        return None
+    import torch  # noqa: F401  (same environment as our arm)
+    from oracle.oracle import Ref
+    W = WORKLOADS[wl]
+    path = ensure_store(wl, 0, 1, None)
+    threads = os.cpu_count() or 1
+    ld = W["loader"]
+    dens = W["out"]["output"] == "dense" and W["synth"]["layout"] == "csr"
+    Ref.throughput(path, ld["fetch_block_rows"], ld["buffer_capacity_rows"], ld["batch_rows"], seed=ld["seed"],
+                   depth=4, epoch0=100, threads=threads, max_batches=max(1, args.warmup // 3), densify=dens)
+    v, rows, wall = Ref.throughput(path, ld["fetch_block_rows"], ld["buffer_capacity_rows"], ld["batch_rows"],
+                                   seed=ld["seed"], depth=4, epoch0=0, threads=threads,
+                                   max_batches=max(1, args.steps // 4), densify=dens)
+    steps = rows / ld["batch_rows"]
+    return {"metric": METRIC, "value": v, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": wall * 1e3 / max(steps, 1e-9), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": W["dtype"],
+            "data": "synthetic (reference synth_store)", "impl": "reference",
+            "config": {"workload": W["desc"], "parallelism": f"{threads} host threads (one iterator each)"},
+            "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
+                             "sample": f"{rows} cells over {threads} concurrent BatchIterators (epochs 0..{threads - 1})"
+                                       f"{' + to_dense' if dens else ''}, wall {wall:.1f}s"},
+            "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if args.impl == "reference":
+        res = run_reference(args, args.workload, rank, world)
+    else:
+        res = run_ours(args, args.workload, rank, world, local, dist)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

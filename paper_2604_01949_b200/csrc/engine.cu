@@ -1,0 +1,497 @@
+// Device store images + GPU BatchIterator (see engine.hpp).
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "engine.hpp"
+
+namespace rfl {
+
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+    cuda_ok(cudaGetDevice(&prev), "cudaGetDevice");
+    if (dev != prev) cuda_ok(cudaSetDevice(dev), "cudaSetDevice");
+}
+DeviceGuard::~DeviceGuard() { cudaSetDevice(prev); }
+
+namespace {
+constexpr uint64_t kAlign = 16;
+constexpr uint64_t kPad = 256;                  // arena tail padding for 16-B over-reads
+constexpr uint64_t kUploadRun = 64ull << 20;    // pinned bounce buffer for uploads
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// decode_record's header checks (store.cpp:81-104), without decoding.
+void check_csr_header(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint64_t len) {
+    if (len < kCsrHeaderBytes) corrupt("chunk " + std::to_string(chunk) + ": csr record shorter than header");
+    const uint32_t rows = rd32(rec);
+    const uint64_t nnz = rd64(rec + 4);
+    if (rows != m.rows_in_chunk(chunk))
+        corrupt("chunk " + std::to_string(chunk) + ": csr record header declares " + std::to_string(rows) +
+                " rows, chunk has " + std::to_string(m.rows_in_chunk(chunk)));
+    const uint64_t is = index_size(*m.index_dtype), vs = value_size(m.value_dtype);
+    const uint64_t expected = kCsrHeaderBytes + (rows + 1ull) * is + nnz * (is + vs);
+    if (len != expected)
+        corrupt("chunk " + std::to_string(chunk) + ": csr record length " + std::to_string(len) + ", expected " +
+                std::to_string(expected));
+}
+
+void parse_row_nnz(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint32_t* out) {
+    const uint32_t rows = rd32(rec);
+    const uint8_t* ip = rec + kCsrHeaderBytes;
+    const uint64_t nnz = rd64(rec + 4);
+    uint64_t prev = 0;
+    for (uint32_t r = 0; r <= rows; ++r) {
+        const uint64_t v = *m.index_dtype == IDtype::u32 ? rd32(ip + 4ull * r) : rd64(ip + 8ull * r);
+        if (r == 0) {
+            if (v != 0) corrupt("chunk " + std::to_string(chunk) + ": csr record invalid: indptr[0] != 0");
+        } else {
+            if (v < prev) corrupt("chunk " + std::to_string(chunk) + ": csr record invalid: indptr decreasing at row " +
+                                  std::to_string(r - 1));
+            out[r - 1] = static_cast<uint32_t>(v - prev);
+        }
+        prev = v;
+    }
+    if (prev != nnz) corrupt("chunk " + std::to_string(chunk) + ": csr record invalid: indices length does not match indptr");
+}
+}  // namespace
+
+// ================================================================= DStore ===
+DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
+    : hs_(std::move(hs)), device_(device), staging_(staging) {
+    const Manifest& m = hs_->manifest();
+    if (m.codec != Codec::none) invalid("GPU path requires codec none (deflate decode is out of scope)");
+    if (staging > kStreamFile) invalid("unknown staging mode");
+    const uint64_t nch = m.chunk_count();
+    rec_off_.resize(nch);
+    rec_len_.resize(nch);
+    uint64_t off = 0;
+    for (uint64_t q = 0; q < nch; ++q) {
+        rec_len_[q] = hs_->record_slot(q).len;
+        rec_off_[q] = off;
+        off = align_up(off + rec_len_[q], kAlign);
+    }
+    image_bytes_ = off;
+    if (m.layout == Layout::csr) row_nnz_.resize(m.n_obs);
+    DeviceGuard g(device_);
+    if (staging_ == kResident) load_records(true);
+    else if (staging_ == kStreamPinned) load_records(false);
+    else if (m.layout == Layout::csr) {  // file streaming: only headers + indptrs now
+        std::vector<uint8_t> buf;
+        for (uint64_t q = 0; q < nch; ++q) {
+            const uint64_t want = std::min<uint64_t>(
+                rec_len_[q], kCsrHeaderBytes + (m.rows_in_chunk(q) + 1) * index_size(*m.index_dtype));
+            buf.resize(want);
+            const Slot s = hs_->record_slot(q);
+            hs_->read_shard_bytes(q / m.chunks_per_shard, s.off, buf.data(), want, false);
+            if (want < kCsrHeaderBytes) corrupt("chunk " + std::to_string(q) + ": csr record shorter than header");
+            check_csr_header(m, q, buf.data(), rec_len_[q]);
+            parse_row_nnz(m, q, buf.data(), row_nnz_.data() + q * m.chunk_rows);
+        }
+    }
+}
+
+void DStore::load_records(bool to_device) {
+    const Manifest& m = hs_->manifest();
+    const uint64_t nch = m.chunk_count();
+    if (to_device) {
+        cuda_ok(cudaMalloc(&d_arena_, image_bytes_ + kPad), "cudaMalloc arena");
+        cuda_ok(cudaMemset(d_arena_ + image_bytes_, 0, kPad), "cudaMemset pad");
+    } else {
+        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&h_image_), image_bytes_ + kPad, cudaHostAllocPortable),
+                "cudaHostAlloc image");
+    }
+    uint64_t max_rec = 0;
+    for (auto l : rec_len_) max_rec = std::max(max_rec, l);
+    const uint64_t run_cap = std::max(kUploadRun, max_rec);
+    uint8_t* bounce[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t st = nullptr;
+    if (to_device) {
+        cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        for (int i = 0; i < 2; ++i) {
+            cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&bounce[i]), run_cap, cudaHostAllocDefault), "bounce");
+            cuda_ok(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "event");
+        }
+    }
+    int which = 0;
+    uint64_t q = 0;
+    while (q < nch) {  // a run of consecutive records of one shard, read with one pread
+        const uint64_t shard = q / m.chunks_per_shard;
+        const Slot first = hs_->record_slot(q);
+        uint64_t end = q + 1, run_len = first.len;
+        while (end < nch && end / m.chunks_per_shard == shard) {
+            const Slot s = hs_->record_slot(end);
+            if (s.off != first.off + run_len || run_len + s.len > run_cap) break;
+            run_len += s.len;
+            ++end;
+        }
+        uint8_t* buf;
+        if (to_device) {
+            cuda_ok(cudaEventSynchronize(ev[which]), "event sync");
+            buf = bounce[which];
+            hs_->read_shard_bytes(shard, first.off, buf, run_len, false);
+        } else {
+            buf = h_image_ + rec_off_[q];  // records land contiguously, then get spread to their slots
+            if (end - q > 1) {
+                buf = static_cast<uint8_t*>(std::malloc(run_len));
+                if (!buf) invalid("out of host memory");
+            }
+            hs_->read_shard_bytes(shard, first.off, buf, run_len, false);
+        }
+        uint64_t rel = 0;
+        for (uint64_t k = q; k < end; ++k) {
+            const uint8_t* rec = buf + rel;
+            if (m.layout == Layout::csr) {
+                check_csr_header(m, k, rec, rec_len_[k]);
+                parse_row_nnz(m, k, rec, row_nnz_.data() + k * m.chunk_rows);
+            } else if (rec_len_[k] != m.rows_in_chunk(k) * m.n_var * value_size(m.value_dtype)) {
+                corrupt("chunk " + std::to_string(k) + ": dense record length mismatch");
+            }
+            if (to_device)
+                cuda_ok(cudaMemcpyAsync(d_arena_ + rec_off_[k], rec, rec_len_[k], cudaMemcpyHostToDevice, st),
+                        "upload");
+            else if (end - q > 1)
+                std::memcpy(h_image_ + rec_off_[k], rec, rec_len_[k]);
+            rel += rec_len_[k];
+        }
+        if (to_device) {
+            cuda_ok(cudaEventRecord(ev[which], st), "event record");
+            which ^= 1;
+        } else if (end - q > 1) {
+            std::free(buf);
+        }
+        q = end;
+    }
+    if (to_device) {
+        cuda_ok(cudaStreamSynchronize(st), "upload sync");
+        for (int i = 0; i < 2; ++i) {
+            cudaFreeHost(bounce[i]);
+            cudaEventDestroy(ev[i]);
+        }
+        cudaStreamDestroy(st);
+    }
+}
+
+DStore::~DStore() {
+    DeviceGuard g(device_);
+    for (auto& s : free_)
+        if (s.released) cudaEventDestroy(s.released);
+    for (void* p : slabs_) cudaFree(p);
+    if (d_arena_) cudaFree(d_arena_);
+    if (h_image_) cudaFreeHost(h_image_);
+}
+
+uint64_t DStore::max_block_bytes(uint64_t f) const {
+    const Manifest& m = manifest();
+    uint64_t best = 0;
+    for (uint64_t s = 0; s < m.n_obs; s += f) {
+        const uint64_t e = std::min(m.n_obs, s + f);
+        uint64_t bytes = 0;
+        for (uint64_t q = s / m.chunk_rows; q <= (e - 1) / m.chunk_rows; ++q) bytes = align_up(bytes + rec_len_[q], kAlign);
+        best = std::max(best, bytes);
+    }
+    return best;
+}
+
+ArenaView DStore::view(const uint8_t* base) const {
+    const Manifest& m = manifest();
+    ArenaView a;
+    a.base = base;
+    a.chunk_rows = m.chunk_rows;
+    a.n_var = m.n_var;
+    a.layout = m.layout;
+    a.vdt = m.value_dtype;
+    a.idt = m.index_dtype.value_or(IDtype::u32);
+    return a;
+}
+
+DStore::SlotRef DStore::acquire_slot(uint64_t bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (bytes > slot_bytes_) {  // first use (or a bigger block geometry): new pool
+        for (auto& s : free_)
+            if (s.released) cudaEventSynchronize(s.released), cudaEventDestroy(s.released);
+        free_.clear();
+        slot_bytes_ = align_up(std::max<uint64_t>(bytes, 1), 256);
+    }
+    if (free_.empty()) {  // grow by a slab of slots
+        const uint64_t n = 32;
+        void* slab = nullptr;
+        cuda_ok(cudaMalloc(&slab, n * slot_bytes_ + kPad), "cudaMalloc slab");
+        slabs_.push_back(slab);
+        for (uint64_t i = 0; i < n; ++i) {
+            SlotRef s;
+            s.ptr = static_cast<uint8_t*>(slab) + i * slot_bytes_;
+            s.bytes = slot_bytes_;
+            cuda_ok(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming), "event");
+            free_.push_back(s);
+        }
+    }
+    SlotRef s = free_.back();
+    free_.pop_back();
+    return s;
+}
+
+void DStore::release_slot(const SlotRef& s) {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (s.bytes == slot_bytes_) free_.push_back(s);
+    else if (s.released) cudaEventDestroy(s.released);  // from a retired pool geometry
+}
+
+// ============================================================== GpuLoader ===
+GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t epoch, const DeviceCfg& dev)
+    : ds_(std::move(ds)), cfg_(cfg), epoch_(epoch), dev_(dev), replay_(ds_->manifest().n_obs, cfg, epoch) {
+    const Manifest& m = ds_->manifest();
+    if (m.layout == Layout::dense && dev_.output == 0) invalid("csr output requested from a dense store");
+    if (dev_.normalize && (m.layout != Layout::csr || dev_.output != 1))
+        invalid("normalize_log1p applies to csr -> dense output");
+    if (dev_.out_slots == 0) dev_.out_slots = 2;
+    DeviceGuard g(ds_->device());
+    if (dev_.stream) {
+        compute_ = dev_.stream;
+    } else {
+        cuda_ok(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking), "stream");
+        own_compute_ = true;
+    }
+    cuda_ok(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "stream");
+    cuda_ok(cudaEventCreateWithFlags(&staged_, cudaEventDisableTiming), "event");
+    slots_.resize(dev_.out_slots);
+    for (auto& s : slots_) cuda_ok(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
+    if (ds_->staging() != kResident) {
+        live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
+        block_bytes_ = ds_->max_block_bytes(cfg_.f);
+        if (ds_->staging() == kStreamFile) {
+            pinned_.resize(std::max<uint32_t>(4, cfg_.prefetch_depth + 2));
+            const uint64_t bytes = block_bytes_;
+            for (auto& p : pinned_) {
+                cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&p.ptr), bytes, cudaHostAllocDefault), "pinned");
+                p.bytes = bytes;
+                cuda_ok(cudaEventCreateWithFlags(&p.free_ev, cudaEventDisableTiming), "event");
+            }
+        }
+    }
+}
+
+GpuLoader::~GpuLoader() {
+    DeviceGuard g(ds_->device());
+    if (compute_) cudaStreamSynchronize(compute_);
+    if (copy_) cudaStreamSynchronize(copy_);
+    for (auto& l : live_)
+        if (l.slot.ptr) {
+            cudaEventRecord(l.slot.released, compute_);
+            ds_->release_slot(l.slot);
+        }
+    for (auto& s : slots_) {
+        cudaFree(s.gidx);
+        cudaFree(s.indptr);
+        cudaFree(s.indices);
+        cudaFree(s.data);
+        cudaFree(s.scratch);
+        cudaFree(s.d_refs);
+        cudaFreeHost(s.h_refs);
+        cudaFreeHost(s.h_gidx);
+        cudaEventDestroy(s.done);
+    }
+    for (auto& p : pinned_) {
+        cudaFreeHost(p.ptr);
+        cudaEventDestroy(p.free_ev);
+    }
+    cudaEventDestroy(staged_);
+    cudaStreamDestroy(copy_);
+    if (own_compute_) cudaStreamDestroy(compute_);
+}
+
+void GpuLoader::stage_block(uint64_t id) {
+    const Manifest& m = ds_->manifest();
+    const uint64_t s = id * cfg_.f, e = std::min(m.n_obs, s + cfg_.f);
+    const uint64_t q0 = s / m.chunk_rows, q1 = (e - 1) / m.chunk_rows;
+    Live& lv = live_[id];
+    lv.first_chunk = q0;
+    lv.chunk_off.clear();
+    uint64_t bytes = 0;
+    for (uint64_t q = q0; q <= q1; ++q) {
+        lv.chunk_off.push_back(bytes);
+        bytes = align_up(bytes + ds_->rec_len()[q], kAlign);
+    }
+    lv.slot = ds_->acquire_slot(block_bytes_);
+    lv.live_rows = e - s;
+    cuda_ok(cudaStreamWaitEvent(copy_, lv.slot.released, 0), "wait slot");
+    const HostStore& hs = ds_->host();
+    if (ds_->staging() == kStreamPinned) {
+        // records of one block are contiguous in the pinned image except for alignment padding
+        const uint64_t img0 = ds_->rec_off()[q0];
+        const uint64_t img1 = ds_->rec_off()[q1] + ds_->rec_len()[q1];
+        cuda_ok(cudaMemcpyAsync(lv.slot.ptr, ds_->h_image() + img0, img1 - img0, cudaMemcpyHostToDevice, copy_),
+                "stage H2D");
+        for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->rec_off()[q] - img0;
+        ctr_.h2d_bytes += img1 - img0;
+        for (uint64_t q = q0; q <= q1; ++q)  // one read op per shard run, as store.cpp:427-447 counts
+            if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard) ctr_.read_ops += 1;
+        for (uint64_t q = q0; q <= q1; ++q) ctr_.bytes_read += ds_->rec_len()[q];
+    } else {
+        Pinned& p = pinned_[next_pinned_++ % pinned_.size()];
+        cuda_ok(cudaEventSynchronize(p.free_ev), "pinned reuse");
+        // coalesced pread of adjacent records of one shard (store.cpp:427-447)
+        uint64_t q = q0;
+        while (q <= q1) {
+            const uint64_t shard = q / m.chunks_per_shard;
+            const Slot first = hs.record_slot(q);
+            uint64_t end = q + 1, run = first.len;
+            while (end <= q1 && end / m.chunks_per_shard == shard) {
+                const Slot sl = hs.record_slot(end);
+                if (sl.off != first.off + run) break;
+                run += sl.len;
+                ++end;
+            }
+            // read the run contiguously, then place records at their aligned slot offsets
+            uint8_t* dst = p.ptr + lv.chunk_off[q - q0];
+            hs.read_shard_bytes(shard, first.off, dst, run, cfg_.cache_bypass);
+            // spread to aligned offsets; targets only move forward, so go back to front
+            std::vector<uint64_t> rel(end - q);
+            for (uint64_t k = q + 1; k < end; ++k) rel[k - q] = rel[k - q - 1] + ds_->rec_len()[k - 1];
+            for (uint64_t k = end - 1; k > q; --k)
+                std::memmove(p.ptr + lv.chunk_off[k - q0], dst + rel[k - q], ds_->rec_len()[k]);
+            ctr_.read_ops += 1;
+            ctr_.bytes_read += run;
+            q = end;
+        }
+        cuda_ok(cudaMemcpyAsync(lv.slot.ptr, p.ptr, bytes, cudaMemcpyHostToDevice, copy_), "stage H2D");
+        cuda_ok(cudaEventRecord(p.free_ev, copy_), "event");
+        ctr_.h2d_bytes += bytes;
+    }
+    ctr_.chunks_decoded += q1 - q0 + 1;
+}
+
+void GpuLoader::ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz) {
+    const Manifest& m = ds_->manifest();
+    const ArenaView av = ds_->view(nullptr);
+    if (rows > s.cap_rows) {
+        cudaFree(s.gidx);
+        cudaFree(s.indptr);
+        cudaFree(s.scratch);
+        cudaFree(s.d_refs);
+        cudaFreeHost(s.h_refs);
+        cudaFreeHost(s.h_gidx);
+        cuda_ok(cudaMalloc(&s.gidx, rows * 8), "malloc");
+        cuda_ok(cudaMalloc(&s.indptr, (rows + 1) * 8), "malloc");
+        cuda_ok(cudaMalloc(&s.scratch, csr_gather_scratch_bytes(rows)), "malloc");
+        cuda_ok(cudaMalloc(reinterpret_cast<void**>(&s.d_refs), rows * sizeof(RowRef)), "malloc");
+        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&s.h_refs), rows * sizeof(RowRef), cudaHostAllocDefault),
+                "pinned");
+        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&s.h_gidx), rows * 8, cudaHostAllocDefault), "pinned");
+        s.cap_rows = rows;
+        if (dev_.output == 1) {
+            cudaFree(s.data);
+            s.data_bytes = rows * m.n_var * dense_out_elem_size(av, dev_.out_dtype);
+            cuda_ok(cudaMalloc(&s.data, s.data_bytes + 16), "malloc");
+        }
+    }
+    if (dev_.output == 0 && nnz > s.cap_nnz) {
+        cudaFree(s.indices);
+        cudaFree(s.data);
+        const uint64_t cap = nnz + nnz / 8 + 1024;
+        cuda_ok(cudaMalloc(&s.indices, cap * index_size(av.idt) + 16), "malloc");
+        cuda_ok(cudaMalloc(&s.data, cap * value_size(av.vdt) + 16), "malloc");
+        s.cap_nnz = cap;
+    }
+}
+
+bool GpuLoader::next(BatchOut& out) {
+    if (done_) return false;
+    DeviceGuard g(ds_->device());
+    const Manifest& m = ds_->manifest();
+    if (!replay_.next(gidx_, consumed_)) {
+        done_ = true;
+        return false;
+    }
+    const bool resident = ds_->staging() == kResident;
+    if (!resident) {
+        for (uint64_t id : consumed_) stage_block(id);
+        cuda_ok(cudaEventRecord(staged_, copy_), "event");
+    }
+    OutSlot& s = slots_[next_slot_++ % slots_.size()];
+    if (s.used) cuda_ok(cudaEventSynchronize(s.done), "slot reuse");  // caller's view of it expires here
+    s.used = true;
+    const uint64_t n = gidx_.size();
+    uint64_t nnz = 0;
+    if (m.layout == Layout::csr)
+        for (uint64_t g : gidx_) nnz += ds_->row_nnz(g);
+    ensure_capacity(s, n, nnz);
+
+    // row references
+    const uint8_t* base = resident ? ds_->d_arena() : nullptr;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t gr = gidx_[i];
+        const uint64_t q = gr / m.chunk_rows;
+        if (resident) {
+            s.h_refs[i] = {ds_->rec_off()[q], gr};
+        } else {
+            const Live& lv = live_[gr / cfg_.f];
+            s.h_refs[i] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
+        }
+        s.h_gidx[i] = gr;
+    }
+    cuda_ok(cudaMemcpyAsync(s.d_refs, s.h_refs, n * sizeof(RowRef), cudaMemcpyHostToDevice, copy_), "refs H2D");
+    ctr_.h2d_bytes += n * sizeof(RowRef);
+    cuda_ok(cudaEventRecord(staged_, copy_), "event");
+    cuda_ok(cudaStreamWaitEvent(compute_, staged_, 0), "wait staged");
+
+    const ArenaView av = ds_->view(base);
+    if (m.layout == Layout::dense) {
+        launch_dense_gather(av, s.d_refs, n, dev_.out_dtype, s.data, static_cast<uint64_t*>(s.gidx), compute_);
+    } else if (dev_.output == 1) {
+        launch_csr_densify(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,
+                           static_cast<uint64_t*>(s.gidx), compute_);
+    } else {
+        launch_csr_gather(av, s.d_refs, n, static_cast<uint64_t*>(s.indptr), s.indices, s.data,
+                          static_cast<uint64_t*>(s.gidx), s.scratch, compute_);
+    }
+    ctr_.kernels_launched += 1;
+    cuda_ok(cudaEventRecord(s.done, compute_), "event");
+
+    // blocks whose rows are all taken go back to the pool once this batch's kernel is done
+    if (!resident) {
+        for (uint64_t i = 0; i < n; ++i) {
+            Live& lv = live_[gidx_[i] / cfg_.f];
+            if (--lv.live_rows == 0) {
+                cuda_ok(cudaEventRecord(lv.slot.released, compute_), "event");
+                ds_->release_slot(lv.slot);
+                lv.slot = DStore::SlotRef{};
+            }
+        }
+    }
+
+    out.epoch = epoch_;
+    out.batch_index = replay_.batch_index() - 1;
+    out.n_rows = n;
+    out.nnz = nnz;
+    out.n_var = m.n_var;
+    out.layout = (m.layout == Layout::csr && dev_.output == 0) ? 1u : 0u;
+    const uint32_t native = static_cast<uint32_t>(m.value_dtype);
+    out.dtype = out.layout == 1 ? native
+                                : (dev_.out_dtype == OutDtype::bf16 ? 4u : dev_.out_dtype == OutDtype::f32 ? 0u : native);
+    out.index_dtype = static_cast<uint32_t>(av.idt);
+    out.d_gidx = s.gidx;
+    out.d_indptr = out.layout == 1 ? s.indptr : nullptr;
+    out.d_indices = out.layout == 1 ? s.indices : nullptr;
+    out.d_data = s.data;
+    out.h_gidx = s.h_gidx;
+    out.ready = s.done;
+    return true;
+}
+
+Counters GpuLoader::counters() const {
+    Counters c = ctr_;
+    c.blocks_fetched = replay_.blocks_fetched();
+    c.peak_buffer_rows = replay_.peak_buffer_rows();
+    return c;
+}
+
+void GpuLoader::sync() {
+    DeviceGuard g(ds_->device());
+    cuda_ok(cudaStreamSynchronize(compute_), "sync");
+}
+
+}  // namespace rfl

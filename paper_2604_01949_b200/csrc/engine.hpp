@@ -1,0 +1,148 @@
+// Device-side store images and the GPU BatchIterator engine.
+//
+// The reference loop (loader.cpp:257-306) interleaves fetch, decode, buffer
+// maintenance and per-row copies on one thread.  Here the host only replays
+// the occupancy-driven schedule (schedule.hpp) and moves raw chunk records;
+// all payload bytes are moved by the sm_100a kernels (kernels.cuh).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "format.hpp"
+#include "kernels.cuh"
+#include "schedule.hpp"
+
+namespace rfl {
+
+enum Staging : uint32_t { kResident = 0, kStreamPinned = 1, kStreamFile = 2 };
+
+void cuda_ok(cudaError_t e, const char* what);
+
+struct DeviceGuard {  // sets and restores the current device
+    int prev = 0;
+    explicit DeviceGuard(int dev);
+    ~DeviceGuard();
+};
+
+// A store image: every chunk record at a 16-B aligned offset of a virtual
+// image, either resident in HBM, in pinned host memory, or left in the files.
+class DStore {
+public:
+    DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging);
+    ~DStore();
+    const Manifest& manifest() const { return hs_->manifest(); }
+    const HostStore& host() const { return *hs_; }
+    int device() const { return device_; }
+    uint32_t staging() const { return staging_; }
+    const uint8_t* d_arena() const { return d_arena_; }
+    const uint8_t* h_image() const { return h_image_; }
+    const std::vector<uint64_t>& rec_off() const { return rec_off_; }
+    const std::vector<uint64_t>& rec_len() const { return rec_len_; }
+    uint64_t image_bytes() const { return image_bytes_; }
+    uint64_t row_nnz(uint64_t row) const { return row_nnz_.empty() ? 0 : row_nnz_[row]; }
+    uint64_t max_block_bytes(uint64_t f) const;  // staged bytes of the largest f-row block
+    ArenaView view(const uint8_t* base) const;
+
+    // streaming slot pool (shared by the iterators over this store)
+    struct SlotRef {
+        uint8_t* ptr = nullptr;
+        cudaEvent_t released = nullptr;  // recorded after the last kernel reading it
+        uint64_t bytes = 0;
+    };
+    SlotRef acquire_slot(uint64_t bytes);
+    void release_slot(const SlotRef& s);
+
+private:
+    void load_records(bool to_device);
+    std::shared_ptr<HostStore> hs_;
+    int device_;
+    uint32_t staging_;
+    std::vector<uint64_t> rec_off_, rec_len_;
+    std::vector<uint32_t> row_nnz_;
+    uint64_t image_bytes_ = 0;
+    uint8_t* d_arena_ = nullptr;
+    uint8_t* h_image_ = nullptr;
+    std::mutex mu_;
+    std::vector<void*> slabs_;
+    std::vector<SlotRef> free_;
+    uint64_t slot_bytes_ = 0;
+};
+
+struct DeviceCfg {
+    uint32_t output = 1;     // 0 csr, 1 dense
+    OutDtype out_dtype = OutDtype::native;
+    bool normalize = false;
+    float target_sum = 1e4f;
+    uint32_t out_slots = 2;
+    cudaStream_t stream = nullptr;
+};
+
+struct BatchOut {
+    uint64_t epoch = 0, batch_index = 0, n_rows = 0, nnz = 0, n_var = 0;
+    uint32_t layout = 0, dtype = 0, index_dtype = 0;
+    void *d_gidx = nullptr, *d_indptr = nullptr, *d_indices = nullptr, *d_data = nullptr;
+    const uint64_t* h_gidx = nullptr;
+    cudaEvent_t ready = nullptr;
+};
+
+struct Counters {
+    uint64_t blocks_fetched = 0, read_ops = 0, bytes_read = 0, chunks_decoded = 0, peak_buffer_rows = 0,
+             h2d_bytes = 0, kernels_launched = 0;
+};
+
+class GpuLoader {
+public:
+    GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t epoch, const DeviceCfg& dev);
+    ~GpuLoader();
+    bool next(BatchOut& out);  // false at end of epoch (idempotent)
+    Counters counters() const;
+    void sync();
+
+private:
+    struct OutSlot {
+        void *gidx = nullptr, *indptr = nullptr, *indices = nullptr, *data = nullptr, *scratch = nullptr;
+        RowRef* d_refs = nullptr;
+        RowRef* h_refs = nullptr;
+        uint64_t* h_gidx = nullptr;
+        uint64_t cap_rows = 0, cap_nnz = 0, data_bytes = 0;
+        cudaEvent_t done = nullptr;
+        bool used = false;
+    };
+    struct Live {
+        DStore::SlotRef slot;
+        uint64_t live_rows = 0;
+        uint64_t first_chunk = 0;
+        std::vector<uint64_t> chunk_off;  // offset of each staged record inside the slot
+    };
+    void stage_block(uint64_t block_id);
+    void ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz);
+
+    std::shared_ptr<DStore> ds_;
+    LoaderCfg cfg_;
+    uint64_t epoch_;
+    DeviceCfg dev_;
+    EpochReplay replay_;
+    cudaStream_t compute_ = nullptr, copy_ = nullptr;
+    bool own_compute_ = false;
+    cudaEvent_t staged_ = nullptr;
+    std::vector<OutSlot> slots_;
+    uint64_t next_slot_ = 0;
+    std::vector<uint64_t> gidx_, consumed_;
+    std::vector<Live> live_;                 // indexed by block id (streaming)
+    uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
+    struct Pinned {
+        uint8_t* ptr = nullptr;
+        uint64_t bytes = 0;
+        cudaEvent_t free_ev = nullptr;
+    };
+    std::vector<Pinned> pinned_;
+    uint64_t next_pinned_ = 0;
+    Counters ctr_;
+    bool done_ = false;
+};
+
+}  // namespace rfl

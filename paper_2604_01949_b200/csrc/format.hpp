@@ -1,0 +1,161 @@
+// riffle on-disk store format, host side.  The format is the contract between
+// the reference and this build, so every byte written here matches the
+// reference writer:
+//   manifest.json         manifest.hpp:16-54, manifest.cpp:49-97 (nlohmann ordered dump(2))
+//   shards/s%08d.bin      shard.hpp:13-67, shard.cpp:18-103 (records, footer, SHRDIDX1)
+//   CSR chunk record      store.cpp:52-64 ([rows u32][nnz u64][indptr][indices][data])
+//   dense chunk record    store.cpp:31-33 (row-major values)
+#pragma once
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace rfl {
+
+// ---- errors (error.hpp:9-32) ------------------------------------------------
+enum Code : int { kOk = 0, kInvalid = 1, kCorrupt = 2, kIo = 3, kCuda = 4, kNccl = 5, kEnd = 6 };
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void invalid(const std::string& m) { throw Error(kInvalid, m); }
+[[noreturn]] inline void corrupt(const std::string& m) { throw Error(kCorrupt, m); }
+[[noreturn]] inline void ioerr(const std::string& m) { throw Error(kIo, m); }
+
+// ---- dtypes (dtype.hpp:10-40) -------------------------------------------------
+enum class Layout : uint8_t { dense = 0, csr = 1 };
+enum class VDtype : uint8_t { f32 = 0, f64 = 1, i32 = 2, u8 = 3 };
+enum class IDtype : uint8_t { u32 = 0, u64 = 1 };
+enum class Codec : uint8_t { none = 0, deflate = 1 };
+
+constexpr size_t value_size(VDtype d) {
+    return d == VDtype::f64 ? 8 : d == VDtype::u8 ? 1 : 4;
+}
+constexpr size_t index_size(IDtype d) { return d == IDtype::u32 ? 4 : 8; }
+const char* to_string(Layout l);
+const char* to_string(VDtype d);
+const char* to_string(IDtype d);
+const char* to_string(Codec c);
+
+// ---- manifest -------------------------------------------------------------------
+struct Manifest {
+    uint32_t format_version = 1;
+    Layout layout = Layout::dense;
+    uint64_t n_obs = 0;
+    uint64_t n_var = 0;
+    VDtype value_dtype = VDtype::f32;
+    std::optional<IDtype> index_dtype;
+    uint64_t chunk_rows = 1;
+    uint64_t chunks_per_shard = 1;
+    Codec codec = Codec::none;
+    std::vector<std::string> var_names;
+    bool has_provenance = false;
+
+    uint64_t chunk_count() const { return (n_obs + chunk_rows - 1) / chunk_rows; }
+    uint64_t shard_count() const { return (chunk_count() + chunks_per_shard - 1) / chunks_per_shard; }
+    uint64_t rows_in_chunk(uint64_t c) const {
+        const uint64_t s = c * chunk_rows;
+        return n_obs - s < chunk_rows ? n_obs - s : chunk_rows;
+    }
+    void validate() const;                      // manifest.cpp:34-47
+    std::string serialize() const;              // manifest.cpp:49-63 (dump(2) + "\n")
+    static Manifest parse(const std::string&);  // manifest.cpp:65-97
+};
+
+std::string shard_file_name(uint64_t shard_index);  // manifest.cpp:99-103
+std::string json_escape(const std::string& s);      // nlohmann dump string escaping
+
+// ---- low-level file I/O (file_io.hpp:23-127) ------------------------------------
+class File {
+public:
+    File() = default;
+    File(const File&) = delete;
+    File& operator=(const File&) = delete;
+    File(File&& o) noexcept : fd_(o.fd_) { o.fd_ = -1; }
+    File& operator=(File&& o) noexcept;
+    ~File();
+    static File open_read(const std::string& p);
+    static File try_open_direct(const std::string& p);
+    static File create_write(const std::string& p);
+    bool valid() const { return fd_ >= 0; }
+    uint64_t size() const;
+    void pread_exact(uint64_t off, void* dst, uint64_t n) const;
+    void write_all(const void* src, uint64_t n);
+
+private:
+    int fd_ = -1;
+};
+
+std::string read_text_file(const std::string& p);
+void write_text_file(const std::string& p, const std::string& text);
+void make_dirs(const std::string& p);
+bool path_exists(const std::string& p);
+bool dir_nonempty(const std::string& p);
+
+// ---- shards ------------------------------------------------------------------------
+struct Slot {
+    uint64_t off = ~0ull;
+    uint64_t len = ~0ull;
+    bool empty() const { return off == ~0ull; }
+};
+// ShardFooter::read (shard.cpp:18-54): magic, size, slot bounds, prefix occupancy.
+std::vector<Slot> read_footer(const File& f, const std::string& path, uint64_t slots);
+
+// ---- a finished store, host side ------------------------------------------------------
+// Thread-safe lazily-opened fds/footers, like StoreReader::Impl (store.cpp:301-368).
+class HostStore {
+public:
+    explicit HostStore(std::string root);
+    const Manifest& manifest() const { return man_; }
+    const std::string& root() const { return root_; }
+    Slot record_slot(uint64_t chunk) const;  // throws CorruptStore on empty slot
+    void read_record(uint64_t chunk, void* dst, uint64_t cap) const;
+    // pread an arbitrary byte range of one shard (coalesced runs, store.cpp:427-447)
+    void read_shard_bytes(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const;
+
+private:
+    const File& fd(uint64_t shard, bool direct) const;
+    std::string root_;
+    Manifest man_;
+    mutable std::mutex mu_;
+    mutable std::unordered_map<uint64_t, File> fds_, dfds_;
+    mutable std::unordered_map<uint64_t, std::vector<Slot>> footers_;
+};
+
+// ---- CSR record header accessors (store.cpp:52-64,81-122) ---------------------------
+constexpr uint64_t kCsrHeaderBytes = 12;
+inline uint32_t rd32(const uint8_t* p) { uint32_t v; std::memcpy(&v, p, 4); return v; }
+inline uint64_t rd64(const uint8_t* p) { uint64_t v; std::memcpy(&v, p, 8); return v; }
+inline void wr32(uint8_t* p, uint32_t v) { std::memcpy(p, &v, 4); }
+inline void wr64(uint8_t* p, uint64_t v) { std::memcpy(p, &v, 8); }
+
+// ---- append-only writer of pre-encoded records (StoreWriter, store.cpp:140-297) ----
+// Records are handed over already encoded (codec none); shards finalize as they fill.
+class RecordWriter {
+public:
+    RecordWriter(std::string root, Manifest man, bool defer_manifest, const char* shard_dir = "shards",
+                 bool write_manifest_file = true);
+    void append_record(const void* rec, uint64_t nbytes, uint64_t rows);
+    // finish(): flush shard footer, write manifest (n_obs = rows appended)
+    Manifest finish();
+    uint64_t rows() const { return man_.n_obs; }
+
+private:
+    void open_shard();
+    void close_shard();
+    std::string root_, shard_dir_;
+    Manifest man_;
+    bool write_manifest_file_;
+    std::optional<File> shard_;
+    std::vector<Slot> slots_;
+    uint64_t shard_bytes_ = 0, chunk_in_shard_ = 0, chunks_emitted_ = 0;
+    bool finished_ = false;
+};
+
+}  // namespace rfl

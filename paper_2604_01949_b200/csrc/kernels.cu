@@ -1,0 +1,596 @@
+// sm_100a kernels of the hot path (see kernels.cuh for the reference map).
+//
+// Data layout in HBM: the arena holds riffle chunk records verbatim
+// (store.cpp:52-64 for CSR, row-major rows for dense), each placed at a 16-B
+// aligned offset.  A batch is described by one RowRef per output row, so the
+// same kernels serve the HBM-resident store and the streamed block arena.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace rfl {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+struct ArenaDev {
+    const uint8_t* base;
+    uint64_t chunk_rows;
+    uint64_t n_var;
+};
+
+ArenaDev dev_view(const ArenaView& a) { return {a.base, a.chunk_rows, a.n_var}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- loads ------
+__device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {
+    return __ldg(reinterpret_cast<const unsigned int*>(p));
+}
+__device__ __forceinline__ uint64_t ld_u64_a4(const uint8_t* p) {  // 4-B aligned u64
+    return static_cast<uint64_t>(ld_u32(p)) | (static_cast<uint64_t>(ld_u32(p + 4)) << 32);
+}
+template <typename T>
+__device__ __forceinline__ uint64_t ld_index(const uint8_t* p);
+template <>
+__device__ __forceinline__ uint64_t ld_index<uint32_t>(const uint8_t* p) { return ld_u32(p); }
+template <>
+__device__ __forceinline__ uint64_t ld_index<uint64_t>(const uint8_t* p) { return ld_u64_a4(p); }
+
+template <typename T>
+__device__ __forceinline__ T ld_value(const uint8_t* p);
+template <>
+__device__ __forceinline__ float ld_value<float>(const uint8_t* p) { return __uint_as_float(ld_u32(p)); }
+template <>
+__device__ __forceinline__ int32_t ld_value<int32_t>(const uint8_t* p) { return static_cast<int32_t>(ld_u32(p)); }
+template <>
+__device__ __forceinline__ double ld_value<double>(const uint8_t* p) {
+    return __longlong_as_double(static_cast<long long>(ld_u64_a4(p)));
+}
+template <>
+__device__ __forceinline__ uint8_t ld_value<uint8_t>(const uint8_t* p) { return __ldg(p); }
+
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t ld_volatile_u64(const unsigned long long* p) {
+    uint64_t v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, uint64_t v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------- TMA bulk (1-D) store ---
+__device__ __forceinline__ void fence_proxy_async_shared() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ssrc))), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// ------------------------------------------------ 128-bit shifted warp copy ---
+// bytes [sh, sh+16) of the 32-byte little-endian string a||b (sh in 1..15)
+template <int WS>
+__device__ __forceinline__ uint4 merge_ws(const uint32_t (&w)[8], uint32_t bs) {
+    uint4 r;
+    r.x = __funnelshift_r(w[WS + 0], w[WS + 1], bs);
+    r.y = __funnelshift_r(w[WS + 1], w[WS + 2], bs);
+    r.z = __funnelshift_r(w[WS + 2], w[WS + 3], bs);
+    r.w = __funnelshift_r(w[WS + 3], w[WS + 4], bs);
+    return r;
+}
+__device__ __forceinline__ uint4 shift_merge(uint4 a, uint4 b, uint32_t sh) {
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t bs = (sh & 3u) * 8u;
+    switch (sh >> 2) {  // warp-uniform
+        case 0: return merge_ws<0>(w, bs);
+        case 1: return merge_ws<1>(w, bs);
+        case 2: return merge_ws<2>(w, bs);
+        default: return merge_ws<3>(w, bs);
+    }
+}
+
+// Warp-cooperative memcpy of n bytes between arbitrary alignments: byte head
+// up to the destination's 16-B boundary, then aligned 16-B stores fed by
+// aligned 16-B loads re-aligned with funnel shifts (neighbour chunk via shfl).
+__device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, uint64_t n,
+                                          uint32_t lane) {
+    if (n == 0) return;
+    uint32_t head = (16u - static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u;
+    if (head > n) head = static_cast<uint32_t>(n);
+    if (lane < head) dst[lane] = src[lane];
+    dst += head;
+    src += head;
+    n -= head;
+    const uint64_t nvec = n >> 4;
+    const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src) & 15u);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    if (sh == 0) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint64_t i = lane;
+        for (; i + 96 < nvec; i += 128) {
+            const uint4 v0 = ld_v4(s4 + i), v1 = ld_v4(s4 + i + 32), v2 = ld_v4(s4 + i + 64),
+                        v3 = ld_v4(s4 + i + 96);
+            st_v4(d4 + i, v0);
+            st_v4(d4 + i + 32, v1);
+            st_v4(d4 + i + 64, v2);
+            st_v4(d4 + i + 96, v3);
+        }
+        for (; i < nvec; i += 32) st_v4(d4 + i, ld_v4(s4 + i));
+    } else {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src - sh);
+        for (uint64_t base = 0; base < nvec; base += 64) {
+            const uint64_t i0 = base + lane, i1 = base + 32 + lane;
+            uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, t0, t1;
+            if (i0 < nvec) a0 = ld_v4(s4 + i0);
+            if (i1 < nvec) a1 = ld_v4(s4 + i1);
+            // chunk i+1: lane+1's chunk, or for lane 31 the next group's lane 0
+            t0.x = __shfl_down_sync(kFull, a0.x, 1);
+            t0.y = __shfl_down_sync(kFull, a0.y, 1);
+            t0.z = __shfl_down_sync(kFull, a0.z, 1);
+            t0.w = __shfl_down_sync(kFull, a0.w, 1);
+            t1.x = __shfl_down_sync(kFull, a1.x, 1);
+            t1.y = __shfl_down_sync(kFull, a1.y, 1);
+            t1.z = __shfl_down_sync(kFull, a1.z, 1);
+            t1.w = __shfl_down_sync(kFull, a1.w, 1);
+            const uint4 n0 = make_uint4(__shfl_sync(kFull, a1.x, 0), __shfl_sync(kFull, a1.y, 0),
+                                        __shfl_sync(kFull, a1.z, 0), __shfl_sync(kFull, a1.w, 0));
+            if (lane == 31) t0 = n0;
+            if (i0 < nvec) {
+                if (i0 + 1 >= nvec) t0 = ld_v4(s4 + i0 + 1);
+                st_v4(d4 + i0, shift_merge(a0, t0, sh));
+            }
+            if (i1 < nvec) {
+                if (lane == 31 || i1 + 1 >= nvec) t1 = ld_v4(s4 + i1 + 1);
+                st_v4(d4 + i1, shift_merge(a1, t1, sh));
+            }
+        }
+    }
+    const uint64_t done = nvec << 4;
+    const uint32_t rem = static_cast<uint32_t>(n - done);
+    if (lane < rem) dst[done + lane] = src[done + lane];
+}
+
+// ------------------------------------------------------- CSR record access ---
+struct CsrRow {
+    const uint8_t* idx;
+    const uint8_t* val;
+    uint64_t nnz;
+};
+
+// Locate a row inside its chunk record: [rows u32][nnz u64][indptr][indices][data]
+template <typename IdxT>
+__device__ __forceinline__ CsrRow csr_row(const ArenaDev& a, const RowRef& r, uint32_t vs) {
+    const uint8_t* rec = a.base + r.rec_off;
+    const uint64_t within = r.gidx % a.chunk_rows;
+    const uint32_t rows = ld_u32(rec);
+    const uint64_t nnz_chunk = ld_u64_a4(rec + 4);
+    const uint8_t* ip = rec + kCsrHeaderBytes;
+    const uint64_t lo = ld_index<IdxT>(ip + within * sizeof(IdxT));
+    const uint64_t hi = ld_index<IdxT>(ip + (within + 1) * sizeof(IdxT));
+    const uint8_t* idx_base = ip + (static_cast<uint64_t>(rows) + 1) * sizeof(IdxT);
+    const uint8_t* val_base = idx_base + nnz_chunk * sizeof(IdxT);
+    return {idx_base + lo * sizeof(IdxT), val_base + lo * vs, hi - lo};
+}
+
+// ============================================================ K1/K2 gather ===
+constexpr int kGatherThreads = 256;
+constexpr int kGatherTile = 16;  // rows per CTA
+constexpr uint64_t kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kGatherThreads) k_csr_gather(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs,
+                                                               uint64_t n_rows, uint64_t* __restrict__ out_indptr,
+                                                               uint8_t* __restrict__ out_idx,
+                                                               uint8_t* __restrict__ out_val,
+                                                               uint64_t* __restrict__ out_gidx,
+                                                               unsigned long long* __restrict__ scratch) {
+    __shared__ uint64_t s_off[kGatherTile];
+    __shared__ uint64_t s_nnz[kGatherTile];
+    __shared__ const uint8_t* s_idx[kGatherTile];
+    __shared__ const uint8_t* s_val[kGatherTile];
+    __shared__ uint64_t s_tile;
+    unsigned long long* counter = scratch;
+    unsigned long long* status = scratch + 1;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+
+    // dynamic tile ids make the look-back deadlock free (earlier tiles are resident)
+    if (tid == 0) s_tile = atomicAdd(counter, 1ull);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t row0 = tile * kGatherTile;
+
+    if (warp == 0) {
+        uint64_t nnz = 0;
+        if (lane < kGatherTile && row0 + lane < n_rows) {
+            const RowRef r = refs[row0 + lane];
+            const CsrRow cr = csr_row<IdxT>(a, r, vs);
+            s_idx[lane] = cr.idx;
+            s_val[lane] = cr.val;
+            s_nnz[lane] = cr.nnz;
+            nnz = cr.nnz;
+            if (out_gidx) out_gidx[row0 + lane] = r.gidx;
+        }
+        uint64_t incl = nnz;  // warp-level indptr scan
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += v;
+        }
+        const uint64_t agg = __shfl_sync(kFull, incl, 31);
+        // decoupled look-back over a 32-tile window
+        uint64_t prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) st_volatile_u64(&status[0], kFlagP | agg);
+        } else {
+            if (lane == 0) st_volatile_u64(&status[tile], kFlagA | agg);
+            int64_t end = static_cast<int64_t>(tile) - 1;
+            for (;;) {
+                const int64_t p = end - static_cast<int64_t>(lane);
+                const uint64_t s = p >= 0 ? ld_volatile_u64(&status[p]) : kFlagP;
+                const uint32_t flag = static_cast<uint32_t>(s >> 62);
+                const uint32_t pmask = __ballot_sync(kFull, flag == 2);
+                const uint32_t zmask = __ballot_sync(kFull, flag == 0);
+                const uint32_t first = pmask ? static_cast<uint32_t>(__ffs(pmask) - 1) : 31u;
+                const uint32_t need = first == 31u ? kFull : ((2u << first) - 1u);
+                if (zmask & need) continue;  // a predecessor has not published yet
+                prefix += warp_sum_u64(lane <= first ? (s & kValMask) : 0);
+                if (pmask) break;
+                end -= 32;
+            }
+            if (lane == 0) st_volatile_u64(&status[tile], kFlagP | (prefix + agg));
+        }
+        const uint64_t excl = prefix + incl - nnz;
+        if (lane < kGatherTile) s_off[lane] = excl;
+        if (lane < kGatherTile && row0 + lane < n_rows) out_indptr[row0 + lane] = excl;
+        if (lane == 0 && row0 + kGatherTile >= n_rows) out_indptr[n_rows] = prefix + agg;
+    }
+    __syncthreads();
+    for (uint32_t r = warp; r < static_cast<uint32_t>(kGatherTile); r += kGatherThreads / 32) {
+        if (row0 + r >= n_rows) break;
+        const uint64_t off = s_off[r], n = s_nnz[r];
+        warp_copy(out_idx + off * sizeof(IdxT), s_idx[r], n * sizeof(IdxT), lane);
+        warp_copy(out_val + off * vs, s_val[r], n * vs, lane);
+    }
+}
+
+// ============================================================ K3 densify =====
+constexpr int kDenseThreads = 512;
+constexpr uint32_t kMaxTileBytes = 100 * 1024;  // two CTAs per SM
+
+template <typename D, typename S>
+struct Conv {
+    __device__ static D go(S x, float scale, int norm);
+};
+template <typename S>
+struct Conv<float, S> {
+    __device__ static float go(S x, float scale, int norm) {
+        const float v = static_cast<float>(x);
+        return norm ? log1pf(v * scale) : v;
+    }
+};
+template <>
+struct Conv<float, double> {
+    __device__ static float go(double x, float scale, int norm) {
+        return norm ? log1pf(static_cast<float>(x * static_cast<double>(scale))) : static_cast<float>(x);
+    }
+};
+template <typename S>
+struct Conv<__nv_bfloat16, S> {
+    __device__ static __nv_bfloat16 go(S x, float scale, int norm) {
+        return __float2bfloat16_rn(Conv<float, S>::go(x, scale, norm));
+    }
+};
+template <>
+struct Conv<double, double> {
+    __device__ static double go(double x, float, int) { return x; }
+};
+template <>
+struct Conv<int32_t, int32_t> {
+    __device__ static int32_t go(int32_t x, float, int) { return x; }
+};
+template <>
+struct Conv<uint8_t, uint8_t> {
+    __device__ static uint8_t go(uint8_t x, float, int) { return x; }
+};
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += red[w];  // fixed order: deterministic
+    __syncthreads();
+    return t;
+}
+
+// One CTA per output row (grid-stride): zero a shared-memory tile, scatter the
+// row's entries into it, then a single cp.async.bulk store writes the dense
+// tile — every output byte hits HBM exactly once, with no read-modify-write.
+template <typename IdxT, typename SrcT, typename DstT>
+__global__ void __launch_bounds__(kDenseThreads, 2)
+    k_csr_densify(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
+                  float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ double s_red[kDenseThreads / 32];
+    DstT* tile = reinterpret_cast<DstT*>(smem);
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+    const uint64_t n_var = a.n_var;
+    constexpr uint32_t U = 4;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+        const RowRef r = refs[row];
+        const CsrRow cr = csr_row<IdxT>(a, r, sizeof(SrcT));
+        if (tid == 0 && out_gidx) out_gidx[row] = r.gidx;
+        float scale = 1.0f;
+        if (norm) {  // library size in fp64
+            double s = 0.0;
+            for (uint64_t k = tid; k < cr.nnz; k += nthr) s += static_cast<double>(ld_value<SrcT>(cr.val + k * sizeof(SrcT)));
+            s = block_sum(s, s_red);
+            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
+        }
+        DstT* orow = out + row * n_var;
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+            const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
+            const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
+            if (bulk && tid == 0) bulk_wait_read0();  // previous tile's bulk store has read smem
+            __syncthreads();
+            uint4* t4 = reinterpret_cast<uint4*>(smem);
+            for (uint32_t i = tid; i < bytes / 16u; i += nthr) t4[i] = make_uint4(0, 0, 0, 0);
+            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) smem[i] = 0;
+            __syncthreads();
+            uint64_t k = tid;
+            for (; k + (U - 1) * nthr < cr.nnz; k += U * nthr) {  // U independent loads in flight
+                uint64_t col[U];
+                SrcT v[U];
+#pragma unroll
+                for (uint32_t u = 0; u < U; ++u) {
+                    col[u] = ld_index<IdxT>(cr.idx + (k + u * nthr) * sizeof(IdxT));
+                    v[u] = ld_value<SrcT>(cr.val + (k + u * nthr) * sizeof(SrcT));
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < U; ++u)
+                    if (col[u] >= c0 && col[u] - c0 < cols) tile[col[u] - c0] = Conv<DstT, SrcT>::go(v[u], scale, norm);
+            }
+            for (; k < cr.nnz; k += nthr) {
+                const uint64_t col = ld_index<IdxT>(cr.idx + k * sizeof(IdxT));
+                if (col >= c0 && col - c0 < cols)
+                    tile[col - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(cr.val + k * sizeof(SrcT)), scale, norm);
+            }
+            if (bulk) {
+                fence_proxy_async_shared();  // make generic-proxy smem writes visible to the bulk engine
+                __syncthreads();
+                if (tid == 0) {
+                    bulk_store(orow + c0, smem, bytes);
+                    bulk_commit();
+                }
+            } else {
+                __syncthreads();
+                for (uint32_t i = tid; i < cols; i += nthr) orow[c0 + i] = tile[i];
+            }
+        }
+    }
+    if (bulk && tid == 0) bulk_wait0();
+}
+
+// ============================================================ K4 dense gather ===
+constexpr int kDenseGatherThreads = 256;
+enum DenseMode { kRaw = 0, kU8ToBf16 = 1, kF32ToBf16 = 2 };
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&p);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kDenseGatherThreads)
+    k_dense_gather(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
+                   uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5, nthr = blockDim.x;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+        const RowRef r = refs[row];
+        const uint8_t* src = a.base + r.rec_off + (r.gidx % a.chunk_rows) * in_row_bytes;
+        uint8_t* dst = out + row * out_row_bytes;
+        if (tid == 0 && out_gidx) out_gidx[row] = r.gidx;
+        if (MODE == kRaw) {
+            // split the row across warps on 16-B destination boundaries
+            const uint32_t nw = nthr / 32;
+            const uint64_t part = ((in_row_bytes + nw - 1) / nw + 15) & ~15ull;
+            const uint64_t s = warp * part;
+            if (s < in_row_bytes) warp_copy(dst + s, src + s, umin64(part, in_row_bytes - s), lane);
+        } else if (MODE == kU8ToBf16) {
+            const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15u) == 0;
+            const uint64_t nvec = vec ? in_row_bytes / 16 : 0;
+            for (uint64_t i = tid; i < nvec; i += nthr) {
+                const uint4 v = ld_v4(src + i * 16);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                uint32_t o[8];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    o[2 * j] = pack_bf16x2(float(w[j] & 0xff), float((w[j] >> 8) & 0xff));
+                    o[2 * j + 1] = pack_bf16x2(float((w[j] >> 16) & 0xff), float(w[j] >> 24));
+                }
+                st_v4(dst + i * 32, make_uint4(o[0], o[1], o[2], o[3]));
+                st_v4(dst + i * 32 + 16, make_uint4(o[4], o[5], o[6], o[7]));
+            }
+            __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dst);
+            for (uint64_t i = nvec * 16 + tid; i < in_row_bytes; i += nthr) d[i] = __float2bfloat16_rn(float(src[i]));
+        } else {  // f32 -> bf16 (records are 4-B aligned)
+            const uint64_t n = in_row_bytes / 4;
+            const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15u) | (reinterpret_cast<uintptr_t>(dst) & 7u)) == 0;
+            const uint64_t nvec = vec ? n / 4 : 0;
+            for (uint64_t i = tid; i < nvec; i += nthr) {
+                const uint4 v = ld_v4(src + i * 16);
+                uint2 o;
+                o.x = pack_bf16x2(__uint_as_float(v.x), __uint_as_float(v.y));
+                o.y = pack_bf16x2(__uint_as_float(v.z), __uint_as_float(v.w));
+                *reinterpret_cast<uint2*>(dst + i * 8) = o;
+            }
+            __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(dst);
+            for (uint64_t i = nvec * 4 + tid; i < n; i += nthr) d[i] = __float2bfloat16_rn(ld_value<float>(src + i * 4));
+        }
+    }
+}
+
+// ------------------------------------------------------------ host helpers ---
+int g_sm_count = 0;
+std::once_flag g_sm_once;
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
+               "cudaFuncSetAttribute");
+}
+
+template <typename IdxT, typename SrcT, typename DstT>
+void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
+               uint64_t* out_gidx, cudaStream_t st) {
+    const uint64_t esz = sizeof(DstT);
+    uint64_t tile_cols = av.n_var;
+    if (av.n_var * esz > kMaxTileBytes) tile_cols = (kMaxTileBytes / esz) & ~15ull;
+    const size_t smem = ((tile_cols * esz + 15) & ~15ull);
+    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    auto kern = k_csr_densify<IdxT, SrcT, DstT>;
+    set_smem(kern, smem);
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDenseThreads, smem), "occupancy");
+    const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
+    kern<<<static_cast<unsigned>(grid), kDenseThreads, smem, st>>>(dev_view(av), refs, n, static_cast<uint32_t>(tile_cols),
+                                                              norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx,
+                                                              bulk);
+    cuda_check(cudaGetLastError(), "k_csr_densify launch");
+}
+
+template <typename IdxT>
+void densify_idx(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, bool norm, float target, void* out,
+                 uint64_t* g, cudaStream_t st) {
+    switch (a.vdt) {
+        case VDtype::f32:
+            if (od == OutDtype::bf16) return densify_t<IdxT, float, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
+            return densify_t<IdxT, float, float>(a, refs, n, norm, target, out, g, st);
+        case VDtype::f64:
+            if (od == OutDtype::bf16) return densify_t<IdxT, double, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
+            if (od == OutDtype::f32) return densify_t<IdxT, double, float>(a, refs, n, norm, target, out, g, st);
+            return densify_t<IdxT, double, double>(a, refs, n, false, target, out, g, st);
+        case VDtype::i32:
+            if (od == OutDtype::bf16) return densify_t<IdxT, int32_t, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
+            if (od == OutDtype::f32) return densify_t<IdxT, int32_t, float>(a, refs, n, norm, target, out, g, st);
+            return densify_t<IdxT, int32_t, int32_t>(a, refs, n, false, target, out, g, st);
+        case VDtype::u8:
+            if (od == OutDtype::bf16) return densify_t<IdxT, uint8_t, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
+            if (od == OutDtype::f32) return densify_t<IdxT, uint8_t, float>(a, refs, n, norm, target, out, g, st);
+            return densify_t<IdxT, uint8_t, uint8_t>(a, refs, n, false, target, out, g, st);
+    }
+}
+
+}  // namespace
+
+int device_sm_count() {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    static int counts[64] = {0};
+    if (dev < 64 && counts[dev]) return counts[dev];
+    int c = 0;
+    cuda_check(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev), "sm count");
+    if (dev < 64) counts[dev] = c;
+    return c;
+}
+
+size_t csr_gather_scratch_bytes(uint64_t n_rows) {
+    const uint64_t tiles = (n_rows + kGatherTile - 1) / kGatherTile;
+    return (1 + tiles) * sizeof(unsigned long long);
+}
+
+void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_indptr, void* out_indices,
+                       void* out_data, uint64_t* out_gidx, void* scratch, cudaStream_t st) {
+    if (a.layout != Layout::csr) invalid("csr_gather: store is not csr");
+    if (n == 0) {
+        cuda_check(cudaMemsetAsync(out_indptr, 0, sizeof(uint64_t), st), "memset");
+        return;
+    }
+    cuda_check(cudaMemsetAsync(scratch, 0, csr_gather_scratch_bytes(n), st), "memset scratch");
+    const uint64_t tiles = (n + kGatherTile - 1) / kGatherTile;
+    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
+    auto* sc = static_cast<unsigned long long*>(scratch);
+    if (a.idt == IDtype::u32)
+        k_csr_gather<uint32_t><<<static_cast<unsigned>(tiles), kGatherThreads, 0, st>>>(
+            dev_view(a), vs, refs, n, out_indptr, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data),
+            out_gidx, sc);
+    else
+        k_csr_gather<uint64_t><<<static_cast<unsigned>(tiles), kGatherThreads, 0, st>>>(
+            dev_view(a), vs, refs, n, out_indptr, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data),
+            out_gidx, sc);
+    cuda_check(cudaGetLastError(), "k_csr_gather launch");
+}
+
+size_t dense_out_elem_size(const ArenaView& a, OutDtype od) {
+    if (od == OutDtype::bf16) return 2;
+    if (od == OutDtype::f32) return 4;
+    return value_size(a.vdt);
+}
+
+void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, bool norm, float target,
+                        void* out, uint64_t* out_gidx, cudaStream_t st) {
+    if (a.layout != Layout::csr) invalid("csr_densify: store is not csr");
+    if (norm && od == OutDtype::native && a.vdt != VDtype::f32)
+        invalid("csr_densify: normalize_log1p needs a floating output dtype (f32 or bf16)");
+    if (n == 0) return;
+    if (a.idt == IDtype::u32) densify_idx<uint32_t>(a, refs, n, od, norm, target, out, out_gidx, st);
+    else densify_idx<uint64_t>(a, refs, n, od, norm, target, out, out_gidx, st);
+}
+
+void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, void* out,
+                         uint64_t* out_gidx, cudaStream_t st) {
+    if (a.layout != Layout::dense) invalid("dense_gather: store is not dense");
+    if (n == 0) return;
+    const uint64_t in_rb = a.n_var * value_size(a.vdt);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, 8ull * device_sm_count()));
+    const ArenaDev d = dev_view(a);
+    auto* o = static_cast<uint8_t*>(out);
+    if (od == OutDtype::bf16) {
+        if (a.vdt == VDtype::u8)
+            k_dense_gather<kU8ToBf16><<<grid, kDenseGatherThreads, 0, st>>>(d, in_rb, refs, n, o, a.n_var * 2, out_gidx);
+        else if (a.vdt == VDtype::f32)
+            k_dense_gather<kF32ToBf16><<<grid, kDenseGatherThreads, 0, st>>>(d, in_rb, refs, n, o, a.n_var * 2, out_gidx);
+        else
+            invalid("dense_gather: bf16 cast supports u8 and f32 stores");
+    } else if (od == OutDtype::native || (od == OutDtype::f32 && a.vdt == VDtype::f32)) {
+        k_dense_gather<kRaw><<<grid, kDenseGatherThreads, 0, st>>>(d, in_rb, refs, n, o, in_rb, out_gidx);
+    } else {
+        invalid("dense_gather: unsupported output dtype for this store");
+    }
+    cuda_check(cudaGetLastError(), "k_dense_gather launch");
+}
+
+}  // namespace rfl

@@ -1,0 +1,54 @@
+// sm_100a kernels of the minibatch-assembly / pre-shuffle hot path.
+//
+//   K1/K2 csr_gather   rows -> CSR block, fused decoupled-look-back indptr scan
+//                      + warp-cooperative 128-bit shifted gathers
+//                      (CsrBuffer::take/append loader.cpp:126-155, read_rows_csr
+//                      store.cpp:590-614, CsrBlock::append_rows block.cpp:92-108)
+//   K3 csr_densify     rows -> dense tile built in shared memory, written once
+//                      with cp.async.bulk (TMA bulk) stores; optional fused
+//                      library-size normalisation + log1p (to_dense block.cpp:135-146)
+//   K4 dense_gather    dense rows -> batch with optional u8/f32 -> bf16 cast
+//                      (DenseBuffer::take loader.cpp:105-117)
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "format.hpp"
+
+namespace rfl {
+
+struct RowRef {  // == rfl_rowref
+    uint64_t rec_off;  // byte offset of the row's chunk record in the arena
+    uint64_t gidx;     // global row id; row-within-chunk = gidx % chunk_rows
+};
+
+struct ArenaView {
+    const uint8_t* base = nullptr;
+    uint64_t chunk_rows = 1;
+    uint64_t n_var = 0;
+    Layout layout = Layout::csr;
+    VDtype vdt = VDtype::f32;
+    IDtype idt = IDtype::u32;
+};
+
+enum class OutDtype : uint8_t { native = 0, f32 = 1, bf16 = 2 };
+
+int device_sm_count();
+
+// K1/K2.  scratch must hold csr_gather_scratch_bytes(n) bytes (zeroed by the launcher).
+size_t csr_gather_scratch_bytes(uint64_t n_rows);
+void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t* out_indptr,
+                       void* out_indices, void* out_data, uint64_t* out_gidx, void* scratch,
+                       cudaStream_t st);
+
+// K3
+void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
+                        float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);
+size_t dense_out_elem_size(const ArenaView& a, OutDtype od);
+
+// K4
+void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, void* out,
+                         uint64_t* out_gidx, cudaStream_t st);
+
+}  // namespace rfl

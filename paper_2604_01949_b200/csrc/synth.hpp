@@ -1,0 +1,31 @@
+// Synthetic store generators (product side).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "format.hpp"
+
+namespace rfl {
+
+// SynthConfig (reference include/riffle/synth.hpp:15-27)
+struct SynthCfg {
+    uint64_t n_obs = 0, n_var = 0;
+    Layout layout = Layout::dense;
+    VDtype value_dtype = VDtype::f32;
+    IDtype index_dtype = IDtype::u32;
+    double density = 0.01;
+    uint64_t seed = 0;
+    uint64_t chunk_rows = 1024, chunks_per_shard = 128;
+    Codec codec = Codec::none;
+    unsigned threads = 0;
+};
+
+// synth_store (reference src/synth.cpp:60-144), byte-identical output.
+Manifest synth_store(const std::string& path, const SynthCfg& c);
+
+// encode_csr_record (store.cpp:52-64) of rows [r0, r1) of an in-memory CSR.
+void encode_csr_rows(const uint64_t* indptr, const uint64_t* indices, const uint8_t* data, size_t vs, IDtype idt,
+                     uint64_t r0, uint64_t r1, std::vector<uint8_t>& rec);
+
+}  // namespace rfl
