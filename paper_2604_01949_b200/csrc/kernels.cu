@@ -200,6 +200,18 @@ __device__ __forceinline__ CsrRow csr_row(const ArenaDev& a, const RowRef& r, ui
     return {idx_base + lo * sizeof(IdxT), val_base + lo * vs, hi - lo};
 }
 
+struct RowDesc {
+    const uint8_t* idx;
+    const uint8_t* val;
+    uint64_t nnz;
+    uint64_t gidx;
+};
+template <typename IdxT>
+__device__ __forceinline__ RowDesc describe_row(const ArenaDev& a, const RowRef& r, uint32_t vs) {
+    const CsrRow c = csr_row<IdxT>(a, r, vs);
+    return {c.idx, c.val, c.nnz, r.gidx};
+}
+
 // ============================================================ K1/K2 gather ===
 constexpr int kGatherThreads = 256;
 constexpr int kGatherTile = 16;  // rows per CTA
@@ -345,18 +357,42 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ double s_red[kDenseThreads / 32];
+    __shared__ RowDesc s_desc[2];  // current / next row, software-pipelined
     DstT* tile = reinterpret_cast<DstT*>(smem);
     const uint32_t tid = threadIdx.x, nthr = blockDim.x;
     const uint64_t n_var = a.n_var;
-    constexpr uint32_t U = 4;
-    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
-        const RowRef r = refs[row];
-        const CsrRow cr = csr_row<IdxT>(a, r, sizeof(SrcT));
-        if (tid == 0 && out_gidx) out_gidx[row] = r.gidx;
+    constexpr uint32_t U = 4;  // entries per thread held in registers across the zero-fill
+    if (tid == 0 && blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
+    __syncthreads();
+    uint32_t cur = 0;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x, cur ^= 1u) {
+        const RowDesc d = s_desc[cur];
+        // 1. issue this row's first U*nthr entry loads; they land while the
+        //    previous row's bulk store drains and the tile is zeroed
+        uint64_t col[U];
+        SrcT v[U];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            const uint64_t k = tid + u * nthr;
+            col[u] = ~0ull;
+            if (k < d.nnz) {
+                col[u] = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
+                v[u] = ld_value<SrcT>(d.val + k * sizeof(SrcT));
+            }
+        }
+        // 2. the next row's record lookup (refs -> header -> indptr chain) in flight too
+        if (tid == 0) {
+            if (row + gridDim.x < n_rows) s_desc[cur ^ 1u] = describe_row<IdxT>(a, refs[row + gridDim.x], sizeof(SrcT));
+            if (out_gidx) out_gidx[row] = d.gidx;
+        }
         float scale = 1.0f;
         if (norm) {  // library size in fp64
             double s = 0.0;
-            for (uint64_t k = tid; k < cr.nnz; k += nthr) s += static_cast<double>(ld_value<SrcT>(cr.val + k * sizeof(SrcT)));
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u)
+                if (col[u] != ~0ull) s += static_cast<double>(v[u]);
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr)
+                s += static_cast<double>(ld_value<SrcT>(d.val + k * sizeof(SrcT)));
             s = block_sum(s, s_red);
             scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
         }
@@ -370,23 +406,27 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
             for (uint32_t i = tid; i < bytes / 16u; i += nthr) t4[i] = make_uint4(0, 0, 0, 0);
             for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) smem[i] = 0;
             __syncthreads();
-            uint64_t k = tid;
-            for (; k + (U - 1) * nthr < cr.nnz; k += U * nthr) {  // U independent loads in flight
-                uint64_t col[U];
-                SrcT v[U];
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u)
+                if (col[u] != ~0ull && col[u] >= c0 && col[u] - c0 < cols)
+                    tile[col[u] - c0] = Conv<DstT, SrcT>::go(v[u], scale, norm);
+            uint64_t k = tid + U * nthr;  // rows longer than U*nthr entries: stream the rest
+            for (; k + (U - 1) * nthr < d.nnz; k += U * nthr) {
+                uint64_t c2[U];
+                SrcT v2[U];
 #pragma unroll
                 for (uint32_t u = 0; u < U; ++u) {
-                    col[u] = ld_index<IdxT>(cr.idx + (k + u * nthr) * sizeof(IdxT));
-                    v[u] = ld_value<SrcT>(cr.val + (k + u * nthr) * sizeof(SrcT));
+                    c2[u] = ld_index<IdxT>(d.idx + (k + u * nthr) * sizeof(IdxT));
+                    v2[u] = ld_value<SrcT>(d.val + (k + u * nthr) * sizeof(SrcT));
                 }
 #pragma unroll
                 for (uint32_t u = 0; u < U; ++u)
-                    if (col[u] >= c0 && col[u] - c0 < cols) tile[col[u] - c0] = Conv<DstT, SrcT>::go(v[u], scale, norm);
+                    if (c2[u] >= c0 && c2[u] - c0 < cols) tile[c2[u] - c0] = Conv<DstT, SrcT>::go(v2[u], scale, norm);
             }
-            for (; k < cr.nnz; k += nthr) {
-                const uint64_t col = ld_index<IdxT>(cr.idx + k * sizeof(IdxT));
-                if (col >= c0 && col - c0 < cols)
-                    tile[col - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(cr.val + k * sizeof(SrcT)), scale, norm);
+            for (; k < d.nnz; k += nthr) {
+                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
+                if (c2 >= c0 && c2 - c0 < cols)
+                    tile[c2 - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(d.val + k * sizeof(SrcT)), scale, norm);
             }
             if (bulk) {
                 fence_proxy_async_shared();  // make generic-proxy smem writes visible to the bulk engine

@@ -168,7 +168,7 @@ def test_densify_tiles_and_unaligned(tmp_path, n_var, vdt, od):
     multiple of 16 (generic store path), plus empty rows."""
     rng = np.random.default_rng(n_var)
     n = 150
-    nnz = rng.integers(0, 400, n)
+    nnz = np.minimum(rng.integers(0, 400, n), n_var)
     nnz[::7] = 0
     nnz[3] = min(n_var, 5000)
     ip = np.zeros(n + 1, np.uint64)
