@@ -199,10 +199,11 @@ def test_empty_rows_and_edges(tmp_path):
     for f, B, b, dl in [(2, 4, 3, False), (1, 6, 6, False), (6, 6, 4, True), (3, 3, 1, False)]:
         ref = list(Ref.iterate(tmp_path / "s", f, B, b, drop_last=dl, want="csr,to_dense"))
         for out in ("csr", "dense"):
-            got = list(R.BatchIterator(tmp_path / "s", R.LoaderConfig(f, B, b, drop_last=dl), 0, output=out))
+            # batches are views into the loader's output ring: materialise each before the next
+            got = [g.to_minibatch()
+                   for g in R.BatchIterator(tmp_path / "s", R.LoaderConfig(f, B, b, drop_last=dl), 0, output=out)]
             assert len(got) == len(ref)
-            for r, g in zip(ref, got):
-                m = g.to_minibatch()
+            for r, m in zip(ref, got):
                 assert (m.global_indices == r["gidx"]).all()
                 if out == "csr":
                     assert (m.block.indptr == r["indptr"]).all() and (m.block.indices == r["indices"]).all()
