@@ -87,7 +87,7 @@ class Ref:
             L.ref_read_rows_dense.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
             L.ref_plan_shuffle.argtypes = [C.c_uint64] * 4 + [u64p, C.c_void_p, C.c_void_p]
             L.ref_run_shuffle.argtypes = [C.POINTER(C.c_char_p), C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
-                                          C.c_uint64, C.c_char_p, C.c_uint64, C.c_uint64, u64p, u64p]
+                                          C.c_uint64, C.c_char_p, C.c_uint64, C.c_uint64, C.c_int, u64p, u64p]
             L.ref_throughput.restype = C.c_double
             L.ref_throughput.argtypes = [C.c_char_p] + [C.c_uint64] * 4 + [C.c_uint32, C.c_uint64, C.c_uint32,
                                                                           C.c_uint64, C.c_int, u64p,
@@ -222,11 +222,12 @@ class Ref:
         return out
 
     @classmethod
-    def run_shuffle(cls, in_paths, out_path, c, m, seed, out_chunk_rows, out_cps, outer=True):
+    def run_shuffle(cls, in_paths, out_path, c, m, seed, out_chunk_rows, out_cps, outer=True, out_idt=None):
         arr = (C.c_char_p * len(in_paths))(*[str(p).encode() for p in in_paths])
         peak, rounds = C.c_uint64(), C.c_uint64()
         cls.check(cls.lib().ref_run_shuffle(arr, len(in_paths), int(outer), c, m, seed, str(out_path).encode(),
-                                            out_chunk_rows, out_cps, C.byref(peak), C.byref(rounds)))
+                                            out_chunk_rows, out_cps, -1 if out_idt is None else IDT[out_idt],
+                                            C.byref(peak), C.byref(rounds)))
         return {"peak_resident_rows": peak.value, "rounds": rounds.value}
 
     @classmethod

@@ -255,7 +255,7 @@ int ref_plan_shuffle(uint64_t total_rows, uint64_t c, uint64_t m, uint64_t seed,
 
 int ref_run_shuffle(const char* const* in_paths, uint64_t n_in, int outer_join, uint64_t c,
                     uint64_t m, uint64_t seed, const char* out_path, uint64_t out_chunk_rows,
-                    uint64_t out_cps, uint64_t* peak_resident, uint64_t* rounds) {
+                    uint64_t out_cps, int out_idt, uint64_t* peak_resident, uint64_t* rounds) {
     try {
         DatasetCollection coll(outer_join ? JoinMode::outer : JoinMode::inner);
         for (uint64_t i = 0; i < n_in; ++i) coll.add(std::make_shared<const StoreReader>(in_paths[i]));
@@ -263,6 +263,7 @@ int ref_run_shuffle(const char* const* in_paths, uint64_t n_in, int outer_join, 
         ShuffleOutputConfig oc;
         oc.chunk_rows = out_chunk_rows;
         oc.chunks_per_shard = out_cps;
+        if (out_idt >= 0) oc.index_dtype = static_cast<IndexDtype>(out_idt);
         ShuffleRunStats st;
         run_shuffle(coll, plan, out_path, oc, &st);
         if (peak_resident) *peak_resident = st.peak_resident_rows;

@@ -289,11 +289,65 @@ __global__ void __launch_bounds__(kGatherThreads) k_csr_gather(ArenaDev a, uint3
         if (lane == 0 && row0 + kGatherTile >= n_rows) out_indptr[n_rows] = prefix + agg;
     }
     __syncthreads();
+    if (out_idx == nullptr) return;  // scan-only launch (pre-shuffle record offsets)
     for (uint32_t r = warp; r < static_cast<uint32_t>(kGatherTile); r += kGatherThreads / 32) {
         if (row0 + r >= n_rows) break;
         const uint64_t off = s_off[r], n = s_nnz[r];
         warp_copy(out_idx + off * sizeof(IdxT), s_idx[r], n * sizeof(IdxT), lane);
         warp_copy(out_val + off * vs, s_val[r], n * vs, lane);
+    }
+}
+
+// ============================================================ K5 record pack ===
+template <typename T>
+__device__ __forceinline__ void st_any(uint8_t* p, T v) {  // little-endian store at any alignment
+    if ((reinterpret_cast<uintptr_t>(p) & (sizeof(T) - 1)) == 0) {
+        *reinterpret_cast<T*>(p) = v;
+        return;
+    }
+    for (uint32_t b = 0; b < sizeof(T); ++b) p[b] = static_cast<uint8_t>(static_cast<uint64_t>(v) >> (8 * b));
+}
+
+constexpr int kPackThreads = 256;
+
+// Rows refs[0..n) -> consecutive encoded CSR chunk records of `cr` rows
+// (encode_csr_record, store.cpp:52-64; only the last chunk may be short).  With
+// P the exclusive nnz prefix over the launch, every record offset is closed
+// form: record q starts at q*(12 + os*(cr+1)) + (os+vs)*P[q*cr].  One warp per
+// row writes its indptr entry and copies its indices/values straight into
+// place, so the payload moves HBM->HBM exactly once.
+template <typename InIdx, typename OutIdx>
+__global__ void __launch_bounds__(kPackThreads)
+    k_csr_pack(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, uint64_t n_rows, uint64_t cr,
+               const uint64_t* __restrict__ P, uint8_t* __restrict__ out) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (kPackThreads / 32);
+    constexpr uint64_t os = sizeof(OutIdx);
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (kPackThreads / 32) + warp; i < n_rows; i += nw) {
+        const uint64_t q = i / cr, r0 = q * cr;
+        const uint64_t rows_q = umin64(cr, n_rows - r0);
+        const uint64_t p0 = P[r0], nnz_q = P[r0 + rows_q] - p0;
+        uint8_t* rec = out + q * (kCsrHeaderBytes + os * (cr + 1)) + (os + vs) * p0;
+        uint8_t* ip = rec + kCsrHeaderBytes;
+        uint8_t* idx = ip + os * (rows_q + 1);
+        uint8_t* val = idx + os * nnz_q;
+        const uint64_t lo = P[i] - p0, hi = P[i + 1] - p0;
+        if (lane == 0) {
+            if (i == r0) {
+                st_any<uint32_t>(rec, static_cast<uint32_t>(rows_q));
+                st_any<uint64_t>(rec + 4, nnz_q);
+                st_any<OutIdx>(ip, OutIdx(0));
+            }
+            st_any<OutIdx>(ip + os * (i - r0 + 1), static_cast<OutIdx>(hi));
+        }
+        const CsrRow src = csr_row<InIdx>(a, refs[i], vs);
+        if (sizeof(InIdx) == sizeof(OutIdx)) {
+            warp_copy(idx + os * lo, src.idx, (hi - lo) * os, lane);
+        } else {
+            for (uint64_t k = lane; k < hi - lo; k += 32)
+                st_any<OutIdx>(idx + os * (lo + k), static_cast<OutIdx>(ld_index<InIdx>(src.idx + k * sizeof(InIdx))));
+        }
+        warp_copy(val + vs * lo, src.val, (hi - lo) * vs, lane);
     }
 }
 
@@ -592,6 +646,30 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
             dev_view(a), vs, refs, n, out_indptr, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data),
             out_gidx, sc);
     cuda_check(cudaGetLastError(), "k_csr_gather launch");
+}
+
+void launch_csr_row_scan(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_prefix, void* scratch,
+                         cudaStream_t st) {
+    launch_csr_gather(a, refs, n, out_prefix, nullptr, nullptr, nullptr, scratch, st);
+}
+
+void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t chunk_rows, IDtype out_idt,
+                     const uint64_t* prefix, uint8_t* out, cudaStream_t st) {
+    if (a.layout != Layout::csr) invalid("csr_pack: store is not csr");
+    if (n == 0) return;
+    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
+    const unsigned grid =
+        static_cast<unsigned>(std::min<uint64_t>((n + kPackThreads / 32 - 1) / (kPackThreads / 32), 16ull * device_sm_count()));
+    const ArenaDev d = dev_view(a);
+    if (a.idt == IDtype::u32 && out_idt == IDtype::u32)
+        k_csr_pack<uint32_t, uint32_t><<<grid, kPackThreads, 0, st>>>(d, vs, refs, n, chunk_rows, prefix, out);
+    else if (a.idt == IDtype::u32)
+        k_csr_pack<uint32_t, uint64_t><<<grid, kPackThreads, 0, st>>>(d, vs, refs, n, chunk_rows, prefix, out);
+    else if (out_idt == IDtype::u32)
+        k_csr_pack<uint64_t, uint32_t><<<grid, kPackThreads, 0, st>>>(d, vs, refs, n, chunk_rows, prefix, out);
+    else
+        k_csr_pack<uint64_t, uint64_t><<<grid, kPackThreads, 0, st>>>(d, vs, refs, n, chunk_rows, prefix, out);
+    cuda_check(cudaGetLastError(), "k_csr_pack launch");
 }
 
 size_t dense_out_elem_size(const ArenaView& a, OutDtype od) {

@@ -42,6 +42,15 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, 
                        void* out_indices, void* out_data, uint64_t* out_gidx, void* scratch,
                        cudaStream_t st);
 
+// K1/K2 scan only: out_prefix[i] = exclusive nnz prefix of rows, out_prefix[n] = total.
+void launch_csr_row_scan(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t* out_prefix, void* scratch,
+                         cudaStream_t st);
+
+// K5: rows -> consecutive encoded CSR chunk records of chunk_rows rows each
+// (encode_csr_record, store.cpp:52-64); `prefix` from launch_csr_row_scan.
+void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t chunk_rows, IDtype out_idt,
+                     const uint64_t* prefix, uint8_t* out, cudaStream_t st);
+
 // K3
 void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
                         float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);

@@ -78,6 +78,11 @@ def run_shuffle(inputs, plan: ShufflePlan, out_path, out_config: ShuffleOutputCo
     oc = out_config or ShuffleOutputConfig()
     if oc.codec != "none":
         raise L.InvalidArgument("GPU pre-shuffle writes codec none only")
+    if inputs:
+        from .store import StoreReader
+        held = sum(StoreReader(p).manifest().n_obs for p in inputs)
+        if plan.total_rows != held:  # preshuffle.cpp:191-194
+            raise L.InvalidArgument(f"run_shuffle: plan covers {plan.total_rows} rows, collection holds {held}")
     paths = [str(p).encode() for p in inputs]
     arr = (C.c_char_p * len(paths))(*paths)
     cfg = L.rfl_shuffle_config(plan.block_rows, plan.buffer_rows, plan.seed, oc.chunk_rows, oc.chunks_per_shard,

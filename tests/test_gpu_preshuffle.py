@@ -1,0 +1,93 @@
+"""GPU pre-shuffle parity: the device writer's output store + provenance
+sidecar are byte-identical to the reference run_shuffle (golden digests and
+live oracle/_ref runs), including multi-member collections, chunks that
+straddle rounds (out chunk_rows > m), index-dtype conversion and dense stores."""
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2604_01949_b200 as R
+from oracle.oracle import Orc, Ref
+
+pytestmark = pytest.mark.gpu
+
+
+def digests(root: Path):
+    return {p.relative_to(root).as_posix(): hex(Orc.fnv1a64(np.frombuffer(p.read_bytes(), np.uint8)))
+            for p in sorted(root.rglob("*")) if p.is_file()}
+
+
+def same_tree(a: Path, b: Path):
+    fa = sorted(p.relative_to(a).as_posix() for p in a.rglob("*") if p.is_file())
+    fb = sorted(p.relative_to(b).as_posix() for p in b.rglob("*") if p.is_file())
+    assert fa == fb
+    for f in fa:
+        assert (a / f).read_bytes() == (b / f).read_bytes(), f
+
+
+def test_golden_shuffles(golden, golden_stores, tmp_path):
+    for case in golden["run_shuffle"]:
+        out = tmp_path / f"gpu_{case['store']}"
+        plan = R.plan_shuffle(golden["stores"][case["store"]]["n_obs"], case["c"], case["m"], case["seed"])
+        st = R.run_shuffle([golden_stores[case["store"]]], plan, out,
+                           R.ShuffleOutputConfig(case["out_chunk_rows"], case["out_cps"]))
+        assert digests(out) == case["files"], case["store"]
+        assert st.peak_resident_rows == case["peak_resident_rows"]
+        assert st.rounds_executed == case["rounds"]
+
+
+@pytest.mark.parametrize("c,m,ocr,ocps,seed", [(64, 512, 100, 4, 7), (7, 50, 333, 2, 1), (1, 40, 16, 3, 2),
+                                               (500, 500, 64, 128, 3), (13, 13, 13, 1, 4)])
+def test_live_reference_multi_member(tmp_path, c, m, ocr, ocps, seed):
+    """Two members (identity columns), rounds crossing members, carried chunks."""
+    a, b = tmp_path / "a", tmp_path / "b"
+    R.synth_store(a, R.SynthConfig(700, 90, "csr", "f32", "u32", 0.1, 1, 32, 4))
+    R.synth_store(b, R.SynthConfig(333, 90, "csr", "f32", "u32", 0.2, 2, 50, 2))
+    Ref.run_shuffle([a, b], tmp_path / "ref", c, m, seed, ocr, ocps)
+    plan = R.plan_shuffle(1033, c, m, seed)
+    R.run_shuffle([a, b], plan, tmp_path / "gpu", R.ShuffleOutputConfig(ocr, ocps))
+    same_tree(tmp_path / "ref", tmp_path / "gpu")
+
+
+@pytest.mark.parametrize("layout,vdt,idt,out_idt", [("csr", "f64", "u64", "u32"), ("csr", "u8", "u32", "u64"),
+                                                    ("dense", "f32", "u32", None), ("dense", "u8", "u32", None),
+                                                    ("csr", "i32", "u32", None)])
+def test_live_reference_dtypes(tmp_path, layout, vdt, idt, out_idt):
+    R.synth_store(tmp_path / "in", R.SynthConfig(1500, 37, layout, vdt, idt, 0.15, 5, 64, 3))
+    Ref.run_shuffle([tmp_path / "in"], tmp_path / "ref", 16, 200, 11, 77, 3, out_idt=out_idt)
+    R.run_shuffle([tmp_path / "in"], R.plan_shuffle(1500, 16, 200, 11), tmp_path / "gpu",
+                  R.ShuffleOutputConfig(77, 3, index_dtype=out_idt))
+    same_tree(tmp_path / "ref", tmp_path / "gpu")
+
+
+def test_shuffle_provenance_is_the_order(tmp_path):
+    R.synth_store(tmp_path / "in", R.SynthConfig(5000, 20, "csr", "f32", "u32", 0.2, 0, 100, 8))
+    R.run_shuffle([tmp_path / "in"], R.plan_shuffle(5000, 50, 1000, 3), tmp_path / "out",
+                  R.ShuffleOutputConfig(256, 4))
+    # column 0 carries the source row id (synth identity channel): read it back through the GPU loader
+    it = R.BatchIterator(tmp_path / "out", R.LoaderConfig(256, 256, 256, 0), 0, output="csr")
+    ids = {}
+    for bt in it:
+        mb = bt.to_minibatch()
+        for k, g in enumerate(mb.global_indices):
+            lo = int(mb.block.indptr[k])
+            assert mb.block.indices[lo] == 0
+            ids[int(g)] = int(mb.block.data[lo])
+    order = R.shuffle_order(5000, 50, 1000, 3)
+    assert [ids[o] for o in range(5000)] == order.tolist()
+
+
+def test_shuffle_errors(tmp_path):
+    R.synth_store(tmp_path / "a", R.SynthConfig(100, 10, "csr", density=0.3, chunk_rows=10))
+    R.synth_store(tmp_path / "d", R.SynthConfig(100, 10, "dense", chunk_rows=10))
+    (tmp_path / "busy").mkdir()
+    (tmp_path / "busy" / "x").write_text("x")
+    plan = R.plan_shuffle(100, 10, 30, 0)
+    with pytest.raises(R.InvalidArgument, match="not fresh"):
+        R.run_shuffle([tmp_path / "a"], plan, tmp_path / "busy")
+    with pytest.raises(R.InvalidArgument, match="empty collection"):
+        R.run_shuffle([], plan, tmp_path / "o1")
+    with pytest.raises(R.InvalidArgument, match="layout"):
+        R.run_shuffle([tmp_path / "a", tmp_path / "d"], R.plan_shuffle(200, 10, 30, 0), tmp_path / "o2")
