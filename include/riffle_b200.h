@@ -239,6 +239,17 @@ rfl_status rfl_plan_shuffle(uint64_t total_rows, uint64_t block_rows, uint64_t b
 rfl_status rfl_shuffle_order(uint64_t total_rows, uint64_t block_rows, uint64_t buffer_rows,
                              uint64_t seed, uint64_t* out_src);
 
+/* Multi-GPU routing of round `round`: for each of its output rows
+ * in output order (global output row = first_out_row + k): the global input
+ * row, the source rank (block b of the round is staged by rank b mod world)
+ * and the destination rank (owner of output shard s == rank (mod world)).
+ * Pass NULL arrays to learn n_rows. */
+rfl_status rfl_shuffle_round_routes(uint64_t total_rows, uint64_t block_rows, uint64_t buffer_rows,
+                                    uint64_t seed, uint64_t out_chunk_rows, uint64_t out_chunks_per_shard,
+                                    uint32_t world, uint64_t round, uint64_t* first_out_row,
+                                    uint64_t* n_rows, uint64_t* src_rows, uint32_t* src_rank,
+                                    uint32_t* dst_rank);
+
 typedef struct rfl_shuffle_config {
     uint64_t block_rows;  /* c */
     uint64_t buffer_rows; /* m */
@@ -267,6 +278,36 @@ typedef struct rfl_shuffle_stats {
  * store + provenance sidecar. */
 rfl_status rfl_run_shuffle(const char* const* in_paths, uint64_t n_inputs, const char* out_path,
                            const rfl_shuffle_config* cfg, rfl_shuffle_stats* stats);
+
+/* Multi-GPU pre-shuffle, one process per GPU.  Per round:
+ *   rfl_pshuf_stage   stage this rank's blocks (block b of the round -> rank
+ *                     b mod world), scan its rows per destination, report the
+ *                     message bytes per destination rank;
+ *   (caller all-gathers the world x world size matrix)
+ *   rfl_pshuf_recv_buffer  receive area >= the bytes addressed to this rank,
+ *                     with its CUDA IPC handle (64 bytes) for the peers;
+ *   rfl_pshuf_send    one K5 pack kernel per destination writes the rows,
+ *                     already encoded as a CSR record, straight into the
+ *                     owner's receive buffer through peer memory (NVLink),
+ *                     at dst[d] = peer base + sum of aligned sizes of lower
+ *                     source ranks;
+ *   (caller barrier)
+ *   rfl_pshuf_emit    owner: pack the now-complete owned chunks (shards
+ *                     s == rank mod world) and write them + provenance.
+ * rfl_pshuf_finish flushes this rank's shards; rank 0 writes manifest.json and
+ * provenance/meta.json (call after a barrier on the other ranks' finish). */
+typedef struct rfl_pshuf rfl_pshuf;
+rfl_status rfl_pshuf_create(const char* const* in_paths, uint64_t n_inputs, const char* out_path,
+                            const rfl_shuffle_config* cfg, rfl_pshuf** out, uint64_t* n_rounds);
+rfl_status rfl_pshuf_stage(rfl_pshuf* h, uint64_t round, uint64_t* send_bytes);
+rfl_status rfl_pshuf_recv_buffer(rfl_pshuf* h, uint64_t bytes, void** dev_ptr, void* ipc_handle, int* changed);
+rfl_status rfl_pshuf_send(rfl_pshuf* h, uint64_t round, void* const* dst);
+rfl_status rfl_pshuf_emit(rfl_pshuf* h, uint64_t round, const uint64_t* recv_bytes);
+rfl_status rfl_pshuf_finish(rfl_pshuf* h, rfl_shuffle_stats* stats);
+void rfl_pshuf_destroy(rfl_pshuf* h);
+/* CUDA IPC helpers for the receive buffers of peer processes */
+rfl_status rfl_ipc_open(const void* ipc_handle, int device, void** dev_ptr);
+rfl_status rfl_ipc_close(void* dev_ptr, int device);
 
 #ifdef __cplusplus
 }

@@ -113,6 +113,17 @@ SIGNATURES = [
     ("rfl_dense_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, vp, vp, vp]),
     ("rfl_plan_shuffle", C.c_int, [u64, u64, u64, u64, u64p, vp, vp]),
     ("rfl_shuffle_order", C.c_int, [u64, u64, u64, u64, vp]),
+    ("rfl_shuffle_round_routes", C.c_int, [u64, u64, u64, u64, u64, u64, u32, u64, u64p, u64p, vp, vp, vp]),
+    ("rfl_pshuf_create", C.c_int, [C.POINTER(C.c_char_p), u64, C.c_char_p, C.POINTER(rfl_shuffle_config),
+                                   C.POINTER(vp), u64p]),
+    ("rfl_pshuf_stage", C.c_int, [vp, u64, vp]),
+    ("rfl_pshuf_recv_buffer", C.c_int, [vp, u64, C.POINTER(vp), vp, C.POINTER(C.c_int)]),
+    ("rfl_pshuf_send", C.c_int, [vp, u64, C.POINTER(vp)]),
+    ("rfl_pshuf_emit", C.c_int, [vp, u64, vp]),
+    ("rfl_pshuf_finish", C.c_int, [vp, C.POINTER(rfl_shuffle_stats)]),
+    ("rfl_pshuf_destroy", None, [vp]),
+    ("rfl_ipc_open", C.c_int, [vp, C.c_int, C.POINTER(vp)]),
+    ("rfl_ipc_close", C.c_int, [vp, C.c_int]),
     ("rfl_run_shuffle", C.c_int, [C.POINTER(C.c_char_p), u64, C.c_char_p, C.POINTER(rfl_shuffle_config),
                                   C.POINTER(rfl_shuffle_stats)]),
 ]

@@ -376,34 +376,135 @@ rfl_status rfl_shuffle_order(uint64_t total, uint64_t c, uint64_t m, uint64_t se
     });
 }
 
-rfl_status rfl_run_shuffle(const char* const* in_paths, uint64_t n_inputs, const char* out_path,
-                           const rfl_shuffle_config* cfg, rfl_shuffle_stats* stats) {
+rfl_status rfl_shuffle_round_routes(uint64_t total, uint64_t c, uint64_t m, uint64_t seed, uint64_t out_chunk_rows,
+                                    uint64_t out_cps, uint32_t world, uint64_t round, uint64_t* first_out_row,
+                                    uint64_t* n_rows, uint64_t* src_rows, uint32_t* src_rank, uint32_t* dst_rank) {
     return guarded([&] {
-        if (!in_paths || !out_path || !cfg) rfl::invalid("null argument");
-        rfl::ShuffleArgs a;
-        for (uint64_t i = 0; i < n_inputs; ++i) a.inputs.emplace_back(in_paths[i]);
-        a.out_path = out_path;
-        a.c = cfg->block_rows;
-        a.m = cfg->buffer_rows;
-        a.seed = cfg->seed;
-        a.out_chunk_rows = cfg->out_chunk_rows;
-        a.out_cps = cfg->out_chunks_per_shard;
-        a.out_idt = cfg->out_index_dtype;
-        a.device = cfg->device;
-        a.outer = cfg->join_outer != 0;
-        a.rank = cfg->rank;
-        a.world = cfg->world ? cfg->world : 1;
-        rfl::ShuffleResult r = rfl::run_shuffle_gpu(a);
-        if (stats) {
-            stats->peak_resident_rows = r.peak_resident_rows;
-            stats->rows_written = r.rows_written;
-            stats->rounds_executed = r.rounds;
-            stats->input_bytes_read = r.input_bytes;
-            stats->h2d_bytes = r.h2d_bytes;
-            stats->d2h_bytes = r.d2h_bytes;
-            stats->gpu_ms = r.gpu_ms;
+        if (world < 1 || out_chunk_rows < 1 || out_cps < 1) rfl::invalid("routes: bad geometry");
+        const rfl::ShufflePlan p = rfl::plan_shuffle(total, c, m, seed);
+        if (round >= p.rounds.size()) rfl::invalid("routes: round out of range");
+        uint64_t base = 0;
+        for (uint64_t r = 0; r < round; ++r)
+            for (uint64_t id : p.rounds[r]) base += p.block_end(id) - p.block_start(id);
+        std::vector<uint64_t> asm_rows;
+        std::vector<uint32_t> asm_src;
+        for (size_t bi = 0; bi < p.rounds[round].size(); ++bi) {
+            const uint64_t id = p.rounds[round][bi];
+            for (uint64_t g = p.block_start(id); g < p.block_end(id); ++g) {
+                asm_rows.push_back(g);
+                asm_src.push_back(static_cast<uint32_t>(bi % world));  // block bi staged by rank bi mod W
+            }
+        }
+        if (first_out_row) *first_out_row = base;
+        if (n_rows) *n_rows = asm_rows.size();
+        if (!src_rows) return;
+        const auto perm = rfl::round_permutation(seed, round, asm_rows.size());
+        const uint64_t shard_rows = out_chunk_rows * out_cps;
+        for (uint64_t k = 0; k < perm.size(); ++k) {
+            src_rows[k] = asm_rows[perm[k]];
+            if (src_rank) src_rank[k] = asm_src[perm[k]];
+            if (dst_rank) dst_rank[k] = static_cast<uint32_t>(((base + k) / shard_rows) % world);  // shard owner
         }
     });
+}
+
+namespace {
+rfl::ShuffleArgs shuffle_args(const char* const* in_paths, uint64_t n_inputs, const char* out_path,
+                              const rfl_shuffle_config* cfg) {
+    if (!in_paths && n_inputs) rfl::invalid("null argument");
+    if (!out_path || !cfg) rfl::invalid("null argument");
+    rfl::ShuffleArgs a;
+    for (uint64_t i = 0; i < n_inputs; ++i) a.inputs.emplace_back(in_paths[i]);
+    a.out_path = out_path;
+    a.c = cfg->block_rows;
+    a.m = cfg->buffer_rows;
+    a.seed = cfg->seed;
+    a.out_chunk_rows = cfg->out_chunk_rows;
+    a.out_cps = cfg->out_chunks_per_shard;
+    a.out_idt = cfg->out_index_dtype;
+    a.device = cfg->device;
+    a.outer = cfg->join_outer != 0;
+    a.rank = cfg->rank;
+    a.world = cfg->world ? cfg->world : 1;
+    return a;
+}
+void fill_stats(const rfl::ShuffleResult& r, rfl_shuffle_stats* stats) {
+    if (!stats) return;
+    stats->peak_resident_rows = r.peak_resident_rows;
+    stats->rows_written = r.rows_written;
+    stats->rounds_executed = r.rounds;
+    stats->input_bytes_read = r.input_bytes;
+    stats->h2d_bytes = r.h2d_bytes;
+    stats->d2h_bytes = r.d2h_bytes;
+    stats->gpu_ms = r.gpu_ms;
+}
+}  // namespace
+
+struct rfl_pshuf {
+    rfl::RankShuffle* h;
+};
+
+rfl_status rfl_pshuf_create(const char* const* in_paths, uint64_t n_inputs, const char* out_path,
+                            const rfl_shuffle_config* cfg, rfl_pshuf** out, uint64_t* n_rounds) {
+    return guarded([&] {
+        if (!out || !n_rounds) rfl::invalid("null argument");
+        *out = new rfl_pshuf{rfl::rank_shuffle_create(shuffle_args(in_paths, n_inputs, out_path, cfg), n_rounds)};
+    });
+}
+rfl_status rfl_pshuf_stage(rfl_pshuf* h, uint64_t round, uint64_t* send_bytes) {
+    return guarded([&] {
+        if (!h || !send_bytes) rfl::invalid("null argument");
+        rfl::rank_shuffle_stage(h->h, round, send_bytes);
+    });
+}
+rfl_status rfl_pshuf_recv_buffer(rfl_pshuf* h, uint64_t bytes, void** dev_ptr, void* ipc_handle, int* changed) {
+    return guarded([&] {
+        if (!h || !dev_ptr || !changed) rfl::invalid("null argument");
+        rfl::rank_shuffle_recv(h->h, bytes, dev_ptr, ipc_handle, changed);
+    });
+}
+rfl_status rfl_pshuf_send(rfl_pshuf* h, uint64_t round, void* const* dst) {
+    return guarded([&] {
+        if (!h || !dst) rfl::invalid("null argument");
+        rfl::rank_shuffle_send(h->h, round, dst);
+    });
+}
+rfl_status rfl_pshuf_emit(rfl_pshuf* h, uint64_t round, const uint64_t* recv_bytes) {
+    return guarded([&] {
+        if (!h || !recv_bytes) rfl::invalid("null argument");
+        rfl::rank_shuffle_emit(h->h, round, recv_bytes);
+    });
+}
+rfl_status rfl_pshuf_finish(rfl_pshuf* h, rfl_shuffle_stats* stats) {
+    return guarded([&] {
+        if (!h) rfl::invalid("null argument");
+        fill_stats(rfl::rank_shuffle_finish(h->h), stats);
+    });
+}
+void rfl_pshuf_destroy(rfl_pshuf* h) {
+    if (h) rfl::rank_shuffle_destroy(h->h);
+    delete h;
+}
+
+rfl_status rfl_ipc_open(const void* handle, int device, void** dev_ptr) {
+    return guarded([&] {
+        if (!handle || !dev_ptr) rfl::invalid("null argument");
+        rfl::DeviceGuard g(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        rfl::cuda_ok(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+rfl_status rfl_ipc_close(void* dev_ptr, int device) {
+    return guarded([&] {
+        rfl::DeviceGuard g(device);
+        rfl::cuda_ok(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+    });
+}
+
+rfl_status rfl_run_shuffle(const char* const* in_paths, uint64_t n_inputs, const char* out_path,
+                           const rfl_shuffle_config* cfg, rfl_shuffle_stats* stats) {
+    return guarded([&] { fill_stats(rfl::run_shuffle_gpu(shuffle_args(in_paths, n_inputs, out_path, cfg)), stats); });
 }
 
 }  // extern "C"

@@ -566,9 +566,24 @@ void RecordWriter::append_record(const void* rec, uint64_t nbytes, uint64_t rows
     if (chunk_in_shard_ >= man_.chunks_per_shard) close_shard();
 }
 
-Manifest RecordWriter::finish() {
+void RecordWriter::append_record_at(uint64_t chunk, const void* rec, uint64_t nbytes, uint64_t rows) {
+    if (finished_) invalid("store writer: append after finish");
+    const uint64_t shard = chunk / man_.chunks_per_shard;
+    if (shard_ && shard != (chunks_emitted_ - 1) / man_.chunks_per_shard) close_shard();
+    if (!shard_) {
+        if (chunk % man_.chunks_per_shard != 0) invalid("store writer: owned shard must be filled from slot 0");
+        chunks_emitted_ = chunk;
+        open_shard();
+    } else if (chunk != chunks_emitted_) {
+        invalid("store writer: non-consecutive chunk " + std::to_string(chunk));
+    }
+    append_record(rec, nbytes, rows);
+}
+
+Manifest RecordWriter::finish(int64_t n_obs_override) {
     if (finished_) invalid("store writer: finish called twice");
     if (shard_) close_shard();
+    if (n_obs_override >= 0) man_.n_obs = static_cast<uint64_t>(n_obs_override);
     if (write_manifest_file_) write_text_file(root_ + "/manifest.json", man_.serialize());
     finished_ = true;
     return man_;

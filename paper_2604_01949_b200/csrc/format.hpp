@@ -142,8 +142,12 @@ public:
     RecordWriter(std::string root, Manifest man, bool defer_manifest, const char* shard_dir = "shards",
                  bool write_manifest_file = true);
     void append_record(const void* rec, uint64_t nbytes, uint64_t rows);
-    // finish(): flush shard footer, write manifest (n_obs = rows appended)
-    Manifest finish();
+    // Sparse writing for multi-rank writers that own a subset of the shards:
+    // chunk ids must increase and fill each owned shard from slot 0.
+    void append_record_at(uint64_t chunk, const void* rec, uint64_t nbytes, uint64_t rows);
+    // finish(): flush shard footer, write manifest (n_obs = rows appended, or
+    // n_obs_override when several ranks wrote the store)
+    Manifest finish(int64_t n_obs_override = -1);
     uint64_t rows() const { return man_.n_obs; }
 
 private:

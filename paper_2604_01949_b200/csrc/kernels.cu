@@ -323,11 +323,12 @@ __global__ void __launch_bounds__(kPackThreads)
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (kPackThreads / 32);
     constexpr uint64_t os = sizeof(OutIdx);
+    const uint64_t pb = P[0];  // P may be a slice of a longer scan
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (kPackThreads / 32) + warp; i < n_rows; i += nw) {
         const uint64_t q = i / cr, r0 = q * cr;
         const uint64_t rows_q = umin64(cr, n_rows - r0);
         const uint64_t p0 = P[r0], nnz_q = P[r0 + rows_q] - p0;
-        uint8_t* rec = out + q * (kCsrHeaderBytes + os * (cr + 1)) + (os + vs) * p0;
+        uint8_t* rec = out + q * (kCsrHeaderBytes + os * (cr + 1)) + (os + vs) * (p0 - pb);
         uint8_t* ip = rec + kCsrHeaderBytes;
         uint8_t* idx = ip + os * (rows_q + 1);
         uint8_t* val = idx + os * nnz_q;

@@ -105,17 +105,32 @@ std::vector<std::string> unify(const std::vector<Member>& ms, bool outer) {
 
 class GpuShuffler {
 public:
-    GpuShuffler(const ShuffleArgs& a) : a_(a) {}
-    ShuffleResult run();
+    explicit GpuShuffler(const ShuffleArgs& a) : a_(a) {}
+    ~GpuShuffler();
+    void init();
+    ShuffleResult run();  // single GPU, whole pass
+
+    // ---- rank API (multi-GPU; the caller drives the control plane) ----
+    uint64_t n_rounds() const { return plan_.rounds.size(); }
+    void stage(uint64_t r, uint64_t* send_bytes);
+    void recv_buffer(uint64_t bytes, void** ptr, void* ipc_handle, int* changed);
+    void send(uint64_t r, void* const* dst);
+    void emit_round(uint64_t r, const uint64_t* recv_bytes);
+    ShuffleResult finish();
 
 private:
-    void stage_round(const std::vector<std::pair<uint32_t, std::pair<uint64_t, uint64_t>>>& segs, DevBuf& arena,
-                     std::vector<RowRef>& refs);
-    void emit(const std::vector<RowRef>& refs, const std::vector<std::pair<uint32_t, uint64_t>>& prov, uint64_t n);
+    using Segs = std::vector<std::pair<uint32_t, std::pair<uint64_t, uint64_t>>>;
+    void round_segments(uint64_t r, Segs& segs, std::vector<std::pair<uint32_t, uint64_t>>& prov,
+                        std::vector<uint32_t>* src_rank);
+    void stage_round(const Segs& segs, DevBuf& arena, std::vector<RowRef>& refs);
+    void emit(const std::vector<RowRef>& refs, const std::vector<std::pair<uint32_t, uint64_t>>& prov, uint64_t n,
+              const std::vector<uint64_t>* out_rows);
     void carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst);
     void upload_refs(const RowRef* refs, uint64_t n);
 
     ShuffleArgs a_;
+    ShufflePlan plan_;
+    uint64_t total_ = 0;
     std::vector<Member> ms_;
     Layout layout_ = Layout::csr;
     VDtype vdt_ = VDtype::f32;
@@ -128,6 +143,17 @@ private:
     PinBuf h_stage_, h_refs_, h_prefix_, h_out_;
     ShuffleResult res_;
     std::vector<uint8_t> prov_rec_;
+    // rank state
+    DevBuf arena_[2], carry_[2], recv_, d_send_refs_, d_send_prefix_;
+    std::vector<RowRef> pending_;
+    std::vector<std::pair<uint32_t, uint64_t>> pend_prov_;
+    std::vector<uint64_t> pend_out_;                 // global output row of each pending row (multi-rank)
+    std::vector<uint64_t> send_start_, send_count_;  // per destination, into d_send_refs_
+    std::vector<uint64_t> round_first_out_;          // first global output row of each round
+    std::vector<uint32_t> mine_src_;                 // per owned output row of the staged round: source rank
+    std::vector<uint64_t> mine_out_;
+    std::vector<std::pair<uint32_t, uint64_t>> mine_prov_;
+    uint64_t staged_round_ = ~0ull;
 };
 
 ArenaView absolute_view(Layout l, VDtype v, IDtype i, uint64_t n_var) {
@@ -236,8 +262,10 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
 }
 
 // Write refs[0..n) as output chunk records (+ provenance records).
+// out_rows (multi-rank) gives the global output row of each ref so records land
+// in the owned chunk slots; single-GPU writes are consecutive.
 void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::pair<uint32_t, uint64_t>>& prov,
-                       uint64_t n) {
+                       uint64_t n, const std::vector<uint64_t>* out_rows) {
     if (n == 0) return;
     const uint64_t cr = a_.out_chunk_rows;
     const uint64_t nq = (n + cr - 1) / cr;
@@ -290,7 +318,8 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
     res_.d2h_bytes += total;
     uint64_t pos = 0;
     for (uint64_t q = 0; q < nq; ++q) {
-        out_->append_record(h_out_.p + pos, rec_len[q], rec_rows[q]);
+        if (out_rows) out_->append_record_at((*out_rows)[q * cr] / cr, h_out_.p + pos, rec_len[q], rec_rows[q]);
+        else out_->append_record(h_out_.p + pos, rec_len[q], rec_rows[q]);
         pos += rec_len[q];
         // provenance: u32 dataset_id + u64 source_row, LE (preshuffle.cpp:27-91)
         prov_rec_.resize(rec_rows[q] * 12);
@@ -299,7 +328,8 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
             wr32(prov_rec_.data() + 12 * k, p.first);
             wr64(prov_rec_.data() + 12 * k + 4, p.second);
         }
-        prov_->append_record(prov_rec_.data(), prov_rec_.size(), rec_rows[q]);
+        if (out_rows) prov_->append_record_at((*out_rows)[q * cr] / cr, prov_rec_.data(), prov_rec_.size(), rec_rows[q]);
+        else prov_->append_record(prov_rec_.data(), prov_rec_.size(), rec_rows[q]);
     }
     res_.rows_written += n;
 }
@@ -331,14 +361,23 @@ void GpuShuffler::carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst) {
     for (uint64_t k = 0; k < n; ++k) refs[from + k] = {reinterpret_cast<uint64_t>(dst.p), k};
 }
 
-ShuffleResult GpuShuffler::run() {
+GpuShuffler::~GpuShuffler() {
+    if (st_) {
+        cudaStreamSynchronize(st_);
+        cudaEventDestroy(e0_);
+        cudaEventDestroy(e1_);
+        cudaStreamDestroy(st_);
+    }
+}
+
+void GpuShuffler::init() {
     if (a_.inputs.empty()) invalid("run_shuffle: empty collection");
-    if (a_.world != 1) invalid("run_shuffle: multi-GPU runs go through the rank API (world must be 1 here)");
-    uint64_t total = 0;
+    if (a_.world < 1 || a_.rank >= a_.world) invalid("run_shuffle: rank must satisfy 0 <= rank < world");
+    total_ = 0;
     for (const auto& p : a_.inputs) {
         Member m;
         m.hs = std::make_shared<HostStore>(p);
-        m.offset = total;
+        m.offset = total_;
         const Manifest& man = m.hs->manifest();
         if (!ms_.empty()) {  // DatasetCollection::add (collection.cpp:10-24)
             const Manifest& f = ms_.front().hs->manifest();
@@ -352,16 +391,19 @@ ShuffleResult GpuShuffler::run() {
                 invalid("run_shuffle: members with different index dtypes are not supported on the GPU path");
         }
         if (man.codec != Codec::none) invalid("GPU path requires codec none (deflate decode is out of scope)");
-        total += man.n_obs;
+        total_ += man.n_obs;
         ms_.push_back(std::move(m));
     }
-    const ShufflePlan plan = plan_shuffle(total, a_.c, a_.m, a_.seed);
-    if (dir_nonempty(a_.out_path)) invalid("run_shuffle: output path '" + a_.out_path + "' is not fresh");
+    plan_ = plan_shuffle(total_, a_.c, a_.m, a_.seed);
+    // every rank creates its own shard files only; the directories may already exist
+    if (a_.rank == 0 && dir_nonempty(a_.out_path))
+        invalid("run_shuffle: output path '" + a_.out_path + "' is not fresh");
     const Manifest& f = ms_.front().hs->manifest();
     layout_ = f.layout;
     vdt_ = f.value_dtype;
     in_idt_ = f.index_dtype.value_or(IDtype::u32);
     out_idt_ = a_.out_idt < 0 ? in_idt_ : static_cast<IDtype>(a_.out_idt);
+    if (a_.out_chunk_rows < 1 || a_.out_cps < 1) invalid("run_shuffle: output chunk geometry must be >= 1");
     Manifest om;
     om.layout = layout_;
     om.var_names = unify(ms_, a_.outer);
@@ -374,74 +416,258 @@ ShuffleResult GpuShuffler::run() {
     om.has_provenance = true;
     n_var_ = om.n_var;
     row_bytes_ = n_var_ * value_size(vdt_);
-    if (a_.out_chunk_rows < 1 || a_.out_cps < 1) invalid("run_shuffle: output chunk geometry must be >= 1");
-    out_ = std::make_unique<RecordWriter>(a_.out_path, om, /*defer_manifest=*/true);
+    // defer_manifest (preshuffle.cpp:217): the manifest lands only when the pass completes (rank 0)
+    out_ = std::make_unique<RecordWriter>(a_.out_path, om, /*defer_manifest=*/true, "shards", a_.rank == 0);
     Manifest pm;  // provenance sidecar: same chunk grid, 12-byte records
     pm.layout = Layout::dense;
     pm.chunk_rows = a_.out_chunk_rows;
     pm.chunks_per_shard = a_.out_cps;
     prov_ = std::make_unique<RecordWriter>(a_.out_path + "/provenance", pm, true, "shards", false);
-
+    round_first_out_.assign(plan_.rounds.size() + 1, 0);
+    for (size_t r = 0; r < plan_.rounds.size(); ++r) {
+        uint64_t rows = 0;
+        for (uint64_t id : plan_.rounds[r]) rows += plan_.block_end(id) - plan_.block_start(id);
+        round_first_out_[r + 1] = round_first_out_[r] + rows;
+    }
     DeviceGuard g(a_.device);
     cuda_ok(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
     cuda_ok(cudaEventCreate(&e0_), "event");
     cuda_ok(cudaEventCreate(&e1_), "event");
-    DevBuf arena[2], carry_buf[2];
-    std::vector<RowRef> pending, round_refs;
-    std::vector<std::pair<uint32_t, uint64_t>> pend_prov;
-    const uint64_t cr = a_.out_chunk_rows;
-    try {
-        for (size_t r = 0; r < plan.rounds.size(); ++r) {
-            // split the round's blocks into per-member segments, in block order (:234-251)
-            std::vector<std::pair<uint32_t, std::pair<uint64_t, uint64_t>>> segs;
-            std::vector<std::pair<uint32_t, uint64_t>> asm_prov;
-            for (const uint64_t id : plan.rounds[r]) {
-                uint64_t row = plan.block_start(id);
-                const uint64_t end = plan.block_end(id);
-                while (row < end) {
-                    size_t mi = 0;
-                    while (mi + 1 < ms_.size() && ms_[mi + 1].offset <= row) ++mi;
-                    const uint64_t mend = ms_[mi].offset + ms_[mi].hs->manifest().n_obs;
-                    const uint64_t stop = std::min(end, mend);
-                    segs.push_back({static_cast<uint32_t>(mi), {row - ms_[mi].offset, stop - ms_[mi].offset}});
-                    for (uint64_t x = row; x < stop; ++x) asm_prov.emplace_back(static_cast<uint32_t>(mi), x - ms_[mi].offset);
-                    row = stop;
-                }
+}
+
+// The round's blocks as per-member segments in block order (:234-251); with
+// src_rank, the rank staging each assembly row (block index in round mod W).
+void GpuShuffler::round_segments(uint64_t r, Segs& segs, std::vector<std::pair<uint32_t, uint64_t>>& prov,
+                                 std::vector<uint32_t>* src_rank) {
+    segs.clear();
+    prov.clear();
+    if (src_rank) src_rank->clear();
+    for (size_t bi = 0; bi < plan_.rounds[r].size(); ++bi) {
+        const uint64_t id = plan_.rounds[r][bi];
+        const uint32_t owner = static_cast<uint32_t>(bi % a_.world);
+        uint64_t row = plan_.block_start(id);
+        const uint64_t end = plan_.block_end(id);
+        while (row < end) {
+            size_t mi = 0;
+            while (mi + 1 < ms_.size() && ms_[mi + 1].offset <= row) ++mi;
+            const uint64_t mend = ms_[mi].offset + ms_[mi].hs->manifest().n_obs;
+            const uint64_t stop = std::min(end, mend);
+            if (!src_rank || owner == a_.rank)
+                segs.push_back({static_cast<uint32_t>(mi), {row - ms_[mi].offset, stop - ms_[mi].offset}});
+            for (uint64_t x = row; x < stop; ++x) {
+                prov.emplace_back(static_cast<uint32_t>(mi), x - ms_[mi].offset);
+                if (src_rank) src_rank->push_back(owner);
             }
-            const uint64_t round_rows = asm_prov.size();
-            res_.peak_resident_rows = std::max(res_.peak_resident_rows, round_rows + std::min(a_.c, round_rows));
-            stage_round(segs, arena[r % 2], round_refs);
-            const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
-            for (uint64_t k = 0; k < round_rows; ++k) {
-                pending.push_back(round_refs[perm[k]]);
-                pend_prov.push_back(asm_prov[perm[k]]);
-            }
-            const bool last = r + 1 == plan.rounds.size();
-            const uint64_t n_emit = last ? pending.size() : pending.size() / cr * cr;
-            emit(pending, pend_prov, n_emit);
-            pending.erase(pending.begin(), pending.begin() + n_emit);
-            pend_prov.erase(pend_prov.begin(), pend_prov.begin() + n_emit);
-            if (!pending.empty()) carry(pending, 0, carry_buf[r % 2]);
-            res_.rounds++;
+            row = stop;
         }
-        out_->finish();
-        prov_->finish();
-        write_text_file(a_.out_path + "/provenance/meta.json", meta_json(a_.seed, a_.c, a_.m));
-    } catch (...) {
-        cudaStreamSynchronize(st_);
-        cudaEventDestroy(e0_);
-        cudaEventDestroy(e1_);
-        cudaStreamDestroy(st_);
-        throw;
     }
-    cudaEventDestroy(e0_);
-    cudaEventDestroy(e1_);
-    cudaStreamDestroy(st_);
+}
+
+ShuffleResult GpuShuffler::run() {
+    init();
+    DeviceGuard g(a_.device);
+    std::vector<RowRef> round_refs;
+    Segs segs;
+    std::vector<std::pair<uint32_t, uint64_t>> asm_prov;
+    const uint64_t cr = a_.out_chunk_rows;
+    for (size_t r = 0; r < plan_.rounds.size(); ++r) {
+        round_segments(r, segs, asm_prov, nullptr);
+        const uint64_t round_rows = asm_prov.size();
+        res_.peak_resident_rows = std::max(res_.peak_resident_rows, round_rows + std::min(a_.c, round_rows));
+        stage_round(segs, arena_[r % 2], round_refs);
+        const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
+        for (uint64_t k = 0; k < round_rows; ++k) {
+            pending_.push_back(round_refs[perm[k]]);
+            pend_prov_.push_back(asm_prov[perm[k]]);
+        }
+        const bool last = r + 1 == plan_.rounds.size();
+        const uint64_t n_emit = last ? pending_.size() : pending_.size() / cr * cr;
+        emit(pending_, pend_prov_, n_emit, nullptr);
+        pending_.erase(pending_.begin(), pending_.begin() + n_emit);
+        pend_prov_.erase(pend_prov_.begin(), pend_prov_.begin() + n_emit);
+        if (!pending_.empty()) carry(pending_, 0, carry_[r % 2]);
+        res_.rounds++;
+    }
+    out_->finish();
+    prov_->finish();
+    write_text_file(a_.out_path + "/provenance/meta.json", meta_json(a_.seed, a_.c, a_.m));
+    return res_;
+}
+
+// ---- rank API ---------------------------------------------------------------
+// Stage this rank's blocks of round r, group its rows by destination (owner of
+// the output shard) in output order, scan them, and report the message size
+// for every destination (one encoded record per destination).
+void GpuShuffler::stage(uint64_t r, uint64_t* send_bytes) {
+    if (r >= plan_.rounds.size()) invalid("run_shuffle: round out of range");
+    DeviceGuard g(a_.device);
+    Segs segs;
+    std::vector<std::pair<uint32_t, uint64_t>> asm_prov;
+    std::vector<uint32_t> asm_src;
+    round_segments(r, segs, asm_prov, &asm_src);
+    const uint64_t round_rows = asm_prov.size();
+    res_.peak_resident_rows = std::max(res_.peak_resident_rows, round_rows + std::min(a_.c, round_rows));
+    std::vector<RowRef> my_refs;
+    stage_round(segs, arena_[r % 2], my_refs);  // refs of my assembly rows, in assembly order
+    std::vector<int64_t> asm_to_mine(round_rows, -1);
+    for (uint64_t a = 0, k = 0; a < round_rows; ++a)
+        if (asm_src[a] == a_.rank) asm_to_mine[a] = static_cast<int64_t>(k++);
+    const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
+    const uint64_t shard_rows = a_.out_chunk_rows * a_.out_cps, first = round_first_out_[r];
+    const uint32_t W = a_.world;
+    std::vector<std::vector<RowRef>> by_dst(W);
+    mine_src_.clear();
+    mine_out_.clear();
+    mine_prov_.clear();
+    for (uint64_t k = 0; k < round_rows; ++k) {
+        const uint64_t a = perm[k];
+        const uint32_t dst = static_cast<uint32_t>(((first + k) / shard_rows) % W);
+        if (asm_src[a] == a_.rank) by_dst[dst].push_back(my_refs[asm_to_mine[a]]);
+        if (dst == a_.rank) {
+            mine_src_.push_back(asm_src[a]);
+            mine_out_.push_back(first + k);
+            mine_prov_.push_back(asm_prov[a]);
+        }
+    }
+    send_start_.assign(W, 0);
+    send_count_.assign(W, 0);
+    std::vector<RowRef> all;
+    for (uint32_t d = 0; d < W; ++d) {
+        send_start_[d] = all.size();
+        send_count_[d] = by_dst[d].size();
+        all.insert(all.end(), by_dst[d].begin(), by_dst[d].end());
+    }
+    const uint64_t n = all.size();
+    d_send_refs_.ensure(std::max<uint64_t>(n, 1) * sizeof(RowRef));
+    h_refs_.ensure(std::max<uint64_t>(n, 1) * sizeof(RowRef));
+    std::memcpy(h_refs_.p, all.data(), n * sizeof(RowRef));
+    if (n) cuda_ok(cudaMemcpyAsync(d_send_refs_.p, h_refs_.p, n * sizeof(RowRef), cudaMemcpyHostToDevice, st_), "H2D");
+    res_.h2d_bytes += n * sizeof(RowRef);
+    const uint64_t is = index_size(in_idt_), vs = value_size(vdt_);
+    if (layout_ == Layout::csr) {
+        d_send_prefix_.ensure((n + 1) * 8);
+        d_scratch_.ensure(csr_gather_scratch_bytes(std::max<uint64_t>(n, 1)));
+        launch_csr_row_scan(absolute_view(layout_, vdt_, in_idt_, n_var_), reinterpret_cast<RowRef*>(d_send_refs_.p),
+                            n, reinterpret_cast<uint64_t*>(d_send_prefix_.p), d_scratch_.p, st_);
+        h_prefix_.ensure((n + 1) * 8);
+        cuda_ok(cudaMemcpyAsync(h_prefix_.p, d_send_prefix_.p, (n + 1) * 8, cudaMemcpyDeviceToHost, st_), "D2H");
+        cuda_ok(cudaStreamSynchronize(st_), "sync");
+        const uint64_t* P = reinterpret_cast<const uint64_t*>(h_prefix_.p);
+        for (uint32_t d = 0; d < W; ++d) {
+            const uint64_t c = send_count_[d];
+            const uint64_t nnz = P[send_start_[d] + c] - P[send_start_[d]];
+            send_bytes[d] = c ? kCsrHeaderBytes + is * (c + 1) + (is + vs) * nnz : 0;
+        }
+    } else {
+        cuda_ok(cudaStreamSynchronize(st_), "sync");
+        for (uint32_t d = 0; d < W; ++d) send_bytes[d] = send_count_[d] * row_bytes_;
+    }
+    staged_round_ = r;
+}
+
+void GpuShuffler::recv_buffer(uint64_t bytes, void** ptr, void* ipc_handle, int* changed) {
+    DeviceGuard g(a_.device);
+    const uint64_t before = recv_.cap;
+    const uint8_t* old = recv_.p;
+    if (bytes > recv_.cap) recv_.ensure(bytes + bytes / 4 + (1 << 20));
+    *changed = (recv_.p != old || recv_.cap != before) ? 1 : 0;
+    *ptr = recv_.p;
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        cuda_ok(cudaIpcGetMemHandle(&h, recv_.p), "cudaIpcGetMemHandle");
+        std::memcpy(ipc_handle, &h, sizeof(h));
+    }
+}
+
+// Pack my message for destination d straight into d's receive buffer (dst[d]
+// = peer address over NVLink/IPC, or local): gather + exchange in one pass.
+void GpuShuffler::send(uint64_t r, void* const* dst) {
+    if (r != staged_round_) invalid("run_shuffle: send() without stage() of the same round");
+    DeviceGuard g(a_.device);
+    const ArenaView av = absolute_view(layout_, vdt_, in_idt_, n_var_);
+    cuda_ok(cudaEventRecord(e0_, st_), "event");
+    uint64_t sent = 0;
+    for (uint32_t d = 0; d < a_.world; ++d) {
+        const uint64_t c = send_count_[d];
+        if (!c) continue;
+        const RowRef* refs = reinterpret_cast<const RowRef*>(d_send_refs_.p) + send_start_[d];
+        if (layout_ == Layout::csr)
+            launch_csr_pack(av, refs, c, c, in_idt_, reinterpret_cast<uint64_t*>(d_send_prefix_.p) + send_start_[d],
+                            static_cast<uint8_t*>(dst[d]), st_);
+        else
+            launch_dense_gather(av, refs, c, OutDtype::native, dst[d], nullptr, st_);
+        sent += c;
+    }
+    cuda_ok(cudaEventRecord(e1_, st_), "event");
+    cuda_ok(cudaStreamSynchronize(st_), "sync");  // peer writes complete before the caller's barrier
+    float ms = 0.f;
+    cuda_ok(cudaEventElapsedTime(&ms, e0_, e1_), "elapsed");
+    res_.gpu_ms += ms;
+}
+
+// Owner side: my rows of round r arrived as one record per source rank in my
+// receive buffer (offsets = running 16-B aligned sums of recv_bytes).  Emit
+// every owned chunk that is now complete; carry the rest.
+void GpuShuffler::emit_round(uint64_t r, const uint64_t* recv_bytes) {
+    if (r != staged_round_) invalid("run_shuffle: emit_round() without stage() of the same round");
+    DeviceGuard g(a_.device);
+    std::vector<uint64_t> off(a_.world, 0), cursor(a_.world, 0);
+    for (uint32_t s = 1; s < a_.world; ++s) off[s] = align_up(off[s - 1] + recv_bytes[s - 1], kAlign);
+    for (size_t i = 0; i < mine_src_.size(); ++i) {
+        const uint32_t s = mine_src_[i];
+        pending_.push_back({reinterpret_cast<uint64_t>(recv_.p) + off[s], cursor[s]++});
+        pend_prov_.push_back(mine_prov_[i]);
+        pend_out_.push_back(mine_out_[i]);
+    }
+    const bool last = r + 1 == plan_.rounds.size();
+    const uint64_t cr = a_.out_chunk_rows;
+    const uint64_t limit = last ? total_ : round_first_out_[r + 1] / cr * cr;  // rows of complete chunks
+    const uint64_t n_emit = std::lower_bound(pend_out_.begin(), pend_out_.end(), limit) - pend_out_.begin();
+    emit(pending_, pend_prov_, n_emit, &pend_out_);
+    pending_.erase(pending_.begin(), pending_.begin() + n_emit);
+    pend_prov_.erase(pend_prov_.begin(), pend_prov_.begin() + n_emit);
+    pend_out_.erase(pend_out_.begin(), pend_out_.begin() + n_emit);
+    if (!pending_.empty()) carry(pending_, 0, carry_[r % 2]);  // the receive buffer is reused next round
+    res_.rounds++;
+}
+
+ShuffleResult GpuShuffler::finish() {
+    out_->finish(static_cast<int64_t>(total_));  // rank 0 writes the manifest (others: shards only)
+    prov_->finish();
+    if (a_.rank == 0) write_text_file(a_.out_path + "/provenance/meta.json", meta_json(a_.seed, a_.c, a_.m));
     return res_;
 }
 
 }  // namespace
 
-ShuffleResult run_shuffle_gpu(const ShuffleArgs& a) { return GpuShuffler(a).run(); }
+ShuffleResult run_shuffle_gpu(const ShuffleArgs& a) {
+    if (a.world != 1) invalid("run_shuffle: multi-GPU runs go through the rank API (rfl_pshuf_*)");
+    return GpuShuffler(a).run();
+}
+
+// ---- rank API wrappers --------------------------------------------------------
+struct RankShuffle {
+    GpuShuffler s;
+    explicit RankShuffle(const ShuffleArgs& a) : s(a) {}
+};
+RankShuffle* rank_shuffle_create(const ShuffleArgs& a, uint64_t* n_rounds) {
+    auto* h = new RankShuffle(a);
+    try {
+        h->s.init();
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *n_rounds = h->s.n_rounds();
+    return h;
+}
+void rank_shuffle_stage(RankShuffle* h, uint64_t r, uint64_t* send_bytes) { h->s.stage(r, send_bytes); }
+void rank_shuffle_recv(RankShuffle* h, uint64_t bytes, void** ptr, void* handle, int* changed) {
+    h->s.recv_buffer(bytes, ptr, handle, changed);
+}
+void rank_shuffle_send(RankShuffle* h, uint64_t r, void* const* dst) { h->s.send(r, dst); }
+void rank_shuffle_emit(RankShuffle* h, uint64_t r, const uint64_t* recv_bytes) { h->s.emit_round(r, recv_bytes); }
+ShuffleResult rank_shuffle_finish(RankShuffle* h) { return h->s.finish(); }
+void rank_shuffle_destroy(RankShuffle* h) { delete h; }
 
 }  // namespace rfl

@@ -25,4 +25,17 @@ struct ShuffleResult {
 
 ShuffleResult run_shuffle_gpu(const ShuffleArgs& a);
 
+// Multi-GPU rank API (one process per GPU; the caller runs the control plane):
+// per round  stage -> [sizes all-gathered] -> recv buffer + IPC handles ->
+// send (pack kernel writes into the owners' receive buffers) -> [barrier] ->
+// emit (owner packs its complete chunks and writes its shards).
+struct RankShuffle;
+RankShuffle* rank_shuffle_create(const ShuffleArgs& a, uint64_t* n_rounds);
+void rank_shuffle_stage(RankShuffle* h, uint64_t round, uint64_t* send_bytes);
+void rank_shuffle_recv(RankShuffle* h, uint64_t bytes, void** ptr, void* ipc_handle, int* changed);
+void rank_shuffle_send(RankShuffle* h, uint64_t round, void* const* dst);
+void rank_shuffle_emit(RankShuffle* h, uint64_t round, const uint64_t* recv_bytes);
+ShuffleResult rank_shuffle_finish(RankShuffle* h);
+void rank_shuffle_destroy(RankShuffle* h);
+
 }  // namespace rfl

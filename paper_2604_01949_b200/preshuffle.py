@@ -51,6 +51,34 @@ def shuffle_order(total_rows: int, block_rows: int, buffer_rows: int, seed: int)
 
 
 @dataclass
+class RoundRoute:
+    """Routing of one round across W ranks."""
+    round: int
+    out_rows: np.ndarray   # global output row of each row, in output order
+    src_rows: np.ndarray   # global input row
+    src_rank: np.ndarray   # rank that staged the row's block (block index in round mod W)
+    dst_rank: np.ndarray   # owner of the output shard holding the row
+
+
+def round_routes(total_rows, block_rows, buffer_rows, seed, out_chunk_rows, out_chunks_per_shard, world):
+    """All rounds' routes (host logic of the multi-GPU pre-shuffle)."""
+    plan = plan_shuffle(total_rows, block_rows, buffer_rows, seed)
+    out = []
+    for r in range(len(plan.rounds)):
+        first, n = C.c_uint64(), C.c_uint64()
+        args = (total_rows, block_rows, buffer_rows, seed, out_chunk_rows, out_chunks_per_shard, world, r)
+        L.check(L.lib().rfl_shuffle_round_routes(*args, C.byref(first), C.byref(n), None, None, None))
+        src = np.zeros(n.value, np.uint64)
+        sr = np.zeros(n.value, np.uint32)
+        dr = np.zeros(n.value, np.uint32)
+        L.check(L.lib().rfl_shuffle_round_routes(*args, C.byref(first), C.byref(n), src.ctypes.data, sr.ctypes.data,
+                                                 dr.ctypes.data))
+        out.append(RoundRoute(r, first.value + np.arange(n.value, dtype=np.uint64), src, sr.astype(np.int64),
+                              dr.astype(np.int64)))
+    return out
+
+
+@dataclass
 class ShuffleOutputConfig:
     """ShuffleOutputConfig (preshuffle.hpp:44-50)."""
     chunk_rows: int = 1024
@@ -71,10 +99,19 @@ class ShuffleRunStats:
     gpu_ms: float = 0.0
 
 
+def _stats(st) -> ShuffleRunStats:
+    return ShuffleRunStats(st.peak_resident_rows, st.rows_written, st.rounds_executed, st.input_bytes_read,
+                           st.h2d_bytes, st.d2h_bytes, st.gpu_ms)
+
+
 def run_shuffle(inputs, plan: ShufflePlan, out_path, out_config: ShuffleOutputConfig | None = None, *,
-                device: int = 0, join: str = "outer", rank: int = 0, world: int = 1) -> ShuffleRunStats:
+                device: int = 0, join: str = "outer", rank: int = 0, world: int = 1, group=None) -> ShuffleRunStats:
     """run_shuffle (preshuffle.cpp:185-378) with the round gather/permute/pack on the GPU.
-    `inputs` is the ordered list of member store paths (DatasetCollection order)."""
+
+    `inputs` is the ordered list of member store paths (DatasetCollection order).
+    world > 1: call on every rank (one process per GPU) with an initialised
+    torch.distributed group for the control plane; row payloads move between
+    GPUs through peer memory, written by the pack kernel (see _run_ranks)."""
     oc = out_config or ShuffleOutputConfig()
     if oc.codec != "none":
         raise L.InvalidArgument("GPU pre-shuffle writes codec none only")
@@ -88,7 +125,84 @@ def run_shuffle(inputs, plan: ShufflePlan, out_path, out_config: ShuffleOutputCo
     cfg = L.rfl_shuffle_config(plan.block_rows, plan.buffer_rows, plan.seed, oc.chunk_rows, oc.chunks_per_shard,
                                -1 if oc.index_dtype is None else {"u32": 0, "u64": 1}[oc.index_dtype], device,
                                int(join == "outer"), rank, world, 0)
+    if world > 1:
+        return _run_ranks(arr, len(paths), str(out_path), cfg, device, rank, world, group)
     st = L.rfl_shuffle_stats()
     L.check(L.lib().rfl_run_shuffle(arr, len(paths), str(out_path).encode(), C.byref(cfg), C.byref(st)))
-    return ShuffleRunStats(st.peak_resident_rows, st.rows_written, st.rounds_executed, st.input_bytes_read,
-                           st.h2d_bytes, st.d2h_bytes, st.gpu_ms)
+    return _stats(st)
+
+
+def _a16(x: int) -> int:
+    return (x + 15) // 16 * 16
+
+
+def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group) -> ShuffleRunStats:
+    """One rank of the multi-GPU pre-shuffle.
+
+    Data plane: block b of round r is staged by rank b mod W; each output row
+    goes to the owner of its shard (s mod W).  The K5 pack kernel of the
+    source rank encodes the rows for owner d as one CSR record and stores it
+    directly into d's receive buffer through CUDA IPC peer pointers (NVLink
+    P2P on a multi-GPU node) — gather and exchange are one kernel pass.
+    Control plane (torch.distributed, any backend): the W x W message-size
+    matrix, the receive buffers' IPC handles, and the round barriers."""
+    import torch.distributed as dist
+    lib = L.lib()
+    h = L.vp()
+    nr = C.c_uint64()
+
+    def create():
+        L.check(lib.rfl_pshuf_create(arr, n_in, out_path.encode(), C.byref(cfg), C.byref(h), C.byref(nr)))
+
+    if rank == 0:  # the fresh-output check runs before any rank creates directories
+        create()
+    dist.barrier(group=group)
+    if rank != 0:
+        create()
+    peers = {}  # rank -> (version, device pointer)
+    version = 0
+    try:
+        for r in range(nr.value):
+            send = np.zeros(world, np.uint64)
+            L.check(lib.rfl_pshuf_stage(h, r, send.ctypes.data))
+            mats = [None] * world
+            dist.all_gather_object(mats, send.tolist(), group=group)
+            mat = np.array(mats, dtype=np.uint64)  # [src, dst]
+            need = sum(_a16(int(mat[s, rank])) for s in range(world))
+            ptr, changed = L.vp(), C.c_int()
+            handle = (C.c_ubyte * 64)()
+            L.check(lib.rfl_pshuf_recv_buffer(h, max(need, 16), C.byref(ptr), handle, C.byref(changed)))
+            version += changed.value
+            infos = [None] * world
+            dist.all_gather_object(infos, (version, bytes(handle)), group=group)
+            for p in range(world):
+                if p == rank:
+                    continue
+                ver, hb = infos[p]
+                if p not in peers or peers[p][0] != ver:
+                    if p in peers:
+                        L.check(lib.rfl_ipc_close(peers[p][1], device))
+                    pp = L.vp()
+                    L.check(lib.rfl_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), device, C.byref(pp)))
+                    peers[p] = (ver, pp.value)
+            dst = (L.vp * world)()
+            for d in range(world):
+                base = ptr.value if d == rank else peers[d][1]
+                dst[d] = base + sum(_a16(int(mat[s, d])) for s in range(rank))
+            L.check(lib.rfl_pshuf_send(h, r, dst))
+            dist.barrier(group=group)  # every peer write of this round has landed
+            recv = np.ascontiguousarray(mat[:, rank])
+            L.check(lib.rfl_pshuf_emit(h, r, recv.ctypes.data))
+            dist.barrier(group=group)  # receive buffers are free again
+        st = L.rfl_shuffle_stats()
+        if rank != 0:
+            L.check(lib.rfl_pshuf_finish(h, C.byref(st)))
+        dist.barrier(group=group)
+        if rank == 0:  # manifest.json + provenance/meta.json once every shard is on disk
+            L.check(lib.rfl_pshuf_finish(h, C.byref(st)))
+        dist.barrier(group=group)
+        return _stats(st)
+    finally:
+        for _, (ver, p) in peers.items():
+            lib.rfl_ipc_close(p, device)
+        lib.rfl_pshuf_destroy(h)

@@ -79,6 +79,30 @@ def test_shuffle_provenance_is_the_order(tmp_path):
     assert [ids[o] for o in range(5000)] == order.tolist()
 
 
+def _rank_shuffle(rank, world, inputs, total, out, c, m, seed, ocr, ocps, out_idt):
+    import paper_2604_01949_b200 as R
+    st = R.run_shuffle(inputs, R.plan_shuffle(total, c, m, seed), out,
+                       R.ShuffleOutputConfig(ocr, ocps, index_dtype=out_idt), device=0, rank=rank, world=world)
+    return st.rows_written
+
+
+@pytest.mark.parametrize("world,c,m,ocr,ocps,layout,out_idt", [
+    (2, 64, 512, 100, 2, "csr", None), (2, 7, 90, 333, 1, "csr", "u64"), (3, 16, 256, 40, 3, "csr", None),
+    (2, 32, 300, 50, 2, "dense", None)])
+def test_multi_rank_shuffle_byte_identical(tmp_path, world, c, m, ocr, ocps, layout, out_idt):
+    """The multi-GPU data path (pack kernel writing into the owners' receive
+    buffers through CUDA IPC peer pointers), with `world` processes sharing this
+    box's GPU(s), gloo for the control plane: output == reference run_shuffle."""
+    from test_multirank import _run
+    a, b = tmp_path / "a", tmp_path / "b"
+    R.synth_store(a, R.SynthConfig(1500, 60, layout, "f32", "u32", 0.1, 1, 32, 4))
+    R.synth_store(b, R.SynthConfig(450, 60, layout, "f32", "u32", 0.2, 2, 50, 2))
+    Ref.run_shuffle([a, b], tmp_path / "ref", c, m, 5, ocr, ocps, out_idt=out_idt)
+    rows = _run(world, _rank_shuffle, [str(a), str(b)], 1950, str(tmp_path / "gpu"), c, m, 5, ocr, ocps, out_idt)
+    assert sum(rows) == 1950
+    same_tree(tmp_path / "ref", tmp_path / "gpu")
+
+
 def test_shuffle_errors(tmp_path):
     R.synth_store(tmp_path / "a", R.SynthConfig(100, 10, "csr", density=0.3, chunk_rows=10))
     R.synth_store(tmp_path / "d", R.SynthConfig(100, 10, "dense", chunk_rows=10))
