@@ -228,6 +228,17 @@ rfl_status rfl_csr_densify(const rfl_arena_desc* a, const rfl_rowref* d_refs, ui
 rfl_status rfl_dense_gather(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,
                             uint32_t out_dtype, void* d_out, uint64_t* d_out_gidx, void* stream);
 
+/* K1 scan only: d_out_prefix[i] = exclusive nnz prefix of the rows,
+ * d_out_prefix[n] = total nnz (the pre-shuffle's record offsets). */
+rfl_status rfl_csr_scan(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,
+                        uint64_t* d_out_prefix, void* stream);
+/* K5: rows -> consecutive encoded CSR chunk records of chunk_rows rows
+ * (encode_csr_record, store.cpp:52-64), d_prefix from rfl_csr_scan; output
+ * byte size = sum over records of 12 + is*(rows+1) + (is+vs)*nnz. */
+rfl_status rfl_csr_pack(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,
+                        uint64_t chunk_rows, uint32_t out_index_dtype, const uint64_t* d_prefix,
+                        void* d_out, void* stream);
+
 /* ----------------------------------------------------------- preshuffle --
  * plan_shuffle (preshuffle.cpp:150-181).  Two-call protocol: pass NULL
  * arrays to learn n_rounds; round_len[n_rounds], ids[ceil(total/c)]. */

@@ -111,6 +111,8 @@ SIGNATURES = [
     ("rfl_csr_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp, vp, vp, vp]),
     ("rfl_csr_densify", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, u32, C.c_float, vp, vp, vp]),
     ("rfl_dense_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, vp, vp, vp]),
+    ("rfl_csr_scan", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp]),
+    ("rfl_csr_pack", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u64, u32, vp, vp, vp]),
     ("rfl_plan_shuffle", C.c_int, [u64, u64, u64, u64, u64p, vp, vp]),
     ("rfl_shuffle_order", C.c_int, [u64, u64, u64, u64, vp]),
     ("rfl_shuffle_round_routes", C.c_int, [u64, u64, u64, u64, u64, u64, u32, u64, u64p, u64p, vp, vp, vp]),

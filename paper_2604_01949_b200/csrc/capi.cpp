@@ -343,6 +343,27 @@ rfl_status rfl_dense_gather(const rfl_arena_desc* a, const rfl_rowref* refs, uin
     });
 }
 
+rfl_status rfl_csr_scan(const rfl_arena_desc* a, const rfl_rowref* refs, uint64_t n, uint64_t* out_prefix,
+                        void* stream) {
+    return guarded([&] {
+        auto st = static_cast<cudaStream_t>(stream);
+        void* scratch = nullptr;
+        rfl::cuda_ok(cudaMallocAsync(&scratch, rfl::csr_gather_scratch_bytes(n), st), "cudaMallocAsync");
+        rfl::launch_csr_row_scan(to_view(a), reinterpret_cast<const rfl::RowRef*>(refs), n, out_prefix, scratch, st);
+        rfl::cuda_ok(cudaFreeAsync(scratch, st), "cudaFreeAsync");
+    });
+}
+
+rfl_status rfl_csr_pack(const rfl_arena_desc* a, const rfl_rowref* refs, uint64_t n, uint64_t chunk_rows,
+                        uint32_t out_idt, const uint64_t* prefix, void* out, void* stream) {
+    return guarded([&] {
+        if (chunk_rows == 0 || out_idt > RFL_IDX_U64) rfl::invalid("csr_pack: bad chunk_rows / index dtype");
+        rfl::launch_csr_pack(to_view(a), reinterpret_cast<const rfl::RowRef*>(refs), n, chunk_rows,
+                             static_cast<rfl::IDtype>(out_idt), prefix, static_cast<uint8_t*>(out),
+                             static_cast<cudaStream_t>(stream));
+    });
+}
+
 // -------------------------------------------------------------- preshuffle --
 rfl_status rfl_plan_shuffle(uint64_t total, uint64_t c, uint64_t m, uint64_t seed, uint64_t* n_rounds,
                             uint64_t* round_len, uint64_t* ids) {

@@ -1,0 +1,164 @@
+"""Kernel micro-benchmark: every hot-path kernel on BASELINE-shaped synthetic
+stores, device-resident, CUDA-event timed (K launches over K different row
+sets, so nothing is served from L2), reported against the measured HBM peak.
+
+    python scripts/kbench.py [--cases densify_cfg1,gather_cfg1,...] [--steps K]
+Prints one JSON object per case.  Product code only (no oracle).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_2604_01949_b200 as R  # noqa: E402
+from paper_2604_01949_b200 import _lib as L  # noqa: E402
+
+STORES = {
+    "cfg1": dict(n_obs=100_000, n_var=20_000, layout="csr", value_dtype="f32", density=0.1, seed=0, chunk_rows=64),
+    "cfg2s": dict(n_obs=200_000, n_var=36_000, layout="csr", value_dtype="f32", density=3000 / 36000, seed=1,
+                  chunk_rows=1024),
+    "cfg3s": dict(n_obs=200_000, n_var=12288, layout="dense", value_dtype="u8", seed=2, chunk_rows=256),
+    "cfg4s": dict(n_obs=1_000_000, n_var=4096, layout="dense", value_dtype="u8", seed=3, chunk_rows=512),
+    "cfg5s": dict(n_obs=65_536, n_var=62_710, layout="csr", value_dtype="f32", density=2000 / 62710, seed=4,
+                  chunk_rows=64),
+}
+CASES = {  # store, kernel, rows per launch, out dtype, transform
+    "densify_cfg1": ("cfg1", "densify", 4096, L.F32, L.XF_NONE),
+    "densify_bf16_cfg1": ("cfg1", "densify", 4096, L.BF16, L.XF_NONE),
+    "gather_cfg1": ("cfg1", "gather", 4096, None, None),
+    "densify_norm_cfg2": ("cfg2s", "densify", 4096, L.F32, L.XF_NORMALIZE_LOG1P),
+    "dense_bf16_cfg3": ("cfg3s", "dense", 1024, L.BF16, None),
+    "dense_raw_cfg4": ("cfg4s", "dense", 2048, L.NATIVE, None),
+    "pack_cfg5": ("cfg5s", "pack", 65536, None, None),
+}
+
+
+def peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6650.0
+
+
+def store(name):
+    base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
+    path = base / f"kb_{name}"
+    if not (path / "manifest.json").exists():
+        base.mkdir(parents=True, exist_ok=True)
+        t = time.time()
+        s = dict(STORES[name])
+        R.synth_store(path, R.SynthConfig(**s))
+        print(f"# synth {name}: {time.time() - t:.1f}s", file=sys.stderr)
+    return path
+
+
+def row_nnz(reader, man):
+    out = np.zeros(man.n_obs, np.int64)
+    for q in range(man.chunk_count()):
+        rec = reader.read_record(q)
+        rows = int(np.frombuffer(rec, np.uint32, 1, 0)[0])
+        ip = np.frombuffer(rec, np.uint32, rows + 1, 12).astype(np.int64)
+        out[q * man.chunk_rows:q * man.chunk_rows + rows] = np.diff(ip)
+    return out
+
+
+def run_case(name, K, W, dstores):
+    import torch
+    st_name, kern, rows, od, xf = CASES[name]
+    if st_name not in dstores:
+        dstores[st_name] = R.DeviceStore(store(st_name), 0, "resident")
+    ds = dstores[st_name]
+    man = ds.manifest()
+    base, offs = ds.arena()
+    desc = ds.arena_desc()
+    rng = np.random.default_rng(0)
+    sets = [rng.choice(man.n_obs, rows, replace=False).astype(np.uint64) for _ in range(K + W)]
+    refs = np.zeros((K + W, rows, 2), np.uint64)
+    for i, g in enumerate(sets):
+        refs[i, :, 0] = offs[g.astype(np.int64) // man.chunk_rows]
+        refs[i, :, 1] = g
+    d_refs = torch.from_numpy(refs.view(np.int64)).cuda()
+    lib = L.lib()
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    vs = {"f32": 4, "f64": 8, "i32": 4, "u8": 1}[man.value_dtype]
+    isz = 4
+    nnz = None
+    if man.layout == "csr":
+        rn = row_nnz(ds.reader, man)
+        nnz = [int(rn[g.astype(np.int64)].sum()) for g in sets]
+    gout = torch.empty(rows, dtype=torch.int64, device="cuda")
+    if kern == "densify":
+        osz = 2 if od == L.BF16 else 4
+        out = torch.empty(rows * man.n_var * osz + 16, dtype=torch.uint8, device="cuda")
+        launch = lambda i: lib.rfl_csr_densify(C.byref(desc), d_refs[i].data_ptr(), rows, od, xf, 1e4,  # noqa
+                                               out.data_ptr(), gout.data_ptr(), sp)
+        alg = lambda i: nnz[i] * (isz + vs) + rows * (16 + 2 * isz + man.n_var * osz + 8)  # noqa
+    elif kern == "gather":
+        mx = max(nnz)
+        o_ip = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+        o_ix = torch.empty(mx * isz + 16, dtype=torch.uint8, device="cuda")
+        o_dv = torch.empty(mx * vs + 16, dtype=torch.uint8, device="cuda")
+        launch = lambda i: lib.rfl_csr_gather(C.byref(desc), d_refs[i].data_ptr(), rows, o_ip.data_ptr(),  # noqa
+                                              o_ix.data_ptr(), o_dv.data_ptr(), gout.data_ptr(), sp)
+        alg = lambda i: nnz[i] * 2 * (isz + vs) + rows * (16 + 2 * isz + 16)  # noqa
+    elif kern == "dense":
+        rb = man.n_var * vs
+        osz = 2 if od == L.BF16 else vs
+        out = torch.empty(rows * man.n_var * osz + 16, dtype=torch.uint8, device="cuda")
+        launch = lambda i: lib.rfl_dense_gather(C.byref(desc), d_refs[i].data_ptr(), rows, od, out.data_ptr(),  # noqa
+                                                gout.data_ptr(), sp)
+        alg = lambda i: rows * (16 + rb + man.n_var * osz + 8)  # noqa
+    else:  # pack: scan + record pack, 4096-row output chunks
+        cr = 4096
+        P = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+        mx = max(nnz)
+        out = torch.empty(mx * (isz + vs) + (rows // cr + 1) * (12 + 4 * (cr + 1)) + 16, dtype=torch.uint8,
+                          device="cuda")
+
+        def launch(i):
+            rc = lib.rfl_csr_scan(C.byref(desc), d_refs[i].data_ptr(), rows, P.data_ptr(), sp)
+            if rc:
+                return rc
+            return lib.rfl_csr_pack(C.byref(desc), d_refs[i].data_ptr(), rows, cr, L.IDX_U32, P.data_ptr(),
+                                    out.data_ptr(), sp)
+        nch = (rows + cr - 1) // cr
+        alg = lambda i: nnz[i] * 2 * (isz + vs) + rows * 2 * (16 + 2 * isz) + 12 * nch + 4 * (rows + nch)  # noqa
+    for i in range(W):
+        L.check(launch(i))
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        ev[k][0].record(stream)
+        L.check(launch(W + k))
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    ms = [s.elapsed_time(e) for s, e in ev]
+    a = [alg(W + k) for k in range(K)]
+    gbs = sum(a) / (sum(ms) / 1e3) / 1e9
+    return {"case": name, "kernel": kern, "rows_per_launch": rows, "ms_mean": float(np.mean(ms)),
+            "ms_min": float(np.min(ms)), "alg_MB_per_launch": float(np.mean(a)) / 1e6, "GBps": gbs,
+            "frac_of_measured_hbm": gbs / peak(), "rows_per_s": rows / (np.mean(ms) / 1e3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", default=",".join(CASES))
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    args = ap.parse_args()
+    dstores = {}
+    for c in args.cases.split(","):
+        print(json.dumps(run_case(c, args.steps, args.warmup, dstores)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
