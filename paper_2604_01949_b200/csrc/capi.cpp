@@ -67,6 +67,26 @@ rfl::ArenaView to_view(const rfl_arena_desc* a) {
     return v;
 }
 
+// Scratch for the raw entry points comes from the stream-ordered allocator;
+// keep freed blocks in the device pool instead of returning them to the driver
+// at every synchronisation (the default threshold of 0 made each call pay a
+// fresh allocation).
+void* scratch_alloc(size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    rfl::cuda_ok(cudaGetDevice(&dev), "cudaGetDevice");
+    static thread_local int configured = -1;
+    if (configured != dev) {
+        cudaMemPool_t pool;
+        rfl::cuda_ok(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool");
+        uint64_t keep = ~0ull;
+        rfl::cuda_ok(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool attr");
+        configured = dev;
+    }
+    void* p = nullptr;
+    rfl::cuda_ok(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
+    return p;
+}
+
 rfl::OutDtype to_od(uint32_t d) {
     switch (d) {
         case RFL_NATIVE: return rfl::OutDtype::native;
@@ -317,8 +337,7 @@ rfl_status rfl_csr_gather(const rfl_arena_desc* a, const rfl_rowref* refs, uint6
     return guarded([&] {
         const rfl::ArenaView v = to_view(a);
         auto st = static_cast<cudaStream_t>(stream);
-        void* scratch = nullptr;
-        rfl::cuda_ok(cudaMallocAsync(&scratch, rfl::csr_gather_scratch_bytes(n), st), "cudaMallocAsync");
+        void* scratch = scratch_alloc(rfl::csr_gather_scratch_bytes(n), st);
         rfl::launch_csr_gather(v, reinterpret_cast<const rfl::RowRef*>(refs), n, out_indptr, out_indices, out_data,
                                out_gidx, scratch, st);
         rfl::cuda_ok(cudaFreeAsync(scratch, st), "cudaFreeAsync");
@@ -347,8 +366,7 @@ rfl_status rfl_csr_scan(const rfl_arena_desc* a, const rfl_rowref* refs, uint64_
                         void* stream) {
     return guarded([&] {
         auto st = static_cast<cudaStream_t>(stream);
-        void* scratch = nullptr;
-        rfl::cuda_ok(cudaMallocAsync(&scratch, rfl::csr_gather_scratch_bytes(n), st), "cudaMallocAsync");
+        void* scratch = scratch_alloc(rfl::csr_gather_scratch_bytes(n), st);
         rfl::launch_csr_row_scan(to_view(a), reinterpret_cast<const rfl::RowRef*>(refs), n, out_prefix, scratch, st);
         rfl::cuda_ok(cudaFreeAsync(scratch, st), "cudaFreeAsync");
     });

@@ -499,6 +499,165 @@ __global__ void __launch_bounds__(kDenseThreads, 2)
     if (bulk && tid == 0) bulk_wait0();
 }
 
+// ============================================================ K3 densify v3 ===
+// Warp-sweep densify.  Per row: one elected thread stages the row's indices
+// and values into shared memory with two 1-D TMA bulk copies (16-B aligned
+// supersets, completion on an mbarrier) and prefetches the next row's record
+// lookup; each warp then sweeps its contiguous share of the row's columns in
+// 512-B spans: zero a 512-B per-warp tile, scatter the span's entries (sorted
+// columns: a ballot over 32 consecutive entries), and write the span with one
+// coalesced 16-B store per lane.  Every output byte is written once, straight
+// from registers; no row-sized tile, so 6 CTAs/SM keep 48 warps of rows in flight.
+constexpr int kSweepThreads = 256;
+constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr uint32_t kSpanBytes = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// index / value reads from shared or global memory at 4-B (or 1-B for u8) alignment
+template <typename T>
+__device__ __forceinline__ uint64_t ld_index_any(const uint8_t* p) {
+    if (sizeof(T) == 4) return *reinterpret_cast<const uint32_t*>(p);
+    return static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p)) |
+           (static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p + 4)) << 32);
+}
+template <typename T>
+__device__ __forceinline__ T ld_value_any(const uint8_t* p) {
+    if constexpr (sizeof(T) == 8) {
+        const uint64_t u = static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p)) |
+                           (static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p + 4)) << 32);
+        return __longlong_as_double(static_cast<long long>(u));
+    } else {
+        return *reinterpret_cast<const T*>(p);
+    }
+}
+
+template <typename IdxT, typename SrcT, typename DstT>
+__global__ void __launch_bounds__(kSweepThreads, 6)
+    k_csr_densify_sweep(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t cap, int norm,
+                        float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int vec_out) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ RowDesc s_desc[2];
+    __shared__ double s_red[kSweepWarps];
+    constexpr uint32_t is = sizeof(IdxT), vs = sizeof(SrcT), os = sizeof(DstT);
+    constexpr uint32_t span_cols = kSpanBytes / os, lane_cols = 16 / os;
+    uint8_t* s_idx = smem;                                                   // cap*is + 16
+    uint8_t* s_val = smem + ((cap * is + 16 + 127) & ~127u);                 // cap*vs + 16
+    uint8_t* s_tile = s_val + ((cap * vs + 16 + 127) & ~127u);               // kSweepWarps * 512
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint8_t* tile = s_tile + warp * kSpanBytes;
+    const uint64_t n_var = a.n_var;
+    const uint64_t n_spans = (n_var + span_cols - 1) / span_cols;
+    const uint64_t spw = (n_spans + kSweepWarps - 1) / kSweepWarps;
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], vs);
+    }
+    __syncthreads();
+    uint32_t phase = 0, cur = 0;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x, cur ^= 1u) {
+        const RowDesc d = s_desc[cur];
+        const bool staged = d.nnz > 0 && d.nnz <= cap;
+        const uintptr_t ia = reinterpret_cast<uintptr_t>(d.idx), va = reinterpret_cast<uintptr_t>(d.val);
+        if (tid == 0) {
+            if (staged) {  // 16-B aligned supersets of the row's indices and values
+                const uint32_t ib = static_cast<uint32_t>(((ia + d.nnz * is + 15) & ~uintptr_t(15)) - (ia & ~uintptr_t(15)));
+                const uint32_t vb = static_cast<uint32_t>(((va + d.nnz * vs + 15) & ~uintptr_t(15)) - (va & ~uintptr_t(15)));
+                mbar_arrive_expect_tx(&s_bar, ib + vb);
+                bulk_load(s_idx, reinterpret_cast<const void*>(ia & ~uintptr_t(15)), ib, &s_bar);
+                bulk_load(s_val, reinterpret_cast<const void*>(va & ~uintptr_t(15)), vb, &s_bar);
+            }
+            if (row + gridDim.x < n_rows) s_desc[cur ^ 1u] = describe_row<IdxT>(a, refs[row + gridDim.x], vs);
+            if (out_gidx) out_gidx[row] = d.gidx;
+        }
+        const uint8_t* E_idx = staged ? s_idx + (ia & 15u) : d.idx;
+        const uint8_t* E_val = staged ? s_val + (va & 15u) : d.val;
+        if (staged) {
+            mbar_wait(&s_bar, phase);
+            phase ^= 1u;
+        }
+        float scale = 1.0f;
+        if (norm) {  // library size in fp64
+            double s = 0.0;
+            for (uint64_t k = tid; k < d.nnz; k += kSweepThreads) s += static_cast<double>(ld_value_any<SrcT>(E_val + k * vs));
+            s = block_sum(s, s_red);
+            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
+        }
+        const uint64_t sp0 = warp * spw, sp1 = umin64(n_spans, sp0 + spw);
+        DstT* orow = out + row * n_var;
+        if (sp0 < sp1) {
+            // first entry of this warp's column range (lower bound over sorted columns)
+            uint64_t cursor = 0;
+            if (lane == 0) {
+                uint64_t lo = 0, hi = d.nnz;
+                const uint64_t c_begin = sp0 * span_cols;
+                while (lo < hi) {
+                    const uint64_t mid = (lo + hi) >> 1;
+                    if (ld_index_any<IdxT>(E_idx + mid * is) < c_begin) lo = mid + 1;
+                    else hi = mid;
+                }
+                cursor = lo;
+            }
+            cursor = __shfl_sync(kFull, cursor, 0);
+            for (uint64_t sp = sp0; sp < sp1; ++sp) {
+                const uint64_t c0 = sp * span_cols, c1 = umin64(n_var, c0 + span_cols);
+                reinterpret_cast<uint4*>(tile)[lane] = make_uint4(0, 0, 0, 0);
+                __syncwarp();
+                for (;;) {  // entries of [c0, c1): a prefix of the next 32 (columns are sorted)
+                    const uint64_t e = cursor + lane;
+                    uint64_t col = ~0ull;
+                    if (e < d.nnz) col = ld_index_any<IdxT>(E_idx + e * is);
+                    const bool in = col < c1;
+                    const uint32_t m = __ballot_sync(kFull, in);
+                    if (in && col >= c0)
+                        reinterpret_cast<DstT*>(tile)[col - c0] =
+                            Conv<DstT, SrcT>::go(ld_value_any<SrcT>(E_val + e * vs), scale, norm);
+                    const uint32_t cnt = __popc(m);
+                    cursor += cnt;
+                    if (cnt < 32) break;
+                }
+                __syncwarp();
+                const uint4 v = reinterpret_cast<const uint4*>(tile)[lane];
+                const uint64_t cl = c0 + static_cast<uint64_t>(lane) * lane_cols;
+                if (vec_out && cl + lane_cols <= c1) {
+                    st_v4(orow + cl, v);
+                } else if (cl < c1) {
+                    const DstT* tv = reinterpret_cast<const DstT*>(&v);
+                    for (uint32_t j = 0; j < lane_cols && cl + j < c1; ++j) orow[cl + j] = tv[j];
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();  // staging buffers are re-filled for the next row
+    }
+}
+
 // ============================================================ K4 dense gather ===
 constexpr int kDenseGatherThreads = 256;
 enum DenseMode { kRaw = 0, kU8ToBf16 = 1, kF32ToBf16 = 2 };
@@ -568,9 +727,32 @@ void set_smem(K kernel, size_t bytes) {
                "cudaFuncSetAttribute");
 }
 
+bool use_densify_v2() {  // A/B switch for the round-1 smem-tile kernel
+    static const bool v2 = [] {
+        const char* e = std::getenv("RFL_DENSIFY_V2");
+        return e && e[0] == '1';
+    }();
+    return v2;
+}
+
 template <typename IdxT, typename SrcT, typename DstT>
 void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                uint64_t* out_gidx, cudaStream_t st) {
+    if (!use_densify_v2()) {
+        constexpr uint32_t is = sizeof(IdxT), vs = sizeof(SrcT);
+        const uint32_t cap = (32768u / (is + vs)) & ~31u;  // entries staged per row (longer rows: global path)
+        const size_t smem = ((cap * is + 16 + 127) & ~127u) + ((cap * vs + 16 + 127) & ~127u) + kSweepWarps * kSpanBytes;
+        const int vec = ((av.n_var * sizeof(DstT)) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+        auto kern = k_csr_densify_sweep<IdxT, SrcT, DstT>;
+        set_smem(kern, smem);
+        int per_sm = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSweepThreads, smem), "occupancy");
+        const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
+        kern<<<static_cast<unsigned>(grid), kSweepThreads, smem, st>>>(dev_view(av), refs, n, cap, norm ? 1 : 0, target,
+                                                                     static_cast<DstT*>(out), out_gidx, vec);
+        cuda_check(cudaGetLastError(), "k_csr_densify_sweep launch");
+        return;
+    }
     const uint64_t esz = sizeof(DstT);
     uint64_t tile_cols = av.n_var;
     if (av.n_var * esz > kMaxTileBytes) tile_cols = (kMaxTileBytes / esz) & ~15ull;
