@@ -406,17 +406,18 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // One CTA per output row (grid-stride): zero a shared-memory tile, scatter the
 // row's entries into it, then a single cp.async.bulk store writes the dense
 // tile — every output byte hits HBM exactly once, with no read-modify-write.
-template <typename IdxT, typename SrcT, typename DstT>
-__global__ void __launch_bounds__(kDenseThreads, 2)
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U>
+__global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     k_csr_densify(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ double s_red[kDenseThreads / 32];
+    __shared__ double s_red[THREADS / 32];
     __shared__ RowDesc s_desc[2];  // current / next row, software-pipelined
     DstT* tile = reinterpret_cast<DstT*>(smem);
-    const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+    const uint32_t tid = threadIdx.x;
+    constexpr uint32_t nthr = THREADS;
     const uint64_t n_var = a.n_var;
-    constexpr uint32_t U = 4;  // entries per thread held in registers across the zero-fill
+    // U entries per thread are held in registers across the zero-fill
     if (tid == 0 && blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
     __syncthreads();
     uint32_t cur = 0;
@@ -727,18 +728,55 @@ void set_smem(K kernel, size_t bytes) {
                "cudaFuncSetAttribute");
 }
 
-bool use_densify_v2() {  // A/B switch for the round-1 smem-tile kernel
-    static const bool v2 = [] {
-        const char* e = std::getenv("RFL_DENSIFY_V2");
-        return e && e[0] == '1';
+// Densify variant (RFL_DENSIFY="v2:<threads>:<tile KB>" | "v3"), for A/B runs.
+struct DensifyCfg {
+    int version = 2, threads = 512, tile_kb = 100;
+};
+const DensifyCfg& densify_cfg() {
+    static const DensifyCfg c = [] {
+        DensifyCfg d;
+        const char* e = std::getenv("RFL_DENSIFY");
+        if (e && e[0] == 'v') {
+            int v = 2, t = 512, kb = 100;
+            const int got = std::sscanf(e, "v%d:%d:%d", &v, &t, &kb);
+            d.version = v;
+            if (got >= 2 && (t == 128 || t == 256 || t == 512)) d.threads = t;
+            if (got >= 3 && kb >= 4 && kb <= 200) d.tile_kb = kb;
+        }
+        return d;
     }();
-    return v2;
+    return c;
+}
+
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U>
+void densify_v2(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
+                uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes) {
+    const uint64_t esz = sizeof(DstT);
+    uint64_t tile_cols = av.n_var;
+    if (av.n_var * esz > max_tile_bytes) tile_cols = (max_tile_bytes / esz) & ~15ull;
+    const size_t smem = ((tile_cols * esz + 15) & ~15ull);
+    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    auto kern = k_csr_densify<IdxT, SrcT, DstT, THREADS, U>;
+    set_smem(kern, smem);
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem), "occupancy");
+    const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
+    kern<<<static_cast<unsigned>(grid), THREADS, smem, st>>>(dev_view(av), refs, n, static_cast<uint32_t>(tile_cols),
+                                                          norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
+    cuda_check(cudaGetLastError(), "k_csr_densify launch");
 }
 
 template <typename IdxT, typename SrcT, typename DstT>
 void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                uint64_t* out_gidx, cudaStream_t st) {
-    if (!use_densify_v2()) {
+    const DensifyCfg& dc = densify_cfg();
+    if (dc.version == 2) {
+        const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
+        if (dc.threads == 512) return densify_v2<IdxT, SrcT, DstT, 512, 4>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        if (dc.threads == 256) return densify_v2<IdxT, SrcT, DstT, 256, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        return densify_v2<IdxT, SrcT, DstT, 128, 16>(av, refs, n, norm, target, out, out_gidx, st, tb);
+    }
+    {
         constexpr uint32_t is = sizeof(IdxT), vs = sizeof(SrcT);
         const uint32_t cap = (32768u / (is + vs)) & ~31u;  // entries staged per row (longer rows: global path)
         const size_t smem = ((cap * is + 16 + 127) & ~127u) + ((cap * vs + 16 + 127) & ~127u) + kSweepWarps * kSpanBytes;
@@ -751,22 +789,7 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
         kern<<<static_cast<unsigned>(grid), kSweepThreads, smem, st>>>(dev_view(av), refs, n, cap, norm ? 1 : 0, target,
                                                                      static_cast<DstT*>(out), out_gidx, vec);
         cuda_check(cudaGetLastError(), "k_csr_densify_sweep launch");
-        return;
     }
-    const uint64_t esz = sizeof(DstT);
-    uint64_t tile_cols = av.n_var;
-    if (av.n_var * esz > kMaxTileBytes) tile_cols = (kMaxTileBytes / esz) & ~15ull;
-    const size_t smem = ((tile_cols * esz + 15) & ~15ull);
-    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    auto kern = k_csr_densify<IdxT, SrcT, DstT>;
-    set_smem(kern, smem);
-    int per_sm = 0;
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDenseThreads, smem), "occupancy");
-    const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
-    kern<<<static_cast<unsigned>(grid), kDenseThreads, smem, st>>>(dev_view(av), refs, n, static_cast<uint32_t>(tile_cols),
-                                                              norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx,
-                                                              bulk);
-    cuda_check(cudaGetLastError(), "k_csr_densify launch");
 }
 
 template <typename IdxT>
