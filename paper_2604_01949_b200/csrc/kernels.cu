@@ -93,6 +93,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // ------------------------------------------------ 128-bit shifted warp copy ---
@@ -406,14 +409,15 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // One CTA per output row (grid-stride): zero a shared-memory tile, scatter the
 // row's entries into it, then a single cp.async.bulk store writes the dense
 // tile — every output byte hits HBM exactly once, with no read-modify-write.
-template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U>
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int NBUF>
 __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
     k_csr_densify(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ double s_red[THREADS / 32];
     __shared__ RowDesc s_desc[2];  // current / next row, software-pipelined
-    DstT* tile = reinterpret_cast<DstT*>(smem);
+    const uint32_t tile_stride = (tile_cols * static_cast<uint32_t>(sizeof(DstT)) + 127u) & ~127u;
+    uint32_t tcount = 0;  // tiles issued by this CTA (selects the buffer)
     const uint32_t tid = threadIdx.x;
     constexpr uint32_t nthr = THREADS;
     const uint64_t n_var = a.n_var;
@@ -453,14 +457,21 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
             scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
         }
         DstT* orow = out + row * n_var;
-        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols, ++tcount) {
             const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
             const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
-            if (bulk && tid == 0) bulk_wait_read0();  // previous tile's bulk store has read smem
+            uint8_t* buf = smem + (NBUF == 1 ? 0u : (tcount & 1u) * tile_stride);
+            DstT* tile = reinterpret_cast<DstT*>(buf);
+            // the bulk store that last read this buffer has drained (NBUF=2: the
+            // other buffer's store may still be in flight while we build this one)
+            if (bulk && tid == 0) {
+                if (NBUF == 1) bulk_wait_read0();
+                else bulk_wait_read1();
+            }
             __syncthreads();
-            uint4* t4 = reinterpret_cast<uint4*>(smem);
+            uint4* t4 = reinterpret_cast<uint4*>(buf);
             for (uint32_t i = tid; i < bytes / 16u; i += nthr) t4[i] = make_uint4(0, 0, 0, 0);
-            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) smem[i] = 0;
+            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) buf[i] = 0;
             __syncthreads();
 #pragma unroll
             for (uint32_t u = 0; u < U; ++u)
@@ -488,7 +499,7 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 fence_proxy_async_shared();  // make generic-proxy smem writes visible to the bulk engine
                 __syncthreads();
                 if (tid == 0) {
-                    bulk_store(orow + c0, smem, bytes);
+                    bulk_store(orow + c0, buf, bytes);
                     bulk_commit();
                 }
             } else {
@@ -748,15 +759,15 @@ const DensifyCfg& densify_cfg() {
     return c;
 }
 
-template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U>
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int NBUF>
 void densify_v2(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                 uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes) {
     const uint64_t esz = sizeof(DstT);
     uint64_t tile_cols = av.n_var;
     if (av.n_var * esz > max_tile_bytes) tile_cols = (max_tile_bytes / esz) & ~15ull;
-    const size_t smem = ((tile_cols * esz + 15) & ~15ull);
+    const size_t smem = NBUF * ((tile_cols * esz + 127) & ~127ull);
     const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    auto kern = k_csr_densify<IdxT, SrcT, DstT, THREADS, U>;
+    auto kern = k_csr_densify<IdxT, SrcT, DstT, THREADS, U, NBUF>;
     set_smem(kern, smem);
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem), "occupancy");
@@ -770,11 +781,16 @@ template <typename IdxT, typename SrcT, typename DstT>
 void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                uint64_t* out_gidx, cudaStream_t st) {
     const DensifyCfg& dc = densify_cfg();
-    if (dc.version == 2) {
+    if (dc.version == 2 || dc.version == 4) {  // v4 = v2 with a double-buffered tile
         const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
-        if (dc.threads == 512) return densify_v2<IdxT, SrcT, DstT, 512, 4>(av, refs, n, norm, target, out, out_gidx, st, tb);
-        if (dc.threads == 256) return densify_v2<IdxT, SrcT, DstT, 256, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
-        return densify_v2<IdxT, SrcT, DstT, 128, 16>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        if (dc.version == 4) {
+            if (dc.threads == 512)
+                return densify_v2<IdxT, SrcT, DstT, 512, 4, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            return densify_v2<IdxT, SrcT, DstT, 256, 8, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        }
+        if (dc.threads == 512)
+            return densify_v2<IdxT, SrcT, DstT, 512, 4, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        return densify_v2<IdxT, SrcT, DstT, 256, 8, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
     }
     {
         constexpr uint32_t is = sizeof(IdxT), vs = sizeof(SrcT);
