@@ -729,6 +729,66 @@ __global__ void __launch_bounds__(kDenseGatherThreads)
     }
 }
 
+// Flat variant for 16-B aligned rows: work unit = (row, span of 32*U 16-B
+// chunks); one lane reads the row's RowRef, every lane issues U independent
+// 16-B loads before any store, so a warp keeps 32*U*16 B in flight and all
+// rows of a (small) batch are in flight at once.
+constexpr int kDgThreads = 256;
+constexpr int kDgU = 4;
+
+template <int MODE>
+__global__ void __launch_bounds__(kDgThreads)
+    k_dense_gather_flat(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
+                        uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t cpr = in_row_bytes / 16;                    // 16-B chunks per input row
+    const uint64_t upr = (cpr + 32 * kDgU - 1) / (32 * kDgU);  // units per row
+    const uint64_t n_units = n_rows * upr;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kDgThreads / 32);
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * (kDgThreads / 32) + (threadIdx.x >> 5); u < n_units;
+         u += warps) {
+        const uint64_t row = u / upr, part = u - row * upr;
+        uint64_t off = 0, g = 0;
+        if (lane == 0) {
+            const RowRef r = refs[row];
+            off = r.rec_off + (r.gidx % a.chunk_rows) * in_row_bytes;
+            g = r.gidx;
+        }
+        off = __shfl_sync(kFull, off, 0);
+        if (part == 0 && lane == 0 && out_gidx) out_gidx[row] = g;
+        const uint4* src = reinterpret_cast<const uint4*>(a.base + off);
+        const uint64_t c0 = part * 32 * kDgU + lane;
+        uint4 v[kDgU];
+#pragma unroll
+        for (int k = 0; k < kDgU; ++k)
+            if (c0 + k * 32 < cpr) v[k] = ld_v4(src + c0 + k * 32);
+        uint8_t* dst = out + row * out_row_bytes;
+#pragma unroll
+        for (int k = 0; k < kDgU; ++k) {
+            const uint64_t c = c0 + k * 32;
+            if (c >= cpr) break;
+            if (MODE == kRaw) {
+                st_v4(dst + c * 16, v[k]);
+            } else if (MODE == kU8ToBf16) {
+                const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                uint32_t o[8];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    o[2 * j] = pack_bf16x2(float(w[j] & 0xff), float((w[j] >> 8) & 0xff));
+                    o[2 * j + 1] = pack_bf16x2(float((w[j] >> 16) & 0xff), float(w[j] >> 24));
+                }
+                st_v4(dst + c * 32, make_uint4(o[0], o[1], o[2], o[3]));
+                st_v4(dst + c * 32 + 16, make_uint4(o[4], o[5], o[6], o[7]));
+            } else {  // f32 -> bf16
+                uint2 o;
+                o.x = pack_bf16x2(__uint_as_float(v[k].x), __uint_as_float(v[k].y));
+                o.y = pack_bf16x2(__uint_as_float(v[k].z), __uint_as_float(v[k].w));
+                *reinterpret_cast<uint2*>(dst + c * 8) = o;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------ host helpers ---
 int g_sm_count = 0;
 std::once_flag g_sm_once;
@@ -740,8 +800,8 @@ void set_smem(K kernel, size_t bytes) {
 }
 
 // Densify variant (RFL_DENSIFY="v2:<threads>:<tile KB>" | "v3"), for A/B runs.
-struct DensifyCfg {
-    int version = 2, threads = 512, tile_kb = 100;
+struct DensifyCfg {  // default = best measured on B200 (scripts/ab_densify.sh, profiles/)
+    int version = 2, threads = 256, tile_kb = 40;
 };
 const DensifyCfg& densify_cfg() {
     static const DensifyCfg c = [] {
@@ -918,6 +978,26 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, 8ull * device_sm_count()));
     const ArenaDev d = dev_view(a);
     auto* o = static_cast<uint8_t*>(out);
+    // records sit at 16-B aligned offsets, so rows are 16-B aligned whenever row_bytes is
+    const bool flat = in_rb % 16 == 0 && reinterpret_cast<uintptr_t>(a.base) % 16 == 0 &&
+                      reinterpret_cast<uintptr_t>(out) % 16 == 0;
+    if (flat) {
+        const uint64_t upr = (in_rb / 16 + 32 * kDgU - 1) / (32 * kDgU);
+        const uint64_t warps_needed = n * upr;
+        const unsigned g2 = static_cast<unsigned>(std::max<uint64_t>(
+            1, std::min<uint64_t>((warps_needed + kDgThreads / 32 - 1) / (kDgThreads / 32), 8ull * device_sm_count())));
+        if (od == OutDtype::bf16 && a.vdt == VDtype::u8) {
+            k_dense_gather_flat<kU8ToBf16><<<g2, kDgThreads, 0, st>>>(d, in_rb, refs, n, o, a.n_var * 2, out_gidx);
+        } else if (od == OutDtype::bf16 && a.vdt == VDtype::f32) {
+            k_dense_gather_flat<kF32ToBf16><<<g2, kDgThreads, 0, st>>>(d, in_rb, refs, n, o, a.n_var * 2, out_gidx);
+        } else if (od == OutDtype::native || (od == OutDtype::f32 && a.vdt == VDtype::f32)) {
+            k_dense_gather_flat<kRaw><<<g2, kDgThreads, 0, st>>>(d, in_rb, refs, n, o, in_rb, out_gidx);
+        } else {
+            invalid("dense_gather: unsupported output dtype for this store");
+        }
+        cuda_check(cudaGetLastError(), "k_dense_gather_flat launch");
+        return;
+    }
     if (od == OutDtype::bf16) {
         if (a.vdt == VDtype::u8)
             k_dense_gather<kU8ToBf16><<<grid, kDenseGatherThreads, 0, st>>>(d, in_rb, refs, n, o, a.n_var * 2, out_gidx);
