@@ -148,31 +148,25 @@ __device__ __forceinline__ void warp_copy(uint8_t* __restrict__ dst, const uint8
         }
         for (; i < nvec; i += 32) st_v4(d4 + i, ld_v4(s4 + i));
     } else {
+        // destination chunk i = source bytes straddling aligned chunks i and i+1;
+        // both are loaded through L1 (chunk i+1 is the next lane's chunk i, an L1
+        // hit), 4 pairs in flight per lane
         const uint4* s4 = reinterpret_cast<const uint4*>(src - sh);
-        for (uint64_t base = 0; base < nvec; base += 64) {
-            const uint64_t i0 = base + lane, i1 = base + 32 + lane;
-            uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, t0, t1;
-            if (i0 < nvec) a0 = ld_v4(s4 + i0);
-            if (i1 < nvec) a1 = ld_v4(s4 + i1);
-            // chunk i+1: lane+1's chunk, or for lane 31 the next group's lane 0
-            t0.x = __shfl_down_sync(kFull, a0.x, 1);
-            t0.y = __shfl_down_sync(kFull, a0.y, 1);
-            t0.z = __shfl_down_sync(kFull, a0.z, 1);
-            t0.w = __shfl_down_sync(kFull, a0.w, 1);
-            t1.x = __shfl_down_sync(kFull, a1.x, 1);
-            t1.y = __shfl_down_sync(kFull, a1.y, 1);
-            t1.z = __shfl_down_sync(kFull, a1.z, 1);
-            t1.w = __shfl_down_sync(kFull, a1.w, 1);
-            const uint4 n0 = make_uint4(__shfl_sync(kFull, a1.x, 0), __shfl_sync(kFull, a1.y, 0),
-                                        __shfl_sync(kFull, a1.z, 0), __shfl_sync(kFull, a1.w, 0));
-            if (lane == 31) t0 = n0;
-            if (i0 < nvec) {
-                if (i0 + 1 >= nvec) t0 = ld_v4(s4 + i0 + 1);
-                st_v4(d4 + i0, shift_merge(a0, t0, sh));
+        constexpr int UC = 4;
+        for (uint64_t base = 0; base < nvec; base += 32 * UC) {
+            uint4 a[UC], b[UC];
+#pragma unroll
+            for (int k = 0; k < UC; ++k) {
+                const uint64_t i = base + k * 32 + lane;
+                if (i < nvec) {
+                    a[k] = __ldg(s4 + i);
+                    b[k] = __ldg(s4 + i + 1);
+                }
             }
-            if (i1 < nvec) {
-                if (lane == 31 || i1 + 1 >= nvec) t1 = ld_v4(s4 + i1 + 1);
-                st_v4(d4 + i1, shift_merge(a1, t1, sh));
+#pragma unroll
+            for (int k = 0; k < UC; ++k) {
+                const uint64_t i = base + k * 32 + lane;
+                if (i < nvec) st_v4(d4 + i, shift_merge(a[k], b[k], sh));
             }
         }
     }
@@ -217,7 +211,7 @@ __device__ __forceinline__ RowDesc describe_row(const ArenaDev& a, const RowRef&
 
 // ============================================================ K1/K2 gather ===
 constexpr int kGatherThreads = 256;
-constexpr int kGatherTile = 16;  // rows per CTA
+constexpr int kGatherTile = 8;  // rows per CTA: one warp per (row, array) copy job
 constexpr uint64_t kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
@@ -293,11 +287,12 @@ __global__ void __launch_bounds__(kGatherThreads) k_csr_gather(ArenaDev a, uint3
     }
     __syncthreads();
     if (out_idx == nullptr) return;  // scan-only launch (pre-shuffle record offsets)
-    for (uint32_t r = warp; r < static_cast<uint32_t>(kGatherTile); r += kGatherThreads / 32) {
+    for (uint32_t job = warp; job < 2u * kGatherTile; job += kGatherThreads / 32) {  // (row, array) jobs
+        const uint32_t r = job >> 1;
         if (row0 + r >= n_rows) break;
         const uint64_t off = s_off[r], n = s_nnz[r];
-        warp_copy(out_idx + off * sizeof(IdxT), s_idx[r], n * sizeof(IdxT), lane);
-        warp_copy(out_val + off * vs, s_val[r], n * vs, lane);
+        if (job & 1u) warp_copy(out_val + off * vs, s_val[r], n * vs, lane);
+        else warp_copy(out_idx + off * sizeof(IdxT), s_idx[r], n * sizeof(IdxT), lane);
     }
 }
 
