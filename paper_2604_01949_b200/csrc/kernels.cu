@@ -210,9 +210,20 @@ __device__ __forceinline__ RowDesc describe_row(const ArenaDev& a, const RowRef&
 }
 
 // ============================================================ K1/K2 gather ===
-constexpr int kGatherThreads = 256;
-constexpr int kGatherTile = 8;  // rows per CTA: one warp per (row, array) copy job
+// Two launches: (1) k_row_scan — one thread per row resolves the row inside its
+// chunk record (ref -> header -> indptr), a block scan plus a decoupled
+// look-back across 128-row tiles (dynamic tile ids, 32-tile windows) writes the
+// output indptr and a per-row job table {indices ptr, values ptr};
+// (2) k_csr_copy — every warp grid-strides over (row, array) copy jobs with the
+// 128-bit shifted warp copy; no barriers, so the whole GPU stays busy.
+constexpr int kScanThreads = 128;
+constexpr int kCopyThreads = 256;
 constexpr uint64_t kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+struct RowJob {
+    const uint8_t* idx;
+    const uint8_t* val;
+};
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -220,45 +231,41 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 }
 
 template <typename IdxT>
-__global__ void __launch_bounds__(kGatherThreads) k_csr_gather(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs,
-                                                               uint64_t n_rows, uint64_t* __restrict__ out_indptr,
-                                                               uint8_t* __restrict__ out_idx,
-                                                               uint8_t* __restrict__ out_val,
-                                                               uint64_t* __restrict__ out_gidx,
-                                                               unsigned long long* __restrict__ scratch) {
-    __shared__ uint64_t s_off[kGatherTile];
-    __shared__ uint64_t s_nnz[kGatherTile];
-    __shared__ const uint8_t* s_idx[kGatherTile];
-    __shared__ const uint8_t* s_val[kGatherTile];
-    __shared__ uint64_t s_tile;
+__global__ void __launch_bounds__(kScanThreads)
+    k_row_scan(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, uint64_t n_rows,
+               uint64_t* __restrict__ out_prefix, RowJob* __restrict__ jobs, uint64_t* __restrict__ out_gidx,
+               unsigned long long* __restrict__ scratch) {
+    __shared__ uint64_t s_warp[kScanThreads / 32];
+    __shared__ uint64_t s_tile, s_prefix;
     unsigned long long* counter = scratch;
     unsigned long long* status = scratch + 1;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-
     // dynamic tile ids make the look-back deadlock free (earlier tiles are resident)
     if (tid == 0) s_tile = atomicAdd(counter, 1ull);
     __syncthreads();
     const uint64_t tile = s_tile;
-    const uint64_t row0 = tile * kGatherTile;
-
-    if (warp == 0) {
-        uint64_t nnz = 0;
-        if (lane < kGatherTile && row0 + lane < n_rows) {
-            const RowRef r = refs[row0 + lane];
-            const CsrRow cr = csr_row<IdxT>(a, r, vs);
-            s_idx[lane] = cr.idx;
-            s_val[lane] = cr.val;
-            s_nnz[lane] = cr.nnz;
-            nnz = cr.nnz;
-            if (out_gidx) out_gidx[row0 + lane] = r.gidx;
-        }
-        uint64_t incl = nnz;  // warp-level indptr scan
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t v = __shfl_up_sync(kFull, incl, o);
-            if (lane >= static_cast<uint32_t>(o)) incl += v;
-        }
-        const uint64_t agg = __shfl_sync(kFull, incl, 31);
-        // decoupled look-back over a 32-tile window
+    const uint64_t row = tile * kScanThreads + tid;
+    uint64_t nnz = 0;
+    if (row < n_rows) {
+        const RowRef r = refs[row];
+        const CsrRow cr = csr_row<IdxT>(a, r, vs);
+        nnz = cr.nnz;
+        if (jobs) jobs[row] = {cr.idx, cr.val};
+        if (out_gidx) out_gidx[row] = r.gidx;
+    }
+    uint64_t incl = nnz;  // warp-level indptr scan, then across the block's warps
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint64_t agg = 0;
+    for (uint32_t w = 0; w < kScanThreads / 32; ++w) {
+        if (w < warp) incl += s_warp[w];
+        agg += s_warp[w];
+    }
+    if (warp == 0) {  // decoupled look-back over a 32-tile window
         uint64_t prefix = 0;
         if (tile == 0) {
             if (lane == 0) st_volatile_u64(&status[0], kFlagP | agg);
@@ -280,19 +287,28 @@ __global__ void __launch_bounds__(kGatherThreads) k_csr_gather(ArenaDev a, uint3
             }
             if (lane == 0) st_volatile_u64(&status[tile], kFlagP | (prefix + agg));
         }
-        const uint64_t excl = prefix + incl - nnz;
-        if (lane < kGatherTile) s_off[lane] = excl;
-        if (lane < kGatherTile && row0 + lane < n_rows) out_indptr[row0 + lane] = excl;
-        if (lane == 0 && row0 + kGatherTile >= n_rows) out_indptr[n_rows] = prefix + agg;
+        if (lane == 0) s_prefix = prefix;
     }
     __syncthreads();
-    if (out_idx == nullptr) return;  // scan-only launch (pre-shuffle record offsets)
-    for (uint32_t job = warp; job < 2u * kGatherTile; job += kGatherThreads / 32) {  // (row, array) jobs
-        const uint32_t r = job >> 1;
-        if (row0 + r >= n_rows) break;
-        const uint64_t off = s_off[r], n = s_nnz[r];
-        if (job & 1u) warp_copy(out_val + off * vs, s_val[r], n * vs, lane);
-        else warp_copy(out_idx + off * sizeof(IdxT), s_idx[r], n * sizeof(IdxT), lane);
+    if (row < n_rows) out_prefix[row] = s_prefix + incl - nnz;
+    if (tid == 0 && (tile + 1) * kScanThreads >= n_rows) out_prefix[n_rows] = s_prefix + agg;
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kCopyThreads, 4)
+    k_csr_copy(const RowJob* __restrict__ jobs, const uint64_t* __restrict__ P, uint64_t n_rows, uint32_t vs,
+               uint8_t* __restrict__ out_idx, uint8_t* __restrict__ out_val) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kCopyThreads / 32);
+    const uint64_t p0 = P[0];
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * (kCopyThreads / 32) + (threadIdx.x >> 5); j < 2 * n_rows;
+         j += warps) {
+        const uint64_t row = j >> 1;
+        const bool val = j & 1u;
+        const uint64_t off = P[row] - p0, cnt = P[row + 1] - P[row];
+        const RowJob jb = jobs[row];
+        const uint32_t es = val ? vs : static_cast<uint32_t>(sizeof(IdxT));
+        warp_copy((val ? out_val : out_idx) + off * es, val ? jb.val : jb.idx, cnt * es, lane);
     }
 }
 
@@ -898,10 +914,26 @@ int device_sm_count() {
     return c;
 }
 
-size_t csr_gather_scratch_bytes(uint64_t n_rows) {
-    const uint64_t tiles = (n_rows + kGatherTile - 1) / kGatherTile;
-    return (1 + tiles) * sizeof(unsigned long long);
+namespace {
+uint64_t scan_status_bytes(uint64_t n_rows) {
+    const uint64_t tiles = (n_rows + kScanThreads - 1) / kScanThreads;
+    return ((1 + tiles) * sizeof(unsigned long long) + 15) & ~15ull;
 }
+void launch_scan(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_prefix, RowJob* jobs,
+                 uint64_t* out_gidx, void* scratch, cudaStream_t st) {
+    cuda_check(cudaMemsetAsync(scratch, 0, scan_status_bytes(n), st), "memset scratch");
+    const unsigned tiles = static_cast<unsigned>((n + kScanThreads - 1) / kScanThreads);
+    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
+    auto* sc = static_cast<unsigned long long*>(scratch);
+    if (a.idt == IDtype::u32)
+        k_row_scan<uint32_t><<<tiles, kScanThreads, 0, st>>>(dev_view(a), vs, refs, n, out_prefix, jobs, out_gidx, sc);
+    else
+        k_row_scan<uint64_t><<<tiles, kScanThreads, 0, st>>>(dev_view(a), vs, refs, n, out_prefix, jobs, out_gidx, sc);
+    cuda_check(cudaGetLastError(), "k_row_scan launch");
+}
+}  // namespace
+
+size_t csr_gather_scratch_bytes(uint64_t n_rows) { return scan_status_bytes(n_rows) + n_rows * sizeof(RowJob); }
 
 void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_indptr, void* out_indices,
                        void* out_data, uint64_t* out_gidx, void* scratch, cudaStream_t st) {
@@ -910,24 +942,27 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
         cuda_check(cudaMemsetAsync(out_indptr, 0, sizeof(uint64_t), st), "memset");
         return;
     }
-    cuda_check(cudaMemsetAsync(scratch, 0, csr_gather_scratch_bytes(n), st), "memset scratch");
-    const uint64_t tiles = (n + kGatherTile - 1) / kGatherTile;
+    RowJob* jobs = reinterpret_cast<RowJob*>(static_cast<uint8_t*>(scratch) + scan_status_bytes(n));
+    launch_scan(a, refs, n, out_indptr, jobs, out_gidx, scratch, st);
+    const unsigned grid = static_cast<unsigned>(
+        std::min<uint64_t>((2 * n + kCopyThreads / 32 - 1) / (kCopyThreads / 32), 8ull * device_sm_count()));
     const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
-    auto* sc = static_cast<unsigned long long*>(scratch);
     if (a.idt == IDtype::u32)
-        k_csr_gather<uint32_t><<<static_cast<unsigned>(tiles), kGatherThreads, 0, st>>>(
-            dev_view(a), vs, refs, n, out_indptr, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data),
-            out_gidx, sc);
+        k_csr_copy<uint32_t><<<grid, kCopyThreads, 0, st>>>(jobs, out_indptr, n, vs, static_cast<uint8_t*>(out_indices),
+                                                           static_cast<uint8_t*>(out_data));
     else
-        k_csr_gather<uint64_t><<<static_cast<unsigned>(tiles), kGatherThreads, 0, st>>>(
-            dev_view(a), vs, refs, n, out_indptr, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data),
-            out_gidx, sc);
-    cuda_check(cudaGetLastError(), "k_csr_gather launch");
+        k_csr_copy<uint64_t><<<grid, kCopyThreads, 0, st>>>(jobs, out_indptr, n, vs, static_cast<uint8_t*>(out_indices),
+                                                           static_cast<uint8_t*>(out_data));
+    cuda_check(cudaGetLastError(), "k_csr_copy launch");
 }
 
 void launch_csr_row_scan(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_prefix, void* scratch,
                          cudaStream_t st) {
-    launch_csr_gather(a, refs, n, out_prefix, nullptr, nullptr, nullptr, scratch, st);
+    if (n == 0) {
+        cuda_check(cudaMemsetAsync(out_prefix, 0, sizeof(uint64_t), st), "memset");
+        return;
+    }
+    launch_scan(a, refs, n, out_prefix, nullptr, nullptr, scratch, st);
 }
 
 void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t chunk_rows, IDtype out_idt,
