@@ -123,6 +123,17 @@ def dist_env():
     return rank, world, local
 
 
+def allreduce_max(x: float, dist) -> float:
+    """Max over ranks (device tensor under NCCL, host tensor under gloo)."""
+    if not dist:
+        return float(x)
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def ensure_store(wl, rank, world, dist):
     import paper_2604_01949_b200 as R
     base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
@@ -216,10 +227,7 @@ def run_ours(args, wl, rank, world, local, dist):
     per = [s.elapsed_time(e) for s, e in ev]
     total_ms = ev[0][0].elapsed_time(ev[-1][1])
     cells = sum(rows[Wm:])
-    t = torch.tensor([total_ms], device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = allreduce_max(total_ms, dist)
 
     # algorithmic bytes per launch: read row refs + indptr pair +
     # indices/values of every nnz; write the dense rows + gidx.
@@ -336,12 +344,10 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
     wall = time.perf_counter() - t0
     ms = s_ev.elapsed_time(e_ev)
     h2d = h2d_done[0] + it.counters().h2d_bytes - h2d0
-    t = torch.tensor([max(ms, wall * 1e3)], device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = allreduce_max(max(ms, wall * 1e3), dist)
     it.close()
     ds.close()
-    return {"value": world * cells / (float(t.item()) / 1e3), "unit": "cells/s",
+    return {"value": world * cells / (t_max / 1e3), "unit": "cells/s",
             "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": 8 * cells / K,
             "staging": "stream_pinned (records in pinned host RAM; blocks cudaMemcpyAsync'd per fetch)",
             "api": "paper_2604_01949_b200.BatchIterator.next -> rfl_loader_next",
@@ -408,8 +414,14 @@ def main():
     if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as dist
+        ndev = torch.cuda.device_count()
+        local = local % max(ndev, 1)  # more ranks than GPUs only in tests (gloo control plane)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("RIFFLE_BENCH_BACKEND", "nccl" if ndev >= world else "gloo")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group("gloo")
     if args.impl == "reference":
         res = run_reference(args, args.workload, rank, world)
     else:
