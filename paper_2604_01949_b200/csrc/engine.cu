@@ -317,14 +317,18 @@ void GpuLoader::stage_block(uint64_t id) {
     }
     lv.slot = ds_->acquire_slot(block_bytes_);
     lv.live_rows = e - s;
-    cuda_ok(cudaStreamWaitEvent(copy_, lv.slot.released, 0), "wait slot");
+    // the slot's previous kernel readers are done (skip the stream wait if already complete)
+    if (cudaEventQuery(lv.slot.released) != cudaSuccess)
+        cuda_ok(cudaStreamWaitEvent(copy_, lv.slot.released, 0), "wait slot");
     const HostStore& hs = ds_->host();
     if (ds_->staging() == kStreamPinned) {
-        // records of one block are contiguous in the pinned image except for alignment padding
+        // records of one block are contiguous in the pinned image except for alignment padding;
+        // the copies of all blocks fetched for this batch go out as one cudaMemcpyBatchAsync
         const uint64_t img0 = ds_->rec_off()[q0];
         const uint64_t img1 = ds_->rec_off()[q1] + ds_->rec_len()[q1];
-        cuda_ok(cudaMemcpyAsync(lv.slot.ptr, ds_->h_image() + img0, img1 - img0, cudaMemcpyHostToDevice, copy_),
-                "stage H2D");
+        batch_dst_.push_back(lv.slot.ptr);
+        batch_src_.push_back(const_cast<uint8_t*>(ds_->h_image() + img0));
+        batch_size_.push_back(img1 - img0);
         for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->rec_off()[q] - img0;
         ctr_.h2d_bytes += img1 - img0;
         for (uint64_t q = q0; q <= q1; ++q)  // one read op per shard run, as store.cpp:427-447 counts
@@ -408,7 +412,19 @@ bool GpuLoader::next(BatchOut& out) {
     }
     const bool resident = ds_->staging() == kResident;
     if (!resident) {
+        batch_dst_.clear();
+        batch_src_.clear();
+        batch_size_.clear();
         for (uint64_t id : consumed_) stage_block(id);
+        if (!batch_dst_.empty()) {
+            cudaMemcpyAttributes attr{};
+            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+            attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+            size_t attr_idx = 0, fail_idx = 0;
+            cuda_ok(cudaMemcpyBatchAsync(batch_dst_.data(), batch_src_.data(), batch_size_.data(), batch_dst_.size(),
+                                         &attr, &attr_idx, 1, &fail_idx, copy_),
+                    "cudaMemcpyBatchAsync");
+        }
         cuda_ok(cudaEventRecord(staged_, copy_), "event");
     }
     OutSlot& s = slots_[next_slot_++ % slots_.size()];

@@ -140,6 +140,8 @@ private:
         cudaEvent_t free_ev = nullptr;
     };
     std::vector<Pinned> pinned_;
+    std::vector<void*> batch_dst_, batch_src_;  // pinned-image staging copies of one next()
+    std::vector<size_t> batch_size_;
     uint64_t next_pinned_ = 0;
     Counters ctr_;
     bool done_ = false;
