@@ -337,8 +337,12 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s_ev.record(stream)
     cells = 0
+    trace = os.environ.get("RIFFLE_E2E_TRACE")
     for _ in range(K):
+        ts = time.perf_counter()
         cells += step()
+        if trace:
+            print(f"# e2e step host {1e3 * (time.perf_counter() - ts):.3f} ms", file=sys.stderr)
     e_ev.record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
