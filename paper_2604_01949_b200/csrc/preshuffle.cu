@@ -15,6 +15,8 @@
 #include <cstring>
 #include <memory>
 #include <numeric>
+#include <future>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 
@@ -31,7 +33,7 @@ namespace {
 
 constexpr uint64_t kAlign = 16;
 constexpr uint64_t kHuge = 1ull << 63;           // chunk_rows of the "absolute" arena view
-constexpr uint64_t kStageBytes = 128ull << 20;   // pinned bounce buffer per direction
+constexpr uint64_t kStageBytes = 512ull << 20;   // pinned staging window for round inputs
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 struct DevBuf {
@@ -140,7 +142,13 @@ private:
     cudaStream_t st_ = nullptr;
     cudaEvent_t e0_ = nullptr, e1_ = nullptr, e2_ = nullptr, e3_ = nullptr;
     DevBuf d_refs_, d_prefix_, d_scratch_, d_out_;
-    PinBuf h_stage_, h_refs_, h_prefix_, h_out_;
+    PinBuf h_stage_, h_refs_, h_prefix_, h_out_[2];
+    std::future<void> wjob_[2];  // background writes of h_out_[k]
+    uint64_t emits_ = 0;
+    void drain_writes() {
+        for (auto& f : wjob_)
+            if (f.valid()) f.get();
+    }
     ShuffleResult res_;
     std::vector<uint8_t> prov_rec_;
     // rank state
@@ -197,16 +205,12 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
         total = align_up(total + len[i], kAlign);
     }
     arena.ensure(std::max<uint64_t>(total, 16));
-    // coalesced reads of adjacent records of one shard (store.cpp:427-447) through a pinned bounce buffer
-    h_stage_.ensure(kStageBytes);
-    uint64_t fill = 0, fill_dst = 0;
-    auto flush = [&] {
-        if (!fill) return;
-        cuda_ok(cudaMemcpyAsync(arena.p + fill_dst, h_stage_.p, fill, cudaMemcpyHostToDevice, st_), "stage H2D");
-        cuda_ok(cudaStreamSynchronize(st_), "stage sync");
-        res_.h2d_bytes += fill;
-        fill = 0;
+    // coalesced reads of adjacent records of one shard (store.cpp:427-447)
+    struct Run {
+        size_t i, j;  // need[i..j)
+        uint64_t shard, file_off, bytes;
     };
+    std::vector<Run> runs;
     for (size_t i = 0; i < need.size();) {
         const HostStore& hs = *ms_[need[i].first].hs;
         const Manifest& m = hs.manifest();
@@ -221,34 +225,48 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
             run += s.len;
             ++j;
         }
-        // bytes [off[i], off[j-1]+len) of the arena, laid out with alignment gaps
-        const uint64_t span = off[j - 1] + len[j - 1] - off[i];
-        if (span > kStageBytes) {  // a huge run: read record by record
-            for (size_t k = i; k < j; ++k) {
-                flush();
-                h_stage_.ensure(len[k]);
-                hs.read_record(need[k].second, h_stage_.p, len[k]);
-                fill = len[k];
-                fill_dst = off[k];
-                flush();
-                h_stage_.ensure(kStageBytes);
-            }
-        } else {
-            // the bounce buffer mirrors arena bytes [fill_dst, fill_dst + fill); alignment gaps ride along
-            if (fill && off[i] + span - fill_dst > kStageBytes) flush();
-            if (!fill) fill_dst = off[i];
-            uint8_t* base = h_stage_.p + (off[i] - fill_dst);
-            hs.read_shard_bytes(shard, first.off, base, run, false);
-            // spread to aligned offsets (targets move forward only: back to front)
-            std::vector<uint64_t> rel(j - i, 0);
-            for (size_t k = i + 1; k < j; ++k) rel[k - i] = rel[k - i - 1] + len[k - 1];
-            for (size_t k = j - 1; k > i; --k) std::memmove(base + (off[k] - off[i]), base + rel[k - i], len[k]);
-            fill = off[j - 1] + len[j - 1] - fill_dst;
-        }
+        runs.push_back({i, j, shard, first.off, run});
         res_.input_bytes += run;
         i = j;
     }
-    flush();
+    // windows of the arena image (<= kStageBytes, or one oversized run) read by a
+    // thread pool into pinned memory — alignment gaps ride along — then one H2D
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (size_t r = 0; r < runs.size();) {
+        const uint64_t w0 = off[runs[r].i];
+        size_t r1 = r + 1;
+        while (r1 < runs.size() && off[runs[r1].j - 1] + len[runs[r1].j - 1] - w0 <= kStageBytes) ++r1;
+        const uint64_t w1 = off[runs[r1 - 1].j - 1] + len[runs[r1 - 1].j - 1];
+        h_stage_.ensure(w1 - w0);
+        std::vector<std::exception_ptr> errs(T);
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < T; ++t) {
+            pool.emplace_back([&, t] {
+                try {
+                    for (size_t x = r + t; x < r1; x += T) {
+                        const Run& ru = runs[x];
+                        const HostStore& hs = *ms_[need[ru.i].first].hs;
+                        uint8_t* base = h_stage_.p + (off[ru.i] - w0);
+                        hs.read_shard_bytes(ru.shard, ru.file_off, base, ru.bytes, false);
+                        // spread to aligned offsets (targets move forward only: back to front)
+                        std::vector<uint64_t> rel(ru.j - ru.i, 0);
+                        for (size_t k = ru.i + 1; k < ru.j; ++k) rel[k - ru.i] = rel[k - ru.i - 1] + len[k - 1];
+                        for (size_t k = ru.j - 1; k > ru.i; --k)
+                            std::memmove(base + (off[k] - off[ru.i]), base + rel[k - ru.i], len[k]);
+                    }
+                } catch (...) {
+                    errs[t] = std::current_exception();
+                }
+            });
+        }
+        for (auto& th : pool) th.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        cuda_ok(cudaMemcpyAsync(arena.p + w0, h_stage_.p, w1 - w0, cudaMemcpyHostToDevice, st_), "stage H2D");
+        cuda_ok(cudaStreamSynchronize(st_), "stage sync");
+        res_.h2d_bytes += w1 - w0;
+        r = r1;
+    }
     // refs per assembly row
     refs.clear();
     for (const auto& s : segs) {
@@ -311,8 +329,14 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
         launch_dense_gather(av, reinterpret_cast<RowRef*>(d_refs_.p), n, OutDtype::native, d_out_.p, nullptr, st_);
         cuda_ok(cudaEventRecord(e1_, st_), "event");
     }
-    h_out_.ensure(std::max<uint64_t>(total, 16));
-    if (total) cuda_ok(cudaMemcpyAsync(h_out_.p, d_out_.p, total, cudaMemcpyDeviceToHost, st_), "records D2H");
+    // double-buffered pinned output: the D2H below may only overwrite a buffer
+    // whose file writes have finished; writes run on one background thread, in
+    // order, overlapping the next round's staging and kernels
+    const int ob = static_cast<int>(emits_++ & 1u);
+    if (wjob_[ob].valid()) wjob_[ob].get();
+    PinBuf& hout = h_out_[ob];
+    hout.ensure(std::max<uint64_t>(total, 16));
+    if (total) cuda_ok(cudaMemcpyAsync(hout.p, d_out_.p, total, cudaMemcpyDeviceToHost, st_), "records D2H");
     cuda_ok(cudaStreamSynchronize(st_), "sync");
     float ms = 0.f, ms2 = 0.f;
     if (layout_ == Layout::csr) {  // kernel time only: scan (e0..e2) + pack (e3..e1)
@@ -323,21 +347,32 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
     }
     res_.gpu_ms += ms + ms2;
     res_.d2h_bytes += total;
-    uint64_t pos = 0;
-    for (uint64_t q = 0; q < nq; ++q) {
-        if (out_rows) out_->append_record_at((*out_rows)[q * cr] / cr, h_out_.p + pos, rec_len[q], rec_rows[q]);
-        else out_->append_record(h_out_.p + pos, rec_len[q], rec_rows[q]);
-        pos += rec_len[q];
-        // provenance: u32 dataset_id + u64 source_row, LE (preshuffle.cpp:27-91)
-        prov_rec_.resize(rec_rows[q] * 12);
-        for (uint64_t k = 0; k < rec_rows[q]; ++k) {
-            const auto& p = prov[q * cr + k];
-            wr32(prov_rec_.data() + 12 * k, p.first);
-            wr64(prov_rec_.data() + 12 * k + 4, p.second);
-        }
-        if (out_rows) prov_->append_record_at((*out_rows)[q * cr] / cr, prov_rec_.data(), prov_rec_.size(), rec_rows[q]);
-        else prov_->append_record(prov_rec_.data(), prov_rec_.size(), rec_rows[q]);
+    std::vector<uint64_t> chunk_id;
+    if (out_rows)
+        for (uint64_t q = 0; q < nq; ++q) chunk_id.push_back((*out_rows)[q * cr] / cr);
+    // provenance: u32 dataset_id + u64 source_row, LE (preshuffle.cpp:27-91)
+    std::vector<uint8_t> prov_bytes(n * 12);
+    for (uint64_t k = 0; k < n; ++k) {
+        wr32(prov_bytes.data() + 12 * k, prov[k].first);
+        wr64(prov_bytes.data() + 12 * k + 4, prov[k].second);
     }
+    const int prev = ob ^ 1;
+    if (wjob_[prev].valid()) wjob_[prev].get();  // keep file writes in order (and surface their errors)
+    wjob_[ob] = std::async(std::launch::async, [this, &hout, rec_len = std::move(rec_len), rec_rows = std::move(rec_rows),
+                                                chunk_id = std::move(chunk_id), prov_bytes = std::move(prov_bytes)] {
+        uint64_t pos = 0, ppos = 0;
+        for (size_t q = 0; q < rec_len.size(); ++q) {
+            if (!chunk_id.empty()) {
+                out_->append_record_at(chunk_id[q], hout.p + pos, rec_len[q], rec_rows[q]);
+                prov_->append_record_at(chunk_id[q], prov_bytes.data() + ppos, rec_rows[q] * 12, rec_rows[q]);
+            } else {
+                out_->append_record(hout.p + pos, rec_len[q], rec_rows[q]);
+                prov_->append_record(prov_bytes.data() + ppos, rec_rows[q] * 12, rec_rows[q]);
+            }
+            pos += rec_len[q];
+            ppos += rec_rows[q] * 12;
+        }
+    });
     res_.rows_written += n;
 }
 
@@ -499,6 +534,7 @@ ShuffleResult GpuShuffler::run() {
         if (!pending_.empty()) carry(pending_, 0, carry_[r % 2]);
         res_.rounds++;
     }
+    drain_writes();
     out_->finish();
     prov_->finish();
     write_text_file(a_.out_path + "/provenance/meta.json", meta_json(a_.seed, a_.c, a_.m));
@@ -643,6 +679,7 @@ void GpuShuffler::emit_round(uint64_t r, const uint64_t* recv_bytes) {
 }
 
 ShuffleResult GpuShuffler::finish() {
+    drain_writes();
     out_->finish(static_cast<int64_t>(total_));  // rank 0 writes the manifest (others: shards only)
     prov_->finish();
     if (a_.rank == 0) write_text_file(a_.out_path + "/provenance/meta.json", meta_json(a_.seed, a_.c, a_.m));
