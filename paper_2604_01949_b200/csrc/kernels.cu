@@ -506,13 +506,18 @@ __global__ void __launch_bounds__(THREADS, 1024 / THREADS)
                 if (c2 >= c0 && c2 - c0 < cols)
                     tile[c2 - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(d.val + k * sizeof(SrcT)), scale, norm);
             }
-            if (bulk) {
+            if (bulk == 1) {
                 fence_proxy_async_shared();  // make generic-proxy smem writes visible to the bulk engine
                 __syncthreads();
                 if (tid == 0) {
                     bulk_store(orow + c0, buf, bytes);
                     bulk_commit();
                 }
+            } else if (bulk == 2) {  // 16-B aligned rows: all threads stream the tile out with STG.128
+                __syncthreads();
+                const uint4* s4 = reinterpret_cast<const uint4*>(buf);
+                uint4* g4 = reinterpret_cast<uint4*>(orow + c0);
+                for (uint32_t i = tid; i < bytes / 16u; i += nthr) st_v4(g4 + i, s4[i]);
             } else {
                 __syncthreads();
                 for (uint32_t i = tid; i < cols; i += nthr) orow[c0 + i] = tile[i];
@@ -813,6 +818,7 @@ void set_smem(K kernel, size_t bytes) {
 // Densify variant (RFL_DENSIFY="v2:<threads>:<tile KB>" | "v3"), for A/B runs.
 struct DensifyCfg {  // default = best measured on B200 (scripts/ab_densify.sh, profiles/)
     int version = 2, threads = 256, tile_kb = 40;
+    char store = 't';  // 't': TMA bulk store of the tile, 'g': STG.128 from all threads
 };
 const DensifyCfg& densify_cfg() {
     static const DensifyCfg c = [] {
@@ -820,7 +826,9 @@ const DensifyCfg& densify_cfg() {
         const char* e = std::getenv("RFL_DENSIFY");
         if (e && e[0] == 'v') {
             int v = 2, t = 512, kb = 100;
-            const int got = std::sscanf(e, "v%d:%d:%d", &v, &t, &kb);
+            char st = 't';
+            const int got = std::sscanf(e, "v%d:%d:%d:%c", &v, &t, &kb, &st);
+            if (got >= 4 && (st == 't' || st == 'g')) d.store = st;
             d.version = v;
             if (got >= 2 && (t == 128 || t == 256 || t == 512)) d.threads = t;
             if (got >= 3 && kb >= 4 && kb <= 200) d.tile_kb = kb;
@@ -837,7 +845,8 @@ void densify_v2(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, 
     uint64_t tile_cols = av.n_var;
     if (av.n_var * esz > max_tile_bytes) tile_cols = (max_tile_bytes / esz) & ~15ull;
     const size_t smem = NBUF * ((tile_cols * esz + 127) & ~127ull);
-    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (bulk && densify_cfg().store == 'g') bulk = 2;
     auto kern = k_csr_densify<IdxT, SrcT, DstT, THREADS, U, NBUF>;
     set_smem(kern, smem);
     int per_sm = 0;
