@@ -421,7 +421,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // row's entries into it, then a single cp.async.bulk store writes the dense
 // tile — every output byte hits HBM exactly once, with no read-modify-write.
 template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int NBUF>
-__global__ void __launch_bounds__(THREADS, 1024 / THREADS)
+__global__ void __launch_bounds__(THREADS, (THREADS == 256 && U == 4) ? 5 : 1024 / THREADS)
     k_csr_densify(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -861,13 +861,10 @@ template <typename IdxT, typename SrcT, typename DstT>
 void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                uint64_t* out_gidx, cudaStream_t st) {
     const DensifyCfg& dc = densify_cfg();
-    if (dc.version == 2 || dc.version == 4) {  // v4 = v2 with a double-buffered tile
+    if (dc.version == 2 || dc.version == 5) {  // v5 = 256 threads, 1,024 entries in registers, 5 CTAs/SM
         const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
-        if (dc.version == 4) {
-            if (dc.threads == 512)
-                return densify_v2<IdxT, SrcT, DstT, 512, 4, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            return densify_v2<IdxT, SrcT, DstT, 256, 8, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
-        }
+        if (dc.version == 5)
+            return densify_v2<IdxT, SrcT, DstT, 256, 4, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
         if (dc.threads == 512)
             return densify_v2<IdxT, SrcT, DstT, 512, 4, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
         return densify_v2<IdxT, SrcT, DstT, 256, 8, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
