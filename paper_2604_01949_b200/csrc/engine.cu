@@ -78,6 +78,23 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     DeviceGuard g(device_);
     if (staging_ == kResident) load_records(true);
     else if (staging_ == kStreamPinned) load_records(false);
+    // CsrBlock::validate of every record, once, on the GPU (the reference
+    // re-validates on each decode, store.cpp:116-120); the pinned image is read
+    // in place over PCIe (mapped pinned memory)
+    if (m.layout == Layout::csr && staging_ != kStreamFile) {
+        const char* nv = std::getenv("RFL_NO_VALIDATE");
+        if (!(nv && nv[0] == '1')) {
+            try {
+                validate_records(staging_ == kResident ? d_arena_ : h_image_);
+            } catch (...) {  // the destructor does not run for a throwing constructor
+                if (d_arena_) cudaFree(d_arena_);
+                if (h_image_) cudaFreeHost(h_image_);
+                d_arena_ = nullptr;
+                h_image_ = nullptr;
+                throw;
+            }
+        }
+    }
     else if (m.layout == Layout::csr) {  // file streaming: only headers + indptrs now
         std::vector<uint8_t> buf;
         for (uint64_t q = 0; q < nch; ++q) {
@@ -173,6 +190,50 @@ void DStore::load_records(bool to_device) {
         }
         cudaStreamDestroy(st);
     }
+}
+
+void DStore::validate_records(const uint8_t* base) {
+    const Manifest& m = hs_->manifest();
+    const uint64_t nch = m.chunk_count();
+    if (nch == 0) return;
+    std::vector<uint64_t> first(nch);
+    for (uint64_t q = 0; q < nch; ++q) first[q] = q * m.chunk_rows;
+    uint64_t* d_tab = nullptr;
+    unsigned long long* d_bad = nullptr;
+    cuda_ok(cudaMalloc(&d_tab, 2 * nch * sizeof(uint64_t)), "cudaMalloc");
+    cuda_ok(cudaMalloc(&d_bad, sizeof(unsigned long long)), "cudaMalloc");
+    cuda_ok(cudaMemcpy(d_tab, rec_off_.data(), nch * 8, cudaMemcpyHostToDevice), "H2D");
+    cuda_ok(cudaMemcpy(d_tab + nch, first.data(), nch * 8, cudaMemcpyHostToDevice), "H2D");
+    cuda_ok(cudaMemset(d_bad, 0xff, sizeof(unsigned long long)), "memset");
+    launch_validate_csr(base, d_tab, d_tab + nch, nch, m.n_var, *m.index_dtype, d_bad, nullptr);
+    unsigned long long bad = 0;
+    cuda_ok(cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(d_tab);
+    cudaFree(d_bad);
+    if (bad == ~0ull) return;
+    // reproduce the reference's message for the first bad row (block.cpp:110-133)
+    const uint64_t q = bad / m.chunk_rows, r = bad % m.chunk_rows;
+    std::vector<uint8_t> rec(rec_len_[q]);
+    hs_->read_record(q, rec.data(), rec.size());
+    const bool u32 = *m.index_dtype == IDtype::u32;
+    const uint64_t is = u32 ? 4 : 8;
+    const uint32_t rows = rd32(rec.data());
+    auto at = [&](const uint8_t* p) { return u32 ? uint64_t{rd32(p)} : rd64(p); };
+    const uint8_t* ip = rec.data() + kCsrHeaderBytes;
+    const uint8_t* idx = ip + (rows + 1ull) * is;
+    const uint64_t lo = at(ip + r * is), hi = at(ip + (r + 1) * is);
+    std::string why = "column indices not strictly increasing in row " + std::to_string(r);
+    for (uint64_t k = lo; k < hi; ++k) {
+        const uint64_t c = at(idx + k * is);
+        if (c >= m.n_var) {
+            why = "column index " + std::to_string(c) + " >= n_var " + std::to_string(m.n_var) + " in row " +
+                  std::to_string(r);
+            break;
+        }
+        if (k > lo && c <= at(idx + (k - 1) * is)) break;
+    }
+    corrupt("chunk " + std::to_string(q) + " in shard " + std::to_string(q / m.chunks_per_shard) +
+            ": csr record invalid: csr block: " + why);
 }
 
 DStore::~DStore() {

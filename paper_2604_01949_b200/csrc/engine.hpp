@@ -58,6 +58,7 @@ public:
 
 private:
     void load_records(bool to_device);
+    void validate_records(const uint8_t* base);
     std::shared_ptr<HostStore> hs_;
     int device_;
     uint32_t staging_;

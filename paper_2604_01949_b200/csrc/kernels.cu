@@ -686,6 +686,37 @@ __global__ void __launch_bounds__(kSweepThreads, 6)
     }
 }
 
+// ============================================================ CSR validation ===
+// CsrBlock::validate (block.cpp:110-133) on device: every column index < n_var
+// and strictly increasing within its row.  One CTA per record, one warp per
+// row; the first violation (lowest global row) is kept with atomicMin and the
+// host re-checks that record to report the reference's exact message.
+template <typename IdxT>
+__global__ void __launch_bounds__(256)
+    k_validate_csr(const uint8_t* __restrict__ base, const uint64_t* __restrict__ rec_off,
+                   const uint64_t* __restrict__ first_row, uint64_t n_recs, uint64_t n_var,
+                   unsigned long long* __restrict__ bad_row) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (uint64_t q = blockIdx.x; q < n_recs; q += gridDim.x) {
+        const uint8_t* rec = base + rec_off[q];
+        const uint32_t rows = ld_u32(rec);
+        const uint64_t nnz = ld_u64_a4(rec + 4);
+        const uint8_t* ip = rec + kCsrHeaderBytes;
+        const uint8_t* idx = ip + (static_cast<uint64_t>(rows) + 1) * sizeof(IdxT);
+        for (uint32_t r = warp; r < rows; r += blockDim.x / 32) {
+            const uint64_t lo = ld_index<IdxT>(ip + r * sizeof(IdxT)), hi = ld_index<IdxT>(ip + (r + 1) * sizeof(IdxT));
+            bool bad = hi < lo || hi > nnz;
+            if (!bad) {
+                for (uint64_t k = lo + lane; k < hi; k += 32) {
+                    const uint64_t c = ld_index<IdxT>(idx + k * sizeof(IdxT));
+                    if (c >= n_var || (k > lo && c <= ld_index<IdxT>(idx + (k - 1) * sizeof(IdxT)))) bad = true;
+                }
+            }
+            if (__any_sync(kFull, bad) && lane == 0) atomicMin(bad_row, static_cast<unsigned long long>(first_row[q] + r));
+        }
+    }
+}
+
 // ============================================================ K4 dense gather ===
 constexpr int kDenseGatherThreads = 256;
 enum DenseMode { kRaw = 0, kU8ToBf16 = 1, kF32ToBf16 = 2 };
@@ -988,6 +1019,17 @@ void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_
     else
         k_csr_pack<uint64_t, uint64_t><<<grid, kPackThreads, 0, st>>>(d, vs, refs, n, chunk_rows, prefix, out);
     cuda_check(cudaGetLastError(), "k_csr_pack launch");
+}
+
+void launch_validate_csr(const uint8_t* base, const uint64_t* d_rec_off, const uint64_t* d_first_row, uint64_t n_recs,
+                         uint64_t n_var, IDtype idt, unsigned long long* d_bad_row, cudaStream_t st) {
+    if (n_recs == 0) return;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n_recs, 8ull * device_sm_count()));
+    if (idt == IDtype::u32)
+        k_validate_csr<uint32_t><<<grid, 256, 0, st>>>(base, d_rec_off, d_first_row, n_recs, n_var, d_bad_row);
+    else
+        k_validate_csr<uint64_t><<<grid, 256, 0, st>>>(base, d_rec_off, d_first_row, n_recs, n_var, d_bad_row);
+    cuda_check(cudaGetLastError(), "k_validate_csr launch");
 }
 
 size_t dense_out_elem_size(const ArenaView& a, OutDtype od) {

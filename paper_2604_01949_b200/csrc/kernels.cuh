@@ -51,6 +51,12 @@ void launch_csr_row_scan(const ArenaView& a, const RowRef* refs, uint64_t n_rows
 void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t chunk_rows, IDtype out_idt,
                      const uint64_t* prefix, uint8_t* out, cudaStream_t st);
 
+// CsrBlock::validate (block.cpp:110-133) over records at base + d_rec_off[q]
+// (first global row d_first_row[q]); *d_bad_row = min(first violating row)
+// (caller initialises it to ~0).
+void launch_validate_csr(const uint8_t* base, const uint64_t* d_rec_off, const uint64_t* d_first_row, uint64_t n_recs,
+                         uint64_t n_var, IDtype idt, unsigned long long* d_bad_row, cudaStream_t st);
+
 // K3
 void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
                         float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);

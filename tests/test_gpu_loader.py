@@ -211,6 +211,26 @@ def test_empty_rows_and_edges(tmp_path):
                     assert m.block.values.tobytes() == r["to_dense"].tobytes()
 
 
+@pytest.mark.parametrize("staging", ["resident", "stream_pinned"])
+@pytest.mark.parametrize("bad", ["range", "order"])
+def test_corrupt_indices_raise_like_reference(tmp_path, staging, bad):
+    """CsrBlock::validate (block.cpp:110-133) runs on the GPU: an out-of-range or
+    non-increasing column index raises CorruptStore with the reference's message."""
+    ip = np.array([0, 2, 5, 6, 8], np.uint64)
+    ix = np.array([0, 3, 1, 4, 7, 2, 5, 9], np.uint64)
+    if bad == "range":
+        ix[6] = 500
+    else:
+        ix[7] = 5  # row 3: 5, 5
+    dv = np.arange(8, dtype=np.float32)
+    write_csr_store(tmp_path / "s", ip, ix, dv, 10, 2, 2)
+    with pytest.raises(RuntimeError) as ref:
+        Ref.read_rows_csr(tmp_path / "s", [(0, 4)])
+    with pytest.raises(R.CorruptStore) as ours:
+        R.DeviceStore(tmp_path / "s", 0, staging)
+    assert str(ours.value) in str(ref.value)
+
+
 def test_epoch_completeness_and_sharding(tmp_path):
     """SPEC acceptance 4 on the device: every row exactly once per epoch, per rank
     disjoint, union complete (SURVEY §8e sharding)."""
