@@ -269,7 +269,7 @@ typedef struct rfl_shuffle_config {
     uint64_t out_chunks_per_shard;
     int32_t out_index_dtype;       /* -1 = first input's */
     int32_t device;
-    uint32_t join_outer;           /* DatasetCollection JoinMode; identity columns only */
+    uint32_t join_outer;           /* DatasetCollection JoinMode (collection.hpp:27): 1 outer (union), 0 inner (intersection) */
     uint32_t rank;                 /* multi-GPU: this rank writes shards s == rank (mod world) */
     uint32_t world;
     uint32_t reserved;

@@ -234,7 +234,7 @@ template <typename IdxT>
 __global__ void __launch_bounds__(kScanThreads)
     k_row_scan(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, uint64_t n_rows,
                uint64_t* __restrict__ out_prefix, RowJob* __restrict__ jobs, uint64_t* __restrict__ out_gidx,
-               unsigned long long* __restrict__ scratch) {
+               unsigned long long* __restrict__ scratch, const uint64_t* __restrict__ counts) {
     __shared__ uint64_t s_warp[kScanThreads / 32];
     __shared__ uint64_t s_tile, s_prefix;
     unsigned long long* counter = scratch;
@@ -246,7 +246,9 @@ __global__ void __launch_bounds__(kScanThreads)
     const uint64_t tile = s_tile;
     const uint64_t row = tile * kScanThreads + tid;
     uint64_t nnz = 0;
-    if (row < n_rows) {
+    if (row < n_rows && counts) {
+        nnz = counts[row];  // scan of given per-row counts (column reprojection)
+    } else if (row < n_rows) {
         const RowRef r = refs[row];
         const CsrRow cr = csr_row<IdxT>(a, r, vs);
         nnz = cr.nnz;
@@ -527,6 +529,110 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 256 && U == 4) ? 5 : 1024
     if (bulk && tid == 0) bulk_wait0();
 }
 
+// ============================================================ K3 densify v6 ===
+// Same smem-tile + TMA bulk store scheme as above, with two rows in flight per
+// CTA: while row i's tiles are zeroed/scattered/stored, row i+1's first U*THREADS
+// entries are already loading into a second register set, and the record
+// lookup (ref -> header -> indptr) runs two rows ahead.  Columns are kept as u32
+// (n_var < 2^32; indices were validated at store open), which keeps both
+// register sets spill-free.
+template <typename IdxT, typename SrcT>
+__device__ __forceinline__ void load_entries(const RowDesc& d, uint32_t tid, uint32_t nthr, uint32_t (&col)[8],
+                                             SrcT (&v)[8], int U) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if (u >= U) break;
+        const uint64_t k = tid + static_cast<uint64_t>(u) * nthr;
+        col[u] = ~0u;
+        if (k < d.nnz) {
+            const uint64_t c = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
+            col[u] = c < 0xFFFFFFFFull ? static_cast<uint32_t>(c) : ~0u;
+            v[u] = ld_value<SrcT>(d.val + k * sizeof(SrcT));
+        }
+    }
+}
+
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_csr_densify6(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
+                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ double s_red[THREADS / 32];
+    __shared__ RowDesc s_desc[3];  // rows i, i+1, i+2 of this CTA
+    const uint32_t tid = threadIdx.x;
+    constexpr uint32_t nthr = THREADS;
+    const uint64_t n_var = a.n_var;
+    const uint64_t g = gridDim.x;
+    if (tid == 0) {
+        if (blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
+        if (blockIdx.x + g < n_rows) s_desc[1] = describe_row<IdxT>(a, refs[blockIdx.x + g], sizeof(SrcT));
+    }
+    __syncthreads();
+    uint32_t colA[8], colB[8];
+    SrcT vA[8], vB[8];
+    if (blockIdx.x < n_rows) load_entries<IdxT, SrcT>(s_desc[0], tid, nthr, colA, vA, U);
+    uint32_t slot = 0;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += g, slot = slot == 2 ? 0 : slot + 1) {
+        const RowDesc d = s_desc[slot];
+        const uint32_t nslot = slot == 2 ? 0 : slot + 1, nnslot = nslot == 2 ? 0 : nslot + 1;
+        const bool has_next = row + g < n_rows;
+        if (has_next) load_entries<IdxT, SrcT>(s_desc[nslot], tid, nthr, colB, vB, U);  // row i+1 in flight
+        if (tid == 0) {
+            if (row + 2 * g < n_rows) s_desc[nnslot] = describe_row<IdxT>(a, refs[row + 2 * g], sizeof(SrcT));
+            if (out_gidx) out_gidx[row] = d.gidx;
+        }
+        float scale = 1.0f;
+        if (norm) {  // library size in fp64
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (colA[u] != ~0u) s += static_cast<double>(vA[u]);
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr)
+                s += static_cast<double>(ld_value<SrcT>(d.val + k * sizeof(SrcT)));
+            s = block_sum(s, s_red);
+            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
+        }
+        DstT* orow = out + row * n_var;
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+            const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
+            const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
+            DstT* tile = reinterpret_cast<DstT*>(smem);
+            if (bulk && tid == 0) bulk_wait_read0();
+            __syncthreads();
+            uint4* t4 = reinterpret_cast<uint4*>(smem);
+            for (uint32_t i = tid; i < bytes / 16u; i += nthr) t4[i] = make_uint4(0, 0, 0, 0);
+            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) smem[i] = 0;
+            __syncthreads();
+            const uint32_t c0u = static_cast<uint32_t>(c0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (colA[u] - c0u < cols) tile[colA[u] - c0u] = Conv<DstT, SrcT>::go(vA[u], scale, norm);
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr) {  // rows longer than U*THREADS
+                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
+                if (c2 >= c0 && c2 - c0 < cols)
+                    tile[c2 - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(d.val + k * sizeof(SrcT)), scale, norm);
+            }
+            if (bulk) {
+                fence_proxy_async_shared();
+                __syncthreads();
+                if (tid == 0) {
+                    bulk_store(orow + c0, smem, bytes);
+                    bulk_commit();
+                }
+            } else {
+                __syncthreads();
+                for (uint32_t i = tid; i < cols; i += nthr) orow[c0 + i] = tile[i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            colA[u] = colB[u];
+            vA[u] = vB[u];
+        }
+    }
+    if (bulk && tid == 0) bulk_wait0();
+}
+
 // ============================================================ K3 densify v3 ===
 // Warp-sweep densify.  Per row: one elected thread stages the row's indices
 // and values into shared memory with two 1-D TMA bulk copies (16-B aligned
@@ -683,6 +789,141 @@ __global__ void __launch_bounds__(kSweepThreads, 6)
             }
         }
         __syncthreads();  // staging buffers are re-filled for the next row
+    }
+}
+
+// ====================================================== column reprojection ===
+// remap_csr_row / scatter_dense_row (preshuffle.cpp:95-134): a member store's
+// rows re-expressed on the collection's unified var axis (col_map[c] = unified
+// column of member column c, or ~0 when an inner join dropped it).
+//
+// CSR is sort-free: per row (one CTA) the mapped columns are set in a
+// shared-memory bitmap over the unified axis; a block scan of the words'
+// popcounts then gives every surviving entry its output slot (= its rank among
+// the row's mapped columns), which is exactly the order std::sort of (u, k)
+// produces when the u are distinct.  Two member columns mapping to the same
+// unified column (duplicate var names) are detected (atomicOr saw the bit) and
+// reported; the reference then fails in StoreWriter::append -> validate.
+constexpr int kRemapThreads = 256;
+
+// a.n_var = the member's n_var (out-of-range indices of a corrupt record map nowhere)
+__device__ __forceinline__ uint32_t map_col(const uint32_t* __restrict__ colmap, uint64_t c, uint64_t in_nv) {
+    return c < in_nv ? __ldg(colmap + c) : ~0u;
+}
+
+template <typename InIdx>
+__global__ void __launch_bounds__(256)
+    k_remap_count(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, uint64_t n_rows,
+                  const uint32_t* __restrict__ colmap, uint64_t* __restrict__ counts) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nw = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t row = static_cast<uint64_t>(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); row < n_rows;
+         row += nw) {
+        const CsrRow src = csr_row<InIdx>(a, refs[row], vs);
+        uint32_t c = 0;
+        for (uint64_t k = lane; k < src.nnz; k += 32)
+            c += map_col(colmap, ld_index<InIdx>(src.idx + k * sizeof(InIdx)), a.n_var) != ~0u;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+        if (lane == 0) counts[row] = c;
+    }
+}
+
+__device__ __forceinline__ void copy_value(uint8_t* dst, const uint8_t* src, uint32_t vs) {
+    if (vs == 1) {
+        *dst = __ldg(src);
+    } else {  // 4-B aligned 4- or 8-byte values
+        for (uint32_t b = 0; b < vs; b += 4)
+            *reinterpret_cast<uint32_t*>(dst + b) = ld_u32(src + b);
+    }
+}
+
+template <typename InIdx, typename OutIdx>
+__global__ void __launch_bounds__(kRemapThreads)
+    k_csr_remap(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, uint64_t n_rows,
+                const uint32_t* __restrict__ colmap, uint32_t n_words, const uint64_t* __restrict__ P,
+                uint8_t* __restrict__ out, unsigned long long* __restrict__ dup_row, uint8_t* __restrict__ dup_flags) {
+    extern __shared__ __align__(16) uint32_t s_bm[];  // [n_words] bitmap, [n_words] word prefix
+    uint32_t* s_wp = s_bm + n_words;
+    __shared__ uint32_t s_part[kRemapThreads / 32];
+    constexpr uint64_t os = sizeof(OutIdx);
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint64_t pb = P[0], nnz_all = P[n_rows] - pb;
+    uint8_t* ip = out + kCsrHeaderBytes;
+    uint8_t* oidx = ip + os * (n_rows + 1);
+    uint8_t* oval = oidx + os * nnz_all;
+    if (blockIdx.x == 0 && tid == 0) {  // one record holding all rows (encode_csr_record layout)
+        st_any<uint32_t>(out, static_cast<uint32_t>(n_rows));
+        st_any<uint64_t>(out + 4, nnz_all);
+        st_any<OutIdx>(ip, OutIdx(0));
+    }
+    const uint32_t wpt = (n_words + kRemapThreads - 1) / kRemapThreads;  // words per thread in the scan
+    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+        for (uint32_t w = tid; w < n_words; w += kRemapThreads) s_bm[w] = 0;
+        __syncthreads();
+        const CsrRow src = csr_row<InIdx>(a, refs[row], vs);
+        bool dup = false;
+        for (uint64_t k = tid; k < src.nnz; k += kRemapThreads) {
+            const uint32_t u = map_col(colmap, ld_index<InIdx>(src.idx + k * sizeof(InIdx)), a.n_var);
+            if (u != ~0u) {
+                const uint32_t bit = 1u << (u & 31u);
+                dup |= (atomicOr(&s_bm[u >> 5], bit) & bit) != 0;
+            }
+        }
+        if (__syncthreads_or(dup) && tid == 0) {
+            atomicMin(dup_row, static_cast<unsigned long long>(row));
+            if (dup_flags) dup_flags[row] = 1;
+        }
+        // exclusive scan of the words' popcounts: thread t owns words [t*wpt, (t+1)*wpt)
+        const uint32_t w0 = tid * wpt, w1 = min(n_words, w0 + wpt);
+        uint32_t mine = 0;
+        for (uint32_t w = w0; w < w1; ++w) mine += __popc(s_bm[w]);
+        uint32_t incl = mine;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += v;
+        }
+        if (lane == 31) s_part[warp] = incl;
+        __syncthreads();
+        uint32_t run = incl - mine;
+        for (uint32_t w = 0; w < warp; ++w) run += s_part[w];
+        for (uint32_t w = w0; w < w1; ++w) {
+            s_wp[w] = run;
+            run += __popc(s_bm[w]);
+        }
+        __syncthreads();
+        const uint64_t base = P[row] - pb;
+        for (uint64_t k = tid; k < src.nnz; k += kRemapThreads) {
+            const uint32_t u = map_col(colmap, ld_index<InIdx>(src.idx + k * sizeof(InIdx)), a.n_var);
+            if (u == ~0u) continue;
+            const uint32_t pos = s_wp[u >> 5] + __popc(s_bm[u >> 5] & ((1u << (u & 31u)) - 1u));
+            st_any<OutIdx>(oidx + os * (base + pos), static_cast<OutIdx>(u));
+            copy_value(oval + vs * (base + pos), src.val + k * vs, vs);
+        }
+        if (tid == 0) st_any<OutIdx>(ip + os * (row + 1), static_cast<OutIdx>(P[row + 1] - pb));
+        __syncthreads();  // bitmap is re-zeroed for the next row
+    }
+}
+
+// Dense: out[row][u] = in[row][inv[u]] (inv[u] = last member column mapping to u,
+// as the reference's in-order memcpy leaves it), zero where no column maps.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_dense_remap(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
+                  const uint32_t* __restrict__ inv, uint64_t out_nv, T* __restrict__ out) {
+    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+        const RowRef r = refs[row];
+        const uint8_t* src = a.base + r.rec_off + (r.gidx % a.chunk_rows) * in_row_bytes;
+        T* dst = out + row * out_nv;
+        for (uint64_t u = threadIdx.x; u < out_nv; u += blockDim.x) {
+            const uint32_t c = __ldg(inv + u);
+            T v{};
+            if (c != ~0u) {
+                if constexpr (sizeof(T) == 1) v = __ldg(src + c);
+                else if constexpr (sizeof(T) == 4) v = ld_u32(src + 4ull * c);
+                else v = ld_u64_a4(src + 8ull * c);
+            }
+            dst[u] = v;
+        }
     }
 }
 
@@ -846,9 +1087,10 @@ void set_smem(K kernel, size_t bytes) {
                "cudaFuncSetAttribute");
 }
 
-// Densify variant (RFL_DENSIFY="v2:<threads>:<tile KB>" | "v3"), for A/B runs.
+// Densify variant (RFL_DENSIFY="v2:<threads>:<tile KB>[:g]" | "v3" | "v5" |
+// "v6:<threads>:<tile KB>:<U>:<CTAs/SM>"), for A/B runs.
 struct DensifyCfg {  // default = best measured on B200 (scripts/ab_densify.sh, profiles/)
-    int version = 2, threads = 256, tile_kb = 40;
+    int version = 2, threads = 256, tile_kb = 40, u = 8, minb = 4;
     char store = 't';  // 't': TMA bulk store of the tile, 'g': STG.128 from all threads
 };
 const DensifyCfg& densify_cfg() {
@@ -856,8 +1098,17 @@ const DensifyCfg& densify_cfg() {
         DensifyCfg d;
         const char* e = std::getenv("RFL_DENSIFY");
         if (e && e[0] == 'v') {
-            int v = 2, t = 512, kb = 100;
+            int v = 2, t = 512, kb = 100, u = 8, mb = 4;
             char st = 't';
+            if (std::sscanf(e, "v%d", &v) == 1 && v == 6) {
+                const int got = std::sscanf(e, "v6:%d:%d:%d:%d", &t, &kb, &u, &mb);
+                d.version = 6;
+                if (got >= 1) d.threads = t;
+                if (got >= 2 && kb >= 4 && kb <= 200) d.tile_kb = kb;
+                if (got >= 3) d.u = u;
+                if (got >= 4) d.minb = mb;
+                return d;
+            }
             const int got = std::sscanf(e, "v%d:%d:%d:%c", &v, &t, &kb, &st);
             if (got >= 4 && (st == 't' || st == 'g')) d.store = st;
             d.version = v;
@@ -867,6 +1118,24 @@ const DensifyCfg& densify_cfg() {
         return d;
     }();
     return c;
+}
+
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB>
+void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
+                uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes) {
+    const uint64_t esz = sizeof(DstT);
+    uint64_t tile_cols = av.n_var;
+    if (av.n_var * esz > max_tile_bytes) tile_cols = (max_tile_bytes / esz) & ~15ull;
+    const size_t smem = (tile_cols * esz + 127) & ~127ull;
+    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    auto kern = k_csr_densify6<IdxT, SrcT, DstT, THREADS, U, MINB>;
+    set_smem(kern, smem);
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem), "occupancy");
+    const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
+    kern<<<static_cast<unsigned>(grid), THREADS, smem, st>>>(dev_view(av), refs, n, static_cast<uint32_t>(tile_cols),
+                                                           norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
+    cuda_check(cudaGetLastError(), "k_csr_densify6 launch");
 }
 
 template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int NBUF>
@@ -892,6 +1161,20 @@ template <typename IdxT, typename SrcT, typename DstT>
 void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                uint64_t* out_gidx, cudaStream_t st) {
     const DensifyCfg& dc = densify_cfg();
+    if constexpr (sizeof(IdxT) == 4 && sizeof(SrcT) == 4) {
+        if (dc.version == 6) {  // A/B set: u32 indices, 4-byte values
+            const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
+            if (dc.threads == 512)
+                return densify_v6<IdxT, SrcT, DstT, 512, 4, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.threads == 128)
+                return densify_v6<IdxT, SrcT, DstT, 128, 8, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.u == 4)
+                return densify_v6<IdxT, SrcT, DstT, 256, 4, 5>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.minb == 3)
+                return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            return densify_v6<IdxT, SrcT, DstT, 256, 8, 4>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        }
+    }
     if (dc.version == 2 || dc.version == 5) {  // v5 = 256 threads, 1,024 entries in registers, 5 CTAs/SM
         const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
         if (dc.version == 5)
@@ -957,15 +1240,17 @@ uint64_t scan_status_bytes(uint64_t n_rows) {
     return ((1 + tiles) * sizeof(unsigned long long) + 15) & ~15ull;
 }
 void launch_scan(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_prefix, RowJob* jobs,
-                 uint64_t* out_gidx, void* scratch, cudaStream_t st) {
+                 uint64_t* out_gidx, void* scratch, cudaStream_t st, const uint64_t* counts = nullptr) {
     cuda_check(cudaMemsetAsync(scratch, 0, scan_status_bytes(n), st), "memset scratch");
     const unsigned tiles = static_cast<unsigned>((n + kScanThreads - 1) / kScanThreads);
     const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
     auto* sc = static_cast<unsigned long long*>(scratch);
     if (a.idt == IDtype::u32)
-        k_row_scan<uint32_t><<<tiles, kScanThreads, 0, st>>>(dev_view(a), vs, refs, n, out_prefix, jobs, out_gidx, sc);
+        k_row_scan<uint32_t><<<tiles, kScanThreads, 0, st>>>(dev_view(a), vs, refs, n, out_prefix, jobs, out_gidx, sc,
+                                                             counts);
     else
-        k_row_scan<uint64_t><<<tiles, kScanThreads, 0, st>>>(dev_view(a), vs, refs, n, out_prefix, jobs, out_gidx, sc);
+        k_row_scan<uint64_t><<<tiles, kScanThreads, 0, st>>>(dev_view(a), vs, refs, n, out_prefix, jobs, out_gidx, sc,
+                                                             counts);
     cuda_check(cudaGetLastError(), "k_row_scan launch");
 }
 }  // namespace
@@ -1019,6 +1304,65 @@ void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_
     else
         k_csr_pack<uint64_t, uint64_t><<<grid, kPackThreads, 0, st>>>(d, vs, refs, n, chunk_rows, prefix, out);
     cuda_check(cudaGetLastError(), "k_csr_pack launch");
+}
+
+void launch_remap_count(const ArenaView& a, const RowRef* refs, uint64_t n, const uint32_t* colmap, uint64_t* counts,
+                        cudaStream_t st) {
+    if (n == 0) return;
+    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 7) / 8, 16ull * device_sm_count()));
+    if (a.idt == IDtype::u32)
+        k_remap_count<uint32_t><<<grid, 256, 0, st>>>(dev_view(a), vs, refs, n, colmap, counts);
+    else
+        k_remap_count<uint64_t><<<grid, 256, 0, st>>>(dev_view(a), vs, refs, n, colmap, counts);
+    cuda_check(cudaGetLastError(), "k_remap_count launch");
+}
+
+void launch_count_scan(const uint64_t* counts, uint64_t n, uint64_t* out_prefix, void* scratch, cudaStream_t st) {
+    if (n == 0) {
+        cuda_check(cudaMemsetAsync(out_prefix, 0, sizeof(uint64_t), st), "memset");
+        return;
+    }
+    ArenaView none;
+    launch_scan(none, nullptr, n, out_prefix, nullptr, nullptr, scratch, st, counts);
+}
+
+size_t csr_remap_smem_bytes(uint64_t out_nv) { return 2 * 4 * ((out_nv + 31) / 32); }
+
+void launch_csr_remap(const ArenaView& a, const RowRef* refs, uint64_t n, const uint32_t* colmap, uint64_t out_nv,
+                      IDtype out_idt, const uint64_t* prefix, uint8_t* out, unsigned long long* dup_row,
+                      uint8_t* dup_flags, cudaStream_t st) {
+    if (n == 0) return;
+    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
+    const uint32_t n_words = static_cast<uint32_t>((out_nv + 31) / 32);
+    const size_t smem = csr_remap_smem_bytes(out_nv);
+    if (smem > 200 * 1024) invalid("column reprojection: unified n_var too large for the device bitmap");
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, 8ull * device_sm_count()));
+    const ArenaDev d = dev_view(a);
+    auto go = [&](auto kern) {
+        set_smem(kern, smem);
+        kern<<<grid, kRemapThreads, smem, st>>>(d, vs, refs, n, colmap, n_words, prefix, out, dup_row, dup_flags);
+    };
+    if (a.idt == IDtype::u32 && out_idt == IDtype::u32) go(k_csr_remap<uint32_t, uint32_t>);
+    else if (a.idt == IDtype::u32) go(k_csr_remap<uint32_t, uint64_t>);
+    else if (out_idt == IDtype::u32) go(k_csr_remap<uint64_t, uint32_t>);
+    else go(k_csr_remap<uint64_t, uint64_t>);
+    cuda_check(cudaGetLastError(), "k_csr_remap launch");
+}
+
+void launch_dense_remap(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t in_nv, const uint32_t* inv,
+                        uint64_t out_nv, void* out, cudaStream_t st) {
+    if (n == 0) return;
+    const uint64_t vs = value_size(a.vdt);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, 8ull * device_sm_count()));
+    const ArenaDev d = dev_view(a);
+    if (vs == 1)
+        k_dense_remap<uint8_t><<<grid, 256, 0, st>>>(d, in_nv, refs, n, inv, out_nv, static_cast<uint8_t*>(out));
+    else if (vs == 4)
+        k_dense_remap<uint32_t><<<grid, 256, 0, st>>>(d, 4 * in_nv, refs, n, inv, out_nv, static_cast<uint32_t*>(out));
+    else
+        k_dense_remap<uint64_t><<<grid, 256, 0, st>>>(d, 8 * in_nv, refs, n, inv, out_nv, static_cast<uint64_t*>(out));
+    cuda_check(cudaGetLastError(), "k_dense_remap launch");
 }
 
 void launch_validate_csr(const uint8_t* base, const uint64_t* d_rec_off, const uint64_t* d_first_row, uint64_t n_recs,

@@ -51,6 +51,23 @@ void launch_csr_row_scan(const ArenaView& a, const RowRef* refs, uint64_t n_rows
 void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t chunk_rows, IDtype out_idt,
                      const uint64_t* prefix, uint8_t* out, cudaStream_t st);
 
+// Column reprojection (remap_csr_row / scatter_dense_row, preshuffle.cpp:95-134).
+// counts[i] = number of row i's columns with colmap[c] != ~0u.
+void launch_remap_count(const ArenaView& a, const RowRef* refs, uint64_t n_rows, const uint32_t* colmap,
+                        uint64_t* counts, cudaStream_t st);
+// out_prefix = exclusive scan of counts (scratch: csr_gather_scratch_bytes(n)).
+void launch_count_scan(const uint64_t* counts, uint64_t n_rows, uint64_t* out_prefix, void* scratch, cudaStream_t st);
+size_t csr_remap_smem_bytes(uint64_t out_nv);
+// rows -> ONE encoded CSR record (all n rows) on the unified axis; *dup_row =
+// min row with two columns mapping to the same unified column (init ~0), and
+// dup_flags[row] = 1 for every such row (optional, init 0).
+void launch_csr_remap(const ArenaView& a, const RowRef* refs, uint64_t n_rows, const uint32_t* colmap, uint64_t out_nv,
+                      IDtype out_idt, const uint64_t* prefix, uint8_t* out, unsigned long long* dup_row,
+                      uint8_t* dup_flags, cudaStream_t st);
+// dense rows (in_nv columns) -> [n_rows, out_nv] rows; inv[u] = member column or ~0u (zero).
+void launch_dense_remap(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t in_nv, const uint32_t* inv,
+                        uint64_t out_nv, void* out, cudaStream_t st);
+
 // CsrBlock::validate (block.cpp:110-133) over records at base + d_rec_off[q]
 // (first global row d_first_row[q]); *d_bad_row = min(first violating row)
 // (caller initialises it to ~0).

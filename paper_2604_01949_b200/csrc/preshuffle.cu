@@ -69,17 +69,25 @@ struct PinBuf {
 struct Member {
     std::shared_ptr<HostStore> hs;
     uint64_t offset = 0;  // first global row
+    // DatasetCollection column map (collection.cpp:55-63): unified column of
+    // each member column, kMissing when an inner join dropped it
+    std::vector<uint64_t> col_map;
+    bool identity = true;
+    bool remap = false;               // rows go through the reprojection kernels
+    std::shared_ptr<DevBuf> d_map;    // CSR: u32 col_map; dense: u32 inverse map (unified -> member col)
 };
+
+constexpr uint64_t kMissing = ~0ull;  // kMissingColumn (collection.hpp:23)
 
 std::string meta_json(uint64_t seed, uint64_t c, uint64_t m) {  // ProvenanceWriter::finish (:32-47)
     return std::string("{\n  \"rng\": \"") + Rng::kName + "\",\n  \"seed\": " + std::to_string(seed) +
            ",\n  \"block_rows\": " + std::to_string(c) + ",\n  \"buffer_rows\": " + std::to_string(m) + "\n}\n";
 }
 
-// DatasetCollection::rebuild_unified (collection.cpp:28-82): unified axis and
-// per-member identity test.  Only identity members are supported on the GPU
-// path (column reprojection is SURVEY §8f "next").
-std::vector<std::string> unify(const std::vector<Member>& ms, bool outer) {
+// DatasetCollection::rebuild_unified (collection.cpp:28-82): the unified axis
+// (intersection in first-member order, or union in first-seen order), each
+// member's column map and identity flag.
+std::vector<std::string> unify(std::vector<Member>& ms, bool outer) {
     std::vector<std::string> uni;
     if (outer) {
         std::unordered_set<std::string> seen;
@@ -96,11 +104,18 @@ std::vector<std::string> unify(const std::vector<Member>& ms, bool outer) {
             if (all) uni.push_back(n);
         }
     }
-    for (size_t i = 0; i < ms.size(); ++i) {
-        const auto& v = ms[i].hs->manifest().var_names;
-        if (v.size() != uni.size() || !std::equal(v.begin(), v.end(), uni.begin()))
-            invalid("run_shuffle: member " + std::to_string(i) +
-                    " needs column reprojection, which the GPU path does not implement yet (identity columns only)");
+    std::unordered_map<std::string, uint64_t> index;
+    index.reserve(uni.size());
+    for (size_t i = 0; i < uni.size(); ++i) index.emplace(uni[i], i);
+    for (auto& m : ms) {
+        const auto& names = m.hs->manifest().var_names;
+        m.col_map.assign(names.size(), kMissing);
+        m.identity = names.size() == uni.size();
+        for (size_t c = 0; c < names.size(); ++c) {
+            const auto it = index.find(names[c]);
+            if (it != index.end()) m.col_map[c] = it->second;
+            if (m.col_map[c] != c) m.identity = false;
+        }
     }
     return uni;
 }
@@ -124,7 +139,10 @@ private:
     using Segs = std::vector<std::pair<uint32_t, std::pair<uint64_t, uint64_t>>>;
     void round_segments(uint64_t r, Segs& segs, std::vector<std::pair<uint32_t, uint64_t>>& prov,
                         std::vector<uint32_t>* src_rank);
-    void stage_round(const Segs& segs, DevBuf& arena, std::vector<RowRef>& refs);
+    void stage_round(const Segs& segs, DevBuf& arena, std::vector<RowRef>& refs, uint64_t r);
+    void reproject(uint32_t mi, std::vector<RowRef>& refs, const std::vector<uint64_t>& pos, DevBuf& out,
+                   std::vector<uint64_t>& bad);
+    void check_duplicates(uint64_t r, const std::vector<uint64_t>& bad_asm, uint64_t round_rows);
     void emit(const std::vector<RowRef>& refs, const std::vector<std::pair<uint32_t, uint64_t>>& prov, uint64_t n,
               const std::vector<uint64_t>* out_rows);
     void carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst);
@@ -153,6 +171,9 @@ private:
     std::vector<uint8_t> prov_rec_;
     // rank state
     DevBuf arena_[2], carry_[2], recv_, d_send_refs_, d_send_prefix_;
+    std::vector<std::shared_ptr<DevBuf>> remap_[2];  // per round parity, per member: reprojected rows
+    DevBuf d_counts_, d_flags_, d_dup_;
+    std::vector<uint64_t> bad_asm_;                  // assembly rows of the staged round with duplicate columns
     std::vector<RowRef> pending_;
     std::vector<std::pair<uint32_t, uint64_t>> pend_prov_;
     std::vector<uint64_t> pend_out_;                 // global output row of each pending row (multi-rank)
@@ -187,7 +208,7 @@ void GpuShuffler::upload_refs(const RowRef* refs, uint64_t n) {
 // `arena`; fill refs[a] for every assembly row a (absolute record address, row
 // within chunk).
 void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<uint64_t, uint64_t>>>& segs,
-                              DevBuf& arena, std::vector<RowRef>& refs) {
+                              DevBuf& arena, std::vector<RowRef>& refs, uint64_t r) {
     // chunks per member, in (member, chunk) order
     std::vector<std::pair<uint32_t, uint64_t>> need;
     for (const auto& s : segs) {
@@ -269,14 +290,86 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
     }
     // refs per assembly row
     refs.clear();
+    std::vector<std::vector<uint64_t>> remap_pos(ms_.size());
     for (const auto& s : segs) {
         const Manifest& m = ms_[s.first].hs->manifest();
-        for (uint64_t r = s.second.first; r < s.second.second; ++r) {
-            const uint64_t q = r / m.chunk_rows;
+        for (uint64_t row = s.second.first; row < s.second.second; ++row) {
+            const uint64_t q = row / m.chunk_rows;
             const size_t k = std::lower_bound(need.begin(), need.end(), std::make_pair(s.first, q)) - need.begin();
-            refs.push_back({reinterpret_cast<uint64_t>(arena.p) + off[k], r - q * m.chunk_rows});
+            if (ms_[s.first].remap) remap_pos[s.first].push_back(refs.size());
+            refs.push_back({reinterpret_cast<uint64_t>(arena.p) + off[k], row - q * m.chunk_rows});
         }
     }
+    // column reprojection of non-identity members (remap_csr_row / scatter_dense_row)
+    bad_asm_.clear();
+    auto& bufs = remap_[r % 2];
+    if (bufs.size() < ms_.size()) bufs.resize(ms_.size());
+    for (uint32_t mi = 0; mi < ms_.size(); ++mi) {
+        if (remap_pos[mi].empty()) continue;
+        if (!bufs[mi]) bufs[mi] = std::make_shared<DevBuf>();
+        reproject(mi, refs, remap_pos[mi], *bufs[mi], bad_asm_);
+    }
+}
+
+// Rows refs[pos[k]] of member mi -> one reprojected record (CSR) / block (dense)
+// in `out`; the refs are re-pointed at it.  Rows with two columns mapping to one
+// unified column are appended to `bad` (as positions into refs).
+void GpuShuffler::reproject(uint32_t mi, std::vector<RowRef>& refs, const std::vector<uint64_t>& pos, DevBuf& out,
+                            std::vector<uint64_t>& bad) {
+    const Manifest& mm = ms_[mi].hs->manifest();
+    const uint64_t n = pos.size();
+    std::vector<RowRef> sub(n);
+    for (uint64_t k = 0; k < n; ++k) sub[k] = refs[pos[k]];
+    upload_refs(sub.data(), n);
+    const RowRef* d_sub = reinterpret_cast<const RowRef*>(d_refs_.p);
+    const ArenaView av = absolute_view(layout_, vdt_, mm.index_dtype.value_or(IDtype::u32), mm.n_var);
+    const uint32_t* map = reinterpret_cast<const uint32_t*>(ms_[mi].d_map->p);
+    if (layout_ == Layout::csr) {
+        d_counts_.ensure(n * 8);
+        d_prefix_.ensure((n + 1) * 8);
+        d_scratch_.ensure(csr_gather_scratch_bytes(n));
+        d_dup_.ensure(8);
+        d_flags_.ensure(n);
+        cuda_ok(cudaMemsetAsync(d_dup_.p, 0xff, 8, st_), "memset");
+        cuda_ok(cudaMemsetAsync(d_flags_.p, 0, n, st_), "memset");
+        launch_remap_count(av, d_sub, n, map, reinterpret_cast<uint64_t*>(d_counts_.p), st_);
+        launch_count_scan(reinterpret_cast<uint64_t*>(d_counts_.p), n, reinterpret_cast<uint64_t*>(d_prefix_.p),
+                          d_scratch_.p, st_);
+        uint64_t nnz = 0;
+        cuda_ok(cudaMemcpyAsync(&nnz, d_prefix_.p + n * 8, 8, cudaMemcpyDeviceToHost, st_), "D2H");
+        cuda_ok(cudaStreamSynchronize(st_), "sync");
+        const uint64_t os = index_size(in_idt_), vs = value_size(vdt_);
+        out.ensure(kCsrHeaderBytes + os * (n + 1) + (os + vs) * nnz);
+        launch_csr_remap(av, d_sub, n, map, n_var_, in_idt_, reinterpret_cast<uint64_t*>(d_prefix_.p), out.p,
+                         reinterpret_cast<unsigned long long*>(d_dup_.p), d_flags_.p, st_);
+        uint64_t dup = 0;
+        cuda_ok(cudaMemcpyAsync(&dup, d_dup_.p, 8, cudaMemcpyDeviceToHost, st_), "D2H");
+        cuda_ok(cudaStreamSynchronize(st_), "sync");
+        if (dup != ~0ull) {
+            std::vector<uint8_t> flags(n);
+            cuda_ok(cudaMemcpy(flags.data(), d_flags_.p, n, cudaMemcpyDeviceToHost), "D2H");
+            for (uint64_t k = 0; k < n; ++k)
+                if (flags[k]) bad.push_back(pos[k]);
+        }
+    } else {
+        out.ensure(std::max<uint64_t>(n * row_bytes_, 16));
+        launch_dense_remap(av, d_sub, n, mm.n_var, map, n_var_, out.p, st_);
+        cuda_ok(cudaStreamSynchronize(st_), "sync");
+    }
+    for (uint64_t k = 0; k < n; ++k) refs[pos[k]] = {reinterpret_cast<uint64_t>(out.p), k};
+}
+
+// StoreWriter::append -> CsrBlock::validate (store.cpp:261-275, block.cpp:127-129)
+// rejects the first emitted c-row slice holding a row with a repeated column;
+// report the same row (its position within that slice).
+void GpuShuffler::check_duplicates(uint64_t r, const std::vector<uint64_t>& bad_asm, uint64_t round_rows) {
+    if (bad_asm.empty()) return;
+    const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
+    std::vector<uint8_t> is_bad(round_rows, 0);
+    for (uint64_t a : bad_asm) is_bad[a] = 1;
+    for (uint64_t k = 0; k < round_rows; ++k)
+        if (is_bad[perm[k]])
+            invalid("csr block: column indices not strictly increasing in row " + std::to_string(k % a_.c));
 }
 
 // Write refs[0..n) as output chunk records (+ provenance records).
@@ -431,8 +524,6 @@ void GpuShuffler::init() {
             if (man.value_dtype != f.value_dtype)
                 invalid(std::string("collection: store value_dtype ") + to_string(man.value_dtype) +
                         " does not match collection value_dtype " + to_string(f.value_dtype));
-            if (man.index_dtype != f.index_dtype)
-                invalid("run_shuffle: members with different index dtypes are not supported on the GPU path");
         }
         if (man.codec != Codec::none) invalid("GPU path requires codec none (deflate decode is out of scope)");
         total_ += man.n_obs;
@@ -452,6 +543,28 @@ void GpuShuffler::init() {
     om.layout = layout_;
     om.var_names = unify(ms_, a_.outer);
     om.n_var = om.var_names.size();
+    if (om.n_var >= 0xFFFFFFFFull) invalid("run_shuffle: unified n_var too large for the GPU column maps");
+    if (layout_ == Layout::csr && in_idt_ == IDtype::u32 && om.n_var > 0x100000000ull)
+        invalid("run_shuffle: unified n_var does not fit index_dtype u32");
+    for (auto& m : ms_) {
+        const Manifest& mm = m.hs->manifest();
+        m.remap = !m.identity || (layout_ == Layout::csr && mm.index_dtype.value_or(IDtype::u32) != in_idt_);
+        if (!m.remap) continue;
+        std::vector<uint32_t> map;
+        if (layout_ == Layout::csr) {  // member column -> unified column
+            map.resize(m.col_map.size());
+            for (size_t c = 0; c < map.size(); ++c)
+                map[c] = m.col_map[c] == kMissing ? ~0u : static_cast<uint32_t>(m.col_map[c]);
+        } else {  // unified column -> last member column mapping to it (scatter_dense_row order)
+            map.assign(om.n_var, ~0u);
+            for (size_t c = 0; c < m.col_map.size(); ++c)
+                if (m.col_map[c] != kMissing) map[m.col_map[c]] = static_cast<uint32_t>(c);
+        }
+        DeviceGuard g(a_.device);
+        m.d_map = std::make_shared<DevBuf>();
+        m.d_map->ensure(std::max<size_t>(map.size() * 4, 16));
+        if (!map.empty()) cuda_ok(cudaMemcpy(m.d_map->p, map.data(), map.size() * 4, cudaMemcpyHostToDevice), "map H2D");
+    }
     om.value_dtype = vdt_;
     if (layout_ == Layout::csr) om.index_dtype = out_idt_;
     om.chunk_rows = a_.out_chunk_rows;
@@ -520,7 +633,8 @@ ShuffleResult GpuShuffler::run() {
         round_segments(r, segs, asm_prov, nullptr);
         const uint64_t round_rows = asm_prov.size();
         res_.peak_resident_rows = std::max(res_.peak_resident_rows, round_rows + std::min(a_.c, round_rows));
-        stage_round(segs, arena_[r % 2], round_refs);
+        stage_round(segs, arena_[r % 2], round_refs, r);
+        check_duplicates(r, bad_asm_, round_rows);
         const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
         for (uint64_t k = 0; k < round_rows; ++k) {
             pending_.push_back(round_refs[perm[k]]);
@@ -555,10 +669,19 @@ void GpuShuffler::stage(uint64_t r, uint64_t* send_bytes) {
     const uint64_t round_rows = asm_prov.size();
     res_.peak_resident_rows = std::max(res_.peak_resident_rows, round_rows + std::min(a_.c, round_rows));
     std::vector<RowRef> my_refs;
-    stage_round(segs, arena_[r % 2], my_refs);  // refs of my assembly rows, in assembly order
+    stage_round(segs, arena_[r % 2], my_refs, r);  // refs of my assembly rows, in assembly order
     std::vector<int64_t> asm_to_mine(round_rows, -1);
+    std::vector<uint64_t> mine_to_asm;
     for (uint64_t a = 0, k = 0; a < round_rows; ++a)
-        if (asm_src[a] == a_.rank) asm_to_mine[a] = static_cast<int64_t>(k++);
+        if (asm_src[a] == a_.rank) {
+            asm_to_mine[a] = static_cast<int64_t>(k++);
+            mine_to_asm.push_back(a);
+        }
+    if (!bad_asm_.empty()) {
+        std::vector<uint64_t> bad;
+        for (uint64_t k : bad_asm_) bad.push_back(mine_to_asm[k]);
+        check_duplicates(r, bad, round_rows);
+    }
     const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
     const uint64_t shard_rows = a_.out_chunk_rows * a_.out_cps, first = round_first_out_[r];
     const uint32_t W = a_.world;

@@ -2,6 +2,7 @@
 sidecar are byte-identical to the reference run_shuffle (golden digests and
 live oracle/_ref runs), including multi-member collections, chunks that
 straddle rounds (out chunk_rows > m), index-dtype conversion and dense stores."""
+import json
 import os
 from pathlib import Path
 
@@ -115,3 +116,82 @@ def test_shuffle_errors(tmp_path):
         R.run_shuffle([], plan, tmp_path / "o1")
     with pytest.raises(R.InvalidArgument, match="layout"):
         R.run_shuffle([tmp_path / "a", tmp_path / "d"], R.plan_shuffle(200, 10, 30, 0), tmp_path / "o2")
+
+
+# ---- column reprojection (DatasetCollection joins, collection.cpp:28-82; preshuffle.cpp:95-134) ----
+def set_var_names(path, names):
+    """Give a store new var names (the shards do not depend on them)."""
+    p = Path(path) / "manifest.json"
+    m = json.loads(p.read_text())
+    assert len(names) == m["n_var"]
+    m["var_names"] = list(names)
+    p.write_text(json.dumps(m, indent=2))
+
+
+def _join_stores(tmp_path, layout, vdt, idt_a="u32", idt_b="u32"):
+    """a: names v0..v89; b: 70 columns = a permuted subset of a's names plus
+    names only b has; c: a's names in reverse order (same axis, not identity)."""
+    rng = np.random.default_rng(3)
+    a, b, c = tmp_path / "a", tmp_path / "b", tmp_path / "c"
+    R.synth_store(a, R.SynthConfig(700, 90, layout, vdt, idt_a, 0.15, 1, 32, 4))
+    R.synth_store(b, R.SynthConfig(333, 70, layout, vdt, idt_b, 0.3, 2, 50, 2))
+    R.synth_store(c, R.SynthConfig(210, 90, layout, vdt, idt_a, 0.1, 3, 40, 2))
+    shared = rng.permutation(90)[:55]
+    names_b = [f"v{j}" for j in shared] + [f"b_only{j}" for j in range(15)]
+    set_var_names(b, list(rng.permutation(names_b)))
+    set_var_names(c, [f"v{j}" for j in reversed(range(90))])
+    return [a, b, c], 1243
+
+
+@pytest.mark.parametrize("layout,vdt,join", [("csr", "f32", "outer"), ("csr", "f32", "inner"),
+                                             ("csr", "f64", "outer"), ("csr", "u8", "inner"),
+                                             ("dense", "f32", "outer"), ("dense", "u8", "inner"),
+                                             ("dense", "f64", "outer")])
+def test_live_reference_reprojection(tmp_path, layout, vdt, join):
+    """Members with differing var axes: GPU reprojection == reference run_shuffle, byte for byte."""
+    ins, total = _join_stores(tmp_path, layout, vdt)
+    Ref.run_shuffle(ins, tmp_path / "ref", 24, 300, 9, 100, 3, outer=(join == "outer"))
+    R.run_shuffle(ins, R.plan_shuffle(total, 24, 300, 9), tmp_path / "gpu", R.ShuffleOutputConfig(100, 3), join=join)
+    same_tree(tmp_path / "ref", tmp_path / "gpu")
+
+
+@pytest.mark.parametrize("out_idt", [None, "u64"])
+def test_live_reference_mixed_index_dtypes(tmp_path, out_idt):
+    """Members with u32 and u64 indices (identity and remapped axes) are converted on the GPU."""
+    ins, total = _join_stores(tmp_path, "csr", "f32", idt_a="u64", idt_b="u32")
+    Ref.run_shuffle(ins, tmp_path / "ref", 16, 256, 4, 64, 2, out_idt=out_idt)
+    R.run_shuffle(ins, R.plan_shuffle(total, 16, 256, 4), tmp_path / "gpu",
+                  R.ShuffleOutputConfig(64, 2, index_dtype=out_idt))
+    same_tree(tmp_path / "ref", tmp_path / "gpu")
+
+
+def test_reprojection_duplicate_names_error(tmp_path):
+    """Two member columns with one name map to one unified column: the reference
+    rejects the emitted block (CsrBlock::validate); so does the GPU path, same message."""
+    a, b = tmp_path / "a", tmp_path / "b"
+    R.synth_store(a, R.SynthConfig(200, 20, "csr", "f32", "u32", 0.5, 1, 20, 4))
+    R.synth_store(b, R.SynthConfig(100, 20, "csr", "f32", "u32", 0.5, 2, 20, 4))
+    set_var_names(b, [f"v{j}" for j in range(19)] + ["v3"])
+    with pytest.raises(Exception) as ref_err:
+        Ref.run_shuffle([a, b], tmp_path / "ref", 10, 100, 1, 50, 2)
+    with pytest.raises(R.InvalidArgument) as gpu_err:
+        R.run_shuffle([a, b], R.plan_shuffle(300, 10, 100, 1), tmp_path / "gpu", R.ShuffleOutputConfig(50, 2))
+    assert str(ref_err.value).split(": ", 1)[-1] in str(gpu_err.value)
+
+
+@pytest.mark.parametrize("world,layout,join", [(2, "csr", "outer"), (3, "dense", "inner")])
+def test_multi_rank_reprojection(tmp_path, world, layout, join):
+    from test_multirank import _run
+    ins, total = _join_stores(tmp_path, layout, "f32")
+    Ref.run_shuffle(ins, tmp_path / "ref", 32, 300, 5, 50, 2, outer=(join == "outer"))
+    rows = _run(world, _rank_shuffle_join, [str(p) for p in ins], total, str(tmp_path / "gpu"), 32, 300, 5, 50, 2,
+                join)
+    assert sum(rows) == total
+    same_tree(tmp_path / "ref", tmp_path / "gpu")
+
+
+def _rank_shuffle_join(rank, world, inputs, total, out, c, m, seed, ocr, ocps, join):
+    import paper_2604_01949_b200 as R
+    st = R.run_shuffle(inputs, R.plan_shuffle(total, c, m, seed), out, R.ShuffleOutputConfig(ocr, ocps),
+                       device=0, rank=rank, world=world, join=join)
+    return st.rows_written
