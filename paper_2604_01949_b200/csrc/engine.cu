@@ -22,41 +22,74 @@ constexpr uint64_t kAlign = 16;
 constexpr uint64_t kPad = 256;                  // arena tail padding for 16-B over-reads
 constexpr uint64_t kUploadRun = 64ull << 20;    // pinned bounce buffer for uploads
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+}  // namespace
 
-// decode_record's header checks (store.cpp:81-104), without decoding.
-void check_csr_header(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint64_t len) {
-    if (len < kCsrHeaderBytes) corrupt("chunk " + std::to_string(chunk) + ": csr record shorter than header");
-    const uint32_t rows = rd32(rec);
+// ====================================================== record checks ===
+namespace {
+std::string chunk_where(const Manifest& m, uint64_t q) {  // process_shard's wrapping (store.cpp:455-457)
+    return "chunk " + std::to_string(q) + " in shard " + std::to_string(q / m.chunks_per_shard) + ": ";
+}
+uint64_t rd_index(const Manifest& m, const uint8_t* p) { return *m.index_dtype == IDtype::u32 ? rd32(p) : rd64(p); }
+}  // namespace
+
+void full_check_csr_record(const Manifest& m, uint64_t q, const uint8_t* rec, uint64_t len) {
+    const std::string at = chunk_where(m, q);
+    if (len < kCsrHeaderBytes) corrupt(at + "csr record shorter than header");
+    const uint64_t rows = m.rows_in_chunk(q);
+    const uint32_t hdr_rows = rd32(rec);
     const uint64_t nnz = rd64(rec + 4);
-    if (rows != m.rows_in_chunk(chunk))
-        corrupt("chunk " + std::to_string(chunk) + ": csr record header declares " + std::to_string(rows) +
-                " rows, chunk has " + std::to_string(m.rows_in_chunk(chunk)));
+    if (hdr_rows != rows)
+        corrupt(at + "csr record header declares " + std::to_string(hdr_rows) + " rows, chunk has " +
+                std::to_string(rows));
     const uint64_t is = index_size(*m.index_dtype), vs = value_size(m.value_dtype);
-    const uint64_t expected = kCsrHeaderBytes + (rows + 1ull) * is + nnz * (is + vs);
+    const uint64_t expected = kCsrHeaderBytes + (rows + 1) * is + nnz * (is + vs);
     if (len != expected)
-        corrupt("chunk " + std::to_string(chunk) + ": csr record length " + std::to_string(len) + ", expected " +
-                std::to_string(expected));
+        corrupt(at + "csr record length " + std::to_string(len) + ", expected " + std::to_string(expected));
+    // CsrBlock::validate (block.cpp:110-133), in its order
+    const std::string inv = at + "csr record invalid: csr block: ";
+    const uint8_t* ip = rec + kCsrHeaderBytes;
+    const uint8_t* idx = ip + (rows + 1) * is;
+    if (rd_index(m, ip) != 0) corrupt(inv + "indptr[0] != 0");
+    for (uint64_t r = 0; r < rows; ++r) {
+        const uint64_t lo = rd_index(m, ip + r * is), hi = rd_index(m, ip + (r + 1) * is);
+        if (hi < lo) corrupt(inv + "indptr decreasing at row " + std::to_string(r));
+        for (uint64_t k = lo; k < hi && k < nnz; ++k) {
+            const uint64_t c = rd_index(m, idx + k * is);
+            if (c >= m.n_var)
+                corrupt(inv + "column index " + std::to_string(c) + " >= n_var " + std::to_string(m.n_var) +
+                        " in row " + std::to_string(r));
+            if (k > lo && c <= rd_index(m, idx + (k - 1) * is))
+                corrupt(inv + "column indices not strictly increasing in row " + std::to_string(r));
+        }
+        if (hi > nnz) corrupt(inv + "indices length does not match indptr");
+    }
+    if (rd_index(m, ip + rows * is) != nnz) corrupt(inv + "indices length does not match indptr");
 }
 
-void parse_row_nnz(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint32_t* out) {
-    const uint32_t rows = rd32(rec);
-    const uint8_t* ip = rec + kCsrHeaderBytes;
+void check_dense_record(const Manifest& m, uint64_t q, uint64_t len) {  // codec_decode none (codec.cpp:40-44)
+    const uint64_t expected = m.rows_in_chunk(q) * m.n_var * value_size(m.value_dtype);
+    if (len != expected)
+        corrupt(chunk_where(m, q) + "chunk record: expected " + std::to_string(expected) + " bytes, found " +
+                std::to_string(len));
+}
+
+bool check_csr_record(const Manifest& m, uint64_t q, const uint8_t* rec, uint64_t len, uint32_t* row_nnz) {
+    if (len < kCsrHeaderBytes) return false;
+    const uint64_t rows = m.rows_in_chunk(q);
     const uint64_t nnz = rd64(rec + 4);
-    uint64_t prev = 0;
-    for (uint32_t r = 0; r <= rows; ++r) {
-        const uint64_t v = *m.index_dtype == IDtype::u32 ? rd32(ip + 4ull * r) : rd64(ip + 8ull * r);
-        if (r == 0) {
-            if (v != 0) corrupt("chunk " + std::to_string(chunk) + ": csr record invalid: indptr[0] != 0");
-        } else {
-            if (v < prev) corrupt("chunk " + std::to_string(chunk) + ": csr record invalid: indptr decreasing at row " +
-                                  std::to_string(r - 1));
-            out[r - 1] = static_cast<uint32_t>(v - prev);
-        }
+    const uint64_t is = index_size(*m.index_dtype), vs = value_size(m.value_dtype);
+    if (rd32(rec) != rows || len != kCsrHeaderBytes + (rows + 1) * is + nnz * (is + vs)) return false;
+    const uint8_t* ip = rec + kCsrHeaderBytes;
+    uint64_t prev = rd_index(m, ip);
+    if (prev != 0) return false;
+    for (uint64_t r = 1; r <= rows; ++r) {
+        const uint64_t v = rd_index(m, ip + r * is);
+        if (v < prev) return false;
+        if (row_nnz) row_nnz[r - 1] = static_cast<uint32_t>(v - prev);
         prev = v;
     }
-    if (prev != nnz) corrupt("chunk " + std::to_string(chunk) + ": csr record invalid: indices length does not match indptr");
+    return prev == nnz;
 }
-}  // namespace
 
 // ================================================================= DStore ===
 DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
@@ -103,9 +136,12 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
             buf.resize(want);
             const Slot s = hs_->record_slot(q);
             hs_->read_shard_bytes(q / m.chunks_per_shard, s.off, buf.data(), want, false);
-            if (want < kCsrHeaderBytes) corrupt("chunk " + std::to_string(q) + ": csr record shorter than header");
-            check_csr_header(m, q, buf.data(), rec_len_[q]);
-            parse_row_nnz(m, q, buf.data(), row_nnz_.data() + q * m.chunk_rows);
+            if (want < kCsrHeaderBytes || !check_csr_record(m, q, buf.data(), rec_len_[q],
+                                                             row_nnz_.data() + q * m.chunk_rows)) {
+                buf.resize(rec_len_[q]);
+                hs_->read_record(q, buf.data(), buf.size());
+                full_check_csr_record(m, q, buf.data(), buf.size());
+            }
         }
     }
 }
@@ -162,10 +198,10 @@ void DStore::load_records(bool to_device) {
         for (uint64_t k = q; k < end; ++k) {
             const uint8_t* rec = buf + rel;
             if (m.layout == Layout::csr) {
-                check_csr_header(m, k, rec, rec_len_[k]);
-                parse_row_nnz(m, k, rec, row_nnz_.data() + k * m.chunk_rows);
-            } else if (rec_len_[k] != m.rows_in_chunk(k) * m.n_var * value_size(m.value_dtype)) {
-                corrupt("chunk " + std::to_string(k) + ": dense record length mismatch");
+                if (!check_csr_record(m, k, rec, rec_len_[k], row_nnz_.data() + k * m.chunk_rows))
+                    full_check_csr_record(m, k, rec, rec_len_[k]);
+            } else {
+                check_dense_record(m, k, rec_len_[k]);
             }
             if (to_device)
                 cuda_ok(cudaMemcpyAsync(d_arena_ + rec_off_[k], rec, rec_len_[k], cudaMemcpyHostToDevice, st),
@@ -211,29 +247,12 @@ void DStore::validate_records(const uint8_t* base) {
     cudaFree(d_tab);
     cudaFree(d_bad);
     if (bad == ~0ull) return;
-    // reproduce the reference's message for the first bad row (block.cpp:110-133)
-    const uint64_t q = bad / m.chunk_rows, r = bad % m.chunk_rows;
+    // reproduce the reference's message (first error of the record, in validate's order)
+    const uint64_t q = bad / m.chunk_rows;
     std::vector<uint8_t> rec(rec_len_[q]);
     hs_->read_record(q, rec.data(), rec.size());
-    const bool u32 = *m.index_dtype == IDtype::u32;
-    const uint64_t is = u32 ? 4 : 8;
-    const uint32_t rows = rd32(rec.data());
-    auto at = [&](const uint8_t* p) { return u32 ? uint64_t{rd32(p)} : rd64(p); };
-    const uint8_t* ip = rec.data() + kCsrHeaderBytes;
-    const uint8_t* idx = ip + (rows + 1ull) * is;
-    const uint64_t lo = at(ip + r * is), hi = at(ip + (r + 1) * is);
-    std::string why = "column indices not strictly increasing in row " + std::to_string(r);
-    for (uint64_t k = lo; k < hi; ++k) {
-        const uint64_t c = at(idx + k * is);
-        if (c >= m.n_var) {
-            why = "column index " + std::to_string(c) + " >= n_var " + std::to_string(m.n_var) + " in row " +
-                  std::to_string(r);
-            break;
-        }
-        if (k > lo && c <= at(idx + (k - 1) * is)) break;
-    }
-    corrupt("chunk " + std::to_string(q) + " in shard " + std::to_string(q / m.chunks_per_shard) +
-            ": csr record invalid: csr block: " + why);
+    full_check_csr_record(m, q, rec.data(), rec.size());
+    corrupt(chunk_where(m, q) + "csr record invalid");
 }
 
 DStore::~DStore() {
@@ -301,6 +320,120 @@ void DStore::release_slot(const SlotRef& s) {
     else if (s.released) cudaEventDestroy(s.released);  // from a retired pool geometry
 }
 
+// ============================================================ BlockReader ===
+BlockReader::BlockReader(std::shared_ptr<DStore> ds, std::vector<uint64_t> order, uint64_t f, uint32_t threads,
+                         uint32_t slots, bool direct)
+    : ds_(std::move(ds)), order_(std::move(order)), f_(f), direct_(direct) {
+    const Manifest& m = ds_->manifest();
+    // a block's records, each run read as its 4 KiB-aligned superset into a page-aligned position
+    const uint64_t bytes = ds_->max_block_bytes(f) + (f / m.chunk_rows + 2) * 3 * 4096;
+    slots_.resize(slots);
+    ev_.resize(slots);
+    released_.assign(slots, ~0ull);
+    DeviceGuard g(ds_->device());
+    for (uint32_t i = 0; i < slots; ++i) {
+        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&slots_[i].buf), bytes, cudaHostAllocDefault), "pinned");
+        cuda_ok(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
+    }
+    for (uint32_t t = 0; t < threads; ++t) th_.emplace_back([this] { worker(); });
+}
+
+BlockReader::~BlockReader() {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+    for (size_t i = 0; i < slots_.size(); ++i) {
+        cudaEventSynchronize(ev_[i]);
+        cudaEventDestroy(ev_[i]);
+        cudaFreeHost(slots_[i].buf);
+    }
+}
+
+void BlockReader::worker() {
+    cudaSetDevice(ds_->device());
+    const Manifest& m = ds_->manifest();
+    const HostStore& hs = ds_->host();
+    const uint64_t S = slots_.size();
+    for (;;) {
+        uint64_t k = 0;
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] {
+                return stop_ || (next_read_ < order_.size() &&
+                                 (next_read_ < S || released_[next_read_ % S] == next_read_ - S));
+            });
+            if (stop_) return;
+            k = next_read_++;
+        }
+        Block& b = slots_[k % S];
+        std::exception_ptr err;
+        try {
+            if (k >= S) cuda_ok(cudaEventSynchronize(ev_[k % S]), "pinned reuse");  // H2D of block k-S done
+            const uint64_t id = order_[k];
+            const uint64_t s = id * f_, e = std::min(m.n_obs, s + f_);
+            const uint64_t q0 = s / m.chunk_rows, q1 = (e - 1) / m.chunk_rows;
+            b.pos.assign(q1 - q0 + 1, 0);
+            uint64_t cursor = 0, q = q0;
+            while (q <= q1) {  // coalesced runs of adjacent records of one shard (store.cpp:427-447)
+                const uint64_t shard = q / m.chunks_per_shard;
+                const Slot first = hs.record_slot(q);
+                uint64_t end = q + 1, run = first.len;
+                while (end <= q1 && end / m.chunks_per_shard == shard) {
+                    const Slot sl = hs.record_slot(end);
+                    if (sl.off != first.off + run) break;
+                    run += sl.len;
+                    ++end;
+                }
+                const uint64_t lead = hs.read_shard_span(shard, first.off, b.buf + cursor, run, direct_);
+                for (uint64_t x = q, rel = 0; x < end; ++x) {
+                    b.pos[x - q0] = cursor + lead + rel;
+                    rel += ds_->rec_len()[x];
+                }
+                cursor += (HostStore::aligned_span(first.off, run) + 4095) & ~4095ull;
+                q = end;
+            }
+        } catch (...) {
+            err = std::current_exception();
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            b.err = err;
+            b.seq = k;
+        }
+        cv_.notify_all();
+    }
+}
+
+const BlockReader::Block& BlockReader::wait(uint64_t seq) {
+    if (seq >= order_.size()) invalid("block reader: read past the fetch order");
+    Block& b = slots_[seq % slots_.size()];
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return b.seq == seq; });
+    if (b.err) {  // BlockPrefetcher rethrows naming the block (loader.cpp:70-73)
+        try {
+            std::rethrow_exception(b.err);
+        } catch (const std::exception& e) {
+            const uint64_t s = order_[seq] * f_;
+            throw Error(kIo, "fetch block [" + std::to_string(s) + ", " +
+                                 std::to_string(std::min(ds_->manifest().n_obs, s + f_)) + "): " + e.what());
+        }
+    }
+    return b;
+}
+
+void BlockReader::release(uint64_t seq, cudaStream_t st) {
+    const uint64_t slot = seq % slots_.size();
+    cuda_ok(cudaEventRecord(ev_[slot], st), "event");
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        released_[slot] = seq;
+    }
+    cv_.notify_all();
+}
+
 // ============================================================== GpuLoader ===
 GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t epoch, const DeviceCfg& dev)
     : ds_(std::move(ds)), cfg_(cfg), epoch_(epoch), dev_(dev), replay_(ds_->manifest().n_obs, cfg, epoch) {
@@ -324,13 +457,9 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
         live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
         block_bytes_ = ds_->max_block_bytes(cfg_.f);
         if (ds_->staging() == kStreamFile) {
-            pinned_.resize(std::max<uint32_t>(4, cfg_.prefetch_depth + 2));
-            const uint64_t bytes = block_bytes_;
-            for (auto& p : pinned_) {
-                cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&p.ptr), bytes, cudaHostAllocDefault), "pinned");
-                p.bytes = bytes;
-                cuda_ok(cudaEventCreateWithFlags(&p.free_ev, cudaEventDisableTiming), "event");
-            }
+            const uint32_t threads = std::min<uint32_t>(16, std::max<uint32_t>(1, cfg_.prefetch_depth));
+            reader_ = std::make_unique<BlockReader>(ds_, replay_.plan(), cfg_.f, threads, 2 * threads + 2,
+                                                    cfg_.cache_bypass);
         }
     }
 }
@@ -355,10 +484,7 @@ GpuLoader::~GpuLoader() {
         cudaFreeHost(s.h_gidx);
         cudaEventDestroy(s.done);
     }
-    for (auto& p : pinned_) {
-        cudaFreeHost(p.ptr);
-        cudaEventDestroy(p.free_ev);
-    }
+    reader_.reset();
     cudaEventDestroy(staged_);
     cudaStreamDestroy(copy_);
     if (own_compute_) cudaStreamDestroy(compute_);
@@ -396,35 +522,21 @@ void GpuLoader::stage_block(uint64_t id) {
             if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard) ctr_.read_ops += 1;
         for (uint64_t q = q0; q <= q1; ++q) ctr_.bytes_read += ds_->rec_len()[q];
     } else {
-        Pinned& p = pinned_[next_pinned_++ % pinned_.size()];
-        cuda_ok(cudaEventSynchronize(p.free_ev), "pinned reuse");
-        // coalesced pread of adjacent records of one shard (store.cpp:427-447)
-        uint64_t q = q0;
-        while (q <= q1) {
-            const uint64_t shard = q / m.chunks_per_shard;
-            const Slot first = hs.record_slot(q);
-            uint64_t end = q + 1, run = first.len;
-            while (end <= q1 && end / m.chunks_per_shard == shard) {
-                const Slot sl = hs.record_slot(end);
-                if (sl.off != first.off + run) break;
-                run += sl.len;
-                ++end;
-            }
-            // read the run contiguously, then place records at their aligned slot offsets
-            uint8_t* dst = p.ptr + lv.chunk_off[q - q0];
-            hs.read_shard_bytes(shard, first.off, dst, run, cfg_.cache_bypass);
-            // spread to aligned offsets; targets only move forward, so go back to front
-            std::vector<uint64_t> rel(end - q);
-            for (uint64_t k = q + 1; k < end; ++k) rel[k - q] = rel[k - q - 1] + ds_->rec_len()[k - 1];
-            for (uint64_t k = end - 1; k > q; --k)
-                std::memmove(p.ptr + lv.chunk_off[k - q0], dst + rel[k - q], ds_->rec_len()[k]);
-            ctr_.read_ops += 1;
-            ctr_.bytes_read += run;
-            q = end;
+        // read ahead by the BlockReader; one copy per record into its aligned slot offset
+        // (copied and released right away: one next() may consume more blocks than there are buffers)
+        const uint64_t seq = read_seq_++;
+        const BlockReader::Block& bk = reader_->wait(seq);
+        for (uint64_t q = q0; q <= q1; ++q) {
+            cuda_ok(cudaMemcpyAsync(lv.slot.ptr + lv.chunk_off[q - q0], bk.buf + bk.pos[q - q0], ds_->rec_len()[q],
+                                    cudaMemcpyHostToDevice, copy_),
+                    "stage H2D");
+            if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard ||
+                hs.record_slot(q).off != hs.record_slot(q - 1).off + ds_->rec_len()[q - 1])
+                ctr_.read_ops += 1;  // one per coalesced run (store.cpp:427-447)
+            ctr_.bytes_read += ds_->rec_len()[q];
+            ctr_.h2d_bytes += ds_->rec_len()[q];
         }
-        cuda_ok(cudaMemcpyAsync(lv.slot.ptr, p.ptr, bytes, cudaMemcpyHostToDevice, copy_), "stage H2D");
-        cuda_ok(cudaEventRecord(p.free_ev, copy_), "event");
-        ctr_.h2d_bytes += bytes;
+        reader_->release(seq, copy_);
     }
     ctr_.chunks_decoded += q1 - q0 + 1;
 }

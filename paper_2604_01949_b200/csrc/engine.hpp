@@ -7,9 +7,12 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <exception>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "format.hpp"
@@ -27,6 +30,14 @@ struct DeviceGuard {  // sets and restores the current device
     explicit DeviceGuard(int dev);
     ~DeviceGuard();
 };
+
+// decode_record + CsrBlock::validate (store.cpp:81-122, block.cpp:110-133) on a
+// raw CSR record, throwing CorruptStore with the reference's text (wrapped as
+// process_shard does, store.cpp:455-457) for the first error in its order.
+void full_check_csr_record(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint64_t len);
+void check_dense_record(const Manifest& m, uint64_t chunk, uint64_t len);
+// Cheap pass (header, length, indptr; optionally per-row nnz); false -> run the full check.
+bool check_csr_record(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint64_t len, uint32_t* row_nnz);
 
 // A store image: every chunk record at a 16-B aligned offset of a virtual
 // image, either resident in HBM, in pinned host memory, or left in the files.
@@ -71,6 +82,41 @@ private:
     std::vector<void*> slabs_;
     std::vector<SlotRef> free_;
     uint64_t slot_bytes_ = 0;
+};
+
+// Read-ahead of a loader's fetch blocks for stream_file staging (the
+// reference's BlockPrefetcher, loader.cpp:21-90, with the order known up front
+// from the replay): I/O threads read blocks k+1 .. k+S-1 of this rank's fetch
+// order into pinned buffers (4 KiB-aligned O_DIRECT reads with cache_bypass)
+// while block k is staged; a buffer is refilled only after its H2D copy ended.
+class BlockReader {
+public:
+    struct Block {
+        uint64_t seq = ~0ull;       // position in the fetch order now held
+        uint8_t* buf = nullptr;     // pinned, page aligned
+        std::vector<uint64_t> pos;  // per record of the block: offset of its bytes in buf
+        std::exception_ptr err;
+    };
+    BlockReader(std::shared_ptr<DStore> ds, std::vector<uint64_t> order, uint64_t f, uint32_t threads, uint32_t slots,
+                bool direct);
+    ~BlockReader();
+    const Block& wait(uint64_t seq);              // the seq-th block of the order, once read
+    void release(uint64_t seq, cudaStream_t st);  // its buffer is free after st's work so far
+
+private:
+    void worker();
+    std::shared_ptr<DStore> ds_;
+    std::vector<uint64_t> order_;
+    uint64_t f_;
+    bool direct_;
+    std::vector<Block> slots_;
+    std::vector<cudaEvent_t> ev_;
+    std::vector<uint64_t> released_;  // per slot: last seq released (~0: none)
+    std::mutex mu_;
+    std::condition_variable cv_;
+    uint64_t next_read_ = 0;
+    bool stop_ = false;
+    std::vector<std::thread> th_;
 };
 
 struct DeviceCfg {
@@ -135,15 +181,10 @@ private:
     std::vector<uint64_t> gidx_, consumed_;
     std::vector<Live> live_;                 // indexed by block id (streaming)
     uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
-    struct Pinned {
-        uint8_t* ptr = nullptr;
-        uint64_t bytes = 0;
-        cudaEvent_t free_ev = nullptr;
-    };
-    std::vector<Pinned> pinned_;
-    std::vector<void*> batch_dst_, batch_src_;  // pinned-image staging copies of one next()
+    std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead
+    uint64_t read_seq_ = 0;
+    std::vector<void*> batch_dst_, batch_src_;  // stream_pinned copies of one next(), one cudaMemcpyBatchAsync
     std::vector<size_t> batch_size_;
-    uint64_t next_pinned_ = 0;
     Counters ctr_;
     bool done_ = false;
 };

@@ -400,6 +400,22 @@ void File::pread_exact(uint64_t off, void* dst, uint64_t n) const {
         done += static_cast<uint64_t>(r);
     }
 }
+void File::pread_upto(uint64_t off, void* dst, uint64_t n, uint64_t need) const {
+    uint64_t done = 0;
+    auto* d = static_cast<uint8_t*>(dst);
+    while (done < n) {
+        const ssize_t r = ::pread(fd_, d + done, n - done, static_cast<off_t>(off + done));
+        if (r < 0) {
+            if (errno == EINTR) continue;
+            ioerr(std::string("pread: ") + std::strerror(errno));
+        }
+        if (r == 0) {
+            if (done >= need) return;
+            ioerr("pread: unexpected end of file at offset " + std::to_string(off + done));
+        }
+        done += static_cast<uint64_t>(r);
+    }
+}
 void File::write_all(const void* src, uint64_t n) {
     uint64_t done = 0;
     const auto* s = static_cast<const uint8_t*>(src);
@@ -520,6 +536,19 @@ void HostStore::read_shard_bytes(uint64_t shard, uint64_t off, void* dst, uint64
         }
     }
     fd(shard, false).pread_exact(off, dst, n);
+}
+
+uint64_t HostStore::read_shard_span(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const {
+    if (direct) {
+        const File& d = fd(shard, true);
+        if (d.valid()) {
+            const uint64_t a0 = off & ~4095ull;
+            d.pread_upto(a0, dst, aligned_span(off, n), off + n - a0);
+            return off - a0;
+        }
+    }
+    fd(shard, false).pread_exact(off, dst, n);
+    return 0;
 }
 
 // ------------------------------------------------------------------ writer ----

@@ -86,6 +86,8 @@ public:
     bool valid() const { return fd_ >= 0; }
     uint64_t size() const;
     void pread_exact(uint64_t off, void* dst, uint64_t n) const;
+    // read up to n bytes at off; end of file is fine once `need` bytes are in
+    void pread_upto(uint64_t off, void* dst, uint64_t n, uint64_t need) const;
     void write_all(const void* src, uint64_t n);
 
 private:
@@ -118,6 +120,14 @@ public:
     void read_record(uint64_t chunk, void* dst, uint64_t cap) const;
     // pread an arbitrary byte range of one shard (coalesced runs, store.cpp:427-447)
     void read_shard_bytes(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const;
+    // Bytes [off, off+n) of a shard into a 4 KiB-aligned dst holding at least
+    // aligned_span(off, n) bytes; returns where they start inside dst.  With
+    // direct, an O_DIRECT read of the 4 KiB-aligned superset (no page-cache
+    // copy, file_io.hpp:50-56), else a plain pread to dst.
+    uint64_t read_shard_span(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const;
+    static uint64_t aligned_span(uint64_t off, uint64_t n) {
+        return ((off + n + 4095) & ~4095ull) - (off & ~4095ull);
+    }
 
 private:
     const File& fd(uint64_t shard, bool direct) const;

@@ -536,12 +536,11 @@ __global__ void __launch_bounds__(THREADS, (THREADS == 256 && U == 4) ? 5 : 1024
 // lookup (ref -> header -> indptr) runs two rows ahead.  Columns are kept as u32
 // (n_var < 2^32; indices were validated at store open), which keeps both
 // register sets spill-free.
-template <typename IdxT, typename SrcT>
-__device__ __forceinline__ void load_entries(const RowDesc& d, uint32_t tid, uint32_t nthr, uint32_t (&col)[8],
-                                             SrcT (&v)[8], int U) {
+template <typename IdxT, typename SrcT, int U>
+__device__ __forceinline__ void load_entries(const RowDesc& d, uint32_t tid, uint32_t nthr, uint32_t (&col)[U],
+                                             SrcT (&v)[U]) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        if (u >= U) break;
+    for (int u = 0; u < U; ++u) {
         const uint64_t k = tid + static_cast<uint64_t>(u) * nthr;
         col[u] = ~0u;
         if (k < d.nnz) {
@@ -568,15 +567,15 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (blockIdx.x + g < n_rows) s_desc[1] = describe_row<IdxT>(a, refs[blockIdx.x + g], sizeof(SrcT));
     }
     __syncthreads();
-    uint32_t colA[8], colB[8];
-    SrcT vA[8], vB[8];
-    if (blockIdx.x < n_rows) load_entries<IdxT, SrcT>(s_desc[0], tid, nthr, colA, vA, U);
+    uint32_t colA[U], colB[U];
+    SrcT vA[U], vB[U];
+    if (blockIdx.x < n_rows) load_entries<IdxT, SrcT, U>(s_desc[0], tid, nthr, colA, vA);
     uint32_t slot = 0;
     for (uint64_t row = blockIdx.x; row < n_rows; row += g, slot = slot == 2 ? 0 : slot + 1) {
         const RowDesc d = s_desc[slot];
         const uint32_t nslot = slot == 2 ? 0 : slot + 1, nnslot = nslot == 2 ? 0 : nslot + 1;
         const bool has_next = row + g < n_rows;
-        if (has_next) load_entries<IdxT, SrcT>(s_desc[nslot], tid, nthr, colB, vB, U);  // row i+1 in flight
+        if (has_next) load_entries<IdxT, SrcT, U>(s_desc[nslot], tid, nthr, colB, vB);  // row i+1 in flight
         if (tid == 0) {
             if (row + 2 * g < n_rows) s_desc[nnslot] = describe_row<IdxT>(a, refs[row + 2 * g], sizeof(SrcT));
             if (out_gidx) out_gidx[row] = d.gidx;
@@ -1170,6 +1169,12 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
                 return densify_v6<IdxT, SrcT, DstT, 128, 8, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
             if (dc.u == 4)
                 return densify_v6<IdxT, SrcT, DstT, 256, 4, 5>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.u == 12)
+                return densify_v6<IdxT, SrcT, DstT, 256, 12, 3>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.u == 16)
+                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.minb == 2)
+                return densify_v6<IdxT, SrcT, DstT, 256, 8, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
             if (dc.minb == 3)
                 return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, tb);
             return densify_v6<IdxT, SrcT, DstT, 256, 8, 4>(av, refs, n, norm, target, out, out_gidx, st, tb);

@@ -172,7 +172,8 @@ private:
     // rank state
     DevBuf arena_[2], carry_[2], recv_, d_send_refs_, d_send_prefix_;
     std::vector<std::shared_ptr<DevBuf>> remap_[2];  // per round parity, per member: reprojected rows
-    DevBuf d_counts_, d_flags_, d_dup_;
+    DevBuf d_counts_, d_flags_, d_dup_, d_vtab_;
+    bool validate_ = true;                           // RFL_NO_VALIDATE=1 skips the staged-record checks
     std::vector<uint64_t> bad_asm_;                  // assembly rows of the staged round with duplicate columns
     std::vector<RowRef> pending_;
     std::vector<std::pair<uint32_t, uint64_t>> pend_prov_;
@@ -267,8 +268,15 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
                     for (size_t x = r + t; x < r1; x += T) {
                         const Run& ru = runs[x];
                         const HostStore& hs = *ms_[need[ru.i].first].hs;
+                        const Manifest& hm = hs.manifest();
                         uint8_t* base = h_stage_.p + (off[ru.i] - w0);
                         hs.read_shard_bytes(ru.shard, ru.file_off, base, ru.bytes, false);
+                        // decode_record's checks (store.cpp:81-122) on each record of the run
+                        for (size_t k = ru.i, rel = 0; k < ru.j; rel += len[k], ++k) {
+                            if (hm.layout == Layout::dense) check_dense_record(hm, need[k].second, len[k]);
+                            else if (!check_csr_record(hm, need[k].second, base + rel, len[k], nullptr))
+                                full_check_csr_record(hm, need[k].second, base + rel, len[k]);
+                        }
                         // spread to aligned offsets (targets move forward only: back to front)
                         std::vector<uint64_t> rel(ru.j - ru.i, 0);
                         for (size_t k = ru.i + 1; k < ru.j; ++k) rel[k - ru.i] = rel[k - ru.i - 1] + len[k - 1];
@@ -287,6 +295,39 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
         cuda_ok(cudaStreamSynchronize(st_), "stage sync");
         res_.h2d_bytes += w1 - w0;
         r = r1;
+    }
+    // column checks of CsrBlock::validate for every staged record, on the GPU
+    if (layout_ == Layout::csr && validate_) {
+        std::vector<uint64_t> tab(2 * need.size());
+        for (size_t i = 0; i < need.size();) {
+            size_t j = i;
+            while (j < need.size() && need[j].first == need[i].first) ++j;  // one member
+            const Manifest& mm = ms_[need[i].first].hs->manifest();
+            const uint64_t n = j - i;
+            for (size_t k = 0; k < n; ++k) {
+                tab[k] = off[i + k];
+                tab[n + k] = need[i + k].second * mm.chunk_rows;
+            }
+            d_vtab_.ensure(16 * n);
+            d_dup_.ensure(8);
+            cuda_ok(cudaMemcpyAsync(d_vtab_.p, tab.data(), 16 * n, cudaMemcpyHostToDevice, st_), "H2D");
+            cuda_ok(cudaMemsetAsync(d_dup_.p, 0xff, 8, st_), "memset");
+            const uint64_t* t = reinterpret_cast<const uint64_t*>(d_vtab_.p);
+            launch_validate_csr(arena.p, t, t + n, n, mm.n_var, mm.index_dtype.value_or(IDtype::u32),
+                                reinterpret_cast<unsigned long long*>(d_dup_.p), st_);
+            uint64_t bad = 0;
+            cuda_ok(cudaMemcpyAsync(&bad, d_dup_.p, 8, cudaMemcpyDeviceToHost, st_), "D2H");
+            cuda_ok(cudaStreamSynchronize(st_), "sync");
+            if (bad != ~0ull) {
+                const uint64_t q = bad / mm.chunk_rows;
+                std::vector<uint8_t> rec(ms_[need[i].first].hs->record_slot(q).len);
+                ms_[need[i].first].hs->read_record(q, rec.data(), rec.size());
+                full_check_csr_record(mm, q, rec.data(), rec.size());
+                corrupt("chunk " + std::to_string(q) + " in shard " + std::to_string(q / mm.chunks_per_shard) +
+                        ": csr record invalid");
+            }
+            i = j;
+        }
     }
     // refs per assembly row
     refs.clear();
@@ -586,6 +627,7 @@ void GpuShuffler::init() {
         for (uint64_t id : plan_.rounds[r]) rows += plan_.block_end(id) - plan_.block_start(id);
         round_first_out_[r + 1] = round_first_out_[r] + rows;
     }
+    if (const char* nv = std::getenv("RFL_NO_VALIDATE")) validate_ = nv[0] != '1';
     DeviceGuard g(a_.device);
     cuda_ok(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
     cuda_ok(cudaEventCreate(&e0_), "event");

@@ -43,6 +43,9 @@ CASES = {  # store, kernel, rows per launch, out dtype, transform
 }
 
 
+GRAPH = False
+
+
 def peak():
     p = ROOT / "MEASURED_PEAKS.json"
     return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6650.0
@@ -135,16 +138,33 @@ def run_case(name, K, W, dstores):
     for i in range(W):
         L.check(launch(i))
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    for k in range(K):
-        ev[k][0].record(stream)
-        L.check(launch(W + k))
-        ev[k][1].record(stream)
-    torch.cuda.synchronize()
-    ms = [s.elapsed_time(e) for s, e in ev]
+    if GRAPH:  # the K launches captured once, replayed back to back: device time without host launch gaps
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+            cs = torch.cuda.current_stream()
+            sp.value = cs.cuda_stream
+            for k in range(K):
+                L.check(launch(W + k))
+        sp.value = stream.cuda_stream
+        g.replay()
+        torch.cuda.synchronize()
+        s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        g.replay()
+        e0.record(stream)
+        torch.cuda.synchronize()
+        ms = [s0.elapsed_time(e0) / K] * K
+    else:
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for k in range(K):
+            ev[k][0].record(stream)
+            L.check(launch(W + k))
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        ms = [s.elapsed_time(e) for s, e in ev]
     a = [alg(W + k) for k in range(K)]
     gbs = sum(a) / (sum(ms) / 1e3) / 1e9
-    return {"case": name, "kernel": kern, "rows_per_launch": rows, "ms_mean": float(np.mean(ms)),
+    return {"case": name, "kernel": kern, "graph": GRAPH, "rows_per_launch": rows, "ms_mean": float(np.mean(ms)),
             "ms_min": float(np.min(ms)), "alg_MB_per_launch": float(np.mean(a)) / 1e6, "GBps": gbs,
             "frac_of_measured_hbm": gbs / peak(), "rows_per_s": rows / (np.mean(ms) / 1e3)}
 
@@ -154,7 +174,10 @@ def main():
     ap.add_argument("--cases", default=",".join(CASES))
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--graph", action="store_true", help="replay the K launches as one CUDA graph")
     args = ap.parse_args()
+    global GRAPH
+    GRAPH = args.graph
     dstores = {}
     for c in args.cases.split(","):
         print(json.dumps(run_case(c, args.steps, args.warmup, dstores)), flush=True)

@@ -231,6 +231,32 @@ def test_corrupt_indices_raise_like_reference(tmp_path, staging, bad):
     assert str(ours.value) in str(ref.value)
 
 
+@pytest.mark.parametrize("staging", ["resident", "stream_pinned", "stream_file"])
+@pytest.mark.parametrize("bad", ["indptr", "tail", "header"])
+def test_corrupt_indptr_raise_like_reference(tmp_path, staging, bad):
+    """decode_record's header/length checks and validate's indptr checks
+    (store.cpp:81-122, block.cpp:110-133): same CorruptStore text as the reference,
+    prefixed "chunk q in shard s:" as process_shard wraps it (store.cpp:455-457)."""
+    ip = np.array([0, 2, 5, 6, 8], np.uint64)
+    ix = np.array([0, 3, 1, 4, 7, 2, 5, 9], np.uint64)
+    dv = np.arange(8, dtype=np.float32)
+    write_csr_store(tmp_path / "s", ip, ix, dv, 10, 2, 2)
+    shard = sorted((tmp_path / "s" / "shards").iterdir())[0]
+    raw = bytearray(shard.read_bytes())
+    if bad == "indptr":  # chunk 0 = rows 0,1: indptr [0, 2, 5] -> [0, 6, 5]
+        raw[12 + 4:12 + 8] = (6).to_bytes(4, "little")
+    elif bad == "tail":  # chunk 0 indptr[2] = 4 != nnz 5
+        raw[12 + 8:12 + 12] = (4).to_bytes(4, "little")
+    else:  # header declares 3 rows
+        raw[0:4] = (3).to_bytes(4, "little")
+    shard.write_bytes(bytes(raw))
+    with pytest.raises(RuntimeError) as ref:
+        Ref.read_rows_csr(tmp_path / "s", [(0, 4)])
+    with pytest.raises(R.CorruptStore) as ours:
+        R.DeviceStore(tmp_path / "s", 0, staging)
+    assert str(ours.value) in str(ref.value)
+
+
 def test_epoch_completeness_and_sharding(tmp_path):
     """SPEC acceptance 4 on the device: every row exactly once per epoch, per rank
     disjoint, union complete (SURVEY §8e sharding)."""
@@ -262,3 +288,40 @@ def test_dense_store_paths(golden, dstores):
         for staging in ("resident", "stream_file"):
             it = R.BatchIterator(dstores[(ld["store"], staging)], _cfg(ld), ld["epoch"])
             assert [hex(fnv([b.to_minibatch().block.values])) for b in it] == ld["dense_fnv"]
+
+
+@pytest.mark.parametrize("depth,bypass", [(0, False), (3, True), (16, True)])
+def test_stream_file_readahead(golden, golden_stores, depth, bypass):
+    """stream_file staging through the BlockReader (read-ahead threads, O_DIRECT
+    4 KiB-aligned spans with cache_bypass) == reference batches and counters."""
+    for ld in golden["loaders"]:
+        st = golden["stores"][ld["store"]]
+        it = R.BatchIterator(golden_stores[ld["store"]], _cfg(ld, prefetch_depth=depth, cache_bypass=bypass),
+                             ld["epoch"], output="dense", staging="stream_file")
+        got = [b.to_minibatch() for b in it]
+        assert [m.global_indices.tolist() for m in got] == ld["gidx"]
+        assert [hex(fnv([m.block.values])) for m in got] == ld["dense_fnv"], ld["store"]
+        c = it.counters()
+        assert c.read_ops == ld["read_ops"] and c.chunks_decoded == ld["chunks_decoded"]
+        assert st["n_var"] == got[0].block.values.shape[1]
+
+
+def test_stream_file_abandoned_and_io_error(tmp_path):
+    """An iterator dropped mid-epoch stops its reader threads; a shard that
+    vanishes under a running iterator surfaces as IoError naming the block
+    (BlockPrefetcher::fetch_guarded, loader.cpp:61-74)."""
+    R.synth_store(tmp_path / "s", R.SynthConfig(4000, 50, "csr", density=0.2, seed=2, chunk_rows=64,
+                                                chunks_per_shard=4))
+    it = R.BatchIterator(tmp_path / "s", R.LoaderConfig(64, 512, 256, 1, prefetch_depth=8), 0, output="csr",
+                         staging="stream_file")
+    it.next()
+    it.close()
+    it = R.BatchIterator(tmp_path / "s", R.LoaderConfig(64, 512, 256, 1, prefetch_depth=1), 0, output="csr",
+                         staging="stream_file")
+    it.next()
+    for p in (tmp_path / "s" / "shards").iterdir():
+        p.write_bytes(b"")  # truncate every shard: reads ahead of the consumer fail
+    with pytest.raises(R.IoError, match=r"fetch block \[\d+, \d+\)"):
+        for _ in range(100):
+            if it.next() is None:
+                break

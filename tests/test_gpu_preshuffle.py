@@ -195,3 +195,38 @@ def _rank_shuffle_join(rank, world, inputs, total, out, c, m, seed, ocr, ocps, j
     st = R.run_shuffle(inputs, R.plan_shuffle(total, c, m, seed), out, R.ShuffleOutputConfig(ocr, ocps),
                        device=0, rank=rank, world=world, join=join)
     return st.rows_written
+
+
+@pytest.mark.parametrize("bad", ["order", "range", "indptr", "header"])
+def test_shuffle_corrupt_input_raises_like_reference(tmp_path, bad):
+    """Staged input records get decode_record's checks (host: header, length,
+    indptr) and CsrBlock::validate's column checks (GPU): same CorruptStore text."""
+    from oracle.oracle import write_csr_store
+    rng = np.random.default_rng(1)
+    rows, nv = 40, 30
+    ip = np.zeros(rows + 1, np.uint64)
+    cols = []
+    for r in range(rows):
+        c = np.sort(rng.choice(nv, 5, replace=False))
+        cols.append(c)
+        ip[r + 1] = ip[r] + 5
+    ix = np.concatenate(cols).astype(np.uint64)
+    dv = rng.random(len(ix)).astype(np.float32)
+    if bad == "order":
+        ix[5 * 17 + 2] = ix[5 * 17 + 1]
+    elif bad == "range":
+        ix[5 * 23] = 99
+    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 8, 2)
+    if bad in ("indptr", "header"):
+        shard = sorted((tmp_path / "s" / "shards").iterdir())[1]
+        raw = bytearray(shard.read_bytes())
+        if bad == "indptr":
+            raw[12 + 12:12 + 16] = (7).to_bytes(4, "little")
+        else:
+            raw[4:12] = (41).to_bytes(8, "little")
+        shard.write_bytes(bytes(raw))
+    with pytest.raises(RuntimeError) as ref:
+        Ref.run_shuffle([tmp_path / "s"], tmp_path / "ref", 4, 16, 3, 10, 2)
+    with pytest.raises(R.CorruptStore) as ours:
+        R.run_shuffle([tmp_path / "s"], R.plan_shuffle(rows, 4, 16, 3), tmp_path / "gpu", R.ShuffleOutputConfig(10, 2))
+    assert str(ours.value) in str(ref.value)
