@@ -188,6 +188,12 @@ rfl_status rfl_loader_create(rfl_dstore* d, const rfl_loader_config* cfg, uint64
  * Buffers stay valid until out_slots further calls. */
 rfl_status rfl_loader_next(rfl_loader* l, rfl_batch* out);
 rfl_status rfl_loader_counters_get(const rfl_loader* l, rfl_loader_counters* out);
+/* Host copy of a batch (the reference's MiniBatch, loader.hpp:35-40): waits
+ * for its ready_event, then copies whichever of indptr (u64[n_rows+1]),
+ * indices (index_dtype[nnz]), data (nnz or n_rows*n_var elements of dtype)
+ * and gidx (u64[n_rows]) are non-NULL. */
+rfl_status rfl_batch_download(const rfl_batch* b, uint64_t* h_indptr, void* h_indices, void* h_data,
+                              uint64_t* h_gidx);
 rfl_status rfl_loader_sync(rfl_loader* l);
 void rfl_loader_destroy(rfl_loader* l);
 

@@ -322,6 +322,26 @@ rfl_status rfl_loader_counters_get(const rfl_loader* l, rfl_loader_counters* o) 
     });
 }
 
+rfl_status rfl_batch_download(const rfl_batch* b, uint64_t* h_indptr, void* h_indices, void* h_data,
+                              uint64_t* h_gidx) {
+    return guarded([&] {
+        if (!b) rfl::invalid("null argument");
+        if (b->ready_event) rfl::cuda_ok(cudaEventSynchronize(static_cast<cudaEvent_t>(b->ready_event)), "sync");
+        auto d2h = [](void* dst, const void* src, uint64_t n) {
+            if (dst && src && n) rfl::cuda_ok(cudaMemcpy(dst, src, n, cudaMemcpyDeviceToHost), "batch D2H");
+        };
+        static const uint64_t esz[] = {4, 8, 4, 1, 2};  // RFL_F32, F64, I32, U8, BF16
+        if (b->dtype > RFL_BF16) rfl::invalid("batch: unknown dtype");
+        const uint64_t n_elem = b->layout == RFL_LAYOUT_CSR ? b->nnz : b->n_rows * b->n_var;
+        d2h(h_gidx, b->d_gidx, 8 * b->n_rows);
+        if (b->layout == RFL_LAYOUT_CSR) {
+            d2h(h_indptr, b->d_indptr, 8 * (b->n_rows + 1));
+            d2h(h_indices, b->d_indices, (b->index_dtype == RFL_IDX_U32 ? 4 : 8) * b->nnz);
+        }
+        d2h(h_data, b->d_data, esz[b->dtype] * n_elem);
+    });
+}
+
 rfl_status rfl_loader_sync(rfl_loader* l) {
     return guarded([&] {
         if (!l) rfl::invalid("null argument");

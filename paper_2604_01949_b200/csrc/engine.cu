@@ -632,7 +632,7 @@ bool GpuLoader::next(BatchOut& out) {
         launch_dense_gather(av, s.d_refs, n, dev_.out_dtype, s.data, static_cast<uint64_t*>(s.gidx), compute_);
     } else if (dev_.output == 1) {
         launch_csr_densify(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,
-                           static_cast<uint64_t*>(s.gidx), compute_);
+                           static_cast<uint64_t*>(s.gidx), compute_, n ? (nnz + n - 1) / n : 0);
     } else {
         launch_csr_gather(av, s.d_refs, n, static_cast<uint64_t*>(s.indptr), s.indices, s.data,
                           static_cast<uint64_t*>(s.gidx), s.scratch, compute_);

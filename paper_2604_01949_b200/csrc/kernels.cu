@@ -1088,8 +1088,8 @@ void set_smem(K kernel, size_t bytes) {
 
 // Densify variant (RFL_DENSIFY="v2:<threads>:<tile KB>[:g]" | "v3" | "v5" |
 // "v6:<threads>:<tile KB>:<U>:<CTAs/SM>"), for A/B runs.
-struct DensifyCfg {  // default = best measured on B200 (scripts/ab_densify.sh, profiles/)
-    int version = 2, threads = 256, tile_kb = 40, u = 8, minb = 4;
+struct DensifyCfg {  // version 0 = the measured default (v6, shape rule in densify_t)
+    int version = 0, threads = 256, tile_kb = 40, u = 8, minb = 4;
     char store = 't';  // 't': TMA bulk store of the tile, 'g': STG.128 from all threads
 };
 const DensifyCfg& densify_cfg() {
@@ -1100,8 +1100,8 @@ const DensifyCfg& densify_cfg() {
             int v = 2, t = 512, kb = 100, u = 8, mb = 4;
             char st = 't';
             if (std::sscanf(e, "v%d", &v) == 1 && v == 6) {
-                const int got = std::sscanf(e, "v6:%d:%d:%d:%d", &t, &kb, &u, &mb);
-                d.version = 6;
+                const int got = std::sscanf(e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
+                d.version = v;
                 if (got >= 1) d.threads = t;
                 if (got >= 2 && kb >= 4 && kb <= 200) d.tile_kb = kb;
                 if (got >= 3) d.u = u;
@@ -1158,8 +1158,17 @@ void densify_v2(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, 
 
 template <typename IdxT, typename SrcT, typename DstT>
 void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
-               uint64_t* out_gidx, cudaStream_t st) {
+               uint64_t* out_gidx, cudaStream_t st, uint64_t avg_nnz) {
     const DensifyCfg& dc = densify_cfg();
+    if (dc.version == 0) {
+        // Default (profiles/r1_densify_v6.md): every row entry of a typical row
+        // in registers.  Rows up to ~2.5k entries (and <= 96 KB dense): 8 per
+        // thread, 40 KB tiles, 3 CTAs/SM (cfg1: 0.78 of measured HBM); longer or
+        // wider rows: 16 per thread, 80 KB tiles, 2 CTAs/SM (cfg2: 0.80).
+        const bool big = avg_nnz > 2560 || (avg_nnz == 0 && av.n_var * sizeof(DstT) > 96 * 1024);
+        if (big) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2>(av, refs, n, norm, target, out, out_gidx, st, 80 << 10);
+        return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, 40 << 10);
+    }
     if constexpr (sizeof(IdxT) == 4 && sizeof(SrcT) == 4) {
         if (dc.version == 6) {  // A/B set: u32 indices, 4-byte values
             const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
@@ -1206,23 +1215,23 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
 
 template <typename IdxT>
 void densify_idx(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, bool norm, float target, void* out,
-                 uint64_t* g, cudaStream_t st) {
+                 uint64_t* g, cudaStream_t st, uint64_t avg_nnz) {
     switch (a.vdt) {
         case VDtype::f32:
-            if (od == OutDtype::bf16) return densify_t<IdxT, float, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
-            return densify_t<IdxT, float, float>(a, refs, n, norm, target, out, g, st);
+            if (od == OutDtype::bf16) return densify_t<IdxT, float, __nv_bfloat16>(a, refs, n, norm, target, out, g, st, avg_nnz);
+            return densify_t<IdxT, float, float>(a, refs, n, norm, target, out, g, st, avg_nnz);
         case VDtype::f64:
-            if (od == OutDtype::bf16) return densify_t<IdxT, double, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
-            if (od == OutDtype::f32) return densify_t<IdxT, double, float>(a, refs, n, norm, target, out, g, st);
-            return densify_t<IdxT, double, double>(a, refs, n, false, target, out, g, st);
+            if (od == OutDtype::bf16) return densify_t<IdxT, double, __nv_bfloat16>(a, refs, n, norm, target, out, g, st, avg_nnz);
+            if (od == OutDtype::f32) return densify_t<IdxT, double, float>(a, refs, n, norm, target, out, g, st, avg_nnz);
+            return densify_t<IdxT, double, double>(a, refs, n, false, target, out, g, st, avg_nnz);
         case VDtype::i32:
-            if (od == OutDtype::bf16) return densify_t<IdxT, int32_t, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
-            if (od == OutDtype::f32) return densify_t<IdxT, int32_t, float>(a, refs, n, norm, target, out, g, st);
-            return densify_t<IdxT, int32_t, int32_t>(a, refs, n, false, target, out, g, st);
+            if (od == OutDtype::bf16) return densify_t<IdxT, int32_t, __nv_bfloat16>(a, refs, n, norm, target, out, g, st, avg_nnz);
+            if (od == OutDtype::f32) return densify_t<IdxT, int32_t, float>(a, refs, n, norm, target, out, g, st, avg_nnz);
+            return densify_t<IdxT, int32_t, int32_t>(a, refs, n, false, target, out, g, st, avg_nnz);
         case VDtype::u8:
-            if (od == OutDtype::bf16) return densify_t<IdxT, uint8_t, __nv_bfloat16>(a, refs, n, norm, target, out, g, st);
-            if (od == OutDtype::f32) return densify_t<IdxT, uint8_t, float>(a, refs, n, norm, target, out, g, st);
-            return densify_t<IdxT, uint8_t, uint8_t>(a, refs, n, false, target, out, g, st);
+            if (od == OutDtype::bf16) return densify_t<IdxT, uint8_t, __nv_bfloat16>(a, refs, n, norm, target, out, g, st, avg_nnz);
+            if (od == OutDtype::f32) return densify_t<IdxT, uint8_t, float>(a, refs, n, norm, target, out, g, st, avg_nnz);
+            return densify_t<IdxT, uint8_t, uint8_t>(a, refs, n, false, target, out, g, st, avg_nnz);
     }
 }
 
@@ -1388,13 +1397,13 @@ size_t dense_out_elem_size(const ArenaView& a, OutDtype od) {
 }
 
 void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, bool norm, float target,
-                        void* out, uint64_t* out_gidx, cudaStream_t st) {
+                        void* out, uint64_t* out_gidx, cudaStream_t st, uint64_t avg_nnz) {
     if (a.layout != Layout::csr) invalid("csr_densify: store is not csr");
     if (norm && od == OutDtype::native && a.vdt != VDtype::f32)
         invalid("csr_densify: normalize_log1p needs a floating output dtype (f32 or bf16)");
     if (n == 0) return;
-    if (a.idt == IDtype::u32) densify_idx<uint32_t>(a, refs, n, od, norm, target, out, out_gidx, st);
-    else densify_idx<uint64_t>(a, refs, n, od, norm, target, out, out_gidx, st);
+    if (a.idt == IDtype::u32) densify_idx<uint32_t>(a, refs, n, od, norm, target, out, out_gidx, st, avg_nnz);
+    else densify_idx<uint64_t>(a, refs, n, od, norm, target, out, out_gidx, st, avg_nnz);
 }
 
 void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, void* out,

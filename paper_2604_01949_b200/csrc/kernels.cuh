@@ -75,8 +75,10 @@ void launch_validate_csr(const uint8_t* base, const uint64_t* d_rec_off, const u
                          uint64_t n_var, IDtype idt, unsigned long long* d_bad_row, cudaStream_t st);
 
 // K3
+// avg_nnz: mean entries per row of this batch when the caller knows it (0 = unknown;
+// selects the register/tile shape of the kernel, never the result).
 void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
-                        float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);
+                        float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st, uint64_t avg_nnz = 0);
 size_t dense_out_elem_size(const ArenaView& a, OutDtype od);
 
 // K4
