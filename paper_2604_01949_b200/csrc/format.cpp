@@ -9,7 +9,9 @@
 #include <cerrno>
 #include <cinttypes>
 #include <cstdio>
+#include <exception>
 #include <filesystem>
+#include <thread>
 
 namespace rfl {
 
@@ -416,6 +418,18 @@ void File::pread_upto(uint64_t off, void* dst, uint64_t n, uint64_t need) const 
         done += static_cast<uint64_t>(r);
     }
 }
+void File::pwrite_all(uint64_t off, const void* src, uint64_t n) const {
+    uint64_t done = 0;
+    const auto* s = static_cast<const uint8_t*>(src);
+    while (done < n) {
+        const ssize_t r = ::pwrite(fd_, s + done, n - done, static_cast<off_t>(off + done));
+        if (r < 0) {
+            if (errno == EINTR) continue;
+            ioerr(std::string("pwrite: ") + std::strerror(errno));
+        }
+        done += static_cast<uint64_t>(r);
+    }
+}
 void File::write_all(const void* src, uint64_t n) {
     uint64_t done = 0;
     const auto* s = static_cast<const uint8_t*>(src);
@@ -579,14 +593,42 @@ void RecordWriter::close_shard() {
         wr64(tail.data() + i * 16 + 8, slots_[i].len);
     }
     std::memcpy(tail.data() + slots_.size() * 16, kMagic, 8);
-    shard_->write_all(tail.data(), tail.size());
+    shard_->pwrite_all(shard_bytes_, tail.data(), tail.size());
     shard_.reset();
+}
+
+// Large records (the pre-shuffle's output chunks are tens of MB) go out as
+// parallel pwrites of disjoint slices: one writer thread is page-cache-copy bound.
+static void write_parallel(const File& f, uint64_t off, const uint8_t* src, uint64_t n) {
+    constexpr uint64_t kSlice = 8ull << 20;
+    const unsigned T = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    if (n < 2 * kSlice || T == 1) {
+        f.pwrite_all(off, src, n);
+        return;
+    }
+    const uint64_t slices = (n + kSlice - 1) / kSlice;
+    std::vector<std::exception_ptr> errs(T);
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            try {
+                for (uint64_t k = t; k < slices; k += T) {
+                    const uint64_t a = k * kSlice, b = std::min(n, a + kSlice);
+                    f.pwrite_all(off + a, src + a, b - a);
+                }
+            } catch (...) {
+                errs[t] = std::current_exception();
+            }
+        });
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
 }
 
 void RecordWriter::append_record(const void* rec, uint64_t nbytes, uint64_t rows) {
     if (finished_) invalid("store writer: append after finish");
     if (!shard_) open_shard();
-    shard_->write_all(rec, nbytes);
+    write_parallel(*shard_, shard_bytes_, static_cast<const uint8_t*>(rec), nbytes);
     slots_[chunk_in_shard_] = {shard_bytes_, nbytes};
     shard_bytes_ += nbytes;
     ++chunk_in_shard_;

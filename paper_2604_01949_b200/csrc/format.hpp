@@ -89,6 +89,7 @@ public:
     // read up to n bytes at off; end of file is fine once `need` bytes are in
     void pread_upto(uint64_t off, void* dst, uint64_t n, uint64_t need) const;
     void write_all(const void* src, uint64_t n);
+    void pwrite_all(uint64_t off, const void* src, uint64_t n) const;
 
 private:
     int fd_ = -1;
