@@ -625,30 +625,42 @@ static void write_parallel(const File& f, uint64_t off, const uint8_t* src, uint
         if (e) std::rethrow_exception(e);
 }
 
-void RecordWriter::append_record(const void* rec, uint64_t nbytes, uint64_t rows) {
+RecordWriter::Placement RecordWriter::reserve_record(uint64_t nbytes, uint64_t rows, int64_t chunk) {
     if (finished_) invalid("store writer: append after finish");
+    if (chunk >= 0) {
+        const uint64_t c = static_cast<uint64_t>(chunk);
+        const uint64_t shard = c / man_.chunks_per_shard;
+        if (shard_ && shard != (chunks_emitted_ - 1) / man_.chunks_per_shard) close_shard();
+        if (!shard_) {
+            if (c % man_.chunks_per_shard != 0) invalid("store writer: owned shard must be filled from slot 0");
+            chunks_emitted_ = c;
+            open_shard();
+        } else if (c != chunks_emitted_) {
+            invalid("store writer: non-consecutive chunk " + std::to_string(c));
+        }
+    }
+    // a full shard is closed lazily, once the records written into it are complete
+    if (shard_ && chunk_in_shard_ >= man_.chunks_per_shard) close_shard();
     if (!shard_) open_shard();
-    write_parallel(*shard_, shard_bytes_, static_cast<const uint8_t*>(rec), nbytes);
+    const Placement p{&*shard_, shard_bytes_};
     slots_[chunk_in_shard_] = {shard_bytes_, nbytes};
     shard_bytes_ += nbytes;
     ++chunk_in_shard_;
     ++chunks_emitted_;
     man_.n_obs += rows;
-    if (chunk_in_shard_ >= man_.chunks_per_shard) close_shard();
+    return p;
+}
+
+void RecordWriter::write_part(const Placement& p, uint64_t rel, const void* src, uint64_t n) {
+    write_parallel(*p.file, p.off + rel, static_cast<const uint8_t*>(src), n);
+}
+
+void RecordWriter::append_record(const void* rec, uint64_t nbytes, uint64_t rows) {
+    write_part(reserve_record(nbytes, rows), 0, rec, nbytes);
 }
 
 void RecordWriter::append_record_at(uint64_t chunk, const void* rec, uint64_t nbytes, uint64_t rows) {
-    if (finished_) invalid("store writer: append after finish");
-    const uint64_t shard = chunk / man_.chunks_per_shard;
-    if (shard_ && shard != (chunks_emitted_ - 1) / man_.chunks_per_shard) close_shard();
-    if (!shard_) {
-        if (chunk % man_.chunks_per_shard != 0) invalid("store writer: owned shard must be filled from slot 0");
-        chunks_emitted_ = chunk;
-        open_shard();
-    } else if (chunk != chunks_emitted_) {
-        invalid("store writer: non-consecutive chunk " + std::to_string(chunk));
-    }
-    append_record(rec, nbytes, rows);
+    write_part(reserve_record(nbytes, rows, static_cast<int64_t>(chunk)), 0, rec, nbytes);
 }
 
 Manifest RecordWriter::finish(int64_t n_obs_override) {

@@ -156,6 +156,15 @@ public:
     // Sparse writing for multi-rank writers that own a subset of the shards:
     // chunk ids must increase and fill each owned shard from slot 0.
     void append_record_at(uint64_t chunk, const void* rec, uint64_t nbytes, uint64_t rows);
+    // Two-step form for streamed records: reserve the next slot (chunk < 0:
+    // consecutive), then write its bytes in any number of parts with
+    // write_part(p, offset in record, ...) before the next reserve/finish.
+    struct Placement {
+        const File* file = nullptr;
+        uint64_t off = 0;  // file offset of the record's first byte
+    };
+    Placement reserve_record(uint64_t nbytes, uint64_t rows, int64_t chunk = -1);
+    static void write_part(const Placement& p, uint64_t rel, const void* src, uint64_t n);
     // finish(): flush shard footer, write manifest (n_obs = rows appended, or
     // n_obs_override when several ranks wrote the store)
     Manifest finish(int64_t n_obs_override = -1);

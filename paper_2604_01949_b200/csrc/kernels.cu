@@ -632,6 +632,97 @@ __global__ void __launch_bounds__(THREADS, MINB)
     if (bulk && tid == 0) bulk_wait0();
 }
 
+// v8: v6 with the per-tile zero fill replaced by un-scattering the stored
+// tile's own entries (smem writes per tile ~ entries instead of tile bytes).
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_csr_densify8(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
+                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ double s_red[THREADS / 32];
+    __shared__ RowDesc s_desc[3];  // rows i, i+1, i+2 of this CTA
+    const uint32_t tid = threadIdx.x;
+    constexpr uint32_t nthr = THREADS;
+    const uint64_t n_var = a.n_var;
+    const uint64_t g = gridDim.x;
+    if (tid == 0) {
+        if (blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
+        if (blockIdx.x + g < n_rows) s_desc[1] = describe_row<IdxT>(a, refs[blockIdx.x + g], sizeof(SrcT));
+    }
+    __syncthreads();
+    // the tile buffer is zeroed once; afterwards each tile's entries are
+    // un-scattered (re-zeroed) once its bulk store has read them
+    for (uint32_t i = tid; i < (tile_cols * static_cast<uint32_t>(sizeof(DstT)) + 15u) / 16u; i += nthr)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    uint32_t colA[U], colB[U];
+    SrcT vA[U], vB[U];
+    if (blockIdx.x < n_rows) load_entries<IdxT, SrcT, U>(s_desc[0], tid, nthr, colA, vA);
+    uint32_t slot = 0;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += g, slot = slot == 2 ? 0 : slot + 1) {
+        const RowDesc d = s_desc[slot];
+        const uint32_t nslot = slot == 2 ? 0 : slot + 1, nnslot = nslot == 2 ? 0 : nslot + 1;
+        const bool has_next = row + g < n_rows;
+        if (has_next) load_entries<IdxT, SrcT, U>(s_desc[nslot], tid, nthr, colB, vB);  // row i+1 in flight
+        if (tid == 0) {
+            if (row + 2 * g < n_rows) s_desc[nnslot] = describe_row<IdxT>(a, refs[row + 2 * g], sizeof(SrcT));
+            if (out_gidx) out_gidx[row] = d.gidx;
+        }
+        float scale = 1.0f;
+        if (norm) {  // library size in fp64
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (colA[u] != ~0u) s += static_cast<double>(vA[u]);
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr)
+                s += static_cast<double>(ld_value<SrcT>(d.val + k * sizeof(SrcT)));
+            s = block_sum(s, s_red);
+            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
+        }
+        DstT* orow = out + row * n_var;
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+            const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
+            const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
+            DstT* tile = reinterpret_cast<DstT*>(smem);
+            __syncthreads();  // previous tile's un-scatter (or the initial zero) is complete
+            const uint32_t c0u = static_cast<uint32_t>(c0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (colA[u] - c0u < cols) tile[colA[u] - c0u] = Conv<DstT, SrcT>::go(vA[u], scale, norm);
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr) {  // rows longer than U*THREADS
+                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
+                if (c2 >= c0 && c2 - c0 < cols)
+                    tile[c2 - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(d.val + k * sizeof(SrcT)), scale, norm);
+            }
+            if (bulk) {
+                fence_proxy_async_shared();
+                __syncthreads();
+                if (tid == 0) {
+                    bulk_store(orow + c0, smem, bytes);
+                    bulk_commit();
+                    bulk_wait_read0();
+                }
+            } else {
+                __syncthreads();
+                for (uint32_t i = tid; i < cols; i += nthr) orow[c0 + i] = tile[i];
+            }
+            __syncthreads();  // the tile has been read out
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (colA[u] - c0u < cols) tile[colA[u] - c0u] = DstT{};
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr) {
+                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
+                if (c2 >= c0 && c2 - c0 < cols) tile[c2 - c0] = DstT{};
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            colA[u] = colB[u];
+            vA[u] = vB[u];
+        }
+    }
+    if (bulk && tid == 0) bulk_wait0();
+}
+
 // ============================================================ K3 densify v3 ===
 // Warp-sweep densify.  Per row: one elected thread stages the row's indices
 // and values into shared memory with two 1-D TMA bulk copies (16-B aligned
@@ -1099,7 +1190,7 @@ const DensifyCfg& densify_cfg() {
         if (e && e[0] == 'v') {
             int v = 2, t = 512, kb = 100, u = 8, mb = 4;
             char st = 't';
-            if (std::sscanf(e, "v%d", &v) == 1 && v == 6) {
+            if (std::sscanf(e, "v%d", &v) == 1 && (v == 6 || v == 8)) {
                 const int got = std::sscanf(e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
                 d.version = v;
                 if (got >= 1) d.threads = t;
@@ -1119,7 +1210,7 @@ const DensifyCfg& densify_cfg() {
     return c;
 }
 
-template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB>
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB, bool UNS = false>
 void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                 uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes) {
     const uint64_t esz = sizeof(DstT);
@@ -1127,7 +1218,10 @@ void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, 
     if (av.n_var * esz > max_tile_bytes) tile_cols = (max_tile_bytes / esz) & ~15ull;
     const size_t smem = (tile_cols * esz + 127) & ~127ull;
     const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    auto kern = k_csr_densify6<IdxT, SrcT, DstT, THREADS, U, MINB>;
+    auto kern = [] {
+        if constexpr (UNS) return k_csr_densify8<IdxT, SrcT, DstT, THREADS, U, MINB>;
+        else return k_csr_densify6<IdxT, SrcT, DstT, THREADS, U, MINB>;
+    }();
     set_smem(kern, smem);
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem), "occupancy");
@@ -1170,6 +1264,14 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
         return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, 40 << 10);
     }
     if constexpr (sizeof(IdxT) == 4 && sizeof(SrcT) == 4) {
+        if (dc.version == 8) {  // v6 + un-scatter
+            const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
+            if (dc.u == 16)
+                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, true>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.minb == 4)
+                return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, true>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, true>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        }
         if (dc.version == 6) {  // A/B set: u32 indices, 4-byte values
             const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
             if (dc.threads == 512)

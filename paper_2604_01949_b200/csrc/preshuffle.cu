@@ -12,6 +12,9 @@
 //
 // Output bytes are identical to the reference's (tests/test_gpu_preshuffle.py).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -33,7 +36,8 @@ namespace {
 
 constexpr uint64_t kAlign = 16;
 constexpr uint64_t kHuge = 1ull << 63;           // chunk_rows of the "absolute" arena view
-constexpr uint64_t kStageBytes = 512ull << 20;   // pinned staging window for round inputs
+constexpr uint64_t kStageBytes = 256ull << 20;   // pinned staging window for round inputs (x2)
+constexpr uint64_t kPieceBytes = 64ull << 20;    // pinned D2H piece of the output records (x2)
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 struct DevBuf {
@@ -120,6 +124,23 @@ std::vector<std::string> unify(std::vector<Member>& ms, bool outer) {
     return uni;
 }
 
+// RFL_TRACE=1: per-phase wall times of the single-GPU pass on stderr.
+struct PhaseTrace {
+    bool on = false;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    PhaseTrace() {
+        const char* e = std::getenv("RFL_TRACE");
+        on = e && e[0] == '1';
+    }
+    void mark(const char* what, uint64_t r) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "# shuffle r%llu %-10s %8.2f ms\n", static_cast<unsigned long long>(r), what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 class GpuShuffler {
 public:
     explicit GpuShuffler(const ShuffleArgs& a) : a_(a) {}
@@ -159,11 +180,14 @@ private:
     std::unique_ptr<RecordWriter> out_, prov_;
     cudaStream_t st_ = nullptr;
     cudaEvent_t e0_ = nullptr, e1_ = nullptr, e2_ = nullptr, e3_ = nullptr;
-    DevBuf d_refs_, d_prefix_, d_scratch_, d_out_;
-    PinBuf h_stage_, h_refs_, h_prefix_, h_out_[2];
-    std::future<void> wjob_[2];  // background writes of h_out_[k]
+    DevBuf d_refs_, d_prefix_, d_scratch_, d_out_[2];
+    PinBuf h_stage_[2], h_refs_, h_prefix_, ring_[2];
+    cudaEvent_t stage_ev_[2] = {nullptr, nullptr}, ring_ev_[2] = {nullptr, nullptr}, packed_[2] = {nullptr, nullptr};
+    cudaStream_t wst_ = nullptr;                  // the writer's D2H stream
+    std::shared_future<void> wjob_[2], last_job_;  // writer job that drains d_out_[k]; the newest job
     uint64_t emits_ = 0;
     void drain_writes() {
+        if (last_job_.valid()) last_job_.get();  // jobs are chained: the newest finishes last
         for (auto& f : wjob_)
             if (f.valid()) f.get();
     }
@@ -184,6 +208,7 @@ private:
     std::vector<uint64_t> mine_out_;
     std::vector<std::pair<uint32_t, uint64_t>> mine_prov_;
     uint64_t staged_round_ = ~0ull;
+    PhaseTrace tr_;
 };
 
 ArenaView absolute_view(Layout l, VDtype v, IDtype i, uint64_t n_var) {
@@ -252,14 +277,17 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
         i = j;
     }
     // windows of the arena image (<= kStageBytes, or one oversized run) read by a
-    // thread pool into pinned memory — alignment gaps ride along — then one H2D
+    // thread pool into one of two pinned buffers — alignment gaps ride along —
+    // then one async H2D, which overlaps the reads of the next window
     const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    for (size_t r = 0; r < runs.size();) {
+    for (size_t r = 0, wi = 0; r < runs.size(); ++wi) {
         const uint64_t w0 = off[runs[r].i];
         size_t r1 = r + 1;
         while (r1 < runs.size() && off[runs[r1].j - 1] + len[runs[r1].j - 1] - w0 <= kStageBytes) ++r1;
         const uint64_t w1 = off[runs[r1 - 1].j - 1] + len[runs[r1 - 1].j - 1];
-        h_stage_.ensure(w1 - w0);
+        PinBuf& stage = h_stage_[wi & 1];
+        cuda_ok(cudaEventSynchronize(stage_ev_[wi & 1]), "stage buffer reuse");  // its previous H2D is done
+        stage.ensure(w1 - w0);
         std::vector<std::exception_ptr> errs(T);
         std::vector<std::thread> pool;
         for (unsigned t = 0; t < T; ++t) {
@@ -269,7 +297,7 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
                         const Run& ru = runs[x];
                         const HostStore& hs = *ms_[need[ru.i].first].hs;
                         const Manifest& hm = hs.manifest();
-                        uint8_t* base = h_stage_.p + (off[ru.i] - w0);
+                        uint8_t* base = stage.p + (off[ru.i] - w0);
                         hs.read_shard_bytes(ru.shard, ru.file_off, base, ru.bytes, false);
                         // decode_record's checks (store.cpp:81-122) on each record of the run
                         for (size_t k = ru.i, rel = 0; k < ru.j; rel += len[k], ++k) {
@@ -291,11 +319,14 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
         for (auto& th : pool) th.join();
         for (auto& e : errs)
             if (e) std::rethrow_exception(e);
-        cuda_ok(cudaMemcpyAsync(arena.p + w0, h_stage_.p, w1 - w0, cudaMemcpyHostToDevice, st_), "stage H2D");
-        cuda_ok(cudaStreamSynchronize(st_), "stage sync");
+        tr_.mark(" read", wi);
+        cuda_ok(cudaMemcpyAsync(arena.p + w0, stage.p, w1 - w0, cudaMemcpyHostToDevice, st_), "stage H2D");
+        cuda_ok(cudaEventRecord(stage_ev_[wi & 1], st_), "event");
         res_.h2d_bytes += w1 - w0;
         r = r1;
     }
+    cuda_ok(cudaStreamSynchronize(st_), "stage sync");
+    tr_.mark(" h2d", r);
     // column checks of CsrBlock::validate for every staged record, on the GPU
     if (layout_ == Layout::csr && validate_) {
         std::vector<uint64_t> tab(2 * need.size());
@@ -329,6 +360,7 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
             i = j;
         }
     }
+    tr_.mark(" validate", r);
     // refs per assembly row
     refs.clear();
     std::vector<std::vector<uint64_t>> remap_pos(ms_.size());
@@ -421,9 +453,13 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
     if (n == 0) return;
     const uint64_t cr = a_.out_chunk_rows;
     const uint64_t nq = (n + cr - 1) / cr;
+    // d_out_[ob] is reused: the writer job that drained it two emits ago is done
+    const int ob = static_cast<int>(emits_++ & 1u);
+    if (wjob_[ob].valid()) wjob_[ob].get();
     upload_refs(refs.data(), n);
     std::vector<uint64_t> rec_len(nq), rec_rows(nq);
     uint64_t total = 0;
+    DevBuf& dout = d_out_[ob];
     if (layout_ == Layout::csr) {
         const ArenaView av = absolute_view(layout_, vdt_, in_idt_, n_var_);
         d_prefix_.ensure((n + 1) * 8);
@@ -446,10 +482,10 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
             rec_len[q] = kCsrHeaderBytes + os * (rows + 1) + (os + vs) * nnz;
             total += rec_len[q];
         }
-        d_out_.ensure(total);
+        dout.ensure(total + total / 8);
         cuda_ok(cudaEventRecord(e3_, st_), "event");
         launch_csr_pack(av, reinterpret_cast<RowRef*>(d_refs_.p), n, cr, out_idt_,
-                        reinterpret_cast<uint64_t*>(d_prefix_.p), d_out_.p, st_);
+                        reinterpret_cast<uint64_t*>(d_prefix_.p), dout.p, st_);
         cuda_ok(cudaEventRecord(e1_, st_), "event");
     } else {
         const ArenaView av = absolute_view(layout_, vdt_, in_idt_, n_var_);
@@ -458,28 +494,13 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
             rec_rows[q] = std::min(cr, n - q * cr);
             rec_len[q] = rec_rows[q] * row_bytes_;
         }
-        d_out_.ensure(std::max<uint64_t>(total, 16));
+        dout.ensure(std::max<uint64_t>(total + total / 8, 16));
         cuda_ok(cudaEventRecord(e0_, st_), "event");
-        launch_dense_gather(av, reinterpret_cast<RowRef*>(d_refs_.p), n, OutDtype::native, d_out_.p, nullptr, st_);
+        launch_dense_gather(av, reinterpret_cast<RowRef*>(d_refs_.p), n, OutDtype::native, dout.p, nullptr, st_);
         cuda_ok(cudaEventRecord(e1_, st_), "event");
     }
-    // double-buffered pinned output: the D2H below may only overwrite a buffer
-    // whose file writes have finished; writes run on one background thread, in
-    // order, overlapping the next round's staging and kernels
-    const int ob = static_cast<int>(emits_++ & 1u);
-    if (wjob_[ob].valid()) wjob_[ob].get();
-    PinBuf& hout = h_out_[ob];
-    hout.ensure(std::max<uint64_t>(total, 16));
-    if (total) cuda_ok(cudaMemcpyAsync(hout.p, d_out_.p, total, cudaMemcpyDeviceToHost, st_), "records D2H");
-    cuda_ok(cudaStreamSynchronize(st_), "sync");
-    float ms = 0.f, ms2 = 0.f;
-    if (layout_ == Layout::csr) {  // kernel time only: scan (e0..e2) + pack (e3..e1)
-        cuda_ok(cudaEventElapsedTime(&ms, e0_, e2_), "elapsed");
-        cuda_ok(cudaEventElapsedTime(&ms2, e3_, e1_), "elapsed");
-    } else {
-        cuda_ok(cudaEventElapsedTime(&ms, e0_, e1_), "elapsed");
-    }
-    res_.gpu_ms += ms + ms2;
+    cuda_ok(cudaEventRecord(packed_[ob], st_), "event");
+    tr_.mark(" kernels", emits_ - 1);
     res_.d2h_bytes += total;
     std::vector<uint64_t> chunk_id;
     if (out_rows)
@@ -490,23 +511,67 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
         wr32(prov_bytes.data() + 12 * k, prov[k].first);
         wr64(prov_bytes.data() + 12 * k + 4, prov[k].second);
     }
-    const int prev = ob ^ 1;
-    if (wjob_[prev].valid()) wjob_[prev].get();  // keep file writes in order (and surface their errors)
-    wjob_[ob] = std::async(std::launch::async, [this, &hout, rec_len = std::move(rec_len), rec_rows = std::move(rec_rows),
-                                                chunk_id = std::move(chunk_id), prov_bytes = std::move(prov_bytes)] {
-        uint64_t pos = 0, ppos = 0;
-        for (size_t q = 0; q < rec_len.size(); ++q) {
-            if (!chunk_id.empty()) {
-                out_->append_record_at(chunk_id[q], hout.p + pos, rec_len[q], rec_rows[q]);
-                prov_->append_record_at(chunk_id[q], prov_bytes.data() + ppos, rec_rows[q] * 12, rec_rows[q]);
-            } else {
-                out_->append_record(hout.p + pos, rec_len[q], rec_rows[q]);
-                prov_->append_record(prov_bytes.data() + ppos, rec_rows[q] * 12, rec_rows[q]);
-            }
-            pos += rec_len[q];
-            ppos += rec_rows[q] * 12;
-        }
-    });
+    // The records leave the device in 64 MB pieces through a two-buffer pinned
+    // ring on the writer's own stream, each piece written (parallel pwrites at
+    // its records' file offsets) while the next one is in flight.  Jobs run in
+    // emit order (each waits for its predecessor), off the staging thread.
+    std::shared_future<void> prev = last_job_;
+    last_job_ = std::async(std::launch::async, [this, ob, total, prev, rec_len = std::move(rec_len),
+                                                rec_rows = std::move(rec_rows), chunk_id = std::move(chunk_id),
+                                                prov_bytes = std::move(prov_bytes)] {
+                    if (prev.valid()) prev.get();
+                    DeviceGuard g(a_.device);
+                    cuda_ok(cudaEventSynchronize(packed_[ob]), "pack done");
+                    const uint8_t* src = d_out_[ob].p;
+                    const uint64_t S = kPieceBytes;
+                    const uint64_t pieces = (total + S - 1) / S;
+                    auto issue = [&](uint64_t i) {
+                        const uint64_t off = i * S, len = std::min(S, total - off);
+                        cuda_ok(cudaMemcpyAsync(ring_[i & 1].p, src + off, len, cudaMemcpyDeviceToHost, wst_), "D2H");
+                        cuda_ok(cudaEventRecord(ring_ev_[i & 1], wst_), "event");
+                    };
+                    if (pieces) issue(0);
+                    size_t q = 0;
+                    uint64_t rstart = 0, ppos = 0;
+                    RecordWriter::Placement cur;
+                    for (uint64_t i = 0; i < pieces; ++i) {
+                        if (i + 1 < pieces) issue(i + 1);
+                        cuda_ok(cudaEventSynchronize(ring_ev_[i & 1]), "D2H done");
+                        const uint64_t p0 = i * S, p1 = std::min(total, p0 + S);
+                        const uint8_t* buf = ring_[i & 1].p;
+                        while (q < rec_len.size() && rstart < p1) {
+                            if (rstart >= p0)  // the record starts in this piece
+                                cur = out_->reserve_record(rec_len[q], rec_rows[q],
+                                                           chunk_id.empty() ? -1 : static_cast<int64_t>(chunk_id[q]));
+                            const uint64_t a = std::max(rstart, p0), b = std::min(rstart + rec_len[q], p1);
+                            RecordWriter::write_part(cur, a - rstart, buf + (a - p0), b - a);
+                            if (rstart + rec_len[q] > p1) break;  // continues in the next piece
+                            const int64_t cid = chunk_id.empty() ? -1 : static_cast<int64_t>(chunk_id[q]);
+                            RecordWriter::write_part(prov_->reserve_record(rec_rows[q] * 12, rec_rows[q], cid), 0,
+                                                     prov_bytes.data() + ppos, rec_rows[q] * 12);
+                            ppos += rec_rows[q] * 12;
+                            rstart += rec_len[q];
+                            ++q;
+                        }
+                    }
+                    for (; q < rec_len.size(); ++q) {  // empty records (total == 0 tail)
+                        const int64_t cid = chunk_id.empty() ? -1 : static_cast<int64_t>(chunk_id[q]);
+                        out_->reserve_record(rec_len[q], rec_rows[q], cid);
+                        RecordWriter::write_part(prov_->reserve_record(rec_rows[q] * 12, rec_rows[q], cid), 0,
+                                                 prov_bytes.data() + ppos, rec_rows[q] * 12);
+                        ppos += rec_rows[q] * 12;
+                    }
+                }).share();
+    wjob_[ob] = last_job_;
+    float ms = 0.f, ms2 = 0.f;
+    cuda_ok(cudaEventSynchronize(e1_), "sync");
+    if (layout_ == Layout::csr) {  // kernel time only: scan (e0..e2) + pack (e3..e1)
+        cuda_ok(cudaEventElapsedTime(&ms, e0_, e2_), "elapsed");
+        cuda_ok(cudaEventElapsedTime(&ms2, e3_, e1_), "elapsed");
+    } else {
+        cuda_ok(cudaEventElapsedTime(&ms, e0_, e1_), "elapsed");
+    }
+    res_.gpu_ms += ms + ms2;
     res_.rows_written += n;
 }
 
@@ -538,6 +603,19 @@ void GpuShuffler::carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst) {
 }
 
 GpuShuffler::~GpuShuffler() {
+    try {  // an abandoned pass (error) still joins its writer job
+        if (last_job_.valid()) last_job_.wait();
+    } catch (...) {
+    }
+    if (wst_) {
+        cudaStreamSynchronize(wst_);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(stage_ev_[k]);
+            cudaEventDestroy(ring_ev_[k]);
+            cudaEventDestroy(packed_[k]);
+        }
+        cudaStreamDestroy(wst_);
+    }
     if (st_) {
         cudaStreamSynchronize(st_);
         cudaEventDestroy(e0_);
@@ -630,6 +708,14 @@ void GpuShuffler::init() {
     if (const char* nv = std::getenv("RFL_NO_VALIDATE")) validate_ = nv[0] != '1';
     DeviceGuard g(a_.device);
     cuda_ok(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+    cuda_ok(cudaStreamCreateWithFlags(&wst_, cudaStreamNonBlocking), "stream");
+    for (int k = 0; k < 2; ++k) {  // pinned staging / output rings, allocated once (cudaHostAlloc is slow)
+        h_stage_[k].ensure(kStageBytes);
+        ring_[k].ensure(kPieceBytes);
+        cuda_ok(cudaEventCreateWithFlags(&stage_ev_[k], cudaEventDisableTiming), "event");
+        cuda_ok(cudaEventCreateWithFlags(&ring_ev_[k], cudaEventDisableTiming), "event");
+        cuda_ok(cudaEventCreateWithFlags(&packed_[k], cudaEventDisableTiming), "event");
+    }
     cuda_ok(cudaEventCreate(&e0_), "event");
     cuda_ok(cudaEventCreate(&e1_), "event");
     cuda_ok(cudaEventCreate(&e2_), "event");
@@ -665,7 +751,9 @@ void GpuShuffler::round_segments(uint64_t r, Segs& segs, std::vector<std::pair<u
 }
 
 ShuffleResult GpuShuffler::run() {
+    PhaseTrace& tr = tr_;
     init();
+    tr.mark("init", 0);
     DeviceGuard g(a_.device);
     std::vector<RowRef> round_refs;
     Segs segs;
@@ -675,22 +763,28 @@ ShuffleResult GpuShuffler::run() {
         round_segments(r, segs, asm_prov, nullptr);
         const uint64_t round_rows = asm_prov.size();
         res_.peak_resident_rows = std::max(res_.peak_resident_rows, round_rows + std::min(a_.c, round_rows));
+        tr.mark("segments", r);
         stage_round(segs, arena_[r % 2], round_refs, r);
+        tr.mark("stage", r);
         check_duplicates(r, bad_asm_, round_rows);
         const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
         for (uint64_t k = 0; k < round_rows; ++k) {
             pending_.push_back(round_refs[perm[k]]);
             pend_prov_.push_back(asm_prov[perm[k]]);
         }
+        tr.mark("permute", r);
         const bool last = r + 1 == plan_.rounds.size();
         const uint64_t n_emit = last ? pending_.size() : pending_.size() / cr * cr;
         emit(pending_, pend_prov_, n_emit, nullptr);
+        tr.mark("emit", r);
         pending_.erase(pending_.begin(), pending_.begin() + n_emit);
         pend_prov_.erase(pend_prov_.begin(), pend_prov_.begin() + n_emit);
         if (!pending_.empty()) carry(pending_, 0, carry_[r % 2]);
+        tr.mark("carry", r);
         res_.rounds++;
     }
     drain_writes();
+    tr.mark("drain", 0);
     out_->finish();
     prov_->finish();
     write_text_file(a_.out_path + "/provenance/meta.json", meta_json(a_.seed, a_.c, a_.m));
