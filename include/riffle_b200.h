@@ -224,6 +224,15 @@ typedef struct rfl_arena_desc {
 rfl_status rfl_csr_gather(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,
                           uint64_t* d_out_indptr, void* d_out_indices, void* d_out_data,
                           uint64_t* d_out_gidx, void* stream);
+/* K2 with the indptr planned on the host: d_prefix[n_rows+1] is the exclusive
+ * nnz prefix of the rows (the host schedule knows every row's nnz), so no
+ * device scan runs; output indices/data start at entry d_prefix[0].  d_prefix
+ * may be the caller's output indptr (rebased to 0 it is the batch's indptr,
+ * CsrBlock::append_rows block.cpp:92-108).  Entries are read only up to each
+ * row's own nnz in its record. */
+rfl_status rfl_csr_gather_prefixed(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,
+                                   const uint64_t* d_prefix, void* d_out_indices, void* d_out_data,
+                                   uint64_t* d_out_gidx, void* stream);
 /* K3: gather + densify (to_dense, block.cpp:135-146) with optional fused
  * library-size normalisation + log1p; out_dtype RFL_NATIVE|RFL_F32|RFL_BF16. */
 rfl_status rfl_csr_densify(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,

@@ -110,6 +110,7 @@ SIGNATURES = [
     ("rfl_loader_sync", C.c_int, [vp]),
     ("rfl_loader_destroy", None, [vp]),
     ("rfl_csr_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp, vp, vp, vp]),
+    ("rfl_csr_gather_prefixed", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp, vp, vp, vp]),
     ("rfl_csr_densify", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, u32, C.c_float, vp, vp, vp]),
     ("rfl_dense_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, vp, vp, vp]),
     ("rfl_csr_scan", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp]),

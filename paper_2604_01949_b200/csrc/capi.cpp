@@ -364,6 +364,15 @@ rfl_status rfl_csr_gather(const rfl_arena_desc* a, const rfl_rowref* refs, uint6
     });
 }
 
+rfl_status rfl_csr_gather_prefixed(const rfl_arena_desc* a, const rfl_rowref* refs, uint64_t n, const uint64_t* prefix,
+                                   void* out_indices, void* out_data, uint64_t* out_gidx, void* stream) {
+    return guarded([&] {
+        if (n && !prefix) rfl::invalid("csr_gather_prefixed: prefix is NULL");
+        rfl::launch_csr_gather_prefixed(to_view(a), reinterpret_cast<const rfl::RowRef*>(refs), n, prefix, out_indices,
+                                        out_data, out_gidx, static_cast<cudaStream_t>(stream));
+    });
+}
+
 rfl_status rfl_csr_densify(const rfl_arena_desc* a, const rfl_rowref* refs, uint64_t n, uint32_t out_dtype,
                            uint32_t transform, float target, void* out, uint64_t* out_gidx, void* stream) {
     return guarded([&] {

@@ -482,6 +482,7 @@ GpuLoader::~GpuLoader() {
         cudaFree(s.d_refs);
         cudaFreeHost(s.h_refs);
         cudaFreeHost(s.h_gidx);
+        cudaFreeHost(s.h_prefix);
         cudaEventDestroy(s.done);
     }
     reader_.reset();
@@ -551,6 +552,8 @@ void GpuLoader::ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz) {
         cudaFree(s.d_refs);
         cudaFreeHost(s.h_refs);
         cudaFreeHost(s.h_gidx);
+        cudaFreeHost(s.h_prefix);
+        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&s.h_prefix), (rows + 1) * 8, cudaHostAllocDefault), "pinned");
         cuda_ok(cudaMalloc(&s.gidx, rows * 8), "malloc");
         cuda_ok(cudaMalloc(&s.indptr, (rows + 1) * 8), "malloc");
         cuda_ok(cudaMalloc(&s.scratch, csr_gather_scratch_bytes(rows)), "malloc");
@@ -624,6 +627,24 @@ bool GpuLoader::next(BatchOut& out) {
     }
     cuda_ok(cudaMemcpyAsync(s.d_refs, s.h_refs, n * sizeof(RowRef), cudaMemcpyHostToDevice, copy_), "refs H2D");
     ctr_.h2d_bytes += n * sizeof(RowRef);
+    // CSR output: the batch indptr is the prefix of the schedule's per-row nnz
+    // (CsrBlock::append_rows rebase, block.cpp:92-108) -- planned here, so the
+    // device runs one balanced copy kernel and no scan
+    static const bool device_scan = [] {
+        const char* e = std::getenv("RFL_GATHER");
+        return e && (std::string(e) == "scan" || std::string(e) == "jobs");
+    }();
+    const bool planned = m.layout == Layout::csr && dev_.output == 0 && !device_scan;
+    if (planned) {
+        uint64_t acc = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            s.h_prefix[i] = acc;
+            acc += ds_->row_nnz(gidx_[i]);
+        }
+        s.h_prefix[n] = acc;
+        cuda_ok(cudaMemcpyAsync(s.indptr, s.h_prefix, (n + 1) * 8, cudaMemcpyHostToDevice, copy_), "indptr H2D");
+        ctr_.h2d_bytes += (n + 1) * 8;
+    }
     cuda_ok(cudaEventRecord(staged_, copy_), "event");
     cuda_ok(cudaStreamWaitEvent(compute_, staged_, 0), "wait staged");
 
@@ -633,6 +654,9 @@ bool GpuLoader::next(BatchOut& out) {
     } else if (dev_.output == 1) {
         launch_csr_densify(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,
                            static_cast<uint64_t*>(s.gidx), compute_, n ? (nnz + n - 1) / n : 0);
+    } else if (planned) {
+        launch_csr_gather_prefixed(av, s.d_refs, n, static_cast<const uint64_t*>(s.indptr), s.indices, s.data,
+                                   static_cast<uint64_t*>(s.gidx), compute_);
     } else {
         launch_csr_gather(av, s.d_refs, n, static_cast<uint64_t*>(s.indptr), s.indices, s.data,
                           static_cast<uint64_t*>(s.gidx), s.scratch, compute_);

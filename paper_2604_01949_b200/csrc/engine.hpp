@@ -155,6 +155,7 @@ private:
         RowRef* d_refs = nullptr;
         RowRef* h_refs = nullptr;
         uint64_t* h_gidx = nullptr;
+        uint64_t* h_prefix = nullptr;  // CSR output: the batch indptr, planned on the host
         uint64_t cap_rows = 0, cap_nnz = 0, data_bytes = 0;
         cudaEvent_t done = nullptr;
         bool used = false;

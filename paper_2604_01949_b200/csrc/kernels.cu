@@ -10,6 +10,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "kernels.cuh"
 
@@ -79,6 +80,15 @@ __device__ __forceinline__ uint64_t ld_volatile_u64(const unsigned long long* p)
 __device__ __forceinline__ void st_volatile_u64(unsigned long long* p, uint64_t v) {
     asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+
+// ------------------------------------- programmatic dependent launch (PDL) ---
+// With the launch attribute set (default; RFL_PDL=0 turns it off) a kernel's CTAs may be scheduled
+// while the previous kernel of the stream drains; griddepcontrol.wait then
+// blocks until that kernel has completed and its writes are visible, so the
+// semantics are unchanged -- only launch latency and ramp-up overlap.  Without
+// the attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---------------------------------------------------- TMA bulk (1-D) store ---
 __device__ __forceinline__ void fence_proxy_async_shared() {
@@ -311,6 +321,92 @@ __global__ void __launch_bounds__(kCopyThreads, 4)
         const RowJob jb = jobs[row];
         const uint32_t es = val ? vs : static_cast<uint32_t>(sizeof(IdxT));
         warp_copy((val ? out_val : out_idx) + off * es, val ? jb.val : jb.idx, cnt * es, lane);
+    }
+}
+
+// Balanced variant of the copy: the output of each array is cut into equal
+// 16-B aligned byte ranges, one per warp of a persistent grid (warps
+// [0, w_idx) take the indices, the rest the values), so every warp moves the
+// same number of bytes whatever the row lengths — no wave quantisation over
+// (row, array) jobs.  A warp finds its first row with a 32-way search of the
+// prefix P, then walks the (usually 1-3) rows its range overlaps, resolving
+// their source rows lane-parallel (from the scan's job table when given, else
+// straight from the chunk records: the host-planned path, where P is the
+// host's prefix of the schedule's per-row nnz and no scan runs).  Reads are
+// clamped to the row's own nnz, so an inconsistent P cannot read out of bounds.
+template <typename IdxT>
+__global__ void __launch_bounds__(kCopyThreads)
+    k_csr_copy_flat(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, const RowJob* __restrict__ jobs,
+                    const uint64_t* __restrict__ P, uint64_t n_rows, uint32_t w_idx, uint8_t* __restrict__ out_idx,
+                    uint8_t* __restrict__ out_val, uint64_t* __restrict__ out_gidx) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t gw = blockIdx.x * (kCopyThreads / 32) + (threadIdx.x >> 5);
+    const uint32_t n_warps = gridDim.x * (kCopyThreads / 32);
+    pdl_wait();
+    pdl_trigger();
+    if (out_gidx && !jobs)  // the scan path writes gidx itself
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kCopyThreads + threadIdx.x; i < n_rows;
+             i += static_cast<uint64_t>(gridDim.x) * kCopyThreads)
+            out_gidx[i] = refs[i].gidx;
+    const bool is_val = gw >= w_idx;
+    const uint32_t es = is_val ? vs : static_cast<uint32_t>(sizeof(IdxT));
+    const uint32_t nw = is_val ? n_warps - w_idx : w_idx, w = is_val ? gw - w_idx : gw;
+    const uint64_t p0 = P[0], total = P[n_rows] - p0;
+    const uint64_t span = (((total * es + nw - 1) / nw) + 15) & ~15ull;
+    const uint64_t e0 = w * span / es;
+    if (e0 >= total) return;
+    const uint64_t e1 = umin64(e0 + span / es, total);
+    uint8_t* const out = is_val ? out_val : out_idx;
+    // largest r with P[r] - p0 <= e0 (32-way narrowing)
+    uint64_t lo = 0, hi = n_rows;  // invariant: answer in [lo, hi)
+    while (hi - lo > 32) {
+        const uint64_t step = (hi - lo + 31) / 32;
+        const uint64_t k = lo + lane * step;
+        const bool ok = k < hi && P[k] - p0 <= e0;
+        const uint32_t c = __popc(__ballot_sync(kFull, ok));  // >= 1 (lane 0 holds lo)
+        lo += (c - 1) * step;
+        hi = umin64(lo + step, hi);
+    }
+    {
+        const uint64_t k = lo + lane;
+        const bool ok = k < hi && P[k] - p0 <= e0;
+        lo += __popc(__ballot_sync(kFull, ok)) - 1;
+    }
+    for (uint64_t r = lo; r < n_rows; r += 32) {
+        const uint64_t rl = r + lane;
+        uint64_t pl = ~0ull, ph = 0;
+        if (rl < n_rows) {
+            pl = P[rl] - p0;
+            ph = P[rl + 1] - p0;
+        }
+        const uint32_t act = __ballot_sync(kFull, rl < n_rows && pl < e1);
+        const uint8_t* src = nullptr;
+        uint64_t avail = 0;
+        if ((act >> lane) & 1u) {
+            if (jobs) {
+                const RowJob jb = jobs[rl];
+                src = is_val ? jb.val : jb.idx;
+                avail = ph - pl;
+            } else {
+                const CsrRow c = csr_row<IdxT>(a, refs[rl], vs);
+                src = is_val ? c.val : c.idx;
+                avail = c.nnz;
+            }
+        }
+        for (uint32_t m = act; m; m &= m - 1) {
+            const int k = __ffs(m) - 1;
+            const uint64_t kpl = __shfl_sync(kFull, pl, k), kph = __shfl_sync(kFull, ph, k);
+            const uint64_t kav = __shfl_sync(kFull, avail, k);
+            const uint8_t* ks = reinterpret_cast<const uint8_t*>(
+                __shfl_sync(kFull, reinterpret_cast<unsigned long long>(src), k));
+            const uint64_t s = kpl > e0 ? kpl : e0, t = umin64(kph, e1);
+            if (s >= t) continue;
+            const uint64_t in_row = s - kpl;
+            const uint64_t cnt = in_row >= kav ? 0 : umin64(t - s, kav - in_row);
+            warp_copy(out + s * es, ks + in_row * es, cnt * es, lane);
+        }
+        if (act != kFull) break;
+        if (__shfl_sync(kFull, ph, 31) >= e1) break;
     }
 }
 
@@ -562,6 +658,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     constexpr uint32_t nthr = THREADS;
     const uint64_t n_var = a.n_var;
     const uint64_t g = gridDim.x;
+    pdl_wait();
+    pdl_trigger();
     if (tid == 0) {
         if (blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
         if (blockIdx.x + g < n_rows) s_desc[1] = describe_row<IdxT>(a, refs[blockIdx.x + g], sizeof(SrcT));
@@ -645,6 +743,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     constexpr uint32_t nthr = THREADS;
     const uint64_t n_var = a.n_var;
     const uint64_t g = gridDim.x;
+    pdl_wait();
+    pdl_trigger();
     if (tid == 0) {
         if (blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
         if (blockIdx.x + g < n_rows) s_desc[1] = describe_row<IdxT>(a, refs[blockIdx.x + g], sizeof(SrcT));
@@ -879,6 +979,225 @@ __global__ void __launch_bounds__(kSweepThreads, 6)
             }
         }
         __syncthreads();  // staging buffers are re-filled for the next row
+    }
+}
+
+// ===================================================== K2 copy, TMA staged ===
+// The balanced range split of k_csr_copy_flat, with the source side moved to
+// the async proxy: each warp streams its output range as pieces of <= 4 KB;
+// one lane issues a 1-D TMA bulk load of the piece's 16-B aligned source
+// superset into the warp's shared stage (completion on an mbarrier), two
+// stages in flight, and the warp writes the piece with aligned 16-B stores,
+// re-aligning neighbouring shared chunks with funnel shifts.  Bytes in flight
+// no longer cost registers: 8 KB per warp regardless of row alignment.
+constexpr int kTcWarps = 4;
+constexpr int kTcThreads = kTcWarps * 32;
+constexpr uint32_t kTcPiece = 4096;
+constexpr uint32_t kTcStage = kTcPiece + 32;
+
+struct TcPiece {
+    const uint8_t* src;
+    uint8_t* dst;
+    uint32_t len;  // bytes; 0 = no piece
+};
+
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(addr));
+    return r;
+}
+__device__ __forceinline__ uint8_t lds_u8(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+    return static_cast<uint8_t>(v);
+}
+
+// Generator of one warp's pieces (all state warp-uniform; rows resolved 32 at
+// a time lane-parallel, as in k_csr_copy_flat).
+template <typename IdxT>
+struct TcGen {
+    ArenaDev a;
+    const RowRef* refs;
+    const RowJob* jobs;
+    const uint64_t* P;
+    uint64_t n_rows, p0, e0, e1, r;
+    uint8_t* out;
+    uint32_t es, vs, lane, act, k;
+    bool is_val, more;
+    uint64_t pl, ph, avail, pos;
+    const uint8_t* src;
+
+    __device__ void load_batch() {
+        const uint64_t rl = r + lane;
+        pl = ~0ull;
+        ph = 0;
+        if (rl < n_rows) {
+            pl = P[rl] - p0;
+            ph = P[rl + 1] - p0;
+        }
+        act = __ballot_sync(kFull, rl < n_rows && pl < e1);
+        src = nullptr;
+        avail = 0;
+        if ((act >> lane) & 1u) {
+            if (jobs) {
+                const RowJob jb = jobs[rl];
+                src = is_val ? jb.val : jb.idx;
+                avail = ph - pl;
+            } else {
+                const CsrRow c = csr_row<IdxT>(a, refs[rl], vs);
+                src = is_val ? c.val : c.idx;
+                avail = c.nnz;
+            }
+        }
+        more = act == kFull && __shfl_sync(kFull, ph, 31) < e1;
+        k = 0;
+        pos = 0;
+    }
+    __device__ TcPiece next() {
+        for (;;) {
+            if (k >= 32 || !((act >> k) & 1u)) {
+                if (!more) return {nullptr, nullptr, 0};
+                r += 32;
+                load_batch();
+                continue;
+            }
+            const uint64_t kpl = __shfl_sync(kFull, pl, k), kph = __shfl_sync(kFull, ph, k);
+            const uint64_t kav = __shfl_sync(kFull, avail, k);
+            const uint64_t s = (kpl > e0 ? kpl : e0) + pos, t = umin64(kph, e1);
+            const uint64_t in_row = s - kpl;
+            const uint64_t lim = kav > in_row ? umin64(t, kpl + kav) : s;  // reads clamped to the row
+            if (s >= lim) {
+                ++k;
+                pos = 0;
+                continue;
+            }
+            uint8_t* dst = out + s * es;
+            const uint64_t room = kTcPiece - (reinterpret_cast<uintptr_t>(dst) & 15u);
+            const uint64_t len = umin64((lim - s) * es, room);
+            const uint8_t* ks =
+                reinterpret_cast<const uint8_t*>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(src), k));
+            pos += len / es;
+            return {ks + in_row * es, dst, static_cast<uint32_t>(len)};
+        }
+    }
+};
+
+__device__ __forceinline__ void tc_issue(const TcPiece& pc, uint8_t* stage, uint64_t* bar, uint32_t lane) {
+    if (lane == 0 && pc.len) {
+        const uintptr_t lo = reinterpret_cast<uintptr_t>(pc.src) & ~uintptr_t(15);
+        const uintptr_t hi = (reinterpret_cast<uintptr_t>(pc.src) + pc.len + 15) & ~uintptr_t(15);
+        const uint32_t bytes = static_cast<uint32_t>(hi - lo);
+        mbar_arrive_expect_tx(bar, bytes);
+        bulk_load(stage, reinterpret_cast<const void*>(lo), bytes, bar);
+    }
+}
+
+__device__ __forceinline__ void tc_write(const TcPiece& pc, const uint8_t* stage, uint32_t lane) {
+    const uint32_t sbase = smem_u32(stage);
+    const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(pc.src) & 15u);
+    uint32_t head = (16u - static_cast<uint32_t>(reinterpret_cast<uintptr_t>(pc.dst) & 15u)) & 15u;
+    if (head > pc.len) head = pc.len;
+    if (lane < head) pc.dst[lane] = lds_u8(sbase + sh + lane);
+    const uint32_t o = sh + head;  // stage offset of the first aligned destination chunk
+    const uint32_t nvec = (pc.len - head) >> 4;
+    const uint32_t s2 = o & 15u;
+    const uint32_t q0 = sbase + (o & ~15u);
+    uint4* d4 = reinterpret_cast<uint4*>(pc.dst + head);
+    if (s2 == 0) {
+        for (uint32_t c = lane; c < nvec; c += 32) st_v4(d4 + c, lds_v4(q0 + 16 * c));
+    } else {
+        for (uint32_t c = lane; c < nvec; c += 32) st_v4(d4 + c, shift_merge(lds_v4(q0 + 16 * c), lds_v4(q0 + 16 * c + 16), s2));
+    }
+    const uint32_t done = head + (nvec << 4);
+    if (lane < pc.len - done) pc.dst[done + lane] = lds_u8(sbase + sh + done + lane);
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kTcThreads)
+    k_csr_copy_tma(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, const RowJob* __restrict__ jobs,
+                   const uint64_t* __restrict__ P, uint64_t n_rows, uint32_t w_idx, uint8_t* __restrict__ out_idx,
+                   uint8_t* __restrict__ out_val, uint64_t* __restrict__ out_gidx) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t s_bar[kTcWarps][2];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * kTcWarps + warp;
+    const uint32_t n_warps = gridDim.x * kTcWarps;
+    uint8_t* st0 = smem + warp * 2 * kTcStage;
+    uint8_t* st1 = st0 + kTcStage;
+    uint64_t* b0 = &s_bar[warp][0];
+    uint64_t* b1 = &s_bar[warp][1];
+    if (lane == 0) {
+        mbar_init(b0, 1);
+        mbar_init(b1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    pdl_wait();
+    pdl_trigger();
+    if (out_gidx && !jobs)
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kTcThreads + threadIdx.x; i < n_rows;
+             i += static_cast<uint64_t>(gridDim.x) * kTcThreads)
+            out_gidx[i] = refs[i].gidx;
+    const bool is_val = gw >= w_idx;
+    const uint32_t es = is_val ? vs : static_cast<uint32_t>(sizeof(IdxT));
+    const uint32_t nw = is_val ? n_warps - w_idx : w_idx, w = is_val ? gw - w_idx : gw;
+    const uint64_t p0 = P[0], total = P[n_rows] - p0;
+    const uint64_t span = (((total * es + nw - 1) / nw) + 15) & ~15ull;
+    const uint64_t e0 = w * span / es;
+    if (e0 >= total) return;
+    const uint64_t e1 = umin64(e0 + span / es, total);
+    uint64_t lo = 0, hi = n_rows;
+    while (hi - lo > 32) {
+        const uint64_t step = (hi - lo + 31) / 32;
+        const uint64_t k = lo + lane * step;
+        const bool ok = k < hi && P[k] - p0 <= e0;
+        const uint32_t c = __popc(__ballot_sync(kFull, ok));
+        lo += (c - 1) * step;
+        hi = umin64(lo + step, hi);
+    }
+    {
+        const uint64_t k = lo + lane;
+        const bool ok = k < hi && P[k] - p0 <= e0;
+        lo += __popc(__ballot_sync(kFull, ok)) - 1;
+    }
+    TcGen<IdxT> gen;
+    gen.a = a;
+    gen.refs = refs;
+    gen.jobs = jobs;
+    gen.P = P;
+    gen.n_rows = n_rows;
+    gen.p0 = p0;
+    gen.e0 = e0;
+    gen.e1 = e1;
+    gen.r = lo;
+    gen.out = is_val ? out_val : out_idx;
+    gen.es = es;
+    gen.vs = vs;
+    gen.lane = lane;
+    gen.is_val = is_val;
+    gen.load_batch();
+    TcPiece p_0 = gen.next();
+    tc_issue(p_0, st0, b0, lane);
+    TcPiece p_1 = gen.next();
+    tc_issue(p_1, st1, b1, lane);
+    uint32_t ph0 = 0, ph1 = 0;
+    for (;;) {
+        if (!p_0.len) break;
+        mbar_wait(b0, ph0);
+        ph0 ^= 1u;
+        tc_write(p_0, st0, lane);
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the next async write
+        p_0 = gen.next();
+        tc_issue(p_0, st0, b0, lane);
+        if (!p_1.len) break;
+        mbar_wait(b1, ph1);
+        ph1 ^= 1u;
+        tc_write(p_1, st1, lane);
+        __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        p_1 = gen.next();
+        tc_issue(p_1, st1, b1, lane);
     }
 }
 
@@ -1118,6 +1437,8 @@ template <int MODE>
 __global__ void __launch_bounds__(kDgThreads)
     k_dense_gather_flat(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
                         uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx) {
+    pdl_wait();
+    pdl_trigger();
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t cpr = in_row_bytes / 16;                    // 16-B chunks per input row
     const uint64_t upr = (cpr + 32 * kDgU - 1) / (32 * kDgU);  // units per row
@@ -1170,6 +1491,32 @@ __global__ void __launch_bounds__(kDgThreads)
 // ------------------------------------------------------------ host helpers ---
 int g_sm_count = 0;
 std::once_flag g_sm_once;
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("RFL_PDL");  // default on; RFL_PDL=0 for plain launches
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// <<<>>> with the programmatic-stream-serialization attribute when PDL is on
+// (inside stream capture this becomes a programmatic graph edge).
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const char* what,
+              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cuda_check(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), what);
+}
 
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
@@ -1226,9 +1573,8 @@ void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, 
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem), "occupancy");
     const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
-    kern<<<static_cast<unsigned>(grid), THREADS, smem, st>>>(dev_view(av), refs, n, static_cast<uint32_t>(tile_cols),
-                                                           norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
-    cuda_check(cudaGetLastError(), "k_csr_densify6 launch");
+    launch_k(kern, dim3(static_cast<unsigned>(grid)), dim3(THREADS), smem, st, "k_csr_densify6 launch", dev_view(av),
+             refs, n, static_cast<uint32_t>(tile_cols), norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
 }
 
 template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int NBUF>
@@ -1371,6 +1717,45 @@ void launch_scan(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* o
 }
 }  // namespace
 
+bool gather_tma() {
+    static const bool on = [] {
+        const char* e = std::getenv("RFL_GATHER");
+        return !(e && std::string(e) == "flat");
+    }();
+    return on;
+}
+
+void launch_copy_flat(const ArenaView& a, uint32_t vs, const RowRef* refs, const RowJob* jobs, const uint64_t* P,
+                      uint64_t n, void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st) {
+    if (gather_tma()) {
+        auto kern = a.idt == IDtype::u32 ? k_csr_copy_tma<uint32_t> : k_csr_copy_tma<uint64_t>;
+        const size_t smem = 2 * kTcStage * kTcWarps;
+        static int per_sm[2] = {0, 0};
+        int& occ = per_sm[a.idt == IDtype::u32 ? 0 : 1];
+        if (!occ) {
+            set_smem(kern, smem);
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTcThreads, smem), "occupancy");
+        }
+        const uint32_t blocks = static_cast<uint32_t>(std::max(occ, 1) * device_sm_count());
+        const uint32_t n_warps = blocks * kTcWarps;
+        const uint32_t is = static_cast<uint32_t>(index_size(a.idt));
+        const uint32_t w_idx = std::max(1u, std::min(n_warps - 1, (n_warps * is + (is + vs) / 2) / (is + vs)));
+        launch_k(kern, dim3(blocks), dim3(kTcThreads), smem, st, "k_csr_copy_tma launch", dev_view(a), vs, refs, jobs,
+                 P, n, w_idx, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data), out_gidx);
+        return;
+    }
+    auto kern = a.idt == IDtype::u32 ? k_csr_copy_flat<uint32_t> : k_csr_copy_flat<uint64_t>;
+    static int per_sm[2] = {0, 0};
+    int& occ = per_sm[a.idt == IDtype::u32 ? 0 : 1];
+    if (!occ) cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCopyThreads, 0), "occupancy");
+    const uint32_t blocks = static_cast<uint32_t>(std::max(occ, 1) * device_sm_count());
+    const uint32_t n_warps = blocks * (kCopyThreads / 32);
+    const uint32_t is = static_cast<uint32_t>(index_size(a.idt));
+    const uint32_t w_idx = std::max(1u, std::min(n_warps - 1, (n_warps * is + (is + vs) / 2) / (is + vs)));
+    launch_k(kern, dim3(blocks), dim3(kCopyThreads), 0, st, "k_csr_copy_flat launch", dev_view(a), vs, refs, jobs, P, n,
+             w_idx, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data), out_gidx);
+}
+
 size_t csr_gather_scratch_bytes(uint64_t n_rows) { return scan_status_bytes(n_rows) + n_rows * sizeof(RowJob); }
 
 void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_indptr, void* out_indices,
@@ -1382,9 +1767,14 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
     }
     RowJob* jobs = reinterpret_cast<RowJob*>(static_cast<uint8_t*>(scratch) + scan_status_bytes(n));
     launch_scan(a, refs, n, out_indptr, jobs, out_gidx, scratch, st);
+    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
+    static const bool legacy = [] {
+        const char* e = std::getenv("RFL_GATHER");
+        return e && std::string(e) == "jobs";
+    }();
+    if (!legacy) return launch_copy_flat(a, vs, refs, jobs, out_indptr, n, out_indices, out_data, nullptr, st);
     const unsigned grid = static_cast<unsigned>(
         std::min<uint64_t>((2 * n + kCopyThreads / 32 - 1) / (kCopyThreads / 32), 8ull * device_sm_count()));
-    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
     if (a.idt == IDtype::u32)
         k_csr_copy<uint32_t><<<grid, kCopyThreads, 0, st>>>(jobs, out_indptr, n, vs, static_cast<uint8_t*>(out_indices),
                                                            static_cast<uint8_t*>(out_data));
@@ -1392,6 +1782,14 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
         k_csr_copy<uint64_t><<<grid, kCopyThreads, 0, st>>>(jobs, out_indptr, n, vs, static_cast<uint8_t*>(out_indices),
                                                            static_cast<uint8_t*>(out_data));
     cuda_check(cudaGetLastError(), "k_csr_copy launch");
+}
+
+void launch_csr_gather_prefixed(const ArenaView& a, const RowRef* refs, uint64_t n, const uint64_t* prefix,
+                                void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st) {
+    if (a.layout != Layout::csr) invalid("csr_gather: store is not csr");
+    if (n == 0) return;
+    launch_copy_flat(a, static_cast<uint32_t>(value_size(a.vdt)), refs, nullptr, prefix, n, out_indices, out_data,
+                     out_gidx, st);
 }
 
 void launch_csr_row_scan(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_prefix, void* scratch,
@@ -1524,16 +1922,19 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         const uint64_t warps_needed = n * upr;
         const unsigned g2 = static_cast<unsigned>(std::max<uint64_t>(
             1, std::min<uint64_t>((warps_needed + kDgThreads / 32 - 1) / (kDgThreads / 32), 8ull * device_sm_count())));
+        const char* what = "k_dense_gather_flat launch";
         if (od == OutDtype::bf16 && a.vdt == VDtype::u8) {
-            k_dense_gather_flat<kU8ToBf16><<<g2, kDgThreads, 0, st>>>(d, in_rb, refs, n, o, a.n_var * 2, out_gidx);
+            launch_k(k_dense_gather_flat<kU8ToBf16>, dim3(g2), dim3(kDgThreads), 0, st, what, d, in_rb, refs, n, o,
+                     a.n_var * 2, out_gidx);
         } else if (od == OutDtype::bf16 && a.vdt == VDtype::f32) {
-            k_dense_gather_flat<kF32ToBf16><<<g2, kDgThreads, 0, st>>>(d, in_rb, refs, n, o, a.n_var * 2, out_gidx);
+            launch_k(k_dense_gather_flat<kF32ToBf16>, dim3(g2), dim3(kDgThreads), 0, st, what, d, in_rb, refs, n, o,
+                     a.n_var * 2, out_gidx);
         } else if (od == OutDtype::native || (od == OutDtype::f32 && a.vdt == VDtype::f32)) {
-            k_dense_gather_flat<kRaw><<<g2, kDgThreads, 0, st>>>(d, in_rb, refs, n, o, in_rb, out_gidx);
+            launch_k(k_dense_gather_flat<kRaw>, dim3(g2), dim3(kDgThreads), 0, st, what, d, in_rb, refs, n, o, in_rb,
+                     out_gidx);
         } else {
             invalid("dense_gather: unsupported output dtype for this store");
         }
-        cuda_check(cudaGetLastError(), "k_dense_gather_flat launch");
         return;
     }
     if (od == OutDtype::bf16) {

@@ -42,6 +42,12 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, 
                        void* out_indices, void* out_data, uint64_t* out_gidx, void* scratch,
                        cudaStream_t st);
 
+// K2 without the device scan: `prefix` (u64[n+1], exclusive nnz prefix of the
+// rows, prefix[0] arbitrary) is the host schedule's, and is the output indptr
+// when rebased to 0 (the loader uploads it straight into its indptr slot).
+void launch_csr_gather_prefixed(const ArenaView& a, const RowRef* refs, uint64_t n_rows, const uint64_t* prefix,
+                                void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st);
+
 // K1/K2 scan only: out_prefix[i] = exclusive nnz prefix of rows, out_prefix[n] = total.
 void launch_csr_row_scan(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t* out_prefix, void* scratch,
                          cudaStream_t st);

@@ -36,6 +36,7 @@ CASES = {  # store, kernel, rows per launch, out dtype, transform
     "densify_cfg1": ("cfg1", "densify", 4096, L.F32, L.XF_NONE),
     "densify_bf16_cfg1": ("cfg1", "densify", 4096, L.BF16, L.XF_NONE),
     "gather_cfg1": ("cfg1", "gather", 4096, None, None),
+    "gather_planned_cfg1": ("cfg1", "gather_planned", 4096, None, None),
     "densify_norm_cfg2": ("cfg2s", "densify", 4096, L.F32, L.XF_NORMALIZE_LOG1P),
     "dense_bf16_cfg3": ("cfg3s", "dense", 1024, L.BF16, None),
     "dense_raw_cfg4": ("cfg4s", "dense", 2048, L.NATIVE, None),
@@ -112,6 +113,18 @@ def run_case(name, K, W, dstores):
         o_dv = torch.empty(mx * vs + 16, dtype=torch.uint8, device="cuda")
         launch = lambda i: lib.rfl_csr_gather(C.byref(desc), d_refs[i].data_ptr(), rows, o_ip.data_ptr(),  # noqa
                                               o_ix.data_ptr(), o_dv.data_ptr(), gout.data_ptr(), sp)
+        alg = lambda i: nnz[i] * 2 * (isz + vs) + rows * (16 + 2 * isz + 16)  # noqa
+    elif kern == "gather_planned":  # indptr planned on the host (the loader's CSR path): one launch
+        mx = max(nnz)
+        pre = np.zeros((K + W, rows + 1), np.int64)
+        for i, g in enumerate(sets):
+            pre[i, 1:] = np.cumsum(rn[g.astype(np.int64)])
+        d_pre = torch.from_numpy(pre).cuda()
+        o_ix = torch.empty(mx * isz + 16, dtype=torch.uint8, device="cuda")
+        o_dv = torch.empty(mx * vs + 16, dtype=torch.uint8, device="cuda")
+        launch = lambda i: lib.rfl_csr_gather_prefixed(C.byref(desc), d_refs[i].data_ptr(), rows,  # noqa
+                                                       d_pre[i].data_ptr(), o_ix.data_ptr(), o_dv.data_ptr(),
+                                                       gout.data_ptr(), sp)
         alg = lambda i: nnz[i] * 2 * (isz + vs) + rows * (16 + 2 * isz + 16)  # noqa
     elif kern == "dense":
         rb = man.n_var * vs

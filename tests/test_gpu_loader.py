@@ -154,6 +154,16 @@ def test_raw_kernels_random_rows(golden_stores):
             assert (gx.astype(np.uint64) == ex).all()
             assert out_dv.cpu().numpy()[:ed.nbytes].tobytes() == ed.tobytes()
             assert (out_g.cpu().numpy().view(np.uint64) == g).all()
+            # host-planned indptr (no device scan), at a nonzero base entry
+            base = 5
+            pre = torch.from_numpy((ei.astype(np.int64) + base)).cuda()
+            out_ix2 = torch.zeros_like(out_ix)
+            out_dv2 = torch.zeros_like(out_dv)
+            out_g2 = torch.zeros_like(out_g)
+            L.check(L.lib().rfl_csr_gather_prefixed(C.byref(desc), refs.data_ptr(), n, pre.data_ptr(),
+                                                    out_ix2.data_ptr(), out_dv2.data_ptr(), out_g2.data_ptr(), None))
+            torch.cuda.synchronize()
+            assert torch.equal(out_ix2, out_ix) and torch.equal(out_dv2, out_dv) and torch.equal(out_g2, out_g)
             dense = torch.zeros(n * m["n_var"] * ed.itemsize, dtype=torch.uint8, device="cuda")
             L.check(L.lib().rfl_csr_densify(C.byref(desc), refs.data_ptr(), n, L.NATIVE, L.XF_NONE, 0.0,
                                             dense.data_ptr(), None, None))
