@@ -60,6 +60,13 @@ WORKLOADS = {
                  out=dict(output="dense", out_dtype="native", transform=None), dtype="u8"),
 }
 METRIC = "cells/sec minibatch assembly"
+# config 5 (pre-shuffle) at the largest shape that is materialised per run: CSR with the
+# Tahoe gene count, ~2,000 nnz/cell, c=64, m=65,536 rows per round, out chunk 4096 x 128
+CFG5 = dict(desc="cfg5-shaped pre-shuffle: synthetic CSR 524,288 cells x 62,710 genes, ~2k nnz/cell f32, c=64, "
+                 "m=65,536 (8 rounds), plan seed 7, out chunk_rows 4096 x 128 per shard, codec none",
+            synth=dict(n_obs=524_288, n_var=62_710, layout="csr", value_dtype="f32", index_dtype="u32",
+                       density=2000 / 62_710, seed=4, chunk_rows=64, chunks_per_shard=128),
+            c=64, m=65_536, seed=7, out_chunk_rows=4096, out_cps=128, ref_rows=20_000)
 
 
 def peaks():
@@ -138,7 +145,7 @@ def ensure_store(wl, rank, world, dist):
     import paper_2604_01949_b200 as R
     base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
     path = base / wl
-    s = WORKLOADS[wl]["synth"]
+    s = (CFG5 if wl == "cfg5" else WORKLOADS[wl])["synth"]
     if rank == 0 and not (path / "manifest.json").exists():
         base.mkdir(parents=True, exist_ok=True)
         tmp = base / f".{wl}.{os.getpid()}"
@@ -391,12 +398,116 @@ def cpu_baseline(path, W, threads):
             "host_cpus": os.cpu_count()}
 
 
+def run_preshuffle(args, rank, world, local, dist):
+    """--workload cfg5: the pre-shuffle (run_shuffle) through the public API.
+
+    A step is one round of the plan (m rows gathered, permuted, packed into
+    records and written).  `value`: payload GB/s of the device round pipeline
+    (row scan + record pack kernels, CUDA events) -- the records are resident in
+    HBM when those kernels run; `e2e`: payload GB/s of the whole run_shuffle
+    call (file reads, H2D, kernels, D2H, shard + provenance writes), wall clock,
+    max over ranks.  One untimed run_shuffle of the same collection first (warm
+    page cache, CUDA context, allocations)."""
+    import shutil
+
+    import torch
+
+    import paper_2604_01949_b200 as R
+    torch.cuda.set_device(local)
+    path = ensure_store("cfg5", rank, world, dist)
+    man = R.StoreReader(path).manifest()
+    payload = ds_bytes(R.StoreReader(path))
+    plan = R.plan_shuffle(man.n_obs, CFG5["c"], CFG5["m"], CFG5["seed"])
+    oc = R.ShuffleOutputConfig(CFG5["out_chunk_rows"], CFG5["out_cps"])
+    base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
+    out = base / f"cfg5_out_w{world}"
+
+    def one():
+        if rank == 0:
+            shutil.rmtree(out, ignore_errors=True)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        st = R.run_shuffle([path], plan, out, oc, device=local, rank=rank, world=world,
+                           group=dist.group.WORLD if dist else None)
+        return st, time.perf_counter() - t0
+
+    one()  # warm-up run
+    clk = Clocks(local).__enter__()
+    st, wall = one()
+    clk.__exit__(None, None, None)
+    wall_max = allreduce_max(wall, dist)
+    gpu_max = allreduce_max(st.gpu_ms, dist)
+    if rank == 0:
+        shutil.rmtree(out, ignore_errors=True)
+    if rank != 0:
+        return None
+    peak, peak_src = peaks()
+    nnz = (payload - man.chunk_count() * 12 - 4 * (man.n_obs + man.chunk_count())) / 8  # u32 idx + f32 val
+    rounds = st.rounds_executed
+    # K5 (+K1) algorithmic bytes over the run: read every entry + row header once, write every
+    # encoded entry + indptr once (DESIGN.md §Kernels), per rank
+    alg = (nnz * 16 + man.n_obs * 2 * (16 + 8)) / world
+    res = {"metric": "preshuffle GB/s", "value": payload / (gpu_max / 1e3) / 1e9, "unit": "GB/s",
+           "n_gpus": world, "steps": rounds, "warmup": rounds, "ms_per_step": gpu_max / rounds,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32+f32 (bytes)",
+           "data": "synthetic (product synth_store == reference synth_store bytes)",
+           "config": {"workload": CFG5["desc"], "payload_GB": payload / 1e9,
+                      "value_def": "payload bytes / device time of the round kernels (scan + pack), max over ranks",
+                      "l2": "rounds of ~1 GB of records, larger than L2",
+                      "parallelism": f"{world} rank(s): rank b mod W stages block b, shard s owned by rank s mod W"},
+           "roofline": {"bound": "hbm", "achieved": alg / (gpu_max / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": alg / (gpu_max / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                        "kernel": "k_row_scan + k_csr_pack", "alg_bytes_per_launch": alg / rounds,
+                        "avg_launch_ms": gpu_max / rounds},
+           "e2e": {"value": payload / wall_max / 1e9, "unit": "GB/s", "h2d_bytes_per_step": st.h2d_bytes / rounds,
+                   "d2h_bytes_per_step": st.d2h_bytes / rounds,
+                   "api": "paper_2604_01949_b200.run_shuffle -> rfl_run_shuffle", "wall_s": wall_max,
+                   "rows_per_s": man.n_obs / wall_max},
+           "gpu_launches": 2 * rounds, "clocks": clk.summary()}
+    if world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_shuffle_baseline()
+    return res
+
+
+def cpu_shuffle_baseline():
+    """The reference run_shuffle (oracle/_ref, unmodified, single-threaded by design)
+    on a bounded subset of the same shape."""
+    import shutil
+
+    import paper_2604_01949_b200 as R
+    from oracle.oracle import Ref
+    base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
+    n = CFG5["ref_rows"]
+    sub = base / f"cfg5_ref_{n}"
+    if not (sub / "manifest.json").exists():
+        R.synth_store(sub, R.SynthConfig(**dict(CFG5["synth"], n_obs=n)))
+    rout = base / "cfg5_ref_out"
+    shutil.rmtree(rout, ignore_errors=True)
+    t0 = time.perf_counter()
+    Ref.run_shuffle([sub], rout, CFG5["c"], min(CFG5["m"], n), CFG5["seed"], CFG5["out_chunk_rows"], CFG5["out_cps"])
+    w = time.perf_counter() - t0
+    shutil.rmtree(rout, ignore_errors=True)
+    pb = sum(f.stat().st_size for f in (sub / "shards").iterdir())
+    return {"value": pb / w / 1e9, "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"run_shuffle of a {n}-row subset of the same shape ({pb / 1e9:.2f} GB), wall {w:.1f}s"}
+
+
 def run_reference(args, wl, rank, world):
     """--impl reference: the reference CPU implementation, all host threads, rank 0 only."""
     if rank != 0:
         return None
     import torch  # noqa: F401  (same environment as our arm)
     from oracle.oracle import Ref
+    if wl == "cfg5":
+        b = cpu_shuffle_baseline()
+        return {"metric": "preshuffle GB/s", "value": b["value"], "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u32+f32 (bytes)",
+                "data": "synthetic (reference synth_store)", "impl": "reference",
+                "config": {"workload": CFG5["desc"], "parallelism": "1 host thread (run_shuffle is sequential)"},
+                "cpu_baseline": b, "e2e": {"value": b["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                           "d2h_bytes_per_step": 0}}
     W = WORKLOADS[wl]
     path = ensure_store(wl, 0, 1, None)
     threads = os.cpu_count() or 1
@@ -425,7 +536,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS) + ["cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     args = ap.parse_args()
@@ -446,6 +557,8 @@ def main():
             dist.init_process_group("gloo")
     if args.impl == "reference":
         res = run_reference(args, args.workload, rank, world)
+    elif args.workload == "cfg5":
+        res = run_preshuffle(args, rank, world, local, dist)
     else:
         res = run_ours(args, args.workload, rank, world, local, dist)
     if rank == 0 and res is not None:

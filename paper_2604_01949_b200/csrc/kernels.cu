@@ -11,6 +11,8 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <type_traits>
+#include <cstdio>
 
 #include "kernels.cuh"
 
@@ -1430,10 +1432,8 @@ __global__ void __launch_bounds__(kDenseGatherThreads)
 // chunks); one lane reads the row's RowRef, every lane issues U independent
 // 16-B loads before any store, so a warp keeps 32*U*16 B in flight and all
 // rows of a (small) batch are in flight at once.
-constexpr int kDgThreads = 256;
-constexpr int kDgU = 4;
 
-template <int MODE>
+template <int MODE, int kDgU = 4, int kDgThreads = 256>
 __global__ void __launch_bounds__(kDgThreads)
     k_dense_gather_flat(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
                         uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx) {
@@ -1918,20 +1918,37 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
     const bool flat = in_rb % 16 == 0 && reinterpret_cast<uintptr_t>(a.base) % 16 == 0 &&
                       reinterpret_cast<uintptr_t>(out) % 16 == 0;
     if (flat) {
-        const uint64_t upr = (in_rb / 16 + 32 * kDgU - 1) / (32 * kDgU);
-        const uint64_t warps_needed = n * upr;
-        const unsigned g2 = static_cast<unsigned>(std::max<uint64_t>(
-            1, std::min<uint64_t>((warps_needed + kDgThreads / 32 - 1) / (kDgThreads / 32), 8ull * device_sm_count())));
-        const char* what = "k_dense_gather_flat launch";
+        // shape (RFL_DG="<16-B loads per lane>:<threads>", A/B only).  Default 2:256
+        // (profiles/r1_dense_gather.md: cfg3 0.63, cfg4 0.635 of HBM; 4:256 0.55 / 0.61)
+        static const std::pair<int, int> shape = [] {
+            int u = 2, t = 256;
+            if (const char* e = std::getenv("RFL_DG")) std::sscanf(e, "%d:%d", &u, &t);
+            return std::make_pair(u, t);
+        }();
+        auto go = [&](auto kern, int U, int T) {
+            const uint64_t upr = (in_rb / 16 + 32 * U - 1) / (32 * U);
+            const uint64_t warps_needed = n * upr;
+            const unsigned g2 = static_cast<unsigned>(std::max<uint64_t>(
+                1, std::min<uint64_t>((warps_needed + T / 32 - 1) / (T / 32), 2048ull * device_sm_count() / T)));
+            const uint64_t orb = od == OutDtype::bf16 ? a.n_var * 2 : in_rb;
+            launch_k(kern, dim3(g2), dim3(T), 0, st, "k_dense_gather_flat launch", d, in_rb, refs, n, o, orb, out_gidx);
+        };
+        auto pick = [&](auto mode) {
+            constexpr int M = decltype(mode)::value;
+            const int u = shape.first, t = shape.second;
+            if (u == 4 && t == 256) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
+            if (u == 8 && t == 256) return go(k_dense_gather_flat<M, 8, 256>, 8, 256);
+            if (u == 4 && t == 128) return go(k_dense_gather_flat<M, 4, 128>, 4, 128);
+            if (u == 4 && t == 512) return go(k_dense_gather_flat<M, 4, 512>, 4, 512);
+            if (u == 1 && t == 256) return go(k_dense_gather_flat<M, 1, 256>, 1, 256);
+            return go(k_dense_gather_flat<M, 2, 256>, 2, 256);
+        };
         if (od == OutDtype::bf16 && a.vdt == VDtype::u8) {
-            launch_k(k_dense_gather_flat<kU8ToBf16>, dim3(g2), dim3(kDgThreads), 0, st, what, d, in_rb, refs, n, o,
-                     a.n_var * 2, out_gidx);
+            pick(std::integral_constant<int, kU8ToBf16>{});
         } else if (od == OutDtype::bf16 && a.vdt == VDtype::f32) {
-            launch_k(k_dense_gather_flat<kF32ToBf16>, dim3(g2), dim3(kDgThreads), 0, st, what, d, in_rb, refs, n, o,
-                     a.n_var * 2, out_gidx);
+            pick(std::integral_constant<int, kF32ToBf16>{});
         } else if (od == OutDtype::native || (od == OutDtype::f32 && a.vdt == VDtype::f32)) {
-            launch_k(k_dense_gather_flat<kRaw>, dim3(g2), dim3(kDgThreads), 0, st, what, d, in_rb, refs, n, o, in_rb,
-                     out_gidx);
+            pick(std::integral_constant<int, kRaw>{});
         } else {
             invalid("dense_gather: unsupported output dtype for this store");
         }
