@@ -288,6 +288,26 @@ ArenaView DStore::view(const uint8_t* base) const {
     return a;
 }
 
+void DStore::reserve_slots(uint64_t bytes, uint64_t n) {
+    release_slot(acquire_slot(bytes));  // adopts the slot geometry
+    std::lock_guard<std::mutex> lk(mu_);
+    while (free_.size() < n) grow_slab();
+}
+
+void DStore::grow_slab() {
+    const uint64_t n = 32;
+    void* slab = nullptr;
+    cuda_ok(cudaMalloc(&slab, n * slot_bytes_ + kPad), "cudaMalloc slab");
+    slabs_.push_back(slab);
+    for (uint64_t i = 0; i < n; ++i) {
+        SlotRef s;
+        s.ptr = static_cast<uint8_t*>(slab) + i * slot_bytes_;
+        s.bytes = slot_bytes_;
+        cuda_ok(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming), "event");
+        free_.push_back(s);
+    }
+}
+
 DStore::SlotRef DStore::acquire_slot(uint64_t bytes) {
     std::lock_guard<std::mutex> lk(mu_);
     if (bytes > slot_bytes_) {  // first use (or a bigger block geometry): new pool
@@ -296,19 +316,7 @@ DStore::SlotRef DStore::acquire_slot(uint64_t bytes) {
         free_.clear();
         slot_bytes_ = align_up(std::max<uint64_t>(bytes, 1), 256);
     }
-    if (free_.empty()) {  // grow by a slab of slots
-        const uint64_t n = 32;
-        void* slab = nullptr;
-        cuda_ok(cudaMalloc(&slab, n * slot_bytes_ + kPad), "cudaMalloc slab");
-        slabs_.push_back(slab);
-        for (uint64_t i = 0; i < n; ++i) {
-            SlotRef s;
-            s.ptr = static_cast<uint8_t*>(slab) + i * slot_bytes_;
-            s.bytes = slot_bytes_;
-            cuda_ok(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming), "event");
-            free_.push_back(s);
-        }
-    }
+    if (free_.empty()) grow_slab();
     SlotRef s = free_.back();
     free_.pop_back();
     return s;
@@ -456,6 +464,10 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     if (ds_->staging() != kResident) {
         live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
         block_bytes_ = ds_->max_block_bytes(cfg_.f);
+        // live blocks peak at ~5x B/f (cfg1 318 for B/f = 64, cfg4 230 for 32)
+        const uint64_t nb = (m.n_obs + cfg_.f - 1) / cfg_.f;
+        const uint64_t want = std::min<uint64_t>(nb, 6 * ((cfg_.B + cfg_.f - 1) / cfg_.f) + 32);
+        ds_->reserve_slots(block_bytes_, std::min<uint64_t>(want, (8ull << 30) / std::max<uint64_t>(block_bytes_, 1)));
         if (ds_->staging() == kStreamFile) {
             const uint32_t threads = std::min<uint32_t>(16, std::max<uint32_t>(1, cfg_.prefetch_depth));
             reader_ = std::make_unique<BlockReader>(ds_, replay_.plan(), cfg_.f, threads, 2 * threads + 2,

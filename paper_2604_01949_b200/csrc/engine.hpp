@@ -65,6 +65,9 @@ public:
         uint64_t bytes = 0;
     };
     SlotRef acquire_slot(uint64_t bytes);
+    // grow the pool (slot geometry `bytes`) until it holds >= n free slots, so a
+    // steady-state epoch never allocates (cudaMalloc stalls the device)
+    void reserve_slots(uint64_t bytes, uint64_t n);
     void release_slot(const SlotRef& s);
 
 private:
@@ -79,6 +82,7 @@ private:
     uint8_t* d_arena_ = nullptr;
     uint8_t* h_image_ = nullptr;
     std::mutex mu_;
+    void grow_slab();  // mu_ held
     std::vector<void*> slabs_;
     std::vector<SlotRef> free_;
     uint64_t slot_bytes_ = 0;

@@ -732,6 +732,101 @@ __global__ void __launch_bounds__(THREADS, MINB)
     if (bulk && tid == 0) bulk_wait0();
 }
 
+// v9: v6 with the CTA's row lookups hoisted out of the row loop: warp 0
+// resolves 32 rows lane-parallel up front instead of thread 0 walking one
+// ref -> header -> indptr chain per row ahead of the tile barriers.
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_csr_densify9(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
+                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ double s_red[THREADS / 32];
+    __shared__ RowDesc s_desc[32];  // this CTA's rows k0 .. k0+31 (row = blockIdx.x + k * gridDim.x)
+    const uint32_t tid = threadIdx.x;
+    constexpr uint32_t nthr = THREADS;
+    const uint64_t n_var = a.n_var;
+    const uint64_t g = gridDim.x;
+    pdl_wait();
+    pdl_trigger();
+    // warp 0 resolves the CTA's next 32 rows lane-parallel (ref -> header ->
+    // indptr, one dependent chain for all of them) and writes their gidx
+    auto describe32 = [&](uint64_t k0) {
+        if (tid < 32) {
+            const uint64_t row = blockIdx.x + (k0 + tid) * g;
+            if (row < n_rows) {
+                const RowDesc rd = describe_row<IdxT>(a, refs[row], sizeof(SrcT));
+                s_desc[tid] = rd;
+                if (out_gidx) out_gidx[row] = rd.gidx;
+            }
+        }
+    };
+    describe32(0);
+    __syncthreads();
+    uint32_t colA[U], colB[U];
+    SrcT vA[U], vB[U];
+    if (blockIdx.x < n_rows) load_entries<IdxT, SrcT, U>(s_desc[0], tid, nthr, colA, vA);
+    uint64_t kk = 0;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += g, ++kk) {
+        const RowDesc d = s_desc[kk & 31];
+        const bool has_next = row + g < n_rows;
+        if (has_next && ((kk + 1) & 31) == 0) {  // CTAs with > 32 rows: next batch of descriptors
+            __syncthreads();
+            describe32(kk + 1);
+            __syncthreads();
+        }
+        if (has_next) load_entries<IdxT, SrcT, U>(s_desc[(kk + 1) & 31], tid, nthr, colB, vB);  // row i+1 in flight
+        float scale = 1.0f;
+        if (norm) {  // library size in fp64
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (colA[u] != ~0u) s += static_cast<double>(vA[u]);
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr)
+                s += static_cast<double>(ld_value<SrcT>(d.val + k * sizeof(SrcT)));
+            s = block_sum(s, s_red);
+            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
+        }
+        DstT* orow = out + row * n_var;
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+            const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
+            const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
+            DstT* tile = reinterpret_cast<DstT*>(smem);
+            if (bulk && tid == 0) bulk_wait_read0();
+            __syncthreads();
+            uint4* t4 = reinterpret_cast<uint4*>(smem);
+            for (uint32_t i = tid; i < bytes / 16u; i += nthr) t4[i] = make_uint4(0, 0, 0, 0);
+            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) smem[i] = 0;
+            __syncthreads();
+            const uint32_t c0u = static_cast<uint32_t>(c0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (colA[u] - c0u < cols) tile[colA[u] - c0u] = Conv<DstT, SrcT>::go(vA[u], scale, norm);
+            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr) {  // rows longer than U*THREADS
+                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
+                if (c2 >= c0 && c2 - c0 < cols)
+                    tile[c2 - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(d.val + k * sizeof(SrcT)), scale, norm);
+            }
+            if (bulk) {
+                fence_proxy_async_shared();
+                __syncthreads();
+                if (tid == 0) {
+                    bulk_store(orow + c0, smem, bytes);
+                    bulk_commit();
+                }
+            } else {
+                __syncthreads();
+                for (uint32_t i = tid; i < cols; i += nthr) orow[c0 + i] = tile[i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            colA[u] = colB[u];
+            vA[u] = vB[u];
+        }
+    }
+    if (bulk && tid == 0) bulk_wait0();
+}
+
 // v8: v6 with the per-tile zero fill replaced by un-scattering the stored
 // tile's own entries (smem writes per tile ~ entries instead of tile bytes).
 template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB>
@@ -1537,7 +1632,7 @@ const DensifyCfg& densify_cfg() {
         if (e && e[0] == 'v') {
             int v = 2, t = 512, kb = 100, u = 8, mb = 4;
             char st = 't';
-            if (std::sscanf(e, "v%d", &v) == 1 && (v == 6 || v == 8)) {
+            if (std::sscanf(e, "v%d", &v) == 1 && (v == 6 || v == 8 || v == 9)) {
                 const int got = std::sscanf(e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
                 d.version = v;
                 if (got >= 1) d.threads = t;
@@ -1557,7 +1652,7 @@ const DensifyCfg& densify_cfg() {
     return c;
 }
 
-template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB, bool UNS = false>
+template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB, int VAR = 6>
 void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                 uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes) {
     const uint64_t esz = sizeof(DstT);
@@ -1566,7 +1661,8 @@ void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, 
     const size_t smem = (tile_cols * esz + 127) & ~127ull;
     const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     auto kern = [] {
-        if constexpr (UNS) return k_csr_densify8<IdxT, SrcT, DstT, THREADS, U, MINB>;
+        if constexpr (VAR == 8) return k_csr_densify8<IdxT, SrcT, DstT, THREADS, U, MINB>;
+        else if constexpr (VAR == 9) return k_csr_densify9<IdxT, SrcT, DstT, THREADS, U, MINB>;
         else return k_csr_densify6<IdxT, SrcT, DstT, THREADS, U, MINB>;
     }();
     set_smem(kern, smem);
@@ -1601,22 +1697,37 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
                uint64_t* out_gidx, cudaStream_t st, uint64_t avg_nnz) {
     const DensifyCfg& dc = densify_cfg();
     if (dc.version == 0) {
-        // Default (profiles/r1_densify_v6.md): every row entry of a typical row
-        // in registers.  Rows up to ~2.5k entries (and <= 96 KB dense): 8 per
-        // thread, 40 KB tiles, 3 CTAs/SM (cfg1: 0.78 of measured HBM); longer or
-        // wider rows: 16 per thread, 80 KB tiles, 2 CTAs/SM (cfg2: 0.80).
-        const bool big = avg_nnz > 2560 || (avg_nnz == 0 && av.n_var * sizeof(DstT) > 96 * 1024);
-        if (big) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2>(av, refs, n, norm, target, out, out_gidx, st, 80 << 10);
-        return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, 40 << 10);
+        // Default (profiles/r1_densify_v9.md): v9 (lane-parallel row lookups, two rows
+        // of entries in registers).  Dense rows wider than 48 KB: 16 entries per
+        // thread, 80 KB tiles, 2 CTAs/SM (cfg1 f32 0.885, cfg2 norm+log1p 0.888 of
+        // measured HBM); narrower rows (e.g. cfg1 -> bf16, 40 KB): 8 per thread,
+        // 40 KB tiles, 3 CTAs/SM (0.81), so a row still fills its tile.
+        (void)avg_nnz;
+        const bool wide = av.n_var * sizeof(DstT) > 48 * 1024;
+        if constexpr (sizeof(IdxT) == 4) {
+            if (wide) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, 80 << 10);
+            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, 40 << 10);
+        } else {  // u64 indices: the v6 register budget
+            if (wide) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2>(av, refs, n, norm, target, out, out_gidx, st, 80 << 10);
+            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, 40 << 10);
+        }
     }
     if constexpr (sizeof(IdxT) == 4 && sizeof(SrcT) == 4) {
+        if (dc.version == 9) {  // v6 + lane-parallel row lookups
+            const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
+            if (dc.u == 16)
+                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.minb == 4)
+                return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        }
         if (dc.version == 8) {  // v6 + un-scatter
             const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
             if (dc.u == 16)
-                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, true>(av, refs, n, norm, target, out, out_gidx, st, tb);
+                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
             if (dc.minb == 4)
-                return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, true>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, true>(av, refs, n, norm, target, out, out_gidx, st, tb);
+                return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
         }
         if (dc.version == 6) {  // A/B set: u32 indices, 4-byte values
             const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
