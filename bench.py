@@ -326,10 +326,11 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
 
     import paper_2604_01949_b200 as R
     K, Wm = args.steps, args.warmup
-    ds = R.DeviceStore(reader, local, "stream_pinned")
+    staging = os.environ.get("RIFFLE_E2E_STAGING", "stream_pinned")  # or stream_file (page cache / O_DIRECT reads)
+    ds = R.DeviceStore(reader, local, staging)
     stream = torch.cuda.current_stream()
     epoch = 0
-    cfg = R.LoaderConfig(**W["loader"], prefetch_depth=4, rank=rank, world=world)
+    cfg = R.LoaderConfig(**W["loader"], prefetch_depth=int(os.environ.get("RIFFLE_E2E_DEPTH", "4")), rank=rank, world=world)
 
     def make_it(e):
         return R.BatchIterator(ds, cfg, e, output=W["out"]["output"], out_dtype=W["out"]["out_dtype"],
@@ -377,7 +378,10 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
     ds.close()
     return {"value": world * cells / (t_max / 1e3), "unit": "cells/s",
             "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": 8 * cells / K,
-            "staging": "stream_pinned (records in pinned host RAM; blocks cudaMemcpyAsync'd per fetch)",
+            "staging": ("stream_pinned (records in pinned host RAM; blocks cudaMemcpyAsync'd per fetch)"
+                        if staging == "stream_pinned" else
+                        "stream_file (BlockReader: prefetch_depth I/O threads pread the fetch order from the shard "
+                        "files into pinned buffers; blocks cudaMemcpyAsync'd per fetch)"),
             "api": "paper_2604_01949_b200.BatchIterator.next -> rfl_loader_next",
             "gpu_launches": K}
 

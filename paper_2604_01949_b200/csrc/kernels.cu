@@ -1119,6 +1119,7 @@ struct TcGen {
     const uint64_t* P;
     uint64_t n_rows, p0, e0, e1, r;
     uint8_t* out;
+    uint64_t cr;  // > 0: K5 mode, rows land in encoded chunk records of cr rows
     uint32_t es, vs, lane, act, k;
     bool is_val, more;
     uint64_t pl, ph, avail, pos;
@@ -1169,6 +1170,14 @@ struct TcGen {
                 continue;
             }
             uint8_t* dst = out + s * es;
+            if (cr) {  // record q = row / cr starts at q*(12 + es_i*(cr+1)) + (es_i+vs)*P[q*cr] (k_csr_pack)
+                const uint64_t row = r + k, q = row / cr, r0 = q * cr, rows_q = umin64(cr, n_rows - r0);
+                const uint64_t p0q = P[r0] - p0, nnz_q = P[r0 + rows_q] - P[r0];
+                const uint64_t is_ = sizeof(IdxT);
+                uint8_t* rec = out + q * (kCsrHeaderBytes + is_ * (cr + 1)) + (is_ + vs) * p0q;
+                uint8_t* ibase = rec + kCsrHeaderBytes + is_ * (rows_q + 1);
+                dst = (is_val ? ibase + is_ * nnz_q : ibase) + (s - p0q) * es;
+            }
             const uint64_t room = kTcPiece - (reinterpret_cast<uintptr_t>(dst) & 15u);
             const uint64_t len = umin64((lim - s) * es, room);
             const uint8_t* ks =
@@ -1213,7 +1222,7 @@ template <typename IdxT>
 __global__ void __launch_bounds__(kTcThreads)
     k_csr_copy_tma(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, const RowJob* __restrict__ jobs,
                    const uint64_t* __restrict__ P, uint64_t n_rows, uint32_t w_idx, uint8_t* __restrict__ out_idx,
-                   uint8_t* __restrict__ out_val, uint64_t* __restrict__ out_gidx) {
+                   uint8_t* __restrict__ out_val, uint64_t* __restrict__ out_gidx, uint64_t cr) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t s_bar[kTcWarps][2];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -1235,6 +1244,23 @@ __global__ void __launch_bounds__(kTcThreads)
         for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kTcThreads + threadIdx.x; i < n_rows;
              i += static_cast<uint64_t>(gridDim.x) * kTcThreads)
             out_gidx[i] = refs[i].gidx;
+    if (cr) {  // K5 mode: record headers + rebased indptr entries (encode_csr_record, store.cpp:52-64)
+        constexpr uint64_t os = sizeof(IdxT);
+        const uint64_t pb = P[0];
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kTcThreads + threadIdx.x; i < n_rows;
+             i += static_cast<uint64_t>(gridDim.x) * kTcThreads) {
+            const uint64_t q = i / cr, r0 = q * cr, rows_q = umin64(cr, n_rows - r0);
+            const uint64_t p0q = P[r0];
+            uint8_t* rec = out_idx + q * (kCsrHeaderBytes + os * (cr + 1)) + (os + vs) * (p0q - pb);
+            uint8_t* ip = rec + kCsrHeaderBytes;
+            if (i == r0) {
+                st_any<uint32_t>(rec, static_cast<uint32_t>(rows_q));
+                st_any<uint64_t>(rec + 4, P[r0 + rows_q] - p0q);
+                st_any<IdxT>(ip, IdxT(0));
+            }
+            st_any<IdxT>(ip + os * (i - r0 + 1), static_cast<IdxT>(P[i + 1] - p0q));
+        }
+    }
     const bool is_val = gw >= w_idx;
     const uint32_t es = is_val ? vs : static_cast<uint32_t>(sizeof(IdxT));
     const uint32_t nw = is_val ? n_warps - w_idx : w_idx, w = is_val ? gw - w_idx : gw;
@@ -1268,6 +1294,7 @@ __global__ void __launch_bounds__(kTcThreads)
     gen.e1 = e1;
     gen.r = lo;
     gen.out = is_val ? out_val : out_idx;
+    gen.cr = cr;
     gen.es = es;
     gen.vs = vs;
     gen.lane = lane;
@@ -1715,6 +1742,14 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
     if constexpr (sizeof(IdxT) == 4 && sizeof(SrcT) == 4) {
         if (dc.version == 9) {  // v6 + lane-parallel row lookups
             const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
+            if (dc.threads == 128 && dc.u == 16 && dc.minb == 4)
+                return densify_v6<IdxT, SrcT, DstT, 128, 16, 4, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.threads == 128 && dc.u == 16)
+                return densify_v6<IdxT, SrcT, DstT, 128, 16, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.threads == 128)
+                return densify_v6<IdxT, SrcT, DstT, 128, 8, 6, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.threads == 512)
+                return densify_v6<IdxT, SrcT, DstT, 512, 4, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
             if (dc.u == 16)
                 return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
             if (dc.minb == 4)
@@ -1837,8 +1872,9 @@ bool gather_tma() {
 }
 
 void launch_copy_flat(const ArenaView& a, uint32_t vs, const RowRef* refs, const RowJob* jobs, const uint64_t* P,
-                      uint64_t n, void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st) {
-    if (gather_tma()) {
+                      uint64_t n, void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st,
+                      uint64_t cr = 0) {
+    if (gather_tma() || cr) {
         auto kern = a.idt == IDtype::u32 ? k_csr_copy_tma<uint32_t> : k_csr_copy_tma<uint64_t>;
         const size_t smem = 2 * kTcStage * kTcWarps;
         static int per_sm[2] = {0, 0};
@@ -1852,7 +1888,7 @@ void launch_copy_flat(const ArenaView& a, uint32_t vs, const RowRef* refs, const
         const uint32_t is = static_cast<uint32_t>(index_size(a.idt));
         const uint32_t w_idx = std::max(1u, std::min(n_warps - 1, (n_warps * is + (is + vs) / 2) / (is + vs)));
         launch_k(kern, dim3(blocks), dim3(kTcThreads), smem, st, "k_csr_copy_tma launch", dev_view(a), vs, refs, jobs,
-                 P, n, w_idx, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data), out_gidx);
+                 P, n, w_idx, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data), out_gidx, cr);
         return;
     }
     auto kern = a.idt == IDtype::u32 ? k_csr_copy_flat<uint32_t> : k_csr_copy_flat<uint64_t>;
@@ -1917,6 +1953,12 @@ void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_
     if (a.layout != Layout::csr) invalid("csr_pack: store is not csr");
     if (n == 0) return;
     const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
+    static const bool legacy = [] {
+        const char* e = std::getenv("RFL_PACK");
+        return e && std::string(e) == "warp";
+    }();
+    if (a.idt == out_idt && !legacy)  // byte-identical index width: the balanced TMA copy in record mode
+        return launch_copy_flat(a, vs, refs, nullptr, prefix, n, out, out, nullptr, st, chunk_rows);
     const unsigned grid =
         static_cast<unsigned>(std::min<uint64_t>((n + kPackThreads / 32 - 1) / (kPackThreads / 32), 16ull * device_sm_count()));
     const ArenaDev d = dev_view(a);

@@ -32,6 +32,7 @@ STORES = {
     "cfg5s": dict(n_obs=65_536, n_var=62_710, layout="csr", value_dtype="f32", density=2000 / 62710, seed=4,
                   chunk_rows=64),
 }
+FULL_ROWS = {"cfg3s": 2_000_000, "cfg4s": 5_000_000}  # KB_FULL=1: BASELINE row counts (24.6 / 20.5 GB)
 CASES = {  # store, kernel, rows per launch, out dtype, transform
     "densify_cfg1": ("cfg1", "densify", 4096, L.F32, L.XF_NONE),
     "densify_bf16_cfg1": ("cfg1", "densify", 4096, L.BF16, L.XF_NONE),
@@ -54,11 +55,14 @@ def peak():
 
 def store(name):
     base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
-    path = base / f"kb_{name}"
+    full = os.environ.get("KB_FULL") and name in FULL_ROWS  # the BASELINE-sized dense stores
+    path = base / (f"kb_{name}_full" if full else f"kb_{name}")
     if not (path / "manifest.json").exists():
         base.mkdir(parents=True, exist_ok=True)
         t = time.time()
         s = dict(STORES[name])
+        if full:
+            s["n_obs"] = FULL_ROWS[name]
         R.synth_store(path, R.SynthConfig(**s))
         print(f"# synth {name}: {time.time() - t:.1f}s", file=sys.stderr)
     return path
@@ -85,6 +89,10 @@ def run_case(name, K, W, dstores):
     desc = ds.arena_desc()
     rng = np.random.default_rng(0)
     sets = [rng.choice(man.n_obs, rows, replace=False).astype(np.uint64) for _ in range(K + W)]
+    if os.environ.get("KB_SCHED"):  # row sets = consecutive batches of the loader's own schedule
+        f = man.chunk_rows
+        it = iter(R.EpochSchedule(man.n_obs, R.LoaderConfig(f, max(16384, rows), rows, 0), 0))
+        sets = [next(it).astype(np.uint64) for _ in range(K + W)]
     refs = np.zeros((K + W, rows, 2), np.uint64)
     for i, g in enumerate(sets):
         refs[i, :, 0] = offs[g.astype(np.int64) // man.chunk_rows]
