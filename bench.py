@@ -482,7 +482,7 @@ def cpu_shuffle_baseline():
     import paper_2604_01949_b200 as R
     from oracle.oracle import Ref
     base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
-    n = CFG5["ref_rows"]
+    n = int(os.environ.get("RIFFLE_CFG5_REF_ROWS", CFG5["ref_rows"]))
     sub = base / f"cfg5_ref_{n}"
     if not (sub / "manifest.json").exists():
         R.synth_store(sub, R.SynthConfig(**dict(CFG5["synth"], n_obs=n)))
