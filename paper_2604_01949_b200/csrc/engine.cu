@@ -604,13 +604,7 @@ bool GpuLoader::next(BatchOut& out) {
         batch_src_.clear();
         batch_size_.clear();
         for (uint64_t id : consumed_) stage_block(id);
-        static const bool pull = [] {
-            const char* e = std::getenv("RFL_PULL");
-            return e && e[0] == '1';
-        }();
-        if (!batch_dst_.empty() && pull) {
-            launch_pull_copy(batch_dst_.data(), batch_src_.data(), batch_size_.data(), batch_dst_.size(), copy_);
-        } else if (!batch_dst_.empty()) {
+        if (!batch_dst_.empty()) {
             cudaMemcpyAttributes attr{};
             attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
             attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;

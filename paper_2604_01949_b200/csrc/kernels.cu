@@ -2071,13 +2071,16 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
     const bool flat = in_rb % 16 == 0 && reinterpret_cast<uintptr_t>(a.base) % 16 == 0 &&
                       reinterpret_cast<uintptr_t>(out) % 16 == 0;
     if (flat) {
-        // shape (RFL_DG="<16-B loads per lane>:<threads>", A/B only).  Default 2:256
-        // (profiles/r1_dense_gather.md: cfg3 0.63, cfg4 0.635 of HBM; 4:256 0.55 / 0.61)
+        // shape (RFL_DG="<16-B loads per lane>:<threads>", A/B only; profiles/r1_dense_gather.md)
         static const std::pair<int, int> shape = [] {
-            int u = 2, t = 256;
+            int u = 0, t = 256;  // u = 0: automatic
             if (const char* e = std::getenv("RFL_DG")) std::sscanf(e, "%d:%d", &u, &t);
             return std::make_pair(u, t);
         }();
+        // automatic = 2 loads per lane: measured best for both dense shapes; a
+        // one-wave unit size (3 for cfg3) is slower (0.58 vs 0.62), shorter
+        // per-warp chains win over filling the tail wave
+        const int u_auto = 2;
         auto go = [&](auto kern, int U, int T) {
             const uint64_t upr = (in_rb / 16 + 32 * U - 1) / (32 * U);
             const uint64_t warps_needed = n * upr;
@@ -2088,7 +2091,9 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         };
         auto pick = [&](auto mode) {
             constexpr int M = decltype(mode)::value;
-            const int u = shape.first, t = shape.second;
+            const int u = shape.first ? shape.first : u_auto, t = shape.second;
+            if (u == 3 && t == 256) return go(k_dense_gather_flat<M, 3, 256>, 3, 256);
+            if (u == 6 && t == 256) return go(k_dense_gather_flat<M, 6, 256>, 6, 256);
             if (u == 4 && t == 256) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
             if (u == 8 && t == 256) return go(k_dense_gather_flat<M, 8, 256>, 8, 256);
             if (u == 4 && t == 128) return go(k_dense_gather_flat<M, 4, 128>, 4, 128);
@@ -2122,70 +2127,4 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
     cuda_check(cudaGetLastError(), "k_dense_gather launch");
 }
 
-}  // namespace rfl
-
-// ===================================================== host -> HBM pull copy ===
-// Stages pinned-host blocks by SM loads over PCIe instead of the copy engine
-// (RFL_PULL=1, A/B): pinned memory is device-addressable under UVA, so a few
-// CTAs with many 16-B loads in flight read the blocks at the link rate
-// whatever the transfer size (the DMA engine pays a per-transfer cost on
-// ~1 MB blocks).
-namespace rfl {
-namespace {
-constexpr int kPullThreads = 256;
-constexpr int kPullSplit = 16;  // pieces per job
-struct PullJobs {
-    uint32_t n;
-    uint8_t* dst[kMaxPullJobs];
-    const uint8_t* src[kMaxPullJobs];
-    uint64_t bytes[kMaxPullJobs];
-};
-
-__global__ void __launch_bounds__(kPullThreads) k_pull_copy(const __grid_constant__ PullJobs jobs) {
-    const uint32_t total = jobs.n * kPullSplit;
-    for (uint32_t w = blockIdx.x; w < total; w += gridDim.x) {
-        const uint32_t j = w / kPullSplit, p = w % kPullSplit;
-        const uint64_t bytes = jobs.bytes[j];
-        const uint64_t piece = ((bytes + kPullSplit - 1) / kPullSplit + 15) & ~15ull;
-        const uint64_t b0 = p * piece, b1 = umin64(b0 + piece, bytes);
-        if (b0 >= b1) continue;
-        const uint8_t* s = jobs.src[j];
-        uint8_t* d = jobs.dst[j];
-        const uint64_t v0 = b0 / 16, v1 = b1 / 16;  // b0 is 16-B aligned; tail bytes below
-        const uint4* s4 = reinterpret_cast<const uint4*>(s);
-        uint4* d4 = reinterpret_cast<uint4*>(d);
-        constexpr int U = 4;
-        for (uint64_t base = v0 + threadIdx.x; base < v1; base += U * kPullThreads) {
-            uint4 v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (base + u * kPullThreads < v1) v[u] = ld_v4(s4 + base + u * kPullThreads);
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (base + u * kPullThreads < v1) st_v4(d4 + base + u * kPullThreads, v[u]);
-        }
-        for (uint64_t i = v1 * 16 + threadIdx.x; i < b1; i += kPullThreads) d[i] = s[i];
-    }
-}
-}  // namespace
-
-void launch_pull_copy(void* const* dst, const void* const* src, const size_t* bytes, size_t n, cudaStream_t st) {
-    for (size_t k0 = 0; k0 < n; k0 += kMaxPullJobs) {
-        PullJobs jobs{};
-        jobs.n = static_cast<uint32_t>(std::min<size_t>(kMaxPullJobs, n - k0));
-        for (uint32_t i = 0; i < jobs.n; ++i) {
-            if ((reinterpret_cast<uintptr_t>(src[k0 + i]) | reinterpret_cast<uintptr_t>(dst[k0 + i])) & 15u)
-                invalid("pull copy: blocks must be 16-B aligned");
-            jobs.dst[i] = static_cast<uint8_t*>(dst[k0 + i]);
-            jobs.src[i] = static_cast<const uint8_t*>(src[k0 + i]);
-            jobs.bytes[i] = bytes[k0 + i];
-        }
-        static const unsigned grid = [] {
-            const char* e = std::getenv("RFL_PULL_CTAS");
-            return e ? static_cast<unsigned>(std::max(1, std::atoi(e))) : 64u;
-        }();
-        k_pull_copy<<<grid, kPullThreads, 0, st>>>(jobs);
-        cuda_check(cudaGetLastError(), "k_pull_copy launch");
-    }
-}
 }  // namespace rfl

@@ -91,8 +91,4 @@ size_t dense_out_elem_size(const ArenaView& a, OutDtype od);
 void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, void* out,
                          uint64_t* out_gidx, cudaStream_t st);
 
-// Pinned-host -> device staging by SM loads (UVA), up to kMaxPullJobs blocks per launch.
-constexpr int kMaxPullJobs = 128;
-void launch_pull_copy(void* const* dst, const void* const* src, const size_t* bytes, size_t n, cudaStream_t st);
-
 }  // namespace rfl
