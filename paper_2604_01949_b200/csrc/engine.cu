@@ -1,5 +1,8 @@
 // Device store images + GPU BatchIterator (see engine.hpp).
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -317,8 +320,10 @@ DStore::SlotRef DStore::acquire_slot(uint64_t bytes) {
         slot_bytes_ = align_up(std::max<uint64_t>(bytes, 1), 256);
     }
     if (free_.empty()) grow_slab();
-    SlotRef s = free_.back();
-    free_.pop_back();
+    // oldest first: a LIFO pop would hand the next batch's copy the slot the
+    // previous batch's kernel just released, serialising copy(i+1) behind kernel(i)
+    SlotRef s = free_.front();
+    free_.pop_front();
     return s;
 }
 
@@ -445,6 +450,8 @@ void BlockReader::release(uint64_t seq, cudaStream_t st) {
 // ============================================================== GpuLoader ===
 GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t epoch, const DeviceCfg& dev)
     : ds_(std::move(ds)), cfg_(cfg), epoch_(epoch), dev_(dev), replay_(ds_->manifest().n_obs, cfg, epoch) {
+    static std::atomic<uint64_t> next_id{1};
+    id_ = next_id++;
     const Manifest& m = ds_->manifest();
     if (m.layout == Layout::dense && dev_.output == 0) invalid("csr output requested from a dense store");
     if (dev_.normalize && (m.layout != Layout::csr || dev_.output != 1))
@@ -464,9 +471,15 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     if (ds_->staging() != kResident) {
         live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
         block_bytes_ = ds_->max_block_bytes(cfg_.f);
-        // live blocks peak at ~5x B/f (cfg1 318 for B/f = 64, cfg4 230 for 32)
+        // live blocks peak at ~5x B/f (cfg1 318 for B/f = 64, cfg4 230 for 32).
+        // On top, (out_slots + 2) batches' worth of free slots: the host runs out_slots
+        // batches ahead, and the FIFO pool must hand batch j a slot whose releasing
+        // kernel already ran, or copy(j) queues behind kernel(j-1) and the copy
+        // engine idles for every kernel (profiles/r1_pcie.md)
         const uint64_t nb = (m.n_obs + cfg_.f - 1) / cfg_.f;
-        const uint64_t want = std::min<uint64_t>(nb, 6 * ((cfg_.B + cfg_.f - 1) / cfg_.f) + 32);
+        const uint64_t per_batch = (cfg_.b + cfg_.f - 1) / cfg_.f + 1;
+        const uint64_t want =
+            std::min<uint64_t>(nb, 6 * ((cfg_.B + cfg_.f - 1) / cfg_.f) + 32 + (dev_.out_slots + 2) * per_batch);
         ds_->reserve_slots(block_bytes_, std::min<uint64_t>(want, (8ull << 30) / std::max<uint64_t>(block_bytes_, 1)));
         if (ds_->staging() == kStreamFile) {
             const uint32_t threads = std::min<uint32_t>(16, std::max<uint32_t>(1, cfg_.prefetch_depth));
@@ -518,8 +531,14 @@ void GpuLoader::stage_block(uint64_t id) {
     lv.slot = ds_->acquire_slot(block_bytes_);
     lv.live_rows = e - s;
     // the slot's previous kernel readers are done (skip the stream wait if already complete)
-    if (cudaEventQuery(lv.slot.released) != cudaSuccess)
+    if (ds_->staging() == kStreamPinned && lv.slot.owner == id_) {
+        if (!pend_ev_ || lv.slot.seq >= pend_seq_) {  // coalesced into one wait in next()
+            pend_ev_ = lv.slot.released;
+            pend_seq_ = lv.slot.seq;
+        }
+    } else if (cudaEventQuery(lv.slot.released) != cudaSuccess) {
         cuda_ok(cudaStreamWaitEvent(copy_, lv.slot.released, 0), "wait slot");
+    }
     const HostStore& hs = ds_->host();
     if (ds_->staging() == kStreamPinned) {
         // records of one block are contiguous in the pinned image except for alignment padding;
@@ -590,21 +609,43 @@ void GpuLoader::ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz) {
     }
 }
 
+namespace {
+// RFL_TRACE_LOADER=1: per next() host phase times on stderr (replay, staging, slot wait, launch)
+struct NextTrace {
+    bool on = [] {
+        const char* e = std::getenv("RFL_TRACE_LOADER");
+        return e && e[0] == '1';
+    }();
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    double lap() {
+        const auto n = std::chrono::steady_clock::now();
+        const double us = std::chrono::duration<double, std::micro>(n - t).count();
+        t = n;
+        return us;
+    }
+};
+}  // namespace
+
 bool GpuLoader::next(BatchOut& out) {
     if (done_) return false;
     DeviceGuard g(ds_->device());
     const Manifest& m = ds_->manifest();
+    NextTrace tr;
+    double t_replay = 0, t_stage = 0, t_slot = 0;
     if (!replay_.next(gidx_, consumed_)) {
         done_ = true;
         return false;
     }
+    if (tr.on) t_replay = tr.lap();
     const bool resident = ds_->staging() == kResident;
     if (!resident) {
         batch_dst_.clear();
         batch_src_.clear();
         batch_size_.clear();
+        pend_ev_ = nullptr;
         for (uint64_t id : consumed_) stage_block(id);
-        if (!batch_dst_.empty()) {
+        if (pend_ev_ && cudaEventQuery(pend_ev_) != cudaSuccess)
+            cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");        if (!batch_dst_.empty()) {
             cudaMemcpyAttributes attr{};
             attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
             attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
@@ -615,8 +656,10 @@ bool GpuLoader::next(BatchOut& out) {
         }
         cuda_ok(cudaEventRecord(staged_, copy_), "event");
     }
+    if (tr.on) t_stage = tr.lap();
     OutSlot& s = slots_[next_slot_++ % slots_.size()];
     if (s.used) cuda_ok(cudaEventSynchronize(s.done), "slot reuse");  // caller's view of it expires here
+    if (tr.on) t_slot = tr.lap();
     s.used = true;
     const uint64_t n = gidx_.size();
     uint64_t nnz = 0;
@@ -675,6 +718,7 @@ bool GpuLoader::next(BatchOut& out) {
     }
     ctr_.kernels_launched += 1;
     cuda_ok(cudaEventRecord(s.done, compute_), "event");
+    ++batch_seq_;
 
     // blocks whose rows are all taken go back to the pool once this batch's kernel is done
     if (!resident) {
@@ -682,12 +726,18 @@ bool GpuLoader::next(BatchOut& out) {
             Live& lv = live_[gidx_[i] / cfg_.f];
             if (--lv.live_rows == 0) {
                 cuda_ok(cudaEventRecord(lv.slot.released, compute_), "event");
+                lv.slot.owner = id_;
+                lv.slot.seq = batch_seq_;
                 ds_->release_slot(lv.slot);
                 lv.slot = DStore::SlotRef{};
             }
         }
     }
 
+    if (tr.on)
+        std::fprintf(stderr, "# next %llu: replay %.1f us, stage %.1f us (%zu blocks), slot wait %.1f us, rest %.1f us\n",
+                     static_cast<unsigned long long>(replay_.batch_index() - 1), t_replay, t_stage, consumed_.size(),
+                     t_slot, tr.lap());
     out.epoch = epoch_;
     out.batch_index = replay_.batch_index() - 1;
     out.n_rows = n;

@@ -10,6 +10,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <exception>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -63,6 +64,8 @@ public:
         uint8_t* ptr = nullptr;
         cudaEvent_t released = nullptr;  // recorded after the last kernel reading it
         uint64_t bytes = 0;
+        uint64_t owner = 0;           // id of the loader that recorded `released` (on its compute stream) ...
+        uint64_t seq = 0;             // ... after its batch `seq`
     };
     SlotRef acquire_slot(uint64_t bytes);
     // grow the pool (slot geometry `bytes`) until it holds >= n free slots, so a
@@ -84,7 +87,7 @@ private:
     std::mutex mu_;
     void grow_slab();  // mu_ held
     std::vector<void*> slabs_;
-    std::vector<SlotRef> free_;
+    std::deque<SlotRef> free_;  // FIFO: reuse the slot released longest ago (its readers are done)
     uint64_t slot_bytes_ = 0;
 };
 
@@ -192,6 +195,13 @@ private:
     std::vector<size_t> batch_size_;
     Counters ctr_;
     bool done_ = false;
+    uint64_t batch_seq_ = 0;
+    uint64_t id_ = 0;  // unique per loader (slot ownership; never reused like an address)
+    // stream_pinned: the newest of this loader's own release events among the slots
+    // acquired for the batch being staged -- one copy-stream wait per batch covers
+    // them all (they were recorded in order on compute_)
+    cudaEvent_t pend_ev_ = nullptr;
+    uint64_t pend_seq_ = 0;
 };
 
 }  // namespace rfl
