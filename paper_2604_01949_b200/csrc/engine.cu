@@ -687,7 +687,7 @@ bool GpuLoader::next(BatchOut& out) {
     // device runs one balanced copy kernel and no scan
     static const bool device_scan = [] {
         const char* e = std::getenv("RFL_GATHER");
-        return e && (std::string(e) == "scan" || std::string(e) == "jobs");
+        return e && std::string(e) == "scan";
     }();
     const bool planned = m.layout == Layout::csr && dev_.output == 0 && !device_scan;
     if (planned) {

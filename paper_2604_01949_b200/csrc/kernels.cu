@@ -229,7 +229,6 @@ __device__ __forceinline__ RowDesc describe_row(const ArenaDev& a, const RowRef&
 // (2) k_csr_copy — every warp grid-strides over (row, array) copy jobs with the
 // 128-bit shifted warp copy; no barriers, so the whole GPU stays busy.
 constexpr int kScanThreads = 128;
-constexpr int kCopyThreads = 256;
 constexpr uint64_t kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 struct RowJob {
@@ -308,110 +307,6 @@ __global__ void __launch_bounds__(kScanThreads)
     if (tid == 0 && (tile + 1) * kScanThreads >= n_rows) out_prefix[n_rows] = s_prefix + agg;
 }
 
-template <typename IdxT>
-__global__ void __launch_bounds__(kCopyThreads, 4)
-    k_csr_copy(const RowJob* __restrict__ jobs, const uint64_t* __restrict__ P, uint64_t n_rows, uint32_t vs,
-               uint8_t* __restrict__ out_idx, uint8_t* __restrict__ out_val) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kCopyThreads / 32);
-    const uint64_t p0 = P[0];
-    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * (kCopyThreads / 32) + (threadIdx.x >> 5); j < 2 * n_rows;
-         j += warps) {
-        const uint64_t row = j >> 1;
-        const bool val = j & 1u;
-        const uint64_t off = P[row] - p0, cnt = P[row + 1] - P[row];
-        const RowJob jb = jobs[row];
-        const uint32_t es = val ? vs : static_cast<uint32_t>(sizeof(IdxT));
-        warp_copy((val ? out_val : out_idx) + off * es, val ? jb.val : jb.idx, cnt * es, lane);
-    }
-}
-
-// Balanced variant of the copy: the output of each array is cut into equal
-// 16-B aligned byte ranges, one per warp of a persistent grid (warps
-// [0, w_idx) take the indices, the rest the values), so every warp moves the
-// same number of bytes whatever the row lengths — no wave quantisation over
-// (row, array) jobs.  A warp finds its first row with a 32-way search of the
-// prefix P, then walks the (usually 1-3) rows its range overlaps, resolving
-// their source rows lane-parallel (from the scan's job table when given, else
-// straight from the chunk records: the host-planned path, where P is the
-// host's prefix of the schedule's per-row nnz and no scan runs).  Reads are
-// clamped to the row's own nnz, so an inconsistent P cannot read out of bounds.
-template <typename IdxT>
-__global__ void __launch_bounds__(kCopyThreads)
-    k_csr_copy_flat(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, const RowJob* __restrict__ jobs,
-                    const uint64_t* __restrict__ P, uint64_t n_rows, uint32_t w_idx, uint8_t* __restrict__ out_idx,
-                    uint8_t* __restrict__ out_val, uint64_t* __restrict__ out_gidx) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t gw = blockIdx.x * (kCopyThreads / 32) + (threadIdx.x >> 5);
-    const uint32_t n_warps = gridDim.x * (kCopyThreads / 32);
-    pdl_wait();
-    pdl_trigger();
-    if (out_gidx && !jobs)  // the scan path writes gidx itself
-        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kCopyThreads + threadIdx.x; i < n_rows;
-             i += static_cast<uint64_t>(gridDim.x) * kCopyThreads)
-            out_gidx[i] = refs[i].gidx;
-    const bool is_val = gw >= w_idx;
-    const uint32_t es = is_val ? vs : static_cast<uint32_t>(sizeof(IdxT));
-    const uint32_t nw = is_val ? n_warps - w_idx : w_idx, w = is_val ? gw - w_idx : gw;
-    const uint64_t p0 = P[0], total = P[n_rows] - p0;
-    const uint64_t span = (((total * es + nw - 1) / nw) + 15) & ~15ull;
-    const uint64_t e0 = w * span / es;
-    if (e0 >= total) return;
-    const uint64_t e1 = umin64(e0 + span / es, total);
-    uint8_t* const out = is_val ? out_val : out_idx;
-    // largest r with P[r] - p0 <= e0 (32-way narrowing)
-    uint64_t lo = 0, hi = n_rows;  // invariant: answer in [lo, hi)
-    while (hi - lo > 32) {
-        const uint64_t step = (hi - lo + 31) / 32;
-        const uint64_t k = lo + lane * step;
-        const bool ok = k < hi && P[k] - p0 <= e0;
-        const uint32_t c = __popc(__ballot_sync(kFull, ok));  // >= 1 (lane 0 holds lo)
-        lo += (c - 1) * step;
-        hi = umin64(lo + step, hi);
-    }
-    {
-        const uint64_t k = lo + lane;
-        const bool ok = k < hi && P[k] - p0 <= e0;
-        lo += __popc(__ballot_sync(kFull, ok)) - 1;
-    }
-    for (uint64_t r = lo; r < n_rows; r += 32) {
-        const uint64_t rl = r + lane;
-        uint64_t pl = ~0ull, ph = 0;
-        if (rl < n_rows) {
-            pl = P[rl] - p0;
-            ph = P[rl + 1] - p0;
-        }
-        const uint32_t act = __ballot_sync(kFull, rl < n_rows && pl < e1);
-        const uint8_t* src = nullptr;
-        uint64_t avail = 0;
-        if ((act >> lane) & 1u) {
-            if (jobs) {
-                const RowJob jb = jobs[rl];
-                src = is_val ? jb.val : jb.idx;
-                avail = ph - pl;
-            } else {
-                const CsrRow c = csr_row<IdxT>(a, refs[rl], vs);
-                src = is_val ? c.val : c.idx;
-                avail = c.nnz;
-            }
-        }
-        for (uint32_t m = act; m; m &= m - 1) {
-            const int k = __ffs(m) - 1;
-            const uint64_t kpl = __shfl_sync(kFull, pl, k), kph = __shfl_sync(kFull, ph, k);
-            const uint64_t kav = __shfl_sync(kFull, avail, k);
-            const uint8_t* ks = reinterpret_cast<const uint8_t*>(
-                __shfl_sync(kFull, reinterpret_cast<unsigned long long>(src), k));
-            const uint64_t s = kpl > e0 ? kpl : e0, t = umin64(kph, e1);
-            if (s >= t) continue;
-            const uint64_t in_row = s - kpl;
-            const uint64_t cnt = in_row >= kav ? 0 : umin64(t - s, kav - in_row);
-            warp_copy(out + s * es, ks + in_row * es, cnt * es, lane);
-        }
-        if (act != kFull) break;
-        if (__shfl_sync(kFull, ph, 31) >= e1) break;
-    }
-}
-
 // ============================================================ K5 record pack ===
 template <typename T>
 __device__ __forceinline__ void st_any(uint8_t* p, T v) {  // little-endian store at any alignment
@@ -467,8 +362,6 @@ __global__ void __launch_bounds__(kPackThreads)
 }
 
 // ============================================================ K3 densify =====
-constexpr int kDenseThreads = 512;
-constexpr uint32_t kMaxTileBytes = 100 * 1024;  // two CTAs per SM
 
 template <typename D, typename S>
 struct Conv {
@@ -520,113 +413,6 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // One CTA per output row (grid-stride): zero a shared-memory tile, scatter the
 // row's entries into it, then a single cp.async.bulk store writes the dense
 // tile — every output byte hits HBM exactly once, with no read-modify-write.
-template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int NBUF>
-__global__ void __launch_bounds__(THREADS, (THREADS == 256 && U == 4) ? 5 : 1024 / THREADS)
-    k_csr_densify(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
-                  float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ double s_red[THREADS / 32];
-    __shared__ RowDesc s_desc[2];  // current / next row, software-pipelined
-    const uint32_t tile_stride = (tile_cols * static_cast<uint32_t>(sizeof(DstT)) + 127u) & ~127u;
-    uint32_t tcount = 0;  // tiles issued by this CTA (selects the buffer)
-    const uint32_t tid = threadIdx.x;
-    constexpr uint32_t nthr = THREADS;
-    const uint64_t n_var = a.n_var;
-    // U entries per thread are held in registers across the zero-fill
-    if (tid == 0 && blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
-    __syncthreads();
-    uint32_t cur = 0;
-    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x, cur ^= 1u) {
-        const RowDesc d = s_desc[cur];
-        // 1. issue this row's first U*nthr entry loads; they land while the
-        //    previous row's bulk store drains and the tile is zeroed
-        uint64_t col[U];
-        SrcT v[U];
-#pragma unroll
-        for (uint32_t u = 0; u < U; ++u) {
-            const uint64_t k = tid + u * nthr;
-            col[u] = ~0ull;
-            if (k < d.nnz) {
-                col[u] = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
-                v[u] = ld_value<SrcT>(d.val + k * sizeof(SrcT));
-            }
-        }
-        // 2. the next row's record lookup (refs -> header -> indptr chain) in flight too
-        if (tid == 0) {
-            if (row + gridDim.x < n_rows) s_desc[cur ^ 1u] = describe_row<IdxT>(a, refs[row + gridDim.x], sizeof(SrcT));
-            if (out_gidx) out_gidx[row] = d.gidx;
-        }
-        float scale = 1.0f;
-        if (norm) {  // library size in fp64
-            double s = 0.0;
-#pragma unroll
-            for (uint32_t u = 0; u < U; ++u)
-                if (col[u] != ~0ull) s += static_cast<double>(v[u]);
-            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr)
-                s += static_cast<double>(ld_value<SrcT>(d.val + k * sizeof(SrcT)));
-            s = block_sum(s, s_red);
-            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
-        }
-        DstT* orow = out + row * n_var;
-        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols, ++tcount) {
-            const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
-            const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
-            uint8_t* buf = smem + (NBUF == 1 ? 0u : (tcount & 1u) * tile_stride);
-            DstT* tile = reinterpret_cast<DstT*>(buf);
-            // the bulk store that last read this buffer has drained (NBUF=2: the
-            // other buffer's store may still be in flight while we build this one)
-            if (bulk && tid == 0) {
-                if (NBUF == 1) bulk_wait_read0();
-                else bulk_wait_read1();
-            }
-            __syncthreads();
-            uint4* t4 = reinterpret_cast<uint4*>(buf);
-            for (uint32_t i = tid; i < bytes / 16u; i += nthr) t4[i] = make_uint4(0, 0, 0, 0);
-            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) buf[i] = 0;
-            __syncthreads();
-#pragma unroll
-            for (uint32_t u = 0; u < U; ++u)
-                if (col[u] != ~0ull && col[u] >= c0 && col[u] - c0 < cols)
-                    tile[col[u] - c0] = Conv<DstT, SrcT>::go(v[u], scale, norm);
-            uint64_t k = tid + U * nthr;  // rows longer than U*nthr entries: stream the rest
-            for (; k + (U - 1) * nthr < d.nnz; k += U * nthr) {
-                uint64_t c2[U];
-                SrcT v2[U];
-#pragma unroll
-                for (uint32_t u = 0; u < U; ++u) {
-                    c2[u] = ld_index<IdxT>(d.idx + (k + u * nthr) * sizeof(IdxT));
-                    v2[u] = ld_value<SrcT>(d.val + (k + u * nthr) * sizeof(SrcT));
-                }
-#pragma unroll
-                for (uint32_t u = 0; u < U; ++u)
-                    if (c2[u] >= c0 && c2[u] - c0 < cols) tile[c2[u] - c0] = Conv<DstT, SrcT>::go(v2[u], scale, norm);
-            }
-            for (; k < d.nnz; k += nthr) {
-                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
-                if (c2 >= c0 && c2 - c0 < cols)
-                    tile[c2 - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(d.val + k * sizeof(SrcT)), scale, norm);
-            }
-            if (bulk == 1) {
-                fence_proxy_async_shared();  // make generic-proxy smem writes visible to the bulk engine
-                __syncthreads();
-                if (tid == 0) {
-                    bulk_store(orow + c0, buf, bytes);
-                    bulk_commit();
-                }
-            } else if (bulk == 2) {  // 16-B aligned rows: all threads stream the tile out with STG.128
-                __syncthreads();
-                const uint4* s4 = reinterpret_cast<const uint4*>(buf);
-                uint4* g4 = reinterpret_cast<uint4*>(orow + c0);
-                for (uint32_t i = tid; i < bytes / 16u; i += nthr) st_v4(g4 + i, s4[i]);
-            } else {
-                __syncthreads();
-                for (uint32_t i = tid; i < cols; i += nthr) orow[c0 + i] = tile[i];
-            }
-        }
-    }
-    if (bulk && tid == 0) bulk_wait0();
-}
-
 // ============================================================ K3 densify v6 ===
 // Same smem-tile + TMA bulk store scheme as above, with two rows in flight per
 // CTA: while row i's tiles are zeroed/scattered/stored, row i+1's first U*THREADS
@@ -827,112 +613,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     if (bulk && tid == 0) bulk_wait0();
 }
 
-// v8: v6 with the per-tile zero fill replaced by un-scattering the stored
-// tile's own entries (smem writes per tile ~ entries instead of tile bytes).
-template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB)
-    k_csr_densify8(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
-                   float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ double s_red[THREADS / 32];
-    __shared__ RowDesc s_desc[3];  // rows i, i+1, i+2 of this CTA
-    const uint32_t tid = threadIdx.x;
-    constexpr uint32_t nthr = THREADS;
-    const uint64_t n_var = a.n_var;
-    const uint64_t g = gridDim.x;
-    pdl_wait();
-    pdl_trigger();
-    if (tid == 0) {
-        if (blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], sizeof(SrcT));
-        if (blockIdx.x + g < n_rows) s_desc[1] = describe_row<IdxT>(a, refs[blockIdx.x + g], sizeof(SrcT));
-    }
-    __syncthreads();
-    // the tile buffer is zeroed once; afterwards each tile's entries are
-    // un-scattered (re-zeroed) once its bulk store has read them
-    for (uint32_t i = tid; i < (tile_cols * static_cast<uint32_t>(sizeof(DstT)) + 15u) / 16u; i += nthr)
-        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
-    uint32_t colA[U], colB[U];
-    SrcT vA[U], vB[U];
-    if (blockIdx.x < n_rows) load_entries<IdxT, SrcT, U>(s_desc[0], tid, nthr, colA, vA);
-    uint32_t slot = 0;
-    for (uint64_t row = blockIdx.x; row < n_rows; row += g, slot = slot == 2 ? 0 : slot + 1) {
-        const RowDesc d = s_desc[slot];
-        const uint32_t nslot = slot == 2 ? 0 : slot + 1, nnslot = nslot == 2 ? 0 : nslot + 1;
-        const bool has_next = row + g < n_rows;
-        if (has_next) load_entries<IdxT, SrcT, U>(s_desc[nslot], tid, nthr, colB, vB);  // row i+1 in flight
-        if (tid == 0) {
-            if (row + 2 * g < n_rows) s_desc[nnslot] = describe_row<IdxT>(a, refs[row + 2 * g], sizeof(SrcT));
-            if (out_gidx) out_gidx[row] = d.gidx;
-        }
-        float scale = 1.0f;
-        if (norm) {  // library size in fp64
-            double s = 0.0;
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (colA[u] != ~0u) s += static_cast<double>(vA[u]);
-            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr)
-                s += static_cast<double>(ld_value<SrcT>(d.val + k * sizeof(SrcT)));
-            s = block_sum(s, s_red);
-            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
-        }
-        DstT* orow = out + row * n_var;
-        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
-            const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
-            const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
-            DstT* tile = reinterpret_cast<DstT*>(smem);
-            __syncthreads();  // previous tile's un-scatter (or the initial zero) is complete
-            const uint32_t c0u = static_cast<uint32_t>(c0);
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (colA[u] - c0u < cols) tile[colA[u] - c0u] = Conv<DstT, SrcT>::go(vA[u], scale, norm);
-            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr) {  // rows longer than U*THREADS
-                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
-                if (c2 >= c0 && c2 - c0 < cols)
-                    tile[c2 - c0] = Conv<DstT, SrcT>::go(ld_value<SrcT>(d.val + k * sizeof(SrcT)), scale, norm);
-            }
-            if (bulk) {
-                fence_proxy_async_shared();
-                __syncthreads();
-                if (tid == 0) {
-                    bulk_store(orow + c0, smem, bytes);
-                    bulk_commit();
-                    bulk_wait_read0();
-                }
-            } else {
-                __syncthreads();
-                for (uint32_t i = tid; i < cols; i += nthr) orow[c0 + i] = tile[i];
-            }
-            __syncthreads();  // the tile has been read out
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (colA[u] - c0u < cols) tile[colA[u] - c0u] = DstT{};
-            for (uint64_t k = tid + U * nthr; k < d.nnz; k += nthr) {
-                const uint64_t c2 = ld_index<IdxT>(d.idx + k * sizeof(IdxT));
-                if (c2 >= c0 && c2 - c0 < cols) tile[c2 - c0] = DstT{};
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            colA[u] = colB[u];
-            vA[u] = vB[u];
-        }
-    }
-    if (bulk && tid == 0) bulk_wait0();
-}
-
-// ============================================================ K3 densify v3 ===
-// Warp-sweep densify.  Per row: one elected thread stages the row's indices
-// and values into shared memory with two 1-D TMA bulk copies (16-B aligned
-// supersets, completion on an mbarrier) and prefetches the next row's record
-// lookup; each warp then sweeps its contiguous share of the row's columns in
-// 512-B spans: zero a 512-B per-warp tile, scatter the span's entries (sorted
-// columns: a ballot over 32 consecutive entries), and write the span with one
-// coalesced 16-B store per lane.  Every output byte is written once, straight
-// from registers; no row-sized tile, so 6 CTAs/SM keep 48 warps of rows in flight.
-constexpr int kSweepThreads = 256;
-constexpr int kSweepWarps = kSweepThreads / 32;
-constexpr uint32_t kSpanBytes = 512;
-
+// ------------------------------------------------ mbarrier + TMA bulk load ---
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -959,128 +640,9 @@ __device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t
                  "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-// index / value reads from shared or global memory at 4-B (or 1-B for u8) alignment
-template <typename T>
-__device__ __forceinline__ uint64_t ld_index_any(const uint8_t* p) {
-    if (sizeof(T) == 4) return *reinterpret_cast<const uint32_t*>(p);
-    return static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p)) |
-           (static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p + 4)) << 32);
-}
-template <typename T>
-__device__ __forceinline__ T ld_value_any(const uint8_t* p) {
-    if constexpr (sizeof(T) == 8) {
-        const uint64_t u = static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p)) |
-                           (static_cast<uint64_t>(*reinterpret_cast<const uint32_t*>(p + 4)) << 32);
-        return __longlong_as_double(static_cast<long long>(u));
-    } else {
-        return *reinterpret_cast<const T*>(p);
-    }
-}
-
-template <typename IdxT, typename SrcT, typename DstT>
-__global__ void __launch_bounds__(kSweepThreads, 6)
-    k_csr_densify_sweep(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t cap, int norm,
-                        float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int vec_out) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t s_bar;
-    __shared__ RowDesc s_desc[2];
-    __shared__ double s_red[kSweepWarps];
-    constexpr uint32_t is = sizeof(IdxT), vs = sizeof(SrcT), os = sizeof(DstT);
-    constexpr uint32_t span_cols = kSpanBytes / os, lane_cols = 16 / os;
-    uint8_t* s_idx = smem;                                                   // cap*is + 16
-    uint8_t* s_val = smem + ((cap * is + 16 + 127) & ~127u);                 // cap*vs + 16
-    uint8_t* s_tile = s_val + ((cap * vs + 16 + 127) & ~127u);               // kSweepWarps * 512
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    uint8_t* tile = s_tile + warp * kSpanBytes;
-    const uint64_t n_var = a.n_var;
-    const uint64_t n_spans = (n_var + span_cols - 1) / span_cols;
-    const uint64_t spw = (n_spans + kSweepWarps - 1) / kSweepWarps;
-    if (tid == 0) {
-        mbar_init(&s_bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (blockIdx.x < n_rows) s_desc[0] = describe_row<IdxT>(a, refs[blockIdx.x], vs);
-    }
-    __syncthreads();
-    uint32_t phase = 0, cur = 0;
-    for (uint64_t row = blockIdx.x; row < n_rows; row += gridDim.x, cur ^= 1u) {
-        const RowDesc d = s_desc[cur];
-        const bool staged = d.nnz > 0 && d.nnz <= cap;
-        const uintptr_t ia = reinterpret_cast<uintptr_t>(d.idx), va = reinterpret_cast<uintptr_t>(d.val);
-        if (tid == 0) {
-            if (staged) {  // 16-B aligned supersets of the row's indices and values
-                const uint32_t ib = static_cast<uint32_t>(((ia + d.nnz * is + 15) & ~uintptr_t(15)) - (ia & ~uintptr_t(15)));
-                const uint32_t vb = static_cast<uint32_t>(((va + d.nnz * vs + 15) & ~uintptr_t(15)) - (va & ~uintptr_t(15)));
-                mbar_arrive_expect_tx(&s_bar, ib + vb);
-                bulk_load(s_idx, reinterpret_cast<const void*>(ia & ~uintptr_t(15)), ib, &s_bar);
-                bulk_load(s_val, reinterpret_cast<const void*>(va & ~uintptr_t(15)), vb, &s_bar);
-            }
-            if (row + gridDim.x < n_rows) s_desc[cur ^ 1u] = describe_row<IdxT>(a, refs[row + gridDim.x], vs);
-            if (out_gidx) out_gidx[row] = d.gidx;
-        }
-        const uint8_t* E_idx = staged ? s_idx + (ia & 15u) : d.idx;
-        const uint8_t* E_val = staged ? s_val + (va & 15u) : d.val;
-        if (staged) {
-            mbar_wait(&s_bar, phase);
-            phase ^= 1u;
-        }
-        float scale = 1.0f;
-        if (norm) {  // library size in fp64
-            double s = 0.0;
-            for (uint64_t k = tid; k < d.nnz; k += kSweepThreads) s += static_cast<double>(ld_value_any<SrcT>(E_val + k * vs));
-            s = block_sum(s, s_red);
-            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
-        }
-        const uint64_t sp0 = warp * spw, sp1 = umin64(n_spans, sp0 + spw);
-        DstT* orow = out + row * n_var;
-        if (sp0 < sp1) {
-            // first entry of this warp's column range (lower bound over sorted columns)
-            uint64_t cursor = 0;
-            if (lane == 0) {
-                uint64_t lo = 0, hi = d.nnz;
-                const uint64_t c_begin = sp0 * span_cols;
-                while (lo < hi) {
-                    const uint64_t mid = (lo + hi) >> 1;
-                    if (ld_index_any<IdxT>(E_idx + mid * is) < c_begin) lo = mid + 1;
-                    else hi = mid;
-                }
-                cursor = lo;
-            }
-            cursor = __shfl_sync(kFull, cursor, 0);
-            for (uint64_t sp = sp0; sp < sp1; ++sp) {
-                const uint64_t c0 = sp * span_cols, c1 = umin64(n_var, c0 + span_cols);
-                reinterpret_cast<uint4*>(tile)[lane] = make_uint4(0, 0, 0, 0);
-                __syncwarp();
-                for (;;) {  // entries of [c0, c1): a prefix of the next 32 (columns are sorted)
-                    const uint64_t e = cursor + lane;
-                    uint64_t col = ~0ull;
-                    if (e < d.nnz) col = ld_index_any<IdxT>(E_idx + e * is);
-                    const bool in = col < c1;
-                    const uint32_t m = __ballot_sync(kFull, in);
-                    if (in && col >= c0)
-                        reinterpret_cast<DstT*>(tile)[col - c0] =
-                            Conv<DstT, SrcT>::go(ld_value_any<SrcT>(E_val + e * vs), scale, norm);
-                    const uint32_t cnt = __popc(m);
-                    cursor += cnt;
-                    if (cnt < 32) break;
-                }
-                __syncwarp();
-                const uint4 v = reinterpret_cast<const uint4*>(tile)[lane];
-                const uint64_t cl = c0 + static_cast<uint64_t>(lane) * lane_cols;
-                if (vec_out && cl + lane_cols <= c1) {
-                    st_v4(orow + cl, v);
-                } else if (cl < c1) {
-                    const DstT* tv = reinterpret_cast<const DstT*>(&v);
-                    for (uint32_t j = 0; j < lane_cols && cl + j < c1; ++j) orow[cl + j] = tv[j];
-                }
-                __syncwarp();
-            }
-        }
-        __syncthreads();  // staging buffers are re-filled for the next row
-    }
-}
-
 // ===================================================== K2 copy, TMA staged ===
-// The balanced range split of k_csr_copy_flat, with the source side moved to
+// The output of each array is cut into equal 16-B aligned byte ranges, one per
+// warp of a persistent grid, with the source side moved to
 // the async proxy: each warp streams its output range as pieces of <= 4 KB;
 // one lane issues a 1-D TMA bulk load of the piece's 16-B aligned source
 // superset into the warp's shared stage (completion on an mbarrier), two
@@ -1110,7 +672,7 @@ __device__ __forceinline__ uint8_t lds_u8(uint32_t addr) {
 }
 
 // Generator of one warp's pieces (all state warp-uniform; rows resolved 32 at
-// a time lane-parallel, as in k_csr_copy_flat).
+// a time lane-parallel).
 template <typename IdxT>
 struct TcGen {
     ArenaDev a;
@@ -1646,33 +1208,23 @@ void set_smem(K kernel, size_t bytes) {
                "cudaFuncSetAttribute");
 }
 
-// Densify variant (RFL_DENSIFY="v2:<threads>:<tile KB>[:g]" | "v3" | "v5" |
-// "v6:<threads>:<tile KB>:<U>:<CTAs/SM>"), for A/B runs.
-struct DensifyCfg {  // version 0 = the measured default (v6, shape rule in densify_t)
-    int version = 0, threads = 256, tile_kb = 40, u = 8, minb = 4;
-    char store = 't';  // 't': TMA bulk store of the tile, 'g': STG.128 from all threads
+// Densify shape override for A/B runs: RFL_DENSIFY="v<6|9>:<threads>:<tile KB>:<U>:<CTAs/SM>"
+// (instantiated shapes: 256:*:16:2, 256:*:8:3, 256:*:8:4; other values fall back to 256:*:8:3).
+struct DensifyCfg {  // version 0 = the measured default (shape rule in densify_t)
+    int version = 0, threads = 256, tile_kb = 40, u = 8, minb = 3;
 };
 const DensifyCfg& densify_cfg() {
     static const DensifyCfg c = [] {
         DensifyCfg d;
         const char* e = std::getenv("RFL_DENSIFY");
-        if (e && e[0] == 'v') {
-            int v = 2, t = 512, kb = 100, u = 8, mb = 4;
-            char st = 't';
-            if (std::sscanf(e, "v%d", &v) == 1 && (v == 6 || v == 8 || v == 9)) {
-                const int got = std::sscanf(e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
-                d.version = v;
-                if (got >= 1) d.threads = t;
-                if (got >= 2 && kb >= 4 && kb <= 200) d.tile_kb = kb;
-                if (got >= 3) d.u = u;
-                if (got >= 4) d.minb = mb;
-                return d;
-            }
-            const int got = std::sscanf(e, "v%d:%d:%d:%c", &v, &t, &kb, &st);
-            if (got >= 4 && (st == 't' || st == 'g')) d.store = st;
+        int v = 0, t = 256, kb = 40, u = 8, mb = 3;
+        if (e && std::sscanf(e, "v%d", &v) == 1 && (v == 6 || v == 9)) {
+            const int got = std::sscanf(e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
             d.version = v;
-            if (got >= 2 && (t == 128 || t == 256 || t == 512)) d.threads = t;
-            if (got >= 3 && kb >= 4 && kb <= 200) d.tile_kb = kb;
+            if (got >= 1) d.threads = t;
+            if (got >= 2 && kb >= 4 && kb <= 200) d.tile_kb = kb;
+            if (got >= 3) d.u = u;
+            if (got >= 4) d.minb = mb;
         }
         return d;
     }();
@@ -1688,8 +1240,7 @@ void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, 
     const size_t smem = (tile_cols * esz + 127) & ~127ull;
     const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     auto kern = [] {
-        if constexpr (VAR == 8) return k_csr_densify8<IdxT, SrcT, DstT, THREADS, U, MINB>;
-        else if constexpr (VAR == 9) return k_csr_densify9<IdxT, SrcT, DstT, THREADS, U, MINB>;
+        if constexpr (VAR == 9) return k_csr_densify9<IdxT, SrcT, DstT, THREADS, U, MINB>;
         else return k_csr_densify6<IdxT, SrcT, DstT, THREADS, U, MINB>;
     }();
     set_smem(kern, smem);
@@ -1698,25 +1249,6 @@ void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, 
     const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
     launch_k(kern, dim3(static_cast<unsigned>(grid)), dim3(THREADS), smem, st, "k_csr_densify6 launch", dev_view(av),
              refs, n, static_cast<uint32_t>(tile_cols), norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
-}
-
-template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int NBUF>
-void densify_v2(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
-                uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes) {
-    const uint64_t esz = sizeof(DstT);
-    uint64_t tile_cols = av.n_var;
-    if (av.n_var * esz > max_tile_bytes) tile_cols = (max_tile_bytes / esz) & ~15ull;
-    const size_t smem = NBUF * ((tile_cols * esz + 127) & ~127ull);
-    int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    if (bulk && densify_cfg().store == 'g') bulk = 2;
-    auto kern = k_csr_densify<IdxT, SrcT, DstT, THREADS, U, NBUF>;
-    set_smem(kern, smem);
-    int per_sm = 0;
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem), "occupancy");
-    const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
-    kern<<<static_cast<unsigned>(grid), THREADS, smem, st>>>(dev_view(av), refs, n, static_cast<uint32_t>(tile_cols),
-                                                          norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
-    cuda_check(cudaGetLastError(), "k_csr_densify launch");
 }
 
 template <typename IdxT, typename SrcT, typename DstT>
@@ -1739,72 +1271,17 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
             return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, 40 << 10);
         }
     }
+    const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
     if constexpr (sizeof(IdxT) == 4 && sizeof(SrcT) == 4) {
-        if (dc.version == 9) {  // v6 + lane-parallel row lookups
-            const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
-            if (dc.threads == 128 && dc.u == 16 && dc.minb == 4)
-                return densify_v6<IdxT, SrcT, DstT, 128, 16, 4, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.threads == 128 && dc.u == 16)
-                return densify_v6<IdxT, SrcT, DstT, 128, 16, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.threads == 128)
-                return densify_v6<IdxT, SrcT, DstT, 128, 8, 6, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.threads == 512)
-                return densify_v6<IdxT, SrcT, DstT, 512, 4, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.u == 16)
-                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.minb == 4)
-                return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+        if (dc.version == 9) {
+            if (dc.u == 16) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            if (dc.minb == 4) return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
             return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
         }
-        if (dc.version == 8) {  // v6 + un-scatter
-            const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
-            if (dc.u == 16)
-                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.minb == 4)
-                return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
-        }
-        if (dc.version == 6) {  // A/B set: u32 indices, 4-byte values
-            const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
-            if (dc.threads == 512)
-                return densify_v6<IdxT, SrcT, DstT, 512, 4, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.threads == 128)
-                return densify_v6<IdxT, SrcT, DstT, 128, 8, 8>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.u == 4)
-                return densify_v6<IdxT, SrcT, DstT, 256, 4, 5>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.u == 12)
-                return densify_v6<IdxT, SrcT, DstT, 256, 12, 3>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.u == 16)
-                return densify_v6<IdxT, SrcT, DstT, 256, 16, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.minb == 2)
-                return densify_v6<IdxT, SrcT, DstT, 256, 8, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.minb == 3)
-                return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            return densify_v6<IdxT, SrcT, DstT, 256, 8, 4>(av, refs, n, norm, target, out, out_gidx, st, tb);
-        }
     }
-    if (dc.version == 2 || dc.version == 5) {  // v5 = 256 threads, 1,024 entries in registers, 5 CTAs/SM
-        const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
-        if (dc.version == 5)
-            return densify_v2<IdxT, SrcT, DstT, 256, 4, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
-        if (dc.threads == 512)
-            return densify_v2<IdxT, SrcT, DstT, 512, 4, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
-        return densify_v2<IdxT, SrcT, DstT, 256, 8, 1>(av, refs, n, norm, target, out, out_gidx, st, tb);
-    }
-    {
-        constexpr uint32_t is = sizeof(IdxT), vs = sizeof(SrcT);
-        const uint32_t cap = (32768u / (is + vs)) & ~31u;  // entries staged per row (longer rows: global path)
-        const size_t smem = ((cap * is + 16 + 127) & ~127u) + ((cap * vs + 16 + 127) & ~127u) + kSweepWarps * kSpanBytes;
-        const int vec = ((av.n_var * sizeof(DstT)) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-        auto kern = k_csr_densify_sweep<IdxT, SrcT, DstT>;
-        set_smem(kern, smem);
-        int per_sm = 0;
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSweepThreads, smem), "occupancy");
-        const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
-        kern<<<static_cast<unsigned>(grid), kSweepThreads, smem, st>>>(dev_view(av), refs, n, cap, norm ? 1 : 0, target,
-                                                                     static_cast<DstT*>(out), out_gidx, vec);
-        cuda_check(cudaGetLastError(), "k_csr_densify_sweep launch");
-    }
+    if (dc.u == 16) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
+    if (dc.minb == 4) return densify_v6<IdxT, SrcT, DstT, 256, 8, 4>(av, refs, n, norm, target, out, out_gidx, st, tb);
+    return densify_v6<IdxT, SrcT, DstT, 256, 8, 3>(av, refs, n, norm, target, out, out_gidx, st, tb);
 }
 
 template <typename IdxT>
@@ -1863,44 +1340,25 @@ void launch_scan(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* o
 }
 }  // namespace
 
-bool gather_tma() {
-    static const bool on = [] {
-        const char* e = std::getenv("RFL_GATHER");
-        return !(e && std::string(e) == "flat");
-    }();
-    return on;
-}
-
-void launch_copy_flat(const ArenaView& a, uint32_t vs, const RowRef* refs, const RowJob* jobs, const uint64_t* P,
-                      uint64_t n, void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st,
-                      uint64_t cr = 0) {
-    if (gather_tma() || cr) {
-        auto kern = a.idt == IDtype::u32 ? k_csr_copy_tma<uint32_t> : k_csr_copy_tma<uint64_t>;
-        const size_t smem = 2 * kTcStage * kTcWarps;
-        static int per_sm[2] = {0, 0};
-        int& occ = per_sm[a.idt == IDtype::u32 ? 0 : 1];
-        if (!occ) {
-            set_smem(kern, smem);
-            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTcThreads, smem), "occupancy");
-        }
-        const uint32_t blocks = static_cast<uint32_t>(std::max(occ, 1) * device_sm_count());
-        const uint32_t n_warps = blocks * kTcWarps;
-        const uint32_t is = static_cast<uint32_t>(index_size(a.idt));
-        const uint32_t w_idx = std::max(1u, std::min(n_warps - 1, (n_warps * is + (is + vs) / 2) / (is + vs)));
-        launch_k(kern, dim3(blocks), dim3(kTcThreads), smem, st, "k_csr_copy_tma launch", dev_view(a), vs, refs, jobs,
-                 P, n, w_idx, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data), out_gidx, cr);
-        return;
-    }
-    auto kern = a.idt == IDtype::u32 ? k_csr_copy_flat<uint32_t> : k_csr_copy_flat<uint64_t>;
+// K2 launcher: the balanced TMA-staged copy (k_csr_copy_tma), from the scan's job
+// table (jobs != nullptr) or resolving rows itself; cr > 0 = K5 record mode.
+void launch_copy_tma(const ArenaView& a, uint32_t vs, const RowRef* refs, const RowJob* jobs, const uint64_t* P,
+                     uint64_t n, void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st,
+                     uint64_t cr = 0) {
+    auto kern = a.idt == IDtype::u32 ? k_csr_copy_tma<uint32_t> : k_csr_copy_tma<uint64_t>;
+    const size_t smem = 2 * kTcStage * kTcWarps;
     static int per_sm[2] = {0, 0};
     int& occ = per_sm[a.idt == IDtype::u32 ? 0 : 1];
-    if (!occ) cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kCopyThreads, 0), "occupancy");
+    if (!occ) {
+        set_smem(kern, smem);
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTcThreads, smem), "occupancy");
+    }
     const uint32_t blocks = static_cast<uint32_t>(std::max(occ, 1) * device_sm_count());
-    const uint32_t n_warps = blocks * (kCopyThreads / 32);
+    const uint32_t n_warps = blocks * kTcWarps;
     const uint32_t is = static_cast<uint32_t>(index_size(a.idt));
     const uint32_t w_idx = std::max(1u, std::min(n_warps - 1, (n_warps * is + (is + vs) / 2) / (is + vs)));
-    launch_k(kern, dim3(blocks), dim3(kCopyThreads), 0, st, "k_csr_copy_flat launch", dev_view(a), vs, refs, jobs, P, n,
-             w_idx, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data), out_gidx);
+    launch_k(kern, dim3(blocks), dim3(kTcThreads), smem, st, "k_csr_copy_tma launch", dev_view(a), vs, refs, jobs, P,
+             n, w_idx, static_cast<uint8_t*>(out_indices), static_cast<uint8_t*>(out_data), out_gidx, cr);
 }
 
 size_t csr_gather_scratch_bytes(uint64_t n_rows) { return scan_status_bytes(n_rows) + n_rows * sizeof(RowJob); }
@@ -1914,28 +1372,15 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
     }
     RowJob* jobs = reinterpret_cast<RowJob*>(static_cast<uint8_t*>(scratch) + scan_status_bytes(n));
     launch_scan(a, refs, n, out_indptr, jobs, out_gidx, scratch, st);
-    const uint32_t vs = static_cast<uint32_t>(value_size(a.vdt));
-    static const bool legacy = [] {
-        const char* e = std::getenv("RFL_GATHER");
-        return e && std::string(e) == "jobs";
-    }();
-    if (!legacy) return launch_copy_flat(a, vs, refs, jobs, out_indptr, n, out_indices, out_data, nullptr, st);
-    const unsigned grid = static_cast<unsigned>(
-        std::min<uint64_t>((2 * n + kCopyThreads / 32 - 1) / (kCopyThreads / 32), 8ull * device_sm_count()));
-    if (a.idt == IDtype::u32)
-        k_csr_copy<uint32_t><<<grid, kCopyThreads, 0, st>>>(jobs, out_indptr, n, vs, static_cast<uint8_t*>(out_indices),
-                                                           static_cast<uint8_t*>(out_data));
-    else
-        k_csr_copy<uint64_t><<<grid, kCopyThreads, 0, st>>>(jobs, out_indptr, n, vs, static_cast<uint8_t*>(out_indices),
-                                                           static_cast<uint8_t*>(out_data));
-    cuda_check(cudaGetLastError(), "k_csr_copy launch");
+    launch_copy_tma(a, static_cast<uint32_t>(value_size(a.vdt)), refs, jobs, out_indptr, n, out_indices, out_data,
+                    nullptr, st);
 }
 
 void launch_csr_gather_prefixed(const ArenaView& a, const RowRef* refs, uint64_t n, const uint64_t* prefix,
                                 void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st) {
     if (a.layout != Layout::csr) invalid("csr_gather: store is not csr");
     if (n == 0) return;
-    launch_copy_flat(a, static_cast<uint32_t>(value_size(a.vdt)), refs, nullptr, prefix, n, out_indices, out_data,
+    launch_copy_tma(a, static_cast<uint32_t>(value_size(a.vdt)), refs, nullptr, prefix, n, out_indices, out_data,
                      out_gidx, st);
 }
 
@@ -1958,7 +1403,7 @@ void launch_csr_pack(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_
         return e && std::string(e) == "warp";
     }();
     if (a.idt == out_idt && !legacy)  // byte-identical index width: the balanced TMA copy in record mode
-        return launch_copy_flat(a, vs, refs, nullptr, prefix, n, out, out, nullptr, st, chunk_rows);
+        return launch_copy_tma(a, vs, refs, nullptr, prefix, n, out, out, nullptr, st, chunk_rows);
     const unsigned grid =
         static_cast<unsigned>(std::min<uint64_t>((n + kPackThreads / 32 - 1) / (kPackThreads / 32), 16ull * device_sm_count()));
     const ArenaDev d = dev_view(a);
@@ -2071,16 +1516,13 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
     const bool flat = in_rb % 16 == 0 && reinterpret_cast<uintptr_t>(a.base) % 16 == 0 &&
                       reinterpret_cast<uintptr_t>(out) % 16 == 0;
     if (flat) {
-        // shape (RFL_DG="<16-B loads per lane>:<threads>", A/B only; profiles/r1_dense_gather.md)
-        static const std::pair<int, int> shape = [] {
-            int u = 0, t = 256;  // u = 0: automatic
-            if (const char* e = std::getenv("RFL_DG")) std::sscanf(e, "%d:%d", &u, &t);
-            return std::make_pair(u, t);
+        // 16-B loads per lane per work unit: 2 (profiles/r1_dense_gather.md: best for both
+        // dense shapes; a one-wave unit of 3 for cfg3 is slower, 0.58 vs 0.62 -- shorter
+        // per-warp chains win over filling the tail wave).  RFL_DG=4 for A/B.
+        static const int u_sel = [] {
+            const char* e = std::getenv("RFL_DG");
+            return e && e[0] == '4' ? 4 : 2;
         }();
-        // automatic = 2 loads per lane: measured best for both dense shapes; a
-        // one-wave unit size (3 for cfg3) is slower (0.58 vs 0.62), shorter
-        // per-warp chains win over filling the tail wave
-        const int u_auto = 2;
         auto go = [&](auto kern, int U, int T) {
             const uint64_t upr = (in_rb / 16 + 32 * U - 1) / (32 * U);
             const uint64_t warps_needed = n * upr;
@@ -2091,14 +1533,7 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         };
         auto pick = [&](auto mode) {
             constexpr int M = decltype(mode)::value;
-            const int u = shape.first ? shape.first : u_auto, t = shape.second;
-            if (u == 3 && t == 256) return go(k_dense_gather_flat<M, 3, 256>, 3, 256);
-            if (u == 6 && t == 256) return go(k_dense_gather_flat<M, 6, 256>, 6, 256);
-            if (u == 4 && t == 256) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
-            if (u == 8 && t == 256) return go(k_dense_gather_flat<M, 8, 256>, 8, 256);
-            if (u == 4 && t == 128) return go(k_dense_gather_flat<M, 4, 128>, 4, 128);
-            if (u == 4 && t == 512) return go(k_dense_gather_flat<M, 4, 512>, 4, 512);
-            if (u == 1 && t == 256) return go(k_dense_gather_flat<M, 1, 256>, 1, 256);
+            if (u_sel == 4) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
             return go(k_dense_gather_flat<M, 2, 256>, 2, 256);
         };
         if (od == OutDtype::bf16 && a.vdt == VDtype::u8) {
