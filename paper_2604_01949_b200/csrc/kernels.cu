@@ -13,6 +13,7 @@
 #include <utility>
 #include <type_traits>
 #include <cstdio>
+#include <cstring>
 
 #include "kernels.cuh"
 
@@ -1219,7 +1220,7 @@ const DensifyCfg& densify_cfg() {
         const char* e = std::getenv("RFL_DENSIFY");
         int v = 0, t = 256, kb = 40, u = 8, mb = 3;
         if (e && std::sscanf(e, "v%d", &v) == 1 && (v == 6 || v == 9)) {
-            const int got = std::sscanf(e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
+            const int got = std::sscanf(std::strchr(e, ':') ? std::strchr(e, ':') : e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
             d.version = v;
             if (got >= 1) d.threads = t;
             if (got >= 2 && kb >= 4 && kb <= 200) d.tile_kb = kb;
