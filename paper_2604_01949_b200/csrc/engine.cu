@@ -4,7 +4,9 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
+#include <thread>
 
 #include "engine.hpp"
 
@@ -131,7 +133,21 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
             }
         }
     }
-    else if (m.layout == Layout::csr) {  // file streaming: only headers + indptrs now
+    img_off_ = rec_off_;
+    img_len_ = rec_len_;
+    if (staging_ == kStreamPinned && m.layout == Layout::csr && m.index_dtype == IDtype::u32 && m.n_var <= 65536) {
+        const char* e = std::getenv("RFL_NARROW");
+        if (!(e && e[0] == '0')) {
+            try {
+                narrow_image();
+            } catch (...) {
+                if (h_image_) cudaFreeHost(h_image_);
+                h_image_ = nullptr;
+                throw;
+            }
+        }
+    }
+    if (m.layout == Layout::csr && staging_ == kStreamFile) {  // file streaming: only headers + indptrs now
         std::vector<uint8_t> buf;
         for (uint64_t q = 0; q < nch; ++q) {
             const uint64_t want = std::min<uint64_t>(
@@ -231,6 +247,51 @@ void DStore::load_records(bool to_device) {
     }
 }
 
+// The pinned staging image with u16 column indices (lossless: n_var <= 65536):
+// 2 of every 8 bytes per stored entry never cross PCIe.  The records were
+// validated in their store encoding first; kernels read this layout through
+// ArenaView::idx16 (csr_row<uint16_t>).
+void DStore::narrow_image() {
+    const Manifest& m = hs_->manifest();
+    const uint64_t nch = m.chunk_count();
+    const uint64_t vs = value_size(m.value_dtype);
+    std::vector<uint64_t> off(nch), len(nch);
+    uint64_t total = 0;
+    for (uint64_t q = 0; q < nch; ++q) {
+        const uint8_t* rec = h_image_ + rec_off_[q];
+        len[q] = idx16_record_bytes(rd32(rec), rd64(rec + 4), vs);
+        off[q] = total;
+        total = align_up(total + len[q], kAlign);
+    }
+    uint8_t* img = nullptr;
+    cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&img), total + kPad, cudaHostAllocPortable), "cudaHostAlloc image");
+    std::memset(img + total, 0, kPad);
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            for (uint64_t q = t; q < nch; q += T) {
+                const uint8_t* src = h_image_ + rec_off_[q];
+                uint8_t* dst = img + off[q];
+                const uint64_t rows = rd32(src), nnz = rd64(src + 4);
+                const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
+                std::memcpy(dst, src, head);  // header + u32 indptr unchanged
+                const uint32_t* si = reinterpret_cast<const uint32_t*>(src + head);
+                uint16_t* di = reinterpret_cast<uint16_t*>(dst + head);
+                for (uint64_t k = 0; k < nnz; ++k) di[k] = static_cast<uint16_t>(si[k]);
+                const uint64_t ib = (2 * nnz + 7) & ~7ull;
+                std::memset(dst + head + 2 * nnz, 0, ib - 2 * nnz);
+                std::memcpy(dst + head + ib, src + head + 4 * nnz, vs * nnz);
+            }
+        });
+    for (auto& th : pool) th.join();
+    cudaFreeHost(h_image_);
+    h_image_ = img;
+    img_off_ = std::move(off);
+    img_len_ = std::move(len);
+    idx16_ = true;
+}
+
 void DStore::validate_records(const uint8_t* base) {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
@@ -273,7 +334,7 @@ uint64_t DStore::max_block_bytes(uint64_t f) const {
     for (uint64_t s = 0; s < m.n_obs; s += f) {
         const uint64_t e = std::min(m.n_obs, s + f);
         uint64_t bytes = 0;
-        for (uint64_t q = s / m.chunk_rows; q <= (e - 1) / m.chunk_rows; ++q) bytes = align_up(bytes + rec_len_[q], kAlign);
+        for (uint64_t q = s / m.chunk_rows; q <= (e - 1) / m.chunk_rows; ++q) bytes = align_up(bytes + img_len_[q], kAlign);
         best = std::max(best, bytes);
     }
     return best;
@@ -288,6 +349,7 @@ ArenaView DStore::view(const uint8_t* base) const {
     a.layout = m.layout;
     a.vdt = m.value_dtype;
     a.idt = m.index_dtype.value_or(IDtype::u32);
+    a.idx16 = idx16_ && staging_ == kStreamPinned;
     return a;
 }
 
@@ -526,7 +588,7 @@ void GpuLoader::stage_block(uint64_t id) {
     uint64_t bytes = 0;
     for (uint64_t q = q0; q <= q1; ++q) {
         lv.chunk_off.push_back(bytes);
-        bytes = align_up(bytes + ds_->rec_len()[q], kAlign);
+        bytes = align_up(bytes + ds_->img_len()[q], kAlign);
     }
     lv.slot = ds_->acquire_slot(block_bytes_);
     lv.live_rows = e - s;
@@ -543,12 +605,12 @@ void GpuLoader::stage_block(uint64_t id) {
     if (ds_->staging() == kStreamPinned) {
         // records of one block are contiguous in the pinned image except for alignment padding;
         // the copies of all blocks fetched for this batch go out as one cudaMemcpyBatchAsync
-        const uint64_t img0 = ds_->rec_off()[q0];
-        const uint64_t img1 = ds_->rec_off()[q1] + ds_->rec_len()[q1];
+        const uint64_t img0 = ds_->img_off()[q0];
+        const uint64_t img1 = ds_->img_off()[q1] + ds_->img_len()[q1];
         batch_dst_.push_back(lv.slot.ptr);
         batch_src_.push_back(const_cast<uint8_t*>(ds_->h_image() + img0));
         batch_size_.push_back(img1 - img0);
-        for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->rec_off()[q] - img0;
+        for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->img_off()[q] - img0;
         ctr_.h2d_bytes += img1 - img0;
         for (uint64_t q = q0; q <= q1; ++q)  // one read op per shard run, as store.cpp:427-447 counts
             if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard) ctr_.read_ops += 1;
@@ -689,7 +751,7 @@ bool GpuLoader::next(BatchOut& out) {
         const char* e = std::getenv("RFL_GATHER");
         return e && std::string(e) == "scan";
     }();
-    const bool planned = m.layout == Layout::csr && dev_.output == 0 && !device_scan;
+    const bool planned = m.layout == Layout::csr && dev_.output == 0 && (!device_scan || ds_->view(nullptr).idx16);
     if (planned) {
         uint64_t acc = 0;
         for (uint64_t i = 0; i < n; ++i) {

@@ -54,6 +54,10 @@ public:
     const uint8_t* h_image() const { return h_image_; }
     const std::vector<uint64_t>& rec_off() const { return rec_off_; }
     const std::vector<uint64_t>& rec_len() const { return rec_len_; }
+    // layout of the staged image (stream_pinned: possibly narrowed, see idx16()); == rec_* otherwise
+    const std::vector<uint64_t>& img_off() const { return img_off_; }
+    const std::vector<uint64_t>& img_len() const { return img_len_; }
+    bool idx16() const { return idx16_; }
     uint64_t image_bytes() const { return image_bytes_; }
     uint64_t row_nnz(uint64_t row) const { return row_nnz_.empty() ? 0 : row_nnz_[row]; }
     uint64_t max_block_bytes(uint64_t f) const;  // staged bytes of the largest f-row block
@@ -76,10 +80,12 @@ public:
 private:
     void load_records(bool to_device);
     void validate_records(const uint8_t* base);
+    void narrow_image();
     std::shared_ptr<HostStore> hs_;
     int device_;
     uint32_t staging_;
-    std::vector<uint64_t> rec_off_, rec_len_;
+    std::vector<uint64_t> rec_off_, rec_len_, img_off_, img_len_;
+    bool idx16_ = false;
     std::vector<uint32_t> row_nnz_;
     uint64_t image_bytes_ = 0;
     uint8_t* d_arena_ = nullptr;

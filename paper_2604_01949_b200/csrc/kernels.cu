@@ -50,6 +50,10 @@ template <>
 __device__ __forceinline__ uint64_t ld_index<uint32_t>(const uint8_t* p) { return ld_u32(p); }
 template <>
 __device__ __forceinline__ uint64_t ld_index<uint64_t>(const uint8_t* p) { return ld_u64_a4(p); }
+template <>
+__device__ __forceinline__ uint64_t ld_index<uint16_t>(const uint8_t* p) {
+    return __ldg(reinterpret_cast<const unsigned short*>(p));
+}
 
 template <typename T>
 __device__ __forceinline__ T ld_value(const uint8_t* p);
@@ -196,17 +200,21 @@ struct CsrRow {
 };
 
 // Locate a row inside its chunk record: [rows u32][nnz u64][indptr][indices][data]
+// IdxT = uint16_t: the narrowed staging layout (u32 indptr, u16 indices padded
+// to 8 B, kernels.cuh ArenaView::idx16).
 template <typename IdxT>
 __device__ __forceinline__ CsrRow csr_row(const ArenaDev& a, const RowRef& r, uint32_t vs) {
+    using PtrT = std::conditional_t<sizeof(IdxT) == 2, uint32_t, IdxT>;
     const uint8_t* rec = a.base + r.rec_off;
     const uint64_t within = r.gidx % a.chunk_rows;
     const uint32_t rows = ld_u32(rec);
     const uint64_t nnz_chunk = ld_u64_a4(rec + 4);
     const uint8_t* ip = rec + kCsrHeaderBytes;
-    const uint64_t lo = ld_index<IdxT>(ip + within * sizeof(IdxT));
-    const uint64_t hi = ld_index<IdxT>(ip + (within + 1) * sizeof(IdxT));
-    const uint8_t* idx_base = ip + (static_cast<uint64_t>(rows) + 1) * sizeof(IdxT);
-    const uint8_t* val_base = idx_base + nnz_chunk * sizeof(IdxT);
+    const uint64_t lo = ld_index<PtrT>(ip + within * sizeof(PtrT));
+    const uint64_t hi = ld_index<PtrT>(ip + (within + 1) * sizeof(PtrT));
+    const uint8_t* idx_base = ip + (static_cast<uint64_t>(rows) + 1) * sizeof(PtrT);
+    const uint64_t idx_bytes = sizeof(IdxT) == 2 ? ((2 * nnz_chunk + 7) & ~7ull) : nnz_chunk * sizeof(IdxT);
+    const uint8_t* val_base = idx_base + idx_bytes;
     return {idx_base + lo * sizeof(IdxT), val_base + lo * vs, hi - lo};
 }
 
@@ -306,6 +314,29 @@ __global__ void __launch_bounds__(kScanThreads)
     __syncthreads();
     if (row < n_rows) out_prefix[row] = s_prefix + incl - nnz;
     if (tid == 0 && (tile + 1) * kScanThreads >= n_rows) out_prefix[n_rows] = s_prefix + agg;
+}
+
+// K2 from narrowed staging (ArenaView::idx16): one warp per row (grid-stride),
+// u16 column ids widened to the store's u32 on the way out, values moved with
+// the shifted 128-bit warp copy; `P` is the host-planned prefix.
+__global__ void __launch_bounds__(256)
+    k_csr_gather_idx16(ArenaDev a, uint32_t vs, const RowRef* __restrict__ refs, const uint64_t* __restrict__ P,
+                       uint64_t n_rows, uint32_t* __restrict__ out_idx, uint8_t* __restrict__ out_val,
+                       uint64_t* __restrict__ out_gidx) {
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * 8;
+    const uint64_t p0 = P[0];
+    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); r < n_rows; r += warps) {
+        const RowRef ref = refs[r];
+        if (lane == 0 && out_gidx) out_gidx[r] = ref.gidx;
+        const CsrRow c = csr_row<uint16_t>(a, ref, vs);
+        const uint64_t off = P[r] - p0, cnt = umin64(P[r + 1] - P[r], c.nnz);
+        const unsigned short* src = reinterpret_cast<const unsigned short*>(c.idx);
+        for (uint64_t k = lane; k < cnt; k += 32) out_idx[off + k] = __ldg(src + k);
+        warp_copy(out_val + off * vs, c.val, cnt * vs, lane);
+    }
 }
 
 // ============================================================ K5 record pack ===
@@ -1264,7 +1295,7 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
         // 40 KB tiles, 3 CTAs/SM (0.81), so a row still fills its tile.
         (void)avg_nnz;
         const bool wide = av.n_var * sizeof(DstT) > 48 * 1024;
-        if constexpr (sizeof(IdxT) == 4) {
+        if constexpr (sizeof(IdxT) <= 4) {
             if (wide) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, 80 << 10);
             return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, 40 << 10);
         } else {  // u64 indices: the v6 register budget
@@ -1367,6 +1398,7 @@ size_t csr_gather_scratch_bytes(uint64_t n_rows) { return scan_status_bytes(n_ro
 void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint64_t* out_indptr, void* out_indices,
                        void* out_data, uint64_t* out_gidx, void* scratch, cudaStream_t st) {
     if (a.layout != Layout::csr) invalid("csr_gather: store is not csr");
+    if (a.idx16) invalid("csr_gather: narrowed staging needs the host-planned indptr (csr_gather_prefixed)");
     if (n == 0) {
         cuda_check(cudaMemsetAsync(out_indptr, 0, sizeof(uint64_t), st), "memset");
         return;
@@ -1381,6 +1413,13 @@ void launch_csr_gather_prefixed(const ArenaView& a, const RowRef* refs, uint64_t
                                 void* out_indices, void* out_data, uint64_t* out_gidx, cudaStream_t st) {
     if (a.layout != Layout::csr) invalid("csr_gather: store is not csr");
     if (n == 0) return;
+    if (a.idx16) {
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 7) / 8, 16ull * device_sm_count()));
+        launch_k(k_csr_gather_idx16, dim3(grid), dim3(256), 0, st, "k_csr_gather_idx16 launch", dev_view(a),
+                 static_cast<uint32_t>(value_size(a.vdt)), refs, prefix, n, static_cast<uint32_t*>(out_indices),
+                 static_cast<uint8_t*>(out_data), out_gidx);
+        return;
+    }
     launch_copy_tma(a, static_cast<uint32_t>(value_size(a.vdt)), refs, nullptr, prefix, n, out_indices, out_data,
                      out_gidx, st);
 }
@@ -1501,7 +1540,8 @@ void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n, OutD
     if (norm && od == OutDtype::native && a.vdt != VDtype::f32)
         invalid("csr_densify: normalize_log1p needs a floating output dtype (f32 or bf16)");
     if (n == 0) return;
-    if (a.idt == IDtype::u32) densify_idx<uint32_t>(a, refs, n, od, norm, target, out, out_gidx, st, avg_nnz);
+    if (a.idx16) densify_idx<uint16_t>(a, refs, n, od, norm, target, out, out_gidx, st, avg_nnz);
+    else if (a.idt == IDtype::u32) densify_idx<uint32_t>(a, refs, n, od, norm, target, out, out_gidx, st, avg_nnz);
     else densify_idx<uint64_t>(a, refs, n, od, norm, target, out, out_gidx, st, avg_nnz);
 }
 

@@ -30,6 +30,10 @@ struct ArenaView {
     Layout layout = Layout::csr;
     VDtype vdt = VDtype::f32;
     IDtype idt = IDtype::u32;
+    // staged records with u16 column indices (the pinned staging image narrows u32
+    // indices when n_var <= 65536): [rows u32][nnz u64][indptr u32 x (rows+1)]
+    // [indices u16 x nnz, zero-padded to 8 B][data]
+    bool idx16 = false;
 };
 
 enum class OutDtype : uint8_t { native = 0, f32 = 1, bf16 = 2 };
@@ -41,6 +45,11 @@ size_t csr_gather_scratch_bytes(uint64_t n_rows);
 void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, uint64_t* out_indptr,
                        void* out_indices, void* out_data, uint64_t* out_gidx, void* scratch,
                        cudaStream_t st);
+
+// Staged-record size of a CSR record with u16 indices (see ArenaView::idx16).
+inline uint64_t idx16_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) {
+    return kCsrHeaderBytes + 4 * (rows + 1) + ((2 * nnz + 7) & ~7ull) + vs * nnz;
+}
 
 // K2 without the device scan: `prefix` (u64[n+1], exclusive nnz prefix of the
 // rows, prefix[0] arbitrary) is the host schedule's, and is the output indptr
