@@ -137,15 +137,7 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     img_len_ = rec_len_;
     if (staging_ == kStreamPinned && m.layout == Layout::csr && m.index_dtype == IDtype::u32 && m.n_var <= 65536) {
         const char* e = std::getenv("RFL_NARROW");
-        if (!(e && e[0] == '0')) {
-            try {
-                narrow_image();
-            } catch (...) {
-                if (h_image_) cudaFreeHost(h_image_);
-                h_image_ = nullptr;
-                throw;
-            }
-        }
+        if (!(e && e[0] == '0')) narrow_image();
     }
     if (m.layout == Layout::csr && staging_ == kStreamFile) {  // file streaming: only headers + indptrs now
         std::vector<uint8_t> buf;
@@ -263,30 +255,34 @@ void DStore::narrow_image() {
         off[q] = total;
         total = align_up(total + len[q], kAlign);
     }
-    uint8_t* img = nullptr;
-    cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&img), total + kPad, cudaHostAllocPortable), "cudaHostAlloc image");
-    std::memset(img + total, 0, kPad);
-    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < T; ++t)
-        pool.emplace_back([&, t] {
-            for (uint64_t q = t; q < nch; q += T) {
-                const uint8_t* src = h_image_ + rec_off_[q];
-                uint8_t* dst = img + off[q];
-                const uint64_t rows = rd32(src), nnz = rd64(src + 4);
-                const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
-                std::memcpy(dst, src, head);  // header + u32 indptr unchanged
-                const uint32_t* si = reinterpret_cast<const uint32_t*>(src + head);
-                uint16_t* di = reinterpret_cast<uint16_t*>(dst + head);
-                for (uint64_t k = 0; k < nnz; ++k) di[k] = static_cast<uint16_t>(si[k]);
-                const uint64_t ib = (2 * nnz + 7) & ~7ull;
-                std::memset(dst + head + 2 * nnz, 0, ib - 2 * nnz);
-                std::memcpy(dst + head + ib, src + head + 4 * nnz, vs * nnz);
-            }
-        });
-    for (auto& th : pool) th.join();
-    cudaFreeHost(h_image_);
-    h_image_ = img;
+    // In place, front to back (no second pinned image): safe when every narrowed
+    // record ends before the next record's old start (it starts at or below its
+    // old offset, and within a record each destination byte lies below every
+    // source byte still to be read).  Only records with < 4 entries can grow
+    // (index padding); if that ever breaks the rule, keep the verbatim image.
+    for (uint64_t q = 0; q < nch; ++q) {
+        const uint64_t next_old = q + 1 < nch ? rec_off_[q + 1] : image_bytes_;
+        if (off[q] > rec_off_[q] || off[q] + len[q] > next_old) return;
+    }
+    for (uint64_t q = 0; q < nch; ++q) {
+        const uint8_t* src = h_image_ + rec_off_[q];
+        uint8_t* dst = h_image_ + off[q];
+        const uint64_t rows = rd32(src), nnz = rd64(src + 4);
+        const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
+        std::memmove(dst, src, head);  // header + u32 indptr unchanged
+        const uint8_t* si = src + head;
+        uint8_t* di = dst + head;
+        for (uint64_t k = 0; k < nnz; ++k) {
+            uint32_t v;
+            std::memcpy(&v, si + 4 * k, 4);
+            const uint16_t w = static_cast<uint16_t>(v);
+            std::memcpy(di + 2 * k, &w, 2);
+        }
+        const uint64_t ib = (2 * nnz + 7) & ~7ull;
+        std::memmove(dst + head + ib, src + head + 4 * nnz, vs * nnz);  // before the pad may overwrite it
+        std::memset(dst + head + 2 * nnz, 0, ib - 2 * nnz);
+    }
+    std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
     img_off_ = std::move(off);
     img_len_ = std::move(len);
     idx16_ = true;
