@@ -1,8 +1,9 @@
 #!/bin/bash
-# dense gather shape sweep (RFL_DG="<loads per lane>:<threads>") + filesystem write calibration
+# dense gather unit sweep (RFL_DG=2|4 loads per lane; the session-3 sweep also had 1/3/6/8 and
+# 128/512-thread CTAs, profiles/r1_dense_gather.md) + filesystem write calibration
 mkdir -p gpurun_out
 T=${1:-s3e}
-for s in 4:256 2:256 8:256 4:128 4:512 1:256; do
+for s in 2 4; do
   echo "== $s" >> gpurun_out/kb_${T}_dg.txt
   RFL_DG=$s timeout 300 python scripts/kbench.py --graph --cases dense_bf16_cfg3,dense_raw_cfg4 >> gpurun_out/kb_${T}_dg.txt 2>&1
 done
