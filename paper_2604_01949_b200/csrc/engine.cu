@@ -137,7 +137,9 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     img_len_ = rec_len_;
     if (staging_ == kStreamPinned && m.layout == Layout::csr && m.index_dtype == IDtype::u32 && m.n_var <= 65536) {
         const char* e = std::getenv("RFL_NARROW");
-        if (!(e && e[0] == '0')) narrow_image();
+        // RFL_NARROW=0: verbatim image; =16: u16 ids only; default: deltas when eligible, else u16
+        const bool off = e && e[0] == '0', only16 = e && std::string(e) == "16";
+        if (!off && (only16 || !delta_image())) narrow_image();
     }
     if (m.layout == Layout::csr && staging_ == kStreamFile) {  // file streaming: only headers + indptrs now
         std::vector<uint8_t> buf;
@@ -243,6 +245,96 @@ void DStore::load_records(bool to_device) {
 // 2 of every 8 bytes per stored entry never cross PCIe.  The records were
 // validated in their store encoding first; kernels read this layout through
 // ArenaView::idx16 (csr_row<uint16_t>).
+// Delta staging image (kernels.cuh d8_*): records whose in-row column gaps are
+// all <= 255 stage as u8 deltas (1 B per stored column id instead of 4), the
+// rest as idx16 records; a kernel expands both into idx16 records in the slot.
+// Checked read-only first (threads), then converted in place front to back
+// through a per-record copy, under the same no-overlap rule as narrow_image()
+// (false: keep the verbatim image for narrow_image()).
+bool DStore::delta_image() {
+    const Manifest& m = hs_->manifest();
+    const uint64_t nch = m.chunk_count();
+    const uint64_t vs = value_size(m.value_dtype);
+    std::vector<uint8_t> elig(nch, 1);  // every in-row gap <= 255 (else the record stages as idx16)
+    {
+        const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                for (uint64_t q = t; q < nch; q += T) {
+                    const uint8_t* rec = h_image_ + rec_off_[q];
+                    const uint64_t rows = rd32(rec);
+                    const uint8_t* ip = rec + kCsrHeaderBytes;
+                    const uint8_t* ix = ip + 4 * (rows + 1);
+                    for (uint64_t r = 0; r < rows && elig[q]; ++r) {
+                        const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+                        for (uint64_t k = lo + 1; k < hi; ++k)
+                            if (rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)) > 255) {
+                                elig[q] = 0;
+                                break;
+                            }
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+    }
+    std::vector<uint64_t> off(nch), len(nch), elen(nch);
+    uint64_t total = 0;
+    for (uint64_t q = 0; q < nch; ++q) {
+        const uint8_t* rec = h_image_ + rec_off_[q];
+        const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
+        elen[q] = idx16_record_bytes(rows, nnz, vs);
+        len[q] = elig[q] ? d8_record_bytes(rows, nnz, vs) : elen[q];
+        off[q] = total;
+        total = align_up(total + len[q], kAlign);
+    }
+    for (uint64_t q = 0; q < nch; ++q) {
+        const uint64_t next_old = q + 1 < nch ? rec_off_[q + 1] : image_bytes_;
+        if (off[q] > rec_off_[q] || off[q] + len[q] > next_old) return false;
+    }
+    std::vector<uint8_t> tmp;
+    for (uint64_t q = 0; q < nch; ++q) {
+        tmp.assign(h_image_ + rec_off_[q], h_image_ + rec_off_[q] + rec_len_[q]);
+        const uint8_t* src = tmp.data();
+        uint8_t* dst = h_image_ + off[q];
+        const uint64_t rows = rd32(src), nnz = rd64(src + 4);
+        const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
+        std::memcpy(dst, src, head);
+        const uint8_t* ip = src + kCsrHeaderBytes;
+        const uint8_t* ix = src + head;
+        if (!elig[q]) {  // idx16 record
+            for (uint64_t k = 0; k < nnz; ++k) {
+                const uint16_t w = static_cast<uint16_t>(rd32(ix + 4 * k));
+                std::memcpy(dst + head + 2 * k, &w, 2);
+            }
+            const uint64_t ib = (2 * nnz + 7) & ~7ull;
+            std::memset(dst + head + 2 * nnz, 0, ib - 2 * nnz);
+            std::memcpy(dst + head + ib, src + head + 4 * nnz, vs * nnz);
+            continue;
+        }
+        uint8_t* first = dst + head;
+        uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
+        std::memset(first, 0, delta - first);
+        for (uint64_t r = 0; r < rows; ++r) {
+            const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+            const uint16_t f = lo < hi ? static_cast<uint16_t>(rd32(ix + 4 * lo)) : 0;
+            std::memcpy(first + 2 * r, &f, 2);
+            for (uint64_t k = lo; k < hi; ++k)
+                delta[k] = k == lo ? 0 : static_cast<uint8_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)));
+        }
+        const uint64_t voff = d8_values_offset(rows, nnz);
+        std::memset(delta + nnz, 0, voff - (delta - dst) - nnz);
+        std::memcpy(dst + voff, src + head + 4 * nnz, vs * nnz);
+    }
+    std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
+    img_off_ = std::move(off);
+    img_len_ = std::move(len);
+    exp_len_ = std::move(elen);
+    d8_rec_ = std::move(elig);
+    idx16_ = d8_ = true;
+    return true;
+}
+
 void DStore::narrow_image() {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
@@ -330,7 +422,10 @@ uint64_t DStore::max_block_bytes(uint64_t f) const {
     for (uint64_t s = 0; s < m.n_obs; s += f) {
         const uint64_t e = std::min(m.n_obs, s + f);
         uint64_t bytes = 0;
-        for (uint64_t q = s / m.chunk_rows; q <= (e - 1) / m.chunk_rows; ++q) bytes = align_up(bytes + img_len_[q], kAlign);
+        for (uint64_t q = s / m.chunk_rows; q <= (e - 1) / m.chunk_rows; ++q) {
+            bytes = align_up(bytes + img_len_[q], kAlign);
+            if (d8_) bytes = align_up(bytes + exp_len_[q], kAlign);  // expanded records + staged deltas
+        }
         best = std::max(best, bytes);
     }
     return best;
@@ -581,10 +676,11 @@ void GpuLoader::stage_block(uint64_t id) {
     Live& lv = live_[id];
     lv.first_chunk = q0;
     lv.chunk_off.clear();
+    const bool d8 = ds_->staging() == kStreamPinned && ds_->d8();
     uint64_t bytes = 0;
     for (uint64_t q = q0; q <= q1; ++q) {
         lv.chunk_off.push_back(bytes);
-        bytes = align_up(bytes + ds_->img_len()[q], kAlign);
+        bytes = align_up(bytes + (d8 ? ds_->exp_len()[q] : ds_->img_len()[q]), kAlign);
     }
     lv.slot = ds_->acquire_slot(block_bytes_);
     lv.live_rows = e - s;
@@ -603,10 +699,17 @@ void GpuLoader::stage_block(uint64_t id) {
         // the copies of all blocks fetched for this batch go out as one cudaMemcpyBatchAsync
         const uint64_t img0 = ds_->img_off()[q0];
         const uint64_t img1 = ds_->img_off()[q1] + ds_->img_len()[q1];
-        batch_dst_.push_back(lv.slot.ptr);
+        uint8_t* land = d8 ? lv.slot.ptr + bytes : lv.slot.ptr;  // delta records land after the expanded area
+        batch_dst_.push_back(land);
         batch_src_.push_back(const_cast<uint8_t*>(ds_->h_image() + img0));
         batch_size_.push_back(img1 - img0);
-        for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->img_off()[q] - img0;
+        if (d8) {
+            for (uint64_t q = q0; q <= q1; ++q)
+                d8_jobs_.push_back({land + (ds_->img_off()[q] - img0), lv.slot.ptr + lv.chunk_off[q - q0],
+                                    ds_->d8_record(q) ? 0 : ds_->exp_len()[q]});
+        } else {
+            for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->img_off()[q] - img0;
+        }
         ctr_.h2d_bytes += img1 - img0;
         for (uint64_t q = q0; q <= q1; ++q)  // one read op per shard run, as store.cpp:427-447 counts
             if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard) ctr_.read_ops += 1;
@@ -701,6 +804,7 @@ bool GpuLoader::next(BatchOut& out) {
         batch_src_.clear();
         batch_size_.clear();
         pend_ev_ = nullptr;
+        d8_jobs_.clear();
         for (uint64_t id : consumed_) stage_block(id);
         if (pend_ev_ && cudaEventQuery(pend_ev_) != cudaSuccess)
             cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");        if (!batch_dst_.empty()) {
@@ -760,6 +864,10 @@ bool GpuLoader::next(BatchOut& out) {
     }
     cuda_ok(cudaEventRecord(staged_, copy_), "event");
     cuda_ok(cudaStreamWaitEvent(compute_, staged_, 0), "wait staged");
+    // delta-staged records expand into idx16 records on the compute stream, so the
+    // copy stream goes straight on to the next batch's blocks
+    if (!d8_jobs_.empty())
+        launch_d8_decode(d8_jobs_.data(), d8_jobs_.size(), static_cast<uint32_t>(value_size(m.value_dtype)), compute_);
 
     const ArenaView av = ds_->view(base);
     if (m.layout == Layout::dense) {

@@ -58,6 +58,11 @@ public:
     const std::vector<uint64_t>& img_off() const { return img_off_; }
     const std::vector<uint64_t>& img_len() const { return img_len_; }
     bool idx16() const { return idx16_; }
+    // delta staging (kernels.cuh d8_*): img_* describe the staged delta records,
+    // exp_len the idx16 records they expand to in a slot
+    bool d8() const { return d8_; }
+    bool d8_record(uint64_t q) const { return d8_rec_[q] != 0; }  // else staged as idx16
+    const std::vector<uint64_t>& exp_len() const { return exp_len_; }
     uint64_t image_bytes() const { return image_bytes_; }
     uint64_t row_nnz(uint64_t row) const { return row_nnz_.empty() ? 0 : row_nnz_[row]; }
     uint64_t max_block_bytes(uint64_t f) const;  // staged bytes of the largest f-row block
@@ -81,11 +86,14 @@ private:
     void load_records(bool to_device);
     void validate_records(const uint8_t* base);
     void narrow_image();
+    bool delta_image();
     std::shared_ptr<HostStore> hs_;
     int device_;
     uint32_t staging_;
     std::vector<uint64_t> rec_off_, rec_len_, img_off_, img_len_;
-    bool idx16_ = false;
+    bool idx16_ = false, d8_ = false;
+    std::vector<uint64_t> exp_len_;
+    std::vector<uint8_t> d8_rec_;
     std::vector<uint32_t> row_nnz_;
     uint64_t image_bytes_ = 0;
     uint8_t* d_arena_ = nullptr;
@@ -198,6 +206,7 @@ private:
     std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead
     uint64_t read_seq_ = 0;
     std::vector<void*> batch_dst_, batch_src_;  // stream_pinned copies of one next(), one cudaMemcpyBatchAsync
+    std::vector<D8Job> d8_jobs_;                 // delta-staged records of this next() to expand
     std::vector<size_t> batch_size_;
     Counters ctr_;
     bool done_ = false;

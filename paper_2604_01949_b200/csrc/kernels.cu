@@ -339,6 +339,64 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Delta-staged record -> idx16 record (kernels.cuh d8_*), one CTA per record:
+// header + indptr and the values are copied word-wise; each warp rebuilds its
+// rows' u16 columns with a warp inclusive scan of the u8 deltas (carry = the
+// row's first column).
+constexpr int kMaxD8Jobs = 128;
+struct D8Jobs {
+    uint32_t n, vs;
+    D8Job job[kMaxD8Jobs];
+};
+
+constexpr uint32_t kD8Split = 8;  // CTAs per record (blockIdx.y)
+
+__global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Jobs jobs) {
+    pdl_wait();
+    pdl_trigger();
+    const D8Job jb = jobs.job[blockIdx.x];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t tid = blockIdx.y * 256 + threadIdx.x;  // within the record's CTAs
+    constexpr uint32_t nt = kD8Split * 256;
+    if (jb.bytes) {  // staged as idx16 already (16-B aligned, 16-B multiple incl. padding reads)
+        const uint4* s4 = reinterpret_cast<const uint4*>(jb.src);
+        uint4* d4 = reinterpret_cast<uint4*>(jb.dst);
+        for (uint64_t i = tid; i < (jb.bytes + 15) / 16; i += nt) d4[i] = ld_v4(s4 + i);
+        return;
+    }
+    const uint64_t rows = ld_u32(jb.src), nnz = ld_u64_a4(jb.src + 4);
+    const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
+    const uint32_t* s32 = reinterpret_cast<const uint32_t*>(jb.src);
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(jb.dst);
+    for (uint64_t i = tid; i < head / 4; i += nt) d32[i] = __ldg(s32 + i);
+    const uint8_t* first = jb.src + head;
+    const uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
+    const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
+    const uint64_t vbytes = nnz * jobs.vs;
+    const uint8_t* sv = jb.src + voff;
+    uint8_t* dv = jb.dst + head + ((2 * nnz + 7) & ~7ull);
+    for (uint64_t i = tid; i < vbytes / 4; i += nt)
+        reinterpret_cast<uint32_t*>(dv)[i] = __ldg(reinterpret_cast<const uint32_t*>(sv) + i);
+    for (uint64_t i = (vbytes & ~3ull) + tid; i < vbytes; i += nt) dv[i] = sv[i];
+    const uint8_t* ip = jb.src + kCsrHeaderBytes;
+    uint16_t* out = reinterpret_cast<uint16_t*>(jb.dst + head);
+    for (uint64_t r = blockIdx.y * 8 + warp; r < rows; r += kD8Split * 8) {
+        const uint64_t lo = ld_u32(ip + 4 * r), hi = ld_u32(ip + 4 * (r + 1));
+        uint32_t carry = __ldg(reinterpret_cast<const unsigned short*>(first) + r);
+        for (uint64_t base = lo; base < hi; base += 32) {
+            const uint64_t k = base + lane;
+            uint32_t v = k < hi ? __ldg(delta + k) : 0u;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, v, o);
+                if (lane >= static_cast<uint32_t>(o)) v += t;
+            }
+            const uint32_t col = carry + v;
+            if (k < hi) out[k] = static_cast<uint16_t>(col);
+            carry = __shfl_sync(kFull, col, 31);
+        }
+    }
+}
+
 // ============================================================ K5 record pack ===
 template <typename T>
 __device__ __forceinline__ void st_any(uint8_t* p, T v) {  // little-endian store at any alignment
@@ -1407,6 +1465,16 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
     launch_scan(a, refs, n, out_indptr, jobs, out_gidx, scratch, st);
     launch_copy_tma(a, static_cast<uint32_t>(value_size(a.vdt)), refs, jobs, out_indptr, n, out_indices, out_data,
                     nullptr, st);
+}
+
+void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, cudaStream_t st) {
+    for (size_t k0 = 0; k0 < n; k0 += kMaxD8Jobs) {
+        D8Jobs j{};
+        j.n = static_cast<uint32_t>(std::min<size_t>(kMaxD8Jobs, n - k0));
+        j.vs = vs;
+        for (uint32_t i = 0; i < j.n; ++i) j.job[i] = jobs[k0 + i];
+        launch_k(k_d8_decode, dim3(j.n, kD8Split), dim3(256), 0, st, "k_d8_decode launch", j);
+    }
 }
 
 void launch_csr_gather_prefixed(const ArenaView& a, const RowRef* refs, uint64_t n, const uint64_t* prefix,

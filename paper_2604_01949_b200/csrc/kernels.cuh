@@ -51,6 +51,24 @@ inline uint64_t idx16_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) {
     return kCsrHeaderBytes + 4 * (rows + 1) + ((2 * nnz + 7) & ~7ull) + vs * nnz;
 }
 
+// Delta staging (the pinned image when every in-row column gap is <= 255): per
+// record [rows u32][nnz u64][indptr u32 x (rows+1)][first column u16 x rows,
+// padded to 4 B][column deltas u8 x nnz (0 for a row's first entry), padded to
+// 8 B from the record start][data].  5 B per stored f32 entry cross PCIe; a
+// decode kernel expands each staged record into the idx16 layout in HBM.
+inline uint64_t d8_values_offset(uint64_t rows, uint64_t nnz) {
+    const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
+    return (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
+}
+inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) { return d8_values_offset(rows, nnz) + vs * nnz; }
+struct D8Job {
+    const uint8_t* src;  // staged record (device): delta layout, or idx16 already when bytes != 0
+    uint8_t* dst;        // idx16 record (device)
+    uint64_t bytes;      // 0: expand a delta record; else copy `bytes` (a record with a gap > 255)
+};
+// expand n staged delta records (value size vs) into idx16 records
+void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, cudaStream_t st);
+
 // K2 without the device scan: `prefix` (u64[n+1], exclusive nnz prefix of the
 // rows, prefix[0] arbitrary) is the host schedule's, and is the output indptr
 // when rebased to 0 (the loader uploads it straight into its indptr slot).
