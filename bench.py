@@ -10,9 +10,11 @@ densify to fp32.
            step's row references precomputed on the device; K timed launches
            of the densify kernel.  Whole-job cells/s = N * cells / max-rank time.
   e2e    — the same metric through the public API (BatchIterator.next()) with
-           the store in pinned host memory: every step stages the fetched
-           blocks host->device (cudaMemcpyAsync), replays the schedule on the
-           host, assembles, and reads the batch's global_indices back.
+           the store in pinned host memory (re-encoded at open with u8 column
+           deltas / u16 ids, lossless): every step stages the fetched blocks
+           host->device (cudaMemcpyAsync), expands them on the GPU, replays the
+           schedule on the host, assembles, and reads the batch's
+           global_indices back.
 
 Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
         [--workload cfg1|cfg2|cfg3|cfg4]; N>1 under torchrun (one rank/GPU).
@@ -386,7 +388,8 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
     ds.close()
     return {"value": world * cells / (t_max / 1e3), "unit": "cells/s",
             "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": 8 * cells / K,
-            "staging": ("stream_pinned (records in pinned host RAM; blocks cudaMemcpyAsync'd per fetch)"
+            "staging": ("stream_pinned (records in pinned host RAM, re-encoded losslessly at open: u8 column "
+                        "deltas or u16 ids; each fetched block cudaMemcpyAsync'd, expanded on the GPU)"
                         if staging == "stream_pinned" else
                         "stream_file (BlockReader: prefetch_depth I/O threads pread the fetch order from the shard "
                         "files into pinned buffers; blocks cudaMemcpyAsync'd per fetch)"),
