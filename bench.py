@@ -349,12 +349,14 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
     it = make_it(epoch)
     host = torch.empty(W["loader"]["batch_rows"], dtype=torch.int64).pin_memory()
     h2d_done = [0]  # bytes staged by iterators already retired
+    k_done = [0]    # kernels launched by iterators already retired
 
     def step():
         nonlocal it, epoch
         b = it.next()
         if b is None:
             h2d_done[0] += it.counters().h2d_bytes
+            k_done[0] += it.counters().kernels_launched
             it.close()
             epoch += 1
             it = make_it(epoch)
@@ -366,6 +368,7 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
         step()
     torch.cuda.synchronize()
     h2d0 = h2d_done[0] + it.counters().h2d_bytes
+    k0 = k_done[0] + it.counters().kernels_launched
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
@@ -383,6 +386,7 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
     wall = time.perf_counter() - t0
     ms = s_ev.elapsed_time(e_ev)
     h2d = h2d_done[0] + it.counters().h2d_bytes - h2d0
+    launches = k_done[0] + it.counters().kernels_launched - k0
     t_max = allreduce_max(max(ms, wall * 1e3), dist)
     it.close()
     ds.close()
@@ -394,7 +398,7 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist):
                         "stream_file (BlockReader: prefetch_depth I/O threads pread the fetch order from the shard "
                         "files into pinned buffers; blocks cudaMemcpyAsync'd per fetch)"),
             "api": "paper_2604_01949_b200.BatchIterator.next -> rfl_loader_next",
-            "gpu_launches": K}
+            "gpu_launches": launches}
 
 
 def cpu_baseline(path, W, threads):

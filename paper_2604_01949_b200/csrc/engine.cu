@@ -866,8 +866,10 @@ bool GpuLoader::next(BatchOut& out) {
     cuda_ok(cudaStreamWaitEvent(compute_, staged_, 0), "wait staged");
     // delta-staged records expand into idx16 records on the compute stream, so the
     // copy stream goes straight on to the next batch's blocks
-    if (!d8_jobs_.empty())
+    if (!d8_jobs_.empty()) {
         launch_d8_decode(d8_jobs_.data(), d8_jobs_.size(), static_cast<uint32_t>(value_size(m.value_dtype)), compute_);
+        ctr_.kernels_launched += (d8_jobs_.size() + kMaxD8Jobs - 1) / kMaxD8Jobs;
+    }
 
     const ArenaView av = ds_->view(base);
     if (m.layout == Layout::dense) {

@@ -343,7 +343,6 @@ __global__ void __launch_bounds__(256)
 // header + indptr and the values are copied word-wise; each warp rebuilds its
 // rows' u16 columns with a warp inclusive scan of the u8 deltas (carry = the
 // row's first column).
-constexpr int kMaxD8Jobs = 128;
 struct D8Jobs {
     uint32_t n, vs;
     D8Job job[kMaxD8Jobs];

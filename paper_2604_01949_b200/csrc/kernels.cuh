@@ -66,7 +66,8 @@ struct D8Job {
     uint8_t* dst;        // idx16 record (device)
     uint64_t bytes;      // 0: expand a delta record; else copy `bytes` (a record with a gap > 255)
 };
-// expand n staged delta records (value size vs) into idx16 records
+// expand n staged delta records (value size vs) into idx16 records (one launch per kMaxD8Jobs)
+constexpr size_t kMaxD8Jobs = 128;
 void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, cudaStream_t st);
 
 // K2 without the device scan: `prefix` (u64[n+1], exclusive nnz prefix of the
