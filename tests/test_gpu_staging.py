@@ -1,0 +1,90 @@
+"""The re-encoded pinned staging image ("Narrowed staging image"):
+delta records (u8 column deltas), idx16 records and the verbatim image must all
+give the reference's batches bit for bit.  The store is built so that every
+boundary is hit: n_var = 65,536 (largest column id 65,535 still fits u16), a
+gap of exactly 255 (delta) next to records with a gap of 256 (idx16 fallback),
+empty rows, single-entry rows, first columns at 0 and at 65,535."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_01949_b200 as R
+from oracle.oracle import csr_gather, normalize_log1p, to_dense, write_csr_store
+
+pytestmark = pytest.mark.gpu
+
+NV = 65536
+
+
+def _rows(rng, n):
+    rows = []
+    for i in range(n):
+        kind = i % 7
+        if kind == 0:
+            cols = []                                        # empty row
+        elif kind == 1:
+            cols = [NV - 1]                                  # single entry at the last column
+        elif kind == 2:
+            cols = [0, 255, 510, 765]                        # gaps of exactly 255
+        elif kind == 3 and (i // 7) % 3 == 0:
+            cols = [5, 261, 300, 65535]                      # a gap of 256 (and 65,235): idx16 record
+        else:
+            start = int(rng.integers(0, NV - 12000))
+            gaps = rng.integers(1, 256, int(rng.integers(20, 40)))
+            cols = list(start + np.cumsum(gaps))
+        rows.append(np.asarray(cols, np.uint64))
+    return rows
+
+
+@pytest.fixture(scope="module")
+def crafted(tmp_path_factory):
+    rng = np.random.default_rng(7)
+    rows = _rows(rng, 336)
+    ip = np.zeros(len(rows) + 1, np.uint64)
+    ip[1:] = np.cumsum([len(r) for r in rows])
+    ix = np.concatenate(rows).astype(np.uint64)
+    dv = (rng.random(len(ix)) + 0.25).astype(np.float32)
+    path = tmp_path_factory.mktemp("staging") / "s"
+    write_csr_store(path, ip, ix, dv, NV, 16, 8)
+    return path, ip, ix, dv
+
+
+@pytest.mark.parametrize("mode", ["delta", "16", "0"])
+def test_staging_encodings_bit_exact(crafted, mode):
+    path, ip, ix, dv = crafted
+    old = os.environ.get("RFL_NARROW")
+    if mode != "delta":
+        os.environ["RFL_NARROW"] = mode
+    try:
+        ds = R.DeviceStore(path, 0, "stream_pinned")
+    finally:
+        if old is None:
+            os.environ.pop("RFL_NARROW", None)
+        else:
+            os.environ["RFL_NARROW"] = old
+    cfg = R.LoaderConfig(16, 96, 40, 3)
+    for out, xf in (("csr", None), ("dense", None), ("dense", "normalize_log1p")):
+        it = R.BatchIterator(ds, cfg, 1, output=out, transform=xf)
+        for b in it:
+            g = b.global_indices_host
+            eip, eix, edv = csr_gather(ip, ix, dv, g)
+            if out == "csr":
+                mb = b.to_minibatch()
+                assert (np.asarray(mb.block.indptr, np.uint64) == eip).all()
+                assert (np.asarray(mb.block.indices, np.uint64) == eix).all()
+                assert np.asarray(mb.block.data).tobytes() == edv.tobytes()
+            elif xf is None:
+                assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, NV).tobytes()
+            else:
+                want = normalize_log1p(to_dense(eip, eix, edv, NV))
+                np.testing.assert_allclose(b.data.cpu().numpy().astype(np.float64), want, rtol=1e-6, atol=0)
+        c = it.counters()
+        if mode == "0":
+            assert c.h2d_bytes >= c.bytes_read  # verbatim records (+ row refs)
+        else:
+            assert c.h2d_bytes < c.bytes_read
+        it.close()
+    ds.close()
+    torch.cuda.synchronize()
