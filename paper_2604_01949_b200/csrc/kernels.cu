@@ -2,8 +2,10 @@
 //
 // Data layout in HBM: the arena holds riffle chunk records verbatim
 // (store.cpp:52-64 for CSR, row-major rows for dense), each placed at a 16-B
-// aligned offset.  A batch is described by one RowRef per output row, so the
-// same kernels serve the HBM-resident store and the streamed block arena.
+// aligned offset; streamed slots from the pinned staging image hold idx16
+// records (u16 column ids, ArenaView::idx16).  A batch is described by one
+// RowRef per output row, so the same kernels serve the HBM-resident store and
+// the streamed block arena.
 #include <cuda_bf16.h>
 
 #include <algorithm>

@@ -1,14 +1,18 @@
 // sm_100a kernels of the minibatch-assembly / pre-shuffle hot path.
 //
-//   K1/K2 csr_gather   rows -> CSR block, fused decoupled-look-back indptr scan
-//                      + warp-cooperative 128-bit shifted gathers
+//   K1 row_scan        decoupled-look-back indptr scan over the rows' nnz (raw
+//                      csr_gather without a host prefix, pre-shuffle rounds)
+//   K2 csr_copy_tma    rows -> CSR block: equal 16-B aligned byte ranges per warp,
+//                      1-D TMA bulk loads into shared stages, aligned 16-B stores
 //                      (CsrBuffer::take/append loader.cpp:126-155, read_rows_csr
-//                      store.cpp:590-614, CsrBlock::append_rows block.cpp:92-108)
-//   K3 csr_densify     rows -> dense tile built in shared memory, written once
+//                      store.cpp:590-614, CsrBlock::append_rows block.cpp:92-108);
+//                      in record mode it is also K5 (encode_csr_record store.cpp:52-64)
+//   K3 csr_densify9    rows -> dense tile built in shared memory, written once
 //                      with cp.async.bulk (TMA bulk) stores; optional fused
 //                      library-size normalisation + log1p (to_dense block.cpp:135-146)
 //   K4 dense_gather    dense rows -> batch with optional u8/f32 -> bf16 cast
 //                      (DenseBuffer::take loader.cpp:105-117)
+//   d8_decode          staged delta records -> idx16 records (pinned staging image)
 #pragma once
 #include <cuda_runtime.h>
 
