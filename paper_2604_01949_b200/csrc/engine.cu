@@ -487,9 +487,38 @@ void DStore::release_slot(const SlotRef& s) {
 }
 
 // ============================================================ BlockReader ===
+namespace {
+// CsrBlock::validate's column checks (block.cpp:110-133) on a record whose header
+// and indptr were already checked: every id < n_var, strictly increasing per row
+bool columns_ok(const Manifest& m, uint64_t q, const uint8_t* rec) {
+    const uint64_t rows = rd32(rec);
+    const uint8_t* ip = rec + kCsrHeaderBytes;
+    if (m.index_dtype == IDtype::u32) {
+        const uint8_t* ix = ip + 4 * (rows + 1);
+        const uint32_t nv = m.n_var > 0xFFFFFFFFull ? 0xFFFFFFFFu : static_cast<uint32_t>(m.n_var);
+        for (uint64_t r = 0; r < rows; ++r) {
+            const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+            if (lo == hi) continue;
+            // branch-free, vectorisable: any id >= n_var, any id <= its predecessor
+            uint32_t bad = rd32(ix + 4 * lo) >= nv;
+            for (uint64_t k = lo + 1; k < hi; ++k) {
+                const uint32_t c = rd32(ix + 4 * k), p = rd32(ix + 4 * (k - 1));
+                bad |= static_cast<uint32_t>(c >= nv) | static_cast<uint32_t>(c <= p);
+            }
+            if (bad) return false;
+        }
+        return true;
+    }
+    (void)q;
+    return false;  // u64 ids: the full check (rare layout)
+}
+}  // namespace
+
 BlockReader::BlockReader(std::shared_ptr<DStore> ds, std::vector<uint64_t> order, uint64_t f, uint32_t threads,
                          uint32_t slots, bool direct)
     : ds_(std::move(ds)), order_(std::move(order)), f_(f), direct_(direct) {
+    const char* nv = std::getenv("RFL_NO_VALIDATE");
+    validate_ = ds_->manifest().layout == Layout::csr && !(nv && nv[0] == '1');
     const Manifest& m = ds_->manifest();
     // a block's records, each run read as its 4 KiB-aligned superset into a page-aligned position
     const uint64_t bytes = ds_->max_block_bytes(f) + (f / m.chunk_rows + 2) * 3 * 4096;
@@ -556,6 +585,10 @@ void BlockReader::worker() {
                 const uint64_t lead = hs.read_shard_span(shard, first.off, b.buf + cursor, run, direct_);
                 for (uint64_t x = q, rel = 0; x < end; ++x) {
                     b.pos[x - q0] = cursor + lead + rel;
+                    // decode_record validates every fetched record (store.cpp:116-120); headers and
+                    // indptrs were checked at open, the columns are checked here, per fetch
+                    if (validate_ && !columns_ok(m, x, b.buf + b.pos[x - q0]))
+                        full_check_csr_record(m, x, b.buf + b.pos[x - q0], ds_->rec_len()[x]);
                     rel += ds_->rec_len()[x];
                 }
                 cursor += (HostStore::aligned_span(first.off, run) + 4095) & ~4095ull;

@@ -130,6 +130,7 @@ private:
     std::vector<uint64_t> order_;
     uint64_t f_;
     bool direct_;
+    bool validate_ = true;  // column checks of every fetched CSR record
     std::vector<Block> slots_;
     std::vector<cudaEvent_t> ev_;
     std::vector<uint64_t> released_;  // per slot: last seq released (~0: none)

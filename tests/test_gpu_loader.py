@@ -241,6 +241,30 @@ def test_corrupt_indices_raise_like_reference(tmp_path, staging, bad):
     assert str(ours.value) in str(ref.value)
 
 
+@pytest.mark.parametrize("bad", ["range", "order"])
+def test_corrupt_indices_stream_file_raise_at_fetch(tmp_path, bad):
+    """stream_file checks columns per fetch, as decode_record does (store.cpp:116-120):
+    the fetch of the bad block raises IoError naming the block (loader.cpp:70-73)
+    around the reference's CorruptStore text; earlier batches come out intact."""
+    ip = np.arange(0, 8 * 2 + 1, 2, dtype=np.uint64)  # 8 rows x 2 entries, chunk_rows 2
+    ix = np.tile(np.array([1, 3], np.uint64), 8)
+    if bad == "range":
+        ix[13] = 500   # row 6
+    else:
+        ix[13] = 1     # row 6: 1, 1
+    dv = np.arange(16, dtype=np.float32)
+    write_csr_store(tmp_path / "s", ip, ix, dv, 10, 2, 2)
+    with pytest.raises(RuntimeError) as ref:
+        Ref.read_rows_csr(tmp_path / "s", [(6, 8)])
+    it = R.BatchIterator(tmp_path / "s", R.LoaderConfig(2, 2, 2, 0, prefetch_depth=2), 0, staging="stream_file")
+    with pytest.raises(R.IoError) as ours:
+        for _ in it:
+            pass
+    msg = str(ours.value)
+    assert "fetch block [6, 8)" in msg
+    assert msg.split("): ", 1)[1] in str(ref.value)
+
+
 @pytest.mark.parametrize("staging", ["resident", "stream_pinned", "stream_file"])
 @pytest.mark.parametrize("bad", ["indptr", "tail", "header"])
 def test_corrupt_indptr_raise_like_reference(tmp_path, staging, bad):
