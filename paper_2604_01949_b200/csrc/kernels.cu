@@ -1263,6 +1263,72 @@ __global__ void __launch_bounds__(kDgThreads)
     }
 }
 
+// Same work units, but each warp converts its unit into a shared-memory slice
+// and one lane writes it with a 1-D TMA bulk store (the store path that wins
+// for densify's write-heavy mix, profiles/r1_densify_v9.md).  A/B: RFL_DG=b.
+template <int MODE, int kDgU = 2, int kDgThreads = 256>
+__global__ void __launch_bounds__(kDgThreads)
+    k_dense_gather_bulk(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
+                        uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx) {
+    constexpr uint32_t kOutPerIn = MODE == kU8ToBf16 ? 2 : 1;  // (f32 -> bf16 halves; not used here)
+    constexpr uint32_t kSlice = 32 * kDgU * 16 * kOutPerIn;
+    __shared__ __align__(128) uint8_t s_out[(kDgThreads / 32) * kSlice];
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint8_t* slice = s_out + warp * kSlice;
+    const uint64_t cpr = in_row_bytes / 16;
+    const uint64_t upr = (cpr + 32 * kDgU - 1) / (32 * kDgU);
+    const uint64_t n_units = n_rows * upr;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kDgThreads / 32);
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * (kDgThreads / 32) + warp; u < n_units; u += warps) {
+        const uint64_t row = u / upr, part = u - row * upr;
+        uint64_t off = 0, g = 0;
+        if (lane == 0) {
+            const RowRef r = refs[row];
+            off = r.rec_off + (r.gidx % a.chunk_rows) * in_row_bytes;
+            g = r.gidx;
+        }
+        off = __shfl_sync(kFull, off, 0);
+        if (part == 0 && lane == 0 && out_gidx) out_gidx[row] = g;
+        const uint4* src = reinterpret_cast<const uint4*>(a.base + off);
+        const uint64_t cbase = part * 32 * kDgU;
+        const uint64_t nvec = umin64(32 * kDgU, cpr - cbase);  // 16-B input chunks of this unit
+        uint4 v[kDgU];
+#pragma unroll
+        for (int k = 0; k < kDgU; ++k)
+            if (k * 32 + lane < nvec) v[k] = ld_v4(src + cbase + k * 32 + lane);
+        if (lane == 0) bulk_wait_read0();  // the slice's previous bulk store has read it
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kDgU; ++k) {
+            const uint32_t c = k * 32 + lane;
+            if (c >= nvec) break;
+            if (MODE == kRaw) {
+                *reinterpret_cast<uint4*>(slice + c * 16) = v[k];
+            } else {
+                const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                uint32_t o[8];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    o[2 * j] = pack_bf16x2(float(w[j] & 0xff), float((w[j] >> 8) & 0xff));
+                    o[2 * j + 1] = pack_bf16x2(float((w[j] >> 16) & 0xff), float(w[j] >> 24));
+                }
+                *reinterpret_cast<uint4*>(slice + c * 32) = make_uint4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<uint4*>(slice + c * 32 + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+        }
+        fence_proxy_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+            bulk_store(out + row * out_row_bytes + cbase * 16 * kOutPerIn, slice,
+                       static_cast<uint32_t>(nvec * 16 * kOutPerIn));
+            bulk_commit();
+        }
+    }
+    if (lane == 0) bulk_wait0();
+}
+
 // ------------------------------------------------------------ host helpers ---
 int g_sm_count = 0;
 std::once_flag g_sm_once;
@@ -1631,7 +1697,9 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         // per-warp chains win over filling the tail wave).  RFL_DG=4 for A/B.
         static const int u_sel = [] {
             const char* e = std::getenv("RFL_DG");
-            return e && e[0] == '4' ? 4 : 2;
+            if (!e) return 0;  // automatic
+            if (e[0] == 'b') return e[1] == '4' ? -4 : -2;  // TMA bulk-store variant, 2 or 4 loads per lane
+            return e[0] == '4' ? 4 : 2;
         }();
         auto go = [&](auto kern, int U, int T) {
             const uint64_t upr = (in_rb / 16 + 32 * U - 1) / (32 * U);
@@ -1644,6 +1712,12 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         auto pick = [&](auto mode) {
             constexpr int M = decltype(mode)::value;
             if (u_sel == 4) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
+            if constexpr (M != kF32ToBf16) {
+                // automatic: the u8 -> bf16 expansion writes through TMA bulk stores
+                // (cfg3 0.63 -> 0.81), raw copies keep the register path (cfg4 0.63 vs 0.55)
+                if (u_sel == -2 || (u_sel == 0 && M == kU8ToBf16)) return go(k_dense_gather_bulk<M, 2, 256>, 2, 256);
+                if (u_sel == -4) return go(k_dense_gather_bulk<M, 4, 256>, 4, 256);
+            }
             return go(k_dense_gather_flat<M, 2, 256>, 2, 256);
         };
         if (od == OutDtype::bf16 && a.vdt == VDtype::u8) {
