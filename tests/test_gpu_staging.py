@@ -38,17 +38,46 @@ def _rows(rng, n):
     return rows
 
 
-@pytest.fixture(scope="module")
-def crafted(tmp_path_factory):
+def _build(tmp_path_factory, vdt):
     rng = np.random.default_rng(7)
     rows = _rows(rng, 336)
     ip = np.zeros(len(rows) + 1, np.uint64)
     ip[1:] = np.cumsum([len(r) for r in rows])
     ix = np.concatenate(rows).astype(np.uint64)
-    dv = (rng.random(len(ix)) + 0.25).astype(np.float32)
-    path = tmp_path_factory.mktemp("staging") / "s"
-    write_csr_store(path, ip, ix, dv, NV, 16, 8)
+    if vdt == "u8":
+        dv = rng.integers(1, 256, len(ix)).astype(np.uint8)
+    else:
+        dv = (rng.random(len(ix)) + 0.25).astype(np.float32 if vdt == "f32" else np.float64)
+    path = tmp_path_factory.mktemp("staging_" + vdt) / "s"
+    write_csr_store(path, ip, ix, dv, NV, 16, 8, vdt=vdt)
     return path, ip, ix, dv
+
+
+@pytest.fixture(scope="module")
+def crafted(tmp_path_factory):
+    return _build(tmp_path_factory, "f32")
+
+
+@pytest.mark.parametrize("vdt", ["u8", "f64"])
+def test_staging_value_widths(tmp_path_factory, vdt):
+    """1- and 8-byte values through the delta staging (value region copied
+    word-wise with a byte tail / 8-B aligned in the expanded record)."""
+    path, ip, ix, dv = _build(tmp_path_factory, vdt)
+    ds = R.DeviceStore(path, 0, "stream_pinned")
+    for out in ("csr", "dense"):
+        it = R.BatchIterator(ds, R.LoaderConfig(16, 96, 40, 5), 0, output=out)
+        for b in it:
+            g = b.global_indices_host
+            eip, eix, edv = csr_gather(ip, ix, dv, g)
+            if out == "csr":
+                mb = b.to_minibatch()
+                assert (np.asarray(mb.block.indices, np.uint64) == eix).all()
+                assert np.asarray(mb.block.data).tobytes() == edv.tobytes()
+            else:
+                assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, NV).tobytes()
+        assert it.counters().h2d_bytes < it.counters().bytes_read
+        it.close()
+    ds.close()
 
 
 @pytest.mark.parametrize("mode", ["delta", "16", "0"])
