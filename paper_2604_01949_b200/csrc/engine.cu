@@ -1,5 +1,6 @@
 // Device store images + GPU BatchIterator (see engine.hpp).
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -245,17 +246,25 @@ void DStore::load_records(bool to_device) {
 // 2 of every 8 bytes per stored entry never cross PCIe.  The records were
 // validated in their store encoding first; kernels read this layout through
 // ArenaView::idx16 (csr_row<uint16_t>).
-// Delta staging image (kernels.cuh d8_*): records whose in-row column gaps are
-// all <= 255 stage as u8 deltas (1 B per stored column id instead of 4), the
-// rest as idx16 records; a kernel expands both into idx16 records in the slot.
-// Checked read-only first (threads), then converted in place front to back
-// through a per-record copy, under the same no-overlap rule as narrow_image()
-// (false: keep the verbatim image for narrow_image()).
+// Delta staging image (kernels.cuh d8_* / d8v_*): records whose in-row column
+// gaps are all <= 255 stage as u8 deltas (1 B per stored column id instead of
+// 4), with 4-byte values also top-byte coded when that is smaller
+// (RFL_NARROW_VALUES=0 keeps them raw); the rest stage as idx16 records.  A
+// kernel expands every kind into idx16 records in the slot.  Checked read-only
+// first (threads), then converted in place front to back through a per-record
+// copy, under the same no-overlap rule as narrow_image() (false: keep the
+// verbatim image for narrow_image()).
 bool DStore::delta_image() {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
     const uint64_t vs = value_size(m.value_dtype);
-    std::vector<uint8_t> elig(nch, 1);  // every in-row gap <= 255 (else the record stages as idx16)
+    // per record: delta-eligible (every in-row gap <= 255)?  With 4-byte values, also
+    // the top-byte dictionary (3 most frequent) and its escape count, kept when smaller
+    std::vector<uint8_t> kind(nch, kD8Raw);
+    std::vector<std::array<uint8_t, 4>> dict(nch);
+    std::vector<uint64_t> n_esc(nch, 0);
+    const char* ve = std::getenv("RFL_NARROW_VALUES");
+    const bool code_values = vs == 4 && !(ve && ve[0] == '0');
     {
         const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         std::vector<std::thread> pool;
@@ -263,16 +272,41 @@ bool DStore::delta_image() {
             pool.emplace_back([&, t] {
                 for (uint64_t q = t; q < nch; q += T) {
                     const uint8_t* rec = h_image_ + rec_off_[q];
-                    const uint64_t rows = rd32(rec);
+                    const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
                     const uint8_t* ip = rec + kCsrHeaderBytes;
                     const uint8_t* ix = ip + 4 * (rows + 1);
-                    for (uint64_t r = 0; r < rows && elig[q]; ++r) {
+                    bool ok = true;
+                    for (uint64_t r = 0; r < rows && ok; ++r) {
                         const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
                         for (uint64_t k = lo + 1; k < hi; ++k)
                             if (rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)) > 255) {
-                                elig[q] = 0;
+                                ok = false;
                                 break;
                             }
+                    }
+                    if (!ok) {
+                        kind[q] = kIdx16Copy;
+                        continue;
+                    }
+                    if (!code_values) continue;
+                    uint64_t hist[256] = {0};
+                    const uint8_t* val = ix + 4 * nnz;
+                    for (uint64_t k = 0; k < nnz; ++k) ++hist[val[4 * k + 3]];
+                    std::array<uint8_t, 4> d{0, 0, 0, 0};
+                    uint64_t covered = 0;
+                    for (int c = 0; c < 3; ++c) {
+                        int best = 0;
+                        for (int b = 1; b < 256; ++b)
+                            if (hist[b] > hist[best]) best = b;
+                        d[c] = static_cast<uint8_t>(best);
+                        covered += hist[best];
+                        hist[best] = 0;
+                    }
+                    const uint64_t esc = nnz - covered;
+                    if (d8v_layout(rows, nnz, esc).bytes < d8_record_bytes(rows, nnz, vs)) {
+                        kind[q] = kD8Coded;
+                        dict[q] = d;
+                        n_esc[q] = esc;
                     }
                 }
             });
@@ -284,7 +318,9 @@ bool DStore::delta_image() {
         const uint8_t* rec = h_image_ + rec_off_[q];
         const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
         elen[q] = idx16_record_bytes(rows, nnz, vs);
-        len[q] = elig[q] ? d8_record_bytes(rows, nnz, vs) : elen[q];
+        len[q] = kind[q] == kIdx16Copy ? elen[q]
+                 : kind[q] == kD8Coded ? d8v_layout(rows, nnz, n_esc[q]).bytes
+                                       : d8_record_bytes(rows, nnz, vs);
         off[q] = total;
         total = align_up(total + len[q], kAlign);
     }
@@ -297,24 +333,23 @@ bool DStore::delta_image() {
         tmp.assign(h_image_ + rec_off_[q], h_image_ + rec_off_[q] + rec_len_[q]);
         const uint8_t* src = tmp.data();
         uint8_t* dst = h_image_ + off[q];
+        std::memset(dst, 0, len[q]);
         const uint64_t rows = rd32(src), nnz = rd64(src + 4);
         const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
         std::memcpy(dst, src, head);
         const uint8_t* ip = src + kCsrHeaderBytes;
         const uint8_t* ix = src + head;
-        if (!elig[q]) {  // idx16 record
+        const uint8_t* val = ix + 4 * nnz;
+        if (kind[q] == kIdx16Copy) {
             for (uint64_t k = 0; k < nnz; ++k) {
                 const uint16_t w = static_cast<uint16_t>(rd32(ix + 4 * k));
                 std::memcpy(dst + head + 2 * k, &w, 2);
             }
-            const uint64_t ib = (2 * nnz + 7) & ~7ull;
-            std::memset(dst + head + 2 * nnz, 0, ib - 2 * nnz);
-            std::memcpy(dst + head + ib, src + head + 4 * nnz, vs * nnz);
+            std::memcpy(dst + head + ((2 * nnz + 7) & ~7ull), val, vs * nnz);
             continue;
         }
         uint8_t* first = dst + head;
         uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
-        std::memset(first, 0, delta - first);
         for (uint64_t r = 0; r < rows; ++r) {
             const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
             const uint16_t f = lo < hi ? static_cast<uint16_t>(rd32(ix + 4 * lo)) : 0;
@@ -322,15 +357,33 @@ bool DStore::delta_image() {
             for (uint64_t k = lo; k < hi; ++k)
                 delta[k] = k == lo ? 0 : static_cast<uint8_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)));
         }
-        const uint64_t voff = d8_values_offset(rows, nnz);
-        std::memset(delta + nnz, 0, voff - (delta - dst) - nnz);
-        std::memcpy(dst + voff, src + head + 4 * nnz, vs * nnz);
+        if (kind[q] == kD8Raw) {
+            std::memcpy(dst + d8_values_offset(rows, nnz), val, vs * nnz);
+            continue;
+        }
+        const D8vLayout L = d8v_layout(rows, nnz, n_esc[q]);
+        const std::array<uint8_t, 4>& d = dict[q];
+        std::memcpy(dst + L.dict, d.data(), 4);
+        const uint32_t ne = static_cast<uint32_t>(n_esc[q]);
+        std::memcpy(dst + L.n_esc, &ne, 4);
+        uint32_t e = 0;
+        for (uint64_t r = 0; r < rows; ++r) {
+            std::memcpy(dst + L.esc_base + 4 * r, &e, 4);
+            const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+            for (uint64_t k = lo; k < hi; ++k) {
+                const uint8_t top = val[4 * k + 3];
+                const uint32_t code = top == d[0] ? 0u : top == d[1] ? 1u : top == d[2] ? 2u : 3u;
+                dst[L.codes + (k >> 2)] |= static_cast<uint8_t>(code << (2 * (k & 3)));
+                if (code == 3) dst[L.esc + e++] = top;
+                std::memcpy(dst + L.low3 + 3 * k, val + 4 * k, 3);
+            }
+        }
     }
     std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
     img_off_ = std::move(off);
     img_len_ = std::move(len);
     exp_len_ = std::move(elen);
-    d8_rec_ = std::move(elig);
+    d8_rec_ = std::move(kind);
     idx16_ = d8_ = true;
     return true;
 }
@@ -739,7 +792,7 @@ void GpuLoader::stage_block(uint64_t id) {
         if (d8) {
             for (uint64_t q = q0; q <= q1; ++q)
                 d8_jobs_.push_back({land + (ds_->img_off()[q] - img0), lv.slot.ptr + lv.chunk_off[q - q0],
-                                    ds_->d8_record(q) ? 0 : ds_->exp_len()[q]});
+                                    ds_->exp_len()[q], ds_->d8_kind(q), 0});
         } else {
             for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->img_off()[q] - img0;
         }
@@ -900,7 +953,8 @@ bool GpuLoader::next(BatchOut& out) {
     // delta-staged records expand into idx16 records on the compute stream, so the
     // copy stream goes straight on to the next batch's blocks
     if (!d8_jobs_.empty()) {
-        launch_d8_decode(d8_jobs_.data(), d8_jobs_.size(), static_cast<uint32_t>(value_size(m.value_dtype)), compute_);
+        launch_d8_decode(d8_jobs_.data(), d8_jobs_.size(), static_cast<uint32_t>(value_size(m.value_dtype)),
+                         m.chunk_rows, compute_);
         ctr_.kernels_launched += (d8_jobs_.size() + kMaxD8Jobs - 1) / kMaxD8Jobs;
     }
 

@@ -61,7 +61,7 @@ public:
     // delta staging (kernels.cuh d8_*): img_* describe the staged delta records,
     // exp_len the idx16 records they expand to in a slot
     bool d8() const { return d8_; }
-    bool d8_record(uint64_t q) const { return d8_rec_[q] != 0; }  // else staged as idx16
+    uint32_t d8_kind(uint64_t q) const { return d8_rec_[q]; }  // D8Kind of staged record q
     const std::vector<uint64_t>& exp_len() const { return exp_len_; }
     uint64_t image_bytes() const { return image_bytes_; }
     uint64_t row_nnz(uint64_t row) const { return row_nnz_.empty() ? 0 : row_nnz_[row]; }

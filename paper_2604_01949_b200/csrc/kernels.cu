@@ -112,9 +112,6 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read1() {
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // ------------------------------------------------ 128-bit shifted warp copy ---
@@ -350,21 +347,21 @@ struct D8Jobs {
     D8Job job[kMaxD8Jobs];
 };
 
-constexpr uint32_t kD8Split = 8;  // CTAs per record (blockIdx.y)
 
 __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Jobs jobs) {
     pdl_wait();
     pdl_trigger();
     const D8Job jb = jobs.job[blockIdx.x];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t tid = blockIdx.y * 256 + threadIdx.x;  // within the record's CTAs
-    constexpr uint32_t nt = kD8Split * 256;
-    if (jb.bytes) {  // staged as idx16 already (16-B aligned, 16-B multiple incl. padding reads)
+    const uint32_t tid = blockIdx.y * 256 + threadIdx.x;  // within the record's CTAs (one warp per row)
+    const uint32_t nt = gridDim.y * 256;
+    if (jb.kind == kIdx16Copy) {  // staged as idx16 already (16-B aligned, 16-B multiple incl. padding reads)
         const uint4* s4 = reinterpret_cast<const uint4*>(jb.src);
         uint4* d4 = reinterpret_cast<uint4*>(jb.dst);
         for (uint64_t i = tid; i < (jb.bytes + 15) / 16; i += nt) d4[i] = ld_v4(s4 + i);
         return;
     }
+    const bool coded = jb.kind == kD8Coded;
     const uint64_t rows = ld_u32(jb.src), nnz = ld_u64_a4(jb.src + 4);
     const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
     const uint32_t* s32 = reinterpret_cast<const uint32_t*>(jb.src);
@@ -372,28 +369,49 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
     for (uint64_t i = tid; i < head / 4; i += nt) d32[i] = __ldg(s32 + i);
     const uint8_t* first = jb.src + head;
     const uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
-    const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
-    const uint64_t vbytes = nnz * jobs.vs;
-    const uint8_t* sv = jb.src + voff;
     uint8_t* dv = jb.dst + head + ((2 * nnz + 7) & ~7ull);
-    for (uint64_t i = tid; i < vbytes / 4; i += nt)
-        reinterpret_cast<uint32_t*>(dv)[i] = __ldg(reinterpret_cast<const uint32_t*>(sv) + i);
-    for (uint64_t i = (vbytes & ~3ull) + tid; i < vbytes; i += nt) dv[i] = sv[i];
+    D8vLayout L{};
+    if (coded) {
+        L = d8v_layout(rows, nnz, ld_u32(jb.src + d8v_layout(rows, nnz, 0).n_esc));
+    } else {  // raw values: copied word-wise (+ byte tail)
+        const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
+        const uint64_t vbytes = nnz * jobs.vs;
+        const uint8_t* sv = jb.src + voff;
+        for (uint64_t i = tid; i < vbytes / 4; i += nt)
+            reinterpret_cast<uint32_t*>(dv)[i] = __ldg(reinterpret_cast<const uint32_t*>(sv) + i);
+        for (uint64_t i = (vbytes & ~3ull) + tid; i < vbytes; i += nt) dv[i] = sv[i];
+    }
     const uint8_t* ip = jb.src + kCsrHeaderBytes;
     uint16_t* out = reinterpret_cast<uint16_t*>(jb.dst + head);
-    for (uint64_t r = blockIdx.y * 8 + warp; r < rows; r += kD8Split * 8) {
+    uint32_t* vout = reinterpret_cast<uint32_t*>(dv);
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint64_t r = blockIdx.y * 8 + warp; r < rows; r += gridDim.y * 8) {
         const uint64_t lo = ld_u32(ip + 4 * r), hi = ld_u32(ip + 4 * (r + 1));
         uint32_t carry = __ldg(reinterpret_cast<const unsigned short*>(first) + r);
+        uint32_t esc_at = coded ? ld_u32(jb.src + L.esc_base + 4 * r) : 0u;
         for (uint64_t base = lo; base < hi; base += 32) {
             const uint64_t k = base + lane;
-            uint32_t v = k < hi ? __ldg(delta + k) : 0u;
+            const bool valid = k < hi;
+            uint32_t v = valid ? __ldg(delta + k) : 0u;
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t t = __shfl_up_sync(kFull, v, o);
                 if (lane >= static_cast<uint32_t>(o)) v += t;
             }
             const uint32_t col = carry + v;
-            if (k < hi) out[k] = static_cast<uint16_t>(col);
+            if (valid) out[k] = static_cast<uint16_t>(col);
             carry = __shfl_sync(kFull, col, 31);
+            if (coded) {  // top byte from the dictionary or the escape list, low 3 bytes verbatim
+                const uint32_t code = valid ? (__ldg(jb.src + L.codes + (k >> 2)) >> (2 * (k & 3))) & 3u : 0u;
+                const uint32_t em = __ballot_sync(kFull, valid && code == 3u);
+                if (valid) {
+                    const uint32_t top = code == 3u ? __ldg(jb.src + L.esc + esc_at + __popc(em & lt))
+                                                    : __ldg(jb.src + L.dict + code);
+                    const uint8_t* l3 = jb.src + L.low3 + 3 * k;
+                    vout[k] = (top << 24) | (static_cast<uint32_t>(__ldg(l3 + 2)) << 16) |
+                              (static_cast<uint32_t>(__ldg(l3 + 1)) << 8) | __ldg(l3);
+                }
+                esc_at += __popc(em);
+            }
         }
     }
 }
@@ -1330,8 +1348,6 @@ __global__ void __launch_bounds__(kDgThreads)
 }
 
 // ------------------------------------------------------------ host helpers ---
-int g_sm_count = 0;
-std::once_flag g_sm_once;
 
 bool pdl_enabled() {
     static const bool on = [] {
@@ -1534,13 +1550,14 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
                     nullptr, st);
 }
 
-void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, cudaStream_t st) {
+void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st) {
+    const unsigned split = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(1, (rows_per_record + 7) / 8), 1024));
     for (size_t k0 = 0; k0 < n; k0 += kMaxD8Jobs) {
         D8Jobs j{};
         j.n = static_cast<uint32_t>(std::min<size_t>(kMaxD8Jobs, n - k0));
         j.vs = vs;
         for (uint32_t i = 0; i < j.n; ++i) j.job[i] = jobs[k0 + i];
-        launch_k(k_d8_decode, dim3(j.n, kD8Split), dim3(256), 0, st, "k_d8_decode launch", j);
+        launch_k(k_d8_decode, dim3(j.n, split), dim3(256), 0, st, "k_d8_decode launch", j);
     }
 }
 

@@ -65,14 +65,45 @@ inline uint64_t d8_values_offset(uint64_t rows, uint64_t nnz) {
     return (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
 }
 inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) { return d8_values_offset(rows, nnz) + vs * nnz; }
+// Delta records with 4-byte values may also code each value's top byte (sign +
+// high exponent bits, a handful of distinct values per record) against a
+// 3-entry dictionary: [head][first u16 x rows, pad 4][deltas u8 x nnz, pad 4]
+// [escapes before row r, u32 x rows][dict u8 x 4][n_esc u32][2-bit codes x nnz,
+// pad 4][escaped top bytes u8 x n_esc, pad 4][low 3 bytes x nnz] -- ~4.3 B per
+// stored f32 entry instead of 5 (code 3 = escape: the top byte is in the list).
+#ifdef __CUDACC__
+#define RFL_HD __host__ __device__
+#else
+#define RFL_HD
+#endif
+struct D8vLayout {
+    uint64_t first, delta, esc_base, dict, n_esc, codes, esc, low3, bytes;
+};
+RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc) {
+    D8vLayout l{};
+    l.first = kCsrHeaderBytes + 4 * (rows + 1);
+    l.delta = l.first + ((2 * rows + 3) & ~3ull);
+    l.esc_base = l.delta + ((nnz + 3) & ~3ull);
+    l.dict = l.esc_base + 4 * rows;
+    l.n_esc = l.dict + 4;
+    l.codes = l.n_esc + 4;
+    l.esc = l.codes + ((((nnz + 3) / 4) + 3) & ~3ull);
+    l.low3 = l.esc + ((n_esc + 3) & ~3ull);
+    l.bytes = l.low3 + 3 * nnz;
+    return l;
+}
+enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2 };
 struct D8Job {
-    const uint8_t* src;  // staged record (device): delta layout, or idx16 already when bytes != 0
+    const uint8_t* src;  // staged record (device)
     uint8_t* dst;        // idx16 record (device)
-    uint64_t bytes;      // 0: expand a delta record; else copy `bytes` (a record with a gap > 255)
+    uint64_t bytes;      // kIdx16Copy: bytes to copy
+    uint32_t kind;       // D8Kind
+    uint32_t pad;
 };
 // expand n staged delta records (value size vs) into idx16 records (one launch per kMaxD8Jobs)
 constexpr size_t kMaxD8Jobs = 128;
-void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, cudaStream_t st);
+// (one warp per row: rows_per_record / 8 CTAs per record)
+void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st);
 
 // K2 without the device scan: `prefix` (u64[n+1], exclusive nnz prefix of the
 // rows, prefix[0] arbitrary) is the host schedule's, and is the output indptr

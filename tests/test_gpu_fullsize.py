@@ -85,9 +85,10 @@ def test_cfg1_full_epoch_csr_streamed(cfg1):
         k += 1
     assert k == len(sched)
     # the pinned staging image carried u8 column deltas (every in-row gap <= 255
-    # in this store): ~5 of every 8 record bytes per entry crossed PCIe
+    # in this store) and top-byte coded values: ~4.3 of every 8 record bytes per
+    # entry crossed PCIe
     c = it.counters()
-    assert 0.55 * c.bytes_read < c.h2d_bytes < 0.7 * c.bytes_read
+    assert 0.45 * c.bytes_read < c.h2d_bytes < 0.6 * c.bytes_read
 
 
 def test_cfg1_normalize_log1p_full_rows(cfg1):

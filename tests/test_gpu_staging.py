@@ -46,9 +46,15 @@ def _build(tmp_path_factory, vdt):
     ix = np.concatenate(rows).astype(np.uint64)
     if vdt == "u8":
         dv = rng.integers(1, 256, len(ix)).astype(np.uint8)
+    elif vdt == "f32wide":  # mostly (0.25, 1.25), 12 % anywhere from -1e8 to 1e8: top-byte escapes
+        dv = (rng.random(len(ix)) + 0.25).astype(np.float32)
+        wide = rng.random(len(ix)) < 0.12
+        dv[wide] = (rng.standard_normal(wide.sum()) * 10.0 ** rng.integers(-8, 9, wide.sum())).astype(np.float32)
+        dv[::97] = 0.0
+        vdt = "f32"
     else:
         dv = (rng.random(len(ix)) + 0.25).astype(np.float32 if vdt == "f32" else np.float64)
-    path = tmp_path_factory.mktemp("staging_" + vdt) / "s"
+    path = tmp_path_factory.mktemp("staging_" + str(dv.dtype)) / "s"
     write_csr_store(path, ip, ix, dv, NV, 16, 8, vdt=vdt)
     return path, ip, ix, dv
 
@@ -58,10 +64,11 @@ def crafted(tmp_path_factory):
     return _build(tmp_path_factory, "f32")
 
 
-@pytest.mark.parametrize("vdt", ["u8", "f64"])
+@pytest.mark.parametrize("vdt", ["u8", "f64", "f32wide"])
 def test_staging_value_widths(tmp_path_factory, vdt):
     """1- and 8-byte values through the delta staging (value region copied
-    word-wise with a byte tail / 8-B aligned in the expanded record)."""
+    word-wise with a byte tail / 8-B aligned in the expanded record), and f32
+    values whose top bytes need the escape list of the coded value layout."""
     path, ip, ix, dv = _build(tmp_path_factory, vdt)
     ds = R.DeviceStore(path, 0, "stream_pinned")
     for out in ("csr", "dense"):
