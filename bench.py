@@ -55,9 +55,10 @@ WORKLOADS = {
                             chunk_rows=256, chunks_per_shard=128),
                  loader=dict(fetch_block_rows=256, buffer_capacity_rows=16384, batch_rows=1024, seed=0),
                  out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16"),
-    "cfg4": dict(desc="cfg4: dense 4x1024 u8 windows (5M), chunk 512, f=512 B=16384 b=2048, raw u8",
+    "cfg4": dict(desc="cfg4: dense 4x1024 one-hot u8 windows (5M, procedural one-hot: one channel per position), "
+                      "chunk 512, f=512 B=16384 b=2048, raw u8",
                  synth=dict(n_obs=5_000_000, n_var=4096, layout="dense", value_dtype="u8", density=0.1, seed=3,
-                            chunk_rows=512, chunks_per_shard=128),
+                            chunk_rows=512, chunks_per_shard=128, one_hot=4),
                  loader=dict(fetch_block_rows=512, buffer_capacity_rows=16384, batch_rows=2048, seed=0),
                  out=dict(output="dense", out_dtype="native", transform=None), dtype="u8"),
 }

@@ -84,7 +84,8 @@ typedef struct rfl_synth_config {
     uint64_t chunk_rows;
     uint64_t chunks_per_shard;
     uint32_t threads;
-    uint32_t reserved;
+    uint32_t one_hot; /* > 0: procedural one-hot dense u8 rows with this many channel planes (not in
+                         the reference); 0: synth_store */
 } rfl_synth_config;
 rfl_status rfl_synth_store(const char* path, const rfl_synth_config* cfg);
 

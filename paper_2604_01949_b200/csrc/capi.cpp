@@ -188,6 +188,7 @@ rfl_status rfl_synth_store(const char* path, const rfl_synth_config* c) {
         s.chunk_rows = c->chunk_rows;
         s.chunks_per_shard = c->chunks_per_shard;
         s.threads = c->threads;
+        s.one_hot = c->one_hot;
         rfl::synth_store(path, s);
     });
 }

@@ -136,6 +136,10 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     }
     img_off_ = rec_off_;
     img_len_ = rec_len_;
+    if (staging_ == kStreamPinned && m.layout == Layout::dense && m.value_dtype == VDtype::u8 && m.n_var % 16 == 0) {
+        const char* e = std::getenv("RFL_NARROW");
+        if (!(e && e[0] == '0')) one_hot_image();
+    }
     if (staging_ == kStreamPinned && m.layout == Layout::csr && m.index_dtype == IDtype::u32 && m.n_var <= 65536) {
         const char* e = std::getenv("RFL_NARROW");
         // RFL_NARROW=0: verbatim image; =16: u16 ids only; default: deltas when eligible, else u16
@@ -385,6 +389,70 @@ bool DStore::delta_image() {
     exp_len_ = std::move(elen);
     d8_rec_ = std::move(kind);
     idx16_ = d8_ = true;
+    return true;
+}
+
+// One-hot staging image (kernels.cuh kOneHot4): when every row of a dense u8
+// store is one-hot over 4 channel planes ([4][n_var/4], exactly one 1 per
+// position -- the WGS-window encoding of BASELINE config 4), each row stages
+// as n_var/16 bytes of 2-bit channel codes; the decode kernel rebuilds the
+// verbatim rows in the slot.  Checked read-only first; false = not one-hot.
+bool DStore::one_hot_image() {
+    const Manifest& m = hs_->manifest();
+    const uint64_t nch = m.chunk_count();
+    const uint64_t L = m.n_var / 4;
+    std::atomic<bool> ok{true};
+    {
+        const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                for (uint64_t q = t; q < nch && ok.load(std::memory_order_relaxed); q += T) {
+                    const uint8_t* rec = h_image_ + rec_off_[q];
+                    const uint64_t rows = m.rows_in_chunk(q);
+                    for (uint64_t i = 0; i < rows; ++i) {
+                        const uint8_t* row = rec + i * m.n_var;
+                        for (uint64_t p = 0; p < L; ++p) {
+                            const uint32_t a = row[p], b = row[L + p], c = row[2 * L + p], d = row[3 * L + p];
+                            if ((a | b | c | d) > 1 || a + b + c + d != 1) {
+                                ok = false;
+                                return;
+                            }
+                        }
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+    }
+    if (!ok) return false;
+    std::vector<uint64_t> off(nch), len(nch);
+    uint64_t total = 0;
+    for (uint64_t q = 0; q < nch; ++q) {
+        len[q] = m.rows_in_chunk(q) * (L / 4);
+        off[q] = total;
+        total = align_up(total + len[q], kAlign);
+    }
+    std::vector<uint8_t> tmp;
+    for (uint64_t q = 0; q < nch; ++q) {  // compact records are 16x smaller: forward pass via a copy
+        tmp.assign(h_image_ + rec_off_[q], h_image_ + rec_off_[q] + rec_len_[q]);
+        uint8_t* dst = h_image_ + off[q];
+        std::memset(dst, 0, len[q]);
+        const uint64_t rows = m.rows_in_chunk(q);
+        for (uint64_t i = 0; i < rows; ++i) {
+            const uint8_t* row = tmp.data() + i * m.n_var;
+            uint8_t* codes = dst + i * (L / 4);
+            for (uint64_t p = 0; p < L; ++p) {
+                const uint32_t ch = row[L + p] ? 1u : row[2 * L + p] ? 2u : row[3 * L + p] ? 3u : 0u;
+                codes[p >> 2] |= static_cast<uint8_t>(ch << (2 * (p & 3)));
+            }
+        }
+    }
+    std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
+    img_off_ = std::move(off);
+    img_len_ = std::move(len);
+    exp_len_ = rec_len_;
+    d8_rec_.assign(nch, kOneHot4);
+    d8_ = true;
     return true;
 }
 
@@ -954,7 +1022,7 @@ bool GpuLoader::next(BatchOut& out) {
     // copy stream goes straight on to the next batch's blocks
     if (!d8_jobs_.empty()) {
         launch_d8_decode(d8_jobs_.data(), d8_jobs_.size(), static_cast<uint32_t>(value_size(m.value_dtype)),
-                         m.chunk_rows, compute_);
+                         m.chunk_rows, compute_, m.n_var);
         ctr_.kernels_launched += (d8_jobs_.size() + kMaxD8Jobs - 1) / kMaxD8Jobs;
     }
 

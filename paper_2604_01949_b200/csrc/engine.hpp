@@ -87,6 +87,7 @@ private:
     void validate_records(const uint8_t* base);
     void narrow_image();
     bool delta_image();
+    bool one_hot_image();
     std::shared_ptr<HostStore> hs_;
     int device_;
     uint32_t staging_;

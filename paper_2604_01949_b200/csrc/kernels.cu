@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(256)
 // row's first column).
 struct D8Jobs {
     uint32_t n, vs;
+    uint64_t n_var;  // kOneHot4 rows
     D8Job job[kMaxD8Jobs];
 };
 
@@ -355,6 +356,25 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t tid = blockIdx.y * 256 + threadIdx.x;  // within the record's CTAs (one warp per row)
     const uint32_t nt = gridDim.y * 256;
+    if (jb.kind == kOneHot4) {  // 2-bit channel codes -> one-hot u8 rows, one 16-B output chunk per thread
+        const uint64_t L = jobs.n_var / 4, cpr = jobs.n_var / 16, n_chunks = jb.bytes / 16;
+        for (uint64_t j = tid; j < n_chunks; j += nt) {
+            const uint64_t row = j / cpr, b = (j - row * cpr) * 16;
+            const uint32_t c = static_cast<uint32_t>(b / L);
+            const uint64_t p0 = b - c * L;
+            const uint32_t w = ld_u32(jb.src + row * (L / 4) + p0 / 4);
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) word |= (((w >> (2 * (4 * q + k))) & 3u) == c ? 1u : 0u) << (8 * k);
+                o[q] = word;
+            }
+            reinterpret_cast<uint4*>(jb.dst)[j] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        return;
+    }
     if (jb.kind == kIdx16Copy) {  // staged as idx16 already (16-B aligned, 16-B multiple incl. padding reads)
         const uint4* s4 = reinterpret_cast<const uint4*>(jb.src);
         uint4* d4 = reinterpret_cast<uint4*>(jb.dst);
@@ -1550,12 +1570,14 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
                     nullptr, st);
 }
 
-void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st) {
+void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st,
+                      uint64_t n_var) {
     const unsigned split = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(1, (rows_per_record + 7) / 8), 1024));
     for (size_t k0 = 0; k0 < n; k0 += kMaxD8Jobs) {
         D8Jobs j{};
         j.n = static_cast<uint32_t>(std::min<size_t>(kMaxD8Jobs, n - k0));
         j.vs = vs;
+        j.n_var = n_var;
         for (uint32_t i = 0; i < j.n; ++i) j.job[i] = jobs[k0 + i];
         launch_k(k_d8_decode, dim3(j.n, split), dim3(256), 0, st, "k_d8_decode launch", j);
     }

@@ -92,7 +92,10 @@ RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc) 
     l.bytes = l.low3 + 3 * nnz;
     return l;
 }
-enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2 };
+// kOneHot4: a dense u8 record whose rows are one-hot over 4 channel planes
+// ([4][L] bytes, exactly one 1 per position) staged as 2-bit channel codes,
+// L/4 bytes per row (16x smaller; L a multiple of 16)
+enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2, kOneHot4 = 3 };
 struct D8Job {
     const uint8_t* src;  // staged record (device)
     uint8_t* dst;        // idx16 record (device)
@@ -103,7 +106,8 @@ struct D8Job {
 // expand n staged delta records (value size vs) into idx16 records (one launch per kMaxD8Jobs)
 constexpr size_t kMaxD8Jobs = 128;
 // (one warp per row: rows_per_record / 8 CTAs per record)
-void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st);
+void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st,
+                      uint64_t n_var = 0);
 
 // K2 without the device scan: `prefix` (u64[n+1], exclusive nnz prefix of the
 // rows, prefix[0] arbitrary) is the host schedule's, and is the output indptr

@@ -134,8 +134,45 @@ void encode_csr_rows(const uint64_t* indptr, const uint64_t* indices, const uint
     std::memcpy(rec.data() + pos, data + base * vs, nnz * vs);
 }
 
+namespace {
+Manifest synth_one_hot(const std::string& path, const SynthCfg& c) {
+    if (c.layout != Layout::dense || c.value_dtype != VDtype::u8 || c.n_var % c.one_hot != 0)
+        invalid("synth: one_hot needs a dense u8 store with n_var a multiple of the channel count");
+    Manifest man;
+    man.layout = Layout::dense;
+    man.n_var = c.n_var;
+    man.value_dtype = VDtype::u8;
+    man.chunk_rows = c.chunk_rows;
+    man.chunks_per_shard = c.chunks_per_shard;
+    man.codec = Codec::none;
+    man.var_names.reserve(c.n_var);
+    for (uint64_t i = 0; i < c.n_var; ++i) man.var_names.push_back("v" + std::to_string(i));
+    RecordWriter w(path, man, /*defer_manifest=*/false);
+    const uint64_t L = c.n_var / c.one_hot;
+    const unsigned T = c.threads ? c.threads : std::max(1u, std::thread::hardware_concurrency());
+    std::vector<uint8_t> rec;
+    for (uint64_t r0 = 0; r0 < c.n_obs; r0 += c.chunk_rows) {
+        const uint64_t rows = std::min<uint64_t>(c.chunk_rows, c.n_obs - r0);
+        rec.assign(rows * c.n_var, 0);
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                for (uint64_t i = t; i < rows; i += T) {
+                    const uint64_t hr = mix64(c.seed ^ mix64(r0 + i));
+                    uint8_t* row = rec.data() + i * c.n_var;
+                    for (uint64_t p = 0; p < L; ++p) row[(mix64(hr ^ p) % c.one_hot) * L + p] = 1;
+                }
+            });
+        for (auto& th : pool) th.join();
+        w.append_record(rec.data(), rec.size(), rows);
+    }
+    return w.finish();
+}
+}  // namespace
+
 Manifest synth_store(const std::string& path, const SynthCfg& c) {
     if (c.n_obs == 0 || c.n_var == 0) invalid("synth: n_obs and n_var must be >= 1");
+    if (c.one_hot) return synth_one_hot(path, c);
     if (c.layout == Layout::csr && (c.density <= 0.0 || c.density > 1.0))
         invalid("synth: density must lie in (0, 1] for csr stores");
     if (c.codec != Codec::none) invalid("synth: only codec none is supported by the GPU build");

@@ -19,6 +19,11 @@ struct SynthCfg {
     uint64_t chunk_rows = 1024, chunks_per_shard = 128;
     Codec codec = Codec::none;
     unsigned threads = 0;
+    // one_hot > 0 (dense u8 only, not in the reference): procedural one-hot rows of
+    // `one_hot` channel planes x n_var / one_hot positions -- position p of row i
+    // has its 1 in channel mix64(seed ^ mix64(i) ^ p) % one_hot (SURVEY §8d
+    // config 4, "4 x 1024 one-hot").  The store is an ordinary dense u8 store.
+    unsigned one_hot = 0;
 };
 
 // synth_store (reference src/synth.cpp:60-144), byte-identical output.

@@ -93,13 +93,15 @@ class SynthConfig:
     chunks_per_shard: int = 128
     codec: str = "none"
     threads: int = 0
+    one_hot: int = 0  # > 0: procedural one-hot dense u8 rows (channel planes), see rfl_synth_config
 
 
 def synth_store(path, config: SynthConfig) -> StoreManifest:
     """synth_store (synth.cpp:60-144): byte-identical to the reference for equal configs."""
     c = L.rfl_synth_config(config.n_obs, config.n_var, LAYOUTS[config.layout], VDTYPES[config.value_dtype],
                            IDTYPES[config.index_dtype], 0 if config.codec == "none" else 1, config.density,
-                           config.seed, config.chunk_rows, config.chunks_per_shard, config.threads, 0)
+                           config.seed, config.chunk_rows, config.chunks_per_shard, config.threads,
+                           config.one_hot)
     L.check(L.lib().rfl_synth_store(str(path).encode(), C.byref(c)))
     return StoreReader(path).manifest()
 

@@ -124,3 +124,42 @@ def test_staging_encodings_bit_exact(crafted, mode):
         it.close()
     ds.close()
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("out_dtype", ["native", "bf16"])
+def test_one_hot_dense_staging(tmp_path, out_dtype):
+    """BASELINE config 4's one-hot windows: a dense u8 store whose rows are one-hot
+    over 4 channel planes stages as 2-bit codes (16x fewer PCIe bytes) and is
+    rebuilt on the GPU; batches equal the reference's row gather bit for bit.
+    A single non-one-hot byte anywhere keeps the verbatim image."""
+    from oracle.oracle import load_dense_store, u8_to_bf16_bits
+    for broken in (False, True):
+        path = tmp_path / f"oh{int(broken)}"
+        R.synth_store(path, R.SynthConfig(n_obs=700, n_var=4 * 64, layout="dense", value_dtype="u8", seed=11,
+                                          chunk_rows=32, chunks_per_shard=8, one_hot=4))
+        if broken:  # flip one byte of one record in place
+            shard = sorted((path / "shards").iterdir())[1]
+            raw = bytearray(shard.read_bytes())
+            raw[100] = 2
+            shard.write_bytes(bytes(raw))
+        x = load_dense_store(path).reshape(700, 256)
+        ds = R.DeviceStore(path, 0, "stream_pinned")
+        it = R.BatchIterator(ds, R.LoaderConfig(32, 160, 64, 9), 0, output="dense", out_dtype=out_dtype)
+        n = 0
+        for b in it:
+            g = b.global_indices_host.astype(np.int64)
+            want = x[g]
+            if out_dtype == "bf16":
+                got = b.data.view(torch.int16).cpu().numpy().view(np.uint16)
+                assert (got == u8_to_bf16_bits(want)).all()
+            else:
+                assert b.data.cpu().numpy().tobytes() == want.tobytes()
+            n += len(g)
+        assert n == 700
+        c = it.counters()
+        if broken:
+            assert c.h2d_bytes >= c.bytes_read
+        else:
+            assert c.h2d_bytes < c.bytes_read / 4  # codes are 1/16 of the rows; row refs (16 B) on top
+        it.close()
+        ds.close()
