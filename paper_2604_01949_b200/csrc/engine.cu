@@ -250,14 +250,26 @@ void DStore::load_records(bool to_device) {
 // 2 of every 8 bytes per stored entry never cross PCIe.  The records were
 // validated in their store encoding first; kernels read this layout through
 // ArenaView::idx16 (csr_row<uint16_t>).
+namespace {
+template <typename F>
+void parallel_records(uint64_t n, F&& f) {
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            for (uint64_t q = t; q < n; q += T) f(q);
+        });
+    for (auto& th : pool) th.join();
+}
+}  // namespace
+
 // Delta staging image (kernels.cuh d8_* / d8v_*): records whose in-row column
 // gaps are all <= 255 stage as u8 deltas (1 B per stored column id instead of
 // 4), with 4-byte values also top-byte coded when that is smaller
 // (RFL_NARROW_VALUES=0 keeps them raw); the rest stage as idx16 records.  A
-// kernel expands every kind into idx16 records in the slot.  Checked read-only
-// first (threads), then converted in place front to back through a per-record
-// copy, under the same no-overlap rule as narrow_image() (false: keep the
-// verbatim image for narrow_image()).
+// kernel expands every kind into idx16 records in the slot.  Analysed read-only
+// and encoded in parallel into a separate buffer, then copied over the
+// verbatim image (false: the encoding would not fit; narrow_image() runs).
 bool DStore::delta_image() {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
@@ -328,16 +340,12 @@ bool DStore::delta_image() {
         off[q] = total;
         total = align_up(total + len[q], kAlign);
     }
-    for (uint64_t q = 0; q < nch; ++q) {
-        const uint64_t next_old = q + 1 < nch ? rec_off_[q + 1] : image_bytes_;
-        if (off[q] > rec_off_[q] || off[q] + len[q] > next_old) return false;
-    }
-    std::vector<uint8_t> tmp;
-    for (uint64_t q = 0; q < nch; ++q) {
-        tmp.assign(h_image_ + rec_off_[q], h_image_ + rec_off_[q] + rec_len_[q]);
-        const uint8_t* src = tmp.data();
-        uint8_t* dst = h_image_ + off[q];
-        std::memset(dst, 0, len[q]);
+    if (total > image_bytes_) return false;
+    // encode in parallel into a separate buffer (the verbatim image stays read-only), then copy back
+    std::vector<uint8_t> img(total, 0);
+    parallel_records(nch, [&](uint64_t q) {
+        const uint8_t* src = h_image_ + rec_off_[q];
+        uint8_t* dst = img.data() + off[q];
         const uint64_t rows = rd32(src), nnz = rd64(src + 4);
         const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
         std::memcpy(dst, src, head);
@@ -350,7 +358,7 @@ bool DStore::delta_image() {
                 std::memcpy(dst + head + 2 * k, &w, 2);
             }
             std::memcpy(dst + head + ((2 * nnz + 7) & ~7ull), val, vs * nnz);
-            continue;
+            return;
         }
         uint8_t* first = dst + head;
         uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
@@ -363,7 +371,7 @@ bool DStore::delta_image() {
         }
         if (kind[q] == kD8Raw) {
             std::memcpy(dst + d8_values_offset(rows, nnz), val, vs * nnz);
-            continue;
+            return;
         }
         const D8vLayout L = d8v_layout(rows, nnz, n_esc[q]);
         const std::array<uint8_t, 4>& d = dict[q];
@@ -382,7 +390,8 @@ bool DStore::delta_image() {
                 std::memcpy(dst + L.low3 + 3 * k, val + 4 * k, 3);
             }
         }
-    }
+    });
+    std::memcpy(h_image_, img.data(), total);
     std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
     img_off_ = std::move(off);
     img_len_ = std::move(len);
@@ -432,21 +441,20 @@ bool DStore::one_hot_image() {
         off[q] = total;
         total = align_up(total + len[q], kAlign);
     }
-    std::vector<uint8_t> tmp;
-    for (uint64_t q = 0; q < nch; ++q) {  // compact records are 16x smaller: forward pass via a copy
-        tmp.assign(h_image_ + rec_off_[q], h_image_ + rec_off_[q] + rec_len_[q]);
-        uint8_t* dst = h_image_ + off[q];
-        std::memset(dst, 0, len[q]);
+    std::vector<uint8_t> img(total, 0);  // encoded in parallel, then copied over the verbatim image
+    parallel_records(nch, [&](uint64_t q) {
+        uint8_t* dst = img.data() + off[q];
         const uint64_t rows = m.rows_in_chunk(q);
         for (uint64_t i = 0; i < rows; ++i) {
-            const uint8_t* row = tmp.data() + i * m.n_var;
+            const uint8_t* row = h_image_ + rec_off_[q] + i * m.n_var;
             uint8_t* codes = dst + i * (L / 4);
             for (uint64_t p = 0; p < L; ++p) {
                 const uint32_t ch = row[L + p] ? 1u : row[2 * L + p] ? 2u : row[3 * L + p] ? 3u : 0u;
                 codes[p >> 2] |= static_cast<uint8_t>(ch << (2 * (p & 3)));
             }
         }
-    }
+    });
+    std::memcpy(h_image_, img.data(), total);
     std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
     img_off_ = std::move(off);
     img_len_ = std::move(len);
