@@ -223,6 +223,18 @@ class BatchIterator:
                                           C.byref(h)))
         self._h = h
         self._b = L.rfl_batch()
+        self._views = {}
+
+    def _view(self, ptr, shape, np_dtype):
+        """cuda_tensor, cached: the loader's output slots are a fixed ring, so the
+        same (pointer, shape) views come back every out_slots batches."""
+        key = (ptr, shape, np_dtype)
+        t = self._views.get(key)
+        if t is None:
+            if len(self._views) > 64:
+                self._views.clear()
+            t = self._views[key] = cuda_tensor(ptr, shape, np_dtype, self.device)
+        return t
 
     def next(self) -> DeviceBatch | None:
         rc = L.check(L.lib().rfl_loader_next(self._h, C.byref(self._b)))
@@ -231,18 +243,16 @@ class BatchIterator:
         b = self._b
         n = b.n_rows
         gh = np.ctypeslib.as_array(b.h_gidx, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
-        dev = self.device
-        g = cuda_tensor(b.d_gidx, (n,), np.int64, dev)
+        g = self._view(b.d_gidx, (n,), np.int64)
         if b.layout == L.LAYOUT_CSR:
             idt = np.uint32 if b.index_dtype == L.IDX_U32 else np.uint64
             return DeviceBatch(b.epoch_index, b.batch_index, n, b.n_var, "csr", g, gh,
-                               indptr=cuda_tensor(b.d_indptr, (n + 1,), np.int64, dev),
-                               indices=cuda_tensor(b.d_indices, (b.nnz,), np.int32 if idt == np.uint32 else np.int64,
-                                                   dev),
-                               data=cuda_tensor(b.d_data, (b.nnz,), _NP[b.dtype], dev), nnz=b.nnz,
+                               indptr=self._view(b.d_indptr, (n + 1,), np.int64),
+                               indices=self._view(b.d_indices, (b.nnz,), np.int32 if idt == np.uint32 else np.int64),
+                               data=self._view(b.d_data, (b.nnz,), _NP[b.dtype]), nnz=b.nnz,
                                dtype=str(b.dtype), index_dtype="u32" if idt == np.uint32 else "u64",
                                _ready_event=b.ready_event or 0)
-        data = cuda_tensor(b.d_data, (n, b.n_var), _NP[b.dtype], dev)
+        data = self._view(b.d_data, (n, b.n_var), _NP[b.dtype])
         if b.dtype == L.BF16:
             import torch
             data = data.view(torch.bfloat16)
