@@ -408,7 +408,11 @@ def cpu_baseline(path, W, threads):
     from oracle.oracle import Ref
     ld = W["loader"]
     dens = W["out"]["output"] == "dense" and W["synth"]["layout"] == "csr"
-    nb = int(os.environ.get("RIFFLE_CPU_BATCHES", "12"))
+    nb = int(os.environ.get("RIFFLE_CPU_BATCHES", "0"))
+    if nb <= 0:  # size the sample for ~10 s of CPU work from a 4-batch probe (epoch 1, untimed)
+        v0, _, _ = Ref.throughput(path, ld["fetch_block_rows"], ld["buffer_capacity_rows"], ld["batch_rows"],
+                                  seed=ld["seed"], depth=4, epoch0=1, threads=threads, max_batches=4, densify=dens)
+        nb = int(min(200, max(8, 10.0 * v0 / ld["batch_rows"])))
     v, rows, wall = Ref.throughput(path, ld["fetch_block_rows"], ld["buffer_capacity_rows"], ld["batch_rows"],
                                    seed=ld["seed"], depth=4, epoch0=0, threads=threads, max_batches=nb,
                                    densify=dens)
