@@ -538,6 +538,8 @@ void DStore::validate_records(const uint8_t* base) {
 
 DStore::~DStore() {
     DeviceGuard g(device_);
+    for (auto& b : out_pool_) b.free_all();
+    for (auto& pb : pinned_pool_) cudaFreeHost(pb.first);
     for (auto& s : free_)
         if (s.released) cudaEventDestroy(s.released);
     for (void* p : slabs_) cudaFree(p);
@@ -609,6 +611,67 @@ DStore::SlotRef DStore::acquire_slot(uint64_t bytes) {
     return s;
 }
 
+void OutBuffers::free_all() {
+    cudaFree(gidx);
+    cudaFree(indptr);
+    cudaFree(indices);
+    cudaFree(data);
+    cudaFree(scratch);
+    cudaFree(d_refs);
+    cudaFreeHost(h_refs);
+    cudaFreeHost(h_gidx);
+    cudaFreeHost(h_prefix);
+    if (done) cudaEventDestroy(done);
+    *this = OutBuffers{};
+}
+
+uint8_t* DStore::take_pinned(uint64_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (size_t i = 0; i < pinned_pool_.size(); ++i)
+            if (pinned_pool_[i].second == bytes) {
+                uint8_t* p = pinned_pool_[i].first;
+                pinned_pool_.erase(pinned_pool_.begin() + static_cast<std::ptrdiff_t>(i));
+                return p;
+            }
+    }
+    uint8_t* p = nullptr;
+    cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocDefault), "pinned");
+    return p;
+}
+
+void DStore::give_pinned(uint8_t* p, uint64_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu_);
+    if (pinned_pool_.size() < 64) pinned_pool_.emplace_back(p, bytes);
+    else cudaFreeHost(p);
+}
+
+OutBuffers DStore::take_out(uint32_t key) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (size_t i = 0; i < out_pool_.size(); ++i)
+        if (out_pool_[i].key == key) {
+            OutBuffers b = out_pool_[i];
+            out_pool_.erase(out_pool_.begin() + static_cast<std::ptrdiff_t>(i));
+            b.used = false;
+            return b;
+        }
+    OutBuffers b;
+    b.key = key;
+    return b;
+}
+
+void DStore::give_out(OutBuffers&& b) {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (out_pool_.size() < 16) {
+        b.used = false;
+        out_pool_.push_back(b);
+    } else {
+        b.free_all();
+    }
+    b = OutBuffers{};
+}
+
 void DStore::release_slot(const SlotRef& s) {
     std::lock_guard<std::mutex> lk(mu_);
     if (s.bytes == slot_bytes_) free_.push_back(s);
@@ -651,12 +714,13 @@ BlockReader::BlockReader(std::shared_ptr<DStore> ds, std::vector<uint64_t> order
     const Manifest& m = ds_->manifest();
     // a block's records, each run read as its 4 KiB-aligned superset into a page-aligned position
     const uint64_t bytes = ds_->max_block_bytes(f) + (f / m.chunk_rows + 2) * 3 * 4096;
+    buf_bytes_ = bytes;
     slots_.resize(slots);
     ev_.resize(slots);
     released_.assign(slots, ~0ull);
     DeviceGuard g(ds_->device());
     for (uint32_t i = 0; i < slots; ++i) {
-        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&slots_[i].buf), bytes, cudaHostAllocDefault), "pinned");
+        slots_[i].buf = ds_->take_pinned(bytes);
         cuda_ok(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
     }
     for (uint32_t t = 0; t < threads; ++t) th_.emplace_back([this] { worker(); });
@@ -672,7 +736,7 @@ BlockReader::~BlockReader() {
     for (size_t i = 0; i < slots_.size(); ++i) {
         cudaEventSynchronize(ev_[i]);
         cudaEventDestroy(ev_[i]);
-        cudaFreeHost(slots_[i].buf);
+        ds_->give_pinned(slots_[i].buf, buf_bytes_);
     }
 }
 
@@ -781,8 +845,12 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     }
     cuda_ok(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "stream");
     cuda_ok(cudaEventCreateWithFlags(&staged_, cudaEventDisableTiming), "event");
+    const uint32_t key = dev_.output | (static_cast<uint32_t>(dev_.out_dtype) << 4) | (dev_.normalize ? 1u << 8 : 0u);
     slots_.resize(dev_.out_slots);
-    for (auto& s : slots_) cuda_ok(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
+    for (auto& s : slots_) {
+        s = ds_->take_out(key);
+        if (!s.done) cuda_ok(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
+    }
     if (ds_->staging() != kResident) {
         live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
         block_bytes_ = ds_->max_block_bytes(cfg_.f);
@@ -813,18 +881,7 @@ GpuLoader::~GpuLoader() {
             cudaEventRecord(l.slot.released, compute_);
             ds_->release_slot(l.slot);
         }
-    for (auto& s : slots_) {
-        cudaFree(s.gidx);
-        cudaFree(s.indptr);
-        cudaFree(s.indices);
-        cudaFree(s.data);
-        cudaFree(s.scratch);
-        cudaFree(s.d_refs);
-        cudaFreeHost(s.h_refs);
-        cudaFreeHost(s.h_gidx);
-        cudaFreeHost(s.h_prefix);
-        cudaEventDestroy(s.done);
-    }
+    for (auto& s : slots_) ds_->give_out(std::move(s));  // the compute stream is drained: reusable as is
     reader_.reset();
     cudaEventDestroy(staged_);
     cudaStreamDestroy(copy_);

@@ -40,6 +40,22 @@ void check_dense_record(const Manifest& m, uint64_t chunk, uint64_t len);
 // Cheap pass (header, length, indptr; optionally per-row nnz); false -> run the full check.
 bool check_csr_record(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint64_t len, uint32_t* row_nnz);
 
+// One output slot of an iterator: batch buffers on the device + pinned row
+// references.  Kept by the DStore between iterators (open_epoch per epoch must
+// not pay cudaMalloc / cudaHostAlloc, which also serialise the device).
+struct OutBuffers {
+    void *gidx = nullptr, *indptr = nullptr, *indices = nullptr, *data = nullptr, *scratch = nullptr;
+    RowRef* d_refs = nullptr;
+    RowRef* h_refs = nullptr;
+    uint64_t* h_gidx = nullptr;
+    uint64_t* h_prefix = nullptr;  // CSR output: the batch indptr, planned on the host
+    uint64_t cap_rows = 0, cap_nnz = 0, data_bytes = 0;
+    cudaEvent_t done = nullptr;
+    bool used = false;
+    uint32_t key = 0;  // output kind the buffers were sized for (output mode, dtype, transform)
+    void free_all();
+};
+
 // A store image: every chunk record at a 16-B aligned offset of a virtual
 // image, either resident in HBM, in pinned host memory, or left in the files.
 class DStore {
@@ -81,6 +97,12 @@ public:
     // steady-state epoch never allocates (cudaMalloc stalls the device)
     void reserve_slots(uint64_t bytes, uint64_t n);
     void release_slot(const SlotRef& s);
+    // output-buffer pool shared by the iterators over this store
+    OutBuffers take_out(uint32_t key);
+    void give_out(OutBuffers&& b);
+    // pinned read-ahead buffers of stream_file iterators, kept the same way
+    uint8_t* take_pinned(uint64_t bytes);
+    void give_pinned(uint8_t* p, uint64_t bytes);
 
 private:
     void load_records(bool to_device);
@@ -103,6 +125,8 @@ private:
     void grow_slab();  // mu_ held
     std::vector<void*> slabs_;
     std::deque<SlotRef> free_;  // FIFO: reuse the slot released longest ago (its readers are done)
+    std::vector<OutBuffers> out_pool_;
+    std::vector<std::pair<uint8_t*, uint64_t>> pinned_pool_;
     uint64_t slot_bytes_ = 0;
 };
 
@@ -133,6 +157,7 @@ private:
     bool direct_;
     bool validate_ = true;  // column checks of every fetched CSR record
     std::vector<Block> slots_;
+    uint64_t buf_bytes_ = 0;
     std::vector<cudaEvent_t> ev_;
     std::vector<uint64_t> released_;  // per slot: last seq released (~0: none)
     std::mutex mu_;
@@ -173,16 +198,7 @@ public:
     void sync();
 
 private:
-    struct OutSlot {
-        void *gidx = nullptr, *indptr = nullptr, *indices = nullptr, *data = nullptr, *scratch = nullptr;
-        RowRef* d_refs = nullptr;
-        RowRef* h_refs = nullptr;
-        uint64_t* h_gidx = nullptr;
-        uint64_t* h_prefix = nullptr;  // CSR output: the batch indptr, planned on the host
-        uint64_t cap_rows = 0, cap_nnz = 0, data_bytes = 0;
-        cudaEvent_t done = nullptr;
-        bool used = false;
-    };
+    using OutSlot = OutBuffers;
     struct Live {
         DStore::SlotRef slot;
         uint64_t live_rows = 0;
