@@ -163,3 +163,24 @@ def test_plan_shuffle_and_order(golden):
         R.plan_shuffle(10, 0, 5, 0)
     with pytest.raises(R.InvalidArgument):
         R.plan_shuffle(10, 6, 5, 0)
+
+
+def test_synth_one_hot_store(tmp_path):
+    """SynthConfig.one_hot (BASELINE config 4's WGS windows, not in the reference):
+    an ordinary dense u8 store (the reference reads it), every row one-hot over
+    the channel planes, deterministic in the seed."""
+    import paper_2604_01949_b200 as R
+    from oracle.oracle import Ref, load_dense_store
+    cfgs = dict(n_obs=200, n_var=4 * 32, layout="dense", value_dtype="u8", seed=5, chunk_rows=48,
+                chunks_per_shard=2, one_hot=4)
+    R.synth_store(tmp_path / "a", R.SynthConfig(**cfgs))
+    R.synth_store(tmp_path / "b", R.SynthConfig(**cfgs))
+    x = load_dense_store(tmp_path / "a").reshape(200, 4, 32)
+    assert ((x == 0) | (x == 1)).all() and (x.sum(axis=1) == 1).all()
+    assert (load_dense_store(tmp_path / "b") == load_dense_store(tmp_path / "a")).all()
+    # the reference loader reads it like any dense store
+    ref = list(Ref.iterate(tmp_path / "a", 48, 96, 50, seed=1, want="dense"))
+    for b in ref:
+        assert b["dense"].tobytes() == x.reshape(200, 128)[b["gidx"].astype(np.int64)].tobytes()
+    with pytest.raises(R.InvalidArgument):
+        R.synth_store(tmp_path / "c", R.SynthConfig(**dict(cfgs, n_var=30)))
