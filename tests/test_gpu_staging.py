@@ -163,3 +163,26 @@ def test_one_hot_dense_staging(tmp_path, out_dtype):
             assert c.h2d_bytes < c.bytes_read / 4  # codes are 1/16 of the rows; row refs (16 B) on top
         it.close()
         ds.close()
+
+
+def test_wide_axis_keeps_verbatim_staging(tmp_path):
+    """n_var > 65,536: column ids do not fit u16, the pinned image stays verbatim
+    (and u64 index stores likewise) -- batches still bit-exact."""
+    rng = np.random.default_rng(3)
+    nv = 70_000
+    rows = [np.sort(rng.choice(nv, int(rng.integers(0, 30)), replace=False)).astype(np.uint64) for _ in range(120)]
+    ip = np.zeros(len(rows) + 1, np.uint64)
+    ip[1:] = np.cumsum([len(r) for r in rows])
+    ix = np.concatenate(rows)
+    dv = (rng.random(len(ix)) + 0.5).astype(np.float32)
+    for idt in ("u32", "u64"):
+        path = tmp_path / idt
+        write_csr_store(path, ip, ix, dv, nv, 16, 4, idt=idt)
+        it = R.BatchIterator(path, R.LoaderConfig(16, 64, 32, 2), 0, staging="stream_pinned", output="csr")
+        for b in it:
+            mb = b.to_minibatch()
+            eip, eix, edv = csr_gather(ip, ix, dv, mb.global_indices)
+            assert (np.asarray(mb.block.indices, np.uint64) == eix).all()
+            assert np.asarray(mb.block.data).tobytes() == edv.tobytes()
+        assert it.counters().h2d_bytes >= it.counters().bytes_read
+        it.close()
