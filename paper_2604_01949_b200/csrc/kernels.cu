@@ -539,9 +539,6 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return t;
 }
 
-// One CTA per output row (grid-stride): zero a shared-memory tile, scatter the
-// row's entries into it, then a single cp.async.bulk store writes the dense
-// tile — every output byte hits HBM exactly once, with no read-modify-write.
 // ============================================================ K3 densify v6 ===
 // Same smem-tile + TMA bulk store scheme as above, with two rows in flight per
 // CTA: while row i's tiles are zeroed/scattered/stored, row i+1's first U*THREADS
