@@ -44,10 +44,11 @@ WORKLOADS = {
                             density=0.1, seed=0, chunk_rows=64, chunks_per_shard=128),
                  loader=dict(fetch_block_rows=64, buffer_capacity_rows=4096, batch_rows=4096, seed=0),
                  out=dict(output="dense", out_dtype="f32", transform=None), dtype="f32"),
-    "cfg2": dict(desc="cfg2-shaped: synthetic CSR 36k genes ~3k nnz/cell f32, 1M cells resident per GPU, "
-                      "f=1024 B=16384 b=4096, densify fp32 + library-size/log1p",
+    "cfg2": dict(desc="cfg2-shaped: synthetic counts CSR, 36k genes, 2k-4k nnz/cell (procedural, SURVEY 8d), "
+                      "values 1..64 as f32, 1M cells resident per GPU, f=1024 B=16384 b=4096, densify fp32 + "
+                      "library-size/log1p",
                  synth=dict(n_obs=1_000_000, n_var=36_000, layout="csr", value_dtype="f32", index_dtype="u32",
-                            density=3000 / 36000, seed=1, chunk_rows=1024, chunks_per_shard=128),
+                            density=3000 / 36000, seed=1, chunk_rows=1024, chunks_per_shard=128, counts=True),
                  loader=dict(fetch_block_rows=1024, buffer_capacity_rows=16384, batch_rows=4096, seed=0),
                  out=dict(output="dense", out_dtype="f32", transform="normalize_log1p"), dtype="f32"),
     "cfg3": dict(desc="cfg3: dense 3x64x64 u8 crops (2M samples), chunk 256, f=256 B=16384 b=1024, cast bf16",

@@ -86,6 +86,8 @@ typedef struct rfl_synth_config {
     uint32_t threads;
     uint32_t one_hot; /* > 0: procedural one-hot dense u8 rows with this many channel planes (not in
                          the reference); 0: synth_store */
+    uint32_t counts;  /* != 0: procedural counts-like csr rows (not in the reference) */
+    uint32_t reserved;
 } rfl_synth_config;
 rfl_status rfl_synth_store(const char* path, const rfl_synth_config* cfg);
 

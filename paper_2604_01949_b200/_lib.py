@@ -36,7 +36,8 @@ class rfl_store_info(C.Structure):
 class rfl_synth_config(C.Structure):
     _fields_ = [("n_obs", u64), ("n_var", u64), ("layout", u32), ("value_dtype", u32),
                 ("index_dtype", u32), ("codec", u32), ("density", C.c_double), ("seed", u64),
-                ("chunk_rows", u64), ("chunks_per_shard", u64), ("threads", u32), ("one_hot", u32)]
+                ("chunk_rows", u64), ("chunks_per_shard", u64), ("threads", u32), ("one_hot", u32),
+                ("counts", u32), ("reserved", u32)]
 
 
 class rfl_loader_config(C.Structure):

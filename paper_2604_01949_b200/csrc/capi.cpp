@@ -189,6 +189,7 @@ rfl_status rfl_synth_store(const char* path, const rfl_synth_config* c) {
         s.chunks_per_shard = c->chunks_per_shard;
         s.threads = c->threads;
         s.one_hot = c->one_hot;
+        s.counts = c->counts != 0;
         rfl::synth_store(path, s);
     });
 }

@@ -319,8 +319,11 @@ bool DStore::delta_image() {
                         hist[best] = 0;
                     }
                     const uint64_t esc = nnz - covered;
-                    if (d8v_layout(rows, nnz, esc).bytes < d8_record_bytes(rows, nnz, vs)) {
-                        kind[q] = kD8Coded;
+                    bool low16_zero = true;
+                    for (uint64_t k = 0; k < nnz && low16_zero; ++k) low16_zero = val[4 * k] == 0 && val[4 * k + 1] == 0;
+                    const uint64_t lb = low16_zero ? 1 : 3;
+                    if (d8v_layout(rows, nnz, esc, lb).bytes < d8_record_bytes(rows, nnz, vs)) {
+                        kind[q] = low16_zero ? kD8Coded16 : kD8Coded;
                         dict[q] = d;
                         n_esc[q] = esc;
                     }
@@ -334,9 +337,10 @@ bool DStore::delta_image() {
         const uint8_t* rec = h_image_ + rec_off_[q];
         const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
         elen[q] = idx16_record_bytes(rows, nnz, vs);
-        len[q] = kind[q] == kIdx16Copy ? elen[q]
-                 : kind[q] == kD8Coded ? d8v_layout(rows, nnz, n_esc[q]).bytes
-                                       : d8_record_bytes(rows, nnz, vs);
+        len[q] = kind[q] == kIdx16Copy  ? elen[q]
+                 : kind[q] == kD8Coded   ? d8v_layout(rows, nnz, n_esc[q]).bytes
+                 : kind[q] == kD8Coded16 ? d8v_layout(rows, nnz, n_esc[q], 1).bytes
+                                         : d8_record_bytes(rows, nnz, vs);
         off[q] = total;
         total = align_up(total + len[q], kAlign);
     }
@@ -373,7 +377,8 @@ bool DStore::delta_image() {
             std::memcpy(dst + d8_values_offset(rows, nnz), val, vs * nnz);
             return;
         }
-        const D8vLayout L = d8v_layout(rows, nnz, n_esc[q]);
+        const bool c16 = kind[q] == kD8Coded16;
+        const D8vLayout L = d8v_layout(rows, nnz, n_esc[q], c16 ? 1 : 3);
         const std::array<uint8_t, 4>& d = dict[q];
         std::memcpy(dst + L.dict, d.data(), 4);
         const uint32_t ne = static_cast<uint32_t>(n_esc[q]);
@@ -387,7 +392,8 @@ bool DStore::delta_image() {
                 const uint32_t code = top == d[0] ? 0u : top == d[1] ? 1u : top == d[2] ? 2u : 3u;
                 dst[L.codes + (k >> 2)] |= static_cast<uint8_t>(code << (2 * (k & 3)));
                 if (code == 3) dst[L.esc + e++] = top;
-                std::memcpy(dst + L.low3 + 3 * k, val + 4 * k, 3);
+                if (c16) dst[L.low3 + k] = val[4 * k + 2];
+                else std::memcpy(dst + L.low3 + 3 * k, val + 4 * k, 3);
             }
         }
     });

@@ -381,7 +381,8 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
         for (uint64_t i = tid; i < (jb.bytes + 15) / 16; i += nt) d4[i] = ld_v4(s4 + i);
         return;
     }
-    const bool coded = jb.kind == kD8Coded;
+    const bool coded = jb.kind == kD8Coded || jb.kind == kD8Coded16;
+    const uint32_t low_b = jb.kind == kD8Coded16 ? 1u : 3u;
     const uint64_t rows = ld_u32(jb.src), nnz = ld_u64_a4(jb.src + 4);
     const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
     const uint32_t* s32 = reinterpret_cast<const uint32_t*>(jb.src);
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
     uint8_t* dv = jb.dst + head + ((2 * nnz + 7) & ~7ull);
     D8vLayout L{};
     if (coded) {
-        L = d8v_layout(rows, nnz, ld_u32(jb.src + d8v_layout(rows, nnz, 0).n_esc));
+        L = d8v_layout(rows, nnz, ld_u32(jb.src + d8v_layout(rows, nnz, 0).n_esc), low_b);
     } else {  // raw values: copied word-wise (+ byte tail)
         const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
         const uint64_t vbytes = nnz * jobs.vs;
@@ -426,9 +427,15 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
                 if (valid) {
                     const uint32_t top = code == 3u ? __ldg(jb.src + L.esc + esc_at + __popc(em & lt))
                                                     : __ldg(jb.src + L.dict + code);
-                    const uint8_t* l3 = jb.src + L.low3 + 3 * k;
-                    vout[k] = (top << 24) | (static_cast<uint32_t>(__ldg(l3 + 2)) << 16) |
-                              (static_cast<uint32_t>(__ldg(l3 + 1)) << 8) | __ldg(l3);
+                    uint32_t low;
+                    if (low_b == 1) {
+                        low = static_cast<uint32_t>(__ldg(jb.src + L.low3 + k)) << 16;
+                    } else {
+                        const uint8_t* l3 = jb.src + L.low3 + 3 * k;
+                        low = (static_cast<uint32_t>(__ldg(l3 + 2)) << 16) | (static_cast<uint32_t>(__ldg(l3 + 1)) << 8) |
+                              __ldg(l3);
+                    }
+                    vout[k] = (top << 24) | low;
                 }
                 esc_at += __popc(em);
             }

@@ -79,7 +79,9 @@ inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) { retu
 struct D8vLayout {
     uint64_t first, delta, esc_base, dict, n_esc, codes, esc, low3, bytes;
 };
-RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc) {
+// low_bytes = 3, or 1 when the low 16 bits of every value of the record are zero
+// (integer counts stored as float: byte 2 carries the exponent LSB + top mantissa bits)
+RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc, uint64_t low_bytes = 3) {
     D8vLayout l{};
     l.first = kCsrHeaderBytes + 4 * (rows + 1);
     l.delta = l.first + ((2 * rows + 3) & ~3ull);
@@ -89,13 +91,14 @@ RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc) 
     l.codes = l.n_esc + 4;
     l.esc = l.codes + ((((nnz + 3) / 4) + 3) & ~3ull);
     l.low3 = l.esc + ((n_esc + 3) & ~3ull);
-    l.bytes = l.low3 + 3 * nnz;
+    l.bytes = l.low3 + low_bytes * nnz;
     return l;
 }
 // kOneHot4: a dense u8 record whose rows are one-hot over 4 channel planes
 // ([4][L] bytes, exactly one 1 per position) staged as 2-bit channel codes,
 // L/4 bytes per row (16x smaller; L a multiple of 16)
-enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2, kOneHot4 = 3 };
+// kD8Coded16: kD8Coded whose values all have a zero low half (1 stored byte each)
+enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2, kOneHot4 = 3, kD8Coded16 = 4 };
 struct D8Job {
     const uint8_t* src;  // staged record (device)
     uint8_t* dst;        // idx16 record (device)

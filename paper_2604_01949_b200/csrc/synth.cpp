@@ -6,6 +6,7 @@
 // chunk records in order (StoreWriter::append -> emit_chunk, store.cpp:170-213).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <thread>
 
 #include "format.hpp"
@@ -170,9 +171,61 @@ Manifest synth_one_hot(const std::string& path, const SynthCfg& c) {
 }
 }  // namespace
 
+Manifest synth_counts(const std::string& path, const SynthCfg& c) {
+    if (c.layout != Layout::csr || (c.value_dtype != VDtype::f32 && c.value_dtype != VDtype::i32))
+        invalid("synth: counts needs a csr store with f32 or i32 values");
+    Manifest man;
+    man.layout = Layout::csr;
+    man.n_var = c.n_var;
+    man.value_dtype = c.value_dtype;
+    man.index_dtype = c.index_dtype;
+    man.chunk_rows = c.chunk_rows;
+    man.chunks_per_shard = c.chunks_per_shard;
+    man.codec = Codec::none;
+    man.var_names.reserve(c.n_var);
+    for (uint64_t i = 0; i < c.n_var; ++i) man.var_names.push_back("v" + std::to_string(i));
+    RecordWriter w(path, man, /*defer_manifest=*/false);
+    const unsigned T = c.threads ? c.threads : std::max(1u, std::thread::hardware_concurrency());
+    const size_t vs = value_size(c.value_dtype);
+    std::vector<uint8_t> rec;
+    for (uint64_t r0 = 0; r0 < c.n_obs; r0 += c.chunk_rows) {
+        const uint64_t rows = std::min<uint64_t>(c.chunk_rows, c.n_obs - r0);
+        std::vector<uint64_t> nnz(rows);
+        for (uint64_t i = 0; i < rows; ++i)
+            nnz[i] = std::min<uint64_t>(c.n_var, 2000 + mix64(c.seed ^ mix64(r0 + i)) % 2001);
+        std::vector<uint64_t> indptr(rows + 1, 0);
+        for (uint64_t i = 0; i < rows; ++i) indptr[i + 1] = indptr[i] + nnz[i];
+        std::vector<uint64_t> indices(indptr[rows]);
+        std::vector<uint8_t> data(indptr[rows] * vs);
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                for (uint64_t i = t; i < rows; i += T) {
+                    const uint64_t h = mix64(c.seed ^ mix64(r0 + i)), n = nnz[i];
+                    for (uint64_t k = 0; k < n; ++k) {
+                        const uint64_t lo = k * c.n_var / n, hi = (k + 1) * c.n_var / n;  // stratum
+                        indices[indptr[i] + k] = lo + mix64(h ^ k) % (hi - lo);
+                        const uint32_t cnt = 1 + static_cast<uint32_t>(mix64(h ^ (k + (1ull << 32))) % 64);
+                        if (c.value_dtype == VDtype::f32) {
+                            const float f = static_cast<float>(cnt);
+                            std::memcpy(data.data() + (indptr[i] + k) * 4, &f, 4);
+                        } else {
+                            std::memcpy(data.data() + (indptr[i] + k) * 4, &cnt, 4);
+                        }
+                    }
+                }
+            });
+        for (auto& th : pool) th.join();
+        encode_csr_rows(indptr.data(), indices.data(), data.data(), vs, c.index_dtype, 0, rows, rec);
+        w.append_record(rec.data(), rec.size(), rows);
+    }
+    return w.finish();
+}
+
 Manifest synth_store(const std::string& path, const SynthCfg& c) {
     if (c.n_obs == 0 || c.n_var == 0) invalid("synth: n_obs and n_var must be >= 1");
     if (c.one_hot) return synth_one_hot(path, c);
+    if (c.counts) return synth_counts(path, c);
     if (c.layout == Layout::csr && (c.density <= 0.0 || c.density > 1.0))
         invalid("synth: density must lie in (0, 1] for csr stores");
     if (c.codec != Codec::none) invalid("synth: only codec none is supported by the GPU build");

@@ -24,6 +24,11 @@ struct SynthCfg {
     // has its 1 in channel mix64(seed ^ mix64(i) ^ p) % one_hot (SURVEY §8d
     // config 4, "4 x 1024 one-hot").  The store is an ordinary dense u8 store.
     unsigned one_hot = 0;
+    // counts (csr f32/i32 only, not in the reference): procedural counts-like rows
+    // (SURVEY §8d config 2): h = mix64(seed ^ mix64(row)); nnz = 2,000 + h % 2,001
+    // (capped at n_var); one column per stratum of n_var / nnz (stratified jitter,
+    // strictly increasing); value = 1 + mix64(h ^ (k + 2^32)) % 64.
+    bool counts = false;
 };
 
 // synth_store (reference src/synth.cpp:60-144), byte-identical output.

@@ -94,6 +94,7 @@ class SynthConfig:
     codec: str = "none"
     threads: int = 0
     one_hot: int = 0  # > 0: procedural one-hot dense u8 rows (channel planes), see rfl_synth_config
+    counts: bool = False  # procedural counts-like csr rows (2k-4k nnz/row, values 1..64), see rfl_synth_config
 
 
 def synth_store(path, config: SynthConfig) -> StoreManifest:
@@ -101,7 +102,7 @@ def synth_store(path, config: SynthConfig) -> StoreManifest:
     c = L.rfl_synth_config(config.n_obs, config.n_var, LAYOUTS[config.layout], VDTYPES[config.value_dtype],
                            IDTYPES[config.index_dtype], 0 if config.codec == "none" else 1, config.density,
                            config.seed, config.chunk_rows, config.chunks_per_shard, config.threads,
-                           config.one_hot)
+                           config.one_hot, int(config.counts), 0)
     L.check(L.lib().rfl_synth_store(str(path).encode(), C.byref(c)))
     return StoreReader(path).manifest()
 

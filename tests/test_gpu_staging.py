@@ -11,7 +11,7 @@ import pytest
 import torch
 
 import paper_2604_01949_b200 as R
-from oracle.oracle import csr_gather, normalize_log1p, to_dense, write_csr_store
+from oracle.oracle import csr_gather, load_csr_store, normalize_log1p, to_dense, write_csr_store
 
 pytestmark = pytest.mark.gpu
 
@@ -185,4 +185,33 @@ def test_wide_axis_keeps_verbatim_staging(tmp_path):
             assert (np.asarray(mb.block.indices, np.uint64) == eix).all()
             assert np.asarray(mb.block.data).tobytes() == edv.tobytes()
         assert it.counters().h2d_bytes >= it.counters().bytes_read
+        it.close()
+
+
+@pytest.mark.parametrize("vdt", ["f32", "i32"])
+def test_counts_store_staging(tmp_path, vdt):
+    """Procedural counts (BASELINE config 2's shape): integer values whose low 16
+    bits are zero as f32 stage with 1 stored byte per value next to the top-byte
+    code; i32 counts keep 3 low bytes.  Batches bit-exact, normalize within 1e-6."""
+    path = tmp_path / "s"
+    R.synth_store(path, R.SynthConfig(n_obs=600, n_var=9000, layout="csr", value_dtype=vdt, seed=4, chunk_rows=64,
+                                      chunks_per_shard=4, counts=True))
+    ip, ix, dv = load_csr_store(path)
+    for out, xf in (("csr", None), ("dense", None), ("dense", "normalize_log1p")):
+        it = R.BatchIterator(path, R.LoaderConfig(64, 256, 100, 1), 0, staging="stream_pinned", output=out,
+                             out_dtype="f32" if xf else "native", transform=xf)
+        for b in it:
+            g = b.global_indices_host
+            eip, eix, edv = csr_gather(ip, ix, dv, g)
+            if out == "csr":
+                mb = b.to_minibatch()
+                assert (np.asarray(mb.block.indices, np.uint64) == eix).all()
+                assert np.asarray(mb.block.data).tobytes() == edv.tobytes()
+            elif xf is None:
+                assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, 9000).tobytes()
+            else:
+                want = normalize_log1p(to_dense(eip, eix, edv.astype(np.float32), 9000))
+                np.testing.assert_allclose(b.data.cpu().numpy().astype(np.float64), want, rtol=1e-6, atol=0)
+        c = it.counters()
+        assert c.h2d_bytes < (0.45 if vdt == "f32" else 0.7) * c.bytes_read
         it.close()
