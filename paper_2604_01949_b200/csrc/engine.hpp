@@ -22,6 +22,12 @@
 
 namespace rfl {
 
+// Record placement in store images: 16-B aligned records, 256 B of tail padding
+// for 16-B over-reads.
+constexpr uint64_t kRecAlign = 16;
+constexpr uint64_t kRecPad = 256;
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
 enum Staging : uint32_t { kResident = 0, kStreamPinned = 1, kStreamFile = 2 };
 
 void cuda_ok(cudaError_t e, const char* what);
