@@ -287,6 +287,18 @@ def run_ours(args, wl, rank, world, local, dist):
 
     # ---------------------------------------------------------------- e2e --
     e2e = run_e2e(args, wl, reader, W, rank, world, local, dist)
+    if not args.no_verbatim_e2e and os.environ.get("RIFFLE_E2E_STAGING", "stream_pinned") == "stream_pinned":
+        # the same e2e leg with the pinned image left verbatim (no re-encoding at open), for reference
+        old_nw = os.environ.get("RFL_NARROW")
+        os.environ["RFL_NARROW"] = "0"
+        try:
+            v = run_e2e(args, wl, reader, W, rank, world, local, dist)
+        finally:
+            if old_nw is None:
+                os.environ.pop("RFL_NARROW", None)
+            else:
+                os.environ["RFL_NARROW"] = old_nw
+        e2e["verbatim_staging"] = {"value": v["value"], "h2d_bytes_per_step": v["h2d_bytes_per_step"]}
     clk.__exit__(None, None, None)
     ds.close()
 
@@ -564,6 +576,8 @@ def main():
     ap.add_argument("--workload", default="cfg1", choices=sorted(WORKLOADS) + ["cfg5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--no-verbatim-e2e", action="store_true",
+                    help="skip the second e2e leg with the verbatim (not re-encoded) pinned image")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
