@@ -215,3 +215,35 @@ def test_counts_store_staging(tmp_path, vdt):
         c = it.counters()
         assert c.h2d_bytes < (0.45 if vdt == "f32" else 0.7) * c.bytes_read
         it.close()
+
+
+def test_two_iterators_share_one_store(crafted):
+    """Two iterators over ONE stream_pinned DeviceStore, next() calls interleaved:
+    they share the store's block-slot pool (slots released by one are reused by
+    the other behind its release event) and, after close, the output-buffer
+    pool.  Both streams stay bit-exact."""
+    path, ip, ix, dv = crafted
+    ds = R.DeviceStore(path, 0, "stream_pinned")
+    for rnd in range(2):  # second round reuses the pooled output buffers
+        its = [R.BatchIterator(ds, R.LoaderConfig(16, 96, 40, 3 + k), k + rnd, output=out)
+               for k, out in enumerate(("csr", "dense"))]
+        live = [True, True]
+        while any(live):
+            for k, it in enumerate(its):
+                if not live[k]:
+                    continue
+                b = it.next()
+                if b is None:
+                    live[k] = False
+                    continue
+                g = b.global_indices_host
+                eip, eix, edv = csr_gather(ip, ix, dv, g)
+                if k == 0:
+                    mb = b.to_minibatch()
+                    assert (np.asarray(mb.block.indices, np.uint64) == eix).all()
+                    assert np.asarray(mb.block.data).tobytes() == edv.tobytes()
+                else:
+                    assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, NV).tobytes()
+        for it in its:
+            it.close()
+    ds.close()
