@@ -247,3 +247,33 @@ def test_two_iterators_share_one_store(crafted):
         for it in its:
             it.close()
     ds.close()
+
+
+def test_iterators_on_threads_share_one_store(crafted):
+    """Many iterators may share one store (loader.hpp:55-57): four host threads
+    each run a whole epoch over one stream_pinned DeviceStore concurrently."""
+    import threading
+    path, ip, ix, dv = crafted
+    ds = R.DeviceStore(path, 0, "stream_pinned")
+    errors = []
+
+    def run(k):
+        try:
+            torch.cuda.set_device(0)
+            it = R.BatchIterator(ds, R.LoaderConfig(16, 96, 40, 10 + k), k, output="csr")
+            for b in it:
+                mb = b.to_minibatch()
+                eip, eix, edv = csr_gather(ip, ix, dv, mb.global_indices)
+                assert (np.asarray(mb.block.indices, np.uint64) == eix).all()
+                assert np.asarray(mb.block.data).tobytes() == edv.tobytes()
+            it.close()
+        except Exception as e:  # noqa: BLE001 -- surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    ds.close()
+    assert not errors, errors
