@@ -309,12 +309,12 @@ def run_ours(args, wl, rank, world, local, dist):
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": K, "warmup": Wm,
             "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": W["dtype"], "data": "synthetic (product synth_store == reference synth_store bytes)",
-            "config": {"workload": W["desc"], "staging": "resident (chunk records in HBM)",
-                       "launch": "K steps replayed as one CUDA graph" if graph is not None else "eager launches",
-                       "l2": "inputs larger than L2 (store %.2f GB, batch output %.0f MB)" % (
-                           ds_bytes(reader) / 1e9, b * man.n_var * esz / 1e6),
-                       "parallelism": f"dp{world} (disjoint plan positions per rank, no collective)",
-                       "cells_per_step_per_rank": cells / K},
+            "config": bench_config(wl, world),
+            "details": {"staging": "resident (chunk records in HBM)",
+                        "launch": "K steps replayed as one CUDA graph" if graph is not None else "eager launches",
+                        "l2": "inputs larger than L2 (store %.2f GB, batch output %.0f MB)" % (
+                            ds_bytes(reader) / 1e9, b * man.n_var * esz / 1e6),
+                        "cells_per_step_per_rank": cells / K},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_csr_densify" if man.layout == "csr" else "k_dense_gather",
@@ -489,10 +489,9 @@ def run_preshuffle(args, rank, world, local, dist):
            "n_gpus": world, "steps": rounds, "warmup": rounds, "ms_per_step": gpu_max / rounds,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32+f32 (bytes)",
            "data": "synthetic (product synth_store == reference synth_store bytes)",
-           "config": {"workload": CFG5["desc"], "payload_GB": payload / 1e9,
-                      "value_def": "payload bytes / device time of the round kernels (scan + pack), max over ranks",
-                      "l2": "rounds of ~1 GB of records, larger than L2",
-                      "parallelism": f"{world} rank(s): rank b mod W stages block b, shard s owned by rank s mod W"},
+           "config": bench_config("cfg5", world),
+           "details": {"payload_GB": payload / 1e9,
+                       "value_def": "payload bytes / device time of the round kernels (scan + pack), max over ranks"},
            "roofline": {"bound": "hbm", "achieved": alg / (gpu_max / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                         "frac": alg / (gpu_max / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                         "kernel": "k_row_scan + k_csr_pack", "alg_bytes_per_launch": alg / rounds,
@@ -530,11 +529,55 @@ def cpu_shuffle_baseline():
             "sample": f"run_shuffle of a {n}-row subset of the same shape ({pb / 1e9:.2f} GB), wall {w:.1f}s"}
 
 
+# --impl reference input sizes: cfg1 is the whole workload (100k cells); the other
+# workloads' reference inputs are bounded subsets of the same shape (whole epochs of
+# the subset are timed; the per-cell cost does not depend on n_obs)
+REF_ROWS = {"cfg1": None, "cfg2": 65_536, "cfg3": 131_072, "cfg4": 524_288}
+
+
+def ensure_ref_store(wl):
+    """The reference arm's input, built without the product: the reference's own
+    synth_store (oracle/_ref) for the reference-synth shapes, the oracle's numpy
+    restatement of the procedural generators for cfg2 (counts) / cfg4 (one-hot).
+    Byte-identical to what the product synthesises for the same config
+    (tests/test_host.py, tests/test_oracle.py)."""
+    from oracle import oracle as O
+    base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
+    s = dict(WORKLOADS[wl]["synth"])
+    n = REF_ROWS[wl] or s["n_obs"]
+    path = base / f"ref_{wl}_{n}"
+    if not (path / "manifest.json").exists():
+        base.mkdir(parents=True, exist_ok=True)
+        tmp = base / f".ref_{wl}.{os.getpid()}"
+        if s.get("counts"):
+            O.synth_counts_np(tmp, n, s["n_var"], s["seed"], s["chunk_rows"], s["chunks_per_shard"], s["value_dtype"])
+        elif s.get("one_hot"):
+            O.synth_one_hot_np(tmp, n, s["n_var"], s["seed"], s["chunk_rows"], s["chunks_per_shard"], s["one_hot"])
+        else:
+            O.Ref.synth(tmp, n, s["n_var"], s["layout"], s["value_dtype"], s.get("index_dtype", "u32"),
+                        s["density"], s["seed"], s["chunk_rows"], s["chunks_per_shard"])
+        os.replace(tmp, path)
+    return path, n
+
+
+def bench_config(wl, world):
+    """`config` of a bench line: the same keys (and workload) in both arms."""
+    if wl == "cfg5":
+        return {"workload": CFG5["desc"], "l2": "rounds of ~1 GB of records, larger than L2",
+                "parallelism": f"{world} rank(s): rank b mod W stages block b, shard s owned by rank s mod W"}
+    W = WORKLOADS[wl]
+    return {"workload": W["desc"], "l2": "inputs larger than L2 (store and per-step output exceed 126 MB)",
+            "parallelism": f"dp{world} (disjoint plan positions per rank, no collective)"}
+
+
 def run_reference(args, wl, rank, world):
-    """--impl reference: the reference CPU implementation, all host threads, rank 0 only."""
+    """--impl reference: the reference CPU implementation (oracle/_ref, the unmodified
+    reference compiled from its sources), all host threads, rank 0 only.  Never
+    imports the product.  Timed like riffle::run_throughput(epochs=1, warmup=1)
+    (metrics.cpp:99-136): every thread drains one whole warm-up epoch, then one
+    whole timed epoch (BatchIterator(prefetch_depth=4) + to_dense per CSR batch)."""
     if rank != 0:
         return None
-    import torch  # noqa: F401  (same environment as our arm)
     from oracle.oracle import Ref
     if wl == "cfg5":
         b = cpu_shuffle_baseline()
@@ -542,28 +585,29 @@ def run_reference(args, wl, rank, world):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32+f32 (bytes)",
                 "data": "synthetic (reference synth_store)", "impl": "reference",
-                "config": {"workload": CFG5["desc"], "parallelism": "1 host thread (run_shuffle is sequential)"},
+                "config": bench_config(wl, world), "threads": 1,
                 "cpu_baseline": b, "e2e": {"value": b["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                                            "d2h_bytes_per_step": 0}}
     W = WORKLOADS[wl]
-    path = ensure_store(wl, 0, 1, None)
+    path, n = ensure_ref_store(wl)
     threads = os.cpu_count() or 1
     ld = W["loader"]
     dens = W["out"]["output"] == "dense" and W["synth"]["layout"] == "csr"
     Ref.throughput(path, ld["fetch_block_rows"], ld["buffer_capacity_rows"], ld["batch_rows"], seed=ld["seed"],
-                   depth=4, epoch0=100, threads=threads, max_batches=max(1, args.warmup // 3), densify=dens)
+                   depth=4, epoch0=1000, threads=threads, max_batches=0, densify=dens)  # warm-up epochs
     v, rows, wall = Ref.throughput(path, ld["fetch_block_rows"], ld["buffer_capacity_rows"], ld["batch_rows"],
-                                   seed=ld["seed"], depth=4, epoch0=0, threads=threads,
-                                   max_batches=max(1, args.steps // 4), densify=dens)
+                                   seed=ld["seed"], depth=4, epoch0=0, threads=threads, max_batches=0,
+                                   densify=dens)
     steps = rows / ld["batch_rows"]
+    sample = (f"{threads} concurrent BatchIterators x one whole epoch each (epochs 0..{threads - 1}; one whole "
+              f"warm-up epoch each before) over {'the workload store' if REF_ROWS[wl] is None else f'a {n}-row subset of the workload shape'}"
+              f" ({rows} cells){' + to_dense' if dens else ''}, wall {wall:.1f}s")
     return {"metric": METRIC, "value": v, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": wall * 1e3 / max(steps, 1e-9), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": W["dtype"],
-            "data": "synthetic (reference synth_store)", "impl": "reference",
-            "config": {"workload": W["desc"], "parallelism": f"{threads} host threads (one iterator each)"},
-            "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference",
-                             "sample": f"{rows} cells over {threads} concurrent BatchIterators (epochs 0..{threads - 1})"
-                                       f"{' + to_dense' if dens else ''}, wall {wall:.1f}s"},
+            "data": "synthetic (reference synth_store; cfg2/cfg4: the oracle's numpy procedural generator)",
+            "impl": "reference", "config": bench_config(wl, world), "threads": threads,
+            "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

@@ -197,6 +197,10 @@ rfl_status rfl_loader_counters_get(const rfl_loader* l, rfl_loader_counters* out
  * and gidx (u64[n_rows]) are non-NULL. */
 rfl_status rfl_batch_download(const rfl_batch* b, uint64_t* h_indptr, void* h_indices, void* h_data,
                               uint64_t* h_gidx);
+/* Order a consumer stream after a batch: cudaStreamWaitEvent(stream, ready_event).
+ * Work the caller queues on `stream` afterwards sees the finished batch
+ * (the reference returns MiniBatch by value, so reading it needs no wait). */
+rfl_status rfl_batch_wait(const rfl_batch* b, void* stream);
 rfl_status rfl_loader_sync(rfl_loader* l);
 void rfl_loader_destroy(rfl_loader* l);
 

@@ -469,3 +469,78 @@ def write_csr_store(path, indptr, indices, data, n_var, chunk_rows, cps, idt="u3
            '  "var_names": %s,\n  "has_provenance": false\n}\n') % (
         n, n_var, vdt, idt, chunk_rows, cps, ("[\n" + names + "\n  ]") if n_var else "[]")
     (p / "manifest.json").write_text(man)
+
+
+# ----------------------------------------------------------------------------
+# Procedural synthetic stores (numpy restatement of the product's synth_counts /
+# synth_one_hot): the reference has no such generator, so bench.py's
+# --impl reference leg builds its cfg2 / cfg4 inputs with these (never with the
+# product).  Pinned byte-for-byte against the product synth in tests/test_host.py.
+# ----------------------------------------------------------------------------
+_M1, _M2, _GOLD = np.uint64(0xbf58476d1ce4e5b9), np.uint64(0x94d049bb133111eb), np.uint64(0x9e3779b97f4a7c15)
+
+
+def mix64_np(x) -> np.ndarray:
+    """rng.hpp:12-17 (splitmix64 finalizer), elementwise over uint64 (wrapping)."""
+    x = np.asarray(x, np.uint64) + _GOLD
+    x = (x ^ (x >> np.uint64(30))) * _M1
+    x = (x ^ (x >> np.uint64(27))) * _M2
+    return x ^ (x >> np.uint64(31))
+
+
+def synth_counts_np(path, n_obs, n_var, seed, chunk_rows, cps, vdt="f32"):
+    """Counts-like CSR (2,000 + h mod 2,001 stratified columns per row, values 1..64)."""
+    sd = np.uint64(seed)
+    rows = np.arange(n_obs, dtype=np.uint64)
+    h = mix64_np(sd ^ mix64_np(rows))
+    nnz = np.minimum(np.uint64(n_var), np.uint64(2000) + h % np.uint64(2001)).astype(np.int64)
+    indptr = np.zeros(n_obs + 1, np.uint64)
+    indptr[1:] = np.cumsum(nnz)
+    r = np.repeat(np.arange(n_obs), nnz)
+    k = (np.arange(int(indptr[-1]), dtype=np.int64) - indptr[r].astype(np.int64)).astype(np.uint64)
+    n = nnz[r].astype(np.uint64)
+    hr = h[r]
+    lo = k * np.uint64(n_var) // n
+    hi = (k + np.uint64(1)) * np.uint64(n_var) // n
+    idx = lo + mix64_np(hr ^ k) % (hi - lo)
+    cnt = np.uint64(1) + mix64_np(hr ^ (k + np.uint64(1 << 32))) % np.uint64(64)
+    data = cnt.astype(np.float32) if vdt == "f32" else cnt.astype(np.int32)
+    write_csr_store(path, indptr, idx, data, n_var, chunk_rows, cps, "u32", vdt)
+
+
+def write_dense_store(path, x: np.ndarray, chunk_rows, cps, vdt="u8"):
+    """StoreWriter restatement for dense stores (row-major records, store.cpp:31-33)."""
+    p = Path(path)
+    (p / "shards").mkdir(parents=True)
+    n, n_var = x.shape
+    recs = [np.ascontiguousarray(x[s:s + chunk_rows]).tobytes() for s in range(0, n, chunk_rows)]
+    for sh in range((len(recs) + cps - 1) // cps):
+        part = recs[sh * cps:(sh + 1) * cps]
+        slots, off = [], 0
+        with open(p / "shards" / f"s{sh:08d}.bin", "wb") as f:
+            for r in part:
+                slots.append((off, len(r)))
+                f.write(r)
+                off += len(r)
+            slots += [(2**64 - 1, 2**64 - 1)] * (cps - len(part))
+            f.write(b"".join(struct.pack("<QQ", a, b) for a, b in slots) + b"SHRDIDX1")
+    names = ",\n".join(f'    "v{i}"' for i in range(n_var))
+    man = ('{\n  "format_version": 1,\n  "layout": "dense",\n  "n_obs": %d,\n  "n_var": %d,\n  "value_dtype": "%s",\n'
+           '  "chunk_rows": %d,\n  "chunks_per_shard": %d,\n  "codec": "none",\n'
+           '  "var_names": %s,\n  "has_provenance": false\n}\n') % (
+        n, n_var, vdt, chunk_rows, cps, ("[\n" + names + "\n  ]") if n_var else "[]")
+    (p / "manifest.json").write_text(man)
+
+
+def synth_one_hot_np(path, n_obs, n_var, seed, chunk_rows, cps, channels=4):
+    """One-hot dense u8 rows: position p of row i is 1 in channel mix64(h_i ^ p) % channels."""
+    L = n_var // channels
+    x = np.zeros((n_obs, n_var), np.uint8)
+    p = np.arange(L, dtype=np.uint64)
+    for s in range(0, n_obs, 65536):
+        e = min(n_obs, s + 65536)
+        h = mix64_np(np.uint64(seed) ^ mix64_np(np.arange(s, e, dtype=np.uint64)))
+        ch = (mix64_np(h[:, None] ^ p[None, :]) % np.uint64(channels)).astype(np.int64)
+        rr = np.arange(e - s)[:, None]
+        x[s + rr, ch * L + p[None, :].astype(np.int64)] = 1
+    write_dense_store(path, x, chunk_rows, cps, "u8")

@@ -108,6 +108,7 @@ SIGNATURES = [
     ("rfl_loader_next", C.c_int, [vp, C.POINTER(rfl_batch)]),
     ("rfl_loader_counters_get", C.c_int, [vp, C.POINTER(rfl_loader_counters)]),
     ("rfl_batch_download", C.c_int, [C.POINTER(rfl_batch), vp, vp, vp, vp]),
+    ("rfl_batch_wait", C.c_int, [C.POINTER(rfl_batch), vp]),
     ("rfl_loader_sync", C.c_int, [vp]),
     ("rfl_loader_destroy", None, [vp]),
     ("rfl_csr_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp, vp, vp, vp]),

@@ -344,6 +344,16 @@ rfl_status rfl_batch_download(const rfl_batch* b, uint64_t* h_indptr, void* h_in
     });
 }
 
+rfl_status rfl_batch_wait(const rfl_batch* b, void* stream) {
+    return guarded([&] {
+        if (!b) rfl::invalid("null argument");
+        if (b->ready_event)
+            rfl::cuda_ok(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream),
+                                             static_cast<cudaEvent_t>(b->ready_event), 0),
+                         "cudaStreamWaitEvent");
+    });
+}
+
 rfl_status rfl_loader_sync(rfl_loader* l) {
     return guarded([&] {
         if (!l) rfl::invalid("null argument");

@@ -114,6 +114,21 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     image_bytes_ = off;
     if (m.layout == Layout::csr) row_nnz_.resize(m.n_obs);
     DeviceGuard g(device_);
+    try {
+        open_image();
+    } catch (...) {  // the destructor does not run for a throwing constructor
+        if (d_arena_) cudaFree(d_arena_);
+        if (h_image_) cudaFreeHost(h_image_);
+        d_arena_ = nullptr;
+        h_image_ = nullptr;
+        throw;
+    }
+}
+
+// load (resident / stream_pinned), validate and re-encode the image; per-row nnz
+void DStore::open_image() {
+    const Manifest& m = hs_->manifest();
+    const uint64_t nch = m.chunk_count();
     if (staging_ == kResident) load_records(true);
     else if (staging_ == kStreamPinned) load_records(false);
     // CsrBlock::validate of every record, once, on the GPU (the reference
@@ -121,21 +136,11 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     // in place over PCIe (mapped pinned memory)
     if (m.layout == Layout::csr && staging_ != kStreamFile) {
         const char* nv = std::getenv("RFL_NO_VALIDATE");
-        if (!(nv && nv[0] == '1')) {
-            try {
-                validate_records(staging_ == kResident ? d_arena_ : h_image_);
-            } catch (...) {  // the destructor does not run for a throwing constructor
-                if (d_arena_) cudaFree(d_arena_);
-                if (h_image_) cudaFreeHost(h_image_);
-                d_arena_ = nullptr;
-                h_image_ = nullptr;
-                throw;
-            }
-        }
+        if (!(nv && nv[0] == '1')) validate_records(staging_ == kResident ? d_arena_ : h_image_);
     }
     img_off_ = rec_off_;
     img_len_ = rec_len_;
-    if (staging_ == kStreamPinned && m.layout == Layout::dense && m.value_dtype == VDtype::u8 && m.n_var % 16 == 0) {
+    if (staging_ == kStreamPinned && m.layout == Layout::dense && m.value_dtype == VDtype::u8 && m.n_var % 64 == 0) {
         const char* e = std::getenv("RFL_NARROW");
         if (!(e && e[0] == '0')) one_hot_image();
     }
@@ -276,8 +281,9 @@ DStore::~DStore() {
     DeviceGuard g(device_);
     for (auto& b : out_pool_) b.free_all();
     for (auto& pb : pinned_pool_) cudaFreeHost(pb.first);
-    for (auto& s : free_)
-        if (s.released) cudaEventDestroy(s.released);
+    for (auto& kv : free_)
+        for (auto& s : kv.second)
+            if (s.released) cudaEventDestroy(s.released);
     for (void* p : slabs_) cudaFree(p);
     if (d_arena_) cudaFree(d_arena_);
     if (h_image_) cudaFreeHost(h_image_);
@@ -312,38 +318,38 @@ ArenaView DStore::view(const uint8_t* base) const {
 }
 
 void DStore::reserve_slots(uint64_t bytes, uint64_t n) {
-    release_slot(acquire_slot(bytes));  // adopts the slot geometry
+    const uint64_t key = align_up(std::max<uint64_t>(bytes, 1), 256);
     std::lock_guard<std::mutex> lk(mu_);
-    while (free_.size() < n) grow_slab();
+    std::deque<SlotRef>& pool = free_[key];
+    while (pool.size() < n) grow_slab(key);
 }
 
-void DStore::grow_slab() {
+void DStore::grow_slab(uint64_t slot_bytes) {
     const uint64_t n = 32;
     void* slab = nullptr;
-    cuda_ok(cudaMalloc(&slab, n * slot_bytes_ + kPad), "cudaMalloc slab");
+    cuda_ok(cudaMalloc(&slab, n * slot_bytes + kPad), "cudaMalloc slab");
     slabs_.push_back(slab);
+    std::deque<SlotRef>& pool = free_[slot_bytes];
     for (uint64_t i = 0; i < n; ++i) {
         SlotRef s;
-        s.ptr = static_cast<uint8_t*>(slab) + i * slot_bytes_;
-        s.bytes = slot_bytes_;
+        s.ptr = static_cast<uint8_t*>(slab) + i * slot_bytes;
+        s.bytes = slot_bytes;
         cuda_ok(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming), "event");
-        free_.push_back(s);
+        pool.push_back(s);
     }
 }
 
 DStore::SlotRef DStore::acquire_slot(uint64_t bytes) {
+    // one FIFO pool per slot size: iterators with different fetch_block_rows over one
+    // store each recycle their own geometry's slabs (nothing is orphaned)
+    const uint64_t key = align_up(std::max<uint64_t>(bytes, 1), 256);
     std::lock_guard<std::mutex> lk(mu_);
-    if (bytes > slot_bytes_) {  // first use (or a bigger block geometry): new pool
-        for (auto& s : free_)
-            if (s.released) cudaEventSynchronize(s.released), cudaEventDestroy(s.released);
-        free_.clear();
-        slot_bytes_ = align_up(std::max<uint64_t>(bytes, 1), 256);
-    }
-    if (free_.empty()) grow_slab();
+    std::deque<SlotRef>& pool = free_[key];
+    if (pool.empty()) grow_slab(key);
     // oldest first: a LIFO pop would hand the next batch's copy the slot the
     // previous batch's kernel just released, serialising copy(i+1) behind kernel(i)
-    SlotRef s = free_.front();
-    free_.pop_front();
+    SlotRef s = pool.front();
+    pool.pop_front();
     return s;
 }
 
@@ -410,8 +416,7 @@ void DStore::give_out(OutBuffers&& b) {
 
 void DStore::release_slot(const SlotRef& s) {
     std::lock_guard<std::mutex> lk(mu_);
-    if (s.bytes == slot_bytes_) free_.push_back(s);
-    else if (s.released) cudaEventDestroy(s.released);  // from a retired pool geometry
+    free_[s.bytes].push_back(s);
 }
 
 // ============================================================ BlockReader ===

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <exception>
 #include <deque>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -111,6 +112,7 @@ public:
     void give_pinned(uint8_t* p, uint64_t bytes);
 
 private:
+    void open_image();
     void load_records(bool to_device);
     void validate_records(const uint8_t* base);
     void narrow_image();
@@ -128,12 +130,12 @@ private:
     uint8_t* d_arena_ = nullptr;
     uint8_t* h_image_ = nullptr;
     std::mutex mu_;
-    void grow_slab();  // mu_ held
+    void grow_slab(uint64_t slot_bytes);  // mu_ held
     std::vector<void*> slabs_;
-    std::deque<SlotRef> free_;  // FIFO: reuse the slot released longest ago (its readers are done)
+    // per slot size, FIFO: reuse the slot released longest ago (its readers are done)
+    std::map<uint64_t, std::deque<SlotRef>> free_;
     std::vector<OutBuffers> out_pool_;
     std::vector<std::pair<uint8_t*, uint64_t>> pinned_pool_;
-    uint64_t slot_bytes_ = 0;
 };
 
 // Read-ahead of a loader's fetch blocks for stream_file staging (the

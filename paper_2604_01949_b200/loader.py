@@ -218,6 +218,11 @@ class BatchIterator:
                                  stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or None))
         if transform not in (None, "normalize_log1p"):
             raise L.InvalidArgument(f"unknown transform {transform!r}")
+        # stream=None: the loader assembles on its own stream, and every next() orders
+        # torch's current stream after the batch (rfl_batch_wait), so `model(b.data)` or
+        # `b.data.cpu()` never reads a buffer the kernel is still writing.  With an
+        # explicit stream, batches are ordered on that stream only.
+        self._own_stream = stream is None
         h = L.vp()
         L.check(L.lib().rfl_loader_create(self.dstore._h, C.byref(config._c()), epoch_index, C.byref(dc),
                                           C.byref(h)))
@@ -241,6 +246,9 @@ class BatchIterator:
         if rc == L.END:
             return None
         b = self._b
+        if self._own_stream:
+            import torch
+            L.check(L.lib().rfl_batch_wait(C.byref(b), C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
         n = b.n_rows
         gh = np.ctypeslib.as_array(b.h_gidx, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
         g = self._view(b.d_gidx, (n,), np.int64)

@@ -184,3 +184,25 @@ def test_synth_one_hot_store(tmp_path):
         assert b["dense"].tobytes() == x.reshape(200, 128)[b["gidx"].astype(np.int64)].tobytes()
     with pytest.raises(R.InvalidArgument):
         R.synth_store(tmp_path / "c", R.SynthConfig(**dict(cfgs, n_var=30)))
+
+
+@pytest.mark.parametrize("kind", ["counts", "one_hot"])
+def test_procedural_synth_matches_oracle_generator(tmp_path, kind):
+    """The product's procedural generators (cfg2 counts, cfg4 one-hot)
+    are byte-identical to the oracle's numpy restatement, which bench.py's
+    --impl reference leg and tests/golden/make_golden_shapes.py use."""
+    import paper_2604_01949_b200 as R
+    from oracle.oracle import synth_counts_np, synth_one_hot_np
+    if kind == "counts":
+        R.synth_store(tmp_path / "a", R.SynthConfig(1100, 36_000, "csr", "f32", seed=1, chunk_rows=256,
+                                                    chunks_per_shard=3, counts=True))
+        synth_counts_np(tmp_path / "b", 1100, 36_000, 1, 256, 3)
+    else:
+        R.synth_store(tmp_path / "a", R.SynthConfig(900, 4096, "dense", "u8", seed=3, chunk_rows=128,
+                                                    chunks_per_shard=4, one_hot=4))
+        synth_one_hot_np(tmp_path / "b", 900, 4096, 3, 128, 4)
+    fa = sorted(p.relative_to(tmp_path / "a") for p in (tmp_path / "a").rglob("*") if p.is_file())
+    fb = sorted(p.relative_to(tmp_path / "b") for p in (tmp_path / "b").rglob("*") if p.is_file())
+    assert fa == fb
+    for f in fa:
+        assert (tmp_path / "a" / f).read_bytes() == (tmp_path / "b" / f).read_bytes(), f
