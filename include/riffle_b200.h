@@ -294,7 +294,7 @@ typedef struct rfl_shuffle_config {
     uint32_t join_outer;           /* DatasetCollection JoinMode (collection.hpp:27): 1 outer (union), 0 inner (intersection) */
     uint32_t rank;                 /* multi-GPU: this rank writes shards s == rank (mod world) */
     uint32_t world;
-    uint32_t reserved;
+    uint32_t out_codec;            /* ShuffleOutputConfig::codec: 0 none, 1 deflate (zlib raw DEFLATE, codec.cpp:16-36) */
 } rfl_shuffle_config;
 
 typedef struct rfl_shuffle_stats {

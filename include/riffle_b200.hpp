@@ -70,6 +70,7 @@ inline void check(rfl_status st) {
 enum class Layout : std::uint32_t { dense = RFL_LAYOUT_DENSE, csr = RFL_LAYOUT_CSR };
 enum class ValueDtype : std::uint32_t { f32 = RFL_F32, f64 = RFL_F64, i32 = RFL_I32, u8 = RFL_U8 };
 enum class IndexDtype : std::uint32_t { u32 = RFL_IDX_U32, u64 = RFL_IDX_U64 };
+enum class Codec : std::uint32_t { none = 0, deflate = 1 };  // dtype.hpp:16 (zlib raw DEFLATE per record)
 
 [[nodiscard]] inline std::size_t value_size(ValueDtype d) noexcept {
     switch (d) {
@@ -94,6 +95,7 @@ struct StoreManifest {  // manifest.hpp:16-54 (the fields the hot path reads)
     std::optional<IndexDtype> index_dtype;
     std::uint64_t chunk_rows = 0;
     std::uint64_t chunks_per_shard = 0;
+    Codec codec = Codec::none;
     bool has_provenance = false;
 };
 
@@ -120,6 +122,7 @@ public:
         if (man_.layout == Layout::csr) man_.index_dtype = static_cast<IndexDtype>(i.index_dtype);
         man_.chunk_rows = i.chunk_rows;
         man_.chunks_per_shard = i.chunks_per_shard;
+        man_.codec = static_cast<Codec>(i.codec);
         man_.has_provenance = i.has_provenance != 0;
     }
     [[nodiscard]] const StoreManifest& manifest() const noexcept { return man_; }
@@ -410,9 +413,10 @@ struct ShufflePlan {  // preshuffle.hpp:19-34
     return p;
 }
 
-struct ShuffleOutputConfig {  // preshuffle.hpp:44-50 (codec none on the GPU path)
+struct ShuffleOutputConfig {  // preshuffle.hpp:44-50
     std::uint64_t chunk_rows = 1024;
     std::uint64_t chunks_per_shard = 128;
+    Codec codec = Codec::none;
     std::optional<IndexDtype> index_dtype;
 };
 
@@ -481,7 +485,7 @@ inline StoreManifest run_shuffle(const DatasetCollection& collection, const Shuf
                                  collection.join_mode() == JoinMode::outer ? 1u : 0u,
                                  0u,
                                  1u,
-                                 0u};
+                                 static_cast<std::uint32_t>(out_config.codec)};
     rfl_shuffle_stats st{};
     check(rfl_run_shuffle(argv.data(), argv.size(), out_path.c_str(), &cfg, &st));
     if (stats) {

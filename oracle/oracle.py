@@ -34,6 +34,7 @@ u64p = C.POINTER(C.c_uint64)
 LAYOUT = {"dense": 0, "csr": 1}
 VDT = {"f32": 0, "f64": 1, "i32": 2, "u8": 3}
 IDT = {"u32": 0, "u64": 1}
+CODEC = {"none": 0, "deflate": 1}
 NP_VDT = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "u8": np.uint8}
 NP_IDT = {"u32": np.uint32, "u64": np.uint64}
 
@@ -77,7 +78,7 @@ class Ref:
             L.ref_iter_to_dense.argtypes = [C.c_void_p, C.c_void_p]
             L.ref_iter_counters.argtypes = [C.c_void_p] + [u64p] * 5
             L.ref_synth.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int,
-                                    C.c_double, C.c_uint64, C.c_uint64, C.c_uint64]
+                                    C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]
             L.ref_rng_next.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_void_p]
             L.ref_rng_bounded.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]
             L.ref_rng_shuffle_iota.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
@@ -87,7 +88,8 @@ class Ref:
             L.ref_read_rows_dense.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
             L.ref_plan_shuffle.argtypes = [C.c_uint64] * 4 + [u64p, C.c_void_p, C.c_void_p]
             L.ref_run_shuffle.argtypes = [C.POINTER(C.c_char_p), C.c_uint64, C.c_int, C.c_uint64, C.c_uint64,
-                                          C.c_uint64, C.c_char_p, C.c_uint64, C.c_uint64, C.c_int, u64p, u64p]
+                                          C.c_uint64, C.c_char_p, C.c_uint64, C.c_uint64, C.c_int, C.c_int,
+                                          u64p, u64p]
             L.ref_throughput.restype = C.c_double
             L.ref_throughput.argtypes = [C.c_char_p] + [C.c_uint64] * 4 + [C.c_uint32, C.c_uint64, C.c_uint32,
                                                                           C.c_uint64, C.c_int, u64p,
@@ -128,9 +130,9 @@ class Ref:
     # -- stores
     @classmethod
     def synth(cls, path, n_obs, n_var, layout="csr", vdtype="f32", idtype="u32", density=0.1,
-              seed=0, chunk_rows=64, cps=128):
+              seed=0, chunk_rows=64, cps=128, codec="none"):
         cls.check(cls.lib().ref_synth(str(path).encode(), n_obs, n_var, LAYOUT[layout], VDT[vdtype],
-                                      IDT[idtype], density, seed, chunk_rows, cps))
+                                      IDT[idtype], density, seed, chunk_rows, cps, CODEC[codec]))
 
     @classmethod
     def read_rows_csr(cls, path, ranges):
@@ -222,12 +224,13 @@ class Ref:
         return out
 
     @classmethod
-    def run_shuffle(cls, in_paths, out_path, c, m, seed, out_chunk_rows, out_cps, outer=True, out_idt=None):
+    def run_shuffle(cls, in_paths, out_path, c, m, seed, out_chunk_rows, out_cps, outer=True, out_idt=None,
+                    codec="none"):
         arr = (C.c_char_p * len(in_paths))(*[str(p).encode() for p in in_paths])
         peak, rounds = C.c_uint64(), C.c_uint64()
         cls.check(cls.lib().ref_run_shuffle(arr, len(in_paths), int(outer), c, m, seed, str(out_path).encode(),
                                             out_chunk_rows, out_cps, -1 if out_idt is None else IDT[out_idt],
-                                            C.byref(peak), C.byref(rounds)))
+                                            CODEC[codec], C.byref(peak), C.byref(rounds)))
         return {"peak_resident_rows": peak.value, "rounds": rounds.value}
 
     @classmethod

@@ -102,7 +102,7 @@ int ref_plan_epoch(uint64_t n_obs, uint64_t f, uint64_t B, uint64_t b, uint64_t 
 
 // ---- synth_store ---------------------------------------------------------------
 int ref_synth(const char* path, uint64_t n_obs, uint64_t n_var, int layout, int vdtype,
-              int idtype, double density, uint64_t seed, uint64_t chunk_rows, uint64_t cps) {
+              int idtype, double density, uint64_t seed, uint64_t chunk_rows, uint64_t cps, int codec) {
     try {
         SynthConfig c;
         c.n_obs = n_obs;
@@ -114,6 +114,7 @@ int ref_synth(const char* path, uint64_t n_obs, uint64_t n_var, int layout, int 
         c.seed = seed;
         c.chunk_rows = chunk_rows;
         c.chunks_per_shard = cps;
+        c.codec = static_cast<Codec>(codec);
         synth_store(path, c);
         return 0;
     } catch (const std::exception& e) {
@@ -255,7 +256,7 @@ int ref_plan_shuffle(uint64_t total_rows, uint64_t c, uint64_t m, uint64_t seed,
 
 int ref_run_shuffle(const char* const* in_paths, uint64_t n_in, int outer_join, uint64_t c,
                     uint64_t m, uint64_t seed, const char* out_path, uint64_t out_chunk_rows,
-                    uint64_t out_cps, int out_idt, uint64_t* peak_resident, uint64_t* rounds) {
+                    uint64_t out_cps, int out_idt, int out_codec, uint64_t* peak_resident, uint64_t* rounds) {
     try {
         DatasetCollection coll(outer_join ? JoinMode::outer : JoinMode::inner);
         for (uint64_t i = 0; i < n_in; ++i) coll.add(std::make_shared<const StoreReader>(in_paths[i]));
@@ -264,6 +265,7 @@ int ref_run_shuffle(const char* const* in_paths, uint64_t n_in, int outer_join, 
         oc.chunk_rows = out_chunk_rows;
         oc.chunks_per_shard = out_cps;
         if (out_idt >= 0) oc.index_dtype = static_cast<IndexDtype>(out_idt);
+        oc.codec = static_cast<Codec>(out_codec);
         ShuffleRunStats st;
         run_shuffle(coll, plan, out_path, oc, &st);
         if (peak_resident) *peak_resident = st.peak_resident_rows;

@@ -43,7 +43,7 @@ class rfl_synth_config(C.Structure):
 class rfl_loader_config(C.Structure):
     _fields_ = [("fetch_block_rows", u64), ("buffer_capacity_rows", u64), ("batch_rows", u64),
                 ("seed", u64), ("prefetch_depth", u32), ("drop_last", u32), ("cache_bypass", u32),
-                ("rank", u32), ("world", u32), ("reserved", u32)]
+                ("rank", u32), ("world", u32), ("out_codec", u32)]
 
 
 class rfl_device_config(C.Structure):

@@ -506,6 +506,8 @@ rfl::ShuffleArgs shuffle_args(const char* const* in_paths, uint64_t n_inputs, co
     a.outer = cfg->join_outer != 0;
     a.rank = cfg->rank;
     a.world = cfg->world ? cfg->world : 1;
+    if (cfg->out_codec > 1) rfl::invalid("run_shuffle: unknown codec");
+    a.out_codec = cfg->out_codec;
     return a;
 }
 void fill_stats(const rfl::ShuffleResult& r, rfl_shuffle_stats* stats) {

@@ -9,6 +9,7 @@
 #include <string>
 #include <thread>
 
+#include "codec.hpp"
 #include "engine.hpp"
 
 namespace rfl {
@@ -96,23 +97,53 @@ bool check_csr_record(const Manifest& m, uint64_t q, const uint8_t* rec, uint64_
     return prev == nnz;
 }
 
+uint64_t csr_record_bytes(const Manifest& m, uint64_t rows, uint64_t nnz) {
+    const uint64_t is = index_size(*m.index_dtype), vs = value_size(m.value_dtype);
+    return kCsrHeaderBytes + (rows + 1) * is + nnz * (is + vs);
+}
+
+std::vector<uint8_t> decode_record_checked(const Manifest& m, uint64_t q, const uint8_t* enc, uint64_t n) {
+    std::vector<uint8_t> raw;
+    if (m.codec == Codec::none) {
+        raw.assign(enc, enc + n);
+    } else {
+        try {
+            if (m.layout == Layout::dense) {  // codec_decode to the known size (store.cpp:84-87)
+                raw.resize(m.rows_in_chunk(q) * m.n_var * value_size(m.value_dtype));
+                inflate_exact(enc, n, raw.data(), raw.size());
+            } else {  // codec_decode_any with the reference's size hint (store.cpp:92-93)
+                raw = inflate_any(enc, n, n * 3 + kCsrHeaderBytes);
+            }
+        } catch (const Error& e) {
+            if (e.code == kCorrupt) corrupt(chunk_where(m, q) + e.what());
+            throw;
+        }
+    }
+    if (m.layout == Layout::dense) check_dense_record(m, q, raw.size());
+    else full_check_csr_record(m, q, raw.data(), raw.size());
+    return raw;
+}
+
 // ================================================================= DStore ===
 DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     : hs_(std::move(hs)), device_(device), staging_(staging) {
     const Manifest& m = hs_->manifest();
-    if (m.codec != Codec::none) invalid("GPU path requires codec none (deflate decode is out of scope)");
     if (staging > kStreamFile) invalid("unknown staging mode");
     const uint64_t nch = m.chunk_count();
     rec_off_.resize(nch);
-    rec_len_.resize(nch);
+    slot_len_.resize(nch);
+    for (uint64_t q = 0; q < nch; ++q) slot_len_[q] = hs_->record_slot(q).len;
+    if (m.layout == Layout::csr) row_nnz_.resize(m.n_obs);
+    // the image holds DECODED records: deflate stores are inflated on the host
+    // (open / read-ahead threads), so every kernel reads plain records
+    if (m.codec == Codec::deflate) deflate_layout();
+    else rec_len_ = slot_len_;
     uint64_t off = 0;
     for (uint64_t q = 0; q < nch; ++q) {
-        rec_len_[q] = hs_->record_slot(q).len;
         rec_off_[q] = off;
         off = align_up(off + rec_len_[q], kAlign);
     }
     image_bytes_ = off;
-    if (m.layout == Layout::csr) row_nnz_.resize(m.n_obs);
     DeviceGuard g(device_);
     try {
         open_image();
@@ -129,8 +160,13 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
 void DStore::open_image() {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
-    if (staging_ == kResident) load_records(true);
-    else if (staging_ == kStreamPinned) load_records(false);
+    if (m.codec == Codec::deflate) {
+        if (staging_ != kStreamFile) load_records_deflate(staging_ == kResident);
+    } else if (staging_ == kResident) {
+        load_records(true);
+    } else if (staging_ == kStreamPinned) {
+        load_records(false);
+    }
     // CsrBlock::validate of every record, once, on the GPU (the reference
     // re-validates on each decode, store.cpp:116-120); the pinned image is read
     // in place over PCIe (mapped pinned memory)
@@ -150,7 +186,8 @@ void DStore::open_image() {
         const bool off = e && e[0] == '0', only16 = e && std::string(e) == "16";
         if (!off && (only16 || !delta_image())) narrow_image();
     }
-    if (m.layout == Layout::csr && staging_ == kStreamFile) {  // file streaming: only headers + indptrs now
+    if (m.layout == Layout::csr && staging_ == kStreamFile && m.codec == Codec::none) {
+        // file streaming: only headers + indptrs now (deflate: read by deflate_layout)
         std::vector<uint8_t> buf;
         for (uint64_t q = 0; q < nch; ++q) {
             const uint64_t want = std::min<uint64_t>(
@@ -250,6 +287,109 @@ void DStore::load_records(bool to_device) {
     }
 }
 
+namespace {
+template <class F>
+void parallel_chunks(uint64_t n, F&& fn) {  // fn(q) over [0, n) on up to 16 threads, first error rethrown
+    const unsigned T = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>({16u, std::max(1u, std::thread::hardware_concurrency()), n})));
+    std::vector<std::exception_ptr> errs(T);
+    std::atomic<uint64_t> next{0};
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            try {
+                for (uint64_t q; (q = next.fetch_add(1)) < n;) fn(q);
+            } catch (...) {
+                errs[t] = std::current_exception();
+                next = n;
+            }
+        });
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
+}
+}  // namespace
+
+// Codec::deflate: decoded record lengths (dense: rows x row bytes; CSR: from
+// the header, by inflating only the record's head) and, for CSR, per-row nnz
+// from the inflated indptr -- the same header / indptr checks as
+// check_csr_record; a record failing them is decoded the reference's way for
+// the exact error.
+void deflate_record_lengths(const HostStore& hs, std::vector<uint64_t>& rec_len, uint32_t* row_nnz) {
+    const Manifest& m = hs.manifest();
+    const uint64_t nch = m.chunk_count();
+    rec_len.assign(nch, 0);
+    if (m.layout == Layout::dense) {
+        for (uint64_t q = 0; q < nch; ++q) rec_len[q] = m.rows_in_chunk(q) * m.n_var * value_size(m.value_dtype);
+        return;
+    }
+    const uint64_t is = index_size(*m.index_dtype);
+    parallel_chunks(nch, [&](uint64_t q) {
+        const Slot sl = hs.record_slot(q);
+        const uint64_t rows = m.rows_in_chunk(q);
+        const uint64_t want = kCsrHeaderBytes + (rows + 1) * is;
+        std::vector<uint8_t> enc, head(want);
+        uint64_t got = 0;
+        for (uint64_t take = std::min<uint64_t>(sl.len, 16384);; take = sl.len) {  // head first, whole record if short
+            enc.resize(take);
+            hs.read_shard_bytes(q / m.chunks_per_shard, sl.off, enc.data(), take, false);
+            got = inflate_prefix(enc.data(), take, head.data(), want);
+            if (got == want || take == sl.len) break;
+        }
+        bool ok = got == want && rd32(head.data()) == rows;
+        if (ok) {
+            const uint64_t nnz = rd64(head.data() + 4);
+            rec_len[q] = csr_record_bytes(m, rows, nnz);
+            // check_csr_record's indptr pass on the inflated head (the length is right by construction)
+            uint64_t prev = is == 4 ? rd32(head.data() + kCsrHeaderBytes) : rd64(head.data() + kCsrHeaderBytes);
+            ok = prev == 0;
+            for (uint64_t r = 1; ok && r <= rows; ++r) {
+                const uint8_t* p = head.data() + kCsrHeaderBytes + r * is;
+                const uint64_t v = is == 4 ? rd32(p) : rd64(p);
+                ok = v >= prev;
+                if (row_nnz) row_nnz[q * m.chunk_rows + r - 1] = static_cast<uint32_t>(v - prev);
+                prev = v;
+            }
+            ok = ok && prev == nnz;
+        }
+        if (!ok) {  // the reference's decode for its message (throws); anything it accepts is still corrupt here
+            if (enc.size() != sl.len) {
+                enc.resize(sl.len);
+                hs.read_shard_bytes(q / m.chunks_per_shard, sl.off, enc.data(), sl.len, false);
+            }
+            decode_record_checked(m, q, enc.data(), enc.size());
+            corrupt(chunk_where(m, q) + "csr record invalid");
+        }
+    });
+}
+
+void DStore::deflate_layout() { deflate_record_lengths(*hs_, rec_len_, row_nnz_.empty() ? nullptr : row_nnz_.data()); }
+
+// Codec::deflate, resident / stream_pinned: every record inflated (in parallel)
+// straight into a pinned image at its aligned offset; resident then uploads the
+// image to HBM and drops it.
+void DStore::load_records_deflate(bool to_device) {
+    const Manifest& m = hs_->manifest();
+    const uint64_t nch = m.chunk_count();
+    cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&h_image_), image_bytes_ + kPad, cudaHostAllocPortable),
+            "cudaHostAlloc image");
+    std::memset(h_image_ + image_bytes_, 0, kPad);
+    parallel_chunks(nch, [&](uint64_t q) {
+        const Slot sl = hs_->record_slot(q);
+        std::vector<uint8_t> enc(sl.len);
+        hs_->read_shard_bytes(q / m.chunks_per_shard, sl.off, enc.data(), sl.len, false);
+        if (!inflate_fits(enc.data(), enc.size(), h_image_ + rec_off_[q], rec_len_[q])) {
+            decode_record_checked(m, q, enc.data(), enc.size());  // throws the reference's error
+            corrupt(chunk_where(m, q) + "csr record invalid");
+        }
+    });
+    if (!to_device) return;
+    cuda_ok(cudaMalloc(&d_arena_, image_bytes_ + kPad), "cudaMalloc arena");
+    cuda_ok(cudaMemcpy(d_arena_, h_image_, image_bytes_ + kPad, cudaMemcpyHostToDevice), "upload");
+    cudaFreeHost(h_image_);
+    h_image_ = nullptr;
+}
+
 void DStore::validate_records(const uint8_t* base) {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
@@ -271,9 +411,9 @@ void DStore::validate_records(const uint8_t* base) {
     if (bad == ~0ull) return;
     // reproduce the reference's message (first error of the record, in validate's order)
     const uint64_t q = bad / m.chunk_rows;
-    std::vector<uint8_t> rec(rec_len_[q]);
+    std::vector<uint8_t> rec(slot_len_[q]);
     hs_->read_record(q, rec.data(), rec.size());
-    full_check_csr_record(m, q, rec.data(), rec.size());
+    decode_record_checked(m, q, rec.data(), rec.size());
     corrupt(chunk_where(m, q) + "csr record invalid");
 }
 
@@ -486,6 +626,12 @@ void BlockReader::worker() {
     const Manifest& m = ds_->manifest();
     const HostStore& hs = ds_->host();
     const uint64_t S = slots_.size();
+    uint8_t* scratch = nullptr;  // deflate stores: the encoded run (4 KiB aligned for O_DIRECT)
+    uint64_t scratch_cap = 0;
+    struct Free {
+        uint8_t*& p;
+        ~Free() { std::free(p); }
+    } free_scratch{scratch};
     for (;;) {
         uint64_t k = 0;
         {
@@ -515,6 +661,35 @@ void BlockReader::worker() {
                     if (sl.off != first.off + run) break;
                     run += sl.len;
                     ++end;
+                }
+                if (ds_->deflate()) {  // inflate the run's records into the pinned buffer (codec.cpp:38-107)
+                    const uint64_t span = HostStore::aligned_span(first.off, run);
+                    if (scratch_cap < span) {
+                        std::free(scratch);
+                        scratch = nullptr;
+                        if (posix_memalign(reinterpret_cast<void**>(&scratch), 4096, span) != 0) {
+                            scratch = nullptr;
+                            scratch_cap = 0;
+                            throw Error(kIo, "out of host memory");
+                        }
+                        scratch_cap = span;
+                    }
+                    const uint64_t lead = hs.read_shard_span(shard, first.off, scratch, run, direct_);
+                    for (uint64_t x = q, rel = 0; x < end; ++x) {
+                        uint8_t* dst = b.buf + cursor;
+                        const uint8_t* enc = scratch + lead + rel;
+                        if (!inflate_fits(enc, ds_->slot_len()[x], dst, ds_->rec_len()[x])) {
+                            decode_record_checked(m, x, enc, ds_->slot_len()[x]);
+                            corrupt("chunk " + std::to_string(x) + " in shard " + std::to_string(shard) +
+                                    ": csr record invalid");
+                        }
+                        b.pos[x - q0] = cursor;
+                        if (validate_ && !columns_ok(m, x, dst)) full_check_csr_record(m, x, dst, ds_->rec_len()[x]);
+                        cursor = align_up(cursor + ds_->rec_len()[x], 16);
+                        rel += ds_->slot_len()[x];
+                    }
+                    q = end;
+                    continue;
                 }
                 const uint64_t lead = hs.read_shard_span(shard, first.off, b.buf + cursor, run, direct_);
                 for (uint64_t x = q, rel = 0; x < end; ++x) {
@@ -673,7 +848,7 @@ void GpuLoader::stage_block(uint64_t id) {
         ctr_.h2d_bytes += img1 - img0;
         for (uint64_t q = q0; q <= q1; ++q)  // one read op per shard run, as store.cpp:427-447 counts
             if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard) ctr_.read_ops += 1;
-        for (uint64_t q = q0; q <= q1; ++q) ctr_.bytes_read += ds_->rec_len()[q];
+        for (uint64_t q = q0; q <= q1; ++q) ctr_.bytes_read += ds_->slot_len()[q];
     } else {
         // read ahead by the BlockReader; one copy per record into its aligned slot offset
         // (copied and released right away: one next() may consume more blocks than there are buffers)
@@ -684,9 +859,9 @@ void GpuLoader::stage_block(uint64_t id) {
                                     cudaMemcpyHostToDevice, copy_),
                     "stage H2D");
             if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard ||
-                hs.record_slot(q).off != hs.record_slot(q - 1).off + ds_->rec_len()[q - 1])
+                hs.record_slot(q).off != hs.record_slot(q - 1).off + ds_->slot_len()[q - 1])
                 ctr_.read_ops += 1;  // one per coalesced run (store.cpp:427-447)
-            ctr_.bytes_read += ds_->rec_len()[q];
+            ctr_.bytes_read += ds_->slot_len()[q];
             ctr_.h2d_bytes += ds_->rec_len()[q];
         }
         reader_->release(seq, copy_);

@@ -46,6 +46,17 @@ void full_check_csr_record(const Manifest& m, uint64_t chunk, const uint8_t* rec
 void check_dense_record(const Manifest& m, uint64_t chunk, uint64_t len);
 // Cheap pass (header, length, indptr; optionally per-row nnz); false -> run the full check.
 bool check_csr_record(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint64_t len, uint32_t* row_nnz);
+// decode_record (store.cpp:81-122) of a stored record: decoded bytes (inflated for
+// Codec::deflate), checked as the reference checks them; CorruptStore errors are
+// wrapped "chunk q in shard s: ..." as process_shard does (store.cpp:455-457).
+std::vector<uint8_t> decode_record_checked(const Manifest& m, uint64_t chunk, const uint8_t* enc, uint64_t n);
+// Decoded CSR record bytes from the record's header: 12 + (rows+1)*is + nnz*(is+vs).
+uint64_t csr_record_bytes(const Manifest& m, uint64_t rows, uint64_t nnz);
+// Codec::deflate store: every record's decoded length (dense: rows x row bytes;
+// CSR: from the inflated header) and, for CSR with row_nnz, per-row nnz from the
+// inflated indptr; header / indptr checks as check_csr_record, errors as the
+// reference reports them.  Parallel over records.
+void deflate_record_lengths(const HostStore& hs, std::vector<uint64_t>& rec_len, uint32_t* row_nnz);
 
 // One output slot of an iterator: batch buffers on the device + pinned row
 // references.  Kept by the DStore between iterators (open_epoch per epoch must
@@ -76,7 +87,9 @@ public:
     const uint8_t* d_arena() const { return d_arena_; }
     const uint8_t* h_image() const { return h_image_; }
     const std::vector<uint64_t>& rec_off() const { return rec_off_; }
-    const std::vector<uint64_t>& rec_len() const { return rec_len_; }
+    const std::vector<uint64_t>& rec_len() const { return rec_len_; }    // decoded record bytes
+    const std::vector<uint64_t>& slot_len() const { return slot_len_; }  // stored (encoded) bytes
+    bool deflate() const { return manifest().codec == Codec::deflate; }
     // layout of the staged image (stream_pinned: possibly narrowed, see idx16()); == rec_* otherwise
     const std::vector<uint64_t>& img_off() const { return img_off_; }
     const std::vector<uint64_t>& img_len() const { return img_len_; }
@@ -114,6 +127,8 @@ public:
 private:
     void open_image();
     void load_records(bool to_device);
+    void deflate_layout();
+    void load_records_deflate(bool to_device);
     void validate_records(const uint8_t* base);
     void narrow_image();
     bool delta_image();
@@ -121,7 +136,7 @@ private:
     std::shared_ptr<HostStore> hs_;
     int device_;
     uint32_t staging_;
-    std::vector<uint64_t> rec_off_, rec_len_, img_off_, img_len_;
+    std::vector<uint64_t> rec_off_, rec_len_, slot_len_, img_off_, img_len_;
     bool idx16_ = false, d8_ = false;
     std::vector<uint64_t> exp_len_;
     std::vector<uint8_t> d8_rec_;

@@ -1,5 +1,6 @@
 // riffle store format, host side (see format.hpp for the reference map).
 #include "format.hpp"
+#include "codec.hpp"
 
 #include <fcntl.h>
 #include <sys/stat.h>
@@ -656,11 +657,25 @@ void RecordWriter::write_part(const Placement& p, uint64_t rel, const void* src,
 }
 
 void RecordWriter::append_record(const void* rec, uint64_t nbytes, uint64_t rows) {
+    if (man_.codec != Codec::none) {  // emit_chunk: codec_encode, then the shard append (store.cpp:200-203)
+        const std::vector<uint8_t> enc = deflate_encode(static_cast<const uint8_t*>(rec), nbytes);
+        write_part(reserve_record(enc.size(), rows), 0, enc.data(), enc.size());
+        return;
+    }
     write_part(reserve_record(nbytes, rows), 0, rec, nbytes);
 }
 
 void RecordWriter::append_record_at(uint64_t chunk, const void* rec, uint64_t nbytes, uint64_t rows) {
+    if (man_.codec != Codec::none) {
+        const std::vector<uint8_t> enc = deflate_encode(static_cast<const uint8_t*>(rec), nbytes);
+        write_part(reserve_record(enc.size(), rows, static_cast<int64_t>(chunk)), 0, enc.data(), enc.size());
+        return;
+    }
     write_part(reserve_record(nbytes, rows, static_cast<int64_t>(chunk)), 0, rec, nbytes);
+}
+
+void RecordWriter::append_encoded(const void* enc, uint64_t nbytes, uint64_t rows, int64_t chunk) {
+    write_part(reserve_record(nbytes, rows, chunk), 0, enc, nbytes);
 }
 
 Manifest RecordWriter::finish(int64_t n_obs_override) {

@@ -152,7 +152,11 @@ class RecordWriter {
 public:
     RecordWriter(std::string root, Manifest man, bool defer_manifest, const char* shard_dir = "shards",
                  bool write_manifest_file = true);
+    // append_record / append_record_at take DECODED records and apply the
+    // manifest's codec (codec_encode, store.cpp:200); append_encoded takes
+    // records already encoded with it.
     void append_record(const void* rec, uint64_t nbytes, uint64_t rows);
+    void append_encoded(const void* enc, uint64_t nbytes, uint64_t rows, int64_t chunk = -1);
     // Sparse writing for multi-rank writers that own a subset of the shards:
     // chunk ids must increase and fill each owned shard from slot 0.
     void append_record_at(uint64_t chunk, const void* rec, uint64_t nbytes, uint64_t rows);
@@ -168,6 +172,7 @@ public:
     // finish(): flush shard footer, write manifest (n_obs = rows appended, or
     // n_obs_override when several ranks wrote the store)
     Manifest finish(int64_t n_obs_override = -1);
+    Codec codec() const { return man_.codec; }
     uint64_t rows() const { return man_.n_obs; }
 
 private:

@@ -12,6 +12,7 @@
 //
 // Output bytes are identical to the reference's (tests/test_gpu_preshuffle.py).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -23,6 +24,7 @@
 #include <unordered_map>
 #include <unordered_set>
 
+#include "codec.hpp"
 #include "engine.hpp"
 #include "format.hpp"
 #include "kernels.cuh"
@@ -79,6 +81,8 @@ struct Member {
     bool identity = true;
     bool remap = false;               // rows go through the reprojection kernels
     std::shared_ptr<DevBuf> d_map;    // CSR: u32 col_map; dense: u32 inverse map (unified -> member col)
+    std::vector<uint64_t> dec_len;    // Codec::deflate: decoded length of every record (empty: codec none)
+    uint64_t rec_bytes(uint64_t q) const { return dec_len.empty() ? hs->record_slot(q).len : dec_len[q]; }
 };
 
 constexpr uint64_t kMissing = ~0ull;  // kMissingColumn (collection.hpp:23)
@@ -247,7 +251,7 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
     std::vector<uint64_t> off(need.size()), len(need.size());
     uint64_t total = 0;
     for (size_t i = 0; i < need.size(); ++i) {
-        len[i] = ms_[need[i].first].hs->record_slot(need[i].second).len;
+        len[i] = ms_[need[i].first].rec_bytes(need[i].second);
         off[i] = total;
         total = align_up(total + len[i], kAlign);
     }
@@ -298,6 +302,25 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
                         const HostStore& hs = *ms_[need[ru.i].first].hs;
                         const Manifest& hm = hs.manifest();
                         uint8_t* base = stage.p + (off[ru.i] - w0);
+                        if (!ms_[need[ru.i].first].dec_len.empty()) {
+                            // deflate member: inflate each record of the run to its aligned offset
+                            // (decode_record, store.cpp:81-122), then the same checks
+                            std::vector<uint8_t> enc(ru.bytes);
+                            hs.read_shard_bytes(ru.shard, ru.file_off, enc.data(), ru.bytes, false);
+                            for (size_t k = ru.i, rel = 0; k < ru.j; ++k) {
+                                const uint64_t slen = hs.record_slot(need[k].second).len;
+                                uint8_t* dst = base + (off[k] - off[ru.i]);
+                                if (!inflate_fits(enc.data() + rel, slen, dst, len[k])) {
+                                    decode_record_checked(hm, need[k].second, enc.data() + rel, slen);
+                                    corrupt("chunk " + std::to_string(need[k].second) + " in shard " +
+                                            std::to_string(ru.shard) + ": csr record invalid");
+                                }
+                                if (hm.layout == Layout::csr && !check_csr_record(hm, need[k].second, dst, len[k], nullptr))
+                                    full_check_csr_record(hm, need[k].second, dst, len[k]);
+                                rel += slen;
+                            }
+                            continue;
+                        }
                         hs.read_shard_bytes(ru.shard, ru.file_off, base, ru.bytes, false);
                         // decode_record's checks (store.cpp:81-122) on each record of the run
                         for (size_t k = ru.i, rel = 0; k < ru.j; rel += len[k], ++k) {
@@ -353,7 +376,7 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
                 const uint64_t q = bad / mm.chunk_rows;
                 std::vector<uint8_t> rec(ms_[need[i].first].hs->record_slot(q).len);
                 ms_[need[i].first].hs->read_record(q, rec.data(), rec.size());
-                full_check_csr_record(mm, q, rec.data(), rec.size());
+                decode_record_checked(mm, q, rec.data(), rec.size());
                 corrupt("chunk " + std::to_string(q) + " in shard " + std::to_string(q / mm.chunks_per_shard) +
                         ": csr record invalid");
             }
@@ -530,6 +553,48 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
                         cuda_ok(cudaMemcpyAsync(ring_[i & 1].p, src + off, len, cudaMemcpyDeviceToHost, wst_), "D2H");
                         cuda_ok(cudaEventRecord(ring_ev_[i & 1], wst_), "event");
                     };
+                    if (out_->codec() == Codec::deflate) {
+                        // whole records to the host, deflated in parallel (codec_encode,
+                        // store.cpp:200 / preshuffle.cpp:70), appended in order
+                        std::vector<uint8_t> host(total);
+                        if (pieces) issue(0);
+                        for (uint64_t i = 0; i < pieces; ++i) {
+                            if (i + 1 < pieces) issue(i + 1);
+                            cuda_ok(cudaEventSynchronize(ring_ev_[i & 1]), "D2H done");
+                            std::memcpy(host.data() + i * S, ring_[i & 1].p, std::min(S, total - i * S));
+                        }
+                        const size_t nq = rec_len.size();
+                        std::vector<uint64_t> rs(nq + 1, 0), ps(nq + 1, 0);
+                        for (size_t q = 0; q < nq; ++q) {
+                            rs[q + 1] = rs[q] + rec_len[q];
+                            ps[q + 1] = ps[q] + rec_rows[q] * 12;
+                        }
+                        std::vector<std::vector<uint8_t>> enc(nq), penc(nq);
+                        std::atomic<size_t> next{0};
+                        std::vector<std::exception_ptr> errs(16);
+                        std::vector<std::thread> pool;
+                        const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+                        for (unsigned t = 0; t < T; ++t)
+                            pool.emplace_back([&, t] {
+                                try {
+                                    for (size_t q; (q = next.fetch_add(1)) < nq;) {
+                                        enc[q] = deflate_encode(host.data() + rs[q], rec_len[q]);
+                                        penc[q] = deflate_encode(prov_bytes.data() + ps[q], rec_rows[q] * 12);
+                                    }
+                                } catch (...) {
+                                    errs[t] = std::current_exception();
+                                }
+                            });
+                        for (auto& th : pool) th.join();
+                        for (auto& e : errs)
+                            if (e) std::rethrow_exception(e);
+                        for (size_t q = 0; q < nq; ++q) {
+                            const int64_t cid = chunk_id.empty() ? -1 : static_cast<int64_t>(chunk_id[q]);
+                            out_->append_encoded(enc[q].data(), enc[q].size(), rec_rows[q], cid);
+                            prov_->append_encoded(penc[q].data(), penc[q].size(), rec_rows[q], cid);
+                        }
+                        return;
+                    }
                     if (pieces) issue(0);
                     size_t q = 0;
                     uint64_t rstart = 0, ppos = 0;
@@ -644,7 +709,7 @@ void GpuShuffler::init() {
                 invalid(std::string("collection: store value_dtype ") + to_string(man.value_dtype) +
                         " does not match collection value_dtype " + to_string(f.value_dtype));
         }
-        if (man.codec != Codec::none) invalid("GPU path requires codec none (deflate decode is out of scope)");
+        if (man.codec == Codec::deflate) deflate_record_lengths(*m.hs, m.dec_len, nullptr);
         total_ += man.n_obs;
         ms_.push_back(std::move(m));
     }
@@ -688,7 +753,7 @@ void GpuShuffler::init() {
     if (layout_ == Layout::csr) om.index_dtype = out_idt_;
     om.chunk_rows = a_.out_chunk_rows;
     om.chunks_per_shard = a_.out_cps;
-    om.codec = Codec::none;
+    om.codec = a_.out_codec ? Codec::deflate : Codec::none;
     om.has_provenance = true;
     n_var_ = om.n_var;
     row_bytes_ = n_var_ * value_size(vdt_);
@@ -698,6 +763,7 @@ void GpuShuffler::init() {
     pm.layout = Layout::dense;
     pm.chunk_rows = a_.out_chunk_rows;
     pm.chunks_per_shard = a_.out_cps;
+    pm.codec = om.codec;  // ProvenanceWriter encodes with the store's codec (preshuffle.cpp:70,219)
     prov_ = std::make_unique<RecordWriter>(a_.out_path + "/provenance", pm, true, "shards", false);
     round_first_out_.assign(plan_.rounds.size() + 1, 0);
     for (size_t r = 0; r < plan_.rounds.size(); ++r) {

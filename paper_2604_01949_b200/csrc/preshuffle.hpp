@@ -16,6 +16,7 @@ struct ShuffleArgs {
     int32_t device = 0;
     bool outer = true;
     uint32_t rank = 0, world = 1;
+    uint32_t out_codec = 0;  // Codec of the output store and its provenance sidecar
 };
 
 struct ShuffleResult {

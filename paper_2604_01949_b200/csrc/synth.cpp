@@ -145,7 +145,7 @@ Manifest synth_one_hot(const std::string& path, const SynthCfg& c) {
     man.value_dtype = VDtype::u8;
     man.chunk_rows = c.chunk_rows;
     man.chunks_per_shard = c.chunks_per_shard;
-    man.codec = Codec::none;
+    man.codec = c.codec;
     man.var_names.reserve(c.n_var);
     for (uint64_t i = 0; i < c.n_var; ++i) man.var_names.push_back("v" + std::to_string(i));
     RecordWriter w(path, man, /*defer_manifest=*/false);
@@ -181,7 +181,7 @@ Manifest synth_counts(const std::string& path, const SynthCfg& c) {
     man.index_dtype = c.index_dtype;
     man.chunk_rows = c.chunk_rows;
     man.chunks_per_shard = c.chunks_per_shard;
-    man.codec = Codec::none;
+    man.codec = c.codec;
     man.var_names.reserve(c.n_var);
     for (uint64_t i = 0; i < c.n_var; ++i) man.var_names.push_back("v" + std::to_string(i));
     RecordWriter w(path, man, /*defer_manifest=*/false);
@@ -228,7 +228,6 @@ Manifest synth_store(const std::string& path, const SynthCfg& c) {
     if (c.counts) return synth_counts(path, c);
     if (c.layout == Layout::csr && (c.density <= 0.0 || c.density > 1.0))
         invalid("synth: density must lie in (0, 1] for csr stores");
-    if (c.codec != Codec::none) invalid("synth: only codec none is supported by the GPU build");
     Manifest man;
     man.layout = c.layout;
     man.n_var = c.n_var;

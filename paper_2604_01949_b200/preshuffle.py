@@ -113,8 +113,8 @@ def run_shuffle(inputs, plan: ShufflePlan, out_path, out_config: ShuffleOutputCo
     torch.distributed group for the control plane; row payloads move between
     GPUs through peer memory, written by the pack kernel (see _run_ranks)."""
     oc = out_config or ShuffleOutputConfig()
-    if oc.codec != "none":
-        raise L.InvalidArgument("GPU pre-shuffle writes codec none only")
+    if oc.codec not in ("none", "deflate"):
+        raise L.InvalidArgument(f"unknown codec {oc.codec!r}")
     if inputs:
         from .store import StoreReader
         held = sum(StoreReader(p).manifest().n_obs for p in inputs)
@@ -124,7 +124,7 @@ def run_shuffle(inputs, plan: ShufflePlan, out_path, out_config: ShuffleOutputCo
     arr = (C.c_char_p * len(paths))(*paths)
     cfg = L.rfl_shuffle_config(plan.block_rows, plan.buffer_rows, plan.seed, oc.chunk_rows, oc.chunks_per_shard,
                                -1 if oc.index_dtype is None else {"u32": 0, "u64": 1}[oc.index_dtype], device,
-                               int(join == "outer"), rank, world, 0)
+                               int(join == "outer"), rank, world, int(oc.codec == "deflate"))
     if world > 1:
         return _run_ranks(arr, len(paths), str(out_path), cfg, device, rank, world, group)
     st = L.rfl_shuffle_stats()

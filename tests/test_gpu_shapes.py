@@ -208,8 +208,8 @@ def test_one_hot_staging_widths(tmp_path, n_var):
         seen += b.n_rows
     assert seen == 700
     c = it.counters()
-    if n_var % 64 == 0:
-        assert c.h2d_bytes < c.bytes_read / 8
+    if n_var % 64 == 0:  # 2-bit codes (1/16 of the row bytes) + the 16-B row references
+        assert c.h2d_bytes <= c.bytes_read / 8
     else:
         assert c.h2d_bytes >= c.bytes_read
 

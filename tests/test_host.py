@@ -48,14 +48,22 @@ def test_no_gpu_here_fails_loudly(tmp_path):
     dict(n_obs=1, n_var=1, layout="csr", value_dtype="u8", index_dtype="u32", density=1.0, seed=0, chunk_rows=1,
          cps=1),
     dict(n_obs=300, n_var=5, layout="dense", value_dtype="i32", density=0.1, seed=8, chunk_rows=7, cps=3),
+    # Codec::deflate stores (codec.cpp:16-36, one raw DEFLATE stream per record)
+    dict(n_obs=3000, n_var=300, layout="csr", value_dtype="f32", index_dtype="u32", density=0.1, seed=5,
+         chunk_rows=64, cps=8, codec="deflate"),
+    dict(n_obs=2000, n_var=96, layout="dense", value_dtype="u8", density=0.1, seed=6, chunk_rows=50, cps=3,
+         codec="deflate"),
+    dict(n_obs=1500, n_var=200, layout="csr", value_dtype="f64", index_dtype="u64", density=0.2, seed=4,
+         chunk_rows=128, cps=4, codec="deflate"),
 ])
 def test_synth_byte_identical(tmp_path, case):
     c = case
     Ref.synth(tmp_path / "ref", c["n_obs"], c["n_var"], c["layout"], c["value_dtype"], c.get("index_dtype", "u32"),
-              c["density"], c["seed"], c["chunk_rows"], c["cps"])
+              c["density"], c["seed"], c["chunk_rows"], c["cps"], codec=c.get("codec", "none"))
     R.synth_store(tmp_path / "gpu", R.SynthConfig(c["n_obs"], c["n_var"], c["layout"], c["value_dtype"],
                                                   c.get("index_dtype", "u32"), c["density"], c["seed"],
-                                                  c["chunk_rows"], c["cps"], threads=3))
+                                                  c["chunk_rows"], c["cps"], codec=c.get("codec", "none"),
+                                                  threads=3))
     a = sorted(os.listdir(tmp_path / "ref" / "shards"))
     assert a == sorted(os.listdir(tmp_path / "gpu" / "shards"))
     for f in a:
