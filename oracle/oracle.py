@@ -70,7 +70,7 @@ class Ref:
             L = C.CDLL(str(REF_SO))
             L.ref_last_error.restype = C.c_char_p
             L.ref_iter_open.restype = C.c_void_p
-            L.ref_iter_open.argtypes = [C.c_char_p] + [C.c_uint64] * 4 + [C.c_uint32, C.c_int, C.c_uint64]
+            L.ref_iter_open.argtypes = [C.c_char_p] + [C.c_uint64] * 4 + [C.c_uint32, C.c_int, C.c_uint64, C.c_int]
             L.ref_iter_next.argtypes = [C.c_void_p, u64p, u64p]
             for n in ("ref_iter_gidx", "ref_iter_dense", "ref_iter_close"):
                 getattr(L, n).argtypes = [C.c_void_p] + ([C.c_void_p] if n != "ref_iter_close" else [])
@@ -162,13 +162,13 @@ class Ref:
 
     # -- loader
     @classmethod
-    def iterate(cls, path, f, B, b, seed=0, epoch=0, depth=0, drop_last=False, want="gidx"):
+    def iterate(cls, path, f, B, b, seed=0, epoch=0, depth=0, drop_last=False, want="gidx", cache_bypass=False):
         """Yields per batch: dict(gidx=..., [indptr, indices, data] | [dense] | [to_dense]).
 
         want: "gidx" | "csr" | "dense" | "to_dense" (comma separated allowed)."""
         L = cls.lib()
         man = read_manifest(path)
-        h = L.ref_iter_open(str(path).encode(), f, B, b, seed, depth, int(drop_last), epoch)
+        h = L.ref_iter_open(str(path).encode(), f, B, b, seed, depth, int(drop_last), epoch, int(cache_bypass))
         if not h:
             raise RuntimeError(cls.err())
         wants = set(want.split(","))

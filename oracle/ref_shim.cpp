@@ -124,11 +124,13 @@ int ref_synth(const char* path, uint64_t n_obs, uint64_t n_var, int layout, int 
 
 // ---- BatchIterator -----------------------------------------------------------
 void* ref_iter_open(const char* path, uint64_t f, uint64_t B, uint64_t b, uint64_t seed,
-                    uint32_t depth, int drop_last, uint64_t epoch) {
+                    uint32_t depth, int drop_last, uint64_t epoch, int cache_bypass) {
     try {
         auto* h = new Iter;
         h->store = std::make_shared<const StoreReader>(path);
-        h->it.emplace(open_epoch(h->store, make_cfg(f, B, b, seed, depth, drop_last), epoch));
+        LoaderConfig cfg = make_cfg(f, B, b, seed, depth, drop_last);
+        cfg.cache_bypass = cache_bypass != 0;
+        h->it.emplace(open_epoch(h->store, cfg, epoch));
         return h;
     } catch (const std::exception& e) {
         fail(e);

@@ -507,6 +507,15 @@ void OutBuffers::free_all() {
     *this = OutBuffers{};
 }
 
+uint64_t DStore::charge_footer(uint64_t shard) {
+    const Manifest& m = manifest();
+    std::lock_guard<std::mutex> lk(mu_);
+    if (footer_charged_.empty()) footer_charged_.assign(m.shard_count(), 0);
+    if (footer_charged_[shard]) return 0;
+    footer_charged_[shard] = 1;
+    return m.chunks_per_shard * 16 + 8;  // ShardFooter::footer_bytes + magic
+}
+
 uint8_t* DStore::take_pinned(uint64_t bytes) {
     {
         std::lock_guard<std::mutex> lk(mu_);
@@ -846,9 +855,6 @@ void GpuLoader::stage_block(uint64_t id) {
             for (uint64_t q = q0; q <= q1; ++q) lv.chunk_off[q - q0] = ds_->img_off()[q] - img0;
         }
         ctr_.h2d_bytes += img1 - img0;
-        for (uint64_t q = q0; q <= q1; ++q)  // one read op per shard run, as store.cpp:427-447 counts
-            if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard) ctr_.read_ops += 1;
-        for (uint64_t q = q0; q <= q1; ++q) ctr_.bytes_read += ds_->slot_len()[q];
     } else {
         // read ahead by the BlockReader; one copy per record into its aligned slot offset
         // (copied and released right away: one next() may consume more blocks than there are buffers)
@@ -858,15 +864,42 @@ void GpuLoader::stage_block(uint64_t id) {
             cuda_ok(cudaMemcpyAsync(lv.slot.ptr + lv.chunk_off[q - q0], bk.buf + bk.pos[q - q0], ds_->rec_len()[q],
                                     cudaMemcpyHostToDevice, copy_),
                     "stage H2D");
-            if (q == q0 || q / m.chunks_per_shard != (q - 1) / m.chunks_per_shard ||
-                hs.record_slot(q).off != hs.record_slot(q - 1).off + ds_->slot_len()[q - 1])
-                ctr_.read_ops += 1;  // one per coalesced run (store.cpp:427-447)
-            ctr_.bytes_read += ds_->slot_len()[q];
             ctr_.h2d_bytes += ds_->rec_len()[q];
         }
         reader_->release(seq, copy_);
     }
-    ctr_.chunks_decoded += q1 - q0 + 1;
+    count_fetch(id);
+}
+
+// IoStats of BlockPrefetcher's read_rows({block}) (store.cpp:371-470): per shard
+// the footer on first use, one read op per run of adjacent records, bytes_read =
+// the run length (cache_bypass: the 4 KiB-aligned superset actually read,
+// store.cpp:374-392), one decode per chunk.  Whatever the staging mode, the
+// counters equal the reference's for the same fetch order.
+void GpuLoader::count_fetch(uint64_t id) {
+    const Manifest& m = ds_->manifest();
+    const HostStore& hs = ds_->host();
+    const uint64_t s = id * cfg_.f, e = std::min(m.n_obs, s + cfg_.f);
+    const uint64_t q0 = s / m.chunk_rows, q1 = (e - 1) / m.chunk_rows;
+    uint64_t q = q0;
+    while (q <= q1) {
+        const uint64_t shard = q / m.chunks_per_shard;
+        ctr_.bytes_read += ds_->charge_footer(shard);
+        const Slot first = hs.record_slot(q);
+        uint64_t end = q + 1, run = ds_->slot_len()[q];
+        while (end <= q1 && end / m.chunks_per_shard == shard && hs.record_slot(end).off == first.off + run)
+            run += ds_->slot_len()[end++];
+        ctr_.read_ops += 1;
+        if (cfg_.cache_bypass && hs.direct_ok(shard)) {
+            const uint64_t a0 = first.off & ~4095ull;
+            const uint64_t span = HostStore::aligned_span(first.off, run);
+            ctr_.bytes_read += std::min(span, hs.shard_bytes(shard) - a0);
+        } else {
+            ctr_.bytes_read += run;
+        }
+        ctr_.chunks_decoded += end - q;
+        q = end;
+    }
 }
 
 void GpuLoader::ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz) {
@@ -940,7 +973,7 @@ bool GpuLoader::next(BatchOut& out) {
         batch_size_.clear();
         pend_ev_ = nullptr;
         d8_jobs_.clear();
-        for (uint64_t id : consumed_) stage_block(id);
+        for (uint64_t id : consumed_) stage_block(id);  // (counts each fetch)
         if (pend_ev_ && cudaEventQuery(pend_ev_) != cudaSuccess)
             cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");        if (!batch_dst_.empty()) {
             cudaMemcpyAttributes attr{};
@@ -953,6 +986,8 @@ bool GpuLoader::next(BatchOut& out) {
         }
         cuda_ok(cudaEventRecord(staged_, copy_), "event");
     }
+    if (resident)
+        for (uint64_t id : consumed_) count_fetch(id);
     if (tr.on) t_stage = tr.lap();
     OutSlot& s = slots_[next_slot_++ % slots_.size()];
     if (s.used) cuda_ok(cudaEventSynchronize(s.done), "slot reuse");  // caller's view of it expires here

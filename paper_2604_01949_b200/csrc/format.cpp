@@ -511,6 +511,9 @@ const File& HostStore::fd(uint64_t shard, bool direct) const {
     return it->second;
 }
 
+uint64_t HostStore::shard_bytes(uint64_t shard) const { return fd(shard, false).size(); }
+bool HostStore::direct_ok(uint64_t shard) const { return fd(shard, true).valid(); }
+
 Slot HostStore::record_slot(uint64_t chunk) const {
     const uint64_t shard = chunk / man_.chunks_per_shard;
     const File& f = fd(shard, false);

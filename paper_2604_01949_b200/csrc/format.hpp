@@ -118,6 +118,8 @@ public:
     const Manifest& manifest() const { return man_; }
     const std::string& root() const { return root_; }
     Slot record_slot(uint64_t chunk) const;  // throws CorruptStore on empty slot
+    uint64_t shard_bytes(uint64_t shard) const;  // file size of a shard
+    bool direct_ok(uint64_t shard) const;        // the shard opens with O_DIRECT
     void read_record(uint64_t chunk, void* dst, uint64_t cap) const;
     // pread an arbitrary byte range of one shard (coalesced runs, store.cpp:427-447)
     void read_shard_bytes(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const;

@@ -45,7 +45,7 @@ def test_deflate_batches_vs_reference(stores, name, staging, depth, bypass):
     path = stores[name]
     f, B, b = 70, 400, 128
     want = "csr,to_dense" if s["layout"] == "csr" else "dense"
-    ref = list(Ref.iterate(path, f, B, b, seed=3, epoch=1, want=want))
+    ref = list(Ref.iterate(path, f, B, b, seed=3, epoch=1, want=want, cache_bypass=bypass))
     rc = dict(Ref.last_counters)
     outs = ["csr", "dense"] if s["layout"] == "csr" else ["dense"]
     for out in outs:
@@ -62,9 +62,8 @@ def test_deflate_batches_vs_reference(stores, name, staging, depth, bypass):
                 assert m.block.values.tobytes() == (r["to_dense"] if s["layout"] == "csr" else r["dense"]).tobytes()
         c = it.counters()
         assert c.blocks_fetched == rc["blocks_fetched"] and c.peak_buffer_rows == rc["peak_buffer_rows"]
-        if staging != "resident":
-            assert (c.read_ops, c.bytes_read, c.chunks_decoded) == (rc["read_ops"], rc["bytes_read"],
-                                                                    rc["chunks_decoded"])
+        assert (c.read_ops, c.bytes_read, c.chunks_decoded) == (rc["read_ops"], rc["bytes_read"],
+                                                                rc["chunks_decoded"])
         it.close()
 
 

@@ -43,8 +43,9 @@ def test_csr_batches_bit_exact(golden, dstores, staging):
         assert [hex(fnv([m.block.indptr, m.block.indices, m.block.data])) for m in got] == ld["csr_fnv"]
         c = it.counters()
         assert c.blocks_fetched == ld["blocks_fetched"] and c.peak_buffer_rows == ld["peak_buffer_rows"]
-        if staging != "resident":  # same read granularity as the reference
-            assert c.read_ops == ld["read_ops"] and c.chunks_decoded == ld["chunks_decoded"]
+        # the reference's IoStats for the same fetches, in every staging mode (footer loads included)
+        assert (c.read_ops, c.bytes_read, c.chunks_decoded) == (ld["read_ops"], ld["bytes_read"],
+                                                                ld["chunks_decoded"])
 
 
 @pytest.mark.parametrize("staging", ["resident", "stream_pinned", "stream_file"])
@@ -338,6 +339,10 @@ def test_stream_file_readahead(golden, golden_stores, depth, bypass):
         c = it.counters()
         assert c.read_ops == ld["read_ops"] and c.chunks_decoded == ld["chunks_decoded"]
         assert st["n_var"] == got[0].block.values.shape[1]
+        # bytes_read as the reference counts it with the same cache_bypass (aligned O_DIRECT spans)
+        list(Ref.iterate(golden_stores[ld["store"]], ld["f"], ld["B"], ld["b"], seed=ld["seed"], epoch=ld["epoch"],
+                         drop_last=ld["drop_last"], cache_bypass=bypass))
+        assert c.bytes_read == Ref.last_counters["bytes_read"]
 
 
 def test_stream_file_abandoned_and_io_error(tmp_path):

@@ -64,8 +64,7 @@ def _cfg(s, **kw):
 def _check_counters(it, s, staging):
     c = it.counters()
     assert c.blocks_fetched == s["blocks_fetched"] and c.peak_buffer_rows == s["peak_buffer_rows"]
-    if staging != "resident":
-        assert c.read_ops == s["read_ops"] and c.chunks_decoded == s["chunks_decoded"]
+    assert (c.read_ops, c.bytes_read, c.chunks_decoded) == (s["read_ops"], s["bytes_read"], s["chunks_decoded"])
 
 
 @pytest.mark.parametrize("staging,output", [("stream_pinned", "csr"), ("resident", "dense"),
