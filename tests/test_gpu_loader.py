@@ -31,12 +31,15 @@ def dstores(golden_stores):
 
 
 @pytest.mark.parametrize("staging", ["resident", "stream_pinned", "stream_file"])
-def test_csr_batches_bit_exact(golden, dstores, staging):
-    """K2 csr_gather == reference MiniBatch (indptr, u64-widened indices, data, global_indices)."""
+def test_csr_batches_bit_exact(golden, golden_stores, staging):
+    """K2 csr_gather == reference MiniBatch (indptr, u64-widened indices, data, global_indices).
+    A fresh DeviceStore per iterator, as the golden run used a fresh StoreReader
+    (its first footer loads count into bytes_read)."""
     for ld in golden["loaders"]:
         if golden["stores"][ld["store"]]["layout"] != "csr":
             continue
-        it = R.BatchIterator(dstores[(ld["store"], staging)], _cfg(ld), ld["epoch"], output="csr")
+        it = R.BatchIterator(R.DeviceStore(golden_stores[ld["store"]], 0, staging), _cfg(ld), ld["epoch"],
+                             output="csr")
         got = [b.to_minibatch() for b in it]
         assert it.next() is None
         assert [m.global_indices.tolist() for m in got] == ld["gidx"]
