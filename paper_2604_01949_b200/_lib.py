@@ -17,7 +17,7 @@ OK, EINVAL, ECORRUPT, EIO, ECUDA, ENCCL, END = range(7)
 LAYOUT_DENSE, LAYOUT_CSR = 0, 1
 F32, F64, I32, U8, BF16, NATIVE = 0, 1, 2, 3, 4, 255
 IDX_U32, IDX_U64 = 0, 1
-STAGE_RESIDENT, STAGE_STREAM_PINNED, STAGE_STREAM_FILE = 0, 1, 2
+STAGE_RESIDENT, STAGE_STREAM_PINNED, STAGE_STREAM_FILE, STAGE_RESIDENT_CODED = 0, 1, 2, 3
 OUT_CSR, OUT_DENSE = 0, 1
 XF_NONE, XF_NORMALIZE_LOG1P = 0, 1
 

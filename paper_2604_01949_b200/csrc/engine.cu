@@ -1,4 +1,6 @@
 // Device store images + GPU BatchIterator (see engine.hpp).
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <array>
 #include <atomic>
@@ -128,7 +130,7 @@ std::vector<uint8_t> decode_record_checked(const Manifest& m, uint64_t q, const 
 DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     : hs_(std::move(hs)), device_(device), staging_(staging) {
     const Manifest& m = hs_->manifest();
-    if (staging > kStreamFile) invalid("unknown staging mode");
+    if (staging > kResidentCoded) invalid("unknown staging mode");
     const uint64_t nch = m.chunk_count();
     rec_off_.resize(nch);
     slot_len_.resize(nch);
@@ -149,17 +151,49 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
         open_image();
     } catch (...) {  // the destructor does not run for a throwing constructor
         if (d_arena_) cudaFree(d_arena_);
-        if (h_image_) cudaFreeHost(h_image_);
         d_arena_ = nullptr;
-        h_image_ = nullptr;
+        free_host_image();
         throw;
     }
+}
+
+void DStore::free_host_image() {
+    if (!h_image_) return;
+    if (h_map_bytes_) {
+        if (h_registered_) cudaHostUnregister(h_image_);
+        munmap(h_image_, h_map_bytes_);
+    } else {
+        cudaFreeHost(h_image_);
+    }
+    h_image_ = nullptr;
+    h_map_bytes_ = 0;
+    h_registered_ = false;
 }
 
 // load (resident / stream_pinned), validate and re-encode the image; per-row nnz
 void DStore::open_image() {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
+    img_off_ = rec_off_;
+    img_len_ = rec_len_;
+    // stream_pinned / resident_coded: the re-encoded staging image, built streaming
+    // from the store (records checked on the host as they are encoded)
+    if (staging_ == kStreamPinned || staging_ == kResidentCoded) {
+        const uint32_t mode = stage_mode();
+        if (mode != kStageVerbatim && build_staged_image(mode)) {
+            if (staging_ == kResidentCoded) {  // the image goes to HBM; the host copy is dropped
+                cuda_ok(cudaMalloc(&d_arena_, staged_bytes_ + kPad), "cudaMalloc staging image");
+                for (uint64_t o = 0; o < staged_bytes_ + kPad; o += kUploadRun)
+                    cuda_ok(cudaMemcpy(d_arena_ + o, h_image_ + o, std::min(kUploadRun, staged_bytes_ + kPad - o),
+                                       cudaMemcpyHostToDevice),
+                            "upload staging image");
+                free_host_image();
+            }
+            return;
+        }
+        if (staging_ == kResidentCoded) invalid("resident_coded staging needs a re-encodable store (csr u32 ids "
+                                                "with n_var <= 65536, or one-hot dense u8 rows)");
+    }
     if (m.codec == Codec::deflate) {
         if (staging_ != kStreamFile) load_records_deflate(staging_ == kResident);
     } else if (staging_ == kResident) {
@@ -173,18 +207,6 @@ void DStore::open_image() {
     if (m.layout == Layout::csr && staging_ != kStreamFile) {
         const char* nv = std::getenv("RFL_NO_VALIDATE");
         if (!(nv && nv[0] == '1')) validate_records(staging_ == kResident ? d_arena_ : h_image_);
-    }
-    img_off_ = rec_off_;
-    img_len_ = rec_len_;
-    if (staging_ == kStreamPinned && m.layout == Layout::dense && m.value_dtype == VDtype::u8 && m.n_var % 64 == 0) {
-        const char* e = std::getenv("RFL_NARROW");
-        if (!(e && e[0] == '0')) one_hot_image();
-    }
-    if (staging_ == kStreamPinned && m.layout == Layout::csr && m.index_dtype == IDtype::u32 && m.n_var <= 65536) {
-        const char* e = std::getenv("RFL_NARROW");
-        // RFL_NARROW=0: verbatim image; =16: u16 ids only; default: deltas when eligible, else u16
-        const bool off = e && e[0] == '0', only16 = e && std::string(e) == "16";
-        if (!off && (only16 || !delta_image())) narrow_image();
     }
     if (m.layout == Layout::csr && staging_ == kStreamFile && m.codec == Codec::none) {
         // file streaming: only headers + indptrs now (deflate: read by deflate_layout)
@@ -426,7 +448,7 @@ DStore::~DStore() {
             if (s.released) cudaEventDestroy(s.released);
     for (void* p : slabs_) cudaFree(p);
     if (d_arena_) cudaFree(d_arena_);
-    if (h_image_) cudaFreeHost(h_image_);
+    free_host_image();
 }
 
 uint64_t DStore::max_block_bytes(uint64_t f) const {
@@ -453,7 +475,7 @@ ArenaView DStore::view(const uint8_t* base) const {
     a.layout = m.layout;
     a.vdt = m.value_dtype;
     a.idt = m.index_dtype.value_or(IDtype::u32);
-    a.idx16 = idx16_ && staging_ == kStreamPinned;
+    a.idx16 = idx16_ && (staging_ == kStreamPinned || staging_ == kResidentCoded);
     return a;
 }
 
@@ -569,7 +591,6 @@ void DStore::release_slot(const SlotRef& s) {
 }
 
 // ============================================================ BlockReader ===
-namespace {
 // CsrBlock::validate's column checks (block.cpp:110-133) on a record whose header
 // and indptr were already checked: every id < n_var, strictly increasing per row
 bool columns_ok(const Manifest& m, uint64_t q, const uint8_t* rec) {
@@ -594,7 +615,6 @@ bool columns_ok(const Manifest& m, uint64_t q, const uint8_t* rec) {
     (void)q;
     return false;  // u64 ids: the full check (rare layout)
 }
-}  // namespace
 
 BlockReader::BlockReader(std::shared_ptr<DStore> ds, std::vector<uint64_t> order, uint64_t f, uint32_t threads,
                          uint32_t slots, bool direct)
@@ -820,7 +840,8 @@ void GpuLoader::stage_block(uint64_t id) {
     Live& lv = live_[id];
     lv.first_chunk = q0;
     lv.chunk_off.clear();
-    const bool d8 = ds_->staging() == kStreamPinned && ds_->d8();
+    const bool coded = ds_->staging() == kResidentCoded;  // staging image in HBM: decode device-to-device
+    const bool d8 = (ds_->staging() == kStreamPinned || coded) && ds_->d8();
     uint64_t bytes = 0;
     for (uint64_t q = q0; q <= q1; ++q) {
         lv.chunk_off.push_back(bytes);
@@ -834,11 +855,17 @@ void GpuLoader::stage_block(uint64_t id) {
             pend_ev_ = lv.slot.released;
             pend_seq_ = lv.slot.seq;
         }
+    } else if (coded) {  // the decode writes the slot on compute_, where this loader's releases were recorded
+        if (lv.slot.owner != id_ && cudaEventQuery(lv.slot.released) != cudaSuccess)
+            cuda_ok(cudaStreamWaitEvent(compute_, lv.slot.released, 0), "wait slot");
     } else if (cudaEventQuery(lv.slot.released) != cudaSuccess) {
         cuda_ok(cudaStreamWaitEvent(copy_, lv.slot.released, 0), "wait slot");
     }
-    const HostStore& hs = ds_->host();
-    if (ds_->staging() == kStreamPinned) {
+    if (coded) {
+        for (uint64_t q = q0; q <= q1; ++q)
+            d8_jobs_.push_back({ds_->d_arena() + ds_->img_off()[q], lv.slot.ptr + lv.chunk_off[q - q0],
+                                ds_->exp_len()[q], ds_->d8_kind(q), 0});
+    } else if (ds_->staging() == kStreamPinned) {
         // records of one block are contiguous in the pinned image except for alignment padding;
         // the copies of all blocks fetched for this batch go out as one cudaMemcpyBatchAsync
         const uint64_t img0 = ds_->img_off()[q0];

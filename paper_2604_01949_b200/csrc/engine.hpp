@@ -7,6 +7,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <array>
 #include <condition_variable>
 #include <cstdint>
 #include <exception>
@@ -29,7 +30,25 @@ constexpr uint64_t kRecAlign = 16;
 constexpr uint64_t kRecPad = 256;
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
-enum Staging : uint32_t { kResident = 0, kStreamPinned = 1, kStreamFile = 2 };
+// resident: verbatim records in HBM; stream_pinned: staging image in pinned host
+// memory, each fetched block copied H2D; stream_file: records read from the
+// shard files per fetch; resident_coded: the (re-encoded) staging image held in
+// HBM, each fetched block expanded device-to-device (a store whose verbatim
+// image exceeds HBM but whose staging image fits).
+enum Staging : uint32_t { kResident = 0, kStreamPinned = 1, kStreamFile = 2, kResidentCoded = 3 };
+enum StageMode : uint32_t { kStageVerbatim = 0, kStageIdx16 = 1, kStageDelta = 2, kStageOneHot = 3 };
+
+// Per-record staging encoding (staging.cpp): kind (D8Kind), staged bytes, bytes
+// of the expanded record, top-byte dictionary + escape count of coded values.
+struct StagePlan {
+    uint8_t kind = 0;
+    std::array<uint8_t, 4> dict{0, 0, 0, 0};
+    uint64_t n_esc = 0, bytes = 0, exp = 0;
+};
+StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values);
+void encode_csr_stage(const uint8_t* rec, uint64_t vs, const StagePlan& p, uint8_t* dst);
+bool one_hot_record(const uint8_t* rec, uint64_t rows, uint64_t n_var);
+void encode_one_hot(const uint8_t* rec, uint64_t rows, uint64_t n_var, uint8_t* dst);
 
 void cuda_ok(cudaError_t e, const char* what);
 
@@ -46,6 +65,9 @@ void full_check_csr_record(const Manifest& m, uint64_t chunk, const uint8_t* rec
 void check_dense_record(const Manifest& m, uint64_t chunk, uint64_t len);
 // Cheap pass (header, length, indptr; optionally per-row nnz); false -> run the full check.
 bool check_csr_record(const Manifest& m, uint64_t chunk, const uint8_t* rec, uint64_t len, uint32_t* row_nnz);
+// CsrBlock::validate's column checks (every id < n_var, strictly increasing per
+// row) on a u32 record whose header and indptr passed; false -> full check.
+bool columns_ok(const Manifest& m, uint64_t chunk, const uint8_t* rec);
 // decode_record (store.cpp:81-122) of a stored record: decoded bytes (inflated for
 // Codec::deflate), checked as the reference checks them; CorruptStore errors are
 // wrapped "chunk q in shard s: ..." as process_shard does (store.cpp:455-457).
@@ -100,6 +122,7 @@ public:
     uint32_t d8_kind(uint64_t q) const { return d8_rec_[q]; }  // D8Kind of staged record q
     const std::vector<uint64_t>& exp_len() const { return exp_len_; }
     uint64_t image_bytes() const { return image_bytes_; }
+    uint64_t staged_bytes() const { return staged_bytes_; }  // staging image (0: verbatim)
     uint64_t row_nnz(uint64_t row) const { return row_nnz_.empty() ? 0 : row_nnz_[row]; }
     uint64_t max_block_bytes(uint64_t f) const;  // staged bytes of the largest f-row block
     ArenaView view(const uint8_t* base) const;
@@ -133,9 +156,10 @@ private:
     void deflate_layout();
     void load_records_deflate(bool to_device);
     void validate_records(const uint8_t* base);
-    void narrow_image();
-    bool delta_image();
-    bool one_hot_image();
+    uint32_t stage_mode() const;
+    bool build_staged_image(uint32_t mode);
+    void read_checked(uint64_t q, uint8_t* dst, std::vector<uint8_t>& scratch, bool validate) const;
+    void free_host_image();
     std::shared_ptr<HostStore> hs_;
     int device_;
     uint32_t staging_;
@@ -147,6 +171,9 @@ private:
     uint64_t image_bytes_ = 0;
     uint8_t* d_arena_ = nullptr;
     uint8_t* h_image_ = nullptr;
+    uint64_t h_map_bytes_ = 0;     // > 0: h_image_ is an mmap'd staging image (else cudaHostAlloc)
+    bool h_registered_ = false;    // ... page-locked with cudaHostRegister
+    uint64_t staged_bytes_ = 0;    // bytes of the staging image
     std::mutex mu_;
     void grow_slab(uint64_t slot_bytes);  // mu_ held
     std::vector<void*> slabs_;

@@ -1,7 +1,14 @@
-// Re-encoding of a stream_pinned store's pinned image for PCIe (DESIGN.md,
-// "Re-encoded staging image"): u16 column ids, u8 column deltas (+ top-byte
-// coded values), one-hot channel codes.  Host-side, once per store at open;
-// the GPU expands the staged records (k_d8_decode) before the batch kernels.
+// The re-encoded staging image of a store ("Re-encoded staging
+// image"): u16 column ids, u8 column deltas (+ top-byte coded values), one-hot
+// channel codes.  Built on the host once per store at open, streaming: records
+// are read (and inflated) a window at a time by a thread pool, checked as
+// decode_record checks them, encoded, and written straight into the image, so
+// the verbatim store never has to fit in host memory.  The image lives in a
+// virtual reservation that is page-locked (cudaHostRegister) once filled --
+// pinned host memory for stream_pinned, or uploaded to HBM for resident_coded.
+// The GPU expands the staged records (k_d8_decode) before the batch kernels.
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <array>
 #include <atomic>
@@ -10,6 +17,7 @@
 #include <string>
 #include <thread>
 
+#include "codec.hpp"
 #include "engine.hpp"
 
 namespace rfl {
@@ -17,275 +25,300 @@ namespace rfl {
 namespace {
 constexpr uint64_t kAlign = kRecAlign;
 constexpr uint64_t kPad = kRecPad;
-}  // namespace
+constexpr uint64_t kWindowBytes = 512ull << 20;  // verbatim records held per window
 
-// The pinned staging image with u16 column indices (lossless: n_var <= 65536):
-// 2 of every 8 bytes per stored entry never cross PCIe.  The records were
-// validated in their store encoding first; kernels read this layout through
-// ArenaView::idx16 (csr_row<uint16_t>).
-namespace {
 template <typename F>
-void parallel_records(uint64_t n, F&& f) {
-    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+void parallel_for(uint64_t n, F&& f) {  // f(i) over [0, n) on up to 16 threads; first error rethrown
+    const unsigned T = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>({16u, std::max(1u, std::thread::hardware_concurrency()), n})));
+    std::atomic<uint64_t> next{0};
+    std::vector<std::exception_ptr> errs(T);
     std::vector<std::thread> pool;
     for (unsigned t = 0; t < T; ++t)
         pool.emplace_back([&, t] {
-            for (uint64_t q = t; q < n; q += T) f(q);
+            try {
+                for (uint64_t i; (i = next.fetch_add(1)) < n;) f(i);
+            } catch (...) {
+                errs[t] = std::current_exception();
+                next = n;
+            }
         });
     for (auto& th : pool) th.join();
+    for (auto& e : errs)
+        if (e) std::rethrow_exception(e);
 }
 }  // namespace
 
-// Delta staging image (kernels.cuh d8_* / d8v_*): records whose in-row column
-// gaps are all <= 255 stage as u8 deltas (1 B per stored column id instead of
-// 4), with 4-byte values also top-byte coded when that is smaller
-// (RFL_NARROW_VALUES=0 keeps them raw); the rest stage as idx16 records.  A
-// kernel expands every kind into idx16 records in the slot.  Analysed read-only
-// and encoded in parallel into a separate buffer, then copied over the
-// verbatim image (false: the encoding would not fit; narrow_image() runs).
-bool DStore::delta_image() {
-    const Manifest& m = hs_->manifest();
+// ---------------------------------------------------------- per-record codecs --
+StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values) {
+    const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
+    const uint8_t* ip = rec + kCsrHeaderBytes;
+    const uint8_t* ix = ip + 4 * (rows + 1);
+    StagePlan p;
+    p.exp = idx16_record_bytes(rows, nnz, vs);
+    p.kind = kIdx16Copy;
+    p.bytes = p.exp;
+    if (!allow_delta) return p;
+    for (uint64_t r = 0; r < rows; ++r) {  // every in-row column gap <= 255?
+        const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+        uint32_t big = 0;
+        for (uint64_t k = lo + 1; k < hi; ++k) big |= static_cast<uint32_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)) > 255);
+        if (big) return p;
+    }
+    p.kind = kD8Raw;
+    p.bytes = d8_record_bytes(rows, nnz, vs);
+    if (!code_values || vs != 4) return p;
+    // top-byte dictionary (3 most frequent) + escapes, kept when smaller
+    uint64_t hist[256] = {0};
+    const uint8_t* val = ix + 4 * nnz;
+    for (uint64_t k = 0; k < nnz; ++k) ++hist[val[4 * k + 3]];
+    std::array<uint8_t, 4> d{0, 0, 0, 0};
+    uint64_t covered = 0;
+    for (int c = 0; c < 3; ++c) {
+        int best = 0;
+        for (int b = 1; b < 256; ++b)
+            if (hist[b] > hist[best]) best = b;
+        d[c] = static_cast<uint8_t>(best);
+        covered += hist[best];
+        hist[best] = 0;
+    }
+    const uint64_t esc = nnz - covered;
+    bool low16_zero = true;
+    for (uint64_t k = 0; k < nnz && low16_zero; ++k) low16_zero = val[4 * k] == 0 && val[4 * k + 1] == 0;
+    const uint64_t bytes = d8v_layout(rows, nnz, esc, low16_zero ? 1 : 3).bytes;
+    if (bytes < p.bytes) {
+        p.kind = low16_zero ? kD8Coded16 : kD8Coded;
+        p.dict = d;
+        p.n_esc = esc;
+        p.bytes = bytes;
+    }
+    return p;
+}
+
+void encode_csr_stage(const uint8_t* src, uint64_t vs, const StagePlan& p, uint8_t* dst) {
+    std::memset(dst, 0, p.bytes);
+    const uint64_t rows = rd32(src), nnz = rd64(src + 4);
+    const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
+    std::memcpy(dst, src, head);  // header + u32 indptr unchanged
+    const uint8_t* ip = src + kCsrHeaderBytes;
+    const uint8_t* ix = src + head;
+    const uint8_t* val = ix + 4 * nnz;
+    if (p.kind == kIdx16Copy) {
+        for (uint64_t k = 0; k < nnz; ++k) {
+            const uint16_t w = static_cast<uint16_t>(rd32(ix + 4 * k));
+            std::memcpy(dst + head + 2 * k, &w, 2);
+        }
+        std::memcpy(dst + head + ((2 * nnz + 7) & ~7ull), val, vs * nnz);
+        return;
+    }
+    uint8_t* first = dst + head;
+    uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
+    for (uint64_t r = 0; r < rows; ++r) {
+        const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+        const uint16_t f = lo < hi ? static_cast<uint16_t>(rd32(ix + 4 * lo)) : 0;
+        std::memcpy(first + 2 * r, &f, 2);
+        for (uint64_t k = lo; k < hi; ++k)
+            delta[k] = k == lo ? 0 : static_cast<uint8_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)));
+    }
+    if (p.kind == kD8Raw) {
+        std::memcpy(dst + d8_values_offset(rows, nnz), val, vs * nnz);
+        return;
+    }
+    const bool c16 = p.kind == kD8Coded16;
+    const D8vLayout L = d8v_layout(rows, nnz, p.n_esc, c16 ? 1 : 3);
+    std::memcpy(dst + L.dict, p.dict.data(), 4);
+    const uint32_t ne = static_cast<uint32_t>(p.n_esc);
+    std::memcpy(dst + L.n_esc, &ne, 4);
+    uint32_t e = 0;
+    for (uint64_t r = 0; r < rows; ++r) {
+        std::memcpy(dst + L.esc_base + 4 * r, &e, 4);
+        const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+        for (uint64_t k = lo; k < hi; ++k) {
+            const uint8_t top = val[4 * k + 3];
+            const uint32_t code = top == p.dict[0] ? 0u : top == p.dict[1] ? 1u : top == p.dict[2] ? 2u : 3u;
+            dst[L.codes + (k >> 2)] |= static_cast<uint8_t>(code << (2 * (k & 3)));
+            if (code == 3) dst[L.esc + e++] = top;
+            if (c16) dst[L.low3 + k] = val[4 * k + 2];
+            else std::memcpy(dst + L.low3 + 3 * k, val + 4 * k, 3);
+        }
+    }
+}
+
+bool one_hot_record(const uint8_t* rec, uint64_t rows, uint64_t n_var) {
+    const uint64_t L = n_var / 4;
+    for (uint64_t i = 0; i < rows; ++i) {
+        const uint8_t* row = rec + i * n_var;
+        uint32_t bad = 0;
+        for (uint64_t p = 0; p < L; ++p) {
+            const uint32_t a = row[p], b = row[L + p], c = row[2 * L + p], d = row[3 * L + p];
+            bad |= static_cast<uint32_t>((a | b | c | d) > 1) | static_cast<uint32_t>(a + b + c + d != 1);
+        }
+        if (bad) return false;
+    }
+    return true;
+}
+
+void encode_one_hot(const uint8_t* rec, uint64_t rows, uint64_t n_var, uint8_t* dst) {
+    const uint64_t L = n_var / 4;
+    std::memset(dst, 0, rows * (L / 4));
+    for (uint64_t i = 0; i < rows; ++i) {
+        const uint8_t* row = rec + i * n_var;
+        uint8_t* codes = dst + i * (L / 4);
+        for (uint64_t p = 0; p < L; ++p) {
+            const uint32_t ch = row[L + p] ? 1u : row[2 * L + p] ? 2u : row[3 * L + p] ? 3u : 0u;
+            codes[p >> 2] |= static_cast<uint8_t>(ch << (2 * (p & 3)));
+        }
+    }
+}
+
+// ------------------------------------------------------------ image builder --
+// Which encoding the staging image of this store can use (kStageVerbatim: none).
+// RFL_NARROW=0 keeps the verbatim image, =16 u16 ids only; default: deltas where
+// every in-row gap <= 255 (+ coded values unless RFL_NARROW_VALUES=0), u16 ids
+// elsewhere; dense u8 rows one-hot over 4 planes (n_var % 64 == 0) as 2-bit codes.
+uint32_t DStore::stage_mode() const {
+    const Manifest& m = manifest();
+    const char* e = std::getenv("RFL_NARROW");
+    if (e && e[0] == '0') return kStageVerbatim;
+    if (m.layout == Layout::csr && m.index_dtype == IDtype::u32 && m.n_var <= 65536)
+        return e && std::string(e) == "16" ? kStageIdx16 : kStageDelta;
+    if (m.layout == Layout::dense && m.value_dtype == VDtype::u8 && m.n_var % 64 == 0) return kStageOneHot;
+    return kStageVerbatim;
+}
+
+// Verbatim (decoded) record q into dst[0, rec_len_[q]), checked like
+// decode_record (store.cpp:81-122) incl. CsrBlock::validate's column checks;
+// per-row nnz of CSR records into row_nnz_.
+void DStore::read_checked(uint64_t q, uint8_t* dst, std::vector<uint8_t>& scratch, bool validate) const {
+    const Manifest& m = manifest();
+    const Slot sl = hs_->record_slot(q);
+    if (m.codec == Codec::deflate) {
+        scratch.resize(sl.len);
+        hs_->read_shard_bytes(q / m.chunks_per_shard, sl.off, scratch.data(), sl.len, false);
+        if (!inflate_fits(scratch.data(), sl.len, dst, rec_len_[q])) {
+            decode_record_checked(m, q, scratch.data(), sl.len);
+            corrupt("chunk " + std::to_string(q) + " in shard " + std::to_string(q / m.chunks_per_shard) +
+                    ": csr record invalid");
+        }
+    } else {
+        hs_->read_shard_bytes(q / m.chunks_per_shard, sl.off, dst, sl.len, false);
+    }
+    if (m.layout == Layout::dense) {
+        check_dense_record(m, q, rec_len_[q]);
+        return;
+    }
+    uint32_t* rn = const_cast<uint32_t*>(row_nnz_.data()) + q * m.chunk_rows;
+    if (!check_csr_record(m, q, dst, rec_len_[q], rn)) full_check_csr_record(m, q, dst, rec_len_[q]);
+    if (validate && !columns_ok(m, q, dst)) full_check_csr_record(m, q, dst, rec_len_[q]);
+}
+
+bool DStore::build_staged_image(uint32_t mode) {
+    const Manifest& m = manifest();
     const uint64_t nch = m.chunk_count();
     const uint64_t vs = value_size(m.value_dtype);
-    // per record: delta-eligible (every in-row gap <= 255)?  With 4-byte values, also
-    // the top-byte dictionary (3 most frequent) and its escape count, kept when smaller
-    std::vector<uint8_t> kind(nch, kD8Raw);
-    std::vector<std::array<uint8_t, 4>> dict(nch);
-    std::vector<uint64_t> n_esc(nch, 0);
+    const char* nv = std::getenv("RFL_NO_VALIDATE");
+    const bool validate = m.layout == Layout::csr && !(nv && nv[0] == '1');
     const char* ve = std::getenv("RFL_NARROW_VALUES");
-    const bool code_values = vs == 4 && !(ve && ve[0] == '0');
-    {
-        const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> pool;
-        for (unsigned t = 0; t < T; ++t)
-            pool.emplace_back([&, t] {
-                for (uint64_t q = t; q < nch; q += T) {
-                    const uint8_t* rec = h_image_ + rec_off_[q];
-                    const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
-                    const uint8_t* ip = rec + kCsrHeaderBytes;
-                    const uint8_t* ix = ip + 4 * (rows + 1);
-                    bool ok = true;
-                    for (uint64_t r = 0; r < rows && ok; ++r) {
-                        const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
-                        for (uint64_t k = lo + 1; k < hi; ++k)
-                            if (rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)) > 255) {
-                                ok = false;
-                                break;
-                            }
-                    }
-                    if (!ok) {
-                        kind[q] = kIdx16Copy;
-                        continue;
-                    }
-                    if (!code_values) continue;
-                    uint64_t hist[256] = {0};
-                    const uint8_t* val = ix + 4 * nnz;
-                    for (uint64_t k = 0; k < nnz; ++k) ++hist[val[4 * k + 3]];
-                    std::array<uint8_t, 4> d{0, 0, 0, 0};
-                    uint64_t covered = 0;
-                    for (int c = 0; c < 3; ++c) {
-                        int best = 0;
-                        for (int b = 1; b < 256; ++b)
-                            if (hist[b] > hist[best]) best = b;
-                        d[c] = static_cast<uint8_t>(best);
-                        covered += hist[best];
-                        hist[best] = 0;
-                    }
-                    const uint64_t esc = nnz - covered;
-                    bool low16_zero = true;
-                    for (uint64_t k = 0; k < nnz && low16_zero; ++k) low16_zero = val[4 * k] == 0 && val[4 * k + 1] == 0;
-                    const uint64_t lb = low16_zero ? 1 : 3;
-                    if (d8v_layout(rows, nnz, esc, lb).bytes < d8_record_bytes(rows, nnz, vs)) {
-                        kind[q] = low16_zero ? kD8Coded16 : kD8Coded;
-                        dict[q] = d;
-                        n_esc[q] = esc;
-                    }
+    const bool code_values = !(ve && ve[0] == '0');
+    // virtual reservation bounding every encoding (each kind is at most the
+    // verbatim record + 2 B per row + padding), committed page by page as filled
+    uint64_t bound = kPad + 4096;
+    for (uint64_t q = 0; q < nch; ++q) bound += align_up(rec_len_[q] + 4 * m.rows_in_chunk(q) + 64, kAlign);
+    void* map = mmap(nullptr, bound, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+    if (map == MAP_FAILED) throw Error(kIo, "staging image: mmap of " + std::to_string(bound) + " bytes failed");
+    uint8_t* img = static_cast<uint8_t*>(map);
+    std::vector<uint64_t> off(nch), len(nch), elen(nch);
+    std::vector<uint8_t> kind(nch);
+    std::vector<uint8_t> win;
+    std::vector<uint64_t> wpos;
+    std::vector<StagePlan> plans;
+    uint64_t cursor = 0;
+    try {
+        for (uint64_t q0 = 0; q0 < nch;) {
+            uint64_t q1 = q0, wb = 0;
+            wpos.clear();
+            while (q1 < nch && (q1 == q0 || wb + rec_len_[q1] <= kWindowBytes)) {
+                wpos.push_back(wb);
+                wb = align_up(wb + rec_len_[q1], kAlign);
+                ++q1;
+            }
+            if (win.size() < wb + kPad) win.resize(wb + kPad);
+            plans.assign(q1 - q0, StagePlan{});
+            std::atomic<bool> one_hot_ok{true};
+            parallel_for(q1 - q0, [&](uint64_t k) {
+                thread_local std::vector<uint8_t> scratch;
+                const uint64_t q = q0 + k;
+                uint8_t* rec = win.data() + wpos[k];
+                read_checked(q, rec, scratch, validate);
+                if (mode == kStageOneHot) {
+                    if (!one_hot_record(rec, m.rows_in_chunk(q), m.n_var)) one_hot_ok = false;
+                    plans[k].kind = kOneHot4;
+                    plans[k].bytes = m.rows_in_chunk(q) * (m.n_var / 16);
+                    plans[k].exp = rec_len_[q];
+                } else {
+                    plans[k] = plan_csr_stage(rec, vs, mode == kStageDelta, code_values);
                 }
             });
-        for (auto& th : pool) th.join();
-    }
-    std::vector<uint64_t> off(nch), len(nch), elen(nch);
-    uint64_t total = 0;
-    for (uint64_t q = 0; q < nch; ++q) {
-        const uint8_t* rec = h_image_ + rec_off_[q];
-        const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
-        elen[q] = idx16_record_bytes(rows, nnz, vs);
-        len[q] = kind[q] == kIdx16Copy  ? elen[q]
-                 : kind[q] == kD8Coded   ? d8v_layout(rows, nnz, n_esc[q]).bytes
-                 : kind[q] == kD8Coded16 ? d8v_layout(rows, nnz, n_esc[q], 1).bytes
-                                         : d8_record_bytes(rows, nnz, vs);
-        off[q] = total;
-        total = align_up(total + len[q], kAlign);
-    }
-    if (total > image_bytes_) return false;
-    // encode in parallel into a separate buffer (the verbatim image stays read-only), then copy back
-    std::vector<uint8_t> img(total, 0);
-    parallel_records(nch, [&](uint64_t q) {
-        const uint8_t* src = h_image_ + rec_off_[q];
-        uint8_t* dst = img.data() + off[q];
-        const uint64_t rows = rd32(src), nnz = rd64(src + 4);
-        const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
-        std::memcpy(dst, src, head);
-        const uint8_t* ip = src + kCsrHeaderBytes;
-        const uint8_t* ix = src + head;
-        const uint8_t* val = ix + 4 * nnz;
-        if (kind[q] == kIdx16Copy) {
-            for (uint64_t k = 0; k < nnz; ++k) {
-                const uint16_t w = static_cast<uint16_t>(rd32(ix + 4 * k));
-                std::memcpy(dst + head + 2 * k, &w, 2);
+            if (!one_hot_ok) {  // not a one-hot store: the verbatim image
+                munmap(map, bound);
+                return false;
             }
-            std::memcpy(dst + head + ((2 * nnz + 7) & ~7ull), val, vs * nnz);
-            return;
-        }
-        uint8_t* first = dst + head;
-        uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
-        for (uint64_t r = 0; r < rows; ++r) {
-            const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
-            const uint16_t f = lo < hi ? static_cast<uint16_t>(rd32(ix + 4 * lo)) : 0;
-            std::memcpy(first + 2 * r, &f, 2);
-            for (uint64_t k = lo; k < hi; ++k)
-                delta[k] = k == lo ? 0 : static_cast<uint8_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)));
-        }
-        if (kind[q] == kD8Raw) {
-            std::memcpy(dst + d8_values_offset(rows, nnz), val, vs * nnz);
-            return;
-        }
-        const bool c16 = kind[q] == kD8Coded16;
-        const D8vLayout L = d8v_layout(rows, nnz, n_esc[q], c16 ? 1 : 3);
-        const std::array<uint8_t, 4>& d = dict[q];
-        std::memcpy(dst + L.dict, d.data(), 4);
-        const uint32_t ne = static_cast<uint32_t>(n_esc[q]);
-        std::memcpy(dst + L.n_esc, &ne, 4);
-        uint32_t e = 0;
-        for (uint64_t r = 0; r < rows; ++r) {
-            std::memcpy(dst + L.esc_base + 4 * r, &e, 4);
-            const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
-            for (uint64_t k = lo; k < hi; ++k) {
-                const uint8_t top = val[4 * k + 3];
-                const uint32_t code = top == d[0] ? 0u : top == d[1] ? 1u : top == d[2] ? 2u : 3u;
-                dst[L.codes + (k >> 2)] |= static_cast<uint8_t>(code << (2 * (k & 3)));
-                if (code == 3) dst[L.esc + e++] = top;
-                if (c16) dst[L.low3 + k] = val[4 * k + 2];
-                else std::memcpy(dst + L.low3 + 3 * k, val + 4 * k, 3);
+            for (uint64_t k = 0; k < q1 - q0; ++k) {
+                const uint64_t q = q0 + k;
+                off[q] = cursor;
+                len[q] = plans[k].bytes;
+                elen[q] = plans[k].exp;
+                kind[q] = plans[k].kind;
+                cursor = align_up(cursor + len[q], kAlign);
             }
+            if (cursor + kPad > bound) throw Error(kIo, "staging image: encoding exceeds its reservation");
+            parallel_for(q1 - q0, [&](uint64_t k) {
+                const uint64_t q = q0 + k;
+                const uint8_t* rec = win.data() + wpos[k];
+                if (mode == kStageOneHot) encode_one_hot(rec, m.rows_in_chunk(q), m.n_var, img + off[q]);
+                else encode_csr_stage(rec, vs, plans[k], img + off[q]);
+                const uint64_t gap = (q + 1 < nch ? align_up(off[q] + len[q], kAlign) : off[q] + len[q] + kPad) -
+                                     (off[q] + len[q]);
+                std::memset(img + off[q] + len[q], 0, gap);
+            });
+            q0 = q1;
         }
-    });
-    std::memcpy(h_image_, img.data(), total);
-    std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
+    } catch (...) {
+        munmap(map, bound);
+        throw;
+    }
+    std::vector<uint8_t>().swap(win);
+    // release the unused tail of the reservation, then page-lock the image
+    const uint64_t used = (cursor + kPad + 4095) & ~4095ull;
+    if (used < bound) munmap(img + used, bound - used);
+    h_map_bytes_ = used;
+    h_image_ = img;
+    if (staging_ == kStreamPinned) {
+        const cudaError_t rc = cudaHostRegister(img, used, cudaHostRegisterPortable);
+        if (rc != cudaSuccess) {
+            munmap(img, used);
+            h_image_ = nullptr;
+            h_map_bytes_ = 0;
+            cuda_ok(rc, "cudaHostRegister staging image");
+        }
+        h_registered_ = true;
+    }
     img_off_ = std::move(off);
     img_len_ = std::move(len);
     exp_len_ = std::move(elen);
     d8_rec_ = std::move(kind);
-    idx16_ = d8_ = true;
+    staged_bytes_ = cursor;
+    if (mode == kStageIdx16 && staging_ == kStreamPinned) {
+        // u16 ids only: the kernels read the staged records in place (no decode)
+        idx16_ = true;
+        d8_ = false;
+        exp_len_.clear();
+        d8_rec_.clear();
+    } else {
+        idx16_ = mode != kStageOneHot;
+        d8_ = true;
+    }
     return true;
-}
-
-// One-hot staging image (kernels.cuh kOneHot4): when every row of a dense u8
-// store is one-hot over 4 channel planes ([4][n_var/4], exactly one 1 per
-// position -- the WGS-window encoding of BASELINE config 4), each row stages
-// as n_var/16 bytes of 2-bit channel codes; the decode kernel rebuilds the
-// verbatim rows in the slot.  Checked read-only first; false = not one-hot.
-bool DStore::one_hot_image() {
-    const Manifest& m = hs_->manifest();
-    const uint64_t nch = m.chunk_count();
-    const uint64_t L = m.n_var / 4;
-    std::atomic<bool> ok{true};
-    {
-        const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> pool;
-        for (unsigned t = 0; t < T; ++t)
-            pool.emplace_back([&, t] {
-                for (uint64_t q = t; q < nch && ok.load(std::memory_order_relaxed); q += T) {
-                    const uint8_t* rec = h_image_ + rec_off_[q];
-                    const uint64_t rows = m.rows_in_chunk(q);
-                    for (uint64_t i = 0; i < rows; ++i) {
-                        const uint8_t* row = rec + i * m.n_var;
-                        for (uint64_t p = 0; p < L; ++p) {
-                            const uint32_t a = row[p], b = row[L + p], c = row[2 * L + p], d = row[3 * L + p];
-                            if ((a | b | c | d) > 1 || a + b + c + d != 1) {
-                                ok = false;
-                                return;
-                            }
-                        }
-                    }
-                }
-            });
-        for (auto& th : pool) th.join();
-    }
-    if (!ok) return false;
-    std::vector<uint64_t> off(nch), len(nch);
-    uint64_t total = 0;
-    for (uint64_t q = 0; q < nch; ++q) {
-        len[q] = m.rows_in_chunk(q) * (L / 4);
-        off[q] = total;
-        total = align_up(total + len[q], kAlign);
-    }
-    std::vector<uint8_t> img(total, 0);  // encoded in parallel, then copied over the verbatim image
-    parallel_records(nch, [&](uint64_t q) {
-        uint8_t* dst = img.data() + off[q];
-        const uint64_t rows = m.rows_in_chunk(q);
-        for (uint64_t i = 0; i < rows; ++i) {
-            const uint8_t* row = h_image_ + rec_off_[q] + i * m.n_var;
-            uint8_t* codes = dst + i * (L / 4);
-            for (uint64_t p = 0; p < L; ++p) {
-                const uint32_t ch = row[L + p] ? 1u : row[2 * L + p] ? 2u : row[3 * L + p] ? 3u : 0u;
-                codes[p >> 2] |= static_cast<uint8_t>(ch << (2 * (p & 3)));
-            }
-        }
-    });
-    std::memcpy(h_image_, img.data(), total);
-    std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
-    img_off_ = std::move(off);
-    img_len_ = std::move(len);
-    exp_len_ = rec_len_;
-    d8_rec_.assign(nch, kOneHot4);
-    d8_ = true;
-    return true;
-}
-
-void DStore::narrow_image() {
-    const Manifest& m = hs_->manifest();
-    const uint64_t nch = m.chunk_count();
-    const uint64_t vs = value_size(m.value_dtype);
-    std::vector<uint64_t> off(nch), len(nch);
-    uint64_t total = 0;
-    for (uint64_t q = 0; q < nch; ++q) {
-        const uint8_t* rec = h_image_ + rec_off_[q];
-        len[q] = idx16_record_bytes(rd32(rec), rd64(rec + 4), vs);
-        off[q] = total;
-        total = align_up(total + len[q], kAlign);
-    }
-    // In place, front to back (no second pinned image): safe when every narrowed
-    // record ends before the next record's old start (it starts at or below its
-    // old offset, and within a record each destination byte lies below every
-    // source byte still to be read).  Only records with < 4 entries can grow
-    // (index padding); if that ever breaks the rule, keep the verbatim image.
-    for (uint64_t q = 0; q < nch; ++q) {
-        const uint64_t next_old = q + 1 < nch ? rec_off_[q + 1] : image_bytes_;
-        if (off[q] > rec_off_[q] || off[q] + len[q] > next_old) return;
-    }
-    for (uint64_t q = 0; q < nch; ++q) {
-        const uint8_t* src = h_image_ + rec_off_[q];
-        uint8_t* dst = h_image_ + off[q];
-        const uint64_t rows = rd32(src), nnz = rd64(src + 4);
-        const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
-        std::memmove(dst, src, head);  // header + u32 indptr unchanged
-        const uint8_t* si = src + head;
-        uint8_t* di = dst + head;
-        for (uint64_t k = 0; k < nnz; ++k) {
-            uint32_t v;
-            std::memcpy(&v, si + 4 * k, 4);
-            const uint16_t w = static_cast<uint16_t>(v);
-            std::memcpy(di + 2 * k, &w, 2);
-        }
-        const uint64_t ib = (2 * nnz + 7) & ~7ull;
-        std::memmove(dst + head + ib, src + head + 4 * nnz, vs * nnz);  // before the pad may overwrite it
-        std::memset(dst + head + 2 * nnz, 0, ib - 2 * nnz);
-    }
-    std::memset(h_image_ + total, 0, std::min<uint64_t>(kPad, image_bytes_ + kPad - total));
-    img_off_ = std::move(off);
-    img_len_ = std::move(len);
-    idx16_ = true;
 }
 
 }  // namespace rfl

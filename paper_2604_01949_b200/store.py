@@ -12,7 +12,7 @@ LAYOUTS = {"dense": L.LAYOUT_DENSE, "csr": L.LAYOUT_CSR}
 VDTYPES = {"f32": L.F32, "f64": L.F64, "i32": L.I32, "u8": L.U8}
 IDTYPES = {"u32": L.IDX_U32, "u64": L.IDX_U64}
 STAGING = {"resident": L.STAGE_RESIDENT, "stream_pinned": L.STAGE_STREAM_PINNED,
-           "stream_file": L.STAGE_STREAM_FILE}
+           "stream_file": L.STAGE_STREAM_FILE, "resident_coded": L.STAGE_RESIDENT_CODED}
 _INV = lambda d: {v: k for k, v in d.items()}  # noqa: E731
 
 
