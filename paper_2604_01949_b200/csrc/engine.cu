@@ -529,15 +529,6 @@ void OutBuffers::free_all() {
     *this = OutBuffers{};
 }
 
-uint64_t DStore::charge_footer(uint64_t shard) {
-    const Manifest& m = manifest();
-    std::lock_guard<std::mutex> lk(mu_);
-    if (footer_charged_.empty()) footer_charged_.assign(m.shard_count(), 0);
-    if (footer_charged_[shard]) return 0;
-    footer_charged_[shard] = 1;
-    return m.chunks_per_shard * 16 + 8;  // ShardFooter::footer_bytes + magic
-}
-
 uint8_t* DStore::take_pinned(uint64_t bytes) {
     {
         std::lock_guard<std::mutex> lk(mu_);
@@ -911,7 +902,7 @@ void GpuLoader::count_fetch(uint64_t id) {
     uint64_t q = q0;
     while (q <= q1) {
         const uint64_t shard = q / m.chunks_per_shard;
-        ctr_.bytes_read += ds_->charge_footer(shard);
+        ctr_.bytes_read += hs.charge_footer(shard);
         const Slot first = hs.record_slot(q);
         uint64_t end = q + 1, run = ds_->slot_len()[q];
         while (end <= q1 && end / m.chunks_per_shard == shard && hs.record_slot(end).off == first.off + run)

@@ -140,9 +140,6 @@ public:
     // steady-state epoch never allocates (cudaMalloc stalls the device)
     void reserve_slots(uint64_t bytes, uint64_t n);
     void release_slot(const SlotRef& s);
-    // IoStats::bytes_read of the first footer load of a shard through this store
-    // (StoreReader::footer, store.cpp:318-328): footer bytes once, then 0
-    uint64_t charge_footer(uint64_t shard);
     // output-buffer pool shared by the iterators over this store
     OutBuffers take_out(uint32_t key);
     void give_out(OutBuffers&& b);
@@ -180,7 +177,6 @@ private:
     // per slot size, FIFO: reuse the slot released longest ago (its readers are done)
     std::map<uint64_t, std::deque<SlotRef>> free_;
     std::vector<OutBuffers> out_pool_;
-    std::vector<uint8_t> footer_charged_;
     std::vector<std::pair<uint8_t*, uint64_t>> pinned_pool_;
 };
 

@@ -514,6 +514,14 @@ const File& HostStore::fd(uint64_t shard, bool direct) const {
 uint64_t HostStore::shard_bytes(uint64_t shard) const { return fd(shard, false).size(); }
 bool HostStore::direct_ok(uint64_t shard) const { return fd(shard, true).valid(); }
 
+uint64_t HostStore::charge_footer(uint64_t shard) const {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (footer_charged_.empty()) footer_charged_.assign(man_.shard_count(), 0);
+    if (footer_charged_[shard]) return 0;
+    footer_charged_[shard] = 1;
+    return man_.chunks_per_shard * 16 + 8;  // ShardFooter::footer_bytes + magic
+}
+
 Slot HostStore::record_slot(uint64_t chunk) const {
     const uint64_t shard = chunk / man_.chunks_per_shard;
     const File& f = fd(shard, false);

@@ -120,6 +120,10 @@ public:
     Slot record_slot(uint64_t chunk) const;  // throws CorruptStore on empty slot
     uint64_t shard_bytes(uint64_t shard) const;  // file size of a shard
     bool direct_ok(uint64_t shard) const;        // the shard opens with O_DIRECT
+    // IoStats::bytes_read of a shard's first footer load through this store
+    // (StoreReader::footer, store.cpp:318-328): the footer bytes once, then 0.
+    // Readers sharing the store share the charge, as they share the reference's footer cache.
+    uint64_t charge_footer(uint64_t shard) const;
     void read_record(uint64_t chunk, void* dst, uint64_t cap) const;
     // pread an arbitrary byte range of one shard (coalesced runs, store.cpp:427-447)
     void read_shard_bytes(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const;
@@ -139,6 +143,7 @@ private:
     mutable std::mutex mu_;
     mutable std::unordered_map<uint64_t, File> fds_, dfds_;
     mutable std::unordered_map<uint64_t, std::vector<Slot>> footers_;
+    mutable std::vector<uint8_t> footer_charged_;
 };
 
 // ---- CSR record header accessors (store.cpp:52-64,81-122) ---------------------------

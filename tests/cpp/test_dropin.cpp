@@ -260,11 +260,11 @@ GPU_CASE("BatchIterator: the MiniBatch stream equals the reference's (csr + dens
             CHECK(!ours.next());  // idempotent end of epoch (loader.cpp:259)
             CHECK(ours.counters().blocks_fetched == ref.counters().blocks_fetched);
             CHECK(ours.peak_buffer_rows() == ref.peak_buffer_rows());
-            if (st != B::Staging::resident) {  // same read granularity as the reference
-                CHECK(ours.counters().io.read_ops == ref.counters().io.read_ops);
-                CHECK(ours.counters().io.chunks_decoded == ref.counters().io.chunks_decoded);
-                CHECK(ours.counters().io.bytes_read == ref.counters().io.bytes_read);
-            }
+            // the reference's IoStats in every staging mode (both store handles are shared
+            // across the stagings, so footer loads are charged to the first iterator in both)
+            CHECK(ours.counters().io.read_ops == ref.counters().io.read_ops);
+            CHECK(ours.counters().io.chunks_decoded == ref.counters().io.chunks_decoded);
+            CHECK(ours.counters().io.bytes_read == ref.counters().io.bytes_read);
         }
     }
 }
