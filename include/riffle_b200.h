@@ -143,11 +143,15 @@ rfl_status rfl_dstore_create(rfl_store* s, int device, uint32_t staging, rfl_dst
 /* device address + byte offsets of every chunk record (resident only) */
 rfl_status rfl_dstore_arena(const rfl_dstore* d, void** base, const uint64_t** chunk_offsets,
                             uint64_t* n_chunks);
+/* Decoded record bytes of the store, and bytes of its re-encoded staging
+ * image (stream_pinned / resident_coded; 0 when the records are staged verbatim). */
+rfl_status rfl_dstore_bytes(const rfl_dstore* d, uint64_t* record_bytes, uint64_t* staged_bytes);
 void rfl_dstore_destroy(rfl_dstore* d);
 
 /* Output of one minibatch, on the device. */
 enum { RFL_OUT_CSR = 0, RFL_OUT_DENSE = 1 };
 enum { RFL_XF_NONE = 0, RFL_XF_NORMALIZE_LOG1P = 1 };
+enum { RFL_DEV_TIME_KERNELS = 1 };
 
 typedef struct rfl_device_config {
     uint32_t output;    /* RFL_OUT_CSR | RFL_OUT_DENSE (CSR stores); dense stores: DENSE */
@@ -155,7 +159,7 @@ typedef struct rfl_device_config {
     uint32_t transform; /* RFL_XF_* (CSR -> dense only) */
     float target_sum;   /* normalize target T (default 1e4 when 0) */
     uint32_t out_slots; /* ring of output buffers (>= 1; default 2) */
-    uint32_t reserved;
+    uint32_t flags;     /* RFL_DEV_TIME_KERNELS: CUDA events around each batch's kernels (counters) */
     void* stream; /* cudaStream_t for assembly; NULL = loader-owned */
 } rfl_device_config;
 
@@ -185,6 +189,8 @@ typedef struct rfl_loader_counters {
     uint64_t peak_buffer_rows;
     uint64_t h2d_bytes;      /* bytes staged host->device (new) */
     uint64_t kernels_launched;
+    double decode_ms;        /* RFL_DEV_TIME_KERNELS: device time of the staged-record expansion */
+    double assembly_ms;      /* ... and of the batch assembly kernels, over finished batches */
 } rfl_loader_counters;
 
 typedef struct rfl_loader rfl_loader;

@@ -17,6 +17,7 @@ OK, EINVAL, ECORRUPT, EIO, ECUDA, ENCCL, END = range(7)
 LAYOUT_DENSE, LAYOUT_CSR = 0, 1
 F32, F64, I32, U8, BF16, NATIVE = 0, 1, 2, 3, 4, 255
 IDX_U32, IDX_U64 = 0, 1
+DEV_TIME_KERNELS = 1
 STAGE_RESIDENT, STAGE_STREAM_PINNED, STAGE_STREAM_FILE, STAGE_RESIDENT_CODED = 0, 1, 2, 3
 OUT_CSR, OUT_DENSE = 0, 1
 XF_NONE, XF_NORMALIZE_LOG1P = 0, 1
@@ -48,7 +49,7 @@ class rfl_loader_config(C.Structure):
 
 class rfl_device_config(C.Structure):
     _fields_ = [("output", u32), ("out_dtype", u32), ("transform", u32), ("target_sum", C.c_float),
-                ("out_slots", u32), ("reserved", u32), ("stream", vp)]
+                ("out_slots", u32), ("flags", u32), ("stream", vp)]
 
 
 class rfl_batch(C.Structure):
@@ -60,7 +61,8 @@ class rfl_batch(C.Structure):
 
 class rfl_loader_counters(C.Structure):
     _fields_ = [("blocks_fetched", u64), ("read_ops", u64), ("bytes_read", u64), ("chunks_decoded", u64),
-                ("peak_buffer_rows", u64), ("h2d_bytes", u64), ("kernels_launched", u64)]
+                ("peak_buffer_rows", u64), ("h2d_bytes", u64), ("kernels_launched", u64),
+                ("decode_ms", C.c_double), ("assembly_ms", C.c_double)]
 
 
 class rfl_rowref(C.Structure):
@@ -110,6 +112,7 @@ SIGNATURES = [
     ("rfl_batch_download", C.c_int, [C.POINTER(rfl_batch), vp, vp, vp, vp]),
     ("rfl_batch_wait", C.c_int, [C.POINTER(rfl_batch), vp]),
     ("rfl_loader_sync", C.c_int, [vp]),
+    ("rfl_dstore_bytes", C.c_int, [vp, u64p, u64p]),
     ("rfl_loader_destroy", None, [vp]),
     ("rfl_csr_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp, vp, vp, vp]),
     ("rfl_csr_gather_prefixed", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp, vp, vp, vp]),

@@ -249,6 +249,14 @@ rfl_status rfl_dstore_create(rfl_store* s, int device, uint32_t staging, rfl_dst
     });
 }
 
+rfl_status rfl_dstore_bytes(const rfl_dstore* d, uint64_t* record_bytes, uint64_t* staged_bytes) {
+    return guarded([&] {
+        if (!d) rfl::invalid("null argument");
+        if (record_bytes) *record_bytes = d->ds->image_bytes();
+        if (staged_bytes) *staged_bytes = d->ds->staged_bytes();
+    });
+}
+
 rfl_status rfl_dstore_arena(const rfl_dstore* d, void** base, const uint64_t** offs, uint64_t* n) {
     return guarded([&] {
         if (!d) rfl::invalid("null argument");
@@ -276,6 +284,7 @@ rfl_status rfl_loader_create(rfl_dstore* d, const rfl_loader_config* c, uint64_t
             dc.target_sum = dev->target_sum > 0 ? dev->target_sum : 1e4f;
             dc.out_slots = dev->out_slots ? dev->out_slots : 2;
             dc.stream = static_cast<cudaStream_t>(dev->stream);
+            dc.time_kernels = (dev->flags & RFL_DEV_TIME_KERNELS) != 0;
         } else {
             dc.output = d->ds->manifest().layout == rfl::Layout::csr ? 0 : 1;
         }
@@ -321,6 +330,8 @@ rfl_status rfl_loader_counters_get(const rfl_loader* l, rfl_loader_counters* o) 
         o->peak_buffer_rows = c.peak_buffer_rows;
         o->h2d_bytes = c.h2d_bytes;
         o->kernels_launched = c.kernels_launched;
+        o->decode_ms = c.decode_ms;
+        o->assembly_ms = c.assembly_ms;
     });
 }
 

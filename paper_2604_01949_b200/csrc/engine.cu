@@ -526,6 +526,8 @@ void OutBuffers::free_all() {
     cudaFreeHost(h_gidx);
     cudaFreeHost(h_prefix);
     if (done) cudaEventDestroy(done);
+    for (auto& e : tk)
+        if (e) cudaEventDestroy(e);
     *this = OutBuffers{};
 }
 
@@ -786,6 +788,10 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     for (auto& s : slots_) {
         s = ds_->take_out(key);
         if (!s.done) cuda_ok(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "event");
+        if (dev_.time_kernels)
+            for (auto& e : s.tk)
+                if (!e) cuda_ok(cudaEventCreate(&e), "event");
+        s.timed = false;
     }
     if (ds_->staging() != kResident) {
         live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
@@ -1008,7 +1014,10 @@ bool GpuLoader::next(BatchOut& out) {
         for (uint64_t id : consumed_) count_fetch(id);
     if (tr.on) t_stage = tr.lap();
     OutSlot& s = slots_[next_slot_++ % slots_.size()];
-    if (s.used) cuda_ok(cudaEventSynchronize(s.done), "slot reuse");  // caller's view of it expires here
+    if (s.used) {
+        cuda_ok(cudaEventSynchronize(s.done), "slot reuse");  // caller's view of it expires here
+        harvest(s);
+    }
     if (tr.on) t_slot = tr.lap();
     s.used = true;
     const uint64_t n = gidx_.size();
@@ -1052,6 +1061,8 @@ bool GpuLoader::next(BatchOut& out) {
     }
     cuda_ok(cudaEventRecord(staged_, copy_), "event");
     cuda_ok(cudaStreamWaitEvent(compute_, staged_, 0), "wait staged");
+    const bool timing = dev_.time_kernels && s.tk[0];
+    if (timing) cuda_ok(cudaEventRecord(s.tk[0], compute_), "event");
     // delta-staged records expand into idx16 records on the compute stream, so the
     // copy stream goes straight on to the next batch's blocks
     if (!d8_jobs_.empty()) {
@@ -1060,6 +1071,7 @@ bool GpuLoader::next(BatchOut& out) {
         ctr_.kernels_launched += (d8_jobs_.size() + kMaxD8Jobs - 1) / kMaxD8Jobs;
     }
 
+    if (timing) cuda_ok(cudaEventRecord(s.tk[1], compute_), "event");
     const ArenaView av = ds_->view(base);
     if (m.layout == Layout::dense) {
         launch_dense_gather(av, s.d_refs, n, dev_.out_dtype, s.data, static_cast<uint64_t*>(s.gidx), compute_);
@@ -1074,6 +1086,10 @@ bool GpuLoader::next(BatchOut& out) {
                           static_cast<uint64_t*>(s.gidx), s.scratch, compute_);
     }
     ctr_.kernels_launched += 1;
+    if (timing) {
+        cuda_ok(cudaEventRecord(s.tk[2], compute_), "event");
+        s.timed = true;
+    }
     cuda_ok(cudaEventRecord(s.done, compute_), "event");
     ++batch_seq_;
 
@@ -1114,7 +1130,20 @@ bool GpuLoader::next(BatchOut& out) {
     return true;
 }
 
+void GpuLoader::harvest(OutBuffers& s) const {
+    if (!s.timed) return;
+    float a = 0.f, b = 0.f;
+    if (cudaEventElapsedTime(&a, s.tk[0], s.tk[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, s.tk[1], s.tk[2]) == cudaSuccess) {
+        ctr_.decode_ms += a;
+        ctr_.assembly_ms += b;
+        s.timed = false;
+    }
+}
+
 Counters GpuLoader::counters() const {
+    for (auto& s : slots_)
+        if (s.timed && cudaEventQuery(s.tk[2]) == cudaSuccess) harvest(s);
     Counters c = ctr_;
     c.blocks_fetched = replay_.blocks_fetched();
     c.peak_buffer_rows = replay_.peak_buffer_rows();

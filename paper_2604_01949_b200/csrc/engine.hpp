@@ -91,6 +91,8 @@ struct OutBuffers {
     uint64_t* h_prefix = nullptr;  // CSR output: the batch indptr, planned on the host
     uint64_t cap_rows = 0, cap_nnz = 0, data_bytes = 0;
     cudaEvent_t done = nullptr;
+    cudaEvent_t tk[3] = {nullptr, nullptr, nullptr};  // time_kernels: before decode, before assembly, after
+    bool timed = false;                               // tk holds an unharvested batch
     bool used = false;
     uint32_t key = 0;  // output kind the buffers were sized for (output mode, dtype, transform)
     void free_all();
@@ -224,6 +226,7 @@ struct DeviceCfg {
     float target_sum = 1e4f;
     uint32_t out_slots = 2;
     cudaStream_t stream = nullptr;
+    bool time_kernels = false;  // CUDA events around each batch's decode / assembly kernels
 };
 
 struct BatchOut {
@@ -237,6 +240,7 @@ struct BatchOut {
 struct Counters {
     uint64_t blocks_fetched = 0, read_ops = 0, bytes_read = 0, chunks_decoded = 0, peak_buffer_rows = 0,
              h2d_bytes = 0, kernels_launched = 0;
+    double decode_ms = 0, assembly_ms = 0;  // DeviceCfg::time_kernels, finished batches
 };
 
 class GpuLoader {
@@ -246,6 +250,7 @@ public:
     bool next(BatchOut& out);  // false at end of epoch (idempotent)
     Counters counters() const;
     void sync();
+    void harvest(OutBuffers& s) const;  // fold a finished batch's kernel times into the counters
 
 private:
     using OutSlot = OutBuffers;
@@ -267,7 +272,7 @@ private:
     cudaStream_t compute_ = nullptr, copy_ = nullptr;
     bool own_compute_ = false;
     cudaEvent_t staged_ = nullptr;
-    std::vector<OutSlot> slots_;
+    mutable std::vector<OutSlot> slots_;
     uint64_t next_slot_ = 0;
     std::vector<uint64_t> gidx_, consumed_;
     std::vector<Live> live_;                 // indexed by block id (streaming)
@@ -277,7 +282,7 @@ private:
     std::vector<void*> batch_dst_, batch_src_;  // stream_pinned copies of one next(), one cudaMemcpyBatchAsync
     std::vector<D8Job> d8_jobs_;                 // delta-staged records of this next() to expand
     std::vector<size_t> batch_size_;
-    Counters ctr_;
+    mutable Counters ctr_;
     bool done_ = false;
     uint64_t batch_seq_ = 0;
     uint64_t id_ = 0;  // unique per loader (slot ownership; never reused like an address)

@@ -495,6 +495,26 @@ std::vector<Slot> read_footer(const File& f, const std::string& path, uint64_t s
 }
 
 HostStore::HostStore(std::string root) : root_(std::move(root)) {
+    if (root_.compare(0, 11, "procedural:") == 0) {
+        src_ = make_record_source(root_, man_);
+        const uint64_t nch = man_.chunk_count();
+        src_slots_.resize(nch);
+        std::vector<uint64_t> len(nch);
+        const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                for (uint64_t q = t; q < nch; q += T) len[q] = src_->record_bytes(q);
+            });
+        for (auto& th : pool) th.join();
+        uint64_t off = 0;
+        for (uint64_t q = 0; q < nch; ++q) {  // records back to back per shard, as the writer lays them out
+            if (q % man_.chunks_per_shard == 0) off = 0;
+            src_slots_[q] = {off, len[q]};
+            off += len[q];
+        }
+        return;
+    }
     const std::string mp = root_ + "/manifest.json";
     if (!path_exists(mp)) ioerr("store '" + root_ + "': no manifest found (absent or unfinished store)");
     man_ = Manifest::parse(read_text_file(mp));
@@ -511,8 +531,29 @@ const File& HostStore::fd(uint64_t shard, bool direct) const {
     return it->second;
 }
 
-uint64_t HostStore::shard_bytes(uint64_t shard) const { return fd(shard, false).size(); }
-bool HostStore::direct_ok(uint64_t shard) const { return fd(shard, true).valid(); }
+uint64_t HostStore::shard_bytes(uint64_t shard) const {
+    if (src_) {
+        const uint64_t last = std::min(man_.chunk_count(), (shard + 1) * man_.chunks_per_shard) - 1;
+        return src_slots_[last].off + src_slots_[last].len + man_.chunks_per_shard * 16 + 8;
+    }
+    return fd(shard, false).size();
+}
+bool HostStore::direct_ok(uint64_t shard) const { return !src_ && fd(shard, true).valid(); }
+
+// procedural store: bytes [off, off + n) of a shard's record area, generated
+void HostStore::gen_range(uint64_t shard, uint64_t off, uint8_t* dst, uint64_t n) const {
+    const uint64_t q_begin = shard * man_.chunks_per_shard;
+    const uint64_t q_end = std::min(man_.chunk_count(), q_begin + man_.chunks_per_shard);
+    std::vector<uint8_t> rec;
+    for (uint64_t q = q_begin; q < q_end && n; ++q) {
+        const Slot s = src_slots_[q];
+        if (s.off + s.len <= off) continue;
+        if (s.off >= off + n) break;
+        src_->record(q, rec);
+        const uint64_t a = std::max(off, s.off), b = std::min(off + n, s.off + s.len);
+        std::memcpy(dst + (a - off), rec.data() + (a - s.off), b - a);
+    }
+}
 
 uint64_t HostStore::charge_footer(uint64_t shard) const {
     std::lock_guard<std::mutex> lk(mu_);
@@ -523,6 +564,10 @@ uint64_t HostStore::charge_footer(uint64_t shard) const {
 }
 
 Slot HostStore::record_slot(uint64_t chunk) const {
+    if (src_) {
+        if (chunk >= src_slots_.size()) invalid("chunk " + std::to_string(chunk) + " out of range");
+        return src_slots_[chunk];
+    }
     const uint64_t shard = chunk / man_.chunks_per_shard;
     const File& f = fd(shard, false);
     std::vector<Slot>* foot;
@@ -547,10 +592,17 @@ Slot HostStore::record_slot(uint64_t chunk) const {
 void HostStore::read_record(uint64_t chunk, void* dst, uint64_t cap) const {
     const Slot s = record_slot(chunk);
     if (s.len > cap) invalid("read_record: buffer too small");
+    if (src_) {
+        std::vector<uint8_t> rec;
+        src_->record(chunk, rec);
+        std::memcpy(dst, rec.data(), s.len);
+        return;
+    }
     fd(chunk / man_.chunks_per_shard, false).pread_exact(s.off, dst, s.len);
 }
 
 void HostStore::read_shard_bytes(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const {
+    if (src_) return gen_range(shard, off, static_cast<uint8_t*>(dst), n);
     if (direct) {
         const File& d = fd(shard, true);
         // O_DIRECT needs 4 KiB-aligned offset/length/buffer; only used when the
@@ -565,6 +617,10 @@ void HostStore::read_shard_bytes(uint64_t shard, uint64_t off, void* dst, uint64
 }
 
 uint64_t HostStore::read_shard_span(uint64_t shard, uint64_t off, void* dst, uint64_t n, bool direct) const {
+    if (src_) {
+        gen_range(shard, off, static_cast<uint8_t*>(dst), n);
+        return 0;
+    }
     if (direct) {
         const File& d = fd(shard, true);
         if (d.valid()) {

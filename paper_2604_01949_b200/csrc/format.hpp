@@ -110,11 +110,25 @@ struct Slot {
 // ShardFooter::read (shard.cpp:18-54): magic, size, slot bounds, prefix occupancy.
 std::vector<Slot> read_footer(const File& f, const std::string& path, uint64_t slots);
 
+// ---- records generated on demand ------------------------------------------------------
+// A store that is never materialised (the bench's 240 GB BASELINE config 2 does
+// not fit the box's disk): every record is generated from its chunk id by a
+// procedural generator, byte-identical to the file the same synth config writes.
+struct RecordSource {
+    virtual ~RecordSource() = default;
+    virtual uint64_t record_bytes(uint64_t chunk) const = 0;
+    virtual void record(uint64_t chunk, std::vector<uint8_t>& out) const = 0;
+};
+// "procedural:counts?n_obs=..&n_var=..&seed=..&chunk_rows=..&chunks_per_shard=..[&value_dtype=f32|i32]"
+// (SynthCfg::counts, synth.hpp); fills the manifest (synth.cpp).
+std::shared_ptr<const RecordSource> make_record_source(const std::string& spec, Manifest& man);
+
 // ---- a finished store, host side ------------------------------------------------------
 // Thread-safe lazily-opened fds/footers, like StoreReader::Impl (store.cpp:301-368).
 class HostStore {
 public:
-    explicit HostStore(std::string root);
+    explicit HostStore(std::string root);  // a store directory, or a "procedural:..." spec
+    bool procedural() const { return src_ != nullptr; }
     const Manifest& manifest() const { return man_; }
     const std::string& root() const { return root_; }
     Slot record_slot(uint64_t chunk) const;  // throws CorruptStore on empty slot
@@ -144,6 +158,10 @@ private:
     mutable std::unordered_map<uint64_t, File> fds_, dfds_;
     mutable std::unordered_map<uint64_t, std::vector<Slot>> footers_;
     mutable std::vector<uint8_t> footer_charged_;
+    // procedural store: the generator and every record's (offset in its shard, length)
+    std::shared_ptr<const RecordSource> src_;
+    std::vector<Slot> src_slots_;
+    void gen_range(uint64_t shard, uint64_t off, uint8_t* dst, uint64_t n) const;
 };
 
 // ---- CSR record header accessors (store.cpp:52-64,81-122) ---------------------------

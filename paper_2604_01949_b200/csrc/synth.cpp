@@ -171,7 +171,8 @@ Manifest synth_one_hot(const std::string& path, const SynthCfg& c) {
 }
 }  // namespace
 
-Manifest synth_counts(const std::string& path, const SynthCfg& c) {
+namespace {
+Manifest counts_manifest(const SynthCfg& c) {
     if (c.layout != Layout::csr || (c.value_dtype != VDtype::f32 && c.value_dtype != VDtype::i32))
         invalid("synth: counts needs a csr store with f32 or i32 values");
     Manifest man;
@@ -184,42 +185,119 @@ Manifest synth_counts(const std::string& path, const SynthCfg& c) {
     man.codec = c.codec;
     man.var_names.reserve(c.n_var);
     for (uint64_t i = 0; i < c.n_var; ++i) man.var_names.push_back("v" + std::to_string(i));
+    man.validate();
+    return man;
+}
+uint64_t counts_row_nnz(const SynthCfg& c, uint64_t row) {
+    return std::min<uint64_t>(c.n_var, 2000 + mix64(c.seed ^ mix64(row)) % 2001);
+}
+}  // namespace
+
+// The counts record of rows [r0, r0 + rows) (encode_csr_record layout), rows
+// generated on `threads` threads (each row owns its hash stream).
+void counts_record(const SynthCfg& c, uint64_t r0, uint64_t rows, std::vector<uint8_t>& rec, unsigned threads) {
+    const size_t vs = value_size(c.value_dtype);
+    std::vector<uint64_t> indptr(rows + 1, 0);
+    for (uint64_t i = 0; i < rows; ++i) indptr[i + 1] = indptr[i] + counts_row_nnz(c, r0 + i);
+    std::vector<uint64_t> indices(indptr[rows]);
+    std::vector<uint8_t> data(indptr[rows] * vs);
+    auto gen = [&](unsigned t, unsigned T) {
+        for (uint64_t i = t; i < rows; i += T) {
+            const uint64_t h = mix64(c.seed ^ mix64(r0 + i)), n = indptr[i + 1] - indptr[i];
+            for (uint64_t k = 0; k < n; ++k) {
+                const uint64_t lo = k * c.n_var / n, hi = (k + 1) * c.n_var / n;  // stratum
+                indices[indptr[i] + k] = lo + mix64(h ^ k) % (hi - lo);
+                const uint32_t cnt = 1 + static_cast<uint32_t>(mix64(h ^ (k + (1ull << 32))) % 64);
+                if (c.value_dtype == VDtype::f32) {
+                    const float f = static_cast<float>(cnt);
+                    std::memcpy(data.data() + (indptr[i] + k) * 4, &f, 4);
+                } else {
+                    std::memcpy(data.data() + (indptr[i] + k) * 4, &cnt, 4);
+                }
+            }
+        }
+    };
+    if (threads <= 1) {
+        gen(0, 1);
+    } else {
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t < threads; ++t) pool.emplace_back(gen, t, threads);
+        for (auto& th : pool) th.join();
+    }
+    encode_csr_rows(indptr.data(), indices.data(), data.data(), vs, c.index_dtype, 0, rows, rec);
+}
+
+Manifest synth_counts(const std::string& path, const SynthCfg& c) {
+    const Manifest man = counts_manifest(c);
     RecordWriter w(path, man, /*defer_manifest=*/false);
     const unsigned T = c.threads ? c.threads : std::max(1u, std::thread::hardware_concurrency());
-    const size_t vs = value_size(c.value_dtype);
     std::vector<uint8_t> rec;
     for (uint64_t r0 = 0; r0 < c.n_obs; r0 += c.chunk_rows) {
         const uint64_t rows = std::min<uint64_t>(c.chunk_rows, c.n_obs - r0);
-        std::vector<uint64_t> nnz(rows);
-        for (uint64_t i = 0; i < rows; ++i)
-            nnz[i] = std::min<uint64_t>(c.n_var, 2000 + mix64(c.seed ^ mix64(r0 + i)) % 2001);
-        std::vector<uint64_t> indptr(rows + 1, 0);
-        for (uint64_t i = 0; i < rows; ++i) indptr[i + 1] = indptr[i] + nnz[i];
-        std::vector<uint64_t> indices(indptr[rows]);
-        std::vector<uint8_t> data(indptr[rows] * vs);
-        std::vector<std::thread> pool;
-        for (unsigned t = 0; t < T; ++t)
-            pool.emplace_back([&, t] {
-                for (uint64_t i = t; i < rows; i += T) {
-                    const uint64_t h = mix64(c.seed ^ mix64(r0 + i)), n = nnz[i];
-                    for (uint64_t k = 0; k < n; ++k) {
-                        const uint64_t lo = k * c.n_var / n, hi = (k + 1) * c.n_var / n;  // stratum
-                        indices[indptr[i] + k] = lo + mix64(h ^ k) % (hi - lo);
-                        const uint32_t cnt = 1 + static_cast<uint32_t>(mix64(h ^ (k + (1ull << 32))) % 64);
-                        if (c.value_dtype == VDtype::f32) {
-                            const float f = static_cast<float>(cnt);
-                            std::memcpy(data.data() + (indptr[i] + k) * 4, &f, 4);
-                        } else {
-                            std::memcpy(data.data() + (indptr[i] + k) * 4, &cnt, 4);
-                        }
-                    }
-                }
-            });
-        for (auto& th : pool) th.join();
-        encode_csr_rows(indptr.data(), indices.data(), data.data(), vs, c.index_dtype, 0, rows, rec);
+        counts_record(c, r0, rows, rec, T);
         w.append_record(rec.data(), rec.size(), rows);
     }
     return w.finish();
+}
+
+// ---- procedural record source ---------------------------------------------------
+namespace {
+class CountsSource : public RecordSource {
+public:
+    explicit CountsSource(SynthCfg c) : c_(std::move(c)) {}
+    uint64_t record_bytes(uint64_t q) const override {
+        const uint64_t r0 = q * c_.chunk_rows, rows = std::min<uint64_t>(c_.chunk_rows, c_.n_obs - r0);
+        uint64_t nnz = 0;
+        for (uint64_t i = 0; i < rows; ++i) nnz += counts_row_nnz(c_, r0 + i);
+        return kCsrHeaderBytes + (rows + 1) * index_size(c_.index_dtype) +
+               nnz * (index_size(c_.index_dtype) + value_size(c_.value_dtype));
+    }
+    void record(uint64_t q, std::vector<uint8_t>& out) const override {
+        const uint64_t r0 = q * c_.chunk_rows, rows = std::min<uint64_t>(c_.chunk_rows, c_.n_obs - r0);
+        counts_record(c_, r0, rows, out, 1);
+    }
+
+private:
+    SynthCfg c_;
+};
+
+uint64_t spec_u64(const std::string& v, const std::string& key) {
+    if (v.empty() || v.find_first_not_of("0123456789") != std::string::npos)
+        invalid("procedural store: bad value for " + key + ": '" + v + "'");
+    return std::stoull(v);
+}
+}  // namespace
+
+std::shared_ptr<const RecordSource> make_record_source(const std::string& spec, Manifest& man) {
+    // procedural:counts?n_obs=N&n_var=V&seed=S&chunk_rows=C&chunks_per_shard=P[&value_dtype=f32|i32]
+    const std::string pre = "procedural:counts";
+    if (spec.compare(0, pre.size(), pre) != 0)
+        invalid("procedural store: unknown generator in '" + spec + "' (known: procedural:counts?...)");
+    SynthCfg c;
+    c.layout = Layout::csr;
+    c.value_dtype = VDtype::f32;
+    c.index_dtype = IDtype::u32;
+    c.counts = true;
+    const size_t qm = spec.find('?');
+    std::string rest = qm == std::string::npos ? "" : spec.substr(qm + 1);
+    while (!rest.empty()) {
+        const size_t amp = rest.find('&');
+        const std::string kv = rest.substr(0, amp);
+        rest = amp == std::string::npos ? "" : rest.substr(amp + 1);
+        const size_t eq = kv.find('=');
+        const std::string k = kv.substr(0, eq), v = eq == std::string::npos ? "" : kv.substr(eq + 1);
+        if (k == "n_obs") c.n_obs = spec_u64(v, k);
+        else if (k == "n_var") c.n_var = spec_u64(v, k);
+        else if (k == "seed") c.seed = spec_u64(v, k);
+        else if (k == "chunk_rows") c.chunk_rows = spec_u64(v, k);
+        else if (k == "chunks_per_shard") c.chunks_per_shard = spec_u64(v, k);
+        else if (k == "value_dtype" && (v == "f32" || v == "i32")) c.value_dtype = v == "f32" ? VDtype::f32 : VDtype::i32;
+        else invalid("procedural store: unknown parameter '" + kv + "'");
+    }
+    if (c.n_obs == 0 || c.n_var == 0) invalid("procedural store: n_obs and n_var must be >= 1");
+    man = counts_manifest(c);
+    man.n_obs = c.n_obs;
+    return std::make_shared<CountsSource>(c);
 }
 
 Manifest synth_store(const std::string& path, const SynthCfg& c) {

@@ -34,6 +34,9 @@ struct SynthCfg {
 // synth_store (reference src/synth.cpp:60-144), byte-identical output.
 Manifest synth_store(const std::string& path, const SynthCfg& c);
 
+// The counts store's record of rows [r0, r0 + rows) (SynthCfg::counts).
+void counts_record(const SynthCfg& c, uint64_t r0, uint64_t rows, std::vector<uint8_t>& rec, unsigned threads);
+
 // encode_csr_record (store.cpp:52-64) of rows [r0, r1) of an in-memory CSR.
 void encode_csr_rows(const uint64_t* indptr, const uint64_t* indices, const uint8_t* data, size_t vs, IDtype idt,
                      uint64_t r0, uint64_t r1, std::vector<uint8_t>& rec);

@@ -187,6 +187,8 @@ class LoaderCounters:
     peak_buffer_rows: int = 0
     h2d_bytes: int = 0
     kernels_launched: int = 0
+    decode_ms: float = 0.0    # time_kernels=True: device time of the staged-record expansion
+    assembly_ms: float = 0.0  # ... and of the batch assembly kernels (finished batches)
 
 
 class BatchIterator:
@@ -199,7 +201,8 @@ class BatchIterator:
 
     def __init__(self, store, config: LoaderConfig, epoch_index: int = 0, *, device: int = 0,
                  staging: str = "resident", output: str | None = None, out_dtype: str = "native",
-                 transform: str | None = None, target_sum: float = 1e4, out_slots: int = 2, stream=None):
+                 transform: str | None = None, target_sum: float = 1e4, out_slots: int = 2, stream=None,
+                 time_kernels: bool = False):
         if isinstance(store, DeviceStore):
             self.dstore = store
         else:
@@ -214,7 +217,7 @@ class BatchIterator:
         self.config = config
         dc = L.rfl_device_config(L.OUT_CSR if output == "csr" else L.OUT_DENSE, OUT_DTYPES[out_dtype],
                                  L.XF_NORMALIZE_LOG1P if transform == "normalize_log1p" else L.XF_NONE,
-                                 float(target_sum), out_slots, 0,
+                                 float(target_sum), out_slots, L.DEV_TIME_KERNELS if time_kernels else 0,
                                  stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or None))
         if transform not in (None, "normalize_log1p"):
             raise L.InvalidArgument(f"unknown transform {transform!r}")
@@ -264,7 +267,7 @@ class BatchIterator:
         if b.dtype == L.BF16:
             import torch
             data = data.view(torch.bfloat16)
-        return DeviceBatch(b.epoch_index, b.batch_index, n, b.n_var, "dense", g, gh, data=data,
+        return DeviceBatch(b.epoch_index, b.batch_index, n, b.n_var, "dense", g, gh, data=data, nnz=b.nnz,
                            dtype=str(b.dtype), _ready_event=b.ready_event or 0)
 
     def __iter__(self):
@@ -275,7 +278,7 @@ class BatchIterator:
         c = L.rfl_loader_counters()
         L.check(L.lib().rfl_loader_counters_get(self._h, C.byref(c)))
         return LoaderCounters(c.blocks_fetched, c.read_ops, c.bytes_read, c.chunks_decoded, c.peak_buffer_rows,
-                              c.h2d_bytes, c.kernels_launched)
+                              c.h2d_bytes, c.kernels_launched, c.decode_ms, c.assembly_ms)
 
     def peak_buffer_rows(self) -> int:
         return self.counters().peak_buffer_rows

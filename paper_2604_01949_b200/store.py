@@ -125,6 +125,12 @@ class DeviceStore:
     def manifest(self) -> StoreManifest:
         return self.reader.manifest()
 
+    def image_bytes(self):
+        """(decoded record bytes of the store, bytes of its re-encoded staging image or 0)."""
+        r, s = C.c_uint64(), C.c_uint64()
+        L.check(L.lib().rfl_dstore_bytes(self._h, C.byref(r), C.byref(s)))
+        return r.value, s.value
+
     def arena(self):
         """(device base pointer, per-chunk record offsets) of a resident image."""
         base, offs, n = L.vp(), L.u64p(), C.c_uint64()

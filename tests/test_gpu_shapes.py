@@ -87,7 +87,7 @@ def test_cfg1_epoch_vs_reference(stores, staging, output):
     it.close()
 
 
-@pytest.mark.parametrize("staging", ["stream_pinned", "resident", "stream_file"])
+@pytest.mark.parametrize("staging", ["stream_pinned", "resident", "stream_file", "resident_coded"])
 def test_cfg2_counts_vs_reference(stores, staging):
     s = SHAPES["cfg2"]
     for output, key in (("csr", "csr_fnv"), ("dense", "dense_fnv")):
@@ -112,7 +112,7 @@ def _normalize_expect(ip, ix, dv, g):
     return eip, eix, edv, nnz, np.log1p(edv.astype(np.float64) * scale)
 
 
-@pytest.mark.parametrize("staging", ["resident", "stream_pinned"])
+@pytest.mark.parametrize("staging", ["resident", "stream_pinned", "resident_coded"])
 def test_cfg2_normalize_log1p(stores, staging):
     """Fused library-size normalisation (fp64 row sums, T=1e4) + log1p at width 36,000."""
     s = SHAPES["cfg2"]
@@ -174,7 +174,7 @@ def test_cfg3_dense_u8_and_bf16_vs_reference(stores, staging):
         it.close()
 
 
-@pytest.mark.parametrize("staging", ["resident", "stream_pinned", "stream_file"])
+@pytest.mark.parametrize("staging", ["resident", "stream_pinned", "stream_file", "resident_coded"])
 def test_cfg4_one_hot_vs_reference(stores, staging):
     s = SHAPES["cfg4"]
     ds = R.DeviceStore(stores["cfg4"], 0, staging)
@@ -261,3 +261,33 @@ def test_read_rows_csr_golden_through_gather(golden, golden_stores):
         assert int(ip[-1]) == nnz
         assert hex(fnv([ip, ix, dv])) == case["fnv"], case
         ds.close()
+
+
+@pytest.mark.parametrize("staging", ["resident_coded", "stream_pinned", "stream_file"])
+def test_cfg2_procedural_source_vs_reference(staging):
+    """The never-materialised record source bench.py uses for config 2 at 10M
+    cells: the same generator config as the golden cfg2 store, addressed as
+    "procedural:counts?...", gives the reference's batches."""
+    s = SHAPES["cfg2"]
+    spec = (f"procedural:counts?n_obs={s['n_obs']}&n_var={s['n_var']}&seed={s['seed']}&chunk_rows={s['chunk_rows']}"
+            f"&chunks_per_shard={s['cps']}")
+    it = R.BatchIterator(R.StoreReader(spec), _cfg(s, prefetch_depth=2), 0, staging=staging, output="csr")
+    got = []
+    for b in it:
+        m = b.to_minibatch()
+        assert hex(fnv([m.global_indices])) == s["gidx_fnv"][len(got)]
+        got.append(hex(fnv([m.block.indptr, m.block.indices, m.block.data])))
+    assert got == s["csr_fnv"]
+    _check_counters(it, s, staging)
+    it.close()
+
+
+def test_loader_kernel_timing_counters(stores):
+    """time_kernels=True: CUDA events around each batch's expansion and assembly
+    kernels accumulate into the counters (bench.py's per-kernel roofline)."""
+    s = SHAPES["cfg2"]
+    it = R.BatchIterator(stores["cfg2"], _cfg(s), 0, staging="resident_coded", output="dense", time_kernels=True)
+    n = sum(1 for _ in it)
+    it.synchronize()
+    c = it.counters()
+    assert n == len(s["rows"]) and c.assembly_ms > 0 and c.decode_ms > 0

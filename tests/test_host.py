@@ -214,3 +214,20 @@ def test_procedural_synth_matches_oracle_generator(tmp_path, kind):
     assert fa == fb
     for f in fa:
         assert (tmp_path / "a" / f).read_bytes() == (tmp_path / "b" / f).read_bytes(), f
+
+
+def test_procedural_store_matches_synth_files(tmp_path):
+    """A "procedural:counts?..." store (records generated on demand, never
+    materialised -- bench.py's 240 GB config 2) reads exactly like the files
+    synth_store writes for the same config: manifest, record slots, raw records."""
+    import paper_2604_01949_b200 as R
+    R.synth_store(tmp_path / "a", R.SynthConfig(5000, 36_000, "csr", "f32", seed=1, chunk_rows=1024,
+                                                chunks_per_shard=2, counts=True))
+    a = R.StoreReader(tmp_path / "a")
+    p = R.StoreReader("procedural:counts?n_obs=5000&n_var=36000&seed=1&chunk_rows=1024&chunks_per_shard=2")
+    assert a.manifest() == p.manifest()
+    assert all(a.read_record(q) == p.read_record(q) for q in range(a.manifest().chunk_count()))
+    with pytest.raises(R.InvalidArgument):
+        R.StoreReader("procedural:counts?n_obs=10&n_var=x")
+    with pytest.raises(R.InvalidArgument):
+        R.StoreReader("procedural:gaussian?n_obs=10&n_var=10")
