@@ -178,7 +178,9 @@ def schedule_batches(n_obs, lcfg, rank, world, need):
 
 
 def procedural_spec(W):
-    s = W["synth"]
+    s = dict(W["synth"])
+    if os.environ.get("RIFFLE_PROC_ROWS"):  # smaller runs of the same shape (diagnostics)
+        s["n_obs"] = int(os.environ["RIFFLE_PROC_ROWS"])
     return (f"procedural:counts?n_obs={s['n_obs']}&n_var={s['n_var']}&seed={s['seed']}&chunk_rows={s['chunk_rows']}"
             f"&chunks_per_shard={s['chunks_per_shard']}&value_dtype={s['value_dtype']}")
 

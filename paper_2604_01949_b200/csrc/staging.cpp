@@ -10,6 +10,7 @@
 #include <sys/mman.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <array>
 #include <atomic>
 #include <cstdlib>
@@ -219,6 +220,8 @@ bool DStore::build_staged_image(uint32_t mode) {
     const char* nv = std::getenv("RFL_NO_VALIDATE");
     const bool validate = m.layout == Layout::csr && !(nv && nv[0] == '1');
     const char* ve = std::getenv("RFL_NARROW_VALUES");
+    const char* te = std::getenv("RFL_TRACE");
+    const bool trace = te && te[0] == '1';
     const bool code_values = !(ve && ve[0] == '0');
     // virtual reservation bounding every encoding (each kind is at most the
     // verbatim record + 2 B per row + padding), committed page by page as filled
@@ -282,6 +285,9 @@ bool DStore::build_staged_image(uint32_t mode) {
                 std::memset(img + off[q] + len[q], 0, gap);
             });
             q0 = q1;
+            if (trace && (q0 == nch || q0 / 1024 != (q0 - (q1 - wpos.size())) / 1024))
+                std::fprintf(stderr, "# staging image: %llu / %llu records, %.2f GB staged\n",
+                             static_cast<unsigned long long>(q0), static_cast<unsigned long long>(nch), cursor / 1e9);
         }
     } catch (...) {
         munmap(map, bound);
@@ -299,7 +305,7 @@ bool DStore::build_staged_image(uint32_t mode) {
             munmap(img, used);
             h_image_ = nullptr;
             h_map_bytes_ = 0;
-            cuda_ok(rc, "cudaHostRegister staging image");
+            cuda_ok(rc, ("cudaHostRegister of the " + std::to_string(used) + "-byte staging image").c_str());
         }
         h_registered_ = true;
     }
