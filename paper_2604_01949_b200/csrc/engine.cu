@@ -160,7 +160,8 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
 void DStore::free_host_image() {
     if (!h_image_) return;
     if (h_map_bytes_) {
-        if (h_registered_) cudaHostUnregister(h_image_);
+        if (h_registered_)
+            for (uint64_t o = 0; o < h_map_bytes_; o += kPinPiece) cudaHostUnregister(h_image_ + o);
         munmap(h_image_, h_map_bytes_);
     } else {
         cudaFreeHost(h_image_);
@@ -868,9 +869,13 @@ void GpuLoader::stage_block(uint64_t id) {
         const uint64_t img0 = ds_->img_off()[q0];
         const uint64_t img1 = ds_->img_off()[q1] + ds_->img_len()[q1];
         uint8_t* land = d8 ? lv.slot.ptr + bytes : lv.slot.ptr;  // delta records land after the expanded area
-        batch_dst_.push_back(land);
-        batch_src_.push_back(const_cast<uint8_t*>(ds_->h_image() + img0));
-        batch_size_.push_back(img1 - img0);
+        for (uint64_t a = img0; a < img1;) {  // one copy per pinned piece the range touches
+            const uint64_t b = std::min(img1, (a / kPinPiece + 1) * kPinPiece);
+            batch_dst_.push_back(land + (a - img0));
+            batch_src_.push_back(const_cast<uint8_t*>(ds_->h_image() + a));
+            batch_size_.push_back(b - a);
+            a = b;
+        }
         if (d8) {
             for (uint64_t q = q0; q <= q1; ++q)
                 d8_jobs_.push_back({land + (ds_->img_off()[q] - img0), lv.slot.ptr + lv.chunk_off[q - q0],

@@ -28,6 +28,9 @@ namespace rfl {
 // for 16-B over-reads.
 constexpr uint64_t kRecAlign = 16;
 constexpr uint64_t kRecPad = 256;
+// Staging images are page-locked in pieces of this size (one registration per
+// piece, staging.cpp); a host->device copy never crosses a piece boundary.
+constexpr uint64_t kPinPiece = 1ull << 30;
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 // resident: verbatim records in HBM; stream_pinned: staging image in pinned host

@@ -300,12 +300,19 @@ bool DStore::build_staged_image(uint32_t mode) {
     h_map_bytes_ = used;
     h_image_ = img;
     if (staging_ == kStreamPinned) {
-        const cudaError_t rc = cudaHostRegister(img, used, cudaHostRegisterPortable);
-        if (rc != cudaSuccess) {
-            munmap(img, used);
-            h_image_ = nullptr;
-            h_map_bytes_ = 0;
-            cuda_ok(rc, ("cudaHostRegister of the " + std::to_string(used) + "-byte staging image").c_str());
+        // page-locked in kPinPiece pieces: one cudaHostRegister of the whole
+        // multi-GB range fails on the B200 boxes ("OS call failed") while every
+        // 1 GiB piece of it registers; copies never cross a piece boundary
+        // (stage_block splits them), so the pieces behave as one pinned image
+        for (uint64_t o = 0; o < used; o += kPinPiece) {
+            const cudaError_t rc = cudaHostRegister(img + o, std::min(kPinPiece, used - o), cudaHostRegisterPortable);
+            if (rc != cudaSuccess) {
+                for (uint64_t u = 0; u < o; u += kPinPiece) cudaHostUnregister(img + u);
+                munmap(img, used);
+                h_image_ = nullptr;
+                h_map_bytes_ = 0;
+                cuda_ok(rc, ("cudaHostRegister of the staging image at byte " + std::to_string(o)).c_str());
+            }
         }
         h_registered_ = true;
     }
