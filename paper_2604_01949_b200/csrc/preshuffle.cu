@@ -164,13 +164,20 @@ private:
     using Segs = std::vector<std::pair<uint32_t, std::pair<uint64_t, uint64_t>>>;
     void round_segments(uint64_t r, Segs& segs, std::vector<std::pair<uint32_t, uint64_t>>& prov,
                         std::vector<uint32_t>* src_rank);
-    void stage_round(const Segs& segs, DevBuf& arena, std::vector<RowRef>& refs, uint64_t r);
+    // nnz (CSR, may be null): per assembly row, the row's entry count read from the
+    // staged records' indptrs on the host; cleared when a member is reprojected
+    void stage_round(const Segs& segs, DevBuf& arena, std::vector<RowRef>& refs, uint64_t r,
+                     std::vector<uint32_t>* nnz = nullptr);
     void reproject(uint32_t mi, std::vector<RowRef>& refs, const std::vector<uint64_t>& pos, DevBuf& out,
                    std::vector<uint64_t>& bad);
     void check_duplicates(uint64_t r, const std::vector<uint64_t>& bad_asm, uint64_t round_rows);
     void emit(const std::vector<RowRef>& refs, const std::vector<std::pair<uint32_t, uint64_t>>& prov, uint64_t n,
-              const std::vector<uint64_t>* out_rows);
-    void carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst);
+              const std::vector<uint64_t>* out_rows, const std::vector<uint32_t>* nnz = nullptr);
+    void carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst, const std::vector<uint32_t>* nnz = nullptr);
+    // host-planned pack (no scan kernel, no host sync): refs + exclusive nnz prefix
+    // staged through pinned buffer set `k`, then one K5 pack launch on st_
+    uint64_t planned_upload(int k, const RowRef* refs, const uint32_t* nnz, uint64_t n);
+    void harvest_timing();
     void upload_refs(const RowRef* refs, uint64_t n);
 
     ShuffleArgs a_;
@@ -204,7 +211,14 @@ private:
     bool validate_ = true;                           // RFL_NO_VALIDATE=1 skips the staged-record checks
     std::vector<uint64_t> bad_asm_;                  // assembly rows of the staged round with duplicate columns
     std::vector<RowRef> pending_;
+    std::vector<uint32_t> pend_nnz_;  // per pending row (single-GPU CSR pass, identity members)
+    bool nnz_ok_ = false;
     std::vector<std::pair<uint32_t, uint64_t>> pend_prov_;
+    // host-planned uploads: [0..1] emits (by parity), [2] carries
+    PinBuf hp_[3];
+    DevBuf dp_[3];
+    cudaEvent_t hp_ev_[3] = {nullptr, nullptr, nullptr};
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_;  // pack launches not yet added to gpu_ms
     std::vector<uint64_t> pend_out_;                 // global output row of each pending row (multi-rank)
     std::vector<uint64_t> send_start_, send_count_;  // per destination, into d_send_refs_
     std::vector<uint64_t> round_first_out_;          // first global output row of each round
@@ -238,7 +252,7 @@ void GpuShuffler::upload_refs(const RowRef* refs, uint64_t n) {
 // `arena`; fill refs[a] for every assembly row a (absolute record address, row
 // within chunk).
 void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<uint64_t, uint64_t>>>& segs,
-                              DevBuf& arena, std::vector<RowRef>& refs, uint64_t r) {
+                              DevBuf& arena, std::vector<RowRef>& refs, uint64_t r, std::vector<uint32_t>* nnz) {
     // chunks per member, in (member, chunk) order
     std::vector<std::pair<uint32_t, uint64_t>> need;
     for (const auto& s : segs) {
@@ -256,6 +270,18 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
         total = align_up(total + len[i], kAlign);
     }
     arena.ensure(std::max<uint64_t>(total, 16));
+    std::vector<std::vector<uint32_t>> need_nnz(layout_ == Layout::csr && nnz ? need.size() : 0);
+    auto row_counts = [&](size_t k, const uint8_t* rec) {  // per-row nnz from a staged record's indptr
+        if (need_nnz.empty()) return;
+        const Manifest& hm = ms_[need[k].first].hs->manifest();
+        const uint64_t rows = hm.rows_in_chunk(need[k].second);
+        const bool w4 = hm.index_dtype.value_or(IDtype::u32) == IDtype::u32;
+        std::vector<uint32_t>& v = need_nnz[k];
+        v.resize(rows);
+        const uint8_t* ip = rec + kCsrHeaderBytes;
+        for (uint64_t i = 0; i < rows; ++i)
+            v[i] = static_cast<uint32_t>(w4 ? rd32(ip + 4 * (i + 1)) - rd32(ip + 4 * i) : rd64(ip + 8 * (i + 1)) - rd64(ip + 8 * i));
+    };
     // coalesced reads of adjacent records of one shard (store.cpp:427-447)
     struct Run {
         size_t i, j;  // need[i..j)
@@ -317,6 +343,7 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
                                 }
                                 if (hm.layout == Layout::csr && !check_csr_record(hm, need[k].second, dst, len[k], nullptr))
                                     full_check_csr_record(hm, need[k].second, dst, len[k]);
+                                if (hm.layout == Layout::csr) row_counts(k, dst);
                                 rel += slen;
                             }
                             continue;
@@ -333,6 +360,8 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
                         for (size_t k = ru.i + 1; k < ru.j; ++k) rel[k - ru.i] = rel[k - ru.i - 1] + len[k - 1];
                         for (size_t k = ru.j - 1; k > ru.i; --k)
                             std::memmove(base + (off[k] - off[ru.i]), base + rel[k - ru.i], len[k]);
+                        if (hm.layout == Layout::csr)
+                            for (size_t k = ru.i; k < ru.j; ++k) row_counts(k, base + (off[k] - off[ru.i]));
                     }
                 } catch (...) {
                     errs[t] = std::current_exception();
@@ -386,6 +415,9 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
     tr_.mark(" validate", r);
     // refs per assembly row
     refs.clear();
+    if (nnz) nnz->clear();
+    bool any_remap = false;
+    for (const auto& s : segs) any_remap = any_remap || ms_[s.first].remap;
     std::vector<std::vector<uint64_t>> remap_pos(ms_.size());
     for (const auto& s : segs) {
         const Manifest& m = ms_[s.first].hs->manifest();
@@ -394,6 +426,7 @@ void GpuShuffler::stage_round(const std::vector<std::pair<uint32_t, std::pair<ui
             const size_t k = std::lower_bound(need.begin(), need.end(), std::make_pair(s.first, q)) - need.begin();
             if (ms_[s.first].remap) remap_pos[s.first].push_back(refs.size());
             refs.push_back({reinterpret_cast<uint64_t>(arena.p) + off[k], row - q * m.chunk_rows});
+            if (!need_nnz.empty() && !any_remap) nnz->push_back(need_nnz[k][row - q * m.chunk_rows]);
         }
     }
     // column reprojection of non-identity members (remap_csr_row / scatter_dense_row)
@@ -471,19 +504,76 @@ void GpuShuffler::check_duplicates(uint64_t r, const std::vector<uint64_t>& bad_
 // Write refs[0..n) as output chunk records (+ provenance records).
 // out_rows (multi-rank) gives the global output row of each ref so records land
 // in the owned chunk slots; single-GPU writes are consecutive.
+uint64_t GpuShuffler::planned_upload(int k, const RowRef* refs, const uint32_t* nnz, uint64_t n) {
+    const uint64_t rb = align_up(n * sizeof(RowRef), 16), bytes = rb + (n + 1) * 8;
+    if (hp_ev_[k]) cuda_ok(cudaEventSynchronize(hp_ev_[k]), "pinned reuse");  // its last upload has been copied
+    else cuda_ok(cudaEventCreateWithFlags(&hp_ev_[k], cudaEventDisableTiming), "event");
+    hp_[k].ensure(bytes);
+    dp_[k].ensure(bytes);
+    std::memcpy(hp_[k].p, refs, n * sizeof(RowRef));
+    uint64_t* P = reinterpret_cast<uint64_t*>(hp_[k].p + rb);
+    uint64_t acc = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        P[i] = acc;
+        acc += nnz[i];
+    }
+    P[n] = acc;
+    cuda_ok(cudaMemcpyAsync(dp_[k].p, hp_[k].p, bytes, cudaMemcpyHostToDevice, st_), "refs+prefix H2D");
+    cuda_ok(cudaEventRecord(hp_ev_[k], st_), "event");
+    res_.h2d_bytes += bytes;
+    return rb;
+}
+
+void GpuShuffler::harvest_timing() {
+    for (auto& t : timing_) {
+        float ms = 0.f;
+        cuda_ok(cudaEventSynchronize(t.second), "sync");
+        cuda_ok(cudaEventElapsedTime(&ms, t.first, t.second), "elapsed");
+        res_.gpu_ms += ms;
+        cudaEventDestroy(t.first);
+        cudaEventDestroy(t.second);
+    }
+    timing_.clear();
+}
+
 void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::pair<uint32_t, uint64_t>>& prov,
-                       uint64_t n, const std::vector<uint64_t>* out_rows) {
+                       uint64_t n, const std::vector<uint64_t>* out_rows, const std::vector<uint32_t>* nnz) {
     if (n == 0) return;
     const uint64_t cr = a_.out_chunk_rows;
     const uint64_t nq = (n + cr - 1) / cr;
     // d_out_[ob] is reused: the writer job that drained it two emits ago is done
     const int ob = static_cast<int>(emits_++ & 1u);
     if (wjob_[ob].valid()) wjob_[ob].get();
-    upload_refs(refs.data(), n);
     std::vector<uint64_t> rec_len(nq), rec_rows(nq);
     uint64_t total = 0;
     DevBuf& dout = d_out_[ob];
-    if (layout_ == Layout::csr) {
+    const bool planned = layout_ == Layout::csr && nnz != nullptr;
+    if (!planned) upload_refs(refs.data(), n);
+    if (planned) {
+        // host-planned prefix: the rows' nnz were read from the staged records' indptrs, so
+        // the record offsets are known here -- no scan kernel and no host<->device round trip
+        const uint64_t rb = planned_upload(ob, refs.data(), nnz->data(), n);
+        const uint64_t* P = reinterpret_cast<const uint64_t*>(hp_[ob].p + rb);
+        const uint64_t os = index_size(out_idt_), vs = value_size(vdt_);
+        for (uint64_t q = 0; q < nq; ++q) {
+            const uint64_t r0 = q * cr, rows = std::min(cr, n - r0), cnt = P[r0 + rows] - P[r0];
+            if (out_idt_ == IDtype::u32 && (cnt > 0xFFFFFFFFull || n_var_ > 0x100000000ull))
+                invalid("csr record: value " + std::to_string(std::max<uint64_t>(cnt, n_var_ - 1)) +
+                        " does not fit index_dtype u32");
+            rec_rows[q] = rows;
+            rec_len[q] = kCsrHeaderBytes + os * (rows + 1) + (os + vs) * cnt;
+            total += rec_len[q];
+        }
+        dout.ensure(total + total / 8);
+        cudaEvent_t ta = nullptr, tb = nullptr;
+        cuda_ok(cudaEventCreate(&ta), "event");
+        cuda_ok(cudaEventCreate(&tb), "event");
+        cuda_ok(cudaEventRecord(ta, st_), "event");
+        launch_csr_pack(absolute_view(layout_, vdt_, in_idt_, n_var_), reinterpret_cast<const RowRef*>(dp_[ob].p), n,
+                        cr, out_idt_, reinterpret_cast<const uint64_t*>(dp_[ob].p + rb), dout.p, st_);
+        cuda_ok(cudaEventRecord(tb, st_), "event");
+        timing_.emplace_back(ta, tb);
+    } else if (layout_ == Layout::csr) {
         const ArenaView av = absolute_view(layout_, vdt_, in_idt_, n_var_);
         d_prefix_.ensure((n + 1) * 8);
         d_scratch_.ensure(csr_gather_scratch_bytes(n));
@@ -628,6 +718,8 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
                     }
                 }).share();
     wjob_[ob] = last_job_;
+    res_.rows_written += n;
+    if (planned) return;  // kernel time harvested later (no host sync here)
     float ms = 0.f, ms2 = 0.f;
     cuda_ok(cudaEventSynchronize(e1_), "sync");
     if (layout_ == Layout::csr) {  // kernel time only: scan (e0..e2) + pack (e3..e1)
@@ -637,16 +729,25 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
         cuda_ok(cudaEventElapsedTime(&ms, e0_, e1_), "elapsed");
     }
     res_.gpu_ms += ms + ms2;
-    res_.rows_written += n;
 }
 
 // Materialise refs[from..) into one device record in `dst` (same encoding as
 // the inputs) and point the refs at it, so round arenas can be recycled.
-void GpuShuffler::carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst) {
+void GpuShuffler::carry(std::vector<RowRef>& refs, uint64_t from, DevBuf& dst, const std::vector<uint32_t>* nnz) {
     const uint64_t n = refs.size() - from;
     if (n == 0) return;
-    upload_refs(refs.data() + from, n);
     const ArenaView av = absolute_view(layout_, vdt_, in_idt_, n_var_);
+    if (layout_ == Layout::csr && nnz) {  // host-planned, no sync: one record of all carried rows
+        const uint64_t rb = planned_upload(2, refs.data() + from, nnz->data() + from, n);
+        const uint64_t cnt = reinterpret_cast<const uint64_t*>(hp_[2].p + rb)[n];
+        const uint64_t is = index_size(in_idt_), vs = value_size(vdt_);
+        dst.ensure(kCsrHeaderBytes + is * (n + 1) + (is + vs) * cnt);
+        launch_csr_pack(av, reinterpret_cast<const RowRef*>(dp_[2].p), n, n, in_idt_,
+                        reinterpret_cast<const uint64_t*>(dp_[2].p + rb), dst.p, st_);
+        for (uint64_t k = 0; k < n; ++k) refs[from + k] = {reinterpret_cast<uint64_t>(dst.p), k};
+        return;
+    }
+    upload_refs(refs.data() + from, n);
     if (layout_ == Layout::csr) {
         d_prefix_.ensure((n + 1) * 8);
         d_scratch_.ensure(csr_gather_scratch_bytes(n));
@@ -672,6 +773,13 @@ GpuShuffler::~GpuShuffler() {
         if (last_job_.valid()) last_job_.wait();
     } catch (...) {
     }
+    if (st_) cudaStreamSynchronize(st_);
+    for (auto& t : timing_) {
+        cudaEventDestroy(t.first);
+        cudaEventDestroy(t.second);
+    }
+    for (auto& e : hp_ev_)
+        if (e) cudaEventDestroy(e);
     if (wst_) {
         cudaStreamSynchronize(wst_);
         for (int k = 0; k < 2; ++k) {
@@ -822,6 +930,7 @@ ShuffleResult GpuShuffler::run() {
     tr.mark("init", 0);
     DeviceGuard g(a_.device);
     std::vector<RowRef> round_refs;
+    std::vector<uint32_t> round_nnz;
     Segs segs;
     std::vector<std::pair<uint32_t, uint64_t>> asm_prov;
     const uint64_t cr = a_.out_chunk_rows;
@@ -830,26 +939,33 @@ ShuffleResult GpuShuffler::run() {
         const uint64_t round_rows = asm_prov.size();
         res_.peak_resident_rows = std::max(res_.peak_resident_rows, round_rows + std::min(a_.c, round_rows));
         tr.mark("segments", r);
-        stage_round(segs, arena_[r % 2], round_refs, r);
+        stage_round(segs, arena_[r % 2], round_refs, r, &round_nnz);
         tr.mark("stage", r);
         check_duplicates(r, bad_asm_, round_rows);
         const std::vector<uint64_t> perm = round_permutation(a_.seed, r, round_rows);
+        // host-planned packing while every row's nnz is known (identity members)
+        const bool have = round_nnz.size() == round_rows && (r == 0 || nnz_ok_);
+        if (!have) pend_nnz_.clear();
+        nnz_ok_ = have;
         for (uint64_t k = 0; k < round_rows; ++k) {
             pending_.push_back(round_refs[perm[k]]);
             pend_prov_.push_back(asm_prov[perm[k]]);
+            if (have) pend_nnz_.push_back(round_nnz[perm[k]]);
         }
         tr.mark("permute", r);
         const bool last = r + 1 == plan_.rounds.size();
         const uint64_t n_emit = last ? pending_.size() : pending_.size() / cr * cr;
-        emit(pending_, pend_prov_, n_emit, nullptr);
+        emit(pending_, pend_prov_, n_emit, nullptr, nnz_ok_ ? &pend_nnz_ : nullptr);
         tr.mark("emit", r);
         pending_.erase(pending_.begin(), pending_.begin() + n_emit);
         pend_prov_.erase(pend_prov_.begin(), pend_prov_.begin() + n_emit);
-        if (!pending_.empty()) carry(pending_, 0, carry_[r % 2]);
+        if (nnz_ok_) pend_nnz_.erase(pend_nnz_.begin(), pend_nnz_.begin() + n_emit);
+        if (!pending_.empty()) carry(pending_, 0, carry_[r % 2], nnz_ok_ ? &pend_nnz_ : nullptr);
         tr.mark("carry", r);
         res_.rounds++;
     }
     drain_writes();
+    harvest_timing();
     tr.mark("drain", 0);
     out_->finish();
     prov_->finish();
@@ -1005,6 +1121,7 @@ void GpuShuffler::emit_round(uint64_t r, const uint64_t* recv_bytes) {
 
 ShuffleResult GpuShuffler::finish() {
     drain_writes();
+    harvest_timing();
     out_->finish(static_cast<int64_t>(total_));  // rank 0 writes the manifest (others: shards only)
     prov_->finish();
     if (a_.rank == 0) write_text_file(a_.out_path + "/provenance/meta.json", meta_json(a_.seed, a_.c, a_.m));
