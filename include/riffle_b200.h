@@ -42,6 +42,10 @@ enum { RFL_CODEC_NONE = 0, RFL_CODEC_DEFLATE = 1 };
 const char* rfl_last_error(void);
 const char* rfl_version(void);
 int rfl_device_count(void);
+/* cudaDeviceCanAccessPeer(device, peer) (1 also for device == peer): whether a
+ * kernel on `device` can store into memory of `peer` (the pre-shuffle's
+ * peer-write exchange); otherwise the exchange runs as an NCCL all-to-all. */
+rfl_status rfl_device_can_access_peer(int device, int peer, int* out);
 
 /* ---------------------------------------------------------------- stores --
  * StoreReader (include/riffle/store.hpp:136-170): manifest + shard footers,
@@ -315,6 +319,8 @@ typedef struct rfl_shuffle_stats {
     uint64_t h2d_bytes;
     uint64_t d2h_bytes;
     double gpu_ms;   /* device time of gather/permute/pack kernels */
+    double send_ms;  /* multi-GPU: device time of the send-side pack kernels (local + peer messages) */
+    uint64_t peer_bytes; /* multi-GPU: message bytes this rank addressed to other ranks */
 } rfl_shuffle_stats;
 
 /* run_shuffle (preshuffle.cpp:185-378) on one GPU: byte-identical output

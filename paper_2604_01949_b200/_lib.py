@@ -82,7 +82,8 @@ class rfl_shuffle_config(C.Structure):
 
 class rfl_shuffle_stats(C.Structure):
     _fields_ = [("peak_resident_rows", u64), ("rows_written", u64), ("rounds_executed", u64),
-                ("input_bytes_read", u64), ("h2d_bytes", u64), ("d2h_bytes", u64), ("gpu_ms", C.c_double)]
+                ("input_bytes_read", u64), ("h2d_bytes", u64), ("d2h_bytes", u64), ("gpu_ms", C.c_double),
+                ("send_ms", C.c_double), ("peer_bytes", u64)]
 
 
 # (name, restype, argtypes) for every symbol the header declares
@@ -111,6 +112,7 @@ SIGNATURES = [
     ("rfl_loader_counters_get", C.c_int, [vp, C.POINTER(rfl_loader_counters)]),
     ("rfl_batch_download", C.c_int, [C.POINTER(rfl_batch), vp, vp, vp, vp]),
     ("rfl_batch_wait", C.c_int, [C.POINTER(rfl_batch), vp]),
+    ("rfl_device_can_access_peer", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
     ("rfl_loader_sync", C.c_int, [vp]),
     ("rfl_dstore_bytes", C.c_int, [vp, u64p, u64p]),
     ("rfl_loader_destroy", None, [vp]),

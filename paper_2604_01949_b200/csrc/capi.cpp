@@ -121,6 +121,19 @@ int rfl_device_count(void) {
     return n;
 }
 
+rfl_status rfl_device_can_access_peer(int device, int peer, int* out) {
+    return guarded([&] {
+        if (!out) rfl::invalid("null argument");
+        if (device == peer) {
+            *out = 1;
+            return;
+        }
+        int ok = 0;
+        rfl::cuda_ok(cudaDeviceCanAccessPeer(&ok, device, peer), "cudaDeviceCanAccessPeer");
+        *out = ok;
+    });
+}
+
 // ------------------------------------------------------------------ stores --
 rfl_status rfl_store_open(const char* root, rfl_store** out) {
     return guarded([&] {
@@ -530,6 +543,8 @@ void fill_stats(const rfl::ShuffleResult& r, rfl_shuffle_stats* stats) {
     stats->h2d_bytes = r.h2d_bytes;
     stats->d2h_bytes = r.d2h_bytes;
     stats->gpu_ms = r.gpu_ms;
+    stats->send_ms = r.send_ms;
+    stats->peer_bytes = r.peer_bytes;
 }
 }  // namespace
 

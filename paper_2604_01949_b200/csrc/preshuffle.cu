@@ -221,6 +221,7 @@ private:
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_;  // pack launches not yet added to gpu_ms
     std::vector<uint64_t> pend_out_;                 // global output row of each pending row (multi-rank)
     std::vector<uint64_t> send_start_, send_count_;  // per destination, into d_send_refs_
+    std::vector<uint64_t> send_bytes_;               // per destination: message bytes of the staged round
     std::vector<uint64_t> round_first_out_;          // first global output row of each round
     std::vector<uint32_t> mine_src_;                 // per owned output row of the staged round: source rank
     std::vector<uint64_t> mine_out_;
@@ -1050,6 +1051,7 @@ void GpuShuffler::stage(uint64_t r, uint64_t* send_bytes) {
         cuda_ok(cudaStreamSynchronize(st_), "sync");
         for (uint32_t d = 0; d < W; ++d) send_bytes[d] = send_count_[d] * row_bytes_;
     }
+    send_bytes_.assign(send_bytes, send_bytes + W);
     staged_round_ = r;
 }
 
@@ -1091,6 +1093,9 @@ void GpuShuffler::send(uint64_t r, void* const* dst) {
     float ms = 0.f;
     cuda_ok(cudaEventElapsedTime(&ms, e0_, e1_), "elapsed");
     res_.gpu_ms += ms;
+    res_.send_ms += ms;
+    for (uint32_t d = 0; d < a_.world; ++d)
+        if (d != a_.rank) res_.peer_bytes += send_bytes_[d];
 }
 
 // Owner side: my rows of round r arrived as one record per source rank in my

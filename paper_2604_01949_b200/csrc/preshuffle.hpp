@@ -22,6 +22,8 @@ struct ShuffleArgs {
 struct ShuffleResult {
     uint64_t peak_resident_rows = 0, rows_written = 0, rounds = 0, input_bytes = 0, h2d_bytes = 0, d2h_bytes = 0;
     double gpu_ms = 0.0;
+    double send_ms = 0.0;     // multi-GPU send-side pack kernels
+    uint64_t peer_bytes = 0;  // message bytes addressed to other ranks
 };
 
 ShuffleResult run_shuffle_gpu(const ShuffleArgs& a);

@@ -97,21 +97,29 @@ class ShuffleRunStats:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     gpu_ms: float = 0.0
+    send_ms: float = 0.0        # multi-GPU: send-side pack kernels (peer stores in "ipc" mode)
+    peer_bytes: int = 0         # multi-GPU: message bytes addressed to other ranks
+    exchange_s: float = 0.0     # multi-GPU: wall time of the exchange phase (send .. all peers landed)
+    a2a: str = ""               # multi-GPU exchange: "ipc" (fused peer stores) or "nccl" (all-to-all)
 
 
 def _stats(st) -> ShuffleRunStats:
     return ShuffleRunStats(st.peak_resident_rows, st.rows_written, st.rounds_executed, st.input_bytes_read,
-                           st.h2d_bytes, st.d2h_bytes, st.gpu_ms)
+                           st.h2d_bytes, st.d2h_bytes, st.gpu_ms, st.send_ms, st.peer_bytes)
 
 
 def run_shuffle(inputs, plan: ShufflePlan, out_path, out_config: ShuffleOutputConfig | None = None, *,
-                device: int = 0, join: str = "outer", rank: int = 0, world: int = 1, group=None) -> ShuffleRunStats:
+                device: int = 0, join: str = "outer", rank: int = 0, world: int = 1, group=None,
+                a2a: str | None = None) -> ShuffleRunStats:
     """run_shuffle (preshuffle.cpp:185-378) with the round gather/permute/pack on the GPU.
 
     `inputs` is the ordered list of member store paths (DatasetCollection order).
     world > 1: call on every rank (one process per GPU) with an initialised
     torch.distributed group for the control plane; row payloads move between
-    GPUs through peer memory, written by the pack kernel (see _run_ranks)."""
+    GPUs through peer memory, written by the pack kernel (a2a="ipc"), or as one
+    NCCL all-to-all per round (a2a="nccl"); default (None / RFL_A2A=auto): ipc
+    when every pair of ranks' GPUs can access each other's memory, else nccl
+    (see _run_ranks)."""
     oc = out_config or ShuffleOutputConfig()
     if oc.codec not in ("none", "deflate"):
         raise L.InvalidArgument(f"unknown codec {oc.codec!r}")
@@ -126,7 +134,7 @@ def run_shuffle(inputs, plan: ShufflePlan, out_path, out_config: ShuffleOutputCo
                                -1 if oc.index_dtype is None else {"u32": 0, "u64": 1}[oc.index_dtype], device,
                                int(join == "outer"), rank, world, int(oc.codec == "deflate"))
     if world > 1:
-        return _run_ranks(arr, len(paths), str(out_path), cfg, device, rank, world, group)
+        return _run_ranks(arr, len(paths), str(out_path), cfg, device, rank, world, group, a2a)
     st = L.rfl_shuffle_stats()
     L.check(L.lib().rfl_run_shuffle(arr, len(paths), str(out_path).encode(), C.byref(cfg), C.byref(st)))
     return _stats(st)
@@ -136,20 +144,73 @@ def _a16(x: int) -> int:
     return (x + 15) // 16 * 16
 
 
-def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group) -> ShuffleRunStats:
+def _ctl_device(group):
+    import torch
+    import torch.distributed as dist
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else \
+        torch.device("cpu")
+
+
+def _all_gather_i64(vals, world, group):
+    """All-gather of a small int64 vector per rank (one collective; tensors, not pickles)."""
+    import torch
+    import torch.distributed as dist
+    dev = _ctl_device(group)
+    t = torch.tensor(vals, dtype=torch.int64, device=dev)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return np.stack([o.cpu().numpy() for o in out])
+
+
+def _ipc_capable(device, rank, world, group) -> bool:
+    """Every pair of ranks on one host, each pair of their GPUs peer-accessible
+    (cudaDeviceCanAccessPeer), agreed by all ranks."""
+    import socket
+    host = int.from_bytes(socket.gethostname().encode()[:8].ljust(8, b"\0"), "little") & ((1 << 63) - 1)
+    info = _all_gather_i64([host, device], world, group)
+    ok = 1
+    for p in range(world):
+        if int(info[p, 0]) != host:
+            ok = 0
+            break
+        flag = C.c_int()
+        if L.lib().rfl_device_can_access_peer(device, int(info[p, 1]), C.byref(flag)) != L.OK or not flag.value:
+            ok = 0
+            break
+    return bool(_all_gather_i64([ok], world, group).min())
+
+
+def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group, a2a=None) -> ShuffleRunStats:
     """One rank of the multi-GPU pre-shuffle.
 
     Data plane: block b of round r is staged by rank b mod W; each output row
-    goes to the owner of its shard (s mod W).  The K5 pack kernel of the
-    source rank encodes the rows for owner d as one CSR record and stores it
-    directly into d's receive buffer through CUDA IPC peer pointers (NVLink
-    P2P on a multi-GPU node) — gather and exchange are one kernel pass.
-    Control plane (torch.distributed, any backend): the W x W message-size
-    matrix, the receive buffers' IPC handles, and the round barriers."""
+    goes to the owner of its shard (s mod W).
+      a2a="ipc":  the K5 pack kernel of the source rank encodes the rows for
+                  owner d as one CSR record and stores it directly into d's
+                  receive buffer through CUDA IPC peer pointers (NVLink P2P on a
+                  multi-GPU node) -- gather and exchange are one kernel pass.
+      a2a="nccl": the pack kernel writes each owner's record into a local send
+                  buffer and one all-to-all(v) per round moves them
+                  (torch.distributed all_to_all_single = grouped ncclSend/ncclRecv
+                  under the nccl backend; staged through host memory under gloo).
+    Control plane (torch.distributed, any backend): per round one all-gather of
+    a small int64 vector (message sizes, receive-buffer version, IPC handle)."""
+    import os
+    import time
+
+    import torch
     import torch.distributed as dist
+
+    from .loader import cuda_tensor
     lib = L.lib()
     h = L.vp()
     nr = C.c_uint64()
+    mode = a2a or os.environ.get("RFL_A2A", "auto")
+    if mode == "auto":
+        mode = "ipc" if _ipc_capable(device, rank, world, group) else "nccl"
+    if mode not in ("ipc", "nccl"):
+        raise L.InvalidArgument(f"unknown a2a mode {mode!r}")
+    nccl = dist.get_backend(group) == "nccl"
 
     def create():
         L.check(lib.rfl_pshuf_create(arr, n_in, out_path.encode(), C.byref(cfg), C.byref(h), C.byref(nr)))
@@ -161,39 +222,83 @@ def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group) -> ShuffleR
         create()
     peers = {}  # rank -> (version, device pointer)
     version = 0
+    sbuf = None
+    exchange_s = 0.0
+    ptr, changed = L.vp(), C.c_int()
+    handle = (C.c_ubyte * 64)()
+    cap, hv = 0, []
     try:
+        if mode == "ipc":  # a first receive buffer, so every round's gather carries a valid handle
+            L.check(lib.rfl_pshuf_recv_buffer(h, 16, C.byref(ptr), handle, C.byref(changed)))
+            version, cap = 1, 16
+            hv = np.frombuffer(bytes(handle), np.int64).tolist()
         for r in range(nr.value):
             send = np.zeros(world, np.uint64)
             L.check(lib.rfl_pshuf_stage(h, r, send.ctypes.data))
-            mats = [None] * world
-            dist.all_gather_object(mats, send.tolist(), group=group)
-            mat = np.array(mats, dtype=np.uint64)  # [src, dst]
-            need = sum(_a16(int(mat[s, rank])) for s in range(world))
-            ptr, changed = L.vp(), C.c_int()
-            handle = (C.c_ubyte * 64)()
-            L.check(lib.rfl_pshuf_recv_buffer(h, max(need, 16), C.byref(ptr), handle, C.byref(changed)))
-            version += changed.value
-            infos = [None] * world
-            dist.all_gather_object(infos, (version, bytes(handle)), group=group)
-            for p in range(world):
-                if p == rank:
-                    continue
-                ver, hb = infos[p]
-                if p not in peers or peers[p][0] != ver:
-                    if p in peers:
-                        L.check(lib.rfl_ipc_close(peers[p][1], device))
-                    pp = L.vp()
-                    L.check(lib.rfl_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), device, C.byref(pp)))
-                    peers[p] = (ver, pp.value)
-            dst = (L.vp * world)()
-            for d in range(world):
-                base = ptr.value if d == rank else peers[d][1]
-                dst[d] = base + sum(_a16(int(mat[s, d])) for s in range(rank))
-            L.check(lib.rfl_pshuf_send(h, r, dst))
-            dist.barrier(group=group)  # every peer write of this round has landed
+            if mode == "ipc":
+                # one all-gather per round: message sizes + every receive buffer's capacity,
+                # version and IPC handle; a second one only when some buffer had to grow
+                infos = _all_gather_i64(send.astype(np.int64).tolist() + [cap, version] + hv, world, group)
+                mat = infos[:, :world].astype(np.uint64)  # [src, dst]
+                needs = [sum(_a16(int(mat[s, p])) for s in range(world)) for p in range(world)]
+                if any(needs[p] > int(infos[p, world]) for p in range(world)):
+                    if needs[rank] > cap:
+                        L.check(lib.rfl_pshuf_recv_buffer(h, needs[rank], C.byref(ptr), handle, C.byref(changed)))
+                        version += changed.value
+                        cap = needs[rank]
+                        hv = np.frombuffer(bytes(handle), np.int64).tolist()
+                    infos = np.concatenate([infos[:, :world + 1],
+                                            _all_gather_i64([version] + hv, world, group)], axis=1)
+                for p in range(world):
+                    if p == rank:
+                        continue
+                    ver = int(infos[p, world + 1])
+                    if p not in peers or peers[p][0] != ver:
+                        if p in peers:
+                            L.check(lib.rfl_ipc_close(peers[p][1], device))
+                        hb = infos[p, world + 2:].astype(np.int64).tobytes()
+                        pp = L.vp()
+                        L.check(lib.rfl_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), device, C.byref(pp)))
+                        peers[p] = (ver, pp.value)
+                dst = (L.vp * world)()
+                for d in range(world):
+                    base = ptr.value if d == rank else peers[d][1]
+                    dst[d] = base + sum(_a16(int(mat[s, d])) for s in range(rank))
+                t0 = time.perf_counter()
+                L.check(lib.rfl_pshuf_send(h, r, dst))
+                dist.barrier(group=group)  # every peer write of this round has landed
+                exchange_s += time.perf_counter() - t0
+            else:
+                mat = _all_gather_i64(send.astype(np.int64).tolist(), world, group).astype(np.uint64)
+                need = sum(_a16(int(mat[s, rank])) for s in range(world))
+                L.check(lib.rfl_pshuf_recv_buffer(h, max(need, 16), C.byref(ptr), None, C.byref(changed)))
+                in_splits = [_a16(int(mat[rank, d])) for d in range(world)]
+                out_splits = [_a16(int(mat[s, rank])) for s in range(world)]
+                total = sum(in_splits)
+                if sbuf is None or sbuf.numel() < max(total, 16):
+                    sbuf = torch.empty(max(total, 16) + max(total, 16) // 4, dtype=torch.uint8,
+                                       device=f"cuda:{device}")
+                dst = (L.vp * world)()
+                o = 0
+                for d in range(world):
+                    dst[d] = sbuf.data_ptr() + o
+                    o += in_splits[d]
+                t0 = time.perf_counter()
+                L.check(lib.rfl_pshuf_send(h, r, dst))  # pack into the send buffer (stream synchronised)
+                rview = cuda_tensor(ptr.value, (max(need, 16),), np.uint8, device)[:need]
+                if nccl:  # grouped ncclSend/ncclRecv over NVLink
+                    dist.all_to_all_single(rview, sbuf[:total], out_splits, in_splits, group=group)
+                    torch.cuda.current_stream(device).synchronize()
+                else:  # gloo: through host memory
+                    host_out = torch.empty(need, dtype=torch.uint8)
+                    dist.all_to_all_single(host_out, sbuf[:total].cpu(), out_splits, in_splits, group=group)
+                    rview.copy_(host_out)
+                    torch.cuda.current_stream(device).synchronize()
+                exchange_s += time.perf_counter() - t0
             recv = np.ascontiguousarray(mat[:, rank])
             L.check(lib.rfl_pshuf_emit(h, r, recv.ctypes.data))
-            dist.barrier(group=group)  # receive buffers are free again
+            if mode == "ipc":
+                dist.barrier(group=group)  # receive buffers are free again (peers write them next round)
         st = L.rfl_shuffle_stats()
         if rank != 0:
             L.check(lib.rfl_pshuf_finish(h, C.byref(st)))
@@ -201,7 +306,10 @@ def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group) -> ShuffleR
         if rank == 0:  # manifest.json + provenance/meta.json once every shard is on disk
             L.check(lib.rfl_pshuf_finish(h, C.byref(st)))
         dist.barrier(group=group)
-        return _stats(st)
+        out = _stats(st)
+        out.exchange_s = exchange_s
+        out.a2a = mode
+        return out
     finally:
         for _, (ver, p) in peers.items():
             lib.rfl_ipc_close(p, device)
