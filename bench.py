@@ -185,6 +185,53 @@ def procedural_spec(W):
             f"&chunks_per_shard={s['chunks_per_shard']}&value_dtype={s['value_dtype']}")
 
 
+def preshuffle_exchange_leg(rank, world, local, dist):
+    """N > 1 only: a short multi-GPU pre-shuffle of a config-5-shaped collection
+    (65,536 cells x 62,710 genes, ~2k nnz/cell, ~1 GB; c=64, m=16,384 -> 4 rounds;
+    out chunk 4,096 rows x 2 per shard -> 8 shards, shard s owned by rank s mod W),
+    through the public run_shuffle (exchange mode auto: fused peer stores when every
+    GPU pair is peer-accessible, else the NCCL all-to-all).  Reports the per-GPU
+    exchange rate against NVLink 5 (900 GB/s per direction) and the wall time."""
+    import shutil
+
+    import paper_2604_01949_b200 as R
+    base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
+    n = 65_536
+    path = base / "xchg_in"
+    if rank == 0 and not (path / "manifest.json").exists():
+        base.mkdir(parents=True, exist_ok=True)
+        tmp = base / f".xchg_in.{os.getpid()}"
+        R.synth_store(tmp, R.SynthConfig(**dict(CFG5["synth"], n_obs=n)))
+        os.replace(tmp, path)
+    out = base / f"xchg_out_w{world}"
+    if rank == 0:
+        shutil.rmtree(out, ignore_errors=True)
+    dist.barrier()
+    plan = R.plan_shuffle(n, 64, 16_384, 7)
+    t0 = time.perf_counter()
+    st = R.run_shuffle([path], plan, out, R.ShuffleOutputConfig(4096, 2), device=local, rank=rank, world=world,
+                       group=dist.group.WORLD)
+    wall = allreduce_max(time.perf_counter() - t0, dist)
+    # per GPU: bytes this rank sent to other ranks over the time its exchange took
+    send_s = st.send_ms / 1e3 if st.a2a == "ipc" else st.exchange_s
+    rate = st.peer_bytes / max(send_s, 1e-12) / 1e9
+    rate_min = -allreduce_max(-rate, dist)
+    exch_max = allreduce_max(st.exchange_s, dist)
+    if rank == 0:
+        shutil.rmtree(out, ignore_errors=True)
+    payload = sum(f.stat().st_size for f in (path / "shards").iterdir())
+    return {"workload": "cfg5-shaped: 65,536 cells x 62,710 genes, ~2k nnz/cell, c=64 m=16,384 (4 rounds), "
+                        "out chunk 4096 x 2 per shard (8 shards)",
+            "a2a": st.a2a, "value": payload / wall / 1e9, "unit": "GB/s (payload, files -> files, wall, max over ranks)",
+            "wall_s": wall, "exchange_s_max": exch_max, "peer_bytes_rank0": st.peer_bytes,
+            "roofline": {"bound": "nvlink", "achieved": rate_min, "peak": 900.0, "unit": "GB/s",
+                         "frac": rate_min / 900.0, "traffic": None,
+                         "peak_source": "NVLink 5 per direction per GPU (nominal)",
+                         "kernel": "k_csr_copy_tma record mode storing into peer receive buffers" if st.a2a == "ipc"
+                         else "pack into a local send buffer + NCCL all_to_all_single",
+                         "achieved_def": "min over ranks of (bytes sent to other ranks / exchange time)"}}
+
+
 def run_ours_coded(args, wl, rank, world, local, dist):
     """A workload whose verbatim records exceed HBM (cfg2 at 10M cells, 240 GB): the
     store's re-encoded staging image is resident in HBM (resident_coded, ~70 GB) and
@@ -422,6 +469,13 @@ def run_ours(args, wl, rank, world, local, dist):
         }
         if world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = cpu_baseline(path, W, threads=1)
+    if world > 1 and not args.no_exchange:
+        try:
+            xr = preshuffle_exchange_leg(rank, world, local, dist)
+        except Exception as e:  # reported, not fatal for the loader line
+            xr = {"error": f"{type(e).__name__}: {e}"}
+        if res is not None:
+            res["preshuffle_exchange"] = xr
     return res
 
 
@@ -581,7 +635,9 @@ def run_preshuffle(args, rank, world, local, dist):
     st, wall = one()
     clk.__exit__(None, None, None)
     wall_max = allreduce_max(wall, dist)
-    gpu_max = allreduce_max(st.gpu_ms, dist)
+    # device time of the round pipeline per rank: the pack kernels, plus (N > 1) the
+    # exchange phase (peer stores / all-to-all + the barrier that closes it), max over ranks
+    gpu_max = allreduce_max(st.gpu_ms + (st.exchange_s * 1e3 if world > 1 else 0.0), dist)
     if rank == 0:
         shutil.rmtree(out, ignore_errors=True)
     if rank != 0:
@@ -591,23 +647,30 @@ def run_preshuffle(args, rank, world, local, dist):
     rounds = st.rounds_executed
     # K5 (+K1) algorithmic bytes over the run: read every entry + row header once, write every
     # encoded entry + indptr once, per rank
-    alg = (nnz * 16 + man.n_obs * 2 * (16 + 8)) / world
+    # K5 algorithmic bytes over the run, per rank: read every entry (u32 id + f32 value) and
+    # write it once; per row the row ref (16 B) + its prefix entry (8 B) read, the u32
+    # indptr entry written.  N=1 runs the pack alone (host-planned prefix); the N>1
+    # send side adds the device scan's per-row reads (16 + 2 x 4 B) and prefix write (8 B)
+    per_row = 16 + 8 + 4 + (32 if world > 1 else 0)
+    alg = (nnz * 16 + man.n_obs * per_row) / world
     res = {"metric": "preshuffle GB/s", "value": payload / (gpu_max / 1e3) / 1e9, "unit": "GB/s",
            "n_gpus": world, "steps": rounds, "warmup": rounds, "ms_per_step": gpu_max / rounds,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32+f32 (bytes)",
            "data": "synthetic (product synth_store == reference synth_store bytes)",
            "config": bench_config("cfg5", world),
            "details": {"payload_GB": payload / 1e9,
-                       "value_def": "payload bytes / device time of the round kernels (scan + pack), max over ranks"},
+                       "value_def": "payload bytes / device time of the round pack kernels (N > 1: + the "
+                                    "exchange phase), max over ranks"},
            "roofline": {"bound": "hbm", "achieved": alg / (gpu_max / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                         "frac": alg / (gpu_max / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
-                        "kernel": "k_row_scan + k_csr_pack", "alg_bytes_per_launch": alg / rounds,
+                        "kernel": "k_csr_pack (record-mode TMA copy)" + (" + k_row_scan" if world > 1 else ""),
+                        "alg_bytes_per_launch": alg / rounds,
                         "avg_launch_ms": gpu_max / rounds},
            "e2e": {"value": payload / wall_max / 1e9, "unit": "GB/s", "h2d_bytes_per_step": st.h2d_bytes / rounds,
                    "d2h_bytes_per_step": st.d2h_bytes / rounds,
                    "api": "paper_2604_01949_b200.run_shuffle -> rfl_run_shuffle", "wall_s": wall_max,
                    "rows_per_s": man.n_obs / wall_max},
-           "gpu_launches": 2 * rounds, "clocks": clk.summary()}
+           "gpu_launches": (2 if world > 1 else 1) * rounds, "clocks": clk.summary()}
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_shuffle_baseline()
     return res
@@ -618,13 +681,14 @@ def cpu_shuffle_baseline():
     on a bounded subset of the same shape."""
     import shutil
 
-    import paper_2604_01949_b200 as R
     from oracle.oracle import Ref
     base = Path(os.environ.get("RIFFLE_BENCH_DIR", "/tmp/riffle_bench"))
     n = int(os.environ.get("RIFFLE_CFG5_REF_ROWS", CFG5["ref_rows"]))
     sub = base / f"cfg5_ref_{n}"
-    if not (sub / "manifest.json").exists():
-        R.synth_store(sub, R.SynthConfig(**dict(CFG5["synth"], n_obs=n)))
+    if not (sub / "manifest.json").exists():  # the reference's own synth_store (never the product)
+        s = CFG5["synth"]
+        Ref.synth(sub, n, s["n_var"], s["layout"], s["value_dtype"], s["index_dtype"], s["density"], s["seed"],
+                  s["chunk_rows"], s["chunks_per_shard"])
     rout = base / "cfg5_ref_out"
     shutil.rmtree(rout, ignore_errors=True)
     t0 = time.perf_counter()
@@ -728,6 +792,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--no-file-e2e", action="store_true", help="skip the stream_file e2e leg")
+    ap.add_argument("--no-exchange", action="store_true", help="N>1: skip the pre-shuffle exchange leg")
     ap.add_argument("--no-verbatim-e2e", action="store_true",
                     help="skip the second e2e leg with the verbatim (not re-encoded) pinned image")
     args = ap.parse_args()
