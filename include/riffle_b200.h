@@ -165,6 +165,10 @@ typedef struct rfl_device_config {
     uint32_t out_slots; /* ring of output buffers (>= 1; default 2) */
     uint32_t flags;     /* RFL_DEV_TIME_KERNELS: CUDA events around each batch's kernels (counters) */
     void* stream; /* cudaStream_t for assembly; NULL = loader-owned */
+    uint32_t batches_per_launch; /* consecutive batches replayed, staged and assembled together
+                                    (one copy batch, one decode, one assembly launch; 0 = 1);
+                                    each stays valid for out_slots further launches */
+    uint32_t reserved2;
 } rfl_device_config;
 
 typedef struct rfl_batch {
@@ -204,6 +208,9 @@ rfl_status rfl_loader_create(rfl_dstore* d, const rfl_loader_config* cfg, uint64
 /* BatchIterator::next (loader.cpp:257-306); RFL_END at end (idempotent).
  * Buffers stay valid until out_slots further calls. */
 rfl_status rfl_loader_next(rfl_loader* l, rfl_batch* out);
+/* Up to `max` further batches into out[0..*n) (*n < max only at the end of the
+ * epoch; RFL_END when none is left): one C call for several batches. */
+rfl_status rfl_loader_next_many(rfl_loader* l, rfl_batch* out, uint32_t max, uint32_t* n);
 rfl_status rfl_loader_counters_get(const rfl_loader* l, rfl_loader_counters* out);
 /* Host copy of a batch (the reference's MiniBatch, loader.hpp:35-40): waits
  * for its ready_event, then copies whichever of indptr (u64[n_rows+1]),

@@ -244,6 +244,7 @@ struct DeviceOptions {
     float target_sum = 1e4f;
     std::uint32_t out_slots = 2;
     void* stream = nullptr;  // cudaStream_t; nullptr = loader-owned
+    std::uint32_t batches_per_launch = 1;  // batches assembled per launch (see rfl_device_config)
 };
 
 /// Device image of a store, shared by the iterators over it (loader.hpp:55-57).
@@ -292,7 +293,7 @@ public:
         const Output out = opts.output.value_or(m.layout == Layout::csr ? Output::csr : Output::dense);
         rfl_device_config dc{static_cast<std::uint32_t>(out), static_cast<std::uint32_t>(opts.out_dtype),
                              static_cast<std::uint32_t>(opts.transform), opts.target_sum, opts.out_slots, 0u,
-                             opts.stream};
+                             opts.stream, opts.batches_per_launch, 0u};
         const rfl_loader_config cc = config_.c();
         rfl_loader* l = nullptr;
         check(rfl_loader_create(ds_->handle(), &cc, epoch_index, &dc, &l));

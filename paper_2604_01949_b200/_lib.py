@@ -49,7 +49,8 @@ class rfl_loader_config(C.Structure):
 
 class rfl_device_config(C.Structure):
     _fields_ = [("output", u32), ("out_dtype", u32), ("transform", u32), ("target_sum", C.c_float),
-                ("out_slots", u32), ("flags", u32), ("stream", vp)]
+                ("out_slots", u32), ("flags", u32), ("stream", vp), ("batches_per_launch", u32),
+                ("reserved2", u32)]
 
 
 class rfl_batch(C.Structure):
@@ -112,6 +113,7 @@ SIGNATURES = [
     ("rfl_loader_counters_get", C.c_int, [vp, C.POINTER(rfl_loader_counters)]),
     ("rfl_batch_download", C.c_int, [C.POINTER(rfl_batch), vp, vp, vp, vp]),
     ("rfl_batch_wait", C.c_int, [C.POINTER(rfl_batch), vp]),
+    ("rfl_loader_next_many", C.c_int, [vp, C.POINTER(rfl_batch), u32, C.POINTER(u32)]),
     ("rfl_device_can_access_peer", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
     ("rfl_loader_sync", C.c_int, [vp]),
     ("rfl_dstore_bytes", C.c_int, [vp, u64p, u64p]),

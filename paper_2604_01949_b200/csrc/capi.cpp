@@ -298,6 +298,8 @@ rfl_status rfl_loader_create(rfl_dstore* d, const rfl_loader_config* c, uint64_t
             dc.out_slots = dev->out_slots ? dev->out_slots : 2;
             dc.stream = static_cast<cudaStream_t>(dev->stream);
             dc.time_kernels = (dev->flags & RFL_DEV_TIME_KERNELS) != 0;
+            dc.group = dev->batches_per_launch ? dev->batches_per_launch : 1;
+            if (dc.group > 64) rfl::invalid("batches_per_launch must be <= 64");
         } else {
             dc.output = d->ds->manifest().layout == rfl::Layout::csr ? 0 : 1;
         }
@@ -305,31 +307,48 @@ rfl_status rfl_loader_create(rfl_dstore* d, const rfl_loader_config* c, uint64_t
     });
 }
 
+namespace {
+void to_batch(const rfl::BatchOut& b, rfl_batch* o) {
+    o->epoch_index = b.epoch;
+    o->batch_index = b.batch_index;
+    o->n_rows = b.n_rows;
+    o->nnz = b.nnz;
+    o->n_var = b.n_var;
+    o->layout = b.layout;
+    o->dtype = b.dtype;
+    o->index_dtype = b.index_dtype;
+    o->reserved = 0;
+    o->d_gidx = b.d_gidx;
+    o->d_indptr = b.d_indptr;
+    o->d_indices = b.d_indices;
+    o->d_data = b.d_data;
+    o->h_gidx = b.h_gidx;
+    o->ready_event = b.ready;
+}
+}  // namespace
+
 rfl_status rfl_loader_next(rfl_loader* l, rfl_batch* o) {
     bool more = false;
     const rfl_status st = guarded([&] {
         if (!l || !o) rfl::invalid("null argument");
         rfl::BatchOut b;
         more = l->l->next(b);
-        if (!more) return;
-        o->epoch_index = b.epoch;
-        o->batch_index = b.batch_index;
-        o->n_rows = b.n_rows;
-        o->nnz = b.nnz;
-        o->n_var = b.n_var;
-        o->layout = b.layout;
-        o->dtype = b.dtype;
-        o->index_dtype = b.index_dtype;
-        o->reserved = 0;
-        o->d_gidx = b.d_gidx;
-        o->d_indptr = b.d_indptr;
-        o->d_indices = b.d_indices;
-        o->d_data = b.d_data;
-        o->h_gidx = b.h_gidx;
-        o->ready_event = b.ready;
+        if (more) to_batch(b, o);
     });
     if (st != RFL_OK) return st;
     return more ? RFL_OK : RFL_END;
+}
+
+rfl_status rfl_loader_next_many(rfl_loader* l, rfl_batch* o, uint32_t max, uint32_t* n) {
+    uint32_t got = 0;
+    const rfl_status st = guarded([&] {
+        if (!l || !o || !n) rfl::invalid("null argument");
+        rfl::BatchOut b;
+        while (got < max && l->l->next(b)) to_batch(b, o + got++);
+        *n = got;
+    });
+    if (st != RFL_OK) return st;
+    return got ? RFL_OK : RFL_END;
 }
 
 rfl_status rfl_loader_counters_get(const rfl_loader* l, rfl_loader_counters* o) {

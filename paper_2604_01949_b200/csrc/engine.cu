@@ -804,8 +804,8 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
         // engine idles for every kernel (profiles/r1_pcie.md)
         const uint64_t nb = (m.n_obs + cfg_.f - 1) / cfg_.f;
         const uint64_t per_batch = (cfg_.b + cfg_.f - 1) / cfg_.f + 1;
-        const uint64_t want =
-            std::min<uint64_t>(nb, 6 * ((cfg_.B + cfg_.f - 1) / cfg_.f) + 32 + (dev_.out_slots + 2) * per_batch);
+        const uint64_t want = std::min<uint64_t>(
+            nb, 6 * ((cfg_.B + cfg_.f - 1) / cfg_.f) + 32 + (dev_.out_slots + 2) * per_batch * std::max<uint32_t>(1, dev_.group));
         ds_->reserve_slots(block_bytes_, std::min<uint64_t>(want, (8ull << 30) / std::max<uint64_t>(block_bytes_, 1)));
         if (ds_->staging() == kStreamFile) {
             const uint32_t threads = std::min<uint32_t>(16, std::max<uint32_t>(1, cfg_.prefetch_depth));
@@ -813,9 +813,17 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
                                                     cfg_.cache_bypass);
         }
     }
+    rq_cap_ = std::max<size_t>(8, 2 * static_cast<size_t>(std::max<uint32_t>(1, dev_.group)) + 2);
+    replay_th_ = std::thread([this] { replay_worker(); });
 }
 
 GpuLoader::~GpuLoader() {
+    {
+        std::lock_guard<std::mutex> lk(rq_mu_);
+        rq_stop_ = true;
+    }
+    rq_cv_.notify_all();
+    if (replay_th_.joinable()) replay_th_.join();
     DeviceGuard g(ds_->device());
     if (compute_) cudaStreamSynchronize(compute_);
     if (copy_) cudaStreamSynchronize(copy_);
@@ -942,9 +950,11 @@ void GpuLoader::ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz) {
         cudaFreeHost(s.h_refs);
         cudaFreeHost(s.h_gidx);
         cudaFreeHost(s.h_prefix);
-        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&s.h_prefix), (rows + 1) * 8, cudaHostAllocDefault), "pinned");
+        // CSR indptrs of a group: the group prefix (rows+1) + each later batch's own (<= rows + group)
+        const uint64_t ip = 2 * (rows + 1) + std::max<uint32_t>(1, dev_.group);
+        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&s.h_prefix), ip * 8, cudaHostAllocDefault), "pinned");
         cuda_ok(cudaMalloc(&s.gidx, rows * 8), "malloc");
-        cuda_ok(cudaMalloc(&s.indptr, (rows + 1) * 8), "malloc");
+        cuda_ok(cudaMalloc(&s.indptr, ip * 8), "malloc");
         cuda_ok(cudaMalloc(&s.scratch, csr_gather_scratch_bytes(rows)), "malloc");
         cuda_ok(cudaMalloc(reinterpret_cast<void**>(&s.d_refs), rows * sizeof(RowRef)), "malloc");
         cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&s.h_refs), rows * sizeof(RowRef), cudaHostAllocDefault),
@@ -984,16 +994,103 @@ struct NextTrace {
 };
 }  // namespace
 
+// ---- replay-ahead: the occupancy-driven schedule runs on its own thread, a few
+// batches ahead of the consumer (the host replay is the one sequential step)
+void GpuLoader::replay_worker() {
+    try {
+        for (;;) {
+            Planned p;
+            {
+                std::unique_lock<std::mutex> lk(rq_mu_);
+                rq_cv_.wait(lk, [&] { return rq_stop_ || rq_.size() < rq_cap_; });
+                if (rq_stop_) return;
+                if (!rq_free_.empty()) {
+                    p = std::move(rq_free_.back());
+                    rq_free_.pop_back();
+                }
+            }
+            const bool more = replay_.next(p.gidx, p.consumed);
+            p.batch_index = replay_.batch_index() - 1;
+            p.blocks_fetched = replay_.blocks_fetched();
+            p.peak = replay_.peak_buffer_rows();
+            {
+                std::lock_guard<std::mutex> lk(rq_mu_);
+                if (more) rq_.push_back(std::move(p));
+                else rq_end_ = true;
+            }
+            rq_cv_.notify_all();
+            if (!more) return;
+        }
+    } catch (...) {
+        {
+            std::lock_guard<std::mutex> lk(rq_mu_);
+            rq_err_ = std::current_exception();
+            rq_end_ = true;
+        }
+        rq_cv_.notify_all();
+    }
+}
+
+bool GpuLoader::pop_planned(Planned& p) {
+    std::unique_lock<std::mutex> lk(rq_mu_);
+    rq_cv_.wait(lk, [&] { return !rq_.empty() || rq_end_; });
+    if (rq_.empty()) {
+        if (rq_err_) std::rethrow_exception(rq_err_);
+        return false;
+    }
+    p = std::move(rq_.front());
+    rq_.pop_front();
+    lk.unlock();
+    rq_cv_.notify_all();
+    return true;
+}
+
 bool GpuLoader::next(BatchOut& out) {
-    if (done_) return false;
+    if (ready_pos_ >= ready_.size()) {
+        if (done_) return false;
+        if (!assemble_group()) {
+            done_ = true;
+            return false;
+        }
+    }
+    out = ready_[ready_pos_];
+    snap_blocks_ = group_[ready_pos_].blocks_fetched;
+    snap_peak_ = group_[ready_pos_].peak;
+    ++ready_pos_;
+    return true;
+}
+
+uint32_t GpuLoader::next_many(BatchOut* out, uint32_t max) {
+    uint32_t n = 0;
+    while (n < max && next(out[n])) ++n;
+    return n;
+}
+
+bool GpuLoader::assemble_group() {
     DeviceGuard g(ds_->device());
     const Manifest& m = ds_->manifest();
     NextTrace tr;
     double t_replay = 0, t_stage = 0, t_slot = 0;
-    if (!replay_.next(gidx_, consumed_)) {
-        done_ = true;
-        return false;
+    {
+        std::lock_guard<std::mutex> lk(rq_mu_);  // recycle the last group's vectors
+        for (auto& p : group_) rq_free_.push_back(std::move(p));
     }
+    group_.clear();
+    ready_.clear();
+    ready_pos_ = 0;
+    static const bool device_scan = [] {
+        const char* e = std::getenv("RFL_GATHER");
+        return e && std::string(e) == "scan";
+    }();
+    const bool planned = m.layout == Layout::csr && dev_.output == 0 && (!device_scan || ds_->view(nullptr).idx16);
+    // the device-scan CSR path writes one batch's indptr itself: one batch per launch
+    const uint32_t k = m.layout == Layout::csr && dev_.output == 0 && !planned ? 1u : std::max<uint32_t>(1, dev_.group);
+    while (group_.size() < k) {
+        Planned p;
+        if (!pop_planned(p)) break;
+        group_.push_back(std::move(p));
+    }
+    if (group_.empty()) return false;
     if (tr.on) t_replay = tr.lap();
     const bool resident = ds_->staging() == kResident;
     if (!resident) {
@@ -1002,9 +1099,11 @@ bool GpuLoader::next(BatchOut& out) {
         batch_size_.clear();
         pend_ev_ = nullptr;
         d8_jobs_.clear();
-        for (uint64_t id : consumed_) stage_block(id);  // (counts each fetch)
+        for (const Planned& p : group_)
+            for (uint64_t id : p.consumed) stage_block(id);  // (counts each fetch)
         if (pend_ev_ && cudaEventQuery(pend_ev_) != cudaSuccess)
-            cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");        if (!batch_dst_.empty()) {
+            cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");
+        if (!batch_dst_.empty()) {
             cudaMemcpyAttributes attr{};
             attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
             attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
@@ -1013,63 +1112,79 @@ bool GpuLoader::next(BatchOut& out) {
                                          &attr, &attr_idx, 1, &fail_idx, copy_),
                     "cudaMemcpyBatchAsync");
         }
-        cuda_ok(cudaEventRecord(staged_, copy_), "event");
+    } else {
+        for (const Planned& p : group_)
+            for (uint64_t id : p.consumed) count_fetch(id);
     }
-    if (resident)
-        for (uint64_t id : consumed_) count_fetch(id);
     if (tr.on) t_stage = tr.lap();
     OutSlot& s = slots_[next_slot_++ % slots_.size()];
     if (s.used) {
-        cuda_ok(cudaEventSynchronize(s.done), "slot reuse");  // caller's view of it expires here
+        cuda_ok(cudaEventSynchronize(s.done), "slot reuse");  // the callers' views of it expire here
         harvest(s);
     }
     if (tr.on) t_slot = tr.lap();
     s.used = true;
-    const uint64_t n = gidx_.size();
+    const size_t nb = group_.size();
+    group_start_.assign(nb + 1, 0);
+    for (size_t i = 0; i < nb; ++i) group_start_[i + 1] = group_start_[i] + group_[i].gidx.size();
+    const uint64_t n = group_start_[nb];
+    std::vector<uint64_t> bnnz(nb, 0);
     uint64_t nnz = 0;
     if (m.layout == Layout::csr)
-        for (uint64_t g : gidx_) nnz += ds_->row_nnz(g);
-    ensure_capacity(s, n, nnz);
-
-    // row references
-    const uint8_t* base = resident ? ds_->d_arena() : nullptr;
-    for (uint64_t i = 0; i < n; ++i) {
-        const uint64_t gr = gidx_[i];
-        const uint64_t q = gr / m.chunk_rows;
-        if (resident) {
-            s.h_refs[i] = {ds_->rec_off()[q], gr};
-        } else {
-            const Live& lv = live_[gr / cfg_.f];
-            s.h_refs[i] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
+        for (size_t i = 0; i < nb; ++i) {
+            for (uint64_t gr : group_[i].gidx) bnnz[i] += ds_->row_nnz(gr);
+            nnz += bnnz[i];
         }
-        s.h_gidx[i] = gr;
+    ensure_capacity(s, std::max<uint64_t>(n, static_cast<uint64_t>(k) * cfg_.b), nnz);
+
+    // row references of every row of the group
+    const uint8_t* base = resident ? ds_->d_arena() : nullptr;
+    for (size_t i = 0; i < nb; ++i) {
+        RowRef* hr = s.h_refs + group_start_[i];
+        uint64_t* hg = s.h_gidx + group_start_[i];
+        const std::vector<uint64_t>& gv = group_[i].gidx;
+        for (size_t j = 0; j < gv.size(); ++j) {
+            const uint64_t gr = gv[j];
+            const uint64_t q = gr / m.chunk_rows;
+            if (resident) {
+                hr[j] = {ds_->rec_off()[q], gr};
+            } else {
+                const Live& lv = live_[gr / cfg_.f];
+                hr[j] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
+            }
+            hg[j] = gr;
+        }
     }
     cuda_ok(cudaMemcpyAsync(s.d_refs, s.h_refs, n * sizeof(RowRef), cudaMemcpyHostToDevice, copy_), "refs H2D");
     ctr_.h2d_bytes += n * sizeof(RowRef);
-    // CSR output: the batch indptr is the prefix of the schedule's per-row nnz
+    // CSR output: the batch indptrs are prefixes of the schedule's per-row nnz
     // (CsrBlock::append_rows rebase, block.cpp:92-108) -- planned here, so the
-    // device runs one balanced copy kernel and no scan
-    static const bool device_scan = [] {
-        const char* e = std::getenv("RFL_GATHER");
-        return e && std::string(e) == "scan";
-    }();
-    const bool planned = m.layout == Layout::csr && dev_.output == 0 && (!device_scan || ds_->view(nullptr).idx16);
+    // device runs one balanced copy kernel and no scan.  [P: the group's prefix,
+    // n+1 entries = batch 0's indptr][batch 1's indptr][batch 2's] ...
+    std::vector<uint64_t> ip_off(nb, 0);
     if (planned) {
-        uint64_t acc = 0;
-        for (uint64_t i = 0; i < n; ++i) {
-            s.h_prefix[i] = acc;
-            acc += ds_->row_nnz(gidx_[i]);
-        }
+        uint64_t acc = 0, w = n + 1, row = 0;
+        for (size_t i = 0; i < nb; ++i)
+            for (uint64_t gr : group_[i].gidx) {
+                s.h_prefix[row++] = acc;
+                acc += ds_->row_nnz(gr);
+            }
         s.h_prefix[n] = acc;
-        cuda_ok(cudaMemcpyAsync(s.indptr, s.h_prefix, (n + 1) * 8, cudaMemcpyHostToDevice, copy_), "indptr H2D");
-        ctr_.h2d_bytes += (n + 1) * 8;
+        for (size_t i = 1; i < nb; ++i) {
+            ip_off[i] = w;
+            const uint64_t r0 = group_start_[i], rn = group_start_[i + 1] - r0, p0 = s.h_prefix[r0];
+            for (uint64_t j = 0; j <= rn; ++j) s.h_prefix[w + j] = s.h_prefix[r0 + j] - p0;
+            w += rn + 1;
+        }
+        cuda_ok(cudaMemcpyAsync(s.indptr, s.h_prefix, w * 8, cudaMemcpyHostToDevice, copy_), "indptr H2D");
+        ctr_.h2d_bytes += w * 8;
     }
     cuda_ok(cudaEventRecord(staged_, copy_), "event");
     cuda_ok(cudaStreamWaitEvent(compute_, staged_, 0), "wait staged");
     const bool timing = dev_.time_kernels && s.tk[0];
     if (timing) cuda_ok(cudaEventRecord(s.tk[0], compute_), "event");
     // delta-staged records expand into idx16 records on the compute stream, so the
-    // copy stream goes straight on to the next batch's blocks
+    // copy stream goes straight on to the next group's blocks
     if (!d8_jobs_.empty()) {
         launch_d8_decode(d8_jobs_.data(), d8_jobs_.size(), static_cast<uint32_t>(value_size(m.value_dtype)),
                          m.chunk_rows, compute_, m.n_var);
@@ -1098,40 +1213,60 @@ bool GpuLoader::next(BatchOut& out) {
     cuda_ok(cudaEventRecord(s.done, compute_), "event");
     ++batch_seq_;
 
-    // blocks whose rows are all taken go back to the pool once this batch's kernel is done
+    // blocks whose rows are all taken go back to the pool once this group's kernel is done
     if (!resident) {
-        for (uint64_t i = 0; i < n; ++i) {
-            Live& lv = live_[gidx_[i] / cfg_.f];
-            if (--lv.live_rows == 0) {
-                cuda_ok(cudaEventRecord(lv.slot.released, compute_), "event");
-                lv.slot.owner = id_;
-                lv.slot.seq = batch_seq_;
-                ds_->release_slot(lv.slot);
-                lv.slot = DStore::SlotRef{};
+        for (const Planned& p : group_)
+            for (uint64_t gr : p.gidx) {
+                Live& lv = live_[gr / cfg_.f];
+                if (--lv.live_rows == 0) {
+                    cuda_ok(cudaEventRecord(lv.slot.released, compute_), "event");
+                    lv.slot.owner = id_;
+                    lv.slot.seq = batch_seq_;
+                    ds_->release_slot(lv.slot);
+                    lv.slot = DStore::SlotRef{};
+                }
             }
-        }
     }
 
+    size_t n_blocks = 0;
+    for (const Planned& p : group_) n_blocks += p.consumed.size();
     if (tr.on)
-        std::fprintf(stderr, "# next %llu: replay %.1f us, stage %.1f us (%zu blocks), slot wait %.1f us, rest %.1f us\n",
-                     static_cast<unsigned long long>(replay_.batch_index() - 1), t_replay, t_stage, consumed_.size(),
+        std::fprintf(stderr,
+                     "# next %llu (+%zu): replay %.1f us, stage %.1f us (%zu blocks), slot wait %.1f us, rest %.1f us\n",
+                     static_cast<unsigned long long>(group_[0].batch_index), nb - 1, t_replay, t_stage, n_blocks,
                      t_slot, tr.lap());
-    out.epoch = epoch_;
-    out.batch_index = replay_.batch_index() - 1;
-    out.n_rows = n;
-    out.nnz = nnz;
-    out.n_var = m.n_var;
-    out.layout = (m.layout == Layout::csr && dev_.output == 0) ? 1u : 0u;
+    const uint32_t layout = (m.layout == Layout::csr && dev_.output == 0) ? 1u : 0u;
     const uint32_t native = static_cast<uint32_t>(m.value_dtype);
-    out.dtype = out.layout == 1 ? native
-                                : (dev_.out_dtype == OutDtype::bf16 ? 4u : dev_.out_dtype == OutDtype::f32 ? 0u : native);
-    out.index_dtype = static_cast<uint32_t>(av.idt);
-    out.d_gidx = s.gidx;
-    out.d_indptr = out.layout == 1 ? s.indptr : nullptr;
-    out.d_indices = out.layout == 1 ? s.indices : nullptr;
-    out.d_data = s.data;
-    out.h_gidx = s.h_gidx;
-    out.ready = s.done;
+    const uint32_t dtype =
+        layout == 1 ? native : (dev_.out_dtype == OutDtype::bf16 ? 4u : dev_.out_dtype == OutDtype::f32 ? 0u : native);
+    const uint64_t out_row = layout == 1 ? 0 : m.n_var * dense_out_elem_size(av, dev_.out_dtype);
+    const uint64_t is = index_size(av.idt), vs = value_size(m.value_dtype);
+    ready_.resize(nb);
+    for (size_t i = 0; i < nb; ++i) {
+        BatchOut& out = ready_[i];
+        const uint64_t r0 = group_start_[i];
+        out.epoch = epoch_;
+        out.batch_index = group_[i].batch_index;
+        out.n_rows = group_start_[i + 1] - r0;
+        out.nnz = bnnz[i];
+        out.n_var = m.n_var;
+        out.layout = layout;
+        out.dtype = dtype;
+        out.index_dtype = static_cast<uint32_t>(av.idt);
+        out.d_gidx = static_cast<uint64_t*>(s.gidx) + r0;
+        out.h_gidx = s.h_gidx + r0;
+        if (layout == 1) {
+            const uint64_t p0 = planned ? s.h_prefix[r0] : 0;
+            out.d_indptr = static_cast<uint64_t*>(s.indptr) + ip_off[i];
+            out.d_indices = static_cast<uint8_t*>(s.indices) + p0 * is;
+            out.d_data = static_cast<uint8_t*>(s.data) + p0 * vs;
+        } else {
+            out.d_indptr = nullptr;
+            out.d_indices = nullptr;
+            out.d_data = static_cast<uint8_t*>(s.data) + r0 * out_row;
+        }
+        out.ready = s.done;
+    }
     return true;
 }
 
@@ -1150,8 +1285,8 @@ Counters GpuLoader::counters() const {
     for (auto& s : slots_)
         if (s.timed && cudaEventQuery(s.tk[2]) == cudaSuccess) harvest(s);
     Counters c = ctr_;
-    c.blocks_fetched = replay_.blocks_fetched();
-    c.peak_buffer_rows = replay_.peak_buffer_rows();
+    c.blocks_fetched = snap_blocks_;  // as of the last batch handed out (the replay runs ahead)
+    c.peak_buffer_rows = snap_peak_;
     return c;
 }
 

@@ -230,6 +230,10 @@ struct DeviceCfg {
     uint32_t out_slots = 2;
     cudaStream_t stream = nullptr;
     bool time_kernels = false;  // CUDA events around each batch's decode / assembly kernels
+    // batches assembled per launch: next() replays, stages and assembles `group`
+    // consecutive batches at once (one copy batch, one refs upload, one decode and one
+    // assembly launch) into one output slot, then hands them out one per call
+    uint32_t group = 1;
 };
 
 struct BatchOut {
@@ -251,6 +255,8 @@ public:
     GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t epoch, const DeviceCfg& dev);
     ~GpuLoader();
     bool next(BatchOut& out);  // false at end of epoch (idempotent)
+    // up to `max` further batches (fewer only at the end of the epoch); 0 at the end
+    uint32_t next_many(BatchOut* out, uint32_t max);
     Counters counters() const;
     void sync();
     void harvest(OutBuffers& s) const;  // fold a finished batch's kernel times into the counters
@@ -263,6 +269,15 @@ private:
         uint64_t first_chunk = 0;
         std::vector<uint64_t> chunk_off;  // offset of each staged record inside the slot
     };
+    // one replayed batch: its rows, the blocks pulled in while it was drawn, and the
+    // replay's counters after it (the replay runs ahead on its own thread)
+    struct Planned {
+        std::vector<uint64_t> gidx, consumed;
+        uint64_t batch_index = 0, blocks_fetched = 0, peak = 0;
+    };
+    void replay_worker();
+    bool pop_planned(Planned& p);
+    bool assemble_group();  // replay -> stage -> one launch for up to dev_.group batches
     void stage_block(uint64_t block_id);
     void count_fetch(uint64_t block_id);  // the reference's IoStats for one block fetch
     void ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz);
@@ -277,7 +292,20 @@ private:
     cudaEvent_t staged_ = nullptr;
     mutable std::vector<OutSlot> slots_;
     uint64_t next_slot_ = 0;
-    std::vector<uint64_t> gidx_, consumed_;
+    std::vector<Planned> group_;             // the batches of the current output group
+    std::vector<uint64_t> group_start_;      // first row of each batch of the group
+    std::vector<BatchOut> ready_;            // assembled, not yet handed out
+    size_t ready_pos_ = 0;
+    uint64_t snap_blocks_ = 0, snap_peak_ = 0;  // replay counters after the last handed-out batch
+    // replay-ahead
+    std::thread replay_th_;
+    std::mutex rq_mu_;
+    std::condition_variable rq_cv_;
+    std::deque<Planned> rq_;
+    std::vector<Planned> rq_free_;  // recycled vectors
+    bool rq_end_ = false, rq_stop_ = false;
+    std::exception_ptr rq_err_;
+    size_t rq_cap_ = 8;
     std::vector<Live> live_;                 // indexed by block id (streaming)
     uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
     std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead

@@ -202,7 +202,7 @@ class BatchIterator:
     def __init__(self, store, config: LoaderConfig, epoch_index: int = 0, *, device: int = 0,
                  staging: str = "resident", output: str | None = None, out_dtype: str = "native",
                  transform: str | None = None, target_sum: float = 1e4, out_slots: int = 2, stream=None,
-                 time_kernels: bool = False):
+                 time_kernels: bool = False, batches_per_launch: int = 1):
         if isinstance(store, DeviceStore):
             self.dstore = store
         else:
@@ -218,7 +218,8 @@ class BatchIterator:
         dc = L.rfl_device_config(L.OUT_CSR if output == "csr" else L.OUT_DENSE, OUT_DTYPES[out_dtype],
                                  L.XF_NORMALIZE_LOG1P if transform == "normalize_log1p" else L.XF_NONE,
                                  float(target_sum), out_slots, L.DEV_TIME_KERNELS if time_kernels else 0,
-                                 stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or None))
+                                 stream.cuda_stream if hasattr(stream, "cuda_stream") else (stream or None),
+                                 int(batches_per_launch), 0)
         if transform not in (None, "normalize_log1p"):
             raise L.InvalidArgument(f"unknown transform {transform!r}")
         # stream=None: the loader assembles on its own stream, and every next() orders
@@ -231,6 +232,7 @@ class BatchIterator:
                                           C.byref(h)))
         self._h = h
         self._b = L.rfl_batch()
+        self._many = (L.rfl_batch * 1)()
         self._views = {}
 
     def _view(self, ptr, shape, np_dtype):
@@ -239,7 +241,7 @@ class BatchIterator:
         key = (ptr, shape, np_dtype)
         t = self._views.get(key)
         if t is None:
-            if len(self._views) > 64:
+            if len(self._views) > 256:
                 self._views.clear()
             t = self._views[key] = cuda_tensor(ptr, shape, np_dtype, self.device)
         return t
@@ -248,7 +250,20 @@ class BatchIterator:
         rc = L.check(L.lib().rfl_loader_next(self._h, C.byref(self._b)))
         if rc == L.END:
             return None
-        b = self._b
+        return self._wrap(self._b)
+
+    def next_many(self, k: int) -> list:
+        """Up to k further batches in one call (fewer only at the end of the epoch;
+        [] at the end).  With batches_per_launch = k they come from one launch."""
+        if len(self._many) < k:
+            self._many = (L.rfl_batch * k)()
+        n = C.c_uint32()
+        rc = L.check(L.lib().rfl_loader_next_many(self._h, self._many, k, C.byref(n)))
+        if rc == L.END:
+            return []
+        return [self._wrap(self._many[i]) for i in range(n.value)]
+
+    def _wrap(self, b) -> DeviceBatch:
         if self._own_stream:
             import torch
             L.check(L.lib().rfl_batch_wait(C.byref(b), C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))

@@ -367,3 +367,35 @@ def test_stream_file_abandoned_and_io_error(tmp_path):
         for _ in range(100):
             if it.next() is None:
                 break
+
+
+@pytest.mark.parametrize("staging", ["resident", "stream_pinned", "stream_file"])
+@pytest.mark.parametrize("group", [3, 8])
+def test_batches_per_launch(golden, golden_stores, staging, group):
+    """batches_per_launch = k: k consecutive batches replayed (ahead, on the
+    replay thread), staged, and assembled by one launch into one output slot,
+    handed out one per next() or several per next_many(): the batch stream,
+    CSR / dense contents and counters are the reference's."""
+    for ld in golden["loaders"]:
+        layout = golden["stores"][ld["store"]]["layout"]
+        outs = ["csr", "dense"] if layout == "csr" else ["dense"]
+        for out in outs:
+            it = R.BatchIterator(R.DeviceStore(golden_stores[ld["store"]], 0, staging), _cfg(ld, prefetch_depth=2),
+                                 ld["epoch"], output=out, batches_per_launch=group, out_slots=2)
+            got = []
+            while True:
+                bs = it.next_many(2) if len(got) % 2 == 0 else [b for b in [it.next()] if b is not None]
+                if not bs:
+                    break
+                got += [b.to_minibatch() for b in bs]
+            assert it.next() is None and it.next_many(4) == []
+            assert [m.global_indices.tolist() for m in got] == ld["gidx"]
+            if out == "csr":
+                assert [hex(fnv([m.block.indptr, m.block.indices, m.block.data])) for m in got] == ld["csr_fnv"]
+            else:
+                assert [hex(fnv([m.block.values])) for m in got] == ld["dense_fnv"]
+            c = it.counters()
+            assert c.blocks_fetched == ld["blocks_fetched"] and c.peak_buffer_rows == ld["peak_buffer_rows"]
+            assert (c.read_ops, c.bytes_read, c.chunks_decoded) == (ld["read_ops"], ld["bytes_read"],
+                                                                    ld["chunks_decoded"])
+            it.close()
