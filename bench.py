@@ -58,13 +58,13 @@ WORKLOADS = {
                  synth=dict(n_obs=2_000_000, n_var=12288, layout="dense", value_dtype="u8", density=0.1, seed=2,
                             chunk_rows=256, chunks_per_shard=128),
                  loader=dict(fetch_block_rows=256, buffer_capacity_rows=16384, batch_rows=1024, seed=0),
-                 out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16"),
+                 out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16", group=2, e2e_group=4),
     "cfg4": dict(desc="cfg4: dense 4x1024 one-hot u8 windows (5M, procedural one-hot: one channel per position), "
                       "chunk 512, f=512 B=16384 b=2048, raw u8",
                  synth=dict(n_obs=5_000_000, n_var=4096, layout="dense", value_dtype="u8", density=0.1, seed=3,
                             chunk_rows=512, chunks_per_shard=128, one_hot=4),
                  loader=dict(fetch_block_rows=512, buffer_capacity_rows=16384, batch_rows=2048, seed=0),
-                 out=dict(output="dense", out_dtype="native", transform=None), dtype="u8"),
+                 out=dict(output="dense", out_dtype="native", transform=None), dtype="u8", group=4, e2e_group=8),
 }
 METRIC = "cells/sec minibatch assembly"
 # config 5 (pre-shuffle) at the largest shape that is materialised per run: CSR with the
@@ -338,25 +338,35 @@ def run_ours(args, wl, rank, world, local, dist):
         refs[i, :len(g), 0] = offs[g.astype(np.int64) // man.chunk_rows]
         refs[i, :len(g), 1] = g
         rows.append(len(g))
-    d_refs = torch.from_numpy(refs.view(np.int64)).cuda()
+    # batches per launch (BatchIterator(batches_per_launch=G) does the same): G consecutive
+    # batches' rows assembled by one launch into one [G*b, n_var] output; a step is still
+    # one batch.  G divides K so that exactly K batches are timed.
+    G = max(g for g in range(1, max(1, args.batches_per_launch or W.get("group", 1)) + 1) if K % g == 0)
+    launches = [(i, 1) for i in range(Wm)] + [(Wm + j * G, G) for j in range(K // G)]
+    d_refs = []
+    for s0, g in launches:  # each launch's rows, contiguous
+        d_refs.append(torch.from_numpy(np.concatenate([refs[i, :rows[i]] for i in range(s0, s0 + g)]).view(
+            np.int64)).cuda())
     esz = {"f32": 4, "bf16": 2, "native": {"f32": 4, "f64": 8, "i32": 4, "u8": 1}[man.value_dtype]}[
         W["out"]["out_dtype"]]
-    out = torch.empty(b * man.n_var * esz + 16, dtype=torch.uint8, device="cuda")
-    gout = torch.empty(b, dtype=torch.int64, device="cuda")
+    out = torch.empty(G * b * man.n_var * esz + 16, dtype=torch.uint8, device="cuda")
+    gout = torch.empty(G * b, dtype=torch.int64, device="cuda")
     stream = torch.cuda.current_stream()
     od = {"f32": L.F32, "bf16": L.BF16, "native": L.NATIVE}[W["out"]["out_dtype"]]
     xf = L.XF_NORMALIZE_LOG1P if W["out"]["transform"] else L.XF_NONE
     lib = L.lib()
 
-    def launch(i, st=stream):
+    def launch(j, st=stream):
+        n = d_refs[j].shape[0]
         if man.layout == "csr":
-            rc = lib.rfl_csr_densify(C.byref(desc), d_refs[i].data_ptr(), rows[i], od, xf, 1e4, out.data_ptr(),
+            rc = lib.rfl_csr_densify(C.byref(desc), d_refs[j].data_ptr(), n, od, xf, 1e4, out.data_ptr(),
                                      gout.data_ptr(), C.c_void_p(st.cuda_stream))
         else:
-            rc = lib.rfl_dense_gather(C.byref(desc), d_refs[i].data_ptr(), rows[i], od, out.data_ptr(),
+            rc = lib.rfl_dense_gather(C.byref(desc), d_refs[j].data_ptr(), n, od, out.data_ptr(),
                                       gout.data_ptr(), C.c_void_p(st.cuda_stream))
         L.check(rc)
 
+    KL = K // G  # timed launches
     for i in range(Wm):
         launch(i)
     torch.cuda.synchronize()
@@ -367,18 +377,18 @@ def run_ours(args, wl, rank, world, local, dist):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, capture_error_mode="relaxed"):
             cap = torch.cuda.current_stream()
-            for k in range(K):
+            for k in range(KL):
                 launch(Wm + k, cap)
         graph.replay()  # upload + warm
         torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(KL)]
     clk = Clocks(local).__enter__()  # sampled across the value and e2e timed regions (starts with a 250 ms sleep)
     # one more untimed pass right before the timed one, so the GPU is not coming out of
     # the sampler's idle gap (clock / power-state ramp) when the clock starts
     if graph is not None:
         graph.replay()
     else:
-        for k in range(K):
+        for k in range(KL):
             launch(Wm + k)
     torch.cuda.synchronize()
     if dist:
@@ -389,7 +399,7 @@ def run_ours(args, wl, rank, world, local, dist):
         graph.replay()
         ev[-1][1].record(stream)
     else:
-        for k in range(K):
+        for k in range(KL):
             ev[k][0].record(stream)
             launch(Wm + k)
             ev[k][1].record(stream)
@@ -397,7 +407,7 @@ def run_ours(args, wl, rank, world, local, dist):
     if dist:
         dist.barrier()
     total_ms = ev[0][0].elapsed_time(ev[-1][1])
-    per = [total_ms / K] * K if graph is not None else [s.elapsed_time(e) for s, e in ev]
+    per = [total_ms / KL] * KL if graph is not None else [s.elapsed_time(e) for s, e in ev]
     cells = sum(rows[Wm:])
     max_ms = allreduce_max(total_ms, dist)
 
@@ -413,7 +423,7 @@ def run_ours(args, wl, rank, world, local, dist):
         alg = nnz_tot * (isz + vsz) + cells * (16 + 2 * isz + man.n_var * esz + 8)
     else:
         alg = cells * (16 + man.n_var * 1 + man.n_var * esz + 8)
-    alg_per_launch = alg / K
+    alg_per_launch = alg / KL
     avg_launch_s = statistics.mean(per) / 1e3
     peak, peak_src = peaks()
     achieved = alg_per_launch / avg_launch_s / 1e9
@@ -455,16 +465,17 @@ def run_ours(args, wl, rank, world, local, dist):
             "dtype": W["dtype"], "data": "synthetic (product synth_store == reference synth_store bytes)",
             "config": bench_config(wl, world),
             "details": {"staging": "resident (chunk records in HBM)",
-                        "launch": "K steps replayed as one CUDA graph" if graph is not None else "eager launches",
+                        "launch": (f"K/{G} launches ({G} batches each) replayed as one CUDA graph" if graph is not None
+                                   else "eager launches"),
                         "l2": "inputs larger than L2 (store %.2f GB, batch output %.0f MB)" % (
                             ds_bytes(reader) / 1e9, b * man.n_var * esz / 1e6),
-                        "cells_per_step_per_rank": cells / K},
+                        "cells_per_step_per_rank": cells / K, "batches_per_launch": G},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k_csr_densify" if man.layout == "csr" else "k_dense_gather",
                          "alg_bytes_per_launch": alg_per_launch, "avg_launch_ms": avg_launch_s * 1e3},
             "e2e": e2e,
-            "gpu_launches": K,
+            "gpu_launches": KL,
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -513,25 +524,33 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist, staging=None):
     depth = int(os.environ.get("RIFFLE_E2E_DEPTH", "16" if staging == "stream_file" else "4"))
     cfg = R.LoaderConfig(**W["loader"], prefetch_depth=depth, rank=rank, world=world)
 
+    # batches per launch / per call (BatchIterator(batches_per_launch=G).next_many(G)): a
+    # step is still one batch; G steps share one staging copy batch, decode and launch
+    G = max(1, args.batches_per_launch or W.get("e2e_group", 1))
+
     def make_it(e):
         return R.BatchIterator(ds, cfg, e, output=W["out"]["output"], out_dtype=W["out"]["out_dtype"],
-                               transform=W["out"]["transform"], out_slots=3, stream=stream)
+                               transform=W["out"]["transform"], out_slots=3, stream=stream, batches_per_launch=G)
 
     it = make_it(epoch)
-    host = torch.empty(W["loader"]["batch_rows"], dtype=torch.int64).pin_memory()
+    host = torch.empty(W["loader"]["batch_rows"] * G, dtype=torch.int64).pin_memory()
     h2d_done = [0]  # bytes staged by iterators already retired
     k_done = [0]    # kernels launched by iterators already retired
+    pend = []
 
     def step():
-        nonlocal it, epoch
-        b = it.next()
-        if b is None:
-            h2d_done[0] += it.counters().h2d_bytes
-            k_done[0] += it.counters().kernels_launched
-            it.close()
-            epoch += 1
-            it = make_it(epoch)
-            b = it.next()
+        nonlocal it, epoch, pend
+        if not pend:
+            pend = it.next_many(G)
+            if not pend:
+                h2d_done[0] += it.counters().h2d_bytes
+                k_done[0] += it.counters().kernels_launched
+                it.close()
+                epoch += 1
+                it = make_it(epoch)
+                pend = it.next_many(G)
+            pend.reverse()
+        b = pend.pop()
         host[:b.n_rows].copy_(b.global_indices, non_blocking=True)  # D2H of the step's result ids
         return b.n_rows
 
@@ -568,7 +587,8 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist, staging=None):
                         if staging == "stream_pinned" else
                         "stream_file (BlockReader: prefetch_depth I/O threads pread the fetch order from the shard "
                         "files into pinned buffers; blocks cudaMemcpyAsync'd per fetch)"),
-            "api": "paper_2604_01949_b200.BatchIterator.next -> rfl_loader_next",
+            "api": ("paper_2604_01949_b200.BatchIterator.next -> rfl_loader_next" if G == 1 else
+                    f"paper_2604_01949_b200.BatchIterator(batches_per_launch={G}).next_many({G}) -> rfl_loader_next_many"),
             "gpu_launches": launches,
             "open_s": open_s,  # DeviceStore open, outside the timed region: reported, not hidden
             "record_gb": rec_b / 1e9, "staging_image_gb": img_b / 1e9,
@@ -793,6 +813,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--no-file-e2e", action="store_true", help="skip the stream_file e2e leg")
     ap.add_argument("--no-exchange", action="store_true", help="N>1: skip the pre-shuffle exchange leg")
+    ap.add_argument("--batches-per-launch", type=int, default=0,
+                    help="batches assembled per launch (default: the workload's; 1 = one launch per batch)")
     ap.add_argument("--no-verbatim-e2e", action="store_true",
                     help="skip the second e2e leg with the verbatim (not re-encoded) pinned image")
     args = ap.parse_args()
