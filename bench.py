@@ -349,8 +349,12 @@ def run_ours(args, wl, rank, world, local, dist):
             np.int64)).cuda())
     esz = {"f32": 4, "bf16": 2, "native": {"f32": 4, "f64": 8, "i32": 4, "u8": 1}[man.value_dtype]}[
         W["out"]["out_dtype"]]
-    out = torch.empty(G * b * man.n_var * esz + 16, dtype=torch.uint8, device="cuda")
-    gout = torch.empty(G * b, dtype=torch.int64, device="cuda")
+    # a ring of output buffers spanning > 2 x L2 (126 MB): every launch writes its batch
+    # rows to HBM, never over the still-cached output of the previous launch
+    out_bytes = G * b * man.n_var * esz + 16
+    n_out = max(2, -(-(256 << 20) // out_bytes))
+    outs = [torch.empty(out_bytes, dtype=torch.uint8, device="cuda") for _ in range(n_out)]
+    gouts = [torch.empty(G * b, dtype=torch.int64, device="cuda") for _ in range(n_out)]
     stream = torch.cuda.current_stream()
     od = {"f32": L.F32, "bf16": L.BF16, "native": L.NATIVE}[W["out"]["out_dtype"]]
     xf = L.XF_NORMALIZE_LOG1P if W["out"]["transform"] else L.XF_NONE
@@ -358,6 +362,7 @@ def run_ours(args, wl, rank, world, local, dist):
 
     def launch(j, st=stream):
         n = d_refs[j].shape[0]
+        out, gout = outs[j % n_out], gouts[j % n_out]
         if man.layout == "csr":
             rc = lib.rfl_csr_densify(C.byref(desc), d_refs[j].data_ptr(), n, od, xf, 1e4, out.data_ptr(),
                                      gout.data_ptr(), C.c_void_p(st.cuda_stream))
@@ -467,8 +472,9 @@ def run_ours(args, wl, rank, world, local, dist):
             "details": {"staging": "resident (chunk records in HBM)",
                         "launch": (f"K/{G} launches ({G} batches each) replayed as one CUDA graph" if graph is not None
                                    else "eager launches"),
-                        "l2": "inputs larger than L2 (store %.2f GB, batch output %.0f MB)" % (
-                            ds_bytes(reader) / 1e9, b * man.n_var * esz / 1e6),
+                        "l2": "inputs larger than L2 (store %.2f GB); outputs rotate over %d buffers of %.0f MB "
+                             "(> 2 x L2), so no launch writes over the cached output of the previous one" % (
+                            ds_bytes(reader) / 1e9, n_out, out_bytes / 1e6),
                         "cells_per_step_per_rank": cells / K, "batches_per_launch": G},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -757,7 +763,8 @@ def bench_config(wl, world):
         return {"workload": CFG5["desc"], "l2": "rounds of ~1 GB of records, larger than L2",
                 "parallelism": f"{world} rank(s): rank b mod W stages block b, shard s owned by rank s mod W"}
     W = WORKLOADS[wl]
-    return {"workload": W["desc"], "l2": "inputs larger than L2 (store and per-step output exceed 126 MB)",
+    return {"workload": W["desc"], "l2": "inputs larger than L2 (the store exceeds 126 MB); the timed launches' "
+                                         "outputs rotate over buffers totalling > 2 x L2",
             "parallelism": f"dp{world} (disjoint plan positions per rank, no collective)"}
 
 

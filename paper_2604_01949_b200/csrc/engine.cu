@@ -134,7 +134,12 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     const uint64_t nch = m.chunk_count();
     rec_off_.resize(nch);
     slot_len_.resize(nch);
-    for (uint64_t q = 0; q < nch; ++q) slot_len_[q] = hs_->record_slot(q).len;
+    slot_off_.resize(nch);
+    for (uint64_t q = 0; q < nch; ++q) {
+        const Slot sl = hs_->record_slot(q);
+        slot_off_[q] = sl.off;
+        slot_len_[q] = sl.len;
+    }
     if (m.layout == Layout::csr) row_nnz_.resize(m.n_obs);
     // the image holds DECODED records: deflate stores are inflated on the host
     // (open / read-ahead threads), so every kernel reads plain records
@@ -813,6 +818,10 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
                                                     cfg_.cache_bypass);
         }
     }
+    footer_seen_.assign(m.shard_count(), 0);
+    // every output slot sized for a full group up front (first-use cudaMalloc /
+    // cudaHostAlloc would stall the first groups' steps)
+    for (auto& s : slots_) ensure_capacity(s, static_cast<uint64_t>(std::max<uint32_t>(1, dev_.group)) * cfg_.b, 0);
     rq_cap_ = std::max<size_t>(8, 2 * static_cast<size_t>(std::max<uint32_t>(1, dev_.group)) + 2);
     replay_th_ = std::thread([this] { replay_worker(); });
 }
@@ -919,17 +928,21 @@ void GpuLoader::count_fetch(uint64_t id) {
     const uint64_t s = id * cfg_.f, e = std::min(m.n_obs, s + cfg_.f);
     const uint64_t q0 = s / m.chunk_rows, q1 = (e - 1) / m.chunk_rows;
     uint64_t q = q0;
+    const std::vector<uint64_t>& so = ds_->slot_off();
     while (q <= q1) {
         const uint64_t shard = q / m.chunks_per_shard;
-        ctr_.bytes_read += hs.charge_footer(shard);
-        const Slot first = hs.record_slot(q);
+        if (!footer_seen_[shard]) {  // (the store's own charge is shared by its readers)
+            footer_seen_[shard] = 1;
+            ctr_.bytes_read += hs.charge_footer(shard);
+        }
+        const uint64_t first_off = so[q];
         uint64_t end = q + 1, run = ds_->slot_len()[q];
-        while (end <= q1 && end / m.chunks_per_shard == shard && hs.record_slot(end).off == first.off + run)
+        while (end <= q1 && end / m.chunks_per_shard == shard && so[end] == first_off + run)
             run += ds_->slot_len()[end++];
         ctr_.read_ops += 1;
         if (cfg_.cache_bypass && hs.direct_ok(shard)) {
-            const uint64_t a0 = first.off & ~4095ull;
-            const uint64_t span = HostStore::aligned_span(first.off, run);
+            const uint64_t a0 = first_off & ~4095ull;
+            const uint64_t span = HostStore::aligned_span(first_off, run);
             ctr_.bytes_read += std::min(span, hs.shard_bytes(shard) - a0);
         } else {
             ctr_.bytes_read += run;

@@ -116,6 +116,7 @@ public:
     const std::vector<uint64_t>& rec_off() const { return rec_off_; }
     const std::vector<uint64_t>& rec_len() const { return rec_len_; }    // decoded record bytes
     const std::vector<uint64_t>& slot_len() const { return slot_len_; }  // stored (encoded) bytes
+    const std::vector<uint64_t>& slot_off() const { return slot_off_; }  // file offset in its shard
     bool deflate() const { return manifest().codec == Codec::deflate; }
     // layout of the staged image (stream_pinned: possibly narrowed, see idx16()); == rec_* otherwise
     const std::vector<uint64_t>& img_off() const { return img_off_; }
@@ -165,7 +166,7 @@ private:
     std::shared_ptr<HostStore> hs_;
     int device_;
     uint32_t staging_;
-    std::vector<uint64_t> rec_off_, rec_len_, slot_len_, img_off_, img_len_;
+    std::vector<uint64_t> rec_off_, rec_len_, slot_len_, slot_off_, img_off_, img_len_;
     bool idx16_ = false, d8_ = false;
     std::vector<uint64_t> exp_len_;
     std::vector<uint8_t> d8_rec_;
@@ -306,6 +307,7 @@ private:
     bool rq_end_ = false, rq_stop_ = false;
     std::exception_ptr rq_err_;
     size_t rq_cap_ = 8;
+    std::vector<uint8_t> footer_seen_;  // shards whose footer charge this loader already applied
     std::vector<Live> live_;                 // indexed by block id (streaming)
     uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
     std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead
