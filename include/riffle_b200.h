@@ -10,7 +10,9 @@
  * rfl_last_error().  Status codes map back to the reference exception
  * hierarchy (include/riffle/error.hpp:9-32):
  *     RFL_EINVAL -> InvalidArgument, RFL_ECORRUPT -> CorruptStore,
- *     RFL_EIO -> IoError, RFL_ECUDA / RFL_ENCCL -> device failures (new).
+ *     RFL_EIO -> IoError, RFL_ECUDA / RFL_ENCCL -> device failures (new),
+ *     RFL_ENOMEM -> std::bad_alloc / cudaErrorMemoryAllocation (new: the
+ *     reference lets std::bad_alloc propagate).
  */
 #ifndef RIFFLE_B200_H
 #define RIFFLE_B200_H
@@ -30,7 +32,8 @@ enum {
     RFL_EIO = 3,
     RFL_ECUDA = 4,
     RFL_ENCCL = 5,
-    RFL_END = 6 /* end of epoch: BatchIterator::next() -> nullopt (loader.cpp:259) */
+    RFL_END = 6, /* end of epoch: BatchIterator::next() -> nullopt (loader.cpp:259) */
+    RFL_ENOMEM = 7 /* host or device allocation failed */
 };
 
 /* dtype.hpp:10-16.  RFL_BF16 is an output-only dtype (new). */
@@ -109,7 +112,11 @@ typedef struct rfl_loader_config {
     uint32_t cache_bypass; /* O_DIRECT best effort for file-streamed staging */
     uint32_t rank;
     uint32_t world;
-    uint32_t reserved;
+    /* new: 1 = every rank of `world` ends the epoch after the smallest per-rank
+     * batch count (plan positions are dealt round-robin, so ranks can differ by
+     * a batch and a DDP step per batch would hang at epoch end); 0 = each rank
+     * drains its own share (world == 1: the reference either way) */
+    uint32_t even_batches;
 } rfl_loader_config;
 
 /* LoaderConfig::validate (loader.cpp:159-168) */

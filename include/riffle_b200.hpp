@@ -22,6 +22,7 @@
 #include <cstring>
 #include <filesystem>
 #include <memory>
+#include <new>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -62,6 +63,7 @@ inline void check(rfl_status st) {
         case RFL_EINVAL: throw InvalidArgument(msg);
         case RFL_ECORRUPT: throw CorruptStore(msg);
         case RFL_EIO: throw IoError(msg);
+        case RFL_ENOMEM: throw std::bad_alloc();  // what the reference would have let propagate
         default: throw DeviceError(msg);
     }
 }
@@ -177,10 +179,11 @@ struct LoaderConfig {  // loader.hpp:12-22
     bool cache_bypass = false;
     std::uint32_t rank = 0;   // rank k of `world` takes plan positions i == k (mod world)
     std::uint32_t world = 1;  // world == 1 is exactly the reference
+    bool even_batches = false;  // new: every rank stops after the smallest per-rank batch count
 
     [[nodiscard]] rfl_loader_config c() const noexcept {
         return {fetch_block_rows, buffer_capacity_rows, batch_rows, seed, prefetch_depth,
-                drop_last ? 1u : 0u, cache_bypass ? 1u : 0u, rank, world, 0u};
+                drop_last ? 1u : 0u, cache_bypass ? 1u : 0u, rank, world, even_batches ? 1u : 0u};
     }
     void validate() const {  // loader.cpp:159-168
         const rfl_loader_config cc = c();

@@ -7,8 +7,8 @@ plan_shuffle / run_shuffle, StoreReader / synth_store.  Every call goes through
 the C-ABI of libriffle_b200.so (include/riffle_b200.h); there is no CPU
 fallback.
 """
-from ._lib import (CorruptStore, CudaError, InvalidArgument, IoError, NcclError, RiffleError,  # noqa: F401
-                   lib)
+from ._lib import (CorruptStore, CudaError, InvalidArgument, IoError, NcclError, OutOfMemory,  # noqa: F401
+                   RiffleError, lib)
 from .loader import (BatchIterator, CsrBlock, DenseBlock, DeviceBatch, EpochPlan, EpochSchedule,  # noqa: F401
                      LoaderConfig, LoaderCounters, MiniBatch, open_epoch, plan_epoch)
 from .preshuffle import (ShuffleOutputConfig, ShufflePlan, ShuffleRunStats, plan_shuffle, run_shuffle,  # noqa: F401

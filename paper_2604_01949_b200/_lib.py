@@ -13,7 +13,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libriffle_b200.so"
 
 # status codes (riffle_b200.h)
-OK, EINVAL, ECORRUPT, EIO, ECUDA, ENCCL, END = range(7)
+OK, EINVAL, ECORRUPT, EIO, ECUDA, ENCCL, END, ENOMEM = range(8)
 LAYOUT_DENSE, LAYOUT_CSR = 0, 1
 F32, F64, I32, U8, BF16, NATIVE = 0, 1, 2, 3, 4, 255
 IDX_U32, IDX_U64 = 0, 1
@@ -44,7 +44,7 @@ class rfl_synth_config(C.Structure):
 class rfl_loader_config(C.Structure):
     _fields_ = [("fetch_block_rows", u64), ("buffer_capacity_rows", u64), ("batch_rows", u64),
                 ("seed", u64), ("prefetch_depth", u32), ("drop_last", u32), ("cache_bypass", u32),
-                ("rank", u32), ("world", u32), ("out_codec", u32)]
+                ("rank", u32), ("world", u32), ("even_batches", u32)]
 
 
 class rfl_device_config(C.Structure):
@@ -182,10 +182,15 @@ class CudaError(RiffleError):
 
 
 class NcclError(RiffleError):
-    pass
+    """Collective failure on the pre-shuffle's exchange (new)."""
 
 
-_EXC = {EINVAL: InvalidArgument, ECORRUPT: CorruptStore, EIO: IoError, ECUDA: CudaError, ENCCL: NcclError}
+class OutOfMemory(RiffleError, MemoryError):
+    """Host (std::bad_alloc) or device (cudaErrorMemoryAllocation) allocation failure (new)."""
+
+
+_EXC = {EINVAL: InvalidArgument, ECORRUPT: CorruptStore, EIO: IoError, ECUDA: CudaError, ENCCL: NcclError,
+        ENOMEM: OutOfMemory}
 
 
 def check(rc: int) -> int:

@@ -30,7 +30,7 @@ rfl_status guarded(F&& f) {
         return e.code;
     } catch (const std::bad_alloc&) {
         g_err = "out of host memory";
-        return RFL_EINVAL;
+        return RFL_ENOMEM;
     } catch (const std::exception& e) {
         g_err = e.what();
         return RFL_EINVAL;
@@ -49,6 +49,7 @@ rfl::LoaderCfg to_cfg(const rfl_loader_config* c) {
     o.cache_bypass = c->cache_bypass != 0;
     o.rank = c->rank;
     o.world = c->world ? c->world : 1;
+    o.even_batches = c->even_batches != 0;
     return o;
 }
 

@@ -17,6 +17,10 @@
 namespace rfl {
 
 void cuda_ok(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // not sticky: clear it so the context stays usable
+        throw Error(kNoMem, std::string(what) + ": " + cudaGetErrorString(e));
+    }
     if (e != cudaSuccess) throw Error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
 }
 

@@ -19,7 +19,7 @@
 namespace rfl {
 
 // ---- errors (error.hpp:9-32) ------------------------------------------------
-enum Code : int { kOk = 0, kInvalid = 1, kCorrupt = 2, kIo = 3, kCuda = 4, kNccl = 5, kEnd = 6 };
+enum Code : int { kOk = 0, kInvalid = 1, kCorrupt = 2, kIo = 3, kCuda = 4, kNccl = 5, kEnd = 6, kNoMem = 7 };
 struct Error : std::runtime_error {
     int code;
     Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}

@@ -1,5 +1,6 @@
 #include "schedule.hpp"
 
+#include <algorithm>
 #include <numeric>
 #include <string>
 
@@ -35,6 +36,18 @@ EpochReplay::EpochReplay(uint64_t n_obs, const LoaderCfg& cfg, uint64_t epoch)
     smp_ = Rng(cfg.seed).stream(2 * epoch + 1);  // loader.cpp:18-19
     if (cfg.world > 1) smp_ = smp_.stream(cfg.rank);
     buf_.reserve(cfg.B + cfg.f);
+    if (cfg.even_batches && cfg.world > 1)
+        for (uint32_t k = 0; k < cfg.world; ++k)
+            max_batches_ = std::min(max_batches_, rank_batch_count(all, n_obs, cfg, k));
+}
+
+uint64_t rank_batch_count(const std::vector<uint64_t>& all_ids, uint64_t n_obs, const LoaderCfg& cfg, uint32_t rank) {
+    uint64_t rows = 0;
+    for (uint64_t i = rank; i < all_ids.size(); i += cfg.world) {
+        const uint64_t s = all_ids[i] * cfg.f;
+        rows += (s + cfg.f < n_obs ? s + cfg.f : n_obs) - s;
+    }
+    return rows / cfg.b + (!cfg.drop_last && rows % cfg.b ? 1 : 0);
 }
 
 void EpochReplay::consume(std::vector<uint64_t>& consumed) {
@@ -50,6 +63,10 @@ bool EpochReplay::next(std::vector<uint64_t>& gidx, std::vector<uint64_t>& consu
     gidx.clear();
     consumed.clear();
     if (done_) return false;
+    if (batch_index_ >= max_batches_) {  // even_batches: this rank stops with the shortest one
+        done_ = true;
+        return false;
+    }
     const uint64_t nb = plan_.size();
     if (!filled_) {  // loader.cpp:261-266
         while (buf_.size() < cfg_.B && next_block_ < nb) consume(consumed);

@@ -20,6 +20,10 @@ struct LoaderCfg {
     bool cache_bypass = false;
     uint32_t rank = 0;
     uint32_t world = 1;
+    // new: every rank of `world` ends the epoch after the smallest per-rank batch
+    // count (rank-sharded epochs can differ by a batch; a DDP step per batch would
+    // otherwise hang at epoch end).  world == 1: no effect.
+    bool even_batches = false;
     void validate() const;  // loader.cpp:159-168 (+ rank < world)
 };
 
@@ -55,8 +59,13 @@ private:
     Rng smp_;
     std::vector<uint64_t> buf_;
     uint64_t next_block_ = 0, peak_ = 0, batch_index_ = 0;
+    uint64_t max_batches_ = ~uint64_t{0};  // even_batches: the minimum over ranks
     bool filled_ = false, done_ = false;
 };
+
+// Batches rank `rank` yields in one epoch (rows of its plan positions / b,
+// rounded up unless drop_last): every batch but the last holds exactly b rows.
+uint64_t rank_batch_count(const std::vector<uint64_t>& all_ids, uint64_t n_obs, const LoaderCfg& cfg, uint32_t rank);
 
 // plan_shuffle (preshuffle.cpp:150-181)
 struct ShufflePlan {

@@ -36,11 +36,12 @@ class LoaderConfig:
     cache_bypass: bool = False
     rank: int = 0
     world: int = 1
+    even_batches: bool = False  # new: every rank stops after the smallest per-rank batch count (DDP-safe epochs)
 
     def _c(self) -> L.rfl_loader_config:
         return L.rfl_loader_config(self.fetch_block_rows, self.buffer_capacity_rows, self.batch_rows, self.seed,
                                    self.prefetch_depth, int(self.drop_last), int(self.cache_bypass), self.rank,
-                                   self.world, 0)
+                                   self.world, int(self.even_batches))
 
     def validate(self) -> None:
         """loader.cpp:159-168."""

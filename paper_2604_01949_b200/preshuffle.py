@@ -286,14 +286,17 @@ def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group, a2a=None) -
                 t0 = time.perf_counter()
                 L.check(lib.rfl_pshuf_send(h, r, dst))  # pack into the send buffer (stream synchronised)
                 rview = cuda_tensor(ptr.value, (max(need, 16),), np.uint8, device)[:need]
-                if nccl:  # grouped ncclSend/ncclRecv over NVLink
-                    dist.all_to_all_single(rview, sbuf[:total], out_splits, in_splits, group=group)
-                    torch.cuda.current_stream(device).synchronize()
-                else:  # gloo: through host memory
-                    host_out = torch.empty(need, dtype=torch.uint8)
-                    dist.all_to_all_single(host_out, sbuf[:total].cpu(), out_splits, in_splits, group=group)
-                    rview.copy_(host_out)
-                    torch.cuda.current_stream(device).synchronize()
+                try:
+                    if nccl:  # grouped ncclSend/ncclRecv over NVLink
+                        dist.all_to_all_single(rview, sbuf[:total], out_splits, in_splits, group=group)
+                        torch.cuda.current_stream(device).synchronize()
+                    else:  # gloo: through host memory
+                        host_out = torch.empty(need, dtype=torch.uint8)
+                        dist.all_to_all_single(host_out, sbuf[:total].cpu(), out_splits, in_splits, group=group)
+                        rview.copy_(host_out)
+                        torch.cuda.current_stream(device).synchronize()
+                except (RuntimeError, dist.DistError) as e:  # DistBackendError & co. -> RFL_ENCCL's exception
+                    raise L.NcclError(f"pre-shuffle round {r}: all-to-all exchange failed: {e}") from e
                 exchange_s += time.perf_counter() - t0
             recv = np.ascontiguousarray(mat[:, rank])
             L.check(lib.rfl_pshuf_emit(h, r, recv.ctypes.data))

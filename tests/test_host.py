@@ -151,6 +151,30 @@ def test_schedule_vs_oracle(n, f, B, b, seed, epoch, dl, world):
         assert sorted(allg) == list(range(n))
 
 
+@pytest.mark.parametrize("n,f,B,b,dl,world", [(5000, 64, 512, 128, False, 3), (7777, 100, 100, 100, False, 8),
+                                                (30011, 64, 1024, 500, True, 4), (4096, 64, 512, 512, False, 2)])
+def test_even_batches_truncates_to_the_shortest_rank(n, f, B, b, dl, world):
+    """even_batches (new, DDP-safe epochs): every rank yields the minimum per-rank
+    batch count, and its batches are exactly the first ones of its plain schedule."""
+    plain = [list(R.EpochSchedule(n, R.LoaderConfig(f, B, b, 5, drop_last=dl, rank=k, world=world), 1))
+             for k in range(world)]
+    even = [list(R.EpochSchedule(n, R.LoaderConfig(f, B, b, 5, drop_last=dl, rank=k, world=world,
+                                                   even_batches=True), 1)) for k in range(world)]
+    m = min(len(p) for p in plain)
+    assert all(len(e) == m for e in even)
+    for p, e in zip(plain, even):
+        assert all((x == y).all() for x, y in zip(p, e))
+    one = list(R.EpochSchedule(n, R.LoaderConfig(f, B, b, 5, drop_last=dl, even_batches=True), 1))
+    ref = list(R.EpochSchedule(n, R.LoaderConfig(f, B, b, 5, drop_last=dl), 1))
+    assert len(one) == len(ref)  # world == 1: the reference schedule
+
+
+def test_allocation_failure_maps_to_out_of_memory():
+    """std::bad_alloc crosses the C-ABI as RFL_ENOMEM -> OutOfMemory (a MemoryError)."""
+    with pytest.raises(MemoryError):
+        R.EpochSchedule(1 << 44, R.LoaderConfig(1, 1, 1), 0)
+
+
 def test_schedule_reference_large():
     """The 24-config survey probe at cfg1 scale: replay == reference iterator."""
     import tempfile
