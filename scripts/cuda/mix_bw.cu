@@ -4,6 +4,7 @@
 // same written through 80 KB shared-memory tiles with 1-D TMA bulk stores (the
 // densify store path).  Reports GB/s of (read + write) bytes, best of 5.
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o mix_bw mix_bw.cu
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -70,6 +71,62 @@ __global__ void __launch_bounds__(256) tile_store(const uint4* __restrict__ in, 
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// tile_store with an L2 evict_first policy on the bulk stores (output lines leave L2 first)
+__global__ void __launch_bounds__(256) tile_store_ef(const uint4* __restrict__ in, size_t n_in, char* __restrict__ out,
+                                                     size_t tiles, unsigned tile_bytes) {
+    extern __shared__ __align__(128) uint4 tile[];
+    unsigned acc = 0;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    for (size_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const size_t per = tile_bytes / 16 / 5;
+        for (size_t i = threadIdx.x; i < per; i += blockDim.x) acc += in[(t * per + i) % n_in].x;
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < tile_bytes / 16; i += blockDim.x) tile[i] = make_uint4(acc, i, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                         ::"l"(out + t * tile_bytes), "r"(static_cast<unsigned>(__cvta_generic_to_shared(tile))),
+                         "r"(tile_bytes), "l"(pol) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// the [b, n_var] f32 output written by 2-D tensor-map TMA stores (cp.async.bulk.tensor.2d):
+// box = 256 columns x BR rows (BR*1 KB of smem), tiles clipped at the n_var edge by the TMA unit
+__global__ void __launch_bounds__(256) tile_tensor2d(const uint4* __restrict__ in, size_t n_in,
+                                                     const __grid_constant__ CUtensorMap tm, unsigned rows,
+                                                     unsigned cols, unsigned br) {
+    extern __shared__ __align__(128) uint4 tile[];
+    const unsigned ct = (cols + 255) / 256, rt = rows / br, tiles = ct * rt, tile_bytes = br * 1024;
+    unsigned acc = 0;
+    for (unsigned t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const size_t per = tile_bytes / 16 / 5;
+        for (size_t i = threadIdx.x; i < per; i += blockDim.x) acc += in[(size_t(t) * per + i) % n_in].x;
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < tile_bytes / 16; i += blockDim.x) tile[i] = make_uint4(acc, i, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int c0 = static_cast<int>((t % ct) * 256), r0 = static_cast<int>((t / ct) * br);
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                         ::"l"(&tm), "r"(c0), "r"(r0), "r"(static_cast<unsigned>(__cvta_generic_to_shared(tile)))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
 int main() {
     const size_t out_bytes = 328ull << 20, in_bytes = out_bytes / 5;
     uint4 *in, *out;
@@ -111,5 +168,34 @@ int main() {
     const size_t tiles = out_bytes / tb;
     bench([&](int r) { tile_store<<<sms * 2, 256, tb>>>(in, n_in, reinterpret_cast<char*>(out) + (r % 4) * out_bytes, tiles, tb); },
           "tma 80KB tiles 1:5", double(in_bytes + out_bytes));
+    CK(cudaFuncSetAttribute(tile_store_ef, cudaFuncAttributeMaxDynamicSharedMemorySize, tb));
+    bench([&](int r) { tile_store_ef<<<sms * 2, 256, tb>>>(in, n_in, reinterpret_cast<char*>(out) + (r % 4) * out_bytes, tiles, tb); },
+          "tma 80KB tiles 1:5 L2 evict_first", double(in_bytes + out_bytes));
+    // 2-D tensor-map stores into a [rows, 20000] f32 matrix (cfg1's dense batch shape)
+    EncodeTiled enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q));
+    const unsigned cols = 20000, rows = static_cast<unsigned>(out_bytes / (cols * 4));
+    for (unsigned br : {32u, 64u, 80u}) {
+        const unsigned rws = rows / br * br;
+        CUtensorMap tm[4];
+        for (int k = 0; k < 4; ++k) {
+            const cuuint64_t dims[2] = {cols, rws}, strides[1] = {cols * 4ull};
+            const cuuint32_t box[2] = {256, br}, es[2] = {1, 1};
+            if (enc(&tm[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, reinterpret_cast<char*>(out) + k * out_bytes, dims,
+                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+                std::printf("tensor map encode failed\n");
+                return 1;
+            }
+        }
+        const unsigned sm_bytes = br * 1024;
+        CK(cudaFuncSetAttribute(tile_tensor2d, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_bytes));
+        const int per_sm = br <= 64 ? 3 : 2;
+        char name[96];
+        std::snprintf(name, sizeof name, "tma tensor 2d 256 cols x %u rows, %d CTAs/SM, 1:5", br, per_sm);
+        bench([&](int r) { tile_tensor2d<<<sms * per_sm, 256, sm_bytes>>>(in, n_in, tm[r % 4], rws, cols, br); }, name,
+              double(in_bytes) + double(rws) * cols * 4);
+    }
     return 0;
 }
