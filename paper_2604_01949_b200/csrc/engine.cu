@@ -158,6 +158,11 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     DeviceGuard g(device_);
     try {
         open_image();
+        if (d8_ && (m.value_dtype == VDtype::f32 || m.value_dtype == VDtype::i32)) {
+            d8_fused_ = true;
+            for (uint8_t k : d8_rec_) d8_fused_ = d8_fused_ && (k == kD8Raw || k == kD8Coded || k == kD8Coded16);
+            for (uint32_t n : row_nnz_) d8_fused_ = d8_fused_ && n <= kD8FusedMaxNnz;
+        }
     } catch (...) {  // the destructor does not run for a throwing constructor
         if (d_arena_) cudaFree(d_arena_);
         d_arena_ = nullptr;
@@ -461,7 +466,7 @@ DStore::~DStore() {
     free_host_image();
 }
 
-uint64_t DStore::max_block_bytes(uint64_t f) const {
+uint64_t DStore::max_block_bytes(uint64_t f, bool expanded) const {
     const Manifest& m = manifest();
     uint64_t best = 0;
     for (uint64_t s = 0; s < m.n_obs; s += f) {
@@ -469,7 +474,7 @@ uint64_t DStore::max_block_bytes(uint64_t f) const {
         uint64_t bytes = 0;
         for (uint64_t q = s / m.chunk_rows; q <= (e - 1) / m.chunk_rows; ++q) {
             bytes = align_up(bytes + img_len_[q], kAlign);
-            if (d8_) bytes = align_up(bytes + exp_len_[q], kAlign);  // expanded records + staged deltas
+            if (d8_ && expanded) bytes = align_up(bytes + exp_len_[q], kAlign);  // expanded records + staged deltas
         }
         best = std::max(best, bytes);
     }
@@ -803,9 +808,15 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
                 if (!e) cuda_ok(cudaEventCreate(&e), "event");
         s.timed = false;
     }
-    if (ds_->staging() != kResident) {
+    {
+        const char* e = std::getenv("RFL_FUSED");  // RFL_FUSED=0: k_d8_decode + idx16 densify (A/B)
+        fused_ = dev_.output == 1 && m.layout == Layout::csr && ds_->d8_fused() && !(e && e[0] == '0') &&
+                 (ds_->staging() == kStreamPinned || ds_->staging() == kResidentCoded);
+    }
+    direct_ = ds_->staging() == kResident || (ds_->staging() == kResidentCoded && fused_);
+    if (!direct_) {
         live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
-        block_bytes_ = ds_->max_block_bytes(cfg_.f);
+        block_bytes_ = ds_->max_block_bytes(cfg_.f, !fused_);
         // live blocks peak at ~5x B/f (cfg1 318 for B/f = 64, cfg4 230 for 32).
         // On top, (out_slots + 2) batches' worth of free slots: the host runs out_slots
         // batches ahead, and the FIFO pool must hand batch j a slot whose releasing
@@ -860,7 +871,7 @@ void GpuLoader::stage_block(uint64_t id) {
     lv.first_chunk = q0;
     lv.chunk_off.clear();
     const bool coded = ds_->staging() == kResidentCoded;  // staging image in HBM: decode device-to-device
-    const bool d8 = (ds_->staging() == kStreamPinned || coded) && ds_->d8();
+    const bool d8 = (ds_->staging() == kStreamPinned || coded) && ds_->d8() && !fused_;  // fused: no expansion
     uint64_t bytes = 0;
     for (uint64_t q = q0; q <= q1; ++q) {
         lv.chunk_off.push_back(bytes);
@@ -1109,7 +1120,7 @@ bool GpuLoader::assemble_group() {
     }
     if (group_.empty()) return false;
     if (tr.on) t_replay = tr.lap();
-    const bool resident = ds_->staging() == kResident;
+    const bool resident = direct_;
     if (!resident) {
         batch_dst_.clear();
         batch_src_.clear();
@@ -1164,11 +1175,12 @@ bool GpuLoader::assemble_group() {
             const uint64_t gr = gv[j];
             const uint64_t q = gr / m.chunk_rows;
             if (resident) {
-                hr[j] = {ds_->rec_off()[q], gr};
+                hr[j] = {fused_ ? ds_->img_off()[q] : ds_->rec_off()[q], gr};
             } else {
                 const Live& lv = live_[gr / cfg_.f];
                 hr[j] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
             }
+            if (fused_) hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
             hg[j] = gr;
         }
     }
@@ -1212,6 +1224,9 @@ bool GpuLoader::assemble_group() {
     const ArenaView av = ds_->view(base);
     if (m.layout == Layout::dense) {
         launch_dense_gather(av, s.d_refs, n, dev_.out_dtype, s.data, static_cast<uint64_t*>(s.gidx), compute_);
+    } else if (dev_.output == 1 && fused_) {
+        launch_csr_densify_d8(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,
+                              static_cast<uint64_t*>(s.gidx), compute_);
     } else if (dev_.output == 1) {
         launch_csr_densify(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,
                            static_cast<uint64_t*>(s.gidx), compute_, n ? (nnz + n - 1) / n : 0);

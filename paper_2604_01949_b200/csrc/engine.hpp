@@ -126,11 +126,15 @@ public:
     // exp_len the idx16 records they expand to in a slot
     bool d8() const { return d8_; }
     uint32_t d8_kind(uint64_t q) const { return d8_rec_[q]; }  // D8Kind of staged record q
+    // every staged record is a delta record with 4-byte values and every row has <=
+    // kD8FusedMaxNnz entries: dense output can densify the staged records directly
+    bool d8_fused() const { return d8_fused_; }
     const std::vector<uint64_t>& exp_len() const { return exp_len_; }
     uint64_t image_bytes() const { return image_bytes_; }
     uint64_t staged_bytes() const { return staged_bytes_; }  // staging image (0: verbatim)
     uint64_t row_nnz(uint64_t row) const { return row_nnz_.empty() ? 0 : row_nnz_[row]; }
-    uint64_t max_block_bytes(uint64_t f) const;  // staged bytes of the largest f-row block
+    // staged bytes of the largest f-row block (+ its idx16 expansion unless !expanded)
+    uint64_t max_block_bytes(uint64_t f, bool expanded = true) const;
     ArenaView view(const uint8_t* base) const;
 
     // streaming slot pool (shared by the iterators over this store)
@@ -167,7 +171,7 @@ private:
     int device_;
     uint32_t staging_;
     std::vector<uint64_t> rec_off_, rec_len_, slot_len_, slot_off_, img_off_, img_len_;
-    bool idx16_ = false, d8_ = false;
+    bool idx16_ = false, d8_ = false, d8_fused_ = false;
     std::vector<uint64_t> exp_len_;
     std::vector<uint8_t> d8_rec_;
     std::vector<uint32_t> row_nnz_;
@@ -308,6 +312,10 @@ private:
     std::exception_ptr rq_err_;
     size_t rq_cap_ = 8;
     std::vector<uint8_t> footer_seen_;  // shards whose footer charge this loader already applied
+    // dense output straight from the delta-staged records (K3d, no k_d8_decode)
+    bool fused_ = false;
+    // rows read in place from a device-resident image (resident, or resident_coded + fused_): no slots
+    bool direct_ = false;
     std::vector<Live> live_;                 // indexed by block id (streaming)
     uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
     std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead

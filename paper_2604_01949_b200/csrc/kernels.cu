@@ -9,6 +9,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -342,6 +343,25 @@ __global__ void __launch_bounds__(256)
 // header + indptr and the values are copied word-wise; each warp rebuilds its
 // rows' u16 columns with a warp inclusive scan of the u8 deltas (carry = the
 // row's first column).
+// 16 bytes at a 4-B aligned address (one 16-B load when it is 16-B aligned)
+__device__ __forceinline__ void ld16_any(const uint8_t* p, uint32_t* w) {
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+        w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = __ldg(reinterpret_cast<const uint32_t*>(p) + q);
+    }
+}
+__device__ __forceinline__ void st16_any(void* p, const uint32_t* w) {
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) reinterpret_cast<uint32_t*>(p)[q] = w[q];
+    }
+}
+
 struct D8Jobs {
     uint32_t n, vs;
     uint64_t n_var;  // kOneHot4 rows
@@ -402,42 +422,115 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
             reinterpret_cast<uint32_t*>(dv)[i] = __ldg(reinterpret_cast<const uint32_t*>(sv) + i);
         for (uint64_t i = (vbytes & ~3ull) + tid; i < vbytes; i += nt) dv[i] = sv[i];
     }
+    // rows: one warp each, 512 entries per step, 16 consecutive entries per lane
+    // starting at a 16-entry boundary of the record (entries outside the row are
+    // masked): vector loads of 16 deltas / 32 code bits / 16 or 48 low bytes, a
+    // lane-local prefix, then ONE warp scan of (delta sum | escape count << 20)
     const uint8_t* ip = jb.src + kCsrHeaderBytes;
-    uint16_t* out = reinterpret_cast<uint16_t*>(jb.dst + head);
-    uint32_t* vout = reinterpret_cast<uint32_t*>(dv);
-    const uint32_t lt = (1u << lane) - 1u;
+    uint8_t* cout = jb.dst + head;  // u16 columns
+    const uint32_t dict = coded ? ld_u32(jb.src + L.dict) : 0u;
     for (uint64_t r = blockIdx.y * 8 + warp; r < rows; r += gridDim.y * 8) {
         const uint64_t lo = ld_u32(ip + 4 * r), hi = ld_u32(ip + 4 * (r + 1));
         uint32_t carry = __ldg(reinterpret_cast<const unsigned short*>(first) + r);
         uint32_t esc_at = coded ? ld_u32(jb.src + L.esc_base + 4 * r) : 0u;
-        for (uint64_t base = lo; base < hi; base += 32) {
-            const uint64_t k = base + lane;
-            const bool valid = k < hi;
-            uint32_t v = valid ? __ldg(delta + k) : 0u;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(kFull, v, o);
-                if (lane >= static_cast<uint32_t>(o)) v += t;
+        for (uint64_t base = lo & ~15ull; base < hi; base += 512) {
+            const uint64_t k0 = base + 16 * lane;
+            const uint32_t a = k0 < lo ? static_cast<uint32_t>(lo - k0) : 0u;
+            const uint32_t b = k0 >= hi ? 0u : static_cast<uint32_t>(umin64(hi - k0, 16));
+            const uint32_t vm = b > a ? ((b == 32u ? 0u : (1u << b)) - (1u << a)) & 0xffffu : 0u;  // valid entries
+            const bool vec = k0 + 16 <= nnz;  // whole 16-entry group inside the record's arrays
+            uint32_t d[4] = {0u, 0u, 0u, 0u}, cw = 0u, lw[12];
+            if (vm) {
+                if (vec) {
+                    ld16_any(delta + k0, d);
+                    if (coded) cw = ld_u32(jb.src + L.codes + (k0 >> 2));
+                    if (coded && low_b == 1) ld16_any(jb.src + L.low3 + k0, lw);
+                    if (coded && low_b == 3) {
+                        ld16_any(jb.src + L.low3 + 3 * k0, lw);
+                        ld16_any(jb.src + L.low3 + 3 * k0 + 16, lw + 4);
+                        ld16_any(jb.src + L.low3 + 3 * k0 + 32, lw + 8);
+                    }
+                } else {  // the record's last group: byte loads of the entries that exist
+#pragma unroll
+                    for (int q = 0; q < 12; ++q) lw[q] = 0u;
+#pragma unroll
+                    for (uint32_t j = 0; j < 16; ++j) {
+                        if (k0 + j >= nnz) continue;
+                        d[j >> 2] |= static_cast<uint32_t>(__ldg(delta + k0 + j)) << (8 * (j & 3));
+                        if (coded) cw |= ((static_cast<uint32_t>(__ldg(jb.src + L.codes + ((k0 + j) >> 2))) >>
+                                           (2 * ((k0 + j) & 3))) & 3u) << (2 * j);
+                        if (coded && low_b == 1)
+                            lw[j >> 2] |= static_cast<uint32_t>(__ldg(jb.src + L.low3 + k0 + j)) << (8 * (j & 3));
+                        if (coded && low_b == 3)
+#pragma unroll
+                            for (uint32_t t = 0; t < 3; ++t)
+                                lw[(3 * j + t) >> 2] |= static_cast<uint32_t>(__ldg(jb.src + L.low3 + 3 * (k0 + j) + t))
+                                                        << (8 * ((3 * j + t) & 3));
+                    }
+                }
             }
-            const uint32_t col = carry + v;
-            if (valid) out[k] = static_cast<uint16_t>(col);
-            carry = __shfl_sync(kFull, col, 31);
-            if (coded) {  // top byte from the dictionary or the escape list, low 3 bytes verbatim
-                const uint32_t code = valid ? (__ldg(jb.src + L.codes + (k >> 2)) >> (2 * (k & 3))) & 3u : 0u;
-                const uint32_t em = __ballot_sync(kFull, valid && code == 3u);
-                if (valid) {
-                    const uint32_t top = code == 3u ? __ldg(jb.src + L.esc + esc_at + __popc(em & lt))
-                                                    : __ldg(jb.src + L.dict + code);
+            uint32_t pre[16], s = 0;
+#pragma unroll
+            for (uint32_t j = 0; j < 16; ++j) {
+                s += (vm >> j) & 1u ? (d[j >> 2] >> (8 * (j & 3))) & 255u : 0u;
+                pre[j] = s;
+            }
+            uint32_t em = 0;  // escape entries (code 3) among the valid ones
+            if (coded) {
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j) em |= (((cw >> (2 * j)) & 3u) == 3u ? 1u : 0u) << j;
+                em &= vm;
+            }
+            const uint32_t mine = s | (static_cast<uint32_t>(__popc(em)) << 20);
+            uint32_t incl = mine;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(kFull, incl, o);
+                if (lane >= static_cast<uint32_t>(o)) incl += t;
+            }
+            const uint32_t tot = __shfl_sync(kFull, incl, 31), excl = incl - mine;
+            const uint32_t cb = carry + (excl & 0xfffffu);
+            uint32_t eb = esc_at + (excl >> 20);
+            carry += tot & 0xfffffu;
+            esc_at += tot >> 20;
+            if (!vm) continue;
+            uint32_t cwd[8];
+#pragma unroll
+            for (uint32_t m = 0; m < 8; ++m) cwd[m] = ((cb + pre[2 * m]) & 0xffffu) | ((cb + pre[2 * m + 1]) << 16);
+            if (vm == 0xffffu) {
+                st16_any(cout + 2 * k0, cwd);
+                st16_any(cout + 2 * k0 + 16, cwd + 4);
+            } else {
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j)
+                    if ((vm >> j) & 1u)
+                        reinterpret_cast<uint16_t*>(cout)[k0 + j] = static_cast<uint16_t>(cb + pre[j]);
+            }
+            if (coded) {  // top byte from the dictionary or the escape list, low bytes verbatim
+                uint32_t v[16];
+#pragma unroll
+                for (uint32_t j = 0; j < 16; ++j) {
+                    const uint32_t code = (cw >> (2 * j)) & 3u;
+                    uint32_t top = (dict >> (8 * code)) & 255u;
+                    if ((em >> j) & 1u) top = __ldg(jb.src + L.esc + eb++);
                     uint32_t low;
                     if (low_b == 1) {
-                        low = static_cast<uint32_t>(__ldg(jb.src + L.low3 + k)) << 16;
+                        low = ((lw[j >> 2] >> (8 * (j & 3))) & 255u) << 16;
                     } else {
-                        const uint8_t* l3 = jb.src + L.low3 + 3 * k;
-                        low = (static_cast<uint32_t>(__ldg(l3 + 2)) << 16) | (static_cast<uint32_t>(__ldg(l3 + 1)) << 8) |
-                              __ldg(l3);
+                        low = 0u;
+#pragma unroll
+                        for (uint32_t t = 0; t < 3; ++t) low |= ((lw[(3 * j + t) >> 2] >> (8 * ((3 * j + t) & 3))) & 255u) << (8 * t);
                     }
-                    vout[k] = (top << 24) | low;
+                    v[j] = (top << 24) | low;
                 }
-                esc_at += __popc(em);
+                uint32_t* vo = reinterpret_cast<uint32_t*>(dv) + k0;
+                if (vm == 0xffffu) {
+#pragma unroll
+                    for (uint32_t q = 0; q < 4; ++q) st16_any(vo + 4 * q, v + 4 * q);
+                } else {
+#pragma unroll
+                    for (uint32_t j = 0; j < 16; ++j)
+                        if ((vm >> j) & 1u) vo[j] = v[j];
+                }
             }
         }
     }
@@ -741,6 +834,253 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int u = 0; u < U; ++u) {
             colA[u] = colB[u];
             vA[u] = vB[u];
+        }
+    }
+    if (bulk && tid == 0) bulk_wait0();
+}
+
+// ============================================ K3d densify from delta records ===
+// K3 reading the staging image's delta records directly (kD8Raw / kD8Coded /
+// kD8Coded16, kernels.cuh d8v_layout) instead of the idx16 records k_d8_decode
+// would expand: the expansion's write + re-read of 6 B per entry disappears.
+// RowRef.rec_off carries the record's D8Kind in bits 60..63.  Thread t holds
+// the 16 consecutive entries [(lo & ~15) + 16 t, +16) of a row (rows of up to
+// kD8FusedMaxNnz entries; the launcher's caller guarantees it): 16 column
+// deltas, 32 code bits and the low value bytes arrive as vector loads one row
+// ahead; at the row's turn ONE block scan of (delta sum | escape count << 17)
+// yields every entry's column and escape rank, and the scatter into the smem
+// tile + TMA bulk store is v9's.
+constexpr uint64_t kKindShift = 60, kOffMask = (1ull << kKindShift) - 1;
+
+struct D8RowDesc {
+    const uint8_t* delta;  // column deltas u8 (record entry 0)
+    const uint8_t* low;    // kD8Raw: raw 4-B values; coded: low value bytes
+    const uint8_t* codes;  // 2-bit top-byte codes
+    const uint8_t* esc;    // escaped top bytes
+    uint64_t gidx;
+    uint32_t lo, hi, nrec;  // row entries [lo, hi) of the record's nrec
+    uint32_t first, esc_at, dict, kind, pad;
+};
+
+__device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef& r) {
+    D8RowDesc d;
+    const uint8_t* rec = a.base + (r.rec_off & kOffMask);
+    d.kind = static_cast<uint32_t>(r.rec_off >> kKindShift);
+    const uint64_t within = r.gidx % a.chunk_rows;
+    const uint32_t rows = ld_u32(rec);
+    const uint64_t nnz = ld_u64_a4(rec + 4);
+    const uint8_t* ip = rec + kCsrHeaderBytes;
+    d.lo = ld_u32(ip + 4 * within);
+    d.hi = ld_u32(ip + 4 * (within + 1));
+    d.nrec = static_cast<uint32_t>(nnz);
+    const uint64_t first_off = kCsrHeaderBytes + 4 * (static_cast<uint64_t>(rows) + 1);
+    d.first = __ldg(reinterpret_cast<const unsigned short*>(rec + first_off) + within);
+    d.delta = rec + first_off + ((2 * static_cast<uint64_t>(rows) + 3) & ~3ull);
+    d.gidx = r.gidx;
+    d.pad = 0;
+    if (d.kind == kD8Raw) {
+        d.low = rec + d8_values_offset(rows, nnz);
+        d.codes = d.esc = nullptr;
+        d.esc_at = d.dict = 0;
+    } else {
+        const D8vLayout L0 = d8v_layout(rows, nnz, 0);
+        const D8vLayout L = d8v_layout(rows, nnz, ld_u32(rec + L0.n_esc), d.kind == kD8Coded16 ? 1 : 3);
+        d.low = rec + L.low3;
+        d.codes = rec + L.codes;
+        d.esc = rec + L.esc;
+        d.esc_at = ld_u32(rec + L.esc_base + 4 * within);
+        d.dict = ld_u32(rec + L.dict);
+    }
+    return d;
+}
+
+struct D8Raw16 {  // one thread's 16 entries of a row, as loaded
+    uint32_t d[4], cw, lw[16], vm;
+};
+
+__device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw16& x) {
+    const uint64_t k0 = (r.lo & ~15u) + 16ull * tid;
+    const uint32_t a = k0 < r.lo ? static_cast<uint32_t>(r.lo - k0) : 0u;
+    const uint32_t b = k0 >= r.hi ? 0u : static_cast<uint32_t>(umin64(r.hi - k0, 16));
+    x.vm = b > a ? ((1u << b) - (1u << a)) & 0xffffu : 0u;
+    x.cw = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x.d[q] = 0u;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) x.lw[q] = 0u;
+    if (!x.vm) return;
+    const uint32_t kind = r.kind;
+    if (k0 + 16 <= r.nrec) {
+        ld16_any(r.delta + k0, x.d);
+        if (kind == kD8Raw) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ld16_any(r.low + 4 * k0 + 16 * q, x.lw + 4 * q);
+        } else {
+            x.cw = ld_u32(r.codes + (k0 >> 2));
+            if (kind == kD8Coded16) {
+                ld16_any(r.low + k0, x.lw);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) ld16_any(r.low + 3 * k0 + 16 * q, x.lw + 4 * q);
+            }
+        }
+        return;
+    }
+    // the record's last entry group: byte loads of the entries that exist
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j) {
+        if (k0 + j >= r.nrec) continue;
+        const uint64_t k = k0 + j;
+        x.d[j >> 2] |= static_cast<uint32_t>(__ldg(r.delta + k)) << (8 * (j & 3));
+        if (kind == kD8Raw) {
+            x.lw[j] = ld_u32(r.low + 4 * k);
+        } else {
+            x.cw |= ((static_cast<uint32_t>(__ldg(r.codes + (k >> 2))) >> (2 * (k & 3))) & 3u) << (2 * j);
+            if (kind == kD8Coded16) {
+                x.lw[j >> 2] |= static_cast<uint32_t>(__ldg(r.low + k)) << (8 * (j & 3));
+            } else {
+#pragma unroll
+                for (uint32_t t = 0; t < 3; ++t)
+                    x.lw[(3 * j + t) >> 2] |= static_cast<uint32_t>(__ldg(r.low + 3 * k + t)) << (8 * ((3 * j + t) & 3));
+            }
+        }
+    }
+}
+
+template <typename SrcT>
+__device__ __forceinline__ SrcT from_bits(uint32_t b) {
+    if constexpr (sizeof(SrcT) == 4 && std::is_floating_point_v<SrcT>) return __uint_as_float(b);
+    else return static_cast<SrcT>(static_cast<int32_t>(b));
+}
+
+// columns (~0u = not an entry of the row) and values of one thread's 16 entries;
+// s_scan: THREADS/32 words (one __syncthreads inside)
+template <typename SrcT, int THREADS>
+__device__ __forceinline__ void decode_d8(const D8RowDesc& r, const D8Raw16& x, uint32_t* s_scan, uint32_t (&col)[16],
+                                          SrcT (&v)[16]) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    uint32_t pre[16], sum = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j) {
+        sum += (x.vm >> j) & 1u ? (x.d[j >> 2] >> (8 * (j & 3))) & 255u : 0u;
+        pre[j] = sum;
+    }
+    uint32_t em = 0;
+    if (r.kind != kD8Raw) {
+#pragma unroll
+        for (uint32_t j = 0; j < 16; ++j) em |= (((x.cw >> (2 * j)) & 3u) == 3u ? 1u : 0u) << j;
+        em &= x.vm;
+    }
+    const uint32_t mine = sum | (static_cast<uint32_t>(__popc(em)) << 17);
+    uint32_t incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += t;
+    }
+    if (lane == 31) s_scan[warp] = incl;
+    __syncthreads();
+    uint32_t excl = incl - mine;
+    for (uint32_t w = 0; w < warp; ++w) excl += s_scan[w];
+    const uint32_t cb = r.first + (excl & 0x1ffffu);
+    uint32_t eb = r.esc_at + (excl >> 17);
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j) {
+        col[j] = (x.vm >> j) & 1u ? cb + pre[j] : ~0u;
+        uint32_t bits;
+        if (r.kind == kD8Raw) {
+            bits = x.lw[j];
+        } else {
+            uint32_t top = (r.dict >> (8 * ((x.cw >> (2 * j)) & 3u))) & 255u;
+            if ((em >> j) & 1u) top = __ldg(r.esc + eb++);
+            uint32_t low;
+            if (r.kind == kD8Coded16) {
+                low = ((x.lw[j >> 2] >> (8 * (j & 3))) & 255u) << 16;
+            } else {
+                low = 0u;
+#pragma unroll
+                for (uint32_t t = 0; t < 3; ++t) low |= ((x.lw[(3 * j + t) >> 2] >> (8 * ((3 * j + t) & 3))) & 255u) << (8 * t);
+            }
+            bits = (top << 24) | low;
+        }
+        v[j] = from_bits<SrcT>(bits);
+    }
+}
+
+template <typename SrcT, typename DstT, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_csr_densify_d8(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
+                     float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ double s_red[THREADS / 32];
+    __shared__ uint32_t s_scan[THREADS / 32];
+    __shared__ D8RowDesc s_desc[32];
+    const uint32_t tid = threadIdx.x;
+    const uint64_t n_var = a.n_var;
+    const uint64_t g = gridDim.x;
+    pdl_wait();
+    pdl_trigger();
+    auto describe32 = [&](uint64_t k0) {
+        if (tid < 32) {
+            const uint64_t row = blockIdx.x + (k0 + tid) * g;
+            if (row < n_rows) {
+                const D8RowDesc rd = describe_d8(a, refs[row]);
+                s_desc[tid] = rd;
+                if (out_gidx) out_gidx[row] = rd.gidx;
+            }
+        }
+    };
+    describe32(0);
+    __syncthreads();
+    D8Raw16 raw;
+    if (blockIdx.x < n_rows) load_d8(s_desc[0], tid, raw);
+    uint32_t col[16];
+    SrcT val[16];
+    uint64_t kk = 0;
+    for (uint64_t row = blockIdx.x; row < n_rows; row += g, ++kk) {
+        const D8RowDesc d = s_desc[kk & 31];
+        decode_d8<SrcT, THREADS>(d, raw, s_scan, col, val);  // (syncs: s_desc reads above are done)
+        const bool has_next = row + g < n_rows;
+        if (has_next && ((kk + 1) & 31) == 0) {
+            __syncthreads();
+            describe32(kk + 1);
+            __syncthreads();
+        }
+        if (has_next) load_d8(s_desc[(kk + 1) & 31], tid, raw);  // row i+1 in flight
+        float scale = 1.0f;
+        if (norm) {  // library size in fp64
+            double s = 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (col[u] != ~0u) s += static_cast<double>(val[u]);
+            s = block_sum(s, s_red);
+            scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
+        }
+        DstT* orow = out + row * n_var;
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+            const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
+            const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
+            DstT* tile = reinterpret_cast<DstT*>(smem);
+            if (bulk && tid == 0) bulk_wait_read0();
+            __syncthreads();
+            uint4* t4 = reinterpret_cast<uint4*>(smem);
+            for (uint32_t i = tid; i < bytes / 16u; i += THREADS) t4[i] = make_uint4(0, 0, 0, 0);
+            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += THREADS) smem[i] = 0;
+            __syncthreads();
+            const uint32_t c0u = static_cast<uint32_t>(c0);
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (col[u] - c0u < cols) tile[col[u] - c0u] = Conv<DstT, SrcT>::go(val[u], scale, norm);
+            if (bulk) {
+                fence_proxy_async_shared();
+                __syncthreads();
+                if (tid == 0) {
+                    bulk_store(orow + c0, smem, bytes);
+                    bulk_commit();
+                }
+            } else {
+                __syncthreads();
+                for (uint32_t i = tid; i < cols; i += THREADS) orow[c0 + i] = tile[i];
+            }
         }
     }
     if (bulk && tid == 0) bulk_wait0();
@@ -1371,6 +1711,114 @@ __global__ void __launch_bounds__(kDgThreads)
     if (lane == 0) bulk_wait0();
 }
 
+// TMA-pipelined variant: work unit = (row, SEG input bytes); every warp runs
+// its own NS-stage pipeline -- lane 0 issues 1-D TMA bulk loads of its next
+// units into shared stages (mbarrier completion) NS-1 ahead, and writes each
+// unit back with one bulk store: raw rows straight from the load stage, u8 ->
+// bf16 rows after the warp converted the stage into one of two output stages.
+// Row refs of the next 32 units are read lane-parallel.  Per SM that keeps
+// (NS-1) x SEG x warps of loads in flight with no registers held, which the
+// register-staged kernels above (2 x 16 B per lane) cannot.
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+template <int MODE, int SEG, int NS, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    k_dense_gather_tma(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
+                       uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx) {
+    static_assert(MODE == kRaw || MODE == kU8ToBf16, "raw or u8 -> bf16");
+    constexpr uint32_t kOut = MODE == kU8ToBf16 ? 2 : 1;
+    constexpr uint32_t kWarpSmem = NS * SEG + (MODE == kRaw ? 0 : 2 * SEG * kOut);
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bars[WARPS][NS];
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint8_t* in_st = smem + warp * kWarpSmem;
+    uint8_t* out_st = in_st + NS * SEG;
+    uint64_t* bar = bars[warp];
+    const uint64_t upr = (in_row_bytes + SEG - 1) / SEG;
+    const uint64_t n_units = n_rows * upr;
+    const uint64_t tw = static_cast<uint64_t>(gridDim.x) * WARPS;
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
+    const uint64_t nk = n_units > w0 ? (n_units - w0 + tw - 1) / tw : 0;
+    if (lane == 0) {
+        for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    // lane i: source offset of issue index rb + i
+    uint64_t rb = 0, my_off = 0;
+    auto refresh = [&](uint64_t base) {
+        rb = base;
+        const uint64_t u = w0 + (base + lane) * tw;
+        if (base + lane < nk) {
+            const uint64_t row = u / upr, part = u - row * upr;
+            const RowRef r = refs[row];
+            my_off = r.rec_off + (r.gidx % a.chunk_rows) * in_row_bytes + part * SEG;
+            if (part == 0 && out_gidx) out_gidx[row] = r.gidx;
+        }
+    };
+    refresh(0);
+    auto issue = [&](uint64_t j) {  // whole warp (shuffle); lane 0 issues
+        if (j - rb >= 32) refresh(j);
+        const uint64_t off = __shfl_sync(kFull, my_off, static_cast<int>(j - rb));
+        if (lane == 0) {
+            const uint64_t u = w0 + j * tw, row = u / upr, part = u - row * upr;
+            const uint32_t bytes = static_cast<uint32_t>(umin64(SEG, in_row_bytes - part * SEG));
+            uint64_t* b = &bar[j % NS];
+            mbar_arrive_expect_tx(b, bytes);
+            bulk_load(in_st + (j % NS) * SEG, a.base + off, bytes, b);
+        }
+    };
+    for (uint64_t j = 0; j + 1 < NS && j < nk; ++j) issue(j);
+    for (uint64_t k = 0; k < nk; ++k) {
+        const uint64_t u = w0 + k * tw, row = u / upr, part = u - row * upr;
+        const uint32_t bytes = static_cast<uint32_t>(umin64(SEG, in_row_bytes - part * SEG));
+        const uint32_t st = static_cast<uint32_t>(k % NS);
+        uint8_t* dst = out + row * out_row_bytes + part * SEG * kOut;
+        if (MODE == kRaw) {
+            if (lane == 0) {
+                mbar_wait(&bar[st], static_cast<uint32_t>((k / NS) & 1));
+                bulk_store(dst, in_st + st * SEG, bytes);
+                bulk_commit();
+                bulk_wait_read1();  // store k-1 has read its stage: (k-1) % NS is free
+            }
+            __syncwarp();
+        } else {
+            mbar_wait(&bar[st], static_cast<uint32_t>((k / NS) & 1));
+            if (lane == 0) bulk_wait_read1();  // output stage k % 2 (store k-2) is free
+            __syncwarp();
+            uint8_t* ob = out_st + (k & 1) * SEG * kOut;
+            const uint8_t* ib = in_st + st * SEG;
+            for (uint32_t c = lane; c < bytes / 16; c += 32) {
+                const uint4 v = *reinterpret_cast<const uint4*>(ib + c * 16);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                uint32_t o[8];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    o[2 * q] = pack_bf16x2(float(w[q] & 0xff), float((w[q] >> 8) & 0xff));
+                    o[2 * q + 1] = pack_bf16x2(float((w[q] >> 16) & 0xff), float(w[q] >> 24));
+                }
+                *reinterpret_cast<uint4*>(ob + c * 32) = make_uint4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<uint4*>(ob + c * 32 + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+            fence_proxy_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+                bulk_store(dst, ob, bytes * kOut);
+                bulk_commit();
+            }
+        }
+        if (k + NS - 1 < nk) issue(k + NS - 1);
+    }
+    if (lane == 0) bulk_wait0();
+}
+
 // ------------------------------------------------------------ host helpers ---
 
 bool pdl_enabled() {
@@ -1723,6 +2171,44 @@ void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n, OutD
     else densify_idx<uint64_t>(a, refs, n, od, norm, target, out, out_gidx, st, avg_nnz);
 }
 
+namespace {
+template <typename SrcT, typename DstT>
+void densify_d8_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
+                  uint64_t* out_gidx, cudaStream_t st) {
+    // the v9 shape rule: rows wider than 48 KB -> 80 KB tiles at 2 CTAs/SM, else 40 KB at 3
+    const uint64_t esz = sizeof(DstT);
+    const bool wide = av.n_var * esz > 48 * 1024;
+    const uint64_t max_tile = wide ? (80u << 10) : (40u << 10);
+    uint64_t tile_cols = av.n_var;
+    if (av.n_var * esz > max_tile) tile_cols = (max_tile / esz) & ~15ull;
+    const size_t smem = (tile_cols * esz + 127) & ~127ull;
+    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    auto kern = wide ? k_csr_densify_d8<SrcT, DstT, 256, 2> : k_csr_densify_d8<SrcT, DstT, 256, 3>;
+    set_smem(kern, smem);
+    int per_sm = 0;
+    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem), "occupancy");
+    const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
+    launch_k(kern, dim3(static_cast<unsigned>(grid)), dim3(256), smem, st, "k_csr_densify_d8 launch", dev_view(av),
+             refs, n, static_cast<uint32_t>(tile_cols), norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
+}
+}  // namespace
+
+void launch_csr_densify_d8(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, bool norm, float target,
+                           void* out, uint64_t* out_gidx, cudaStream_t st) {
+    if (a.layout != Layout::csr) invalid("csr_densify_d8: store is not csr");
+    if (n == 0) return;
+    if (a.vdt == VDtype::f32) {
+        if (od == OutDtype::bf16) return densify_d8_t<float, __nv_bfloat16>(a, refs, n, norm, target, out, out_gidx, st);
+        return densify_d8_t<float, float>(a, refs, n, norm, target, out, out_gidx, st);
+    }
+    if (a.vdt == VDtype::i32) {
+        if (od == OutDtype::bf16) return densify_d8_t<int32_t, __nv_bfloat16>(a, refs, n, norm, target, out, out_gidx, st);
+        if (od == OutDtype::f32) return densify_d8_t<int32_t, float>(a, refs, n, norm, target, out, out_gidx, st);
+        return densify_d8_t<int32_t, int32_t>(a, refs, n, false, target, out, out_gidx, st);
+    }
+    invalid("csr_densify_d8: delta records carry 4-byte values (f32 / i32)");
+}
+
 void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, void* out,
                          uint64_t* out_gidx, cudaStream_t st) {
     if (a.layout != Layout::dense) invalid("dense_gather: store is not dense");
@@ -1741,9 +2227,33 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         static const int u_sel = [] {
             const char* e = std::getenv("RFL_DG");
             if (!e) return 0;  // automatic
+            if (e[0] == 't') return 100 + (e[1] ? e[1] - '0' : 0);  // TMA-pipelined variant (shape digit)
             if (e[0] == 'b') return e[1] == '4' ? -4 : -2;  // TMA bulk-store variant, 2 or 4 loads per lane
             return e[0] == '4' ? 4 : 2;
         }();
+        // TMA-pipelined kernel: persistent grid (occupancy x SMs, at most one warp per unit)
+        auto go_tma = [&](auto kern, uint64_t seg, uint32_t warps, size_t smem) {
+            set_smem(kern, smem);
+            static std::mutex mu;
+            static std::map<const void*, int> occ_of;
+            int occ = 0;
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                auto it = occ_of.find(reinterpret_cast<const void*>(kern));
+                if (it == occ_of.end()) {
+                    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem), "occupancy");
+                    occ_of[reinterpret_cast<const void*>(kern)] = occ;
+                } else {
+                    occ = it->second;
+                }
+            }
+            const uint64_t units = n * ((in_rb + seg - 1) / seg);
+            const unsigned g2 = static_cast<unsigned>(std::max<uint64_t>(
+                1, std::min<uint64_t>((units + warps - 1) / warps, static_cast<uint64_t>(std::max(occ, 1)) * device_sm_count())));
+            const uint64_t orb = od == OutDtype::bf16 ? a.n_var * 2 : in_rb;
+            launch_k(kern, dim3(g2), dim3(warps * 32), smem, st, "k_dense_gather_tma launch", d, in_rb, refs, n, o, orb,
+                     out_gidx);
+        };
         auto go = [&](auto kern, int U, int T) {
             const uint64_t upr = (in_rb / 16 + 32 * U - 1) / (32 * U);
             const uint64_t warps_needed = n * upr;
@@ -1754,6 +2264,16 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         };
         auto pick = [&](auto mode) {
             constexpr int M = decltype(mode)::value;
+            if constexpr (M == kRaw) {
+                if (u_sel == 100) return go_tma(k_dense_gather_tma<kRaw, 4096, 4, 4>, 4096, 4, 4 * 4 * 4096);
+                if (u_sel == 101) return go_tma(k_dense_gather_tma<kRaw, 8192, 3, 4>, 8192, 4, 4 * 3 * 8192);
+                if (u_sel == 102) return go_tma(k_dense_gather_tma<kRaw, 2048, 6, 8>, 2048, 8, 8 * 6 * 2048);
+            }
+            if constexpr (M == kU8ToBf16) {
+                if (u_sel == 100) return go_tma(k_dense_gather_tma<kU8ToBf16, 2048, 4, 4>, 2048, 4, 4 * (4 * 2048 + 2 * 4096));
+                if (u_sel == 101) return go_tma(k_dense_gather_tma<kU8ToBf16, 4096, 3, 2>, 4096, 2, 2 * (3 * 4096 + 2 * 8192));
+                if (u_sel == 102) return go_tma(k_dense_gather_tma<kU8ToBf16, 1024, 6, 8>, 1024, 8, 8 * (6 * 1024 + 2 * 2048));
+            }
             if (u_sel == 4) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
             if constexpr (M != kF32ToBf16) {
                 // automatic: the u8 -> bf16 expansion writes through TMA bulk stores

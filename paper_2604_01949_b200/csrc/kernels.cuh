@@ -55,12 +55,17 @@ inline uint64_t idx16_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) {
     return kCsrHeaderBytes + 4 * (rows + 1) + ((2 * nnz + 7) & ~7ull) + vs * nnz;
 }
 
+#ifdef __CUDACC__
+#define RFL_HD __host__ __device__
+#else
+#define RFL_HD
+#endif
 // Delta staging (the pinned image when every in-row column gap is <= 255): per
 // record [rows u32][nnz u64][indptr u32 x (rows+1)][first column u16 x rows,
 // padded to 4 B][column deltas u8 x nnz (0 for a row's first entry), padded to
 // 8 B from the record start][data].  5 B per stored f32 entry cross PCIe; a
 // decode kernel expands each staged record into the idx16 layout in HBM.
-inline uint64_t d8_values_offset(uint64_t rows, uint64_t nnz) {
+RFL_HD inline uint64_t d8_values_offset(uint64_t rows, uint64_t nnz) {
     const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
     return (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
 }
@@ -71,11 +76,6 @@ inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) { retu
 // [escapes before row r, u32 x rows][dict u8 x 4][n_esc u32][2-bit codes x nnz,
 // pad 4][escaped top bytes u8 x n_esc, pad 4][low 3 bytes x nnz] -- ~4.3 B per
 // stored f32 entry instead of 5 (code 3 = escape: the top byte is in the list).
-#ifdef __CUDACC__
-#define RFL_HD __host__ __device__
-#else
-#define RFL_HD
-#endif
 struct D8vLayout {
     uint64_t first, delta, esc_base, dict, n_esc, codes, esc, low3, bytes;
 };
@@ -156,6 +156,13 @@ void launch_validate_csr(const uint8_t* base, const uint64_t* d_rec_off, const u
 void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
                         float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st, uint64_t avg_nnz = 0);
 size_t dense_out_elem_size(const ArenaView& a, OutDtype od);
+// K3d: densify straight from delta-staged records (kD8Raw / kD8Coded / kD8Coded16
+// with 4-byte values), no k_d8_decode.  refs[i].rec_off = record offset |
+// (D8Kind << kRowKindShift); every row must have <= kD8FusedMaxNnz entries.
+constexpr unsigned kRowKindShift = 60;
+constexpr uint64_t kD8FusedMaxNnz = 16 * 256 - 15;
+void launch_csr_densify_d8(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
+                           float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);
 
 // K4
 void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, void* out,

@@ -41,6 +41,8 @@ CASES = {  # store, kernel, rows per launch, out dtype, transform
     "densify_norm_cfg2": ("cfg2s", "densify", 4096, L.F32, L.XF_NORMALIZE_LOG1P),
     "dense_bf16_cfg3": ("cfg3s", "dense", 1024, L.BF16, None),
     "dense_raw_cfg4": ("cfg4s", "dense", 2048, L.NATIVE, None),
+    "dense_bf16_cfg3_g2": ("cfg3s", "dense", 2048, L.BF16, None),   # bench.py's 2 batches per launch
+    "dense_raw_cfg4_g4": ("cfg4s", "dense", 8192, L.NATIVE, None),  # bench.py's 4 batches per launch
     "pack_cfg5": ("cfg5s", "pack", 65536, None, None),
 }
 
@@ -108,11 +110,14 @@ def run_case(name, K, W, dstores):
         rn = row_nnz(ds.reader, man)
         nnz = [int(rn[g.astype(np.int64)].sum()) for g in sets]
     gout = torch.empty(rows, dtype=torch.int64, device="cuda")
+    def rotating(nbytes):  # output buffers totalling > 2 x L2: no launch writes over cached output
+        n_out = max(2, -(-(256 << 20) // nbytes))
+        return [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(n_out)]
     if kern == "densify":
         osz = 2 if od == L.BF16 else 4
-        out = torch.empty(rows * man.n_var * osz + 16, dtype=torch.uint8, device="cuda")
+        outs = rotating(rows * man.n_var * osz + 16)
         launch = lambda i: lib.rfl_csr_densify(C.byref(desc), d_refs[i].data_ptr(), rows, od, xf, 1e4,  # noqa
-                                               out.data_ptr(), gout.data_ptr(), sp)
+                                               outs[i % len(outs)].data_ptr(), gout.data_ptr(), sp)
         alg = lambda i: nnz[i] * (isz + vs) + rows * (16 + 2 * isz + man.n_var * osz + 8)  # noqa
     elif kern == "gather":
         mx = max(nnz)
@@ -137,9 +142,9 @@ def run_case(name, K, W, dstores):
     elif kern == "dense":
         rb = man.n_var * vs
         osz = 2 if od == L.BF16 else vs
-        out = torch.empty(rows * man.n_var * osz + 16, dtype=torch.uint8, device="cuda")
-        launch = lambda i: lib.rfl_dense_gather(C.byref(desc), d_refs[i].data_ptr(), rows, od, out.data_ptr(),  # noqa
-                                                gout.data_ptr(), sp)
+        outs = rotating(rows * man.n_var * osz + 16)
+        launch = lambda i: lib.rfl_dense_gather(C.byref(desc), d_refs[i].data_ptr(), rows, od,  # noqa
+                                                outs[i % len(outs)].data_ptr(), gout.data_ptr(), sp)
         alg = lambda i: rows * (16 + rb + man.n_var * osz + 8)  # noqa
     else:  # pack: scan + record pack, 4096-row output chunks
         cr = 4096

@@ -277,3 +277,100 @@ def test_iterators_on_threads_share_one_store(crafted):
         t.join()
     ds.close()
     assert not errors, errors
+
+
+def _fused_store(tmp_path, values, seed=11):
+    """Rows of 0, 1, 2 and 1,000 .. 4,081 entries (4,081 = the fused kernel's
+    limit with an unaligned row start) over 6,000 columns: every gap <= 255, so
+    every record stages as a delta record and the store qualifies for K3d."""
+    rng = np.random.default_rng(seed)
+    n, nv = 200, 6000
+    nnz = rng.integers(1000, 4082, n)
+    nnz[::17] = 4081
+    nnz[3::29] = 0
+    nnz[5::31] = 1
+    nnz[7::37] = 2
+    ip = np.zeros(n + 1, np.uint64)
+    ip[1:] = np.cumsum(nnz)
+    def cols(k):
+        if k == 2:  # a gap of exactly 255 (the delta limit)
+            c = int(rng.integers(0, nv - 256))
+            return np.array([c, c + 255])
+        return np.sort(rng.choice(nv, k, replace=False))
+    ix = np.concatenate([cols(k) for k in nnz]).astype(np.uint64)
+    if values == "counts":    # integer counts as f32: low 16 bits zero -> kD8Coded16
+        dv = rng.integers(1, 64, len(ix)).astype(np.float32)
+    elif values == "i32":
+        dv = rng.integers(-50, 5000, len(ix)).astype(np.int32)
+    else:                      # random floats with top-byte escapes -> kD8Coded
+        dv = (rng.random(len(ix)) + 0.25).astype(np.float32)
+        wide = rng.random(len(ix)) < 0.05
+        dv[wide] = (rng.standard_normal(wide.sum()) * 10.0 ** rng.integers(-8, 9, wide.sum())).astype(np.float32)
+    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 64, 2, vdt="i32" if values == "i32" else "f32")
+    return tmp_path / "s", ip, ix, dv, nv
+
+
+@pytest.mark.parametrize("values,raw", [("counts", False), ("floats", False), ("floats", True), ("i32", False)])
+@pytest.mark.parametrize("staging", ["stream_pinned", "resident_coded"])
+def test_fused_densify_from_delta_records(tmp_path, monkeypatch, values, raw, staging):
+    """K3d (densify straight from the staged delta records, no k_d8_decode):
+    bit-exact f32 / bf16 / native dense batches and normalize+log1p within 1e-6,
+    one kernel per batch; RFL_FUSED=0 (decode + idx16 densify) gives the same bytes."""
+    if raw:
+        monkeypatch.setenv("RFL_NARROW_VALUES", "0")  # delta records with raw 4-byte values (kD8Raw)
+    path, ip, ix, dv, nv = _fused_store(tmp_path, values)
+    ds = R.DeviceStore(R.StoreReader(path), 0, staging)
+    assert ds.image_bytes()[1] > 0  # re-encoded staging image (delta records)
+    outs = [("native", None), ("bf16", None)] + ([] if values == "i32" else [("f32", "normalize_log1p")])
+    for od, xf in outs:
+        got = {}
+        for fused in ("1", "0"):
+            monkeypatch.setenv("RFL_FUSED", fused)
+            it = R.BatchIterator(ds, R.LoaderConfig(64, 128, 96, 3), 0, output="dense", out_dtype=od, transform=xf)
+            nb, batches = 0, []
+            for b in it:
+                g = b.global_indices_host
+                eip, eix, edv = csr_gather(ip, ix, dv, g)
+                dense = to_dense(eip, eix, edv, nv)
+                if xf:
+                    want = normalize_log1p(dense.astype(np.float32))
+                    np.testing.assert_allclose(b.data.cpu().numpy().astype(np.float64), want, rtol=1e-6, atol=0)
+                elif od == "bf16":
+                    from oracle.oracle import f32_to_bf16_bits
+                    gb = b.data.view(torch.int16).cpu().numpy().view(np.uint16)
+                    assert (gb == f32_to_bf16_bits(dense.astype(np.float32))).all()
+                else:
+                    assert b.data.cpu().numpy().tobytes() == dense.tobytes()
+                batches.append(b.data.cpu().numpy().tobytes())
+                nb += 1
+            c = it.counters()
+            if fused == "1":
+                assert c.kernels_launched == nb  # no decode launches
+            else:
+                assert c.kernels_launched > nb
+            it.close()
+            got[fused] = batches
+        assert got["1"] == got["0"]
+    ds.close()
+
+
+def test_fused_falls_back_for_long_rows(tmp_path):
+    """A store with a row of 4,082 entries (one past K3d's limit) densifies through
+    k_d8_decode + the idx16 densify instead, still bit-exact."""
+    rng = np.random.default_rng(3)
+    n, nv = 64, 6000
+    nnz = rng.integers(100, 3000, n)
+    nnz[10] = 4082
+    ip = np.zeros(n + 1, np.uint64)
+    ip[1:] = np.cumsum(nnz)
+    ix = np.concatenate([np.sort(rng.choice(nv, k, replace=False)) for k in nnz]).astype(np.uint64)
+    dv = rng.integers(1, 64, len(ix)).astype(np.float32)
+    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 32, 2)
+    it = R.BatchIterator(tmp_path / "s", R.LoaderConfig(32, 64, 64, 0), 0, staging="stream_pinned", output="dense")
+    nb = 0
+    for b in it:
+        eip, eix, edv = csr_gather(ip, ix, dv, b.global_indices_host)
+        assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, nv).tobytes()
+        nb += 1
+    assert it.counters().kernels_launched > nb
+    it.close()
