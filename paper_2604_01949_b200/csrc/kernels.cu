@@ -9,7 +9,6 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
-#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -1711,114 +1710,6 @@ __global__ void __launch_bounds__(kDgThreads)
     if (lane == 0) bulk_wait0();
 }
 
-// TMA-pipelined variant: work unit = (row, SEG input bytes); every warp runs
-// its own NS-stage pipeline -- lane 0 issues 1-D TMA bulk loads of its next
-// units into shared stages (mbarrier completion) NS-1 ahead, and writes each
-// unit back with one bulk store: raw rows straight from the load stage, u8 ->
-// bf16 rows after the warp converted the stage into one of two output stages.
-// Row refs of the next 32 units are read lane-parallel.  Per SM that keeps
-// (NS-1) x SEG x warps of loads in flight with no registers held, which the
-// register-staged kernels above (2 x 16 B per lane) cannot.
-__device__ __forceinline__ void bulk_wait_read1() {
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-template <int MODE, int SEG, int NS, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_dense_gather_tma(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
-                       uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx) {
-    static_assert(MODE == kRaw || MODE == kU8ToBf16, "raw or u8 -> bf16");
-    constexpr uint32_t kOut = MODE == kU8ToBf16 ? 2 : 1;
-    constexpr uint32_t kWarpSmem = NS * SEG + (MODE == kRaw ? 0 : 2 * SEG * kOut);
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ __align__(8) uint64_t bars[WARPS][NS];
-    pdl_wait();
-    pdl_trigger();
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    uint8_t* in_st = smem + warp * kWarpSmem;
-    uint8_t* out_st = in_st + NS * SEG;
-    uint64_t* bar = bars[warp];
-    const uint64_t upr = (in_row_bytes + SEG - 1) / SEG;
-    const uint64_t n_units = n_rows * upr;
-    const uint64_t tw = static_cast<uint64_t>(gridDim.x) * WARPS;
-    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * WARPS + warp;
-    const uint64_t nk = n_units > w0 ? (n_units - w0 + tw - 1) / tw : 0;
-    if (lane == 0) {
-        for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    // lane i: source offset of issue index rb + i
-    uint64_t rb = 0, my_off = 0;
-    auto refresh = [&](uint64_t base) {
-        rb = base;
-        const uint64_t u = w0 + (base + lane) * tw;
-        if (base + lane < nk) {
-            const uint64_t row = u / upr, part = u - row * upr;
-            const RowRef r = refs[row];
-            my_off = r.rec_off + (r.gidx % a.chunk_rows) * in_row_bytes + part * SEG;
-            if (part == 0 && out_gidx) out_gidx[row] = r.gidx;
-        }
-    };
-    refresh(0);
-    auto issue = [&](uint64_t j) {  // whole warp (shuffle); lane 0 issues
-        if (j - rb >= 32) refresh(j);
-        const uint64_t off = __shfl_sync(kFull, my_off, static_cast<int>(j - rb));
-        if (lane == 0) {
-            const uint64_t u = w0 + j * tw, row = u / upr, part = u - row * upr;
-            const uint32_t bytes = static_cast<uint32_t>(umin64(SEG, in_row_bytes - part * SEG));
-            uint64_t* b = &bar[j % NS];
-            mbar_arrive_expect_tx(b, bytes);
-            bulk_load(in_st + (j % NS) * SEG, a.base + off, bytes, b);
-        }
-    };
-    for (uint64_t j = 0; j + 1 < NS && j < nk; ++j) issue(j);
-    for (uint64_t k = 0; k < nk; ++k) {
-        const uint64_t u = w0 + k * tw, row = u / upr, part = u - row * upr;
-        const uint32_t bytes = static_cast<uint32_t>(umin64(SEG, in_row_bytes - part * SEG));
-        const uint32_t st = static_cast<uint32_t>(k % NS);
-        uint8_t* dst = out + row * out_row_bytes + part * SEG * kOut;
-        if (MODE == kRaw) {
-            if (lane == 0) {
-                mbar_wait(&bar[st], static_cast<uint32_t>((k / NS) & 1));
-                bulk_store(dst, in_st + st * SEG, bytes);
-                bulk_commit();
-                bulk_wait_read1();  // store k-1 has read its stage: (k-1) % NS is free
-            }
-            __syncwarp();
-        } else {
-            mbar_wait(&bar[st], static_cast<uint32_t>((k / NS) & 1));
-            if (lane == 0) bulk_wait_read1();  // output stage k % 2 (store k-2) is free
-            __syncwarp();
-            uint8_t* ob = out_st + (k & 1) * SEG * kOut;
-            const uint8_t* ib = in_st + st * SEG;
-            for (uint32_t c = lane; c < bytes / 16; c += 32) {
-                const uint4 v = *reinterpret_cast<const uint4*>(ib + c * 16);
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-                uint32_t o[8];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    o[2 * q] = pack_bf16x2(float(w[q] & 0xff), float((w[q] >> 8) & 0xff));
-                    o[2 * q + 1] = pack_bf16x2(float((w[q] >> 16) & 0xff), float(w[q] >> 24));
-                }
-                *reinterpret_cast<uint4*>(ob + c * 32) = make_uint4(o[0], o[1], o[2], o[3]);
-                *reinterpret_cast<uint4*>(ob + c * 32 + 16) = make_uint4(o[4], o[5], o[6], o[7]);
-            }
-            fence_proxy_async_shared();
-            __syncwarp();
-            if (lane == 0) {
-                bulk_store(dst, ob, bytes * kOut);
-                bulk_commit();
-            }
-        }
-        if (k + NS - 1 < nk) issue(k + NS - 1);
-    }
-    if (lane == 0) bulk_wait0();
-}
-
 // ------------------------------------------------------------ host helpers ---
 
 bool pdl_enabled() {
@@ -2227,33 +2118,9 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         static const int u_sel = [] {
             const char* e = std::getenv("RFL_DG");
             if (!e) return 0;  // automatic
-            if (e[0] == 't') return 100 + (e[1] ? e[1] - '0' : 0);  // TMA-pipelined variant (shape digit)
             if (e[0] == 'b') return e[1] == '4' ? -4 : -2;  // TMA bulk-store variant, 2 or 4 loads per lane
             return e[0] == '4' ? 4 : 2;
         }();
-        // TMA-pipelined kernel: persistent grid (occupancy x SMs, at most one warp per unit)
-        auto go_tma = [&](auto kern, uint64_t seg, uint32_t warps, size_t smem) {
-            set_smem(kern, smem);
-            static std::mutex mu;
-            static std::map<const void*, int> occ_of;
-            int occ = 0;
-            {
-                std::lock_guard<std::mutex> lk(mu);
-                auto it = occ_of.find(reinterpret_cast<const void*>(kern));
-                if (it == occ_of.end()) {
-                    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem), "occupancy");
-                    occ_of[reinterpret_cast<const void*>(kern)] = occ;
-                } else {
-                    occ = it->second;
-                }
-            }
-            const uint64_t units = n * ((in_rb + seg - 1) / seg);
-            const unsigned g2 = static_cast<unsigned>(std::max<uint64_t>(
-                1, std::min<uint64_t>((units + warps - 1) / warps, static_cast<uint64_t>(std::max(occ, 1)) * device_sm_count())));
-            const uint64_t orb = od == OutDtype::bf16 ? a.n_var * 2 : in_rb;
-            launch_k(kern, dim3(g2), dim3(warps * 32), smem, st, "k_dense_gather_tma launch", d, in_rb, refs, n, o, orb,
-                     out_gidx);
-        };
         auto go = [&](auto kern, int U, int T) {
             const uint64_t upr = (in_rb / 16 + 32 * U - 1) / (32 * U);
             const uint64_t warps_needed = n * upr;
@@ -2264,16 +2131,6 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         };
         auto pick = [&](auto mode) {
             constexpr int M = decltype(mode)::value;
-            if constexpr (M == kRaw) {
-                if (u_sel == 100) return go_tma(k_dense_gather_tma<kRaw, 4096, 4, 4>, 4096, 4, 4 * 4 * 4096);
-                if (u_sel == 101) return go_tma(k_dense_gather_tma<kRaw, 8192, 3, 4>, 8192, 4, 4 * 3 * 8192);
-                if (u_sel == 102) return go_tma(k_dense_gather_tma<kRaw, 2048, 6, 8>, 2048, 8, 8 * 6 * 2048);
-            }
-            if constexpr (M == kU8ToBf16) {
-                if (u_sel == 100) return go_tma(k_dense_gather_tma<kU8ToBf16, 2048, 4, 4>, 2048, 4, 4 * (4 * 2048 + 2 * 4096));
-                if (u_sel == 101) return go_tma(k_dense_gather_tma<kU8ToBf16, 4096, 3, 2>, 4096, 2, 2 * (3 * 4096 + 2 * 8192));
-                if (u_sel == 102) return go_tma(k_dense_gather_tma<kU8ToBf16, 1024, 6, 8>, 1024, 8, 8 * (6 * 1024 + 2 * 2048));
-            }
             if (u_sel == 4) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
             if constexpr (M != kF32ToBf16) {
                 // automatic: the u8 -> bf16 expansion writes through TMA bulk stores

@@ -341,7 +341,7 @@ def test_fused_densify_from_delta_records(tmp_path, monkeypatch, values, raw, st
                     assert (gb == f32_to_bf16_bits(dense.astype(np.float32))).all()
                 else:
                     assert b.data.cpu().numpy().tobytes() == dense.tobytes()
-                batches.append(b.data.cpu().numpy().tobytes())
+                batches.append(b.data.view(torch.uint8).cpu().numpy().tobytes())
                 nb += 1
             c = it.counters()
             if fused == "1":
