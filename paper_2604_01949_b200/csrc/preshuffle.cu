@@ -569,6 +569,11 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
         cudaEvent_t ta = nullptr, tb = nullptr;
         cuda_ok(cudaEventCreate(&ta), "event");
         cuda_ok(cudaEventCreate(&tb), "event");
+        static const bool isolate = [] {  // diagnostics: the pack kernel alone on the device
+            const char* e = std::getenv("RFL_PACK_ISOLATE");
+            return e && e[0] == '1';
+        }();
+        if (isolate) cuda_ok(cudaDeviceSynchronize(), "isolate");
         cuda_ok(cudaEventRecord(ta, st_), "event");
         launch_csr_pack(absolute_view(layout_, vdt_, in_idt_, n_var_), reinterpret_cast<const RowRef*>(dp_[ob].p), n,
                         cr, out_idt_, reinterpret_cast<const uint64_t*>(dp_[ob].p + rb), dout.p, st_);
