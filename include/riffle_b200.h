@@ -145,9 +145,11 @@ void rfl_schedule_destroy(rfl_schedule* s);
  *   RFL_STAGE_STREAM_FILE:   records pread (O_DIRECT if cache_bypass) into
  *                            pinned staging buffers, then as above. */
 /*   RFL_STAGE_RESIDENT_CODED: the staging image of stream_pinned (u8 column
- *                            deltas / u16 ids / one-hot codes) held in HBM;
- *                            fetched blocks are expanded device-to-device
- *                            (stores whose verbatim image exceeds HBM). */
+ *                            deltas / u16 ids / one-hot codes) held in HBM
+ *                            (stores whose verbatim image exceeds HBM);
+ *                            dense output of delta records is densified
+ *                            straight from it, other outputs expand the
+ *                            fetched blocks device-to-device. */
 enum { RFL_STAGE_RESIDENT = 0, RFL_STAGE_STREAM_PINNED = 1, RFL_STAGE_STREAM_FILE = 2, RFL_STAGE_RESIDENT_CODED = 3 };
 typedef struct rfl_dstore rfl_dstore;
 rfl_status rfl_dstore_create(rfl_store* s, int device, uint32_t staging, rfl_dstore** out);

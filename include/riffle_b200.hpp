@@ -230,7 +230,7 @@ enum class Staging : std::uint32_t {
     resident = RFL_STAGE_RESIDENT,            // every chunk record in HBM
     stream_pinned = RFL_STAGE_STREAM_PINNED,  // records in pinned host RAM, blocks copied per fetch
     stream_file = RFL_STAGE_STREAM_FILE,      // read-ahead from the files (O_DIRECT with cache_bypass)
-    resident_coded = RFL_STAGE_RESIDENT_CODED,  // re-encoded staging image in HBM, expanded per fetch
+    resident_coded = RFL_STAGE_RESIDENT_CODED,  // re-encoded staging image in HBM (dense output reads it directly)
 };
 enum class Output : std::uint32_t { csr = RFL_OUT_CSR, dense = RFL_OUT_DENSE };
 enum class OutDtype : std::uint32_t { native = RFL_NATIVE, f32 = RFL_F32, bf16 = RFL_BF16 };
