@@ -113,6 +113,16 @@ __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+// `bulk` of the densify kernels: 0 = threads store the tile, 1 = one smem tile written by a
+// TMA bulk store (the next tile waits for it to be read), 2 = two tiles alternating (the next
+// tile is zeroed / scattered while the previous store still drains)
+__device__ __forceinline__ void bulk_tile_wait(int bulk) {
+    if (bulk == 2) bulk_wait_read1();
+    else if (bulk == 1) bulk_wait_read0();
+}
 
 // ------------------------------------------------ 128-bit shifted warp copy ---
 // bytes [sh, sh+16) of the 32-byte little-endian string a||b (sh in 1..15)
@@ -777,6 +787,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     SrcT vA[U], vB[U];
     if (blockIdx.x < n_rows) load_entries<IdxT, SrcT, U>(s_desc[0], tid, nthr, colA, vA);
     uint64_t kk = 0;
+    uint32_t tcount = 0;
+    const uint32_t tile_stride = (tile_cols * static_cast<uint32_t>(sizeof(DstT)) + 127u) & ~127u;
     for (uint64_t row = blockIdx.x; row < n_rows; row += g, ++kk) {
         const RowDesc d = s_desc[kk & 31];
         const bool has_next = row + g < n_rows;
@@ -798,15 +810,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
             scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
         }
         DstT* orow = out + row * n_var;
-        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols, ++tcount) {
             const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
             const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
-            DstT* tile = reinterpret_cast<DstT*>(smem);
-            if (bulk && tid == 0) bulk_wait_read0();
+            uint8_t* tb = smem + (bulk == 2 ? (tcount & 1u) * tile_stride : 0u);
+            DstT* tile = reinterpret_cast<DstT*>(tb);
+            if (tid == 0) bulk_tile_wait(bulk);
             __syncthreads();
-            uint4* t4 = reinterpret_cast<uint4*>(smem);
+            uint4* t4 = reinterpret_cast<uint4*>(tb);
             for (uint32_t i = tid; i < bytes / 16u; i += nthr) t4[i] = make_uint4(0, 0, 0, 0);
-            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) smem[i] = 0;
+            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += nthr) tb[i] = 0;
             __syncthreads();
             const uint32_t c0u = static_cast<uint32_t>(c0);
 #pragma unroll
@@ -821,7 +834,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 fence_proxy_async_shared();
                 __syncthreads();
                 if (tid == 0) {
-                    bulk_store(orow + c0, smem, bytes);
+                    bulk_store(orow + c0, tb, bytes);
                     bulk_commit();
                 }
             } else {
@@ -1035,6 +1048,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
     uint32_t col[16];
     SrcT val[16];
     uint64_t kk = 0;
+    uint32_t tcount = 0;
+    const uint32_t tile_stride = (tile_cols * static_cast<uint32_t>(sizeof(DstT)) + 127u) & ~127u;
     for (uint64_t row = blockIdx.x; row < n_rows; row += g, ++kk) {
         const D8RowDesc d = s_desc[kk & 31];
         decode_d8<SrcT, THREADS>(d, raw, s_scan, col, val);  // (syncs: s_desc reads above are done)
@@ -1055,15 +1070,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
             scale = s != 0.0 ? static_cast<float>(static_cast<double>(target) / s) : 0.0f;
         }
         DstT* orow = out + row * n_var;
-        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols) {
+        for (uint64_t c0 = 0; c0 < n_var; c0 += tile_cols, ++tcount) {
             const uint32_t cols = static_cast<uint32_t>(umin64(tile_cols, n_var - c0));
             const uint32_t bytes = cols * static_cast<uint32_t>(sizeof(DstT));
-            DstT* tile = reinterpret_cast<DstT*>(smem);
-            if (bulk && tid == 0) bulk_wait_read0();
+            uint8_t* tb = smem + (bulk == 2 ? (tcount & 1u) * tile_stride : 0u);
+            DstT* tile = reinterpret_cast<DstT*>(tb);
+            if (tid == 0) bulk_tile_wait(bulk);
             __syncthreads();
-            uint4* t4 = reinterpret_cast<uint4*>(smem);
+            uint4* t4 = reinterpret_cast<uint4*>(tb);
             for (uint32_t i = tid; i < bytes / 16u; i += THREADS) t4[i] = make_uint4(0, 0, 0, 0);
-            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += THREADS) smem[i] = 0;
+            for (uint32_t i = (bytes & ~15u) + tid; i < bytes; i += THREADS) tb[i] = 0;
             __syncthreads();
             const uint32_t c0u = static_cast<uint32_t>(c0);
 #pragma unroll
@@ -1073,7 +1089,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 fence_proxy_async_shared();
                 __syncthreads();
                 if (tid == 0) {
-                    bulk_store(orow + c0, smem, bytes);
+                    bulk_store(orow + c0, tb, bytes);
                     bulk_commit();
                 }
             } else {
@@ -1747,20 +1763,41 @@ void set_smem(K kernel, size_t bytes) {
 // Densify shape override for A/B runs: RFL_DENSIFY="v<6|9>:<threads>:<tile KB>:<U>:<CTAs/SM>"
 // (instantiated shapes: 256:*:16:2, 256:*:8:3, 256:*:8:4; other values fall back to 256:*:8:3).
 struct DensifyCfg {  // version 0 = the measured default (shape rule in densify_t)
-    int version = 0, threads = 256, tile_kb = 40, u = 8, minb = 3;
+    int version = 0, threads = 256, tile_kb = 40, u = 8, minb = 3, nbuf = 1;
 };
 const DensifyCfg& densify_cfg() {
     static const DensifyCfg c = [] {
         DensifyCfg d;
         const char* e = std::getenv("RFL_DENSIFY");
-        int v = 0, t = 256, kb = 40, u = 8, mb = 3;
+        int v = 0, t = 256, kb = 40, u = 8, mb = 3, nb = 1;
         if (e && std::sscanf(e, "v%d", &v) == 1 && (v == 6 || v == 9)) {
-            const int got = std::sscanf(std::strchr(e, ':') ? std::strchr(e, ':') : e + 2, ":%d:%d:%d:%d", &t, &kb, &u, &mb);
+            const int got = std::sscanf(std::strchr(e, ':') ? std::strchr(e, ':') : e + 2, ":%d:%d:%d:%d:%d", &t, &kb,
+                                        &u, &mb, &nb);
             d.version = v;
             if (got >= 1) d.threads = t;
             if (got >= 2 && kb >= 4 && kb <= 200) d.tile_kb = kb;
             if (got >= 3) d.u = u;
             if (got >= 4) d.minb = mb;
+            if (got >= 5 && (nb == 1 || nb == 2)) d.nbuf = nb;
+        }
+        return d;
+    }();
+    return c;
+}
+// K3d shape override: RFL_DENSIFY_D8=<tile KB>:<CTAs/SM 2|3>:<tile buffers 1|2> (A/B)
+struct D8Shape {
+    int tile_kb = 0, minb = 0, nbuf = 0;  // 0 = the default shape rule
+};
+const D8Shape& d8_shape() {
+    static const D8Shape c = [] {
+        D8Shape d;
+        const char* e = std::getenv("RFL_DENSIFY_D8");
+        int kb = 0, mb = 0, nb = 0;
+        if (e && std::sscanf(e, "%d:%d:%d", &kb, &mb, &nb) == 3 && kb >= 4 && kb <= 200 && (mb == 2 || mb == 3) &&
+            (nb == 1 || nb == 2)) {
+            d.tile_kb = kb;
+            d.minb = mb;
+            d.nbuf = nb;
         }
         return d;
     }();
@@ -1769,12 +1806,13 @@ const DensifyCfg& densify_cfg() {
 
 template <typename IdxT, typename SrcT, typename DstT, int THREADS, int U, int MINB, int VAR = 6>
 void densify_v6(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
-                uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes) {
+                uint64_t* out_gidx, cudaStream_t st, uint64_t max_tile_bytes, int nbuf = 1) {
     const uint64_t esz = sizeof(DstT);
     uint64_t tile_cols = av.n_var;
     if (av.n_var * esz > max_tile_bytes) tile_cols = (max_tile_bytes / esz) & ~15ull;
-    const size_t smem = (tile_cols * esz + 127) & ~127ull;
-    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (bulk && VAR == 9 && nbuf == 2 && tile_cols < av.n_var) bulk = 2;  // two alternating tiles (v9 only)
+    const size_t smem = ((tile_cols * esz + 127) & ~127ull) * (bulk == 2 ? 2 : 1);
     auto kern = [] {
         if constexpr (VAR == 9) return k_csr_densify9<IdxT, SrcT, DstT, THREADS, U, MINB>;
         else return k_csr_densify6<IdxT, SrcT, DstT, THREADS, U, MINB>;
@@ -1810,9 +1848,10 @@ void densify_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, f
     const uint64_t tb = static_cast<uint64_t>(dc.tile_kb) * 1024;
     if constexpr (sizeof(IdxT) == 4 && sizeof(SrcT) == 4) {
         if (dc.version == 9) {
-            if (dc.u == 16) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            if (dc.minb == 4) return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
-            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, tb);
+            const int nb = dc.nbuf;
+            if (dc.u == 16) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2, 9>(av, refs, n, norm, target, out, out_gidx, st, tb, nb);
+            if (dc.minb == 4) return densify_v6<IdxT, SrcT, DstT, 256, 8, 4, 9>(av, refs, n, norm, target, out, out_gidx, st, tb, nb);
+            return densify_v6<IdxT, SrcT, DstT, 256, 8, 3, 9>(av, refs, n, norm, target, out, out_gidx, st, tb, nb);
         }
     }
     if (dc.u == 16) return densify_v6<IdxT, SrcT, DstT, 256, 16, 2>(av, refs, n, norm, target, out, out_gidx, st, tb);
@@ -2068,13 +2107,16 @@ void densify_d8_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm
                   uint64_t* out_gidx, cudaStream_t st) {
     // the v9 shape rule: rows wider than 48 KB -> 80 KB tiles at 2 CTAs/SM, else 40 KB at 3
     const uint64_t esz = sizeof(DstT);
+    const D8Shape& ov = d8_shape();
     const bool wide = av.n_var * esz > 48 * 1024;
-    const uint64_t max_tile = wide ? (80u << 10) : (40u << 10);
+    const uint64_t max_tile = ov.tile_kb ? static_cast<uint64_t>(ov.tile_kb) << 10 : wide ? (80u << 10) : (40u << 10);
+    const int minb = ov.minb ? ov.minb : wide ? 2 : 3, nbuf = ov.nbuf ? ov.nbuf : 1;
     uint64_t tile_cols = av.n_var;
     if (av.n_var * esz > max_tile) tile_cols = (max_tile / esz) & ~15ull;
-    const size_t smem = (tile_cols * esz + 127) & ~127ull;
-    const int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    auto kern = wide ? k_csr_densify_d8<SrcT, DstT, 256, 2> : k_csr_densify_d8<SrcT, DstT, 256, 3>;
+    int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (bulk && nbuf == 2 && tile_cols < av.n_var) bulk = 2;
+    const size_t smem = ((tile_cols * esz + 127) & ~127ull) * (bulk == 2 ? 2 : 1);
+    auto kern = minb == 2 ? k_csr_densify_d8<SrcT, DstT, 256, 2> : k_csr_densify_d8<SrcT, DstT, 256, 3>;
     set_smem(kern, smem);
     int per_sm = 0;
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem), "occupancy");
