@@ -798,6 +798,20 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     }
     cuda_ok(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "stream");
     cuda_ok(cudaEventCreateWithFlags(&staged_, cudaEventDisableTiming), "event");
+    if (ds_->staging() == kStreamPinned) {
+        static const unsigned n_lanes = [] {  // RFL_COPY_LANES: copy streams per loader (A/B; default 2)
+            const char* e = std::getenv("RFL_COPY_LANES");
+            const int v = e ? std::atoi(e) : 2;
+            return static_cast<unsigned>(std::max(1, std::min(8, v)));
+        }();
+        lanes_.resize(n_lanes - 1);
+        lane_ev_.resize(n_lanes - 1);
+        for (unsigned l = 0; l + 1 < n_lanes; ++l) {
+            cuda_ok(cudaStreamCreateWithFlags(&lanes_[l], cudaStreamNonBlocking), "stream");
+            cuda_ok(cudaEventCreateWithFlags(&lane_ev_[l], cudaEventDisableTiming), "event");
+        }
+        cuda_ok(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "event");
+    }
     const uint32_t key = dev_.output | (static_cast<uint32_t>(dev_.out_dtype) << 4) | (dev_.normalize ? 1u << 8 : 0u);
     slots_.resize(dev_.out_slots);
     for (auto& s : slots_) {
@@ -859,6 +873,12 @@ GpuLoader::~GpuLoader() {
     for (auto& s : slots_) ds_->give_out(std::move(s));  // the compute stream is drained: reusable as is
     reader_.reset();
     cudaEventDestroy(staged_);
+    for (size_t l = 0; l < lanes_.size(); ++l) {
+        cudaStreamSynchronize(lanes_[l]);
+        cudaStreamDestroy(lanes_[l]);
+        cudaEventDestroy(lane_ev_[l]);
+    }
+    if (fork_ev_) cudaEventDestroy(fork_ev_);
     cudaStreamDestroy(copy_);
     if (own_compute_) cudaStreamDestroy(compute_);
 }
@@ -897,7 +917,8 @@ void GpuLoader::stage_block(uint64_t id) {
                                 ds_->exp_len()[q], ds_->d8_kind(q), 0});
     } else if (ds_->staging() == kStreamPinned) {
         // records of one block are contiguous in the pinned image except for alignment padding;
-        // the copies of all blocks fetched for this batch go out as one cudaMemcpyBatchAsync
+        // the copies of all blocks fetched for this group are issued together, round-robin
+        // over the copy lanes (assemble_group)
         const uint64_t img0 = ds_->img_off()[q0];
         const uint64_t img1 = ds_->img_off()[q1] + ds_->img_len()[q1];
         uint8_t* land = d8 ? lv.slot.ptr + bytes : lv.slot.ptr;  // delta records land after the expanded area
@@ -1132,13 +1153,23 @@ bool GpuLoader::assemble_group() {
         if (pend_ev_ && cudaEventQuery(pend_ev_) != cudaSuccess)
             cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");
         if (!batch_dst_.empty()) {
-            cudaMemcpyAttributes attr{};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-            size_t attr_idx = 0, fail_idx = 0;
-            cuda_ok(cudaMemcpyBatchAsync(batch_dst_.data(), batch_src_.data(), batch_size_.data(), batch_dst_.size(),
-                                         &attr, &attr_idx, 1, &fail_idx, copy_),
-                    "cudaMemcpyBatchAsync");
+            // one cudaMemcpyAsync per piece, dealt round-robin over copy_ and the extra
+            // lanes; the lanes fork from copy_ (after its slot wait) and join back into it
+            const size_t L = std::min(lanes_.size(), batch_dst_.size() - 1);
+            if (L) {
+                cuda_ok(cudaEventRecord(fork_ev_, copy_), "event");
+                for (size_t l = 0; l < L; ++l) cuda_ok(cudaStreamWaitEvent(lanes_[l], fork_ev_, 0), "fork");
+            }
+            for (size_t i = 0; i < batch_dst_.size(); ++i) {
+                const size_t l = i % (L + 1);
+                cuda_ok(cudaMemcpyAsync(batch_dst_[i], batch_src_[i], batch_size_[i], cudaMemcpyHostToDevice,
+                                        l == 0 ? copy_ : lanes_[l - 1]),
+                        "stage H2D");
+            }
+            for (size_t l = 0; l < L; ++l) {
+                cuda_ok(cudaEventRecord(lane_ev_[l], lanes_[l]), "event");
+                cuda_ok(cudaStreamWaitEvent(copy_, lane_ev_[l], 0), "join");
+            }
         }
     } else {
         for (const Planned& p : group_)
