@@ -153,7 +153,8 @@ void rfl_schedule_destroy(rfl_schedule* s);
 enum { RFL_STAGE_RESIDENT = 0, RFL_STAGE_STREAM_PINNED = 1, RFL_STAGE_STREAM_FILE = 2, RFL_STAGE_RESIDENT_CODED = 3 };
 typedef struct rfl_dstore rfl_dstore;
 rfl_status rfl_dstore_create(rfl_store* s, int device, uint32_t staging, rfl_dstore** out);
-/* device address + byte offsets of every chunk record (resident only) */
+/* device address + byte offsets of every chunk record (resident), or of every
+ * staged record of the HBM-resident coded image (resident_coded) */
 rfl_status rfl_dstore_arena(const rfl_dstore* d, void** base, const uint64_t** chunk_offsets,
                             uint64_t* n_chunks);
 /* Decoded record bytes of the store, and bytes of its re-encoded staging
@@ -279,6 +280,14 @@ rfl_status rfl_csr_densify(const rfl_arena_desc* a, const rfl_rowref* d_refs, ui
  * u8/f32 -> bf16 cast. */
 rfl_status rfl_dense_gather(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,
                             uint32_t out_dtype, void* d_out, uint64_t* d_out_gidx, void* stream);
+/* K4o: the same dense row gather, reading rows staged as one-hot channel codes
+ * (a resident_coded one-hot store's arena: rfl_dstore_arena; 2 bits per
+ * position, n_var / 16 bytes per row, n_var % 64 == 0) -- DenseBuffer::take
+ * (loader.cpp:105-117) of the rows the codes stand for; out_dtype
+ * RFL_NATIVE (u8) or RFL_BF16.  Bit-identical to rfl_dense_gather over the
+ * verbatim records. */
+rfl_status rfl_onehot_gather(const rfl_arena_desc* a, const rfl_rowref* d_refs, uint64_t n_rows,
+                             uint32_t out_dtype, void* d_out, uint64_t* d_out_gidx, void* stream);
 
 /* K1 scan only: d_out_prefix[i] = exclusive nnz prefix of the rows,
  * d_out_prefix[n] = total nnz (the pre-shuffle's record offsets). */

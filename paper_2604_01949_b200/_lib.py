@@ -122,6 +122,7 @@ SIGNATURES = [
     ("rfl_csr_gather_prefixed", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp, vp, vp, vp]),
     ("rfl_csr_densify", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, u32, C.c_float, vp, vp, vp]),
     ("rfl_dense_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, vp, vp, vp]),
+    ("rfl_onehot_gather", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u32, vp, vp, vp]),
     ("rfl_csr_scan", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, vp, vp]),
     ("rfl_csr_pack", C.c_int, [C.POINTER(rfl_arena_desc), vp, u64, u64, u32, vp, vp, vp]),
     ("rfl_plan_shuffle", C.c_int, [u64, u64, u64, u64, u64p, vp, vp]),

@@ -274,10 +274,13 @@ rfl_status rfl_dstore_bytes(const rfl_dstore* d, uint64_t* record_bytes, uint64_
 rfl_status rfl_dstore_arena(const rfl_dstore* d, void** base, const uint64_t** offs, uint64_t* n) {
     return guarded([&] {
         if (!d) rfl::invalid("null argument");
-        if (d->ds->staging() != rfl::kResident) rfl::invalid("arena only exists for resident stores");
+        const bool coded = d->ds->staging() == rfl::kResidentCoded;
+        if (d->ds->staging() != rfl::kResident && !coded)
+            rfl::invalid("arena only exists for resident / resident_coded stores");
         if (base) *base = const_cast<uint8_t*>(d->ds->d_arena());
-        if (offs) *offs = d->ds->rec_off().data();
-        if (n) *n = d->ds->rec_off().size();
+        const std::vector<uint64_t>& o = coded ? d->ds->img_off() : d->ds->rec_off();
+        if (offs) *offs = o.data();
+        if (n) *n = o.size();
     });
 }
 
@@ -444,6 +447,14 @@ rfl_status rfl_dense_gather(const rfl_arena_desc* a, const rfl_rowref* refs, uin
     return guarded([&] {
         rfl::launch_dense_gather(to_view(a), reinterpret_cast<const rfl::RowRef*>(refs), n, to_od(out_dtype), out,
                                  out_gidx, static_cast<cudaStream_t>(stream));
+    });
+}
+
+rfl_status rfl_onehot_gather(const rfl_arena_desc* a, const rfl_rowref* refs, uint64_t n, uint32_t out_dtype,
+                             void* out, uint64_t* out_gidx, void* stream) {
+    return guarded([&] {
+        rfl::launch_onehot_gather(to_view(a), reinterpret_cast<const rfl::RowRef*>(refs), n, to_od(out_dtype), out,
+                                  out_gidx, static_cast<cudaStream_t>(stream));
     });
 }
 

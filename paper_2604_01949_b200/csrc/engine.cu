@@ -824,8 +824,11 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     }
     {
         const char* e = std::getenv("RFL_FUSED");  // RFL_FUSED=0: k_d8_decode + idx16 densify (A/B)
-        fused_ = dev_.output == 1 && m.layout == Layout::csr && ds_->d8_fused() && !(e && e[0] == '0') &&
-                 (ds_->staging() == kStreamPinned || ds_->staging() == kResidentCoded);
+        const bool coded = ds_->staging() == kStreamPinned || ds_->staging() == kResidentCoded;
+        // CSR -> dense from delta records (K3d), or dense rows from one-hot records (K4o)
+        fused_ = !(e && e[0] == '0') && coded &&
+                 ((dev_.output == 1 && m.layout == Layout::csr && ds_->d8_fused()) ||
+                  (m.layout == Layout::dense && ds_->d8()));
     }
     direct_ = ds_->staging() == kResident || (ds_->staging() == kResidentCoded && fused_);
     if (!direct_) {
@@ -1211,7 +1214,8 @@ bool GpuLoader::assemble_group() {
                 const Live& lv = live_[gr / cfg_.f];
                 hr[j] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
             }
-            if (fused_) hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
+            if (fused_ && m.layout == Layout::csr)
+                hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
             hg[j] = gr;
         }
     }
@@ -1253,7 +1257,9 @@ bool GpuLoader::assemble_group() {
 
     if (timing) cuda_ok(cudaEventRecord(s.tk[1], compute_), "event");
     const ArenaView av = ds_->view(base);
-    if (m.layout == Layout::dense) {
+    if (m.layout == Layout::dense && fused_) {
+        launch_onehot_gather(av, s.d_refs, n, dev_.out_dtype, s.data, static_cast<uint64_t*>(s.gidx), compute_);
+    } else if (m.layout == Layout::dense) {
         launch_dense_gather(av, s.d_refs, n, dev_.out_dtype, s.data, static_cast<uint64_t*>(s.gidx), compute_);
     } else if (dev_.output == 1 && fused_) {
         launch_csr_densify_d8(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,

@@ -1726,6 +1726,84 @@ __global__ void __launch_bounds__(kDgThreads)
     if (lane == 0) bulk_wait0();
 }
 
+
+// K4o: dense rows straight from one-hot staged records (kOneHot4: 2-bit channel
+// codes, L/4 bytes per row, L = n_var / 4 positions) -- no k_d8_decode expansion.
+// Work unit = (row, 32 x kOhU code words) per warp; a code word covers 16
+// positions, and the lane writes those 16 positions of all 4 channel planes
+// (u8: 4 x 16 B, bf16: 4 x 32 B, f32: 4 x 64 B), so each plane's stores are
+// contiguous across the warp.  Reads 1/16 of what it writes (u8).
+enum OneHotOut { kOhU8 = 0, kOhBf16 = 1, kOhF32 = 2 };
+__device__ __forceinline__ uint32_t onehot_mask16(uint32_t w, uint32_t c) {
+    const uint32_t x = w ^ (c * 0x55555555u);  // a pair is 00 where the code equals c
+    uint32_t m = ~(x | (x >> 1)) & 0x55555555u;
+    m = (m | (m >> 1)) & 0x33333333u;
+    m = (m | (m >> 2)) & 0x0F0F0F0Fu;
+    m = (m | (m >> 4)) & 0x00FF00FFu;
+    return (m | (m >> 8)) & 0x0000FFFFu;  // bit k = position k of the word is in plane c
+}
+template <int OUT, int kOhU = 2, int kOhThreads = 256>
+__global__ void __launch_bounds__(kOhThreads)
+    k_onehot_gather(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint8_t* __restrict__ out,
+                    uint64_t* __restrict__ out_gidx) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : OUT == kOhBf16 ? 2 : 4;  // output element bytes
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t L = a.n_var / 4, wpr = L / 16;  // code words per row
+    const uint64_t upr = (wpr + 32 * kOhU - 1) / (32 * kOhU);
+    const uint64_t n_units = n_rows * upr;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kOhThreads / 32);
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * (kOhThreads / 32) + (threadIdx.x >> 5); u < n_units;
+         u += warps) {
+        const uint64_t row = u / upr, part = u - row * upr;
+        uint64_t off = 0, g = 0;
+        if (lane == 0) {
+            const RowRef r = refs[row];
+            off = (r.rec_off & ((1ull << 60) - 1)) + (r.gidx % a.chunk_rows) * (L / 4);
+            g = r.gidx;
+        }
+        off = __shfl_sync(kFull, off, 0);
+        if (part == 0 && lane == 0 && out_gidx) out_gidx[row] = g;
+        const uint64_t w0 = part * 32 * kOhU + lane;
+        uint32_t w[kOhU];
+#pragma unroll
+        for (int k = 0; k < kOhU; ++k)
+            if (w0 + k * 32 < wpr) w[k] = ld_u32(a.base + off + 4 * (w0 + k * 32));
+        uint8_t* dst = out + row * a.n_var * kEs;
+#pragma unroll
+        for (int k = 0; k < kOhU; ++k) {
+            const uint64_t wi = w0 + k * 32;
+            if (wi >= wpr) break;
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                const uint32_t m = onehot_mask16(w[k], c);
+                uint8_t* p = dst + (c * L + 16 * wi) * kEs;
+                if (OUT == kOhU8) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    st_v4(p, make_uint4(o[0], o[1], o[2], o[3]));
+                } else if (OUT == kOhBf16) {
+                    uint32_t o[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
+                    st_v4(p, make_uint4(o[0], o[1], o[2], o[3]));
+                    st_v4(p + 16, make_uint4(o[4], o[5], o[6], o[7]));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        st_v4(p + 16 * q, make_uint4(((m >> (4 * q)) & 1u) * 0x3F800000u,
+                                                     ((m >> (4 * q + 1)) & 1u) * 0x3F800000u,
+                                                     ((m >> (4 * q + 2)) & 1u) * 0x3F800000u,
+                                                     ((m >> (4 * q + 3)) & 1u) * 0x3F800000u));
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------ host helpers ---
 
 bool pdl_enabled() {
@@ -2206,6 +2284,25 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         invalid("dense_gather: unsupported output dtype for this store");
     }
     cuda_check(cudaGetLastError(), "k_dense_gather launch");
+}
+
+void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, void* out,
+                          uint64_t* out_gidx, cudaStream_t st) {
+    if (a.layout != Layout::dense || a.vdt != VDtype::u8 || a.n_var % 64 != 0)
+        invalid("onehot_gather: needs one-hot staged dense u8 rows with n_var % 64 == 0");
+    if (n == 0) return;
+    const uint64_t wpr = a.n_var / 64, upr = (wpr + 63) / 64;
+    const uint64_t warps_needed = n * upr;
+    const unsigned grid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 7) / 8, 8ull * device_sm_count())));
+    const ArenaDev d = dev_view(a);
+    auto* o = static_cast<uint8_t*>(out);
+    if (od == OutDtype::bf16)
+        launch_k(k_onehot_gather<kOhBf16>, dim3(grid), dim3(256), 0, st, "k_onehot_gather launch", d, refs, n, o, out_gidx);
+    else if (od == OutDtype::f32)  // as launch_dense_gather: u8 rows cast to bf16 only
+        invalid("dense_gather: unsupported output dtype for this store");
+    else
+        launch_k(k_onehot_gather<kOhU8>, dim3(grid), dim3(256), 0, st, "k_onehot_gather launch", d, refs, n, o, out_gidx);
 }
 
 }  // namespace rfl

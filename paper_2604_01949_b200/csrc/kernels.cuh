@@ -164,6 +164,11 @@ constexpr uint64_t kD8FusedMaxNnz = 16 * 256 - 15;
 void launch_csr_densify_d8(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
                            float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);
 
+// K4o: dense output straight from kOneHot4 staged records (2-bit channel codes);
+// refs[i].rec_off = staged record offset.  od: native (u8) / f32 / bf16.
+void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, void* out,
+                          uint64_t* out_gidx, cudaStream_t st);
+
 // K4
 void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, void* out,
                          uint64_t* out_gidx, cudaStream_t st);

@@ -399,3 +399,43 @@ def test_batches_per_launch(golden, golden_stores, staging, group):
             assert (c.read_ops, c.bytes_read, c.chunks_decoded) == (ld["read_ops"], ld["bytes_read"],
                                                                     ld["chunks_decoded"])
             it.close()
+
+
+@pytest.mark.parametrize("n_var", [64, 4096, 8192])
+def test_raw_onehot_gather_random_rows(tmp_path, n_var):
+    """rfl_onehot_gather (K4o) over a resident_coded one-hot store's arena on
+    arbitrary row lists (repeats, any order): bit-identical to rfl_dense_gather
+    over the verbatim resident records and to the numpy row gather, u8 and bf16."""
+    path = tmp_path / "oh"
+    R.synth_store(path, R.SynthConfig(n_obs=1500, n_var=n_var, layout="dense", value_dtype="u8", seed=4,
+                                      chunk_rows=128, chunks_per_shard=4, one_hot=4))
+    x = load_dense_store(path).reshape(1500, n_var)
+    coded = R.DeviceStore(path, 0, "resident_coded")
+    plain = R.DeviceStore(path, 0, "resident")
+    assert coded.image_bytes()[1] * 16 <= coded.image_bytes()[0] + 16 * 256 * 12
+    rng = np.random.default_rng(1)
+    for n in (1, 33, 1000, 4097):
+        g = rng.integers(0, 1500, n).astype(np.uint64)
+        for od, esz in ((L.NATIVE, 1), (L.BF16, 2)):
+            outs = []
+            for ds, fn in ((coded, L.lib().rfl_onehot_gather), (plain, L.lib().rfl_dense_gather)):
+                desc = ds.arena_desc()
+                refs = _arena_refs(ds, g)
+                out = torch.full((n * n_var * esz,), 0x5A, dtype=torch.uint8, device="cuda")
+                og = torch.zeros(n, dtype=torch.int64, device="cuda")
+                L.check(fn(C.byref(desc), refs.data_ptr(), n, od, out.data_ptr(), og.data_ptr(), None))
+                torch.cuda.synchronize()
+                assert (og.cpu().numpy().view(np.uint64) == g).all()
+                outs.append(out.cpu().numpy())
+            want = x[g.astype(np.int64)]
+            if od == L.BF16:
+                want = u8_to_bf16_bits(want)
+            assert outs[0].tobytes() == want.tobytes()
+            assert outs[1].tobytes() == outs[0].tobytes()
+    with pytest.raises(R.InvalidArgument):  # u8 rows cast to bf16 only, as rfl_dense_gather
+        desc = coded.arena_desc()
+        refs = _arena_refs(coded, np.zeros(1, np.uint64))
+        out = torch.zeros(4 * n_var, dtype=torch.uint8, device="cuda")
+        L.check(L.lib().rfl_onehot_gather(C.byref(desc), refs.data_ptr(), 1, L.F32, out.data_ptr(), None, None))
+    coded.close()
+    plain.close()

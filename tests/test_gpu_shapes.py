@@ -192,11 +192,12 @@ def test_cfg4_one_hot_vs_reference(stores, staging):
     ds.close()
 
 
-@pytest.mark.parametrize("n_var", [48, 4000, 4096 + 16, 256])
+@pytest.mark.parametrize("n_var", [48, 4000, 4096 + 16, 256, 64, 8192])
 def test_one_hot_staging_widths(tmp_path, n_var):
     """One-hot rows whose width is not a multiple of 64 bytes stage verbatim (the
     2-bit decode needs 16-B chunks inside one channel plane); multiples of 64 use
-    the coded image.  Bit-exact either way."""
+    the coded image, read straight by K4o (64: one code word per row, 8192: two
+    work units per row).  Bit-exact either way."""
     R.synth_store(tmp_path / "s", R.SynthConfig(700, n_var, "dense", "u8", seed=9, chunk_rows=64,
                                                 chunks_per_shard=4, one_hot=4))
     x = load_dense_store(tmp_path / "s")
@@ -208,7 +209,7 @@ def test_one_hot_staging_widths(tmp_path, n_var):
     assert seen == 700
     c = it.counters()
     if n_var % 64 == 0:  # 2-bit codes (1/16 of the row bytes) + the 16-B row references
-        assert c.h2d_bytes <= c.bytes_read / 8
+        assert c.h2d_bytes <= c.bytes_read * (1 / 16 + 16 / n_var) * 1.25
     else:
         assert c.h2d_bytes >= c.bytes_read
 

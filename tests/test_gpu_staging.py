@@ -126,12 +126,17 @@ def test_staging_encodings_bit_exact(crafted, mode):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("staging", ["stream_pinned", "resident_coded"])
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("out_dtype", ["native", "bf16"])
-def test_one_hot_dense_staging(tmp_path, out_dtype):
+def test_one_hot_dense_staging(tmp_path, out_dtype, fused, staging, monkeypatch):
     """BASELINE config 4's one-hot windows: a dense u8 store whose rows are one-hot
     over 4 channel planes stages as 2-bit codes (16x fewer PCIe bytes) and is
-    rebuilt on the GPU; batches equal the reference's row gather bit for bit.
-    A single non-one-hot byte anywhere keeps the verbatim image."""
+    rebuilt on the GPU -- by K4o straight from the codes (default) or by
+    k_d8_decode + the dense gather (RFL_FUSED=0); batches equal the reference's
+    row gather bit for bit, 3 batches per launch included.  A single non-one-hot
+    byte anywhere keeps the verbatim image (resident_coded then refuses)."""
+    monkeypatch.setenv("RFL_FUSED", fused)
     from oracle.oracle import load_dense_store, u8_to_bf16_bits
     for broken in (False, True):
         path = tmp_path / f"oh{int(broken)}"
@@ -143,8 +148,13 @@ def test_one_hot_dense_staging(tmp_path, out_dtype):
             raw[100] = 2
             shard.write_bytes(bytes(raw))
         x = load_dense_store(path).reshape(700, 256)
-        ds = R.DeviceStore(path, 0, "stream_pinned")
-        it = R.BatchIterator(ds, R.LoaderConfig(32, 160, 64, 9), 0, output="dense", out_dtype=out_dtype)
+        if broken and staging == "resident_coded":
+            with pytest.raises(R.InvalidArgument):
+                R.DeviceStore(path, 0, staging)
+            continue
+        ds = R.DeviceStore(path, 0, staging)
+        it = R.BatchIterator(ds, R.LoaderConfig(32, 160, 64, 9), 0, output="dense", out_dtype=out_dtype,
+                             batches_per_launch=3)
         n = 0
         for b in it:
             g = b.global_indices_host.astype(np.int64)
@@ -159,8 +169,10 @@ def test_one_hot_dense_staging(tmp_path, out_dtype):
         c = it.counters()
         if broken:
             assert c.h2d_bytes >= c.bytes_read
-        else:
+        elif staging == "stream_pinned":
             assert c.h2d_bytes < c.bytes_read / 4  # codes are 1/16 of the rows; row refs (16 B) on top
+        if not broken:  # 11 batches in 4 groups of <= 3: K4o is one launch per group, no decode
+            assert c.kernels_launched == 4 if fused == "1" else c.kernels_launched > 4
         it.close()
         ds.close()
 
