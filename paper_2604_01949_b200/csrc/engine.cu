@@ -798,20 +798,6 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     }
     cuda_ok(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking), "stream");
     cuda_ok(cudaEventCreateWithFlags(&staged_, cudaEventDisableTiming), "event");
-    if (ds_->staging() == kStreamPinned) {
-        static const unsigned n_lanes = [] {  // RFL_COPY_LANES: copy streams per loader (A/B; default 2)
-            const char* e = std::getenv("RFL_COPY_LANES");
-            const int v = e ? std::atoi(e) : 2;
-            return static_cast<unsigned>(std::max(1, std::min(8, v)));
-        }();
-        lanes_.resize(n_lanes - 1);
-        lane_ev_.resize(n_lanes - 1);
-        for (unsigned l = 0; l + 1 < n_lanes; ++l) {
-            cuda_ok(cudaStreamCreateWithFlags(&lanes_[l], cudaStreamNonBlocking), "stream");
-            cuda_ok(cudaEventCreateWithFlags(&lane_ev_[l], cudaEventDisableTiming), "event");
-        }
-        cuda_ok(cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming), "event");
-    }
     const uint32_t key = dev_.output | (static_cast<uint32_t>(dev_.out_dtype) << 4) | (dev_.normalize ? 1u << 8 : 0u);
     slots_.resize(dev_.out_slots);
     for (auto& s : slots_) {
@@ -876,12 +862,6 @@ GpuLoader::~GpuLoader() {
     for (auto& s : slots_) ds_->give_out(std::move(s));  // the compute stream is drained: reusable as is
     reader_.reset();
     cudaEventDestroy(staged_);
-    for (size_t l = 0; l < lanes_.size(); ++l) {
-        cudaStreamSynchronize(lanes_[l]);
-        cudaStreamDestroy(lanes_[l]);
-        cudaEventDestroy(lane_ev_[l]);
-    }
-    if (fork_ev_) cudaEventDestroy(fork_ev_);
     cudaStreamDestroy(copy_);
     if (own_compute_) cudaStreamDestroy(compute_);
 }
@@ -920,8 +900,7 @@ void GpuLoader::stage_block(uint64_t id) {
                                 ds_->exp_len()[q], ds_->d8_kind(q), 0});
     } else if (ds_->staging() == kStreamPinned) {
         // records of one block are contiguous in the pinned image except for alignment padding;
-        // the copies of all blocks fetched for this group are issued together, round-robin
-        // over the copy lanes (assemble_group)
+        // the copies of all blocks fetched for this group are issued together (assemble_group)
         const uint64_t img0 = ds_->img_off()[q0];
         const uint64_t img1 = ds_->img_off()[q1] + ds_->img_len()[q1];
         uint8_t* land = d8 ? lv.slot.ptr + bytes : lv.slot.ptr;  // delta records land after the expanded area
@@ -1156,22 +1135,33 @@ bool GpuLoader::assemble_group() {
         if (pend_ev_ && cudaEventQuery(pend_ev_) != cudaSuccess)
             cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");
         if (!batch_dst_.empty()) {
-            // one cudaMemcpyAsync per piece, dealt round-robin over copy_ and the extra
-            // lanes; the lanes fork from copy_ (after its slot wait) and join back into it
-            const size_t L = std::min(lanes_.size(), batch_dst_.size() - 1);
-            if (L) {
-                cuda_ok(cudaEventRecord(fork_ev_, copy_), "event");
-                for (size_t l = 0; l < L; ++l) cuda_ok(cudaStreamWaitEvent(lanes_[l], fork_ev_, 0), "fork");
-            }
-            for (size_t i = 0; i < batch_dst_.size(); ++i) {
-                const size_t l = i % (L + 1);
-                cuda_ok(cudaMemcpyAsync(batch_dst_[i], batch_src_[i], batch_size_[i], cudaMemcpyHostToDevice,
-                                        l == 0 ? copy_ : lanes_[l - 1]),
-                        "stage H2D");
-            }
-            for (size_t l = 0; l < L; ++l) {
-                cuda_ok(cudaEventRecord(lane_ev_[l], lanes_[l]), "event");
-                cuda_ok(cudaStreamWaitEvent(copy_, lane_ev_[l], 0), "join");
+            // the group's block copies: ONE TMA pull kernel on the copy stream (default), or
+            // one copy-engine transfer per block (RFL_STAGE=ce; ~4.7 us setup each)
+            static const bool ce = [] {
+                const char* e = std::getenv("RFL_STAGE");
+                return e && std::string(e) == "ce";
+            }();
+            if (ce) {
+                for (size_t i = 0; i < batch_dst_.size(); ++i)
+                    cuda_ok(cudaMemcpyAsync(batch_dst_[i], batch_src_[i], batch_size_[i], cudaMemcpyHostToDevice,
+                                            copy_),
+                            "stage H2D");
+            } else {
+                const uint64_t P = stage_pull_piece_bytes();
+                for (size_t i0 = 0; i0 < batch_dst_.size(); i0 += kMaxPullJobs) {
+                    pull_.n = static_cast<uint32_t>(std::min<size_t>(kMaxPullJobs, batch_dst_.size() - i0));
+                    pull_.first_piece[0] = 0;
+                    for (uint32_t k = 0; k < pull_.n; ++k) {
+                        // 16-B multiples: records sit at 16-B aligned image offsets with zeroed gaps,
+                        // and slots hold the aligned sizes
+                        const uint64_t bytes = align_up(batch_size_[i0 + k], kAlign);
+                        pull_.job[k] = {static_cast<const uint8_t*>(batch_src_[i0 + k]),
+                                        static_cast<uint8_t*>(batch_dst_[i0 + k]), bytes};
+                        pull_.first_piece[k + 1] = pull_.first_piece[k] + static_cast<uint32_t>((bytes + P - 1) / P);
+                    }
+                    launch_stage_pull(pull_, copy_);
+                    ctr_.kernels_launched += 1;
+                }
             }
         }
     } else {

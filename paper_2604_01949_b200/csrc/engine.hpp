@@ -320,15 +320,10 @@ private:
     uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
     std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead
     uint64_t read_seq_ = 0;
-    std::vector<void*> batch_dst_, batch_src_;  // stream_pinned copies of one group, spread over the copy lanes
+    std::vector<void*> batch_dst_, batch_src_;  // stream_pinned copies of one group (one pull kernel)
     std::vector<D8Job> d8_jobs_;                 // delta-staged records of this next() to expand
     std::vector<size_t> batch_size_;
-    // stream_pinned: extra copy streams; a group's block copies go round-robin over
-    // copy_ + lanes_ (fork / join events), so one copy's setup gap on the link is
-    // hidden behind another lane's transfer
-    std::vector<cudaStream_t> lanes_;
-    std::vector<cudaEvent_t> lane_ev_;
-    cudaEvent_t fork_ev_ = nullptr;
+    PullJobs pull_;                              // the pull kernel's job table (by value)
     mutable Counters ctr_;
     bool done_ = false;
     uint64_t batch_seq_ = 0;

@@ -14,6 +14,7 @@
 #include <string>
 #include <utility>
 #include <type_traits>
+#include <array>
 #include <cstdio>
 #include <cstring>
 
@@ -1804,6 +1805,62 @@ __global__ void __launch_bounds__(kOhThreads)
     }
 }
 
+
+// ======================================================== staging pull ===
+// Host -> HBM staging of a group's fetched blocks by TMA instead of one copy-engine
+// transfer per block: each copy engine transfer pays a fixed ~4.7 us setup
+// (37 GB/s for cfg1's ~0.5 MB blocks, profiles/r2/s3/pcie_staging.md), while 1-D
+// bulk loads of the mapped pinned image into shared stages + bulk stores to the
+// slots keep ~2 MB in flight across a small grid (51 GB/s, any block size).
+// One thread per CTA; the CTAs take the (job, piece) pairs round-robin.
+__global__ void __launch_bounds__(32) k_stage_pull(const __grid_constant__ PullJobs jobs, uint32_t P, uint32_t S) {
+    extern __shared__ __align__(128) uint8_t pull_smem[];
+    __shared__ __align__(8) uint64_t bar[kMaxPullStages];
+    pdl_wait();
+    if (threadIdx.x != 0) return;
+    const uint32_t total = jobs.first_piece[jobs.n];
+    for (uint32_t s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // global piece g -> (job, byte offset): binary search of the per-job piece prefix
+    auto locate = [&](uint32_t g, uint32_t& bytes) -> uint64_t {
+        uint32_t lo = 0, hi = jobs.n;  // first_piece[lo] <= g < first_piece[hi]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (jobs.first_piece[mid] <= g) lo = mid;
+            else hi = mid;
+        }
+        const uint64_t off = static_cast<uint64_t>(g - jobs.first_piece[lo]) * P;
+        const uint64_t left = jobs.job[lo].bytes - off;
+        bytes = static_cast<uint32_t>(left < P ? left : P);
+        return (static_cast<uint64_t>(lo) << 40) | off;
+    };
+    uint32_t phases = 0, issue = blockIdx.x, done = blockIdx.x, si = 0, sd = 0;
+    auto load = [&](uint32_t g, uint32_t slot) {
+        uint32_t bytes;
+        const uint64_t jo = locate(g, bytes);
+        const PullJob& jb = jobs.job[jo >> 40];
+        mbar_arrive_expect_tx(&bar[slot], bytes);
+        bulk_load(pull_smem + slot * P, jb.src + (jo & ((1ull << 40) - 1)), bytes, &bar[slot]);
+    };
+    for (uint32_t k = 0; k < S && issue < total; ++k, issue += gridDim.x, si = si + 1 == S ? 0 : si + 1)
+        load(issue, si);
+    for (; done < total; done += gridDim.x) {
+        mbar_wait(&bar[sd], (phases >> sd) & 1u);
+        phases ^= 1u << sd;
+        uint32_t bytes;
+        const uint64_t jo = locate(done, bytes);
+        bulk_store(jobs.job[jo >> 40].dst + (jo & ((1ull << 40) - 1)), pull_smem + sd * P, bytes);
+        bulk_commit();
+        bulk_wait_read0();  // the stage is free again
+        if (issue < total) {
+            load(issue, sd);
+            issue += gridDim.x;
+        }
+        sd = sd + 1 == S ? 0 : sd + 1;
+    }
+    bulk_wait0();
+}
+
 // ------------------------------------------------------------ host helpers ---
 
 bool pdl_enabled() {
@@ -2303,6 +2360,37 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         invalid("dense_gather: unsupported output dtype for this store");
     else
         launch_k(k_onehot_gather<kOhU8>, dim3(grid), dim3(256), 0, st, "k_onehot_gather launch", d, refs, n, o, out_gidx);
+}
+
+namespace {
+// RFL_PULL=<piece KB>:<stages>:<CTAs> (A/B; default 16 KB x 4 stages x 32 CTAs = 2 MB in flight)
+const std::array<uint32_t, 3>& pull_shape() {
+    static const std::array<uint32_t, 3> v = [] {
+        std::array<uint32_t, 3> x{16, 4, 32};
+        if (const char* e = std::getenv("RFL_PULL")) std::sscanf(e, "%u:%u:%u", &x[0], &x[1], &x[2]);
+        x[0] = std::max(1u, std::min(64u, x[0]));
+        x[1] = std::max(2u, std::min<uint32_t>(kMaxPullStages, x[1]));
+        x[2] = std::max(1u, std::min(256u, x[2]));
+        if (x[0] * x[1] > 192) x[1] = 192 / x[0];
+        return x;
+    }();
+    return v;
+}
+}  // namespace
+
+uint32_t stage_pull_piece_bytes() { return pull_shape()[0] << 10; }
+
+void launch_stage_pull(const PullJobs& jobs, cudaStream_t st) {
+    if (jobs.n == 0) return;
+    const uint32_t P = pull_shape()[0] << 10, S = pull_shape()[1];
+    static const bool attr = [] {
+        set_smem(k_stage_pull, 192u << 10);
+        return true;
+    }();
+    (void)attr;
+    const uint32_t total = jobs.first_piece[jobs.n];
+    const unsigned grid = std::max(1u, std::min(pull_shape()[2], total));
+    launch_k(k_stage_pull, dim3(grid), dim3(32), static_cast<size_t>(P) * S, st, "k_stage_pull launch", jobs, P, S);
 }
 
 }  // namespace rfl

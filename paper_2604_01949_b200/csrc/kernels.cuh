@@ -164,6 +164,24 @@ constexpr uint64_t kD8FusedMaxNnz = 16 * 256 - 15;
 void launch_csr_densify_d8(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
                            float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);
 
+// Staging pull: copy jobs (16-B aligned host-mapped src, 16-B aligned device dst,
+// bytes a multiple of 16) moved by TMA bulk loads/stores from a small grid, on
+// `st` (stream_pinned staging; replaces one copy-engine transfer per block).
+constexpr uint32_t kMaxPullJobs = 256;
+constexpr uint32_t kMaxPullStages = 8;
+struct PullJob {
+    const uint8_t* src;
+    uint8_t* dst;
+    uint64_t bytes;
+};
+struct PullJobs {
+    uint32_t n;
+    uint32_t first_piece[kMaxPullJobs + 1];  // exclusive prefix of ceil(bytes / piece bytes)
+    PullJob job[kMaxPullJobs];
+};
+uint32_t stage_pull_piece_bytes();
+void launch_stage_pull(const PullJobs& jobs, cudaStream_t st);
+
 // K4o: dense output straight from kOneHot4 staged records (2-bit channel codes);
 // refs[i].rec_off = staged record offset.  od: native (u8) / f32 / bf16.
 void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, void* out,
