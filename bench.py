@@ -64,7 +64,7 @@ WORKLOADS = {
                  synth=dict(n_obs=5_000_000, n_var=4096, layout="dense", value_dtype="u8", density=0.1, seed=3,
                             chunk_rows=512, chunks_per_shard=128, one_hot=4),
                  loader=dict(fetch_block_rows=512, buffer_capacity_rows=16384, batch_rows=2048, seed=0),
-                 out=dict(output="dense", out_dtype="native", transform=None), dtype="u8", group=4, e2e_group=8,
+                 out=dict(output="dense", out_dtype="native", transform=None), dtype="u8", group=10, e2e_group=8,
                  # the value leg reads the rows from the store's HBM-resident coded image (2-bit channel
                  # codes, 1/16 of the records) like cfg2's: K4o writes each one-hot row from its codes
                  value_staging="resident_coded"),

@@ -1,38 +1,65 @@
-"""Where the end-to-end loader step goes: host time inside BatchIterator.next(),
-device time per step, staged bytes, for one bench workload (stream_pinned)."""
-import json
+"""Where the host time of an e2e step goes (cfg1 / cfg4 stores from bench.py):
+per next_many(G) call, the C call (rfl_loader_next_many: replay hand-off,
+staging pull launch, assembly launch) vs the Python wrapping of the G batches
+vs the per-step D2H read of the result ids, over N steps.
+
+usage: python scripts/e2e_probe.py [cfg4|cfg1] [G] [steps]
+"""
+import ctypes as C
+import os
 import sys
 import time
 from pathlib import Path
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_2604_01949_b200 as R  # noqa: E402
+from paper_2604_01949_b200 import _lib as L  # noqa: E402
 
-wl = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+wl = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+G = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else 400
 W = bench.WORKLOADS[wl]
 path = bench.ensure_store(wl, 0, 1, None)
-t = time.perf_counter()
-ds = R.DeviceStore(R.StoreReader(path), 0, sys.argv[3] if len(sys.argv) > 3 else "stream_pinned")
-t_ds = time.perf_counter() - t
+ds = R.DeviceStore(R.StoreReader(path), 0, os.environ.get("RIFFLE_E2E_STAGING", "stream_pinned"))
 stream = torch.cuda.current_stream()
-it = R.BatchIterator(ds, R.LoaderConfig(**W["loader"], prefetch_depth=4), 0, output=W["out"]["output"],
-                     out_dtype=W["out"]["out_dtype"], transform=W["out"]["transform"], out_slots=3, stream=stream)
-host = torch.empty(W["loader"]["batch_rows"], dtype=torch.int64).pin_memory()
-rows = []
-for k in range(steps):
-    t0 = time.perf_counter()
-    b = it.next()
-    t1 = time.perf_counter()
-    host[:b.n_rows].copy_(b.global_indices, non_blocking=True)
-    torch.cuda.synchronize()
-    t2 = time.perf_counter()
-    c = it.counters()
-    rows.append({"step": k, "next_ms": (t1 - t0) * 1e3, "sync_ms": (t2 - t1) * 1e3, "h2d_MB": c.h2d_bytes / 1e6,
-                 "blocks": c.blocks_fetched})
-print(json.dumps({"workload": wl, "dstore_s": t_ds, "steps": rows}))
+cfg = R.LoaderConfig(**W["loader"], prefetch_depth=4)
+it = R.BatchIterator(ds, cfg, 0, output=W["out"]["output"], out_dtype=W["out"]["out_dtype"],
+                     transform=W["out"]["transform"], out_slots=3, stream=stream, batches_per_launch=G)
+host = torch.empty(W["loader"]["batch_rows"] * G, dtype=torch.int64).pin_memory()
+arr = (L.rfl_batch * G)()
+n = C.c_uint32()
+t_c = t_wrap = t_d2h = 0.0
+done = 0
+for warm in (True, False):
+    if not warm:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+    k = 0
+    while k < (4 * G if warm else steps):
+        a = time.perf_counter()
+        rc = L.check(L.lib().rfl_loader_next_many(it._h, arr, G, C.byref(n)))
+        b = time.perf_counter()
+        bs = [it._wrap(arr[i]) for i in range(n.value)]
+        c = time.perf_counter()
+        for bb in bs:
+            host[:bb.n_rows].copy_(bb.global_indices, non_blocking=True)
+        d = time.perf_counter()
+        if not warm:
+            t_c += b - a
+            t_wrap += c - b
+            t_d2h += d - c
+        k += n.value
+    if not warm:
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        done = k
+rows = done * W["loader"]["batch_rows"]
+print({"workload": wl, "G": G, "steps": done, "wall_ms": wall * 1e3, "rows_per_s": rows / wall,
+       "us_per_step": {"c_call": 1e6 * t_c / done, "wrap": 1e6 * t_wrap / done, "d2h": 1e6 * t_d2h / done,
+                       "total": 1e6 * wall / done},
+       "h2d_bytes_per_step": it.counters().h2d_bytes / (done + 4 * G)})
