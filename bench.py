@@ -58,13 +58,15 @@ WORKLOADS = {
                  synth=dict(n_obs=2_000_000, n_var=12288, layout="dense", value_dtype="u8", density=0.1, seed=2,
                             chunk_rows=256, chunks_per_shard=128),
                  loader=dict(fetch_block_rows=256, buffer_capacity_rows=16384, batch_rows=1024, seed=0),
-                 out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16", group=2, e2e_group=4),
+                 out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16", group=2, e2e_group=4,
+                 e2e_min_steps=200),
     "cfg4": dict(desc="cfg4: dense 4x1024 one-hot u8 windows (5M, procedural one-hot: one channel per position), "
                       "chunk 512, f=512 B=16384 b=2048, raw u8",
                  synth=dict(n_obs=5_000_000, n_var=4096, layout="dense", value_dtype="u8", density=0.1, seed=3,
                             chunk_rows=512, chunks_per_shard=128, one_hot=4),
                  loader=dict(fetch_block_rows=512, buffer_capacity_rows=16384, batch_rows=2048, seed=0),
                  out=dict(output="dense", out_dtype="native", transform=None), dtype="u8", group=10, e2e_group=8,
+                 e2e_min_steps=800,
                  # the value leg reads the rows from the store's HBM-resident coded image (2-bit channel
                  # codes, 1/16 of the records) like cfg2's: K4o writes each one-hot row from its codes
                  value_staging="resident_coded"),
@@ -559,7 +561,9 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist, staging=None):
     # whole groups only: the warm-up ends on a group boundary and the timed steps are a
     # multiple of G, so every group assembled inside the timed region is counted in full
     Wm = -(-Wm // G) * G
-    K = -(-K // G) * G
+    # workloads with ~10-30 us steps time at least e2e_min_steps of them (a 20-step region
+    # would be ~1 ms, dominated by the first group's ramp); the count is in the line
+    K = -(-max(K, W.get("e2e_min_steps", 0)) // G) * G
 
     def make_it(e):
         return R.BatchIterator(ds, cfg, e, output=W["out"]["output"], out_dtype=W["out"]["out_dtype"],

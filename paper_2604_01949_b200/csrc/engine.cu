@@ -837,6 +837,8 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
         }
     }
     footer_seen_.assign(m.shard_count(), 0);
+    div_chunk_ = FastDiv(m.chunk_rows);
+    div_f_ = FastDiv(cfg_.f);
     // every output slot sized for a full group up front (first-use cudaMalloc /
     // cudaHostAlloc would stall the first groups' steps)
     for (auto& s : slots_) ensure_capacity(s, static_cast<uint64_t>(std::max<uint32_t>(1, dev_.group)) * cfg_.b, 0);
@@ -1195,19 +1197,20 @@ bool GpuLoader::assemble_group() {
         RowRef* hr = s.h_refs + group_start_[i];
         uint64_t* hg = s.h_gidx + group_start_[i];
         const std::vector<uint64_t>& gv = group_[i].gidx;
+        const uint64_t* offs = resident ? (fused_ ? ds_->img_off().data() : ds_->rec_off().data()) : nullptr;
+        const bool kinds = fused_ && m.layout == Layout::csr;
         for (size_t j = 0; j < gv.size(); ++j) {
             const uint64_t gr = gv[j];
-            const uint64_t q = gr / m.chunk_rows;
+            const uint64_t q = div_chunk_.div(gr);
             if (resident) {
-                hr[j] = {fused_ ? ds_->img_off()[q] : ds_->rec_off()[q], gr};
+                hr[j] = {offs[q], gr};
             } else {
-                const Live& lv = live_[gr / cfg_.f];
+                const Live& lv = live_[div_f_.div(gr)];
                 hr[j] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
             }
-            if (fused_ && m.layout == Layout::csr)
-                hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
-            hg[j] = gr;
+            if (kinds) hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
         }
+        std::memcpy(hg, gv.data(), gv.size() * sizeof(uint64_t));
     }
     cuda_ok(cudaMemcpyAsync(s.d_refs, s.h_refs, n * sizeof(RowRef), cudaMemcpyHostToDevice, copy_), "refs H2D");
     ctr_.h2d_bytes += n * sizeof(RowRef);
@@ -1276,7 +1279,7 @@ bool GpuLoader::assemble_group() {
     if (!resident) {
         for (const Planned& p : group_)
             for (uint64_t gr : p.gidx) {
-                Live& lv = live_[gr / cfg_.f];
+                Live& lv = live_[div_f_.div(gr)];
                 if (--lv.live_rows == 0) {
                     cuda_ok(cudaEventRecord(lv.slot.released, compute_), "event");
                     lv.slot.owner = id_;

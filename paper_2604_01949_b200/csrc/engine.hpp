@@ -31,6 +31,26 @@ constexpr uint64_t kRecPad = 256;
 // Staging images are page-locked in pieces of this size (one registration per
 // piece, staging.cpp); a host->device copy never crosses a piece boundary.
 constexpr uint64_t kPinPiece = 1ull << 30;
+
+// n / d for the per-row loops of a group (tens of thousands of rows per call):
+// a shift for powers of two, else Lemire's multiply-high (exact for 32-bit n
+// and d), else the hardware divide
+struct FastDiv {
+    uint64_t d = 1, m = 0;
+    unsigned sh = 0;
+    bool pow2 = true;
+    FastDiv() = default;
+    explicit FastDiv(uint64_t dv) : d(dv ? dv : 1) {
+        pow2 = (d & (d - 1)) == 0;
+        while ((1ull << sh) < d) ++sh;
+        m = d <= 0xFFFFFFFFull ? ~0ull / d + 1 : 0;
+    }
+    uint64_t div(uint64_t n) const {
+        if (pow2) return n >> sh;
+        if (m && n <= 0xFFFFFFFFull) return static_cast<uint64_t>((static_cast<unsigned __int128>(m) * n) >> 64);
+        return n / d;
+    }
+};
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 // resident: verbatim records in HBM; stream_pinned: staging image in pinned host
@@ -317,6 +337,7 @@ private:
     // rows read in place from a device-resident image (resident, or resident_coded + fused_): no slots
     bool direct_ = false;
     std::vector<Live> live_;                 // indexed by block id (streaming)
+    FastDiv div_chunk_, div_f_;              // row -> chunk, row -> block
     uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
     std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead
     uint64_t read_seq_ = 0;

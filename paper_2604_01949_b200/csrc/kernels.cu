@@ -1806,6 +1806,84 @@ __global__ void __launch_bounds__(kOhThreads)
 }
 
 
+// K4o through shared memory: the warp builds its unit's output (32 x kOhU code
+// words = 512 x kOhU positions of each of the 4 planes) in one of two shared
+// slices and one lane writes it with 1-D TMA bulk stores (one per plane segment,
+// one for the whole row when the unit is the row); the other slice is filled
+// while that store drains.  A/B: RFL_OH=bulk.
+template <int OUT, int kOhU = 2, int kOhWarps = 4>
+__global__ void __launch_bounds__(kOhWarps * 32)
+    k_onehot_gather_bulk(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint8_t* __restrict__ out,
+                         uint64_t* __restrict__ out_gidx) {
+    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : 2;
+    constexpr uint32_t kSeg = 32 * kOhU * 16 * kEs;  // bytes of one plane's segment of a unit
+    extern __shared__ __align__(128) uint8_t oh_smem[];
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint8_t* slices = oh_smem + warp * 2 * 4 * kSeg;
+    const uint64_t L = a.n_var / 4, wpr = L / 16;
+    const uint64_t upr = (wpr + 32 * kOhU - 1) / (32 * kOhU);
+    const uint64_t n_units = n_rows * upr;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * kOhWarps;
+    uint32_t it = 0;
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * kOhWarps + warp; u < n_units; u += warps, ++it) {
+        const uint64_t row = u / upr, part = u - row * upr;
+        uint64_t off = 0, g = 0;
+        if (lane == 0) {
+            const RowRef r = refs[row];
+            off = (r.rec_off & ((1ull << 60) - 1)) + (r.gidx % a.chunk_rows) * (L / 4);
+            g = r.gidx;
+        }
+        off = __shfl_sync(kFull, off, 0);
+        if (part == 0 && lane == 0 && out_gidx) out_gidx[row] = g;
+        const uint64_t wb = part * 32 * kOhU, nw = umin64(32 * kOhU, wpr - wb);  // words of this unit
+        uint32_t w[kOhU];
+#pragma unroll
+        for (int k = 0; k < kOhU; ++k)
+            if (k * 32 + lane < nw) w[k] = ld_u32(a.base + off + 4 * (wb + k * 32 + lane));
+        uint8_t* sl = slices + (it & 1u) * 4 * kSeg;
+        if (lane == 0) bulk_wait_read1();  // this slice's store (two units ago) has been read
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < kOhU; ++k) {
+            const uint32_t wi = k * 32 + lane;
+            if (wi >= nw) break;
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                const uint32_t m = onehot_mask16(w[k], c);
+                uint8_t* p = sl + c * kSeg + wi * 16 * kEs;
+                if (OUT == kOhU8) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                } else {
+                    uint32_t o[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<uint4*>(p + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+                }
+            }
+        }
+        fence_proxy_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+            uint8_t* dst = out + row * a.n_var * kEs;
+            const uint32_t seg = static_cast<uint32_t>(nw * 16 * kEs);
+            if (upr == 1 && seg == kSeg) {
+                bulk_store(dst, sl, 4 * kSeg);  // the whole row: the 4 plane segments are adjacent
+            } else {
+                for (uint32_t c = 0; c < 4; ++c) bulk_store(dst + (c * L + wb * 16) * kEs, sl + c * kSeg, seg);
+            }
+            bulk_commit();
+        }
+    }
+    if (lane == 0) bulk_wait0();
+}
+
 // ======================================================== staging pull ===
 // Host -> HBM staging of a group's fetched blocks by TMA instead of one copy-engine
 // transfer per block: each copy engine transfer pays a fixed ~4.7 us setup
@@ -2354,6 +2432,24 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 7) / 8, 8ull * device_sm_count())));
     const ArenaDev d = dev_view(a);
     auto* o = static_cast<uint8_t*>(out);
+    static const bool bulk = [] {
+        const char* e = std::getenv("RFL_OH");
+        return e && std::string(e) == "bulk";
+    }();
+    if (bulk && od != OutDtype::f32) {
+        const uint32_t es = od == OutDtype::bf16 ? 2 : 1;
+        const size_t smem = 4 * 2 * 4 * (32 * 2 * 16 * es);  // 4 warps x 2 slices x 4 planes x segment
+        const unsigned g4 = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 3) / 4, 16ull * device_sm_count())));
+        auto kern = od == OutDtype::bf16 ? k_onehot_gather_bulk<kOhBf16> : k_onehot_gather_bulk<kOhU8>;
+        static bool attr[2] = {false, false};
+        if (!attr[es - 1]) {
+            set_smem(kern, smem);
+            attr[es - 1] = true;
+        }
+        launch_k(kern, dim3(g4), dim3(128), smem, st, "k_onehot_gather_bulk launch", d, refs, n, o, out_gidx);
+        return;
+    }
     if (od == OutDtype::bf16)
         launch_k(k_onehot_gather<kOhBf16>, dim3(grid), dim3(256), 0, st, "k_onehot_gather launch", d, refs, n, o, out_gidx);
     else if (od == OutDtype::f32)  // as launch_dense_gather: u8 rows cast to bf16 only
