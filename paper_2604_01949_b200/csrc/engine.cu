@@ -171,6 +171,20 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
     }
 }
 
+bool DStore::pull_ok() const {
+    if (pull_ok_ < 0) {
+        bool ok = h_image_ != nullptr;
+        const uint64_t bytes = h_map_bytes_ ? h_map_bytes_ : image_bytes_ + kPad;
+        for (uint64_t o = 0; ok && o < bytes; o += kPinPiece) {
+            void* dp = nullptr;
+            ok = cudaHostGetDevicePointer(&dp, h_image_ + o, 0) == cudaSuccess && dp == h_image_ + o;
+        }
+        cudaGetLastError();
+        pull_ok_ = ok ? 1 : 0;
+    }
+    return pull_ok_ == 1;
+}
+
 void DStore::free_host_image() {
     if (!h_image_) return;
     if (h_map_bytes_) {
@@ -249,7 +263,7 @@ void DStore::load_records(bool to_device) {
         cuda_ok(cudaMalloc(&d_arena_, image_bytes_ + kPad), "cudaMalloc arena");
         cuda_ok(cudaMemset(d_arena_ + image_bytes_, 0, kPad), "cudaMemset pad");
     } else {
-        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&h_image_), image_bytes_ + kPad, cudaHostAllocPortable),
+        cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&h_image_), image_bytes_ + kPad, cudaHostAllocPortable | cudaHostAllocMapped),
                 "cudaHostAlloc image");
     }
     uint64_t max_rec = 0;
@@ -408,7 +422,7 @@ void DStore::deflate_layout() { deflate_record_lengths(*hs_, rec_len_, row_nnz_.
 void DStore::load_records_deflate(bool to_device) {
     const Manifest& m = hs_->manifest();
     const uint64_t nch = m.chunk_count();
-    cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&h_image_), image_bytes_ + kPad, cudaHostAllocPortable),
+    cuda_ok(cudaHostAlloc(reinterpret_cast<void**>(&h_image_), image_bytes_ + kPad, cudaHostAllocPortable | cudaHostAllocMapped),
             "cudaHostAlloc image");
     std::memset(h_image_ + image_bytes_, 0, kPad);
     parallel_chunks(nch, [&](uint64_t q) {
@@ -458,9 +472,7 @@ DStore::~DStore() {
     DeviceGuard g(device_);
     for (auto& b : out_pool_) b.free_all();
     for (auto& pb : pinned_pool_) cudaFreeHost(pb.first);
-    for (auto& kv : free_)
-        for (auto& s : kv.second)
-            if (s.released) cudaEventDestroy(s.released);
+    for (cudaEvent_t e : ev_all_) cudaEventDestroy(e);
     for (void* p : slabs_) cudaFree(p);
     if (d_arena_) cudaFree(d_arena_);
     free_host_image();
@@ -511,7 +523,6 @@ void DStore::grow_slab(uint64_t slot_bytes) {
         SlotRef s;
         s.ptr = static_cast<uint8_t*>(slab) + i * slot_bytes;
         s.bytes = slot_bytes;
-        cuda_ok(cudaEventCreateWithFlags(&s.released, cudaEventDisableTiming), "event");
         pool.push_back(s);
     }
 }
@@ -596,6 +607,30 @@ void DStore::give_out(OutBuffers&& b) {
 void DStore::release_slot(const SlotRef& s) {
     std::lock_guard<std::mutex> lk(mu_);
     free_[s.bytes].push_back(s);
+}
+
+std::vector<cudaEvent_t> DStore::take_events(size_t n) {
+    std::lock_guard<std::mutex> lk(mu_);
+    std::vector<cudaEvent_t> out;
+    while (out.size() < n && !ev_free_.empty()) {
+        out.push_back(ev_free_.back());
+        ev_free_.pop_back();
+    }
+    while (out.size() < n) {
+        cudaEvent_t e = nullptr;
+        cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        ev_all_.push_back(e);
+        out.push_back(e);
+    }
+    return out;
+}
+
+// (the giving loader has drained its stream: every record of these events is complete,
+// so slots still pointing at them wait on nothing, or on a later point of a later user)
+void DStore::give_events(std::vector<cudaEvent_t>&& ev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    ev_free_.insert(ev_free_.end(), ev.begin(), ev.end());
+    ev.clear();
 }
 
 // ============================================================ BlockReader ===
@@ -837,6 +872,7 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
         }
     }
     footer_seen_.assign(m.shard_count(), 0);
+    if (!direct_) rel_ring_ = ds_->take_events(kReleaseRing);
     div_chunk_ = FastDiv(m.chunk_rows);
     div_f_ = FastDiv(cfg_.f);
     // every output slot sized for a full group up front (first-use cudaMalloc /
@@ -856,11 +892,14 @@ GpuLoader::~GpuLoader() {
     DeviceGuard g(ds_->device());
     if (compute_) cudaStreamSynchronize(compute_);
     if (copy_) cudaStreamSynchronize(copy_);
+    cudaEvent_t last = rel_ring_.empty() ? nullptr : rel_ring_[rel_pos_ % rel_ring_.size()];
+    if (last) cudaEventRecord(last, compute_);
     for (auto& l : live_)
         if (l.slot.ptr) {
-            cudaEventRecord(l.slot.released, compute_);
+            l.slot.released = last;
             ds_->release_slot(l.slot);
         }
+    if (!rel_ring_.empty()) ds_->give_events(std::move(rel_ring_));
     for (auto& s : slots_) ds_->give_out(std::move(s));  // the compute stream is drained: reusable as is
     reader_.reset();
     cudaEventDestroy(staged_);
@@ -885,11 +924,13 @@ void GpuLoader::stage_block(uint64_t id) {
     lv.slot = ds_->acquire_slot(block_bytes_);
     lv.live_rows = e - s;
     // the slot's previous kernel readers are done (skip the stream wait if already complete)
-    if (ds_->staging() == kStreamPinned && lv.slot.owner == id_) {
+    if (ds_->staging() == kStreamPinned && lv.slot.owner == id_ && lv.slot.released) {
         if (!pend_ev_ || lv.slot.seq >= pend_seq_) {  // coalesced into one wait in next()
             pend_ev_ = lv.slot.released;
             pend_seq_ = lv.slot.seq;
         }
+    } else if (!lv.slot.released) {
+        // never used: nothing to wait for
     } else if (coded) {  // the decode writes the slot on compute_, where this loader's releases were recorded
         if (lv.slot.owner != id_ && cudaEventQuery(lv.slot.released) != cudaSuccess)
             cuda_ok(cudaStreamWaitEvent(compute_, lv.slot.released, 0), "wait slot");
@@ -1143,7 +1184,7 @@ bool GpuLoader::assemble_group() {
                 const char* e = std::getenv("RFL_STAGE");
                 return e && std::string(e) == "ce";
             }();
-            if (ce) {
+            if (ce || !ds_->pull_ok()) {
                 for (size_t i = 0; i < batch_dst_.size(); ++i)
                     cuda_ok(cudaMemcpyAsync(batch_dst_[i], batch_src_[i], batch_size_[i], cudaMemcpyHostToDevice,
                                             copy_),
@@ -1205,8 +1246,10 @@ bool GpuLoader::assemble_group() {
             if (resident) {
                 hr[j] = {offs[q], gr};
             } else {
-                const Live& lv = live_[div_f_.div(gr)];
+                const uint64_t blk = div_f_.div(gr);
+                Live& lv = live_[blk];
                 hr[j] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
+                if (--lv.live_rows == 0) done_blocks_.push_back(blk);  // released after this group's kernel
             }
             if (kinds) hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
         }
@@ -1276,18 +1319,18 @@ bool GpuLoader::assemble_group() {
     ++batch_seq_;
 
     // blocks whose rows are all taken go back to the pool once this group's kernel is done
-    if (!resident) {
-        for (const Planned& p : group_)
-            for (uint64_t gr : p.gidx) {
-                Live& lv = live_[div_f_.div(gr)];
-                if (--lv.live_rows == 0) {
-                    cuda_ok(cudaEventRecord(lv.slot.released, compute_), "event");
-                    lv.slot.owner = id_;
-                    lv.slot.seq = batch_seq_;
-                    ds_->release_slot(lv.slot);
-                    lv.slot = DStore::SlotRef{};
-                }
-            }
+    if (!done_blocks_.empty()) {
+        cudaEvent_t e = rel_ring_[rel_pos_++ % rel_ring_.size()];
+        cuda_ok(cudaEventRecord(e, compute_), "event");
+        for (uint64_t blk : done_blocks_) {
+            Live& lv = live_[blk];
+            lv.slot.released = e;
+            lv.slot.owner = id_;
+            lv.slot.seq = batch_seq_;
+            ds_->release_slot(lv.slot);
+            lv.slot = DStore::SlotRef{};
+        }
+        done_blocks_.clear();
     }
 
     size_t n_blocks = 0;

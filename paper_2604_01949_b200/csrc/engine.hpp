@@ -133,6 +133,9 @@ public:
     uint32_t staging() const { return staging_; }
     const uint8_t* d_arena() const { return d_arena_; }
     const uint8_t* h_image() const { return h_image_; }
+    // the pinned image is device-addressable at its host address (every registered
+    // piece): the staging pull kernel reads it in place; else copy-engine transfers
+    bool pull_ok() const;
     const std::vector<uint64_t>& rec_off() const { return rec_off_; }
     const std::vector<uint64_t>& rec_len() const { return rec_len_; }    // decoded record bytes
     const std::vector<uint64_t>& slot_len() const { return slot_len_; }  // stored (encoded) bytes
@@ -160,7 +163,7 @@ public:
     // streaming slot pool (shared by the iterators over this store)
     struct SlotRef {
         uint8_t* ptr = nullptr;
-        cudaEvent_t released = nullptr;  // recorded after the last kernel reading it
+        cudaEvent_t released = nullptr;  // recorded after the last kernel reading it (null: never used)
         uint64_t bytes = 0;
         uint64_t owner = 0;           // id of the loader that recorded `released` (on its compute stream) ...
         uint64_t seq = 0;             // ... after its batch `seq`
@@ -170,6 +173,11 @@ public:
     // steady-state epoch never allocates (cudaMalloc stalls the device)
     void reserve_slots(uint64_t bytes, uint64_t n);
     void release_slot(const SlotRef& s);
+    // release events: a loader records ONE event per group on its compute stream and
+    // every slot freed by that group points at it (SlotRef::released); the events
+    // live as long as the store, handed out / back per loader
+    std::vector<cudaEvent_t> take_events(size_t n);
+    void give_events(std::vector<cudaEvent_t>&& ev);
     // output-buffer pool shared by the iterators over this store
     OutBuffers take_out(uint32_t key);
     void give_out(OutBuffers&& b);
@@ -200,10 +208,12 @@ private:
     uint8_t* h_image_ = nullptr;
     uint64_t h_map_bytes_ = 0;     // > 0: h_image_ is an mmap'd staging image (else cudaHostAlloc)
     bool h_registered_ = false;    // ... page-locked with cudaHostRegister
+    mutable int pull_ok_ = -1;     // pull_ok() cache
     uint64_t staged_bytes_ = 0;    // bytes of the staging image
     std::mutex mu_;
     void grow_slab(uint64_t slot_bytes);  // mu_ held
     std::vector<void*> slabs_;
+    std::vector<cudaEvent_t> ev_free_, ev_all_;
     // per slot size, FIFO: reuse the slot released longest ago (its readers are done)
     std::map<uint64_t, std::deque<SlotRef>> free_;
     std::vector<OutBuffers> out_pool_;
@@ -338,6 +348,13 @@ private:
     bool direct_ = false;
     std::vector<Live> live_;                 // indexed by block id (streaming)
     FastDiv div_chunk_, div_f_;              // row -> chunk, row -> block
+    // one release event per group, from a ring of kReleaseRing store-owned events: a
+    // ring event is re-recorded only kReleaseRing groups later on the same stream, so a
+    // slot still pointing at it waits on a later point of that stream (never earlier)
+    static constexpr size_t kReleaseRing = 256;
+    std::vector<cudaEvent_t> rel_ring_;
+    size_t rel_pos_ = 0;
+    std::vector<uint64_t> done_blocks_;      // blocks whose last rows this group took
     uint64_t block_bytes_ = 0;               // slot size: staged bytes of the largest block
     std::unique_ptr<BlockReader> reader_;        // stream_file read-ahead
     uint64_t read_seq_ = 0;

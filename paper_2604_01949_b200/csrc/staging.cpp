@@ -305,7 +305,7 @@ bool DStore::build_staged_image(uint32_t mode) {
         // 1 GiB piece of it registers; copies never cross a piece boundary
         // (stage_block splits them), so the pieces behave as one pinned image
         for (uint64_t o = 0; o < used; o += kPinPiece) {
-            const cudaError_t rc = cudaHostRegister(img + o, std::min(kPinPiece, used - o), cudaHostRegisterPortable);
+            const cudaError_t rc = cudaHostRegister(img + o, std::min(kPinPiece, used - o), cudaHostRegisterPortable | cudaHostRegisterMapped);
             if (rc != cudaSuccess) {
                 for (uint64_t u = 0; u < o; u += kPinPiece) cudaHostUnregister(img + u);
                 munmap(img, used);

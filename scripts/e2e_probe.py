@@ -28,8 +28,15 @@ path = bench.ensure_store(wl, 0, 1, None)
 ds = R.DeviceStore(R.StoreReader(path), 0, os.environ.get("RIFFLE_E2E_STAGING", "stream_pinned"))
 stream = torch.cuda.current_stream()
 cfg = R.LoaderConfig(**W["loader"], prefetch_depth=4)
-it = R.BatchIterator(ds, cfg, 0, output=W["out"]["output"], out_dtype=W["out"]["out_dtype"],
-                     transform=W["out"]["transform"], out_slots=3, stream=stream, batches_per_launch=G)
+epoch = 0
+
+
+def mk(e):
+    return R.BatchIterator(ds, cfg, e, output=W["out"]["output"], out_dtype=W["out"]["out_dtype"],
+                           transform=W["out"]["transform"], out_slots=3, stream=stream, batches_per_launch=G)
+
+
+it = mk(0)
 host = torch.empty(W["loader"]["batch_rows"] * G, dtype=torch.int64).pin_memory()
 arr = (L.rfl_batch * G)()
 n = C.c_uint32()
@@ -43,6 +50,11 @@ for warm in (True, False):
     while k < (4 * G if warm else steps):
         a = time.perf_counter()
         rc = L.check(L.lib().rfl_loader_next_many(it._h, arr, G, C.byref(n)))
+        if rc == L.END:  # next epoch (as open_epoch), inside the timed region like bench.py's e2e leg
+            epoch += 1
+            it.close()
+            it = mk(epoch)
+            continue
         b = time.perf_counter()
         bs = [it._wrap(arr[i]) for i in range(n.value)]
         c = time.perf_counter()
@@ -62,4 +74,4 @@ rows = done * W["loader"]["batch_rows"]
 print({"workload": wl, "G": G, "steps": done, "wall_ms": wall * 1e3, "rows_per_s": rows / wall,
        "us_per_step": {"c_call": 1e6 * t_c / done, "wrap": 1e6 * t_wrap / done, "d2h": 1e6 * t_d2h / done,
                        "total": 1e6 * wall / done},
-       "h2d_bytes_per_step": it.counters().h2d_bytes / (done + 4 * G)})
+       "epochs": epoch + 1})
