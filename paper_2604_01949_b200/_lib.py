@@ -57,7 +57,7 @@ class rfl_batch(C.Structure):
     _fields_ = [("epoch_index", u64), ("batch_index", u64), ("n_rows", u64), ("nnz", u64), ("n_var", u64),
                 ("layout", u32), ("dtype", u32), ("index_dtype", u32), ("reserved", u32),
                 ("d_gidx", vp), ("d_indptr", vp), ("d_indices", vp), ("d_data", vp),
-                ("h_gidx", u64p), ("ready_event", vp)]
+                ("h_gidx", vp), ("ready_event", vp)]  # h_gidx: const uint64_t* (read as an address)
 
 
 class rfl_loader_counters(C.Structure):

@@ -235,6 +235,7 @@ class BatchIterator:
         self._b = L.rfl_batch()
         self._many = (L.rfl_batch * 1)()
         self._views = {}
+        self._hviews = {}
 
     def _view(self, ptr, shape, np_dtype):
         """cuda_tensor, cached: the loader's output slots are a fixed ring, so the
@@ -246,6 +247,16 @@ class BatchIterator:
                 self._views.clear()
             t = self._views[key] = cuda_tensor(ptr, shape, np_dtype, self.device)
         return t
+
+    def _host_view(self, addr, n):
+        """numpy view of the loader's pinned host ids (a fixed ring like the device views)."""
+        key = (addr, n)
+        v = self._hviews.get(key)
+        if v is None:
+            if len(self._hviews) > 256:
+                self._hviews.clear()
+            v = self._hviews[key] = np.ctypeslib.as_array((C.c_uint64 * n).from_address(addr))
+        return v
 
     def next(self) -> DeviceBatch | None:
         rc = L.check(L.lib().rfl_loader_next(self._h, C.byref(self._b)))
@@ -269,7 +280,7 @@ class BatchIterator:
             import torch
             L.check(L.lib().rfl_batch_wait(C.byref(b), C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
         n = b.n_rows
-        gh = np.ctypeslib.as_array(b.h_gidx, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
+        gh = self._host_view(b.h_gidx, n).copy() if n else np.zeros(0, np.uint64)
         g = self._view(b.d_gidx, (n,), np.int64)
         if b.layout == L.LAYOUT_CSR:
             idt = np.uint32 if b.index_dtype == L.IDX_U32 else np.uint64
