@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -195,6 +196,48 @@ private:
     PinBuf h_stage_[2], h_refs_, h_prefix_, ring_[2];
     cudaEvent_t stage_ev_[2] = {nullptr, nullptr}, ring_ev_[2] = {nullptr, nullptr}, packed_[2] = {nullptr, nullptr};
     cudaStream_t wst_ = nullptr;                  // the writer's D2H stream
+    // pack / D2H gate: the record pack never runs beside a D2H piece of an earlier
+    // round (the pack waits for the pieces already issued; the writer issues no new
+    // piece while a pack is launched but not finished).  A piece is 64 MB (~1.2 ms)
+    // against a round of ~100+ ms of file writes, so the e2e does not move; the pack
+    // gets the HBM to itself.  RFL_PACK_GATE=0 turns it off (A/B).
+    bool gate_on_ = true;
+    std::mutex gate_mu_;
+    std::condition_variable gate_cv_;
+    bool gate_busy_ = false;                      // a pack is being enqueued
+    uint64_t gate_seq_ = 0, gate_seen_ = 0;       // packs enqueued / known complete
+    cudaEvent_t gate_ev_ = nullptr, wgate_ = nullptr;
+    void gate_begin() {
+        if (!gate_on_) return;
+        std::lock_guard<std::mutex> lk(gate_mu_);
+        gate_busy_ = true;
+        cuda_ok(cudaEventRecord(wgate_, wst_), "event");  // every piece issued so far
+        cuda_ok(cudaStreamWaitEvent(st_, wgate_, 0), "wait D2H");
+    }
+    void gate_end() {
+        if (!gate_on_) return;
+        {
+            std::lock_guard<std::mutex> lk(gate_mu_);
+            cuda_ok(cudaEventRecord(gate_ev_, st_), "event");
+            gate_busy_ = false;
+            ++gate_seq_;
+        }
+        gate_cv_.notify_all();
+    }
+    // writer side: returns with the lock held once no pack is pending or running
+    std::unique_lock<std::mutex> gate_wait() {
+        std::unique_lock<std::mutex> lk(gate_mu_);
+        if (!gate_on_) return lk;
+        for (;;) {
+            gate_cv_.wait(lk, [&] { return !gate_busy_; });
+            if (gate_seen_ == gate_seq_) return lk;
+            const uint64_t s = gate_seq_;
+            lk.unlock();
+            cuda_ok(cudaEventSynchronize(gate_ev_), "pack done");  // (the newest record: covers pack s)
+            lk.lock();
+            if (gate_seen_ < s) gate_seen_ = s;
+        }
+    }
     std::shared_future<void> wjob_[2], last_job_;  // writer job that drains d_out_[k]; the newest job
     uint64_t emits_ = 0;
     void drain_writes() {
@@ -574,10 +617,12 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
             return e && e[0] == '1';
         }();
         if (isolate) cuda_ok(cudaDeviceSynchronize(), "isolate");
+        gate_begin();
         cuda_ok(cudaEventRecord(ta, st_), "event");
         launch_csr_pack(absolute_view(layout_, vdt_, in_idt_, n_var_), reinterpret_cast<const RowRef*>(dp_[ob].p), n,
                         cr, out_idt_, reinterpret_cast<const uint64_t*>(dp_[ob].p + rb), dout.p, st_);
         cuda_ok(cudaEventRecord(tb, st_), "event");
+        gate_end();
         timing_.emplace_back(ta, tb);
     } else if (layout_ == Layout::csr) {
         const ArenaView av = absolute_view(layout_, vdt_, in_idt_, n_var_);
@@ -646,6 +691,7 @@ void GpuShuffler::emit(const std::vector<RowRef>& refs, const std::vector<std::p
                     const uint64_t pieces = (total + S - 1) / S;
                     auto issue = [&](uint64_t i) {
                         const uint64_t off = i * S, len = std::min(S, total - off);
+                        std::unique_lock<std::mutex> lk = gate_wait();  // held while the piece is enqueued
                         cuda_ok(cudaMemcpyAsync(ring_[i & 1].p, src + off, len, cudaMemcpyDeviceToHost, wst_), "D2H");
                         cuda_ok(cudaEventRecord(ring_ev_[i & 1], wst_), "event");
                     };
@@ -793,6 +839,8 @@ GpuShuffler::~GpuShuffler() {
             cudaEventDestroy(ring_ev_[k]);
             cudaEventDestroy(packed_[k]);
         }
+        cudaEventDestroy(gate_ev_);
+        cudaEventDestroy(wgate_);
         cudaStreamDestroy(wst_);
     }
     if (st_) {
@@ -889,6 +937,9 @@ void GpuShuffler::init() {
     DeviceGuard g(a_.device);
     cuda_ok(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
     cuda_ok(cudaStreamCreateWithFlags(&wst_, cudaStreamNonBlocking), "stream");
+    cuda_ok(cudaEventCreateWithFlags(&gate_ev_, cudaEventDisableTiming), "event");
+    cuda_ok(cudaEventCreateWithFlags(&wgate_, cudaEventDisableTiming), "event");
+    if (const char* ge = std::getenv("RFL_PACK_GATE")) gate_on_ = ge[0] != '0';
     for (int k = 0; k < 2; ++k) {  // pinned staging / output rings, allocated once (cudaHostAlloc is slow)
         h_stage_[k].ensure(kStageBytes);
         ring_[k].ensure(kPieceBytes);
