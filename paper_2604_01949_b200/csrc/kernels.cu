@@ -1884,6 +1884,70 @@ __global__ void __launch_bounds__(kOhWarps * 32)
     if (lane == 0) bulk_wait0();
 }
 
+// K4o, tiled (default): a CTA builds R consecutive output rows (a contiguous
+// R x row-bytes range of the batch, <= 32 KB) in one of two shared tiles and one
+// thread writes the tile with a single 1-D TMA bulk store -- the large-tile store
+// path that reaches ~5.8 TB/s for write-heavy mixes (profiles/r2/mix_bw_b.jsonl);
+// the next tile's codes are loaded and its rows built while that store drains.
+template <int OUT>
+__global__ void __launch_bounds__(256)
+    k_onehot_gather_tile(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t R,
+                         uint8_t* __restrict__ out, uint64_t* __restrict__ out_gidx) {
+    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : 2;
+    extern __shared__ __align__(128) uint8_t oh_tiles[];
+    __shared__ uint64_t s_off[64];
+    pdl_wait();
+    pdl_trigger();
+    const uint64_t L = a.n_var / 4, wpr = L / 16;          // code words per row
+    const uint64_t row_bytes = a.n_var * kEs;
+    const uint32_t tile_bytes = static_cast<uint32_t>(R * row_bytes);
+    const uint64_t n_tiles = (n_rows + R - 1) / R;
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+        const uint64_t r0 = t * R;
+        const uint32_t rows = static_cast<uint32_t>(umin64(R, n_rows - r0));
+        if (threadIdx.x < rows) {
+            const RowRef r = refs[r0 + threadIdx.x];
+            s_off[threadIdx.x] = (r.rec_off & ((1ull << 60) - 1)) + (r.gidx % a.chunk_rows) * (L / 4);
+            if (out_gidx) out_gidx[r0 + threadIdx.x] = r.gidx;
+        }
+        uint8_t* tile = oh_tiles + (it & 1u) * tile_bytes;
+        if (threadIdx.x == 0) bulk_wait_read1();  // this tile's store (two tiles ago) has read it
+        __syncthreads();
+        const uint32_t words = rows * static_cast<uint32_t>(wpr);
+        for (uint32_t k = threadIdx.x; k < words; k += 256) {
+            const uint32_t rr = k / static_cast<uint32_t>(wpr), wi = k - rr * static_cast<uint32_t>(wpr);
+            const uint32_t w = ld_u32(a.base + s_off[rr] + 4ull * wi);
+            uint8_t* rowp = tile + rr * row_bytes;
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                const uint32_t m = onehot_mask16(w, c);
+                uint8_t* p = rowp + (c * L + 16ull * wi) * kEs;
+                if (OUT == kOhU8) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                } else {
+                    uint32_t o[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<uint4*>(p + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+                }
+            }
+        }
+        fence_proxy_async_shared();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            bulk_store(out + r0 * row_bytes, tile, static_cast<uint32_t>(rows * row_bytes));
+            bulk_commit();
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait0();
+}
+
 // ======================================================== staging pull ===
 // Host -> HBM staging of a group's fetched blocks by TMA instead of one copy-engine
 // transfer per block: each copy engine transfer pays a fixed ~4.7 us setup
@@ -2432,10 +2496,33 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 7) / 8, 8ull * device_sm_count())));
     const ArenaDev d = dev_view(a);
     auto* o = static_cast<uint8_t*>(out);
-    static const bool bulk = [] {
+    static const int variant = [] {  // RFL_OH=plain | bulk (A/B); default: tiled
         const char* e = std::getenv("RFL_OH");
-        return e && std::string(e) == "bulk";
+        if (e && std::string(e) == "bulk") return 1;
+        if (e && std::string(e) == "plain") return 2;
+        return 0;
     }();
+    const bool bulk = variant == 1;
+    const uint64_t row_bytes = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
+    if (variant == 0 && od != OutDtype::f32 && row_bytes <= (32u << 10)) {
+        const uint32_t R = static_cast<uint32_t>(std::min<uint64_t>(64, (32u << 10) / row_bytes));
+        const size_t smem = 2ull * R * row_bytes;
+        auto kern = od == OutDtype::bf16 ? k_onehot_gather_tile<kOhBf16> : k_onehot_gather_tile<kOhU8>;
+        static int occ[2] = {0, 0};
+        int& oc = occ[od == OutDtype::bf16 ? 1 : 0];
+        static size_t set_for[2] = {0, 0};
+        size_t& sf = set_for[od == OutDtype::bf16 ? 1 : 0];
+        if (sf < smem) {
+            set_smem(kern, std::max<size_t>(smem, 64u << 10));
+            sf = std::max<size_t>(smem, 64u << 10);
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, kern, 256, smem), "occupancy");
+        }
+        const uint64_t n_tiles = (n + R - 1) / R;
+        const unsigned g = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, static_cast<uint64_t>(std::max(oc, 1)) * device_sm_count())));
+        launch_k(kern, dim3(g), dim3(256), smem, st, "k_onehot_gather_tile launch", d, refs, n, R, o, out_gidx);
+        return;
+    }
     if (bulk && od != OutDtype::f32) {
         const uint32_t es = od == OutDtype::bf16 ? 2 : 1;
         const size_t smem = 4 * 2 * 4 * (32 * 2 * 16 * es);  // 4 warps x 2 slices x 4 planes x segment
