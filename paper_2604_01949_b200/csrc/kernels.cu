@@ -1884,7 +1884,8 @@ __global__ void __launch_bounds__(kOhWarps * 32)
     if (lane == 0) bulk_wait0();
 }
 
-// K4o, tiled (default): a CTA builds R consecutive output rows (a contiguous
+// K4o, tiled (A/B: RFL_OH=tile; 763 vs 922 M rows/s for the plain kernel on cfg4,
+// profiles/r2/s3/README.md): a CTA builds R consecutive output rows (a contiguous
 // R x row-bytes range of the batch, <= 32 KB) in one of two shared tiles and one
 // thread writes the tile with a single 1-D TMA bulk store -- the large-tile store
 // path that reaches ~5.8 TB/s for write-heavy mixes (profiles/r2/mix_bw_b.jsonl);
@@ -2496,11 +2497,11 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 7) / 8, 8ull * device_sm_count())));
     const ArenaDev d = dev_view(a);
     auto* o = static_cast<uint8_t*>(out);
-    static const int variant = [] {  // RFL_OH=plain | bulk (A/B); default: tiled
+    static const int variant = [] {  // RFL_OH=tile | bulk (A/B); default: plain 16-B stores
         const char* e = std::getenv("RFL_OH");
         if (e && std::string(e) == "bulk") return 1;
-        if (e && std::string(e) == "plain") return 2;
-        return 0;
+        if (e && std::string(e) == "tile") return 0;
+        return 2;
     }();
     const bool bulk = variant == 1;
     const uint64_t row_bytes = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
