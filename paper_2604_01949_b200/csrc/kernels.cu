@@ -2383,12 +2383,14 @@ namespace {
 template <typename SrcT, typename DstT>
 void densify_d8_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
                   uint64_t* out_gidx, cudaStream_t st) {
-    // the v9 shape rule: rows wider than 48 KB -> 80 KB tiles at 2 CTAs/SM, else 40 KB at 3
+    // shape rule: rows wider than 48 KB -> two alternating 40 KB tiles at 2 CTAs/SM (the next
+    // tile is built while the previous bulk store drains; cfg2 116.8 -> 114.9 us per batch vs one
+    // 80 KB tile, profiles/r2/s3/k3d_tiles.txt), else one 40 KB tile at 3
     const uint64_t esz = sizeof(DstT);
     const D8Shape& ov = d8_shape();
     const bool wide = av.n_var * esz > 48 * 1024;
-    const uint64_t max_tile = ov.tile_kb ? static_cast<uint64_t>(ov.tile_kb) << 10 : wide ? (80u << 10) : (40u << 10);
-    const int minb = ov.minb ? ov.minb : wide ? 2 : 3, nbuf = ov.nbuf ? ov.nbuf : 1;
+    const uint64_t max_tile = ov.tile_kb ? static_cast<uint64_t>(ov.tile_kb) << 10 : (40u << 10);
+    const int minb = ov.minb ? ov.minb : wide ? 2 : 3, nbuf = ov.nbuf ? ov.nbuf : wide ? 2 : 1;
     uint64_t tile_cols = av.n_var;
     if (av.n_var * esz > max_tile) tile_cols = (max_tile / esz) & ~15ull;
     int bulk = ((av.n_var * esz) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
