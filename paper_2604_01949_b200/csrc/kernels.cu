@@ -1949,6 +1949,79 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) bulk_wait0();
 }
 
+// K4 by whole rows through TMA (A/B, RFL_DG=row): each CTA streams rows through
+// 2 shared stages -- one 1-D bulk load of the row (mbarrier completion), the
+// block converts it (u8 -> bf16) into the stage's out buffer (raw: in place), one
+// bulk store of the row -- so both directions move as one large bulk op per row.
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    k_dense_gather_rows(ArenaDev a, uint64_t in_row_bytes, const RowRef* __restrict__ refs, uint64_t n_rows,
+                        uint8_t* __restrict__ out, uint64_t out_row_bytes, uint64_t* __restrict__ out_gidx,
+                        uint32_t stage_bytes) {
+    extern __shared__ __align__(128) uint8_t dr_smem[];
+    __shared__ __align__(8) uint64_t bar[2];
+    const uint32_t in_b = static_cast<uint32_t>(in_row_bytes);
+    const uint32_t in_pad = (in_b + 127u) & ~127u;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    pdl_trigger();
+    auto issue = [&](uint64_t r, uint32_t st) {  // thread 0
+        const RowRef rf = refs[r];
+        if (out_gidx) out_gidx[r] = rf.gidx;
+        mbar_arrive_expect_tx(&bar[st], in_b);
+        bulk_load(dr_smem + st * stage_bytes, a.base + rf.rec_off + (rf.gidx % a.chunk_rows) * in_row_bytes, in_b,
+                  &bar[st]);
+    };
+    const uint64_t stride = gridDim.x;
+    uint64_t r = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (r < n_rows) issue(r, 0);
+        if (r + stride < n_rows) issue(r + stride, 1);
+    }
+    uint32_t ph[2] = {0, 0};
+    for (uint32_t it = 0; r < n_rows; r += stride, ++it) {
+        const uint32_t st = it & 1u;
+        uint8_t* in = dr_smem + st * stage_bytes;
+        uint8_t* ob = MODE == kRaw ? in : in + in_pad;
+        mbar_wait(&bar[st], ph[st]);
+        ph[st] ^= 1u;
+        if (MODE != kRaw) {
+            if (threadIdx.x == 0) bulk_wait_read1();  // this stage's out buffer (two rows ago) has been read
+            __syncthreads();
+            for (uint32_t c = threadIdx.x; c < in_b / 16; c += 256) {
+                const uint4 v = *reinterpret_cast<const uint4*>(in + c * 16);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                uint32_t o[8];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    o[2 * j] = pack_bf16x2(float(w[j] & 0xff), float((w[j] >> 8) & 0xff));
+                    o[2 * j + 1] = pack_bf16x2(float((w[j] >> 16) & 0xff), float(w[j] >> 24));
+                }
+                *reinterpret_cast<uint4*>(ob + c * 32) = make_uint4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<uint4*>(ob + c * 32 + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+            }
+            fence_proxy_async_shared();
+        }
+        __syncthreads();  // (raw: every thread is past the wait; converted: the out buffer is complete)
+        if (threadIdx.x == 0) {
+            bulk_store(out + r * out_row_bytes, ob, static_cast<uint32_t>(out_row_bytes));
+            bulk_commit();
+            if (r + 2 * stride < n_rows) {
+                // raw: the stage is reloaded only once its store has read it; converted: the
+                // in buffer was consumed by the conversion above
+                if (MODE == kRaw) bulk_wait_read0();
+                issue(r + 2 * stride, st);
+            }
+        }
+    }
+    if (threadIdx.x == 0) bulk_wait0();
+}
+
 // ======================================================== staging pull ===
 // Host -> HBM staging of a group's fetched blocks by TMA instead of one copy-engine
 // transfer per block: each copy engine transfer pays a fixed ~4.7 us setup
@@ -2441,6 +2514,7 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
             const char* e = std::getenv("RFL_DG");
             if (!e) return 0;  // automatic
             if (e[0] == 'b') return e[1] == '4' ? -4 : -2;  // TMA bulk-store variant, 2 or 4 loads per lane
+            if (e[0] == 'r') return 8;                      // whole rows through TMA
             return e[0] == '4' ? 4 : 2;
         }();
         auto go = [&](auto kern, int U, int T) {
@@ -2453,6 +2527,26 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         };
         auto pick = [&](auto mode) {
             constexpr int M = decltype(mode)::value;
+            if constexpr (M != kF32ToBf16) {
+                if (u_sel == 8 && in_rb <= (24u << 10)) {  // RFL_DG=row: whole rows through TMA (A/B)
+                    const uint64_t orb = M == kU8ToBf16 ? in_rb * 2 : in_rb;
+                    const uint32_t stage = static_cast<uint32_t>(
+                        M == kRaw ? ((in_rb + 127) & ~127ull) : ((in_rb + 127) & ~127ull) + orb);
+                    const size_t smem = 2ull * stage;
+                    auto kern = k_dense_gather_rows<M>;
+                    static size_t set_to = 0;
+                    static int occ = 0;
+                    if (set_to < smem) {
+                        set_smem(kern, smem);
+                        set_to = smem;
+                        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem), "occupancy");
+                    }
+                    const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
+                        1, std::min<uint64_t>(n, static_cast<uint64_t>(std::max(occ, 1)) * device_sm_count())));
+                    return launch_k(kern, dim3(g), dim3(256), smem, st, "k_dense_gather_rows launch", d, in_rb, refs, n,
+                                    o, orb, out_gidx, stage);
+                }
+            }
             if (u_sel == 4) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
             if constexpr (M != kF32ToBf16) {
                 // automatic: the u8 -> bf16 expansion writes through TMA bulk stores
