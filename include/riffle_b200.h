@@ -139,9 +139,10 @@ void rfl_schedule_destroy(rfl_schedule* s);
 
 /* Device-side store image shared by many iterators (loader.hpp:55-57).
  *   RFL_STAGE_RESIDENT:      every chunk record copied once into HBM.
- *   RFL_STAGE_STREAM_PINNED: records kept in pinned host memory; each
- *                            fetched block is cudaMemcpyAsync'd into an
- *                            HBM arena on a side stream.
+ *   RFL_STAGE_STREAM_PINNED: records kept in pinned host memory (re-encoded
+ *                            losslessly where possible); the blocks fetched
+ *                            for a group are pulled into HBM slots by one TMA
+ *                            kernel on a side stream.
  *   RFL_STAGE_STREAM_FILE:   records pread (O_DIRECT if cache_bypass) into
  *                            pinned staging buffers, then as above. */
 /*   RFL_STAGE_RESIDENT_CODED: the staging image of stream_pinned (u8 column
@@ -176,7 +177,7 @@ typedef struct rfl_device_config {
     uint32_t flags;     /* RFL_DEV_TIME_KERNELS: CUDA events around each batch's kernels (counters) */
     void* stream; /* cudaStream_t for assembly; NULL = loader-owned */
     uint32_t batches_per_launch; /* consecutive batches replayed, staged and assembled together
-                                    (one copy batch, one decode, one assembly launch; 0 = 1);
+                                    (one staging pull, one decode, one assembly launch; 0 = 1);
                                     each stays valid for out_slots further launches */
     uint32_t reserved2;
 } rfl_device_config;

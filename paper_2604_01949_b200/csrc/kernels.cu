@@ -1949,7 +1949,7 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) bulk_wait0();
 }
 
-// K4 by whole rows through TMA (A/B, RFL_DG=row): each CTA streams rows through
+// K4 by whole rows through TMA (the grouped launches; RFL_DG=row forces it): each CTA streams rows through
 // 2 shared stages -- one 1-D bulk load of the row (mbarrier completion), the
 // block converts it (u8 -> bf16) into the stage's out buffer (raw: in place), one
 // bulk store of the row -- so both directions move as one large bulk op per row.
@@ -2528,7 +2528,12 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
         auto pick = [&](auto mode) {
             constexpr int M = decltype(mode)::value;
             if constexpr (M != kF32ToBf16) {
-                if (u_sel == 8 && in_rb <= (24u << 10)) {  // RFL_DG=row: whole rows through TMA (A/B)
+                // whole rows through TMA when every CTA streams >= 4 rows through its two
+                // stages (the grouped launches: cfg3 x2 0.75 -> 0.78, cfg4 raw x4 0.75 -> 0.80;
+                // a single 1,024-row cfg3 batch is faster with the warp units, 0.65 vs 0.61,
+                // profiles/r2/s3/kb_dense_rows.txt).  RFL_DG=row forces it, other RFL_DG values
+                // keep the warp-unit kernels.
+                if ((u_sel == 8 || u_sel == 0) && in_rb <= (24u << 10)) {
                     const uint64_t orb = M == kU8ToBf16 ? in_rb * 2 : in_rb;
                     const uint32_t stage = static_cast<uint32_t>(
                         M == kRaw ? ((in_rb + 127) & ~127ull) : ((in_rb + 127) & ~127ull) + orb);
@@ -2541,10 +2546,12 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
                         set_to = smem;
                         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem), "occupancy");
                     }
-                    const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
-                        1, std::min<uint64_t>(n, static_cast<uint64_t>(std::max(occ, 1)) * device_sm_count())));
-                    return launch_k(kern, dim3(g), dim3(256), smem, st, "k_dense_gather_rows launch", d, in_rb, refs, n,
-                                    o, orb, out_gidx, stage);
+                    const uint64_t ctas = static_cast<uint64_t>(std::max(occ, 1)) * device_sm_count();
+                    if (u_sel == 8 || n >= 4 * ctas) {
+                        const unsigned g = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(n, ctas)));
+                        return launch_k(kern, dim3(g), dim3(256), smem, st, "k_dense_gather_rows launch", d, in_rb,
+                                        refs, n, o, orb, out_gidx, stage);
+                    }
                 }
             }
             if (u_sel == 4) return go(k_dense_gather_flat<M, 4, 256>, 4, 256);
