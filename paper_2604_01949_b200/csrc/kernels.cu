@@ -2022,6 +2022,72 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) bulk_wait0();
 }
 
+// K4o by whole rows (A/B: RFL_OH=rows): a 64-thread CTA streams output rows through
+// two shared stages; the next row's code words are loaded into registers before
+// the current row is built, and each row leaves with one 1-D bulk store.
+template <int OUT>
+__global__ void __launch_bounds__(64)
+    k_onehot_gather_rows(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint8_t* __restrict__ out,
+                         uint64_t* __restrict__ out_gidx) {
+    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : 2;
+    constexpr uint32_t kMaxW = 8;  // code words per thread (rows up to 64 x 8 x 64 = 32,768 positions)
+    extern __shared__ __align__(128) uint8_t ohr_smem[];
+    pdl_wait();
+    pdl_trigger();
+    const uint64_t L = a.n_var / 4, wpr = L / 16;
+    const uint64_t row_bytes = a.n_var * kEs;
+    const uint32_t tid = threadIdx.x;
+    auto load = [&](uint64_t r, uint32_t (&w)[kMaxW]) {
+        const RowRef rf = refs[r];  // (every thread: one broadcast L1 line)
+        const uint8_t* src = a.base + (rf.rec_off & ((1ull << 60) - 1)) + (rf.gidx % a.chunk_rows) * (L / 4);
+#pragma unroll
+        for (uint32_t k = 0; k < kMaxW; ++k)
+            if (tid + 64 * k < wpr) w[k] = ld_u32(src + 4 * (tid + 64 * k));
+        if (tid == 0 && out_gidx) out_gidx[r] = rf.gidx;
+    };
+    uint32_t cur[kMaxW], nxt[kMaxW];
+    uint64_t r = blockIdx.x;
+    if (r < n_rows) load(r, cur);
+    for (uint32_t it = 0; r < n_rows; r += gridDim.x, ++it) {
+        if (r + gridDim.x < n_rows) load(r + gridDim.x, nxt);
+        uint8_t* stage = ohr_smem + (it & 1u) * row_bytes;
+        if (tid == 0) bulk_wait_read1();  // this stage's store (two rows ago) has been read
+        __syncthreads();
+#pragma unroll
+        for (uint32_t k = 0; k < kMaxW; ++k) {
+            const uint64_t wi = tid + 64 * k;
+            if (wi >= wpr) break;
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                const uint32_t m = onehot_mask16(cur[k], c);
+                uint8_t* p = stage + (c * L + 16 * wi) * kEs;
+                if (OUT == kOhU8) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                } else {
+                    uint32_t o[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<uint4*>(p + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+                }
+            }
+        }
+        fence_proxy_async_shared();
+        __syncthreads();
+        if (tid == 0) {
+            bulk_store(out + r * row_bytes, stage, static_cast<uint32_t>(row_bytes));
+            bulk_commit();
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kMaxW; ++k) cur[k] = nxt[k];
+    }
+    if (tid == 0) bulk_wait0();
+}
+
 // ======================================================== staging pull ===
 // Host -> HBM staging of a group's fetched blocks by TMA instead of one copy-engine
 // transfer per block: each copy engine transfer pays a fixed ~4.7 us setup
@@ -2600,12 +2666,31 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 7) / 8, 8ull * device_sm_count())));
     const ArenaDev d = dev_view(a);
     auto* o = static_cast<uint8_t*>(out);
-    static const int variant = [] {  // RFL_OH=tile | bulk (A/B); default: plain 16-B stores
+    static const int variant = [] {  // RFL_OH=tile | bulk | rows (A/B); default: plain 16-B stores
         const char* e = std::getenv("RFL_OH");
         if (e && std::string(e) == "bulk") return 1;
         if (e && std::string(e) == "tile") return 0;
+        if (e && std::string(e) == "rows") return 3;
         return 2;
     }();
+    if (variant == 3 && od != OutDtype::f32 && a.n_var <= 32768) {
+        const uint64_t rb = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
+        const size_t smem = 2 * rb;
+        auto kern = od == OutDtype::bf16 ? k_onehot_gather_rows<kOhBf16> : k_onehot_gather_rows<kOhU8>;
+        static size_t set_to[2] = {0, 0};
+        static int occ[2] = {0, 0};
+        const int ki = od == OutDtype::bf16 ? 1 : 0;
+        if (set_to[ki] < smem) {
+            set_smem(kern, std::max<size_t>(smem, 16u << 10));
+            set_to[ki] = std::max<size_t>(smem, 16u << 10);
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, 64, smem), "occupancy");
+        }
+        const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
+            1, std::min<uint64_t>(n, static_cast<uint64_t>(std::max(occ[ki], 1)) * device_sm_count())));
+        launch_k(kern, dim3(g), dim3(64), smem, st, "k_onehot_gather_rows launch", dev_view(a), refs, n,
+                 static_cast<uint8_t*>(out), out_gidx);
+        return;
+    }
     const bool bulk = variant == 1;
     const uint64_t row_bytes = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
     if (variant == 0 && od != OutDtype::f32 && row_bytes <= (32u << 10)) {
