@@ -2022,7 +2022,7 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) bulk_wait0();
 }
 
-// K4o by whole rows (A/B: RFL_OH=rows): a 64-thread CTA streams output rows through
+// K4o by whole rows (default; RFL_OH=plain for the register-store kernel): a 64-thread CTA streams output rows through
 // two shared stages; the next row's code words are loaded into registers before
 // the current row is built, and each row leaves with one 1-D bulk store.
 template <int OUT>
@@ -2666,12 +2666,15 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 7) / 8, 8ull * device_sm_count())));
     const ArenaDev d = dev_view(a);
     auto* o = static_cast<uint8_t*>(out);
-    static const int variant = [] {  // RFL_OH=tile | bulk | rows (A/B); default: plain 16-B stores
+    // RFL_OH=plain | tile | bulk (A/B); default: whole rows through two shared stages + one
+    // bulk store per row (cfg4 950-998 vs 936 M rows/s for plain 16-B stores,
+    // profiles/r2/s3/README.md)
+    static const int variant = [] {
         const char* e = std::getenv("RFL_OH");
         if (e && std::string(e) == "bulk") return 1;
         if (e && std::string(e) == "tile") return 0;
-        if (e && std::string(e) == "rows") return 3;
-        return 2;
+        if (e && std::string(e) == "plain") return 2;
+        return 3;
     }();
     if (variant == 3 && od != OutDtype::f32 && a.n_var <= 32768) {
         const uint64_t rb = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
