@@ -29,6 +29,7 @@ STORES = {
                   chunk_rows=1024),
     "cfg3s": dict(n_obs=200_000, n_var=12288, layout="dense", value_dtype="u8", seed=2, chunk_rows=256),
     "cfg4s": dict(n_obs=1_000_000, n_var=4096, layout="dense", value_dtype="u8", seed=3, chunk_rows=512),
+    "cfg4oh": dict(n_obs=1_000_000, n_var=4096, layout="dense", value_dtype="u8", seed=3, chunk_rows=512, one_hot=4),
     "cfg5s": dict(n_obs=65_536, n_var=62_710, layout="csr", value_dtype="f32", density=2000 / 62710, seed=4,
                   chunk_rows=64),
 }
@@ -44,6 +45,10 @@ CASES = {  # store, kernel, rows per launch, out dtype, transform
     "dense_bf16_cfg3_g2": ("cfg3s", "dense", 2048, L.BF16, None),   # bench.py's 2 batches per launch
     "dense_raw_cfg4_g4": ("cfg4s", "dense", 8192, L.NATIVE, None),  # bench.py's 4 batches per launch
     "pack_cfg5": ("cfg5s", "pack", 65536, None, None),
+    # K4o: one-hot rows from the HBM-resident 2-bit code image (resident_coded), as bench.py's value leg
+    "onehot_cfg4": ("cfg4oh", "onehot", 2048, L.NATIVE, None),
+    "onehot_cfg4_g10": ("cfg4oh", "onehot", 20480, L.NATIVE, None),
+    "onehot_bf16_cfg4_g4": ("cfg4oh", "onehot", 8192, L.BF16, None),
 }
 
 
@@ -84,7 +89,7 @@ def run_case(name, K, W, dstores):
     import torch
     st_name, kern, rows, od, xf = CASES[name]
     if st_name not in dstores:
-        dstores[st_name] = R.DeviceStore(store(st_name), 0, "resident")
+        dstores[st_name] = R.DeviceStore(store(st_name), 0, "resident_coded" if kern == "onehot" else "resident")
     ds = dstores[st_name]
     man = ds.manifest()
     base, offs = ds.arena()
@@ -146,6 +151,12 @@ def run_case(name, K, W, dstores):
         launch = lambda i: lib.rfl_dense_gather(C.byref(desc), d_refs[i].data_ptr(), rows, od,  # noqa
                                                 outs[i % len(outs)].data_ptr(), gout.data_ptr(), sp)
         alg = lambda i: rows * (16 + rb + man.n_var * osz + 8)  # noqa
+    elif kern == "onehot":
+        osz = 2 if od == L.BF16 else 1
+        outs = rotating(rows * man.n_var * osz + 16)
+        launch = lambda i: lib.rfl_onehot_gather(C.byref(desc), d_refs[i].data_ptr(), rows, od,  # noqa
+                                                 outs[i % len(outs)].data_ptr(), gout.data_ptr(), sp)
+        alg = lambda i: rows * (16 + man.n_var // 16 + man.n_var * osz + 8)  # noqa
     else:  # pack: scan + record pack, 4096-row output chunks
         cr = 4096
         P = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
