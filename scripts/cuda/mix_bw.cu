@@ -71,6 +71,32 @@ __global__ void __launch_bounds__(256) tile_store(const uint4* __restrict__ in, 
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// write-only ceilings (K4o writes 16 B per byte it reads): STG.128 grid-stride, and
+// shared tiles of tile_bytes written by 1-D TMA bulk stores (two tiles alternating)
+__global__ void fill_stg(uint4* __restrict__ out, size_t n) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = make_uint4(unsigned(i), 1, 2, 3);
+}
+__global__ void __launch_bounds__(256) fill_tma(char* __restrict__ out, size_t tiles, unsigned tile_bytes) {
+    extern __shared__ __align__(128) uint4 tile[];
+    unsigned it = 0;
+    for (size_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        uint4* tb = tile + (it & 1u) * (tile_bytes / 16);
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < tile_bytes / 16; i += blockDim.x) tb[i] = make_uint4(unsigned(t), i, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + t * tile_bytes),
+                         "r"(static_cast<unsigned>(__cvta_generic_to_shared(tb))), "r"(tile_bytes) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // tile_store with an L2 evict_first policy on the bulk stores (output lines leave L2 first)
 __global__ void __launch_bounds__(256) tile_store_ef(const uint4* __restrict__ in, size_t n_in, char* __restrict__ out,
                                                      size_t tiles, unsigned tile_bytes) {
@@ -171,6 +197,18 @@ int main() {
     CK(cudaFuncSetAttribute(tile_store_ef, cudaFuncAttributeMaxDynamicSharedMemorySize, tb));
     bench([&](int r) { tile_store_ef<<<sms * 2, 256, tb>>>(in, n_in, reinterpret_cast<char*>(out) + (r % 4) * out_bytes, tiles, tb); },
           "tma 80KB tiles 1:5 L2 evict_first", double(in_bytes + out_bytes));
+    // write-only (out_bytes per launch, rotating over 4 buffers)
+    bench([&](int r) { fill_stg<<<sms * 8, 256>>>(out + (r % 4) * (out_bytes / 16), out_bytes / 16); },
+          "stg write-only", double(out_bytes));
+    for (unsigned wb : {4096u, 16384u, 40960u}) {
+        CK(cudaFuncSetAttribute(fill_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * wb));
+        const int per_sm = wb <= 4096 ? 8 : wb <= 16384 ? 6 : 2;
+        char name[96];
+        std::snprintf(name, sizeof name, "tma %u KB tiles write-only", wb / 1024);
+        bench([&](int r) { fill_tma<<<sms * per_sm, 256, 2 * wb>>>(reinterpret_cast<char*>(out) + (r % 4) * out_bytes,
+                                                                  out_bytes / wb, wb); },
+              name, double(out_bytes));
+    }
     // 2-D tensor-map stores into a [rows, 20000] f32 matrix (cfg1's dense batch shape)
     EncodeTiled enc = nullptr;
     cudaDriverEntryPointQueryResult q;

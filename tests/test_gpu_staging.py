@@ -398,3 +398,39 @@ def test_fused_falls_back_for_long_rows(tmp_path):
         nb += 1
     assert it.counters().kernels_launched > nb
     it.close()
+
+
+@pytest.mark.parametrize("stage", ["pull", "ce"])
+def test_staging_pull_many_blocks_per_group(tmp_path, monkeypatch, stage):
+    """stream_pinned groups that fetch more than the pull kernel's 256 jobs per
+    launch (f = 4 rows per block, 3 x 700-row batches per group: ~525 blocks), with
+    records of odd sizes (not multiples of 16 B) and chunks smaller than blocks and
+    larger; the staging pull (default) and the per-block copy-engine fallback
+    (RFL_STAGE=ce) give the reference's CSR and dense batches bit for bit."""
+    if stage == "ce":
+        monkeypatch.setenv("RFL_STAGE", "ce")
+    rng = np.random.default_rng(17)
+    nv, n = 3001, 2100
+    nnz = rng.integers(0, 40, n)
+    ip = np.zeros(n + 1, np.uint64)
+    ip[1:] = np.cumsum(nnz)
+    ix = np.concatenate([np.sort(rng.choice(nv, k, replace=False)) for k in nnz]).astype(np.uint64)
+    dv = rng.random(len(ix)).astype(np.float32)
+    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 2, 64)  # 2-row chunks: a 4-row block spans 2 records
+    ds = R.DeviceStore(R.StoreReader(tmp_path / "s"), 0, "stream_pinned")
+    for output in ("csr", "dense"):
+        it = R.BatchIterator(ds, R.LoaderConfig(4, 2048, 700, 5), 0, output=output, batches_per_launch=3)
+        seen = 0
+        for b in it:
+            g = b.global_indices_host
+            eip, eix, edv = csr_gather(ip, ix, dv, g)
+            if output == "csr":
+                mb = b.to_minibatch()
+                assert (mb.block.indptr == eip).all() and (mb.block.indices == eix).all()
+                assert mb.block.data.tobytes() == edv.tobytes()
+            else:
+                assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, nv).tobytes()
+            seen += len(g)
+        assert seen == n
+        it.close()
+    ds.close()
