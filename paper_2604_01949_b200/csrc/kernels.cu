@@ -15,6 +15,7 @@
 #include <utility>
 #include <type_traits>
 #include <array>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 
@@ -2303,11 +2304,14 @@ void densify_idx(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od
 int device_sm_count() {
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    static int counts[64] = {0};
-    if (dev < 64 && counts[dev]) return counts[dev];
+    static std::atomic<int> counts[64];  // (zero-initialised: static storage)
+    if (dev < 64) {
+        const int c = counts[dev].load(std::memory_order_relaxed);
+        if (c) return c;
+    }
     int c = 0;
     cuda_check(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev), "sm count");
-    if (dev < 64) counts[dev] = c;
+    if (dev < 64) counts[dev].store(c, std::memory_order_relaxed);
     return c;
 }
 
@@ -2339,11 +2343,12 @@ void launch_copy_tma(const ArenaView& a, uint32_t vs, const RowRef* refs, const 
                      uint64_t cr = 0) {
     auto kern = a.idt == IDtype::u32 ? k_csr_copy_tma<uint32_t> : k_csr_copy_tma<uint64_t>;
     const size_t smem = 2 * kTcStage * kTcWarps;
-    static int per_sm[2] = {0, 0};
-    int& occ = per_sm[a.idt == IDtype::u32 ? 0 : 1];
+    static std::atomic<int> per_sm[2];
+    int occ = per_sm[a.idt == IDtype::u32 ? 0 : 1].load(std::memory_order_relaxed);
     if (!occ) {
         set_smem(kern, smem);
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTcThreads, smem), "occupancy");
+        per_sm[a.idt == IDtype::u32 ? 0 : 1].store(occ, std::memory_order_relaxed);
     }
     const uint32_t blocks = static_cast<uint32_t>(std::max(occ, 1) * device_sm_count());
     const uint32_t n_warps = blocks * kTcWarps;
@@ -2605,12 +2610,19 @@ void launch_dense_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Out
                         M == kRaw ? ((in_rb + 127) & ~127ull) : ((in_rb + 127) & ~127ull) + orb);
                     const size_t smem = 2ull * stage;
                     auto kern = k_dense_gather_rows<M>;
-                    static size_t set_to = 0;
-                    static int occ = 0;
-                    if (set_to < smem) {
-                        set_smem(kern, smem);
-                        set_to = smem;
-                        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem), "occupancy");
+                    int occ = 0;
+                    {  // (loaders on several host threads launch concurrently)
+                        static std::mutex mu;
+                        static size_t set_to = 0;
+                        static int occ_at = 0;
+                        std::lock_guard<std::mutex> lk(mu);
+                        if (set_to != smem) {
+                            set_smem(kern, std::max(smem, set_to));
+                            set_to = std::max(smem, set_to);
+                            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_at, kern, 256, smem),
+                                       "occupancy");
+                        }
+                        occ = occ_at;
                     }
                     const uint64_t ctas = static_cast<uint64_t>(std::max(occ, 1)) * device_sm_count();
                     if (u_sel == 8 || n >= 4 * ctas) {
@@ -2680,16 +2692,22 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         const uint64_t rb = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
         const size_t smem = 2 * rb;
         auto kern = od == OutDtype::bf16 ? k_onehot_gather_rows<kOhBf16> : k_onehot_gather_rows<kOhU8>;
-        static size_t set_to[2] = {0, 0};
-        static int occ[2] = {0, 0};
         const int ki = od == OutDtype::bf16 ? 1 : 0;
-        if (set_to[ki] < smem) {
-            set_smem(kern, std::max<size_t>(smem, 16u << 10));
-            set_to[ki] = std::max<size_t>(smem, 16u << 10);
-            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, 64, smem), "occupancy");
+        int oc = 0;
+        {
+            static std::mutex mu;
+            static size_t set_to[2] = {0, 0};
+            static int occ[2] = {0, 0};
+            std::lock_guard<std::mutex> lk(mu);
+            if (set_to[ki] < smem) {
+                set_smem(kern, std::max<size_t>(smem, 16u << 10));
+                set_to[ki] = std::max<size_t>(smem, 16u << 10);
+                cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, 64, smem), "occupancy");
+            }
+            oc = occ[ki];
         }
         const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
-            1, std::min<uint64_t>(n, static_cast<uint64_t>(std::max(occ[ki], 1)) * device_sm_count())));
+            1, std::min<uint64_t>(n, static_cast<uint64_t>(std::max(oc, 1)) * device_sm_count())));
         launch_k(kern, dim3(g), dim3(64), smem, st, "k_onehot_gather_rows launch", dev_view(a), refs, n,
                  static_cast<uint8_t*>(out), out_gidx);
         return;
@@ -2700,14 +2718,19 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         const uint32_t R = static_cast<uint32_t>(std::min<uint64_t>(64, (32u << 10) / row_bytes));
         const size_t smem = 2ull * R * row_bytes;
         auto kern = od == OutDtype::bf16 ? k_onehot_gather_tile<kOhBf16> : k_onehot_gather_tile<kOhU8>;
-        static int occ[2] = {0, 0};
-        int& oc = occ[od == OutDtype::bf16 ? 1 : 0];
-        static size_t set_for[2] = {0, 0};
-        size_t& sf = set_for[od == OutDtype::bf16 ? 1 : 0];
-        if (sf < smem) {
-            set_smem(kern, std::max<size_t>(smem, 64u << 10));
-            sf = std::max<size_t>(smem, 64u << 10);
-            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, kern, 256, smem), "occupancy");
+        int oc = 0;
+        {
+            static std::mutex mu;
+            static int occ[2] = {0, 0};
+            static size_t set_for[2] = {0, 0};
+            const int ki = od == OutDtype::bf16 ? 1 : 0;
+            std::lock_guard<std::mutex> lk(mu);
+            if (set_for[ki] < smem) {
+                set_smem(kern, std::max<size_t>(smem, 64u << 10));
+                set_for[ki] = std::max<size_t>(smem, 64u << 10);
+                cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, 256, smem), "occupancy");
+            }
+            oc = occ[ki];
         }
         const uint64_t n_tiles = (n + R - 1) / R;
         const unsigned g = static_cast<unsigned>(
@@ -2721,11 +2744,8 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         const unsigned g4 = static_cast<unsigned>(
             std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 3) / 4, 16ull * device_sm_count())));
         auto kern = od == OutDtype::bf16 ? k_onehot_gather_bulk<kOhBf16> : k_onehot_gather_bulk<kOhU8>;
-        static bool attr[2] = {false, false};
-        if (!attr[es - 1]) {
-            set_smem(kern, smem);
-            attr[es - 1] = true;
-        }
+        static std::once_flag once[2];
+        std::call_once(once[es - 1], [&] { set_smem(kern, smem); });
         launch_k(kern, dim3(g4), dim3(128), smem, st, "k_onehot_gather_bulk launch", d, refs, n, o, out_gidx);
         return;
     }

@@ -20,4 +20,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_on
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dense_gather -s 3 -c 1 \
    -o $O/prof_dense_cfg3 -f python bench.py --workload cfg3 --steps 4 --warmup 3 --no-cpu-baseline --no-verbatim-e2e --no-file-e2e > $O/ncu_dense.log 2>&1
 timeout 1800 python bench.py --workload cfg2 > $O/bench_cfg2.json 2> $O/bench_cfg2.err
+# (gpurun brings back <= 64 MiB: the reports are summarised here and dropped)
+for r in $O/*.ncu-rep; do python scripts/ncu_summary.py $r > ${r%.ncu-rep}.json 2>&1; done
+rm -f $O/*.ncu-rep
 echo done >> $O/gpu.txt
