@@ -160,7 +160,8 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
         open_image();
         if (d8_ && (m.value_dtype == VDtype::f32 || m.value_dtype == VDtype::i32)) {
             d8_fused_ = true;
-            for (uint8_t k : d8_rec_) d8_fused_ = d8_fused_ && (k == kD8Raw || k == kD8Coded || k == kD8Coded16);
+            for (uint8_t k : d8_rec_)
+                d8_fused_ = d8_fused_ && (k == kD8Raw || k == kD8Coded || k == kD8Coded16 || k == kD8Int8);
             for (uint32_t n : row_nnz_) d8_fused_ = d8_fused_ && n <= kD8FusedMaxNnz;
         }
     } catch (...) {  // the destructor does not run for a throwing constructor
@@ -1287,7 +1288,7 @@ bool GpuLoader::assemble_group() {
     // copy stream goes straight on to the next group's blocks
     if (!d8_jobs_.empty()) {
         launch_d8_decode(d8_jobs_.data(), d8_jobs_.size(), static_cast<uint32_t>(value_size(m.value_dtype)),
-                         m.chunk_rows, compute_, m.n_var);
+                         m.chunk_rows, compute_, m.n_var, m.value_dtype != VDtype::i32);
         ctr_.kernels_launched += (d8_jobs_.size() + kMaxD8Jobs - 1) / kMaxD8Jobs;
     }
 

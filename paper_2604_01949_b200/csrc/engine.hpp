@@ -68,7 +68,7 @@ struct StagePlan {
     std::array<uint8_t, 4> dict{0, 0, 0, 0};
     uint64_t n_esc = 0, bytes = 0, exp = 0;
 };
-StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values);
+StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat = true);
 void encode_csr_stage(const uint8_t* rec, uint64_t vs, const StagePlan& p, uint8_t* dst);
 bool one_hot_record(const uint8_t* rec, uint64_t rows, uint64_t n_var);
 void encode_one_hot(const uint8_t* rec, uint64_t rows, uint64_t n_var, uint8_t* dst);

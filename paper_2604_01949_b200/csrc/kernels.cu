@@ -375,7 +375,9 @@ __device__ __forceinline__ void st16_any(void* p, const uint32_t* w) {
 
 struct D8Jobs {
     uint32_t n, vs;
-    uint64_t n_var;  // kOneHot4 rows
+    uint64_t n_var;   // kOneHot4 rows
+    uint32_t vfloat;  // kD8Int8: values are f32 (else i32)
+    uint32_t pad;
     D8Job job[kMaxD8Jobs];
 };
 
@@ -425,6 +427,13 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
     D8vLayout L{};
     if (coded) {
         L = d8v_layout(rows, nnz, ld_u32(jb.src + d8v_layout(rows, nnz, 0).n_esc), low_b);
+    } else if (jb.kind == kD8Int8) {  // 1-byte integer values -> 4-byte f32 / i32
+        const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
+        const uint8_t* sv = jb.src + voff;
+        for (uint64_t i = tid; i < nnz; i += nt) {
+            const uint32_t u = __ldg(sv + i);
+            reinterpret_cast<uint32_t*>(dv)[i] = jobs.vfloat ? __float_as_uint(static_cast<float>(u)) : u;
+        }
     } else {  // raw values: copied word-wise (+ byte tail)
         const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
         const uint64_t vbytes = nnz * jobs.vs;
@@ -892,7 +901,7 @@ __device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef
     d.delta = rec + first_off + ((2 * static_cast<uint64_t>(rows) + 3) & ~3ull);
     d.gidx = r.gidx;
     d.pad = 0;
-    if (d.kind == kD8Raw) {
+    if (d.kind == kD8Raw || d.kind == kD8Int8) {
         d.low = rec + d8_values_offset(rows, nnz);
         d.codes = d.esc = nullptr;
         d.esc_at = d.dict = 0;
@@ -929,6 +938,8 @@ __device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw1
         if (kind == kD8Raw) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) ld16_any(r.low + 4 * k0 + 16 * q, x.lw + 4 * q);
+        } else if (kind == kD8Int8) {
+            ld16_any(r.low + k0, x.lw);
         } else {
             x.cw = ld_u32(r.codes + (k0 >> 2));
             if (kind == kD8Coded16) {
@@ -948,6 +959,8 @@ __device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw1
         x.d[j >> 2] |= static_cast<uint32_t>(__ldg(r.delta + k)) << (8 * (j & 3));
         if (kind == kD8Raw) {
             x.lw[j] = ld_u32(r.low + 4 * k);
+        } else if (kind == kD8Int8) {
+            x.lw[j >> 2] |= static_cast<uint32_t>(__ldg(r.low + k)) << (8 * (j & 3));
         } else {
             x.cw |= ((static_cast<uint32_t>(__ldg(r.codes + (k >> 2))) >> (2 * (k & 3))) & 3u) << (2 * j);
             if (kind == kD8Coded16) {
@@ -980,7 +993,7 @@ __device__ __forceinline__ void decode_d8(const D8RowDesc& r, const D8Raw16& x, 
         pre[j] = sum;
     }
     uint32_t em = 0;
-    if (r.kind != kD8Raw) {
+    if (r.kind == kD8Coded || r.kind == kD8Coded16) {
 #pragma unroll
         for (uint32_t j = 0; j < 16; ++j) em |= (((x.cw >> (2 * j)) & 3u) == 3u ? 1u : 0u) << j;
         em &= x.vm;
@@ -1003,6 +1016,9 @@ __device__ __forceinline__ void decode_d8(const D8RowDesc& r, const D8Raw16& x, 
         uint32_t bits;
         if (r.kind == kD8Raw) {
             bits = x.lw[j];
+        } else if (r.kind == kD8Int8) {
+            const uint32_t u = (x.lw[j >> 2] >> (8 * (j & 3))) & 255u;
+            bits = std::is_floating_point_v<SrcT> ? __float_as_uint(static_cast<float>(u)) : u;
         } else {
             uint32_t top = (r.dict >> (8 * ((x.cw >> (2 * j)) & 3u))) & 255u;
             if ((em >> j) & 1u) top = __ldg(r.esc + eb++);
@@ -2375,13 +2391,14 @@ void launch_csr_gather(const ArenaView& a, const RowRef* refs, uint64_t n, uint6
 }
 
 void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st,
-                      uint64_t n_var) {
+                      uint64_t n_var, bool vfloat) {
     const unsigned split = static_cast<unsigned>(std::min<uint64_t>(std::max<uint64_t>(1, (rows_per_record + 7) / 8), 1024));
     for (size_t k0 = 0; k0 < n; k0 += kMaxD8Jobs) {
         D8Jobs j{};
         j.n = static_cast<uint32_t>(std::min<size_t>(kMaxD8Jobs, n - k0));
         j.vs = vs;
         j.n_var = n_var;
+        j.vfloat = vfloat ? 1u : 0u;
         for (uint32_t i = 0; i < j.n; ++i) j.job[i] = jobs[k0 + i];
         launch_k(k_d8_decode, dim3(j.n, split), dim3(256), 0, st, "k_d8_decode launch", j);
     }

@@ -98,7 +98,10 @@ RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc, 
 // ([4][L] bytes, exactly one 1 per position) staged as 2-bit channel codes,
 // L/4 bytes per row (16x smaller; L a multiple of 16)
 // kD8Coded16: kD8Coded whose values all have a zero low half (1 stored byte each)
-enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2, kOneHot4 = 3, kD8Coded16 = 4 };
+// kD8Int8: the kD8Raw layout with 1-byte values, for 4-byte-value records whose every
+// value is an integer in [0, 255] (raw counts: f32 bits of float(u), or i32 u) --
+// no top-byte codes; the value byte IS the value
+enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2, kOneHot4 = 3, kD8Coded16 = 4, kD8Int8 = 5 };
 struct D8Job {
     const uint8_t* src;  // staged record (device)
     uint8_t* dst;        // idx16 record (device)
@@ -110,7 +113,7 @@ struct D8Job {
 constexpr size_t kMaxD8Jobs = 128;
 // (one warp per row: rows_per_record / 8 CTAs per record)
 void launch_d8_decode(const D8Job* jobs, size_t n, uint32_t vs, uint64_t rows_per_record, cudaStream_t st,
-                      uint64_t n_var = 0);
+                      uint64_t n_var = 0, bool vfloat = true);
 
 // K2 without the device scan: `prefix` (u64[n+1], exclusive nnz prefix of the
 // rows, prefix[0] arbitrary) is the host schedule's, and is the output indptr

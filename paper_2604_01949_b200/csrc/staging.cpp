@@ -51,7 +51,7 @@ void parallel_for(uint64_t n, F&& f) {  // f(i) over [0, n) on up to 16 threads;
 }  // namespace
 
 // ---------------------------------------------------------- per-record codecs --
-StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values) {
+StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat) {
     const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
     const uint8_t* ip = rec + kCsrHeaderBytes;
     const uint8_t* ix = ip + 4 * (rows + 1);
@@ -69,6 +69,29 @@ StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool
     p.kind = kD8Raw;
     p.bytes = d8_record_bytes(rows, nnz, vs);
     if (!code_values || vs != 4) return p;
+    {  // every value an integer in [0, 255]: one byte per value, nothing else (kD8Int8)
+        const uint8_t* v = ix + 4 * nnz;
+        bool small = true;
+        for (uint64_t k = 0; k < nnz && small; ++k) {
+            uint32_t b;
+            std::memcpy(&b, v + 4 * k, 4);
+            if (vfloat) {
+                float f;
+                std::memcpy(&f, &b, 4);
+                uint32_t back;
+                const float r = static_cast<float>(static_cast<uint32_t>(f >= 0.f && f <= 255.f ? f : 0.f));
+                std::memcpy(&back, &r, 4);
+                small = f >= 0.f && f <= 255.f && back == b;  // exact (and not -0.0)
+            } else {
+                small = b <= 255u;
+            }
+        }
+        if (small) {
+            p.kind = kD8Int8;
+            p.bytes = d8_record_bytes(rows, nnz, 1);
+            return p;
+        }
+    }
     // top-byte dictionary (3 most frequent) + escapes, kept when smaller
     uint64_t hist[256] = {0};
     const uint8_t* val = ix + 4 * nnz;
@@ -123,6 +146,20 @@ void encode_csr_stage(const uint8_t* src, uint64_t vs, const StagePlan& p, uint8
     }
     if (p.kind == kD8Raw) {
         std::memcpy(dst + d8_values_offset(rows, nnz), val, vs * nnz);
+        return;
+    }
+    if (p.kind == kD8Int8) {
+        uint8_t* v8 = dst + d8_values_offset(rows, nnz);
+        for (uint64_t k = 0; k < nnz; ++k) {
+            uint32_t b;
+            std::memcpy(&b, val + 4 * k, 4);
+            if (vs == 4 && b > 255u) {  // f32 bits of an integer value
+                float f;
+                std::memcpy(&f, &b, 4);
+                b = static_cast<uint32_t>(f);
+            }
+            v8[k] = static_cast<uint8_t>(b);
+        }
         return;
     }
     const bool c16 = p.kind == kD8Coded16;
@@ -259,7 +296,7 @@ bool DStore::build_staged_image(uint32_t mode) {
                     plans[k].bytes = m.rows_in_chunk(q) * (m.n_var / 16);
                     plans[k].exp = rec_len_[q];
                 } else {
-                    plans[k] = plan_csr_stage(rec, vs, mode == kStageDelta, code_values);
+                    plans[k] = plan_csr_stage(rec, vs, mode == kStageDelta, code_values, m.value_dtype != VDtype::i32);
                 }
             });
             if (!one_hot_ok) {  // not a one-hot store: the verbatim image

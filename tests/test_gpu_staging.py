@@ -207,9 +207,9 @@ def test_wide_axis_keeps_verbatim_staging(tmp_path):
 
 @pytest.mark.parametrize("vdt", ["f32", "i32"])
 def test_counts_store_staging(tmp_path, vdt):
-    """Procedural counts (BASELINE config 2's shape): integer values whose low 16
-    bits are zero as f32 stage with 1 stored byte per value next to the top-byte
-    code; i32 counts keep 3 low bytes.  Batches bit-exact, normalize within 1e-6."""
+    """Procedural counts (BASELINE config 2's shape): integer values in [1, 64]
+    stage as one byte per value (kD8Int8), f32 and i32 alike.  Batches bit-exact,
+    normalize within 1e-6."""
     path = tmp_path / "s"
     R.synth_store(path, R.SynthConfig(n_obs=600, n_var=9000, layout="csr", value_dtype=vdt, seed=4, chunk_rows=64,
                                       chunks_per_shard=4, counts=True))
@@ -230,7 +230,7 @@ def test_counts_store_staging(tmp_path, vdt):
                 want = normalize_log1p(to_dense(eip, eix, edv.astype(np.float32), 9000))
                 np.testing.assert_allclose(b.data.cpu().numpy().astype(np.float64), want, rtol=1e-6, atol=0)
         c = it.counters()
-        assert c.h2d_bytes < (0.45 if vdt == "f32" else 0.7) * c.bytes_read
+        assert c.h2d_bytes < 0.45 * c.bytes_read
         it.close()
 
 
@@ -315,8 +315,13 @@ def _fused_store(tmp_path, values, seed=11):
             return np.array([c, c + 255])
         return np.sort(rng.choice(nv, k, replace=False))
     ix = np.concatenate([cols(k) for k in nnz]).astype(np.uint64)
-    if values == "counts":    # integer counts as f32: low 16 bits zero -> kD8Coded16
-        dv = rng.integers(1, 64, len(ix)).astype(np.float32)
+    if values == "counts":    # integer counts in [0, 255] as f32 -> kD8Int8 (one byte per value)
+        dv = rng.integers(0, 64, len(ix)).astype(np.float32)
+        dv[::97] = 255.0
+    elif values == "halves":  # k / 2 as f32: <= 8 significant bits, low 16 bits zero -> kD8Coded16
+        dv = (rng.integers(1, 200, len(ix)) / 2.0).astype(np.float32)
+    elif values == "i32_small":  # i32 counts in [0, 255] -> kD8Int8
+        dv = rng.integers(0, 256, len(ix)).astype(np.int32)
     elif values == "i32":
         dv = rng.integers(-50, 5000, len(ix)).astype(np.int32)
     else:                      # random floats with top-byte escapes -> kD8Coded ("signed": some negative)
@@ -324,12 +329,12 @@ def _fused_store(tmp_path, values, seed=11):
         wide = rng.random(len(ix)) < 0.05
         mag = rng.standard_normal(wide.sum()) * 10.0 ** rng.integers(-8, 9, wide.sum())
         dv[wide] = (mag if values == "signed" else np.abs(mag)).astype(np.float32)
-    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 64, 2, vdt="i32" if values == "i32" else "f32")
+    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 64, 2, vdt="i32" if values.startswith("i32") else "f32")
     return tmp_path / "s", ip, ix, dv, nv
 
 
-@pytest.mark.parametrize("values,raw", [("counts", False), ("floats", False), ("floats", True), ("signed", False),
-                                        ("i32", False)])
+@pytest.mark.parametrize("values,raw", [("counts", False), ("halves", False), ("floats", False), ("floats", True),
+                                        ("signed", False), ("i32", False), ("i32_small", False)])
 @pytest.mark.parametrize("staging", ["stream_pinned", "resident_coded"])
 def test_fused_densify_from_delta_records(tmp_path, monkeypatch, values, raw, staging):
     """K3d (densify straight from the staged delta records, no k_d8_decode):
@@ -342,7 +347,8 @@ def test_fused_densify_from_delta_records(tmp_path, monkeypatch, values, raw, st
     assert ds.image_bytes()[1] > 0  # re-encoded staging image (delta records)
     # (normalize+log1p on non-negative values, where the north-star 1e-6 applies: with
     # negative entries x * T / sum can approach -1 and log1p is ill-conditioned there)
-    outs = [("native", None), ("bf16", None)] + ([] if values in ("i32", "signed") else [("f32", "normalize_log1p")])
+    outs = [("native", None), ("bf16", None)] + (
+        [] if values in ("i32", "i32_small", "signed") else [("f32", "normalize_log1p")])
     for od, xf in outs:
         got, launched = {}, {}
         for fused in ("1", "0"):
@@ -420,6 +426,45 @@ def test_staging_pull_many_blocks_per_group(tmp_path, monkeypatch, stage):
     ds = R.DeviceStore(R.StoreReader(tmp_path / "s"), 0, "stream_pinned")
     for output in ("csr", "dense"):
         it = R.BatchIterator(ds, R.LoaderConfig(4, 2048, 700, 5), 0, output=output, batches_per_launch=3)
+        seen = 0
+        for b in it:
+            g = b.global_indices_host
+            eip, eix, edv = csr_gather(ip, ix, dv, g)
+            if output == "csr":
+                mb = b.to_minibatch()
+                assert (mb.block.indptr == eip).all() and (mb.block.indices == eix).all()
+                assert mb.block.data.tobytes() == edv.tobytes()
+            else:
+                assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, nv).tobytes()
+            seen += len(g)
+        assert seen == n
+        it.close()
+    ds.close()
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_int8_value_kind_edges(tmp_path, monkeypatch, fused):
+    """kD8Int8 eligibility is exact: a record holding 255.0 / 0.0 stages one byte
+    per value, while one holding -0.0, 256.0, 255.5 or a denormal keeps a coded
+    value kind -- CSR and dense batches bit-exact either way (K3d and the
+    decode path)."""
+    monkeypatch.setenv("RFL_FUSED", fused)
+    rng = np.random.default_rng(5)
+    n, nv = 64 * 6, 700
+    nnz = rng.integers(0, 60, n)
+    ip = np.zeros(n + 1, np.uint64)
+    ip[1:] = np.cumsum(nnz)
+    ix = np.concatenate([np.sort(rng.choice(nv, k, replace=False)) for k in nnz]).astype(np.uint64)
+    dv = rng.integers(0, 256, len(ix)).astype(np.float32)
+    edges = [np.float32(-0.0), np.float32(256.0), np.float32(255.5), np.float32(1e-45), np.float32(255.0)]
+    for r, e in enumerate(edges):  # one edge value in each of the first records (64 rows each)
+        k0, k1 = int(ip[64 * r]), int(ip[64 * (r + 1)])
+        if k1 > k0:
+            dv[k0 + (k1 - k0) // 2] = e
+    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 64, 3)
+    ds = R.DeviceStore(R.StoreReader(tmp_path / "s"), 0, "stream_pinned")
+    for output in ("csr", "dense"):
+        it = R.BatchIterator(ds, R.LoaderConfig(64, 256, 96, 2), 0, output=output)
         seen = 0
         for b in it:
             g = b.global_indices_host
