@@ -64,11 +64,13 @@ enum StageMode : uint32_t { kStageVerbatim = 0, kStageIdx16 = 1, kStageDelta = 2
 // Per-record staging encoding (staging.cpp): kind (D8Kind), staged bytes, bytes
 // of the expanded record, top-byte dictionary + escape count of coded values.
 struct StagePlan {
-    uint8_t kind = 0;
+    uint8_t kind = 0;  // D8Kind, | kD8Packed when the column deltas are bit-packed
     std::array<uint8_t, 4> dict{0, 0, 0, 0};
     uint64_t n_esc = 0, bytes = 0, exp = 0;
+    uint64_t pbytes = 0;  // packed delta bits, bytes (kD8Packed)
 };
-StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat = true);
+StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat = true,
+                         bool pack_deltas = false);
 void encode_csr_stage(const uint8_t* rec, uint64_t vs, const StagePlan& p, uint8_t* dst);
 bool one_hot_record(const uint8_t* rec, uint64_t rows, uint64_t n_var);
 void encode_one_hot(const uint8_t* rec, uint64_t rows, uint64_t n_var, uint8_t* dst);

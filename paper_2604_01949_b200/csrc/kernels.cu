@@ -373,6 +373,45 @@ __device__ __forceinline__ void st16_any(void* p, const uint32_t* w) {
     }
 }
 
+// ---- bit-packed column deltas (kD8Packed, kernels.cuh d8_packed_layout) ----
+__device__ __forceinline__ uint32_t nibble_sum(uint32_t x) {
+    return (((x & 0x0F0F0F0Fu) + ((x >> 4) & 0x0F0F0F0Fu)) * 0x01010101u) >> 24;
+}
+// bit offset of group g's deltas (from the record's packed-bits start) and its width
+__device__ __forceinline__ uint32_t packed_group(const uint8_t* widths, const uint8_t* skip, uint64_t g,
+                                                 uint32_t& w) {
+    const uint64_t s = g >> 5;
+    const uint32_t n = static_cast<uint32_t>(g & 31);  // widths of groups 32s .. g-1 to add
+    uint32_t sum = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+        const int k = static_cast<int>(n) - 8 * static_cast<int>(q);  // nibbles of this word before g
+        if (k <= 0) break;
+        const uint32_t word = ld_u32(widths + 16 * s + 4 * q);
+        sum += nibble_sum(k >= 8 ? word : word & ((1u << (4 * k)) - 1u));
+    }
+    w = (static_cast<uint32_t>(__ldg(widths + (g >> 1))) >> (4 * (g & 1))) & 15u;
+    return ld_u32(skip + 4 * s) + 16u * sum;
+}
+// the 16 deltas of a group as bytes of d[4] (LSB-first w-bit fields; the stream has 16 B slack)
+__device__ __forceinline__ void unpack16(const uint8_t* bits, uint32_t off, uint32_t w, uint32_t (&d)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = 0u;
+    if (w == 0) return;
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(bits) + (off >> 5);
+    uint32_t x[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) x[q] = __ldg(p + q);
+    const uint32_t sh = off & 31u, mask = (1u << w) - 1u;
+#pragma unroll
+    for (uint32_t j = 0; j < 16; ++j) {
+        const uint32_t pos = sh + j * w, wi = pos >> 5, b = pos & 31u;
+        const uint32_t lo = wi == 0 ? x[0] : wi == 1 ? x[1] : wi == 2 ? x[2] : wi == 3 ? x[3] : x[4];
+        const uint32_t hi = wi == 0 ? x[1] : wi == 1 ? x[2] : wi == 2 ? x[3] : x[4];
+        d[j >> 2] |= ((__funnelshift_r(lo, hi, b) & mask) << (8 * (j & 3)));
+    }
+}
+
 struct D8Jobs {
     uint32_t n, vs;
     uint64_t n_var;   // kOneHot4 rows
@@ -414,9 +453,17 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
         for (uint64_t i = tid; i < (jb.bytes + 15) / 16; i += nt) d4[i] = ld_v4(s4 + i);
         return;
     }
-    const bool coded = jb.kind == kD8Coded || jb.kind == kD8Coded16;
-    const uint32_t low_b = jb.kind == kD8Coded16 ? 1u : 3u;
+    const uint32_t kind = jb.kind & ~kD8Packed;
+    const bool packed = (jb.kind & kD8Packed) != 0;
+    const bool coded = kind == kD8Coded || kind == kD8Coded16;
+    const uint32_t low_b = kind == kD8Coded16 ? 1u : 3u;
     const uint64_t rows = ld_u32(jb.src), nnz = ld_u64_a4(jb.src + 4);
+    uint64_t dsec = ~0ull;
+    D8Packed PL{};
+    if (packed) {
+        PL = d8_packed_layout(rows, nnz, ld_u32(jb.src + d8_packed_layout(rows, nnz, 0).pbytes_at));
+        dsec = PL.end - PL.pbytes_at;
+    }
     const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
     const uint32_t* s32 = reinterpret_cast<const uint32_t*>(jb.src);
     uint32_t* d32 = reinterpret_cast<uint32_t*>(jb.dst);
@@ -426,16 +473,16 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
     uint8_t* dv = jb.dst + head + ((2 * nnz + 7) & ~7ull);
     D8vLayout L{};
     if (coded) {
-        L = d8v_layout(rows, nnz, ld_u32(jb.src + d8v_layout(rows, nnz, 0).n_esc), low_b);
-    } else if (jb.kind == kD8Int8) {  // 1-byte integer values -> 4-byte f32 / i32
-        const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
+        L = d8v_layout(rows, nnz, ld_u32(jb.src + d8v_layout(rows, nnz, 0, low_b, dsec).n_esc), low_b, dsec);
+    } else if (kind == kD8Int8) {  // 1-byte integer values -> 4-byte f32 / i32
+        const uint64_t voff = d8_values_offset(rows, nnz, dsec);
         const uint8_t* sv = jb.src + voff;
         for (uint64_t i = tid; i < nnz; i += nt) {
             const uint32_t u = __ldg(sv + i);
             reinterpret_cast<uint32_t*>(dv)[i] = jobs.vfloat ? __float_as_uint(static_cast<float>(u)) : u;
         }
     } else {  // raw values: copied word-wise (+ byte tail)
-        const uint64_t voff = (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
+        const uint64_t voff = d8_values_offset(rows, nnz, dsec);
         const uint64_t vbytes = nnz * jobs.vs;
         const uint8_t* sv = jb.src + voff;
         for (uint64_t i = tid; i < vbytes / 4; i += nt)
@@ -460,9 +507,14 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
             const uint32_t vm = b > a ? ((b == 32u ? 0u : (1u << b)) - (1u << a)) & 0xffffu : 0u;  // valid entries
             const bool vec = k0 + 16 <= nnz;  // whole 16-entry group inside the record's arrays
             uint32_t d[4] = {0u, 0u, 0u, 0u}, cw = 0u, lw[12];
+            if (vm && packed) {
+                uint32_t w;
+                const uint32_t off = packed_group(jb.src + PL.widths, jb.src + PL.skip, k0 >> 4, w);
+                unpack16(jb.src + PL.bits, off, w, d);
+            }
             if (vm) {
                 if (vec) {
-                    ld16_any(delta + k0, d);
+                    if (!packed) ld16_any(delta + k0, d);
                     if (coded) cw = ld_u32(jb.src + L.codes + (k0 >> 2));
                     if (coded && low_b == 1) ld16_any(jb.src + L.low3 + k0, lw);
                     if (coded && low_b == 3) {
@@ -476,7 +528,7 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
 #pragma unroll
                     for (uint32_t j = 0; j < 16; ++j) {
                         if (k0 + j >= nnz) continue;
-                        d[j >> 2] |= static_cast<uint32_t>(__ldg(delta + k0 + j)) << (8 * (j & 3));
+                        if (!packed) d[j >> 2] |= static_cast<uint32_t>(__ldg(delta + k0 + j)) << (8 * (j & 3));
                         if (coded) cw |= ((static_cast<uint32_t>(__ldg(jb.src + L.codes + ((k0 + j) >> 2))) >>
                                            (2 * ((k0 + j) & 3))) & 3u) << (2 * j);
                         if (coded && low_b == 1)
@@ -876,19 +928,23 @@ __global__ void __launch_bounds__(THREADS, MINB)
 constexpr uint64_t kKindShift = 60, kOffMask = (1ull << kKindShift) - 1;
 
 struct D8RowDesc {
-    const uint8_t* delta;  // column deltas u8 (record entry 0)
+    const uint8_t* delta;  // column deltas u8 (record entry 0); packed: the group widths
+    const uint8_t* pskip;  // packed: bit offset of every 32nd group
+    const uint8_t* pbits;  // packed: the delta bit stream
     const uint8_t* low;    // kD8Raw: raw 4-B values; coded: low value bytes
     const uint8_t* codes;  // 2-bit top-byte codes
     const uint8_t* esc;    // escaped top bytes
     uint64_t gidx;
     uint32_t lo, hi, nrec;  // row entries [lo, hi) of the record's nrec
-    uint32_t first, esc_at, dict, kind, pad;
+    uint32_t first, esc_at, dict, kind, packed;  // kind without the kD8Packed flag
 };
 
 __device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef& r) {
     D8RowDesc d;
     const uint8_t* rec = a.base + (r.rec_off & kOffMask);
     d.kind = static_cast<uint32_t>(r.rec_off >> kKindShift);
+    d.packed = d.kind & kD8Packed;
+    d.kind &= ~kD8Packed;
     const uint64_t within = r.gidx % a.chunk_rows;
     const uint32_t rows = ld_u32(rec);
     const uint64_t nnz = ld_u64_a4(rec + 4);
@@ -900,14 +956,23 @@ __device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef
     d.first = __ldg(reinterpret_cast<const unsigned short*>(rec + first_off) + within);
     d.delta = rec + first_off + ((2 * static_cast<uint64_t>(rows) + 3) & ~3ull);
     d.gidx = r.gidx;
-    d.pad = 0;
+    uint64_t dsec = ~0ull;
+    d.pskip = d.pbits = nullptr;
+    if (d.packed) {
+        const D8Packed P = d8_packed_layout(rows, nnz, ld_u32(d.delta));
+        dsec = P.end - P.pbytes_at;
+        d.delta = rec + P.widths;
+        d.pskip = rec + P.skip;
+        d.pbits = rec + P.bits;
+    }
     if (d.kind == kD8Raw || d.kind == kD8Int8) {
-        d.low = rec + d8_values_offset(rows, nnz);
+        d.low = rec + d8_values_offset(rows, nnz, dsec);
         d.codes = d.esc = nullptr;
         d.esc_at = d.dict = 0;
     } else {
-        const D8vLayout L0 = d8v_layout(rows, nnz, 0);
-        const D8vLayout L = d8v_layout(rows, nnz, ld_u32(rec + L0.n_esc), d.kind == kD8Coded16 ? 1 : 3);
+        const uint32_t lb = d.kind == kD8Coded16 ? 1 : 3;
+        const D8vLayout L0 = d8v_layout(rows, nnz, 0, lb, dsec);
+        const D8vLayout L = d8v_layout(rows, nnz, ld_u32(rec + L0.n_esc), lb, dsec);
         d.low = rec + L.low3;
         d.codes = rec + L.codes;
         d.esc = rec + L.esc;
@@ -933,8 +998,13 @@ __device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw1
     for (int q = 0; q < 16; ++q) x.lw[q] = 0u;
     if (!x.vm) return;
     const uint32_t kind = r.kind;
+    if (r.packed) {
+        uint32_t w;
+        const uint32_t off = packed_group(r.delta, r.pskip, k0 >> 4, w);
+        unpack16(r.pbits, off, w, x.d);
+    }
     if (k0 + 16 <= r.nrec) {
-        ld16_any(r.delta + k0, x.d);
+        if (!r.packed) ld16_any(r.delta + k0, x.d);
         if (kind == kD8Raw) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) ld16_any(r.low + 4 * k0 + 16 * q, x.lw + 4 * q);
@@ -956,7 +1026,7 @@ __device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw1
     for (uint32_t j = 0; j < 16; ++j) {
         if (k0 + j >= r.nrec) continue;
         const uint64_t k = k0 + j;
-        x.d[j >> 2] |= static_cast<uint32_t>(__ldg(r.delta + k)) << (8 * (j & 3));
+        if (!r.packed) x.d[j >> 2] |= static_cast<uint32_t>(__ldg(r.delta + k)) << (8 * (j & 3));
         if (kind == kD8Raw) {
             x.lw[j] = ld_u32(r.low + 4 * k);
         } else if (kind == kD8Int8) {

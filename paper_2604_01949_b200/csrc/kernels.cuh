@@ -65,11 +65,39 @@ inline uint64_t idx16_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) {
 // padded to 4 B][column deltas u8 x nnz (0 for a row's first entry), padded to
 // 8 B from the record start][data].  5 B per stored f32 entry cross PCIe; a
 // decode kernel expands each staged record into the idx16 layout in HBM.
-RFL_HD inline uint64_t d8_values_offset(uint64_t rows, uint64_t nnz) {
+// dsec = bytes of the column-delta section (nnz for u8 deltas; d8_packed_layout for
+// bit-packed ones)
+RFL_HD inline uint64_t d8_values_offset(uint64_t rows, uint64_t nnz, uint64_t dsec = ~0ull) {
     const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
-    return (head + ((2 * rows + 3) & ~3ull) + nnz + 7) & ~7ull;
+    return (head + ((2 * rows + 3) & ~3ull) + (dsec == ~0ull ? nnz : dsec) + 7) & ~7ull;
 }
-inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs) { return d8_values_offset(rows, nnz) + vs * nnz; }
+inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs, uint64_t dsec = ~0ull) {
+    return d8_values_offset(rows, nnz, dsec) + vs * nnz;
+}
+// Bit-packed column deltas (the pinned staging image; kind | kD8Packed): the delta
+// section becomes [packed bytes u32][bit width u4 per group of 16 record entries,
+// pad 4][bit offset u32 of every 32nd group][pad to 16 from the record start]
+// [group g: 16 deltas of width_g bits, LSB first][32 B slack] -- a group's width
+// is that of its largest delta (column gaps are ~geometric: 5-6 bits instead of 8).
+// Entry k0 = 16g's offset = skip[g / 32] + 16 x (widths of groups 32(g/32) .. g-1).
+constexpr uint32_t kD8Packed = 8;
+struct D8Packed {
+    uint64_t pbytes_at, widths, skip, bits, end;  // record offsets
+};
+RFL_HD inline D8Packed d8_packed_layout(uint64_t rows, uint64_t nnz, uint64_t packed_bytes) {
+    D8Packed d{};
+    const uint64_t groups = (nnz + 15) / 16;
+    d.pbytes_at = kCsrHeaderBytes + 4 * (rows + 1) + ((2 * rows + 3) & ~3ull);
+    d.widths = d.pbytes_at + 4;
+    d.skip = d.widths + ((((groups + 1) / 2) + 3) & ~3ull);
+    d.bits = (d.skip + 4 * ((groups + 31) / 32) + 15) & ~15ull;
+    d.end = d.bits + ((packed_bytes + 15) & ~15ull) + 32;
+    return d;
+}
+RFL_HD inline uint64_t d8_packed_section(uint64_t rows, uint64_t nnz, uint64_t packed_bytes) {
+    const D8Packed d = d8_packed_layout(rows, nnz, packed_bytes);
+    return d.end - d.pbytes_at;
+}
 // Delta records with 4-byte values may also code each value's top byte (sign +
 // high exponent bits, a handful of distinct values per record) against a
 // 3-entry dictionary: [head][first u16 x rows, pad 4][deltas u8 x nnz, pad 4]
@@ -81,11 +109,12 @@ struct D8vLayout {
 };
 // low_bytes = 3, or 1 when the low 16 bits of every value of the record are zero
 // (integer counts stored as float: byte 2 carries the exponent LSB + top mantissa bits)
-RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc, uint64_t low_bytes = 3) {
+RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc, uint64_t low_bytes = 3,
+                                   uint64_t dsec = ~0ull) {
     D8vLayout l{};
     l.first = kCsrHeaderBytes + 4 * (rows + 1);
     l.delta = l.first + ((2 * rows + 3) & ~3ull);
-    l.esc_base = l.delta + ((nnz + 3) & ~3ull);
+    l.esc_base = l.delta + (((dsec == ~0ull ? nnz : dsec) + 3) & ~3ull);
     l.dict = l.esc_base + 4 * rows;
     l.n_esc = l.dict + 4;
     l.codes = l.n_esc + 4;

@@ -51,7 +51,61 @@ void parallel_for(uint64_t n, F&& f) {  // f(i) over [0, n) on up to 16 threads;
 }  // namespace
 
 // ---------------------------------------------------------- per-record codecs --
-StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat) {
+namespace {
+// column delta of record entry k (0 at a row's first entry)
+struct Deltas {
+    const uint8_t* ip;
+    const uint8_t* ix;
+    uint64_t rows, nnz;
+    std::vector<uint8_t> d;
+    Deltas(const uint8_t* rec) : ip(rec + kCsrHeaderBytes) {
+        rows = rd32(rec);
+        nnz = rd64(rec + 4);
+        ix = ip + 4 * (rows + 1);
+        d.assign(nnz, 0);
+        for (uint64_t r = 0; r < rows; ++r) {
+            const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
+            for (uint64_t k = lo + 1; k < hi; ++k) d[k] = static_cast<uint8_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)));
+        }
+    }
+};
+uint32_t bit_width(uint32_t v) {
+    uint32_t w = 0;
+    while (v >> w) ++w;
+    return w;
+}
+// bytes of the bit-packed delta stream (sum over groups of 16 x width)
+uint64_t packed_bits_bytes(const std::vector<uint8_t>& d) {
+    uint64_t bits = 0;
+    for (uint64_t g = 0; g * 16 < d.size(); ++g) {
+        uint32_t mx = 0;
+        for (uint64_t k = g * 16; k < std::min<uint64_t>(d.size(), g * 16 + 16); ++k) mx = std::max<uint32_t>(mx, d[k]);
+        bits += 16ull * bit_width(mx);
+    }
+    return (bits + 7) / 8;
+}
+}  // namespace
+
+StagePlan plan_csr_stage_u8(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat);
+
+StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat,
+                         bool pack_deltas) {
+    StagePlan p = plan_csr_stage_u8(rec, vs, allow_delta, code_values, vfloat);
+    if (!pack_deltas || (p.kind != kD8Raw && p.kind != kD8Coded && p.kind != kD8Coded16 && p.kind != kD8Int8)) return p;
+    const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
+    const Deltas dl(rec);
+    const uint64_t pb = packed_bits_bytes(dl.d);
+    const uint64_t dsec = d8_packed_section(rows, nnz, pb);
+    if (dsec >= nnz) return p;  // (tiny records: the u8 deltas are smaller)
+    const uint64_t ovs = p.kind == kD8Int8 ? 1 : vs;
+    p.pbytes = pb;
+    if (p.kind == kD8Raw || p.kind == kD8Int8) p.bytes = d8_record_bytes(rows, nnz, ovs, dsec);
+    else p.bytes = d8v_layout(rows, nnz, p.n_esc, p.kind == kD8Coded16 ? 1 : 3, dsec).bytes;
+    p.kind |= kD8Packed;
+    return p;
+}
+
+StagePlan plan_csr_stage_u8(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat) {
     const uint64_t rows = rd32(rec), nnz = rd64(rec + 4);
     const uint8_t* ip = rec + kCsrHeaderBytes;
     const uint8_t* ix = ip + 4 * (rows + 1);
@@ -137,19 +191,47 @@ void encode_csr_stage(const uint8_t* src, uint64_t vs, const StagePlan& p, uint8
     }
     uint8_t* first = dst + head;
     uint8_t* delta = first + ((2 * rows + 3) & ~3ull);
+    const bool packed = (p.kind & kD8Packed) != 0;
+    const uint32_t kind = p.kind & ~kD8Packed;
     for (uint64_t r = 0; r < rows; ++r) {
         const uint64_t lo = rd32(ip + 4 * r), hi = rd32(ip + 4 * (r + 1));
         const uint16_t f = lo < hi ? static_cast<uint16_t>(rd32(ix + 4 * lo)) : 0;
         std::memcpy(first + 2 * r, &f, 2);
-        for (uint64_t k = lo; k < hi; ++k)
-            delta[k] = k == lo ? 0 : static_cast<uint8_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)));
+        if (!packed)
+            for (uint64_t k = lo; k < hi; ++k)
+                delta[k] = k == lo ? 0 : static_cast<uint8_t>(rd32(ix + 4 * k) - rd32(ix + 4 * (k - 1)));
     }
-    if (p.kind == kD8Raw) {
-        std::memcpy(dst + d8_values_offset(rows, nnz), val, vs * nnz);
+    uint64_t dsec = ~0ull;
+    if (packed) {
+        const Deltas dl(src);
+        const D8Packed L = d8_packed_layout(rows, nnz, p.pbytes);
+        dsec = L.end - L.pbytes_at;
+        const uint32_t pb32 = static_cast<uint32_t>(p.pbytes);
+        std::memcpy(dst + L.pbytes_at, &pb32, 4);
+        uint64_t bit = 0;
+        for (uint64_t g = 0; g * 16 < nnz; ++g) {
+            if (g % 32 == 0) {
+                const uint32_t b32 = static_cast<uint32_t>(bit);
+                std::memcpy(dst + L.skip + 4 * (g / 32), &b32, 4);
+            }
+            uint32_t mx = 0;
+            const uint64_t k1 = std::min<uint64_t>(nnz, g * 16 + 16);
+            for (uint64_t k = g * 16; k < k1; ++k) mx = std::max<uint32_t>(mx, dl.d[k]);
+            const uint32_t w = bit_width(mx);
+            dst[L.widths + g / 2] |= static_cast<uint8_t>(w << (4 * (g & 1)));
+            for (uint64_t k = g * 16; k < g * 16 + 16; ++k, bit += w) {
+                const uint32_t v = k < k1 ? dl.d[k] : 0u;
+                for (uint32_t b = 0; b < w; ++b)
+                    if ((v >> b) & 1u) dst[L.bits + ((bit + b) >> 3)] |= static_cast<uint8_t>(1u << ((bit + b) & 7));
+            }
+        }
+    }
+    if (kind == kD8Raw) {
+        std::memcpy(dst + d8_values_offset(rows, nnz, dsec), val, vs * nnz);
         return;
     }
-    if (p.kind == kD8Int8) {
-        uint8_t* v8 = dst + d8_values_offset(rows, nnz);
+    if (kind == kD8Int8) {
+        uint8_t* v8 = dst + d8_values_offset(rows, nnz, dsec);
         for (uint64_t k = 0; k < nnz; ++k) {
             uint32_t b;
             std::memcpy(&b, val + 4 * k, 4);
@@ -162,8 +244,8 @@ void encode_csr_stage(const uint8_t* src, uint64_t vs, const StagePlan& p, uint8
         }
         return;
     }
-    const bool c16 = p.kind == kD8Coded16;
-    const D8vLayout L = d8v_layout(rows, nnz, p.n_esc, c16 ? 1 : 3);
+    const bool c16 = kind == kD8Coded16;
+    const D8vLayout L = d8v_layout(rows, nnz, p.n_esc, c16 ? 1 : 3, dsec);
     std::memcpy(dst + L.dict, p.dict.data(), 4);
     const uint32_t ne = static_cast<uint32_t>(p.n_esc);
     std::memcpy(dst + L.n_esc, &ne, 4);
@@ -260,6 +342,10 @@ bool DStore::build_staged_image(uint32_t mode) {
     const char* te = std::getenv("RFL_TRACE");
     const bool trace = te && te[0] == '1';
     const bool code_values = !(ve && ve[0] == '0');
+    // bit-packed column deltas for the PCIe-bound pinned image (RFL_PACK_DELTAS=0: u8 deltas);
+    // the HBM-resident coded image keeps u8 deltas (K3d there is bound by its dense writes)
+    const char* pe = std::getenv("RFL_PACK_DELTAS");
+    const bool pack = staging_ == kStreamPinned && !(pe && pe[0] == '0');
     // virtual reservation bounding every encoding (each kind is at most the
     // verbatim record + 2 B per row + padding), committed page by page as filled
     uint64_t bound = kPad + 4096;
@@ -296,7 +382,7 @@ bool DStore::build_staged_image(uint32_t mode) {
                     plans[k].bytes = m.rows_in_chunk(q) * (m.n_var / 16);
                     plans[k].exp = rec_len_[q];
                 } else {
-                    plans[k] = plan_csr_stage(rec, vs, mode == kStageDelta, code_values, m.value_dtype != VDtype::i32);
+                    plans[k] = plan_csr_stage(rec, vs, mode == kStageDelta, code_values, m.value_dtype != VDtype::i32, pack);
                 }
             });
             if (!one_hot_ok) {  // not a one-hot store: the verbatim image
