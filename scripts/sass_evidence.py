@@ -19,6 +19,11 @@ HOT = [  # (label, mangled-name regex)
     ("K4 dense gather bulk u8->bf16 (cfg3)", r"k_dense_gather_bulkILi1ELi2ELi256E"),
     ("d8 decode (delta / coded / one-hot staging)", r"k_d8_decode"),
     ("K1 row scan (decoupled look-back)", r"k_row_scan"),
+    ("K3d densify from the coded staging records (f32)", r"k_csr_densify_d8IffLi256ELi2E"),
+    ("K4 dense gather by whole rows u8->bf16 (cfg3)", r"k_dense_gather_rowsILi1E"),
+    ("K4 dense gather by whole rows raw", r"k_dense_gather_rowsILi0E"),
+    ("K4o one-hot rows from 2-bit codes (u8)", r"k_onehot_gather_rowsILi0E"),
+    ("staging pull (pinned image -> HBM slots, TMA)", r"k_stage_pull"),
 ]
 CLASSES = [
     ("UBLKCP (1-D TMA bulk copy)", r"\bUBLKCP"),
@@ -49,7 +54,7 @@ def main():
             continue
         body = hits[0]
         name = body.split("\n", 1)[0].strip()
-        lines = [l for l in body.split("\n") if re.search(r"/\*[0-9a-f]{4}\*/", l)]
+        lines = [l for l in body.split("\n") if re.search(r"/\*[0-9a-f]{4,}\*/", l)]
         out.append(f"## {label}\n\n`{name}` — {len(lines)} instructions\n")
         out.append("| class | count |\n|---|---|")
         for cname, cre in CLASSES:
@@ -57,7 +62,7 @@ def main():
         k = next((i for i, l in enumerate(lines) if "UBLKCP" in l), None)
         if k is None:
             k = next((i for i, l in enumerate(lines) if re.search(r"LDG\.E\S*\.128", l)), 0)
-        ex = [re.sub(r"\s+/\*[0-9a-f]{4}\*/\s*", " ", l).strip() for l in lines[max(0, k - 6):k + 8]]
+        ex = [re.sub(r"\s+/\*[0-9a-f]{4,}\*/\s*", " ", l).strip() for l in lines[max(0, k - 6):k + 8]]
         ex = [re.sub(r"\s*/\*.*?\*/", "", l) for l in ex]
         out.append("\n```\n" + "\n".join(ex) + "\n```\n")
     sys.stdout.write("\n".join(out) + "\n")
