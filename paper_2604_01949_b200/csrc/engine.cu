@@ -977,6 +977,8 @@ void GpuLoader::stage_block(uint64_t id) {
         }
         reader_->release(seq, copy_);
     }
+    lv.off0 = reinterpret_cast<uint64_t>(lv.slot.ptr) + lv.chunk_off[0];
+    lv.single = q0 == q1;
     count_fetch(id);
 }
 
@@ -1249,8 +1251,9 @@ bool GpuLoader::assemble_group() {
                 hr[j] = {offs[q], gr};
             } else {
                 const uint64_t blk = div_f_.div(gr);
-                Live& lv = live_[blk];
-                hr[j] = {static_cast<uint64_t>(lv.slot.ptr - base) + lv.chunk_off[q - lv.first_chunk], gr};
+                Live& lv = live_[blk];  // (streamed: base == nullptr, row refs hold device addresses)
+                hr[j] = {lv.single ? lv.off0 : reinterpret_cast<uint64_t>(lv.slot.ptr) + lv.chunk_off[q - lv.first_chunk],
+                         gr};
                 if (--lv.live_rows == 0) done_blocks_.push_back(blk);  // released after this group's kernel
             }
             if (kinds) hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;

@@ -304,6 +304,8 @@ private:
         DStore::SlotRef slot;
         uint64_t live_rows = 0;
         uint64_t first_chunk = 0;
+        uint64_t off0 = 0;     // device address of the block's first staged record
+        bool single = false;   // the block is one chunk record (row refs skip chunk_off)
         std::vector<uint64_t> chunk_off;  // offset of each staged record inside the slot
     };
     // one replayed batch: its rows, the blocks pulled in while it was drawn, and the
