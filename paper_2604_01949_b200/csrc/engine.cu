@@ -162,7 +162,8 @@ DStore::DStore(std::shared_ptr<HostStore> hs, int device, uint32_t staging)
             d8_fused_ = true;
             for (uint8_t k : d8_rec_)
                 d8_fused_ = d8_fused_ && ((k & ~kD8Packed) == kD8Raw || (k & ~kD8Packed) == kD8Coded ||
-                                          (k & ~kD8Packed) == kD8Coded16 || (k & ~kD8Packed) == kD8Int8);
+                                          (k & ~kD8Packed) == kD8Coded16 || (k & ~kD8Packed) == kD8Int8 ||
+                                          (k & ~kD8Packed) == kD8IntP);
             for (uint32_t n : row_nnz_) d8_fused_ = d8_fused_ && n <= kD8FusedMaxNnz;
         }
     } catch (...) {  // the destructor does not run for a throwing constructor

@@ -67,7 +67,8 @@ struct StagePlan {
     uint8_t kind = 0;  // D8Kind, | kD8Packed when the column deltas are bit-packed
     std::array<uint8_t, 4> dict{0, 0, 0, 0};
     uint64_t n_esc = 0, bytes = 0, exp = 0;
-    uint64_t pbytes = 0;  // packed delta bits, bytes (kD8Packed)
+    uint64_t pbytes = 0;    // packed delta bits, bytes (kD8Packed)
+    uint64_t pbytes_v = 0;  // packed value bits, bytes (kD8IntP)
 };
 StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat = true,
                          bool pack_deltas = false);

@@ -474,6 +474,18 @@ __global__ void __launch_bounds__(256) k_d8_decode(const __grid_constant__ D8Job
     D8vLayout L{};
     if (coded) {
         L = d8v_layout(rows, nnz, ld_u32(jb.src + d8v_layout(rows, nnz, 0, low_b, dsec).n_esc), low_b, dsec);
+    } else if (kind == kD8IntP) {  // bit-packed integer values, one group of 16 per thread
+        const uint64_t vo = d8_values_offset(rows, nnz, dsec);
+        const D8Packed V = d8_packed_at(vo, nnz, ld_u32(jb.src + vo));
+        for (uint64_t g = tid; g * 16 < nnz; g += nt) {
+            uint32_t w, v4[4];
+            const uint32_t off = packed_group(jb.src + V.widths, jb.src + V.skip, g, w);
+            unpack16(jb.src + V.bits, off, w, v4);
+            for (uint32_t j = 0; j < 16 && g * 16 + j < nnz; ++j) {
+                const uint32_t u = (v4[j >> 2] >> (8 * (j & 3))) & 255u;
+                reinterpret_cast<uint32_t*>(dv)[g * 16 + j] = jobs.vfloat ? __float_as_uint(static_cast<float>(u)) : u;
+            }
+        }
     } else if (kind == kD8Int8) {  // 1-byte integer values -> 4-byte f32 / i32
         const uint64_t voff = d8_values_offset(rows, nnz, dsec);
         const uint8_t* sv = jb.src + voff;
@@ -965,7 +977,14 @@ __device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef
         d.pskip = rec + P.skip;
         d.pbits = rec + P.bits;
     }
-    if (d.kind == kD8Raw || d.kind == kD8Int8) {
+    if (d.kind == kD8IntP) {  // packed value bytes: codes = widths, esc = skip, low = bits
+        const uint64_t vo = d8_values_offset(rows, nnz, dsec);
+        const D8Packed V = d8_packed_at(vo, nnz, ld_u32(rec + vo));
+        d.codes = rec + V.widths;
+        d.esc = rec + V.skip;
+        d.low = rec + V.bits;
+        d.esc_at = d.dict = 0;
+    } else if (d.kind == kD8Raw || d.kind == kD8Int8) {
         d.low = rec + d8_values_offset(rows, nnz, dsec);
         d.codes = d.esc = nullptr;
         d.esc_at = d.dict = 0;
@@ -1002,6 +1021,18 @@ __device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw1
         uint32_t w;
         const uint32_t off = packed_group(r.delta, r.pskip, k0 >> 4, w);
         unpack16(r.pbits, off, w, x.d);
+    }
+    if (kind == kD8IntP) {  // 16 value bytes -> lw[0..3], like kD8Int8's
+        uint32_t w, v4[4];
+        const uint32_t off = packed_group(r.codes, r.esc, k0 >> 4, w);
+        unpack16(r.low, off, w, v4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x.lw[q] = v4[q];
+        if (k0 + 16 <= r.nrec && !r.packed) ld16_any(r.delta + k0, x.d);
+        if (k0 + 16 > r.nrec && !r.packed)
+            for (uint32_t j = 0; j < 16; ++j)
+                if (k0 + j < r.nrec) x.d[j >> 2] |= static_cast<uint32_t>(__ldg(r.delta + k0 + j)) << (8 * (j & 3));
+        return;
     }
     if (k0 + 16 <= r.nrec) {
         if (!r.packed) ld16_any(r.delta + k0, x.d);
@@ -1086,7 +1117,7 @@ __device__ __forceinline__ void decode_d8(const D8RowDesc& r, const D8Raw16& x, 
         uint32_t bits;
         if (r.kind == kD8Raw) {
             bits = x.lw[j];
-        } else if (r.kind == kD8Int8) {
+        } else if (r.kind == kD8Int8 || r.kind == kD8IntP) {
             const uint32_t u = (x.lw[j >> 2] >> (8 * (j & 3))) & 255u;
             bits = std::is_floating_point_v<SrcT> ? __float_as_uint(static_cast<float>(u)) : u;
         } else {

@@ -84,15 +84,18 @@ constexpr uint32_t kD8Packed = 8;
 struct D8Packed {
     uint64_t pbytes_at, widths, skip, bits, end;  // record offsets
 };
-RFL_HD inline D8Packed d8_packed_layout(uint64_t rows, uint64_t nnz, uint64_t packed_bytes) {
+RFL_HD inline D8Packed d8_packed_at(uint64_t at, uint64_t nnz, uint64_t packed_bytes) {  // at: 4-B aligned
     D8Packed d{};
     const uint64_t groups = (nnz + 15) / 16;
-    d.pbytes_at = kCsrHeaderBytes + 4 * (rows + 1) + ((2 * rows + 3) & ~3ull);
+    d.pbytes_at = at;
     d.widths = d.pbytes_at + 4;
     d.skip = d.widths + ((((groups + 1) / 2) + 3) & ~3ull);
     d.bits = (d.skip + 4 * ((groups + 31) / 32) + 15) & ~15ull;
     d.end = d.bits + ((packed_bytes + 15) & ~15ull) + 32;
     return d;
+}
+RFL_HD inline D8Packed d8_packed_layout(uint64_t rows, uint64_t nnz, uint64_t packed_bytes) {
+    return d8_packed_at(kCsrHeaderBytes + 4 * (rows + 1) + ((2 * rows + 3) & ~3ull), nnz, packed_bytes);
 }
 RFL_HD inline uint64_t d8_packed_section(uint64_t rows, uint64_t nnz, uint64_t packed_bytes) {
     const D8Packed d = d8_packed_layout(rows, nnz, packed_bytes);
@@ -130,7 +133,10 @@ RFL_HD inline D8vLayout d8v_layout(uint64_t rows, uint64_t nnz, uint64_t n_esc, 
 // kD8Int8: the kD8Raw layout with 1-byte values, for 4-byte-value records whose every
 // value is an integer in [0, 255] (raw counts: f32 bits of float(u), or i32 u) --
 // no top-byte codes; the value byte IS the value
-enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2, kOneHot4 = 3, kD8Coded16 = 4, kD8Int8 = 5 };
+// kD8IntP: kD8Int8 with the value bytes bit-packed per group of 16 like packed deltas
+// (d8_packed_at at the values offset; counts 1..64 take 6 bits)
+enum D8Kind : uint32_t { kD8Raw = 0, kD8Coded = 1, kIdx16Copy = 2, kOneHot4 = 3, kD8Coded16 = 4, kD8Int8 = 5,
+                         kD8IntP = 6 };
 struct D8Job {
     const uint8_t* src;  // staged record (device)
     uint8_t* dst;        // idx16 record (device)

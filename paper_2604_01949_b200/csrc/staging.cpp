@@ -74,6 +74,46 @@ uint32_t bit_width(uint32_t v) {
     while (v >> w) ++w;
     return w;
 }
+// write v[0..n) as the packed groups of d8_packed_at(at, n, pb) into rec (zeroed)
+void write_packed(uint8_t* rec, uint64_t at, const std::vector<uint8_t>& v, uint64_t pb) {
+    const uint64_t n = v.size();
+    const D8Packed L = d8_packed_at(at, n, pb);
+    const uint32_t pb32 = static_cast<uint32_t>(pb);
+    std::memcpy(rec + L.pbytes_at, &pb32, 4);
+    uint64_t bit = 0;
+    for (uint64_t g = 0; g * 16 < n; ++g) {
+        if (g % 32 == 0) {
+            const uint32_t b32 = static_cast<uint32_t>(bit);
+            std::memcpy(rec + L.skip + 4 * (g / 32), &b32, 4);
+        }
+        uint32_t mx = 0;
+        const uint64_t k1 = std::min<uint64_t>(n, g * 16 + 16);
+        for (uint64_t k = g * 16; k < k1; ++k) mx = std::max<uint32_t>(mx, v[k]);
+        uint32_t w = 0;
+        while (mx >> w) ++w;
+        rec[L.widths + g / 2] |= static_cast<uint8_t>(w << (4 * (g & 1)));
+        for (uint64_t k = g * 16; k < g * 16 + 16; ++k, bit += w) {
+            const uint32_t x = k < k1 ? v[k] : 0u;
+            for (uint32_t b = 0; b < w; ++b)
+                if ((x >> b) & 1u) rec[L.bits + ((bit + b) >> 3)] |= static_cast<uint8_t>(1u << ((bit + b) & 7));
+        }
+    }
+}
+// the value byte of each entry of an integer-valued record (kD8Int8 eligibility holds)
+std::vector<uint8_t> int8_values(const uint8_t* val, uint64_t nnz) {
+    std::vector<uint8_t> v(nnz);
+    for (uint64_t k = 0; k < nnz; ++k) {
+        uint32_t b;
+        std::memcpy(&b, val + 4 * k, 4);
+        if (b > 255u) {  // f32 bits of an integer value
+            float f;
+            std::memcpy(&f, &b, 4);
+            b = static_cast<uint32_t>(f);
+        }
+        v[k] = static_cast<uint8_t>(b);
+    }
+    return v;
+}
 // bytes of the bit-packed delta stream (sum over groups of 16 x width)
 uint64_t packed_bits_bytes(const std::vector<uint8_t>& d) {
     uint64_t bits = 0;
@@ -101,6 +141,17 @@ StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool
     p.pbytes = pb;
     if (p.kind == kD8Raw || p.kind == kD8Int8) p.bytes = d8_record_bytes(rows, nnz, ovs, dsec);
     else p.bytes = d8v_layout(rows, nnz, p.n_esc, p.kind == kD8Coded16 ? 1 : 3, dsec).bytes;
+    if (p.kind == kD8Int8) {  // the value bytes bit-packed too (kD8IntP) when smaller
+        const uint8_t* val = rec + kCsrHeaderBytes + 4 * (rows + 1) + 4 * nnz;
+        const uint64_t pbv = packed_bits_bytes(int8_values(val, nnz));
+        const uint64_t vo = d8_values_offset(rows, nnz, dsec);
+        const D8Packed V = d8_packed_at(vo, nnz, pbv);
+        if (V.end - vo < nnz) {
+            p.kind = kD8IntP;
+            p.pbytes_v = pbv;
+            p.bytes = V.end;
+        }
+    }
     p.kind |= kD8Packed;
     return p;
 }
@@ -206,25 +257,11 @@ void encode_csr_stage(const uint8_t* src, uint64_t vs, const StagePlan& p, uint8
         const Deltas dl(src);
         const D8Packed L = d8_packed_layout(rows, nnz, p.pbytes);
         dsec = L.end - L.pbytes_at;
-        const uint32_t pb32 = static_cast<uint32_t>(p.pbytes);
-        std::memcpy(dst + L.pbytes_at, &pb32, 4);
-        uint64_t bit = 0;
-        for (uint64_t g = 0; g * 16 < nnz; ++g) {
-            if (g % 32 == 0) {
-                const uint32_t b32 = static_cast<uint32_t>(bit);
-                std::memcpy(dst + L.skip + 4 * (g / 32), &b32, 4);
-            }
-            uint32_t mx = 0;
-            const uint64_t k1 = std::min<uint64_t>(nnz, g * 16 + 16);
-            for (uint64_t k = g * 16; k < k1; ++k) mx = std::max<uint32_t>(mx, dl.d[k]);
-            const uint32_t w = bit_width(mx);
-            dst[L.widths + g / 2] |= static_cast<uint8_t>(w << (4 * (g & 1)));
-            for (uint64_t k = g * 16; k < g * 16 + 16; ++k, bit += w) {
-                const uint32_t v = k < k1 ? dl.d[k] : 0u;
-                for (uint32_t b = 0; b < w; ++b)
-                    if ((v >> b) & 1u) dst[L.bits + ((bit + b) >> 3)] |= static_cast<uint8_t>(1u << ((bit + b) & 7));
-            }
-        }
+        write_packed(dst, L.pbytes_at, dl.d, p.pbytes);
+    }
+    if (kind == kD8IntP) {
+        write_packed(dst, d8_values_offset(rows, nnz, dsec), int8_values(val, nnz), p.pbytes_v);
+        return;
     }
     if (kind == kD8Raw) {
         std::memcpy(dst + d8_values_offset(rows, nnz, dsec), val, vs * nnz);

@@ -1,6 +1,6 @@
 #!/bin/bash
 # full GPU tests, smoke, N=2 (two ranks sharing the box's GPU, gloo control plane) for cfg1 and cfg5
-O=gpurun_out/s3m; mkdir -p $O
+O=gpurun_out/${1:-s3m}; mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo "pytest exit $?" >> $O/pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
