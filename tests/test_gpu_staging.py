@@ -479,3 +479,55 @@ def test_int8_value_kind_edges(tmp_path, monkeypatch, fused):
         assert seen == n
         it.close()
     ds.close()
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_packed_delta_widths(tmp_path, monkeypatch, fused):
+    """Bit-packed deltas at every group width: runs of single-entry rows (16-entry
+    groups of row starts only: width 0), consecutive columns (width 1), gaps of 255
+    (width 8), a record of 3,000+ entries (skip table past 32 groups), nnz not a
+    multiple of 16 -- CSR and dense batches bit-exact through the pinned image
+    (K3d and the decode path)."""
+    monkeypatch.setenv("RFL_FUSED", fused)
+    rng = np.random.default_rng(23)
+    nv = 6000
+    rows = []
+    for i in range(640):
+        kind = (i // 32) % 5
+        if kind == 0:
+            rows.append(np.array([int(rng.integers(0, nv))]))                  # single entries
+        elif kind == 1:
+            s0 = int(rng.integers(0, nv - 100))
+            rows.append(np.arange(s0, s0 + int(rng.integers(2, 90))))          # consecutive columns
+        elif kind == 2:
+            s0 = int(rng.integers(0, 300))
+            rows.append(s0 + 255 * np.arange(int(rng.integers(2, 22))))        # gaps of 255
+        elif kind == 3:
+            rows.append(np.sort(rng.choice(nv, int(rng.integers(150, 400)), replace=False)))
+        else:
+            rows.append(np.array([], dtype=np.int64))
+    rows[100] = np.sort(rng.choice(nv, 3100, replace=False))                    # a long row (many groups)
+    nnz = np.array([len(r) for r in rows])
+    ip = np.zeros(len(rows) + 1, np.uint64)
+    ip[1:] = np.cumsum(nnz)
+    ix = np.concatenate(rows).astype(np.uint64)
+    dv = (rng.random(len(ix)) + 0.5).astype(np.float32)
+    write_csr_store(tmp_path / "s", ip, ix, dv, nv, 64, 4)
+    n = len(rows)
+    ds = R.DeviceStore(R.StoreReader(tmp_path / "s"), 0, "stream_pinned")
+    for output in ("csr", "dense"):
+        it = R.BatchIterator(ds, R.LoaderConfig(64, 256, 100, 4), 0, output=output)
+        seen = 0
+        for b in it:
+            g = b.global_indices_host
+            eip, eix, edv = csr_gather(ip, ix, dv, g)
+            if output == "csr":
+                mb = b.to_minibatch()
+                assert (mb.block.indptr == eip).all() and (mb.block.indices == eix).all()
+                assert mb.block.data.tobytes() == edv.tobytes()
+            else:
+                assert b.data.cpu().numpy().tobytes() == to_dense(eip, eix, edv, nv).tobytes()
+            seen += len(g)
+        assert seen == n
+        it.close()
+    ds.close()
