@@ -8,13 +8,17 @@
 // pinned host memory for stream_pinned, or uploaded to HBM for resident_coded.
 // The GPU expands the staged records (k_d8_decode) before the batch kernels.
 #include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdio>
 #include <array>
 #include <atomic>
 #include <cstdlib>
+#include <cctype>
 #include <cstring>
+#include <fstream>
 #include <string>
 #include <thread>
 
@@ -27,6 +31,36 @@ namespace {
 constexpr uint64_t kAlign = kRecAlign;
 constexpr uint64_t kPad = kRecPad;
 constexpr uint64_t kWindowBytes = 512ull << 20;  // verbatim records held per window
+
+// NUMA node of the GPU's PCIe attachment (sysfs), -1 when unknown
+int gpu_numa_node(int dev) {
+    char bus[64] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::string b(bus);
+    for (char& c : b) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+    const size_t colon = b.find(':');
+    if (colon != std::string::npos && colon > 4) b = b.substr(colon - 4);  // 8-digit PCI domain -> 4
+    std::ifstream f("/sys/bus/pci/devices/" + b + "/numa_node");
+    int node = -1;
+    if (!(f >> node)) return -1;
+    return node;
+}
+
+// Prefer the GPU's NUMA node for the pages of [p, p + bytes) (first touched later):
+// on a multi-socket node the staging pull then reads socket-local memory instead
+// of crossing the socket interconnect for half the image.  Best effort, no-op on
+// one-node hosts.
+void prefer_gpu_node(void* p, uint64_t bytes, int dev) {
+    const int node = gpu_numa_node(dev);
+    if (node < 0 || node >= 256) return;
+    unsigned long mask[4] = {0, 0, 0, 0};
+    mask[node / 64] |= 1ul << (node % 64);
+    constexpr int kMpolPreferred = 1;
+    syscall(SYS_mbind, p, bytes, kMpolPreferred, mask, 256ul, 0u);
+}
 
 template <typename F>
 void parallel_for(uint64_t n, F&& f) {  // f(i) over [0, n) on up to 16 threads; first error rethrown
@@ -389,6 +423,7 @@ bool DStore::build_staged_image(uint32_t mode) {
     for (uint64_t q = 0; q < nch; ++q) bound += align_up(rec_len_[q] + 4 * m.rows_in_chunk(q) + 64, kAlign);
     void* map = mmap(nullptr, bound, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
     if (map == MAP_FAILED) throw Error(kIo, "staging image: mmap of " + std::to_string(bound) + " bytes failed");
+    if (staging_ == kStreamPinned) prefer_gpu_node(map, bound, device_);
     uint8_t* img = static_cast<uint8_t*>(map);
     std::vector<uint64_t> off(nch), len(nch), elen(nch);
     std::vector<uint8_t> kind(nch);
