@@ -2206,6 +2206,86 @@ __global__ void __launch_bounds__(64)
     if (tid == 0) bulk_wait0();
 }
 
+// K4o by groups of consecutive output rows (A/B: RFL_OH=rows4): a 128-thread CTA
+// builds R consecutive rows (R x row bytes <= 16 KB: the write-only TMA ceiling
+// reaches ~6.06 TB/s from 16 KB tiles vs 5.37 from 4 KB ones,
+// profiles/r2/s3/mix_bw_writeonly.jsonl) in one of two shared stages, the next
+// group's code words loaded into registers first, one bulk store per group.
+template <int OUT>
+__global__ void __launch_bounds__(128)
+    k_onehot_gather_rowsR(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t R,
+                          uint8_t* __restrict__ out, uint64_t* __restrict__ out_gidx) {
+    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : 2;
+    constexpr uint32_t kMaxW = 8;  // code words per thread per group (R x wpr <= 1,024)
+    extern __shared__ __align__(128) uint8_t ohg_smem[];
+    pdl_wait();
+    pdl_trigger();
+    const uint64_t L = a.n_var / 4, wpr = L / 16;
+    const uint64_t row_bytes = a.n_var * kEs;
+    const uint32_t tid = threadIdx.x;
+    const uint64_t n_groups = (n_rows + R - 1) / R;
+    auto load = [&](uint64_t t, uint32_t (&w)[kMaxW]) {
+        const uint64_t r0 = t * R;
+        const uint32_t rows = static_cast<uint32_t>(umin64(R, n_rows - r0));
+        const uint64_t words = rows * wpr;
+#pragma unroll
+        for (uint32_t k = 0; k < kMaxW; ++k) {
+            const uint64_t i = tid + 128ull * k;
+            if (i < words) {
+                const uint64_t rr = i / wpr, wi = i - rr * wpr;
+                const RowRef rf = refs[r0 + rr];  // (L1-resident: R refs per group)
+                w[k] = ld_u32(a.base + (rf.rec_off & ((1ull << 60) - 1)) + (rf.gidx % a.chunk_rows) * (L / 4) + 4 * wi);
+            }
+        }
+        if (tid < rows && out_gidx) out_gidx[r0 + tid] = refs[r0 + tid].gidx;
+    };
+    uint32_t cur[kMaxW], nxt[kMaxW];
+    uint64_t t = blockIdx.x;
+    if (t < n_groups) load(t, cur);
+    for (uint32_t it = 0; t < n_groups; t += gridDim.x, ++it) {
+        if (t + gridDim.x < n_groups) load(t + gridDim.x, nxt);
+        const uint64_t r0 = t * R;
+        const uint32_t rows = static_cast<uint32_t>(umin64(R, n_rows - r0));
+        uint8_t* stage = ohg_smem + (it & 1u) * (R * row_bytes);
+        if (tid == 0) bulk_wait_read1();
+        __syncthreads();
+#pragma unroll
+        for (uint32_t k = 0; k < kMaxW; ++k) {
+            const uint64_t i = tid + 128ull * k;
+            if (i >= rows * wpr) break;
+            const uint64_t rr = i / wpr, wi = i - rr * wpr;
+            uint8_t* rowp = stage + rr * row_bytes;
+#pragma unroll
+            for (uint32_t c = 0; c < 4; ++c) {
+                const uint32_t m = onehot_mask16(cur[k], c);
+                uint8_t* p = rowp + (c * L + 16 * wi) * kEs;
+                if (OUT == kOhU8) {
+                    uint32_t o[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                } else {
+                    uint32_t o[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
+                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<uint4*>(p + 16) = make_uint4(o[4], o[5], o[6], o[7]);
+                }
+            }
+        }
+        fence_proxy_async_shared();
+        __syncthreads();
+        if (tid == 0) {
+            bulk_store(out + r0 * row_bytes, stage, static_cast<uint32_t>(rows * row_bytes));
+            bulk_commit();
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kMaxW; ++k) cur[k] = nxt[k];
+    }
+    if (tid == 0) bulk_wait0();
+}
+
 // ======================================================== staging pull ===
 // Host -> HBM staging of a group's fetched blocks by TMA instead of one copy-engine
 // transfer per block: each copy engine transfer pays a fixed ~4.7 us setup
@@ -2804,8 +2884,37 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         if (e && std::string(e) == "bulk") return 1;
         if (e && std::string(e) == "tile") return 0;
         if (e && std::string(e) == "plain") return 2;
+        if (e && std::string(e) == "rows4") return 4;
         return 3;
     }();
+    if (variant == 4 && od != OutDtype::f32) {
+        const uint64_t rb = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
+        const uint32_t R = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(64, (16u << 10) / rb)));
+        if (R * (a.n_var / 64) <= 128 * 8) {
+            const size_t smem = 2ull * R * rb;
+            auto kern = od == OutDtype::bf16 ? k_onehot_gather_rowsR<kOhBf16> : k_onehot_gather_rowsR<kOhU8>;
+            int oc = 0;
+            {
+                static std::mutex mu;
+                static size_t set_to[2] = {0, 0};
+                static int occ[2] = {0, 0};
+                const int ki = od == OutDtype::bf16 ? 1 : 0;
+                std::lock_guard<std::mutex> lk(mu);
+                if (set_to[ki] != smem) {
+                    set_smem(kern, std::max<size_t>(smem, set_to[ki]));
+                    set_to[ki] = std::max<size_t>(smem, set_to[ki]);
+                    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, 128, smem), "occupancy");
+                }
+                oc = occ[ki];
+            }
+            const uint64_t groups = (n + R - 1) / R;
+            const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
+                1, std::min<uint64_t>(groups, static_cast<uint64_t>(std::max(oc, 1)) * device_sm_count())));
+            launch_k(kern, dim3(g), dim3(128), smem, st, "k_onehot_gather_rowsR launch", dev_view(a), refs, n, R,
+                     static_cast<uint8_t*>(out), out_gidx);
+            return;
+        }
+    }
     if (variant == 3 && od != OutDtype::f32 && a.n_var <= 32768) {
         const uint64_t rb = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
         const size_t smem = 2 * rb;
