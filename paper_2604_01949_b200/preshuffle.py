@@ -227,6 +227,7 @@ def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group, a2a=None) -
     ptr, changed = L.vp(), C.c_int()
     handle = (C.c_ubyte * 64)()
     cap, hv = 0, []
+    seen_vers = None  # receive-buffer versions of the last round (IPC opens are agreed when they change)
     try:
         if mode == "ipc":  # a first receive buffer, so every round's gather carries a valid handle
             L.check(lib.rfl_pshuf_recv_buffer(h, 16, C.byref(ptr), handle, C.byref(changed)))
@@ -249,17 +250,33 @@ def _run_ranks(arr, n_in, out_path, cfg, device, rank, world, group, a2a=None) -
                         hv = np.frombuffer(bytes(handle), np.int64).tolist()
                     infos = np.concatenate([infos[:, :world + 1],
                                             _all_gather_i64([version] + hv, world, group)], axis=1)
+                opened, err = False, None
                 for p in range(world):
                     if p == rank:
                         continue
                     ver = int(infos[p, world + 1])
                     if p not in peers or peers[p][0] != ver:
-                        if p in peers:
-                            L.check(lib.rfl_ipc_close(peers[p][1], device))
-                        hb = infos[p, world + 2:].astype(np.int64).tobytes()
-                        pp = L.vp()
-                        L.check(lib.rfl_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), device, C.byref(pp)))
-                        peers[p] = (ver, pp.value)
+                        opened = True
+                        try:
+                            if p in peers:
+                                L.check(lib.rfl_ipc_close(peers[p][1], device))
+                                del peers[p]
+                            hb = infos[p, world + 2:].astype(np.int64).tobytes()
+                            pp = L.vp()
+                            L.check(lib.rfl_ipc_open((C.c_ubyte * 64).from_buffer_copy(hb), device, C.byref(pp)))
+                            peers[p] = (ver, pp.value)
+                        except L.RiffleError as e:  # (agreed below: no rank may run ahead into the exchange)
+                            err = e
+                            break
+                # (decided from the gathered versions, identically on every rank)
+                vers = [int(infos[p, world + 1]) for p in range(world)]
+                if vers != seen_vers:
+                    seen_vers = vers
+                    ok = _all_gather_i64([0 if err is not None else 1, 1 if opened else 0], world, group)
+                    if ok[:, 0].min() == 0:
+                        raise L.CudaError(f"pre-shuffle round {r}: opening a peer receive buffer (CUDA IPC) failed on "
+                                          f"rank(s) {[int(q) for q in np.nonzero(ok[:, 0] == 0)[0]]}"
+                                          + (f": {err}" if err is not None else "") + "; RFL_A2A=nccl avoids peer mappings")
                 dst = (L.vp * world)()
                 for d in range(world):
                     base = ptr.value if d == rank else peers[d][1]
