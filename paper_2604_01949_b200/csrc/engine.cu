@@ -1305,7 +1305,7 @@ bool GpuLoader::assemble_group() {
         launch_dense_gather(av, s.d_refs, n, dev_.out_dtype, s.data, static_cast<uint64_t*>(s.gidx), compute_);
     } else if (dev_.output == 1 && fused_) {
         launch_csr_densify_d8(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,
-                              static_cast<uint64_t*>(s.gidx), compute_, ds_->d8_bases() && direct_);
+                              static_cast<uint64_t*>(s.gidx), compute_);
     } else if (dev_.output == 1) {
         launch_csr_densify(av, s.d_refs, n, dev_.out_dtype, dev_.normalize, dev_.target_sum, s.data,
                            static_cast<uint64_t*>(s.gidx), compute_, n ? (nnz + n - 1) / n : 0);

@@ -69,7 +69,6 @@ struct StagePlan {
     uint64_t n_esc = 0, bytes = 0, exp = 0;
     uint64_t pbytes = 0;    // packed delta bits, bytes (kD8Packed)
     uint64_t pbytes_v = 0;  // packed value bits, bytes (kD8IntP)
-    uint64_t gbase_at = 0;  // > 0: group bases written at this record offset (resident_coded image)
 };
 StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat = true,
                          bool pack_deltas = false);
@@ -156,7 +155,6 @@ public:
     // every staged record is a delta record with 4-byte values and every row has <=
     // kD8FusedMaxNnz entries: dense output can densify the staged records directly
     bool d8_fused() const { return d8_fused_; }
-    bool d8_bases() const { return d8_bases_; }  // delta records carry group bases (resident_coded)
     const std::vector<uint64_t>& exp_len() const { return exp_len_; }
     uint64_t image_bytes() const { return image_bytes_; }
     uint64_t staged_bytes() const { return staged_bytes_; }  // staging image (0: verbatim)
@@ -204,7 +202,7 @@ private:
     int device_;
     uint32_t staging_;
     std::vector<uint64_t> rec_off_, rec_len_, slot_len_, slot_off_, img_off_, img_len_;
-    bool idx16_ = false, d8_ = false, d8_fused_ = false, d8_bases_ = false;
+    bool idx16_ = false, d8_ = false, d8_fused_ = false;
     std::vector<uint64_t> exp_len_;
     std::vector<uint8_t> d8_rec_;
     std::vector<uint32_t> row_nnz_;

@@ -943,8 +943,6 @@ struct D8RowDesc {
     const uint8_t* delta;  // column deltas u8 (record entry 0); packed: the group widths
     const uint8_t* pskip;  // packed: bit offset of every 32nd group
     const uint8_t* pbits;  // packed: the delta bit stream
-    const uint8_t* gcol;   // group bases (resident_coded image): column of every 16th entry, or null
-    const uint8_t* gesc;   // ... and escapes before it (top-byte-coded records)
     const uint8_t* low;    // kD8Raw: raw 4-B values; coded: low value bytes
     const uint8_t* codes;  // 2-bit top-byte codes
     const uint8_t* esc;    // escaped top bytes
@@ -953,7 +951,7 @@ struct D8RowDesc {
     uint32_t first, esc_at, dict, kind, packed;  // kind without the kD8Packed flag
 };
 
-__device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef& r, int bases = 0) {
+__device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef& r) {
     D8RowDesc d;
     const uint8_t* rec = a.base + (r.rec_off & kOffMask);
     d.kind = static_cast<uint32_t>(r.rec_off >> kKindShift);
@@ -979,7 +977,6 @@ __device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef
         d.pskip = rec + P.skip;
         d.pbits = rec + P.bits;
     }
-    d.gcol = d.gesc = nullptr;
     if (d.kind == kD8IntP) {  // packed value bytes: codes = widths, esc = skip, low = bits
         const uint64_t vo = d8_values_offset(rows, nnz, dsec);
         const D8Packed V = d8_packed_at(vo, nnz, ld_u32(rec + vo));
@@ -1001,20 +998,11 @@ __device__ __forceinline__ D8RowDesc describe_d8(const ArenaDev& a, const RowRef
         d.esc_at = ld_u32(rec + L.esc_base + 4 * within);
         d.dict = ld_u32(rec + L.dict);
     }
-    if (bases && !d.packed && d.kind != kD8IntP) {
-        uint64_t rb;
-        if (d.kind == kD8Raw) rb = d8_record_bytes(rows, nnz, 4);
-        else if (d.kind == kD8Int8) rb = d8_record_bytes(rows, nnz, 1);
-        else rb = d8v_layout(rows, nnz, ld_u32(rec + d8v_layout(rows, nnz, 0).n_esc), d.kind == kD8Coded16 ? 1 : 3).bytes;
-        d.gcol = rec + d8_bases_at(rb);
-        if (d.kind == kD8Coded || d.kind == kD8Coded16) d.gesc = d.gcol + ((2 * ((nnz + 15) / 16) + 3) & ~3ull);
-    }
     return d;
 }
 
 struct D8Raw16 {  // one thread's 16 entries of a row, as loaded
     uint32_t d[4], cw, lw[16], vm;
-    uint32_t gcol, gesc;  // group bases of the thread's group (when the record has them)
 };
 
 __device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw16& x) {
@@ -1029,10 +1017,6 @@ __device__ __forceinline__ void load_d8(const D8RowDesc& r, uint32_t tid, D8Raw1
     for (int q = 0; q < 16; ++q) x.lw[q] = 0u;
     if (!x.vm) return;
     const uint32_t kind = r.kind;
-    if (r.gcol) {  // (k0 is a multiple of 16: the thread's group)
-        x.gcol = __ldg(reinterpret_cast<const unsigned short*>(r.gcol) + (k0 >> 4));
-        x.gesc = r.gesc ? ld_u32(r.gesc + 4 * (k0 >> 4)) : 0u;
-    }
     if (r.packed) {
         uint32_t w;
         const uint32_t off = packed_group(r.delta, r.pskip, k0 >> 4, w);
@@ -1115,36 +1099,18 @@ __device__ __forceinline__ void decode_d8(const D8RowDesc& r, const D8Raw16& x, 
         for (uint32_t j = 0; j < 16; ++j) em |= (((x.cw >> (2 * j)) & 3u) == 3u ? 1u : 0u) << j;
         em &= x.vm;
     }
-    uint32_t cb, eb;
-    if (r.gcol) {
-        // group bases: the thread's first valid entry is the row's first (the row starts in
-        // this group: column `first`, delta 0) or the group's first entry (its column is
-        // gcol; its own delta is already counted in pre[]) -- no block scan
-        const uint64_t k0 = (r.lo & ~15u) + 16ull * tid;
-        if (r.lo >= k0) {
-            cb = r.first;
-            eb = r.esc_at;
-        } else {
-            cb = x.gcol - (x.d[0] & 255u);
-            eb = x.gesc;
-        }
-        (void)lane;
-        (void)warp;
-        (void)s_scan;
-    } else {
-        const uint32_t mine = sum | (static_cast<uint32_t>(__popc(em)) << 17);
-        uint32_t incl = mine;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= static_cast<uint32_t>(o)) incl += t;
-        }
-        if (lane == 31) s_scan[warp] = incl;
-        __syncthreads();
-        uint32_t excl = incl - mine;
-        for (uint32_t w = 0; w < warp; ++w) excl += s_scan[w];
-        cb = r.first + (excl & 0x1ffffu);
-        eb = r.esc_at + (excl >> 17);
+    const uint32_t mine = sum | (static_cast<uint32_t>(__popc(em)) << 17);
+    uint32_t incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += t;
     }
+    if (lane == 31) s_scan[warp] = incl;
+    __syncthreads();
+    uint32_t excl = incl - mine;
+    for (uint32_t w = 0; w < warp; ++w) excl += s_scan[w];
+    const uint32_t cb = r.first + (excl & 0x1ffffu);
+    uint32_t eb = r.esc_at + (excl >> 17);
 #pragma unroll
     for (uint32_t j = 0; j < 16; ++j) {
         col[j] = (x.vm >> j) & 1u ? cb + pre[j] : ~0u;
@@ -1174,7 +1140,7 @@ __device__ __forceinline__ void decode_d8(const D8RowDesc& r, const D8Raw16& x, 
 template <typename SrcT, typename DstT, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_csr_densify_d8(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t tile_cols, int norm,
-                     float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk, int bases) {
+                     float target, DstT* __restrict__ out, uint64_t* __restrict__ out_gidx, int bulk) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ double s_red[THREADS / 32];
     __shared__ uint32_t s_scan[THREADS / 32];
@@ -1188,7 +1154,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (tid < 32) {
             const uint64_t row = blockIdx.x + (k0 + tid) * g;
             if (row < n_rows) {
-                const D8RowDesc rd = describe_d8(a, refs[row], bases);
+                const D8RowDesc rd = describe_d8(a, refs[row]);
                 s_desc[tid] = rd;
                 if (out_gidx) out_gidx[row] = rd.gidx;
             }
@@ -2758,7 +2724,7 @@ void launch_csr_densify(const ArenaView& a, const RowRef* refs, uint64_t n, OutD
 namespace {
 template <typename SrcT, typename DstT>
 void densify_d8_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm, float target, void* out,
-                  uint64_t* out_gidx, cudaStream_t st, bool bases) {
+                  uint64_t* out_gidx, cudaStream_t st) {
     // shape rule: rows wider than 48 KB -> two alternating 40 KB tiles at 2 CTAs/SM (the next
     // tile is built while the previous bulk store drains; cfg2 116.8 -> 114.9 us per batch vs one
     // 80 KB tile, profiles/r2/s3/k3d_tiles.txt), else one 40 KB tile at 3
@@ -2778,23 +2744,22 @@ void densify_d8_t(const ArenaView& av, const RowRef* refs, uint64_t n, bool norm
     cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem), "occupancy");
     const uint64_t grid = std::min<uint64_t>(n, static_cast<uint64_t>(std::max(per_sm, 1)) * device_sm_count());
     launch_k(kern, dim3(static_cast<unsigned>(grid)), dim3(256), smem, st, "k_csr_densify_d8 launch", dev_view(av),
-             refs, n, static_cast<uint32_t>(tile_cols), norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk,
-             bases ? 1 : 0);
+             refs, n, static_cast<uint32_t>(tile_cols), norm ? 1 : 0, target, static_cast<DstT*>(out), out_gidx, bulk);
 }
 }  // namespace
 
 void launch_csr_densify_d8(const ArenaView& a, const RowRef* refs, uint64_t n, OutDtype od, bool norm, float target,
-                           void* out, uint64_t* out_gidx, cudaStream_t st, bool bases) {
+                           void* out, uint64_t* out_gidx, cudaStream_t st) {
     if (a.layout != Layout::csr) invalid("csr_densify_d8: store is not csr");
     if (n == 0) return;
     if (a.vdt == VDtype::f32) {
-        if (od == OutDtype::bf16) return densify_d8_t<float, __nv_bfloat16>(a, refs, n, norm, target, out, out_gidx, st, bases);
-        return densify_d8_t<float, float>(a, refs, n, norm, target, out, out_gidx, st, bases);
+        if (od == OutDtype::bf16) return densify_d8_t<float, __nv_bfloat16>(a, refs, n, norm, target, out, out_gidx, st);
+        return densify_d8_t<float, float>(a, refs, n, norm, target, out, out_gidx, st);
     }
     if (a.vdt == VDtype::i32) {
-        if (od == OutDtype::bf16) return densify_d8_t<int32_t, __nv_bfloat16>(a, refs, n, norm, target, out, out_gidx, st, bases);
-        if (od == OutDtype::f32) return densify_d8_t<int32_t, float>(a, refs, n, norm, target, out, out_gidx, st, bases);
-        return densify_d8_t<int32_t, int32_t>(a, refs, n, false, target, out, out_gidx, st, bases);
+        if (od == OutDtype::bf16) return densify_d8_t<int32_t, __nv_bfloat16>(a, refs, n, norm, target, out, out_gidx, st);
+        if (od == OutDtype::f32) return densify_d8_t<int32_t, float>(a, refs, n, norm, target, out, out_gidx, st);
+        return densify_d8_t<int32_t, int32_t>(a, refs, n, false, target, out, out_gidx, st);
     }
     invalid("csr_densify_d8: delta records carry 4-byte values (f32 / i32)");
 }

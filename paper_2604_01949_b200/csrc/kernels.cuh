@@ -71,7 +71,7 @@ RFL_HD inline uint64_t d8_values_offset(uint64_t rows, uint64_t nnz, uint64_t ds
     const uint64_t head = kCsrHeaderBytes + 4 * (rows + 1);
     return (head + ((2 * rows + 3) & ~3ull) + (dsec == ~0ull ? nnz : dsec) + 7) & ~7ull;
 }
-RFL_HD inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs, uint64_t dsec = ~0ull) {
+inline uint64_t d8_record_bytes(uint64_t rows, uint64_t nnz, uint64_t vs, uint64_t dsec = ~0ull) {
     return d8_values_offset(rows, nnz, dsec) + vs * nnz;
 }
 // Bit-packed column deltas (the pinned staging image; kind | kD8Packed): the delta
@@ -100,15 +100,6 @@ RFL_HD inline D8Packed d8_packed_layout(uint64_t rows, uint64_t nnz, uint64_t pa
 RFL_HD inline uint64_t d8_packed_section(uint64_t rows, uint64_t nnz, uint64_t packed_bytes) {
     const D8Packed d = d8_packed_layout(rows, nnz, packed_bytes);
     return d.end - d.pbytes_at;
-}
-// Group bases (the HBM-resident coded image): after a delta record's own bytes, at
-// d8_bases_at(its length), the column of every 16th record entry (u16 per group,
-// padded to 4 B) and, for top-byte-coded records, the escapes before it (u32 per
-// group) -- K3d then places a thread's 16 entries with no block scan.
-RFL_HD inline uint64_t d8_bases_at(uint64_t rec_bytes) { return (rec_bytes + 3) & ~3ull; }
-RFL_HD inline uint64_t d8_bases_bytes(uint64_t nnz, bool coded) {
-    const uint64_t groups = (nnz + 15) / 16;
-    return ((2 * groups + 3) & ~3ull) + (coded ? 4 * groups : 0);
 }
 // Delta records with 4-byte values may also code each value's top byte (sign +
 // high exponent bits, a handful of distinct values per record) against a
@@ -208,9 +199,8 @@ size_t dense_out_elem_size(const ArenaView& a, OutDtype od);
 // (D8Kind << kRowKindShift); every row must have <= kD8FusedMaxNnz entries.
 constexpr unsigned kRowKindShift = 60;
 constexpr uint64_t kD8FusedMaxNnz = 16 * 256 - 15;
-// bases: the records carry group bases (resident_coded image): decode without a block scan
 void launch_csr_densify_d8(const ArenaView& a, const RowRef* refs, uint64_t n_rows, OutDtype od, bool normalize,
-                           float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st, bool bases = false);
+                           float target_sum, void* out, uint64_t* out_gidx, cudaStream_t st);
 
 // Staging pull: copy jobs (16-B aligned host-mapped src, 16-B aligned device dst,
 // bytes a multiple of 16) moved by TMA bulk loads/stores from a small grid, on

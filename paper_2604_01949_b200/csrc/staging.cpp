@@ -162,30 +162,6 @@ uint64_t packed_bits_bytes(const std::vector<uint8_t>& d) {
 
 StagePlan plan_csr_stage_u8(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat);
 
-// group bases of a staged delta record (d8_bases_at): the column of record entries
-// 0, 16, 32, ... and, top-byte-coded, the escapes before each
-void write_group_bases(const uint8_t* src, const StagePlan& p, uint8_t* dst) {
-    const uint64_t rows = rd32(src), nnz = rd64(src + 4);
-    const uint8_t* ix = src + kCsrHeaderBytes + 4 * (rows + 1);
-    const uint8_t* val = ix + 4 * nnz;
-    const bool coded = p.kind == kD8Coded || p.kind == kD8Coded16;
-    const uint64_t groups = (nnz + 15) / 16;
-    uint8_t* cb = dst + p.gbase_at;
-    uint8_t* eb = cb + ((2 * groups + 3) & ~3ull);
-    uint32_t esc = 0;
-    for (uint64_t k = 0; k < nnz; ++k) {
-        if (k % 16 == 0) {
-            const uint16_t c = static_cast<uint16_t>(rd32(ix + 4 * k));
-            std::memcpy(cb + 2 * (k / 16), &c, 2);
-            if (coded) std::memcpy(eb + 4 * (k / 16), &esc, 4);
-        }
-        if (coded) {
-            const uint8_t top = val[4 * k + 3];
-            esc += top != p.dict[0] && top != p.dict[1] && top != p.dict[2];
-        }
-    }
-}
-
 StagePlan plan_csr_stage(const uint8_t* rec, uint64_t vs, bool allow_delta, bool code_values, bool vfloat,
                          bool pack_deltas) {
     StagePlan p = plan_csr_stage_u8(rec, vs, allow_delta, code_values, vfloat);
@@ -441,9 +417,6 @@ bool DStore::build_staged_image(uint32_t mode) {
     // the HBM-resident coded image keeps u8 deltas (K3d there is bound by its dense writes)
     const char* pe = std::getenv("RFL_PACK_DELTAS");
     const bool pack = staging_ == kStreamPinned && !(pe && pe[0] == '0');
-    // group bases for the HBM-resident image's K3d (RFL_GROUP_BASES=0 for A/B)
-    const char* ge = std::getenv("RFL_GROUP_BASES");
-    const bool bases = staging_ == kResidentCoded && mode == kStageDelta && !(ge && ge[0] == '0');
     // virtual reservation bounding every encoding (each kind is at most the
     // verbatim record + 2 B per row + padding), committed page by page as filled
     uint64_t bound = kPad + 4096;
@@ -482,12 +455,6 @@ bool DStore::build_staged_image(uint32_t mode) {
                     plans[k].exp = rec_len_[q];
                 } else {
                     plans[k] = plan_csr_stage(rec, vs, mode == kStageDelta, code_values, m.value_dtype != VDtype::i32, pack);
-                    const uint32_t kd = plans[k].kind;
-                    if (bases && (kd == kD8Raw || kd == kD8Coded || kd == kD8Coded16 || kd == kD8Int8)) {
-                        plans[k].gbase_at = d8_bases_at(plans[k].bytes);
-                        plans[k].bytes = plans[k].gbase_at +
-                                         d8_bases_bytes(rd64(rec + 4), kd == kD8Coded || kd == kD8Coded16);
-                    }
                 }
             });
             if (!one_hot_ok) {  // not a one-hot store: the verbatim image
@@ -508,7 +475,6 @@ bool DStore::build_staged_image(uint32_t mode) {
                 const uint8_t* rec = win.data() + wpos[k];
                 if (mode == kStageOneHot) encode_one_hot(rec, m.rows_in_chunk(q), m.n_var, img + off[q]);
                 else encode_csr_stage(rec, vs, plans[k], img + off[q]);
-                if (plans[k].gbase_at) write_group_bases(rec, plans[k], img + off[q]);
                 const uint64_t gap = (q + 1 < nch ? align_up(off[q] + len[q], kAlign) : off[q] + len[q] + kPad) -
                                      (off[q] + len[q]);
                 std::memset(img + off[q] + len[q], 0, gap);
@@ -559,7 +525,6 @@ bool DStore::build_staged_image(uint32_t mode) {
     } else {
         idx16_ = mode != kStageOneHot;
         d8_ = true;
-        d8_bases_ = bases;
     }
     return true;
 }
