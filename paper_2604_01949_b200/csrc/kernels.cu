@@ -1924,148 +1924,6 @@ __global__ void __launch_bounds__(kOhThreads)
 }
 
 
-// K4o through shared memory: the warp builds its unit's output (32 x kOhU code
-// words = 512 x kOhU positions of each of the 4 planes) in one of two shared
-// slices and one lane writes it with 1-D TMA bulk stores (one per plane segment,
-// one for the whole row when the unit is the row); the other slice is filled
-// while that store drains.  A/B: RFL_OH=bulk.
-template <int OUT, int kOhU = 2, int kOhWarps = 4>
-__global__ void __launch_bounds__(kOhWarps * 32)
-    k_onehot_gather_bulk(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint8_t* __restrict__ out,
-                         uint64_t* __restrict__ out_gidx) {
-    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : 2;
-    constexpr uint32_t kSeg = 32 * kOhU * 16 * kEs;  // bytes of one plane's segment of a unit
-    extern __shared__ __align__(128) uint8_t oh_smem[];
-    pdl_wait();
-    pdl_trigger();
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    uint8_t* slices = oh_smem + warp * 2 * 4 * kSeg;
-    const uint64_t L = a.n_var / 4, wpr = L / 16;
-    const uint64_t upr = (wpr + 32 * kOhU - 1) / (32 * kOhU);
-    const uint64_t n_units = n_rows * upr;
-    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * kOhWarps;
-    uint32_t it = 0;
-    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * kOhWarps + warp; u < n_units; u += warps, ++it) {
-        const uint64_t row = u / upr, part = u - row * upr;
-        uint64_t off = 0, g = 0;
-        if (lane == 0) {
-            const RowRef r = refs[row];
-            off = (r.rec_off & ((1ull << 60) - 1)) + (r.gidx % a.chunk_rows) * (L / 4);
-            g = r.gidx;
-        }
-        off = __shfl_sync(kFull, off, 0);
-        if (part == 0 && lane == 0 && out_gidx) out_gidx[row] = g;
-        const uint64_t wb = part * 32 * kOhU, nw = umin64(32 * kOhU, wpr - wb);  // words of this unit
-        uint32_t w[kOhU];
-#pragma unroll
-        for (int k = 0; k < kOhU; ++k)
-            if (k * 32 + lane < nw) w[k] = ld_u32(a.base + off + 4 * (wb + k * 32 + lane));
-        uint8_t* sl = slices + (it & 1u) * 4 * kSeg;
-        if (lane == 0) bulk_wait_read1();  // this slice's store (two units ago) has been read
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < kOhU; ++k) {
-            const uint32_t wi = k * 32 + lane;
-            if (wi >= nw) break;
-#pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
-                const uint32_t m = onehot_mask16(w[k], c);
-                uint8_t* p = sl + c * kSeg + wi * 16 * kEs;
-                if (OUT == kOhU8) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
-                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
-                } else {
-                    uint32_t o[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
-                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
-                    *reinterpret_cast<uint4*>(p + 16) = make_uint4(o[4], o[5], o[6], o[7]);
-                }
-            }
-        }
-        fence_proxy_async_shared();
-        __syncwarp();
-        if (lane == 0) {
-            uint8_t* dst = out + row * a.n_var * kEs;
-            const uint32_t seg = static_cast<uint32_t>(nw * 16 * kEs);
-            if (upr == 1 && seg == kSeg) {
-                bulk_store(dst, sl, 4 * kSeg);  // the whole row: the 4 plane segments are adjacent
-            } else {
-                for (uint32_t c = 0; c < 4; ++c) bulk_store(dst + (c * L + wb * 16) * kEs, sl + c * kSeg, seg);
-            }
-            bulk_commit();
-        }
-    }
-    if (lane == 0) bulk_wait0();
-}
-
-// K4o, tiled (A/B: RFL_OH=tile; 763 vs 922 M rows/s for the plain kernel on cfg4,
-// profiles/r2/s3/README.md): a CTA builds R consecutive output rows (a contiguous
-// R x row-bytes range of the batch, <= 32 KB) in one of two shared tiles and one
-// thread writes the tile with a single 1-D TMA bulk store -- the large-tile store
-// path that reaches ~5.8 TB/s for write-heavy mixes (profiles/r2/mix_bw_b.jsonl);
-// the next tile's codes are loaded and its rows built while that store drains.
-template <int OUT>
-__global__ void __launch_bounds__(256)
-    k_onehot_gather_tile(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t R,
-                         uint8_t* __restrict__ out, uint64_t* __restrict__ out_gidx) {
-    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : 2;
-    extern __shared__ __align__(128) uint8_t oh_tiles[];
-    __shared__ uint64_t s_off[64];
-    pdl_wait();
-    pdl_trigger();
-    const uint64_t L = a.n_var / 4, wpr = L / 16;          // code words per row
-    const uint64_t row_bytes = a.n_var * kEs;
-    const uint32_t tile_bytes = static_cast<uint32_t>(R * row_bytes);
-    const uint64_t n_tiles = (n_rows + R - 1) / R;
-    uint32_t it = 0;
-    for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
-        const uint64_t r0 = t * R;
-        const uint32_t rows = static_cast<uint32_t>(umin64(R, n_rows - r0));
-        if (threadIdx.x < rows) {
-            const RowRef r = refs[r0 + threadIdx.x];
-            s_off[threadIdx.x] = (r.rec_off & ((1ull << 60) - 1)) + (r.gidx % a.chunk_rows) * (L / 4);
-            if (out_gidx) out_gidx[r0 + threadIdx.x] = r.gidx;
-        }
-        uint8_t* tile = oh_tiles + (it & 1u) * tile_bytes;
-        if (threadIdx.x == 0) bulk_wait_read1();  // this tile's store (two tiles ago) has read it
-        __syncthreads();
-        const uint32_t words = rows * static_cast<uint32_t>(wpr);
-        for (uint32_t k = threadIdx.x; k < words; k += 256) {
-            const uint32_t rr = k / static_cast<uint32_t>(wpr), wi = k - rr * static_cast<uint32_t>(wpr);
-            const uint32_t w = ld_u32(a.base + s_off[rr] + 4ull * wi);
-            uint8_t* rowp = tile + rr * row_bytes;
-#pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
-                const uint32_t m = onehot_mask16(w, c);
-                uint8_t* p = rowp + (c * L + 16ull * wi) * kEs;
-                if (OUT == kOhU8) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
-                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
-                } else {
-                    uint32_t o[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
-                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
-                    *reinterpret_cast<uint4*>(p + 16) = make_uint4(o[4], o[5], o[6], o[7]);
-                }
-            }
-        }
-        fence_proxy_async_shared();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            bulk_store(out + r0 * row_bytes, tile, static_cast<uint32_t>(rows * row_bytes));
-            bulk_commit();
-        }
-    }
-    if (threadIdx.x == 0) bulk_wait0();
-}
 
 // K4 by whole rows through TMA (the grouped launches; RFL_DG=row forces it): each CTA streams rows through
 // 2 shared stages -- one 1-D bulk load of the row (mbarrier completion), the
@@ -2206,85 +2064,6 @@ __global__ void __launch_bounds__(64)
     if (tid == 0) bulk_wait0();
 }
 
-// K4o by groups of consecutive output rows (A/B: RFL_OH=rows4): a 128-thread CTA
-// builds R consecutive rows (R x row bytes <= 16 KB: the write-only TMA ceiling
-// reaches ~6.06 TB/s from 16 KB tiles vs 5.37 from 4 KB ones,
-// profiles/r2/s3/mix_bw_writeonly.jsonl) in one of two shared stages, the next
-// group's code words loaded into registers first, one bulk store per group.
-template <int OUT>
-__global__ void __launch_bounds__(128)
-    k_onehot_gather_rowsR(ArenaDev a, const RowRef* __restrict__ refs, uint64_t n_rows, uint32_t R,
-                          uint8_t* __restrict__ out, uint64_t* __restrict__ out_gidx) {
-    constexpr uint32_t kEs = OUT == kOhU8 ? 1 : 2;
-    constexpr uint32_t kMaxW = 8;  // code words per thread per group (R x wpr <= 1,024)
-    extern __shared__ __align__(128) uint8_t ohg_smem[];
-    pdl_wait();
-    pdl_trigger();
-    const uint64_t L = a.n_var / 4, wpr = L / 16;
-    const uint64_t row_bytes = a.n_var * kEs;
-    const uint32_t tid = threadIdx.x;
-    const uint64_t n_groups = (n_rows + R - 1) / R;
-    auto load = [&](uint64_t t, uint32_t (&w)[kMaxW]) {
-        const uint64_t r0 = t * R;
-        const uint32_t rows = static_cast<uint32_t>(umin64(R, n_rows - r0));
-        const uint64_t words = rows * wpr;
-#pragma unroll
-        for (uint32_t k = 0; k < kMaxW; ++k) {
-            const uint64_t i = tid + 128ull * k;
-            if (i < words) {
-                const uint64_t rr = i / wpr, wi = i - rr * wpr;
-                const RowRef rf = refs[r0 + rr];  // (L1-resident: R refs per group)
-                w[k] = ld_u32(a.base + (rf.rec_off & ((1ull << 60) - 1)) + (rf.gidx % a.chunk_rows) * (L / 4) + 4 * wi);
-            }
-        }
-        if (tid < rows && out_gidx) out_gidx[r0 + tid] = refs[r0 + tid].gidx;
-    };
-    uint32_t cur[kMaxW], nxt[kMaxW];
-    uint64_t t = blockIdx.x;
-    if (t < n_groups) load(t, cur);
-    for (uint32_t it = 0; t < n_groups; t += gridDim.x, ++it) {
-        if (t + gridDim.x < n_groups) load(t + gridDim.x, nxt);
-        const uint64_t r0 = t * R;
-        const uint32_t rows = static_cast<uint32_t>(umin64(R, n_rows - r0));
-        uint8_t* stage = ohg_smem + (it & 1u) * (R * row_bytes);
-        if (tid == 0) bulk_wait_read1();
-        __syncthreads();
-#pragma unroll
-        for (uint32_t k = 0; k < kMaxW; ++k) {
-            const uint64_t i = tid + 128ull * k;
-            if (i >= rows * wpr) break;
-            const uint64_t rr = i / wpr, wi = i - rr * wpr;
-            uint8_t* rowp = stage + rr * row_bytes;
-#pragma unroll
-            for (uint32_t c = 0; c < 4; ++c) {
-                const uint32_t m = onehot_mask16(cur[k], c);
-                uint8_t* p = rowp + (c * L + 16 * wi) * kEs;
-                if (OUT == kOhU8) {
-                    uint32_t o[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) o[q] = (((m >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;
-                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
-                } else {
-                    uint32_t o[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        o[q] = ((m >> (2 * q)) & 1u) * 0x3F80u | ((m >> (2 * q + 1)) & 1u) * 0x3F800000u;
-                    *reinterpret_cast<uint4*>(p) = make_uint4(o[0], o[1], o[2], o[3]);
-                    *reinterpret_cast<uint4*>(p + 16) = make_uint4(o[4], o[5], o[6], o[7]);
-                }
-            }
-        }
-        fence_proxy_async_shared();
-        __syncthreads();
-        if (tid == 0) {
-            bulk_store(out + r0 * row_bytes, stage, static_cast<uint32_t>(rows * row_bytes));
-            bulk_commit();
-        }
-#pragma unroll
-        for (uint32_t k = 0; k < kMaxW; ++k) cur[k] = nxt[k];
-    }
-    if (tid == 0) bulk_wait0();
-}
 
 // ======================================================== staging pull ===
 // Host -> HBM staging of a group's fetched blocks by TMA instead of one copy-engine
@@ -2876,45 +2655,14 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
         std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 7) / 8, 8ull * device_sm_count())));
     const ArenaDev d = dev_view(a);
     auto* o = static_cast<uint8_t*>(out);
-    // RFL_OH=plain | tile | bulk (A/B); default: whole rows through two shared stages + one
-    // bulk store per row (cfg4 950-998 vs 936 M rows/s for plain 16-B stores,
-    // profiles/r2/s3/README.md)
-    static const int variant = [] {
+    // RFL_OH=plain (A/B): register 16-B stores; default: whole rows through two shared stages +
+    // one bulk store per row (cfg4 950-998 vs 936 M rows/s for plain stores; R-row shared tiles,
+    // per-warp bulk stores and 16 KB row groups measured slower, profiles/r2/s3/README.md)
+    static const bool plain = [] {
         const char* e = std::getenv("RFL_OH");
-        if (e && std::string(e) == "bulk") return 1;
-        if (e && std::string(e) == "tile") return 0;
-        if (e && std::string(e) == "plain") return 2;
-        if (e && std::string(e) == "rows4") return 4;
-        return 3;
+        return e && std::string(e) == "plain";
     }();
-    if (variant == 4 && od != OutDtype::f32) {
-        const uint64_t rb = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
-        const uint32_t R = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(64, (16u << 10) / rb)));
-        if (R * (a.n_var / 64) <= 128 * 8) {
-            const size_t smem = 2ull * R * rb;
-            auto kern = od == OutDtype::bf16 ? k_onehot_gather_rowsR<kOhBf16> : k_onehot_gather_rowsR<kOhU8>;
-            int oc = 0;
-            {
-                static std::mutex mu;
-                static size_t set_to[2] = {0, 0};
-                static int occ[2] = {0, 0};
-                const int ki = od == OutDtype::bf16 ? 1 : 0;
-                std::lock_guard<std::mutex> lk(mu);
-                if (set_to[ki] != smem) {
-                    set_smem(kern, std::max<size_t>(smem, set_to[ki]));
-                    set_to[ki] = std::max<size_t>(smem, set_to[ki]);
-                    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, 128, smem), "occupancy");
-                }
-                oc = occ[ki];
-            }
-            const uint64_t groups = (n + R - 1) / R;
-            const unsigned g = static_cast<unsigned>(std::max<uint64_t>(
-                1, std::min<uint64_t>(groups, static_cast<uint64_t>(std::max(oc, 1)) * device_sm_count())));
-            launch_k(kern, dim3(g), dim3(128), smem, st, "k_onehot_gather_rowsR launch", dev_view(a), refs, n, R,
-                     static_cast<uint8_t*>(out), out_gidx);
-            return;
-        }
-    }
+    const int variant = plain ? 2 : 3;
     if (variant == 3 && od != OutDtype::f32 && a.n_var <= 32768) {
         const uint64_t rb = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
         const size_t smem = 2 * rb;
@@ -2937,43 +2685,6 @@ void launch_onehot_gather(const ArenaView& a, const RowRef* refs, uint64_t n, Ou
             1, std::min<uint64_t>(n, static_cast<uint64_t>(std::max(oc, 1)) * device_sm_count())));
         launch_k(kern, dim3(g), dim3(64), smem, st, "k_onehot_gather_rows launch", dev_view(a), refs, n,
                  static_cast<uint8_t*>(out), out_gidx);
-        return;
-    }
-    const bool bulk = variant == 1;
-    const uint64_t row_bytes = a.n_var * (od == OutDtype::bf16 ? 2 : 1);
-    if (variant == 0 && od != OutDtype::f32 && row_bytes <= (32u << 10)) {
-        const uint32_t R = static_cast<uint32_t>(std::min<uint64_t>(64, (32u << 10) / row_bytes));
-        const size_t smem = 2ull * R * row_bytes;
-        auto kern = od == OutDtype::bf16 ? k_onehot_gather_tile<kOhBf16> : k_onehot_gather_tile<kOhU8>;
-        int oc = 0;
-        {
-            static std::mutex mu;
-            static int occ[2] = {0, 0};
-            static size_t set_for[2] = {0, 0};
-            const int ki = od == OutDtype::bf16 ? 1 : 0;
-            std::lock_guard<std::mutex> lk(mu);
-            if (set_for[ki] < smem) {
-                set_smem(kern, std::max<size_t>(smem, 64u << 10));
-                set_for[ki] = std::max<size_t>(smem, 64u << 10);
-                cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ki], kern, 256, smem), "occupancy");
-            }
-            oc = occ[ki];
-        }
-        const uint64_t n_tiles = (n + R - 1) / R;
-        const unsigned g = static_cast<unsigned>(
-            std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, static_cast<uint64_t>(std::max(oc, 1)) * device_sm_count())));
-        launch_k(kern, dim3(g), dim3(256), smem, st, "k_onehot_gather_tile launch", d, refs, n, R, o, out_gidx);
-        return;
-    }
-    if (bulk && od != OutDtype::f32) {
-        const uint32_t es = od == OutDtype::bf16 ? 2 : 1;
-        const size_t smem = 4 * 2 * 4 * (32 * 2 * 16 * es);  // 4 warps x 2 slices x 4 planes x segment
-        const unsigned g4 = static_cast<unsigned>(
-            std::max<uint64_t>(1, std::min<uint64_t>((warps_needed + 3) / 4, 16ull * device_sm_count())));
-        auto kern = od == OutDtype::bf16 ? k_onehot_gather_bulk<kOhBf16> : k_onehot_gather_bulk<kOhU8>;
-        static std::once_flag once[2];
-        std::call_once(once[es - 1], [&] { set_smem(kern, smem); });
-        launch_k(kern, dim3(g4), dim3(128), smem, st, "k_onehot_gather_bulk launch", d, refs, n, o, out_gidx);
         return;
     }
     if (od == OutDtype::bf16)
