@@ -675,14 +675,10 @@ BlockReader::BlockReader(std::shared_ptr<DStore> ds, std::vector<uint64_t> order
     ev_.resize(slots);
     released_.assign(slots, ~0ull);
     DeviceGuard g(ds_->device());
-    pull_ok_ = true;
     for (uint32_t i = 0; i < slots; ++i) {
         slots_[i].buf = ds_->take_pinned(bytes);
         cuda_ok(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
-        void* dp = nullptr;
-        pull_ok_ = pull_ok_ && cudaHostGetDevicePointer(&dp, slots_[i].buf, 0) == cudaSuccess && dp == slots_[i].buf;
     }
-    cudaGetLastError();
     for (uint32_t t = 0; t < threads; ++t) th_.emplace_back([this] { worker(); });
 }
 
@@ -974,32 +970,13 @@ void GpuLoader::stage_block(uint64_t id) {
         // (copied and released right away: one next() may consume more blocks than there are buffers)
         const uint64_t seq = read_seq_++;
         const BlockReader::Block& bk = reader_->wait(seq);
-        static const bool ce = [] {
-            const char* e = std::getenv("RFL_STAGE");
-            return e && std::string(e) == "ce";
-        }();
-        bool pulled = false;
         for (uint64_t q = q0; q <= q1; ++q) {
-            uint8_t* dst = lv.slot.ptr + lv.chunk_off[q - q0];
-            const uint8_t* src = bk.buf + bk.pos[q - q0];
-            if (!ce && reader_->pull_ok() && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {
-                // (page-cache reads put a run's first record page aligned; O_DIRECT / later
-                // records of a run keep their file alignment and take a copy-engine transfer)
-                fdst_.push_back(dst);
-                fsrc_.push_back(const_cast<uint8_t*>(src));
-                fsize_.push_back(ds_->rec_len()[q]);
-                pulled = true;
-            } else {
-                cuda_ok(cudaMemcpyAsync(dst, src, ds_->rec_len()[q], cudaMemcpyHostToDevice, copy_), "stage H2D");
-            }
+            cuda_ok(cudaMemcpyAsync(lv.slot.ptr + lv.chunk_off[q - q0], bk.buf + bk.pos[q - q0], ds_->rec_len()[q],
+                                    cudaMemcpyHostToDevice, copy_),
+                    "stage H2D");
             ctr_.h2d_bytes += ds_->rec_len()[q];
         }
-        if (pulled) {
-            fseq_.push_back(seq);  // released once its pull is enqueued
-            if (fseq_.size() * 2 >= reader_->slots()) flush_file_pull();  // the reader needs buffers back
-        } else {
-            reader_->release(seq, copy_);
-        }
+        reader_->release(seq, copy_);
     }
     lv.off0 = reinterpret_cast<uint64_t>(lv.slot.ptr) + lv.chunk_off[0];
     lv.single = q0 == q1;
@@ -1039,36 +1016,6 @@ void GpuLoader::count_fetch(uint64_t id) {
         ctr_.chunks_decoded += end - q;
         q = end;
     }
-}
-
-// One staging pull kernel per <= kMaxPullJobs copies on the copy stream.  Sizes go up
-// to 16-B multiples: pinned-image records sit at 16-B aligned offsets with zeroed
-// gaps, read-ahead buffers have slack, and slots hold the aligned sizes.
-void GpuLoader::launch_pulls(const std::vector<void*>& dst, const std::vector<void*>& src,
-                             const std::vector<size_t>& size) {
-    const uint64_t P = stage_pull_piece_bytes();
-    for (size_t i0 = 0; i0 < dst.size(); i0 += kMaxPullJobs) {
-        pull_.n = static_cast<uint32_t>(std::min<size_t>(kMaxPullJobs, dst.size() - i0));
-        pull_.first_piece[0] = 0;
-        for (uint32_t k = 0; k < pull_.n; ++k) {
-            const uint64_t bytes = align_up(size[i0 + k], kAlign);
-            pull_.job[k] = {static_cast<const uint8_t*>(src[i0 + k]), static_cast<uint8_t*>(dst[i0 + k]), bytes};
-            pull_.first_piece[k + 1] = pull_.first_piece[k] + static_cast<uint32_t>((bytes + P - 1) / P);
-        }
-        launch_stage_pull(pull_, copy_);
-        ctr_.kernels_launched += 1;
-    }
-}
-
-// stream_file: pull the queued records out of the read-ahead buffers, then hand the
-// buffers back to the reader behind that pull
-void GpuLoader::flush_file_pull() {
-    if (!fdst_.empty()) launch_pulls(fdst_, fsrc_, fsize_);
-    for (uint64_t seq : fseq_) reader_->release(seq, copy_);
-    fdst_.clear();
-    fsrc_.clear();
-    fsize_.clear();
-    fseq_.clear();
 }
 
 void GpuLoader::ensure_capacity(OutSlot& s, uint64_t rows, uint64_t nnz) {
@@ -1233,7 +1180,6 @@ bool GpuLoader::assemble_group() {
         d8_jobs_.clear();
         for (const Planned& p : group_)
             for (uint64_t id : p.consumed) stage_block(id);  // (counts each fetch)
-        if (reader_) flush_file_pull();
         if (pend_ev_ && cudaEventQuery(pend_ev_) != cudaSuccess)
             cuda_ok(cudaStreamWaitEvent(copy_, pend_ev_, 0), "wait slots");
         if (!batch_dst_.empty()) {
@@ -1249,7 +1195,21 @@ bool GpuLoader::assemble_group() {
                                             copy_),
                             "stage H2D");
             } else {
-                launch_pulls(batch_dst_, batch_src_, batch_size_);
+                const uint64_t P = stage_pull_piece_bytes();
+                for (size_t i0 = 0; i0 < batch_dst_.size(); i0 += kMaxPullJobs) {
+                    pull_.n = static_cast<uint32_t>(std::min<size_t>(kMaxPullJobs, batch_dst_.size() - i0));
+                    pull_.first_piece[0] = 0;
+                    for (uint32_t k = 0; k < pull_.n; ++k) {
+                        // 16-B multiples: records sit at 16-B aligned image offsets with zeroed gaps,
+                        // and slots hold the aligned sizes
+                        const uint64_t bytes = align_up(batch_size_[i0 + k], kAlign);
+                        pull_.job[k] = {static_cast<const uint8_t*>(batch_src_[i0 + k]),
+                                        static_cast<uint8_t*>(batch_dst_[i0 + k]), bytes};
+                        pull_.first_piece[k + 1] = pull_.first_piece[k] + static_cast<uint32_t>((bytes + P - 1) / P);
+                    }
+                    launch_stage_pull(pull_, copy_);
+                    ctr_.kernels_launched += 1;
+                }
             }
         }
     } else {

@@ -241,8 +241,6 @@ public:
     ~BlockReader();
     const Block& wait(uint64_t seq);              // the seq-th block of the order, once read
     void release(uint64_t seq, cudaStream_t st);  // its buffer is free after st's work so far
-    size_t slots() const { return slots_.size(); }
-    bool pull_ok() const { return pull_ok_; }     // the buffers are device-addressable at their host address
 
 private:
     void worker();
@@ -251,7 +249,6 @@ private:
     uint64_t f_;
     bool direct_;
     bool validate_ = true;  // column checks of every fetched CSR record
-    bool pull_ok_ = false;
     std::vector<Block> slots_;
     uint64_t buf_bytes_ = 0;
     std::vector<cudaEvent_t> ev_;
@@ -370,13 +367,6 @@ private:
     std::vector<D8Job> d8_jobs_;                 // delta-staged records of this next() to expand
     std::vector<size_t> batch_size_;
     PullJobs pull_;                              // the pull kernel's job table (by value)
-    // stream_file: records pulled from the read-ahead buffers (16-B aligned ones), and the
-    // buffers held until the pull that reads them is enqueued
-    std::vector<void*> fdst_, fsrc_;
-    std::vector<size_t> fsize_;
-    std::vector<uint64_t> fseq_;
-    void flush_file_pull();
-    void launch_pulls(const std::vector<void*>& dst, const std::vector<void*>& src, const std::vector<size_t>& size);
     mutable Counters ctr_;
     bool done_ = false;
     uint64_t batch_seq_ = 0;
