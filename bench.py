@@ -572,6 +572,7 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist, staging=None):
 
     it = make_it(epoch)
     host = torch.empty(W["loader"]["batch_rows"] * G, dtype=torch.int64).pin_memory()
+    host_views = {}  # pinned slices by row count
     h2d_done = [0]  # bytes staged by iterators already retired
     k_done = [0]    # kernels launched by iterators already retired
     pend = []
@@ -589,8 +590,12 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist, staging=None):
                 pend = it.next_many(G)
             pend.reverse()
         b = pend.pop()
-        host[:b.n_rows].copy_(b.global_indices, non_blocking=True)  # D2H of the step's result ids
-        return b.n_rows
+        n = b.n_rows
+        hv = host_views.get(n)
+        if hv is None:
+            hv = host_views[n] = host[:n]
+        hv.copy_(b.global_indices, non_blocking=True)  # D2H of the step's result ids
+        return n
 
     for _ in range(Wm):
         step()

@@ -857,6 +857,8 @@ GpuLoader::GpuLoader(std::shared_ptr<DStore> ds, const LoaderCfg& cfg, uint64_t 
     direct_ = ds_->staging() == kResident || (ds_->staging() == kResidentCoded && fused_);
     if (!direct_) {
         live_.resize((m.n_obs + cfg_.f - 1) / cfg_.f);
+        blk_addr_.assign(live_.size(), 0);
+        blk_live_.assign(live_.size(), 0);
         block_bytes_ = ds_->max_block_bytes(cfg_.f, !fused_);
         // live blocks peak at ~5x B/f (cfg1 318 for B/f = 64, cfg4 230 for 32).
         // On top, (out_slots + 2) batches' worth of free slots: the host runs out_slots
@@ -980,6 +982,8 @@ void GpuLoader::stage_block(uint64_t id) {
     }
     lv.off0 = reinterpret_cast<uint64_t>(lv.slot.ptr) + lv.chunk_off[0];
     lv.single = q0 == q1;
+    blk_addr_[id] = lv.single ? lv.off0 : 0;
+    blk_live_[id] = lv.live_rows;
     count_fetch(id);
 }
 
@@ -1239,28 +1243,41 @@ bool GpuLoader::assemble_group() {
 
     // row references of every row of the group
     const uint8_t* base = resident ? ds_->d_arena() : nullptr;
+    const bool kinds = fused_ && m.layout == Layout::csr;
+    const uint64_t* offs = resident ? (fused_ ? ds_->img_off().data() : ds_->rec_off().data()) : nullptr;
+    uint64_t* const baddr = blk_addr_.data();
+    uint64_t* const blive = blk_live_.data();
     for (size_t i = 0; i < nb; ++i) {
         RowRef* hr = s.h_refs + group_start_[i];
         uint64_t* hg = s.h_gidx + group_start_[i];
         const std::vector<uint64_t>& gv = group_[i].gidx;
-        const uint64_t* offs = resident ? (fused_ ? ds_->img_off().data() : ds_->rec_off().data()) : nullptr;
-        const bool kinds = fused_ && m.layout == Layout::csr;
-        for (size_t j = 0; j < gv.size(); ++j) {
-            const uint64_t gr = gv[j];
-            const uint64_t q = div_chunk_.div(gr);
-            if (resident) {
+        const size_t ng = gv.size();
+        const uint64_t* g = gv.data();
+        if (resident) {
+            for (size_t j = 0; j < ng; ++j) {
+                const uint64_t gr = g[j], q = div_chunk_.div(gr);
                 hr[j] = {offs[q], gr};
-            } else {
-                const uint64_t blk = div_f_.div(gr);
-                Live& lv = live_[blk];  // (streamed: base == nullptr, row refs hold device addresses)
-                hr[j] = {lv.single ? lv.off0 : reinterpret_cast<uint64_t>(lv.slot.ptr) + lv.chunk_off[q - lv.first_chunk],
-                         gr};
-                if (--lv.live_rows == 0) done_blocks_.push_back(blk);  // released after this group's kernel
+                if (kinds) hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
             }
-            if (kinds) hr[j].rec_off |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
+        } else {
+            // streamed: base == nullptr, row refs hold device addresses
+            for (size_t j = 0; j < ng; ++j) {
+                const uint64_t gr = g[j], blk = div_f_.div(gr);
+                uint64_t a = baddr[blk];
+                if (!a || kinds) {  // a block of several records (or a kind tag): its chunk's record
+                    const uint64_t q = div_chunk_.div(gr);
+                    const Live& lv = live_[blk];
+                    if (!a) a = reinterpret_cast<uint64_t>(lv.slot.ptr) + lv.chunk_off[q - lv.first_chunk];
+                    if (kinds) a |= static_cast<uint64_t>(ds_->d8_kind(q)) << kRowKindShift;
+                }
+                hr[j] = {a, gr};
+                if (--blive[blk] == 0) done_blocks_.push_back(blk);  // released after this group's kernel
+            }
         }
-        std::memcpy(hg, gv.data(), gv.size() * sizeof(uint64_t));
+        std::memcpy(hg, g, ng * sizeof(uint64_t));
     }
+    double t_refs = 0;
+    if (tr.on) t_refs = tr.lap();
     cuda_ok(cudaMemcpyAsync(s.d_refs, s.h_refs, n * sizeof(RowRef), cudaMemcpyHostToDevice, copy_), "refs H2D");
     ctr_.h2d_bytes += n * sizeof(RowRef);
     // CSR output: the batch indptrs are prefixes of the schedule's per-row nnz
@@ -1343,9 +1360,10 @@ bool GpuLoader::assemble_group() {
     for (const Planned& p : group_) n_blocks += p.consumed.size();
     if (tr.on)
         std::fprintf(stderr,
-                     "# next %llu (+%zu): replay %.1f us, stage %.1f us (%zu blocks), slot wait %.1f us, rest %.1f us\n",
+                     "# next %llu (+%zu): replay %.1f us, stage %.1f us (%zu blocks), slot wait %.1f us, "
+                     "row refs %.1f us, rest %.1f us\n",
                      static_cast<unsigned long long>(group_[0].batch_index), nb - 1, t_replay, t_stage, n_blocks,
-                     t_slot, tr.lap());
+                     t_slot, t_refs, tr.lap());
     const uint32_t layout = (m.layout == Layout::csr && dev_.output == 0) ? 1u : 0u;
     const uint32_t native = static_cast<uint32_t>(m.value_dtype);
     const uint32_t dtype =

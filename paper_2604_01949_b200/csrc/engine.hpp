@@ -352,6 +352,11 @@ private:
     // rows read in place from a device-resident image (resident, or resident_coded + fused_): no slots
     bool direct_ = false;
     std::vector<Live> live_;                 // indexed by block id (streaming)
+    // the per-row reference loop's view of live_: the device address of a staged
+    // single-record block (0: multi-record, look up chunk_off) and its rows still to
+    // be handed out, as flat arrays (16 B per block instead of a Live per row)
+    std::vector<uint64_t> blk_addr_;
+    std::vector<uint64_t> blk_live_;
     FastDiv div_chunk_, div_f_;              // row -> chunk, row -> block
     // one release event per group, from a ring of kReleaseRing store-owned events: a
     // ring event is re-recorded only kReleaseRing groups later on the same stream, so a

@@ -237,15 +237,20 @@ class BatchIterator:
         self._views = {}
         self._hviews = {}
 
-    def _view(self, ptr, shape, np_dtype):
+    def _view(self, ptr, shape, np_dtype, bf16=False):
         """cuda_tensor, cached: the loader's output slots are a fixed ring, so the
-        same (pointer, shape) views come back every out_slots batches."""
-        key = (ptr, shape, np_dtype)
+        same (pointer, shape) views come back every out_slots batches (bf16: the
+        u16 view reinterpreted, cached as well)."""
+        key = (ptr, shape, np_dtype, bf16)
         t = self._views.get(key)
         if t is None:
             if len(self._views) > 256:
                 self._views.clear()
-            t = self._views[key] = cuda_tensor(ptr, shape, np_dtype, self.device)
+            t = cuda_tensor(ptr, shape, np_dtype, self.device)
+            if bf16:
+                import torch
+                t = t.view(torch.bfloat16)
+            self._views[key] = t
         return t
 
     def _host_view(self, addr, n):
@@ -290,12 +295,10 @@ class BatchIterator:
                                data=self._view(b.d_data, (b.nnz,), _NP[b.dtype]), nnz=b.nnz,
                                dtype=str(b.dtype), index_dtype="u32" if idt == np.uint32 else "u64",
                                _ready_event=b.ready_event or 0)
-        data = self._view(b.d_data, (n, b.n_var), _NP[b.dtype])
-        if b.dtype == L.BF16:
-            import torch
-            data = data.view(torch.bfloat16)
+        dt = b.dtype
+        data = self._view(b.d_data, (n, b.n_var), _NP[dt], dt == L.BF16)
         return DeviceBatch(b.epoch_index, b.batch_index, n, b.n_var, "dense", g, gh, data=data, nnz=b.nnz,
-                           dtype=str(b.dtype), _ready_event=b.ready_event or 0)
+                           dtype=str(dt), _ready_event=b.ready_event or 0)
 
     def __iter__(self):
         while (b := self.next()) is not None:
