@@ -572,7 +572,7 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist, staging=None):
 
     it = make_it(epoch)
     host = torch.empty(W["loader"]["batch_rows"] * G, dtype=torch.int64).pin_memory()
-    host_views = {}  # pinned slices by row count
+    host_ptr, stream_h = host.data_ptr(), stream.cuda_stream
     h2d_done = [0]  # bytes staged by iterators already retired
     k_done = [0]    # kernels launched by iterators already retired
     pend = []
@@ -591,10 +591,7 @@ def run_e2e(args, wl, reader, W, rank, world, local, dist, staging=None):
             pend.reverse()
         b = pend.pop()
         n = b.n_rows
-        hv = host_views.get(n)
-        if hv is None:
-            hv = host_views[n] = host[:n]
-        hv.copy_(b.global_indices, non_blocking=True)  # D2H of the step's result ids
+        b.ids_to_host(host_ptr, stream_h)  # D2H of the step's result ids (one cudaMemcpyAsync)
         return n
 
     for _ in range(Wm):

@@ -233,6 +233,12 @@ rfl_status rfl_batch_download(const rfl_batch* b, uint64_t* h_indptr, void* h_in
  * Work the caller queues on `stream` afterwards sees the finished batch
  * (the reference returns MiniBatch by value, so reading it needs no wait). */
 rfl_status rfl_batch_wait(const rfl_batch* b, void* stream);
+/* Queue the copy of n_rows global row ids (u64, a batch's d_gidx) into host
+ * memory h_gidx on `stream` (no host wait; pinned h_gidx makes it
+ * asynchronous).  Ordered after the batch when `stream` is the loader's stream
+ * or was ordered by rfl_batch_wait.  (New: the one-call form of the
+ * per-step result read, instead of a torch copy.) */
+rfl_status rfl_ids_download_async(const uint64_t* d_gidx, uint64_t n_rows, uint64_t* h_gidx, void* stream);
 rfl_status rfl_loader_sync(rfl_loader* l);
 void rfl_loader_destroy(rfl_loader* l);
 

@@ -113,6 +113,7 @@ SIGNATURES = [
     ("rfl_loader_counters_get", C.c_int, [vp, C.POINTER(rfl_loader_counters)]),
     ("rfl_batch_download", C.c_int, [C.POINTER(rfl_batch), vp, vp, vp, vp]),
     ("rfl_batch_wait", C.c_int, [C.POINTER(rfl_batch), vp]),
+    ("rfl_ids_download_async", C.c_int, [vp, u64, vp, vp]),
     ("rfl_loader_next_many", C.c_int, [vp, C.POINTER(rfl_batch), u32, C.POINTER(u32)]),
     ("rfl_device_can_access_peer", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_int)]),
     ("rfl_loader_sync", C.c_int, [vp]),

@@ -401,6 +401,16 @@ rfl_status rfl_batch_wait(const rfl_batch* b, void* stream) {
     });
 }
 
+rfl_status rfl_ids_download_async(const uint64_t* d_gidx, uint64_t n_rows, uint64_t* h_gidx, void* stream) {
+    return guarded([&] {
+        if (n_rows && (!d_gidx || !h_gidx)) rfl::invalid("null argument");
+        if (n_rows)
+            rfl::cuda_ok(cudaMemcpyAsync(h_gidx, d_gidx, n_rows * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                         static_cast<cudaStream_t>(stream)),
+                         "ids D2H");
+    });
+}
+
 rfl_status rfl_loader_sync(rfl_loader* l) {
     return guarded([&] {
         if (!l) rfl::invalid("null argument");

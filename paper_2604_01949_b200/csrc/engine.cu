@@ -983,7 +983,7 @@ void GpuLoader::stage_block(uint64_t id) {
     lv.off0 = reinterpret_cast<uint64_t>(lv.slot.ptr) + lv.chunk_off[0];
     lv.single = q0 == q1;
     blk_addr_[id] = lv.single ? lv.off0 : 0;
-    blk_live_[id] = lv.live_rows;
+    blk_live_[id] = static_cast<uint32_t>(lv.live_rows);
     count_fetch(id);
 }
 
@@ -1246,7 +1246,7 @@ bool GpuLoader::assemble_group() {
     const bool kinds = fused_ && m.layout == Layout::csr;
     const uint64_t* offs = resident ? (fused_ ? ds_->img_off().data() : ds_->rec_off().data()) : nullptr;
     uint64_t* const baddr = blk_addr_.data();
-    uint64_t* const blive = blk_live_.data();
+    uint32_t* const blive = blk_live_.data();
     for (size_t i = 0; i < nb; ++i) {
         RowRef* hr = s.h_refs + group_start_[i];
         uint64_t* hg = s.h_gidx + group_start_[i];

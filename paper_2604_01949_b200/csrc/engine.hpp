@@ -356,7 +356,7 @@ private:
     // single-record block (0: multi-record, look up chunk_off) and its rows still to
     // be handed out, as flat arrays (16 B per block instead of a Live per row)
     std::vector<uint64_t> blk_addr_;
-    std::vector<uint64_t> blk_live_;
+    std::vector<uint32_t> blk_live_;
     FastDiv div_chunk_, div_f_;              // row -> chunk, row -> block
     // one release event per group, from a ring of kReleaseRing store-owned events: a
     // ring event is re-recorded only kReleaseRing groups later on the same stream, so a

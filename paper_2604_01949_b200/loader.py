@@ -161,6 +161,17 @@ class DeviceBatch:
     dtype: str = ""
     index_dtype: str = "u32"
     _ready_event: int = 0
+    _d_gidx: int = 0
+
+    def ids_to_host(self, dst: int, stream=None):
+        """Queue the D2H copy of global_indices (u64[n_rows]) into host memory at
+        address `dst` (pinned: asynchronous) on `stream` (a torch stream or a raw
+        handle; default torch's current stream) -- rfl_ids_download_async."""
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream()
+        h = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        L.check(L.lib().rfl_ids_download_async(self._d_gidx, self.n_rows, dst, h))
 
     def to_minibatch(self) -> MiniBatch:
         """Host MiniBatch exactly as the reference returns it (u64 indices, raw value bytes)."""
@@ -294,11 +305,11 @@ class BatchIterator:
                                indices=self._view(b.d_indices, (b.nnz,), np.int32 if idt == np.uint32 else np.int64),
                                data=self._view(b.d_data, (b.nnz,), _NP[b.dtype]), nnz=b.nnz,
                                dtype=str(b.dtype), index_dtype="u32" if idt == np.uint32 else "u64",
-                               _ready_event=b.ready_event or 0)
+                               _ready_event=b.ready_event or 0, _d_gidx=b.d_gidx or 0)
         dt = b.dtype
         data = self._view(b.d_data, (n, b.n_var), _NP[dt], dt == L.BF16)
         return DeviceBatch(b.epoch_index, b.batch_index, n, b.n_var, "dense", g, gh, data=data, nnz=b.nnz,
-                           dtype=str(dt), _ready_event=b.ready_event or 0)
+                           dtype=str(dt), _ready_event=b.ready_event or 0, _d_gidx=b.d_gidx or 0)
 
     def __iter__(self):
         while (b := self.next()) is not None:

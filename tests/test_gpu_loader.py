@@ -439,3 +439,26 @@ def test_raw_onehot_gather_random_rows(tmp_path, n_var):
         L.check(L.lib().rfl_onehot_gather(C.byref(desc), refs.data_ptr(), 1, L.F32, out.data_ptr(), None, None))
     coded.close()
     plain.close()
+
+
+@pytest.mark.parametrize("staging", ["resident", "stream_pinned"])
+def test_ids_to_host_async(golden, golden_stores, staging):
+    """DeviceBatch.ids_to_host (rfl_ids_download_async): the queued D2H of each
+    batch's device ids lands the reference's global row ids, in batch order,
+    grouped launches included."""
+    ld = golden["loaders"][0]
+    it = R.BatchIterator(R.DeviceStore(golden_stores[ld["store"]], 0, staging), _cfg(ld), ld["epoch"],
+                         batches_per_launch=3, out_slots=2, stream=torch.cuda.current_stream())
+    host = torch.zeros(ld["b"] * 3, dtype=torch.int64).pin_memory()
+    got = []
+    while bs := it.next_many(3):
+        off = 0
+        for b in bs:
+            b.ids_to_host(host.data_ptr() + 8 * off)
+            off += b.n_rows
+        torch.cuda.current_stream().synchronize()
+        off = 0
+        for b in bs:
+            got.append(host[off:off + b.n_rows].tolist())
+            off += b.n_rows
+    assert got == ld["gidx"]
