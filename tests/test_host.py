@@ -28,6 +28,15 @@ def test_library_exports_every_header_symbol():
     assert lib.rfl_version().startswith(b"riffle_b200")
 
 
+def test_ids_download_argument_checks():
+    """rfl_ids_download_async: null buffers with rows to copy are EINVAL (checked
+    before any CUDA call); zero rows is a no-op."""
+    lib = L.lib()
+    assert lib.rfl_ids_download_async(None, 4, None, None) == L.EINVAL
+    assert b"null" in lib.rfl_last_error()
+    assert lib.rfl_ids_download_async(None, 0, None, None) == L.OK
+
+
 def test_no_gpu_here_fails_loudly(tmp_path):
     """No CPU fallback: on a GPU-less host, device entry points raise CudaError."""
     if L.lib().rfl_device_count() > 0:
