@@ -58,7 +58,7 @@ WORKLOADS = {
                  synth=dict(n_obs=2_000_000, n_var=12288, layout="dense", value_dtype="u8", density=0.1, seed=2,
                             chunk_rows=256, chunks_per_shard=128),
                  loader=dict(fetch_block_rows=256, buffer_capacity_rows=16384, batch_rows=1024, seed=0),
-                 out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16", group=2, e2e_group=4,
+                 out=dict(output="dense", out_dtype="bf16", transform=None), dtype="u8->bf16", group=4, e2e_group=4,
                  e2e_min_steps=200),
     "cfg4": dict(desc="cfg4: dense 4x1024 one-hot u8 windows (5M, procedural one-hot: one channel per position), "
                       "chunk 512, f=512 B=16384 b=2048, raw u8",
